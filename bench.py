@@ -1,0 +1,345 @@
+"""bench.py -- B200 SA-AMG NS-Block hot path benchmark (one JSON line).
+
+Metric (BASELINE.json): "BSR SpMV HBM GB/s (% roofline); AMG setup+solve
+seconds at 1/2/4/8 B200".  ``value`` is the 3x3-BSR SpMV throughput in
+algorithmic GB/s on the C1 fine matrix (64^3-node cube, free-DOF form,
+774,144 unknowns, 6,750,700 blocks = 527 MB > 126 MB L2, so no L2 flush is
+needed); one step = one y = A x over the whole matrix, inputs resident in
+HBM, timed with CUDA events on the launching stream.  ``amg`` carries the
+full ns_block setup + SPAI0-preconditioned CG solve seconds on the same
+problem.  ``e2e`` is the SpMV through the C-ABI with host vectors (H2D of x
+and D2H of y inside the timed region).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+For N>1 (torchrun, one rank per GPU) every rank runs the same per-GPU
+workload (replicas, weak scaling); the timed region is bracketed by a
+barrier + synchronize and the max over ranks is reported.
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "BSR SpMV HBM GB/s (% roofline); AMG setup+solve seconds at 1/2/4/8 B200"
+C1 = dict(nx=63, ny=63, nz=63, dirichlet="eliminate", noise=0.01, seed=2022)
+WORKLOAD = ("C1: 64x64x64-node unit cube, trilinear hex8 elasticity (E=1, nu=0.3), x=0 face "
+            "clamped (free-DOF form: 774,144 unknowns), body force -z + U[-0.01,0.01] noise, "
+            "3x3 BSR fp64; SA-AMG ns_block + SPAI0, CG rtol 1e-8")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--amg-repeats", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    return ap.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def dist_init(args):
+    rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl" if args.impl == "b200" else "gloo")
+    return rank, world, local, dist
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    def __init__(self, device):
+        self.samples, self.reasons = [], set()
+        self.stop_ev = threading.Event()
+        self.ok = False
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nv = nv
+            self.h = nv.nvmlDeviceGetHandleByIndex(device)
+            self.max = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max = None
+
+    NAMES = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+             0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+             0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+             0x100: "display_clock_setting"}
+
+    def _run(self):
+        nv = self.nv
+        while not self.stop_ev.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.NAMES.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self.stop_ev.set()
+            self.t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def ncu_traffic():
+    """dram bytes per launch of the SpMV kernel from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_spmv_c1.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    return None
+
+
+def make_problem(pb):
+    return pb.generate_hex(**C1)
+
+
+def cpu_reference_spmv(p, seconds, steps=None):
+    """The reference's spmv<static_block<3>> (csr.hpp:129-160) from
+    oracle/_ref on one host core over the C1 matrix: time-bounded sample."""
+    from oracle.oracle import Ref
+    ref = Ref()
+    A = ref.bsr3(p.nbrows, p.nbrows, p.ptr, p.col, p.val.reshape(-1))
+    x = np.random.default_rng(1).uniform(-1, 1, p.n)
+    y = np.zeros(p.n)
+    A.spmv(x, y)
+    times = []
+    t_end = time.perf_counter() + seconds
+    while (steps is None and (time.perf_counter() < t_end or len(times) < 3)) or \
+            (steps is not None and len(times) < steps):
+        t0 = time.perf_counter()
+        A.spmv(x, y)
+        times.append(time.perf_counter() - t0)
+    return times
+
+
+def spmv_bytes(p):
+    return p.nnzb * 76 + (p.nbrows + 1) * 4 + p.nbrows * 24 + p.nbrows * 24
+
+
+def run_reference(args, rank, world, dist):
+    """--impl reference: the reference's own CPU path, rank 0 only."""
+    if rank != 0:
+        return
+    import paper_2202_09056_b200 as pb  # host-only generator (no GPU work)
+    p = make_problem(pb)
+    nbytes = spmv_bytes(p)
+    cores = 1
+    # each step: one full SpMV (23 ms class); bound the run to a few minutes
+    steps = args.steps
+    budget = 120.0
+    warm = cpu_reference_spmv(p, 0, steps=max(1, min(args.warmup, 3)))
+    per = statistics.median(warm)
+    sample_steps = int(min(steps, max(3, budget / max(per, 1e-6))))
+    times = cpu_reference_spmv(p, 0, steps=sample_steps)
+    t = statistics.median(times)
+    gbs = nbytes / t / 1e9
+    amg = None
+    if os.environ.get("SAMG_BENCH_REF_AMG", "1") == "1":
+        from oracle.oracle import Params, Ref, SM_SPAI0
+        ref = Ref()
+        n, ptr, col, val = p.csr()
+        B = p.nullspace()
+        t0 = time.perf_counter()
+        h = ref.setup(n, ptr, col, val, B, Params(smoother=SM_SPAI0))
+        t_setup = time.perf_counter() - t0
+        u, rep = h.cg_solve(p.rhs)
+        amg = {"setup_s": t_setup, "solve_s": rep["solve_seconds"], "iterations": rep["iterations"],
+               "relative_residual": rep["relative_residual"], "levels": h.nlevels,
+               "converged": rep["converged"], "cores": 1}
+    line = {
+        "metric": METRIC, "value": gbs, "unit": "GB/s", "impl": "reference",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "unknowns": p.n, "nnzb": p.nnzb},
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "reference",
+                         "sample": f"{len(times)} x samg::spmv<static_block<3>> over the full C1 "
+                                   f"matrix (median), oracle/_ref, 1 thread (reference is "
+                                   f"single-threaded)"},
+        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "amg": amg,
+    }
+    print(json.dumps(line))
+
+
+def run_b200(args, rank, world, local, dist):
+    import torch
+
+    import paper_2202_09056_b200 as pb
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    p = make_problem(pb)
+    nbytes = spmv_bytes(p)
+    A = pb.Bsr3.from_host(p.nbrows, p.nbrows, p.ptr, p.col, p.val.reshape(-1), device=local)
+    x = torch.rand(p.n, dtype=torch.float64, device=dev) * 2 - 1
+    y = torch.zeros(p.n, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    sh = stream.cuda_stream
+    for _ in range(max(args.warmup, 3)):
+        A.spmv_device(x.data_ptr(), y.data_ptr(), 1.0, 0.0, sh)
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            A.spmv_device(x.data_ptr(), y.data_ptr(), 1.0, 0.0, sh)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    ms_per = ms / args.steps
+    gbs_rank = nbytes / (ms_per * 1e-3) / 1e9
+    value = gbs_rank * world
+
+    # e2e: host vectors through the C-ABI (H2D x, kernel, D2H y per step)
+    xh = torch.empty(p.n, dtype=torch.float64, pin_memory=True).numpy()
+    yh = torch.empty(p.n, dtype=torch.float64, pin_memory=True).numpy()
+    xh[:] = np.random.default_rng(3).uniform(-1, 1, p.n)
+    from paper_2202_09056_b200._lib import check, lib
+    import ctypes as C
+    fp = C.POINTER(C.c_double)
+    xp, yp = xh.ctypes.data_as(fp), yh.ctypes.data_as(fp)
+    for _ in range(3):
+        check(lib.samg_bsr3_spmv(A.h, 1.0, xp, 0.0, yp))
+    e2e_steps = max(10, min(args.steps, 500))
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        check(lib.samg_bsr3_spmv(A.h, 1.0, xp, 0.0, yp))
+    e2e_t = (time.perf_counter() - t0) / e2e_steps
+    if dist:
+        t = torch.tensor([e2e_t], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_t = float(t.item())
+    e2e_val = nbytes / e2e_t / 1e9 * world
+
+    # full AMG setup + solve on the same problem (device-resident after upload)
+    amg = None
+    if args.amg_repeats > 0:
+        n, ptr, col, val = p.csr()
+        B = p.nullspace()
+        prm = pb.AmgParams(smoother="spai0", device=local)
+        setups, solves, rep, h = [], [], None, None
+        f_d = torch.from_numpy(p.rhs).to(dev)
+        u_d = torch.zeros_like(f_d)
+        for _ in range(args.amg_repeats):
+            if h is not None:
+                h.close()
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            h = pb.setup_bsr3(p.nbrows, p.ptr, p.col, p.val.reshape(-1), B, "ns_block", prm)
+            torch.cuda.synchronize(dev)
+            setups.append(time.perf_counter() - t0)
+            t0 = time.perf_counter()
+            rep = h.cg_solve_device(f_d.data_ptr(), u_d.data_ptr())
+            torch.cuda.synchronize(dev)
+            solves.append(time.perf_counter() - t0)
+        levels = [h.level_info(l)[0] for l in range(h.nlevels)]
+        amg = {"setup_s": statistics.median(setups), "solve_s": statistics.median(solves),
+               "setup_s_all": setups, "solve_s_all": solves,
+               "iterations": rep["iterations"], "relative_residual": rep["relative_residual"],
+               "converged": rep["converged"], "levels_block_rows": levels,
+               "coarse_dim": h.coarse_dim, "preconditioner_bytes": rep["preconditioner_bytes"],
+               "smoother": "spai0 (M_i = A_ii / sum_j ||A_ij||_F^2)", "input": "host BSR3 upload "
+               "inside setup_s"}
+        h.close()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            times = cpu_reference_spmv(p, args.cpu_seconds)
+            tc = statistics.median(times)
+            cpu = {"value": nbytes / tc / 1e9, "unit": "GB/s", "cores": 1, "kind": "reference",
+                   "sample": f"{len(times)} x samg::spmv<static_block<3>> over the full C1 "
+                             f"matrix in ~{args.cpu_seconds:.0f} s (median), oracle/_ref, 1 thread"}
+        except Exception as e:  # reference not built on this box
+            cpu = {"value": None, "unit": "GB/s", "cores": 1, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    peak, peak_src = peaks()
+    traffic = ncu_traffic()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "unknowns": p.n, "block_rows": p.nbrows,
+                       "nnzb": p.nnzb, "spmv_bytes_per_step": nbytes,
+                       "l2": "no flush: matrix stream 527 MB > 126 MB L2",
+                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
+            "roofline": {"bound": "hbm", "achieved": gbs_rank, "peak": peak, "unit": "GB/s",
+                         "frac": gbs_rank / peak, "traffic": traffic, "peak_source": peak_src,
+                         "kernel": "k_bsr3<G,EpiSpmv> (solve.cu)"},
+            "e2e": {"value": e2e_val, "unit": "GB/s", "h2d_bytes_per_step": 8 * p.n,
+                    "d2h_bytes_per_step": 8 * p.n,
+                    "path": "samg_bsr3_spmv (C-ABI, pinned host x/y)"},
+            "gpu_launches": args.steps,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+            "amg": amg,
+        }
+        print(json.dumps(line))
+
+
+def main():
+    args = parse()
+    rank, world, local, dist = dist_init(args)
+    try:
+        if args.impl == "reference":
+            run_reference(args, rank, world, dist)
+        else:
+            run_b200(args, rank, world, local, dist)
+    finally:
+        if dist:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

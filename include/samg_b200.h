@@ -1,0 +1,238 @@
+/*
+ * samg_b200.h -- C-ABI of the B200-native SA-AMG "NS Block" solver.
+ *
+ * This is the drop-in boundary for the reference's ns_block hot path
+ * (/root/reference/proj/include/samg).  The reference has no FFI of its own;
+ * each entry point below names the reference interface it replaces.  Plain
+ * pointers and sizes only; every call returns an int status whose values
+ * map 1:1 onto the reference's exception classes (common.hpp:12-28), plus
+ * CUDA failures.  Calls on one handle are not thread-safe (the reference's
+ * hierarchy is likewise single-threaded); distinct handles are independent.
+ *
+ * There is no CPU fallback: without a CUDA device every compute entry point
+ * returns SAMG_NO_DEVICE.
+ */
+#ifndef SAMG_B200_H
+#define SAMG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define SAMG_API __attribute__((visibility("default")))
+#else
+#define SAMG_API
+#endif
+
+/* Status codes; 1..14 mirror samg::error subclasses (common.hpp:12-28). */
+enum samg_status {
+    SAMG_OK = 0,
+    SAMG_ERROR = 1,                /* samg::error                        */
+    SAMG_DIMENSION_MISMATCH = 2,   /* samg::dimension_mismatch           */
+    SAMG_NOT_DIVISIBLE = 3,        /* samg::not_divisible                */
+    SAMG_SINGULAR_BLOCK = 4,       /* samg::singular_block               */
+    SAMG_MISSING_DIAGONAL = 5,     /* samg::missing_diagonal             */
+    SAMG_ZERO_DIAGONAL = 6,        /* samg::zero_diagonal                */
+    SAMG_NON_SQUARE = 7,           /* samg::non_square                   */
+    SAMG_BAD_NULLSPACE_SHAPE = 8,  /* samg::bad_nullspace_shape          */
+    SAMG_BREAKDOWN_NON_SPD = 9,    /* samg::breakdown_non_spd            */
+    SAMG_INVALID_MATERIAL = 10,    /* samg::invalid_material             */
+    SAMG_SHAPE_MISMATCH = 11,      /* samg::shape_mismatch               */
+    SAMG_CUDA_ERROR = 100,
+    SAMG_NCCL_ERROR = 101,
+    SAMG_OUT_OF_MEMORY = 102,
+    SAMG_NO_DEVICE = 103,
+    SAMG_UNSUPPORTED = 104,        /* pipeline / smoother not on this path */
+    SAMG_INVALID_ARGUMENT = 105
+};
+
+/* samg::pipeline (hierarchy.hpp:30).  Only SAMG_PIPELINE_NS_BLOCK is the
+ * B200 hot path; the others return SAMG_UNSUPPORTED. */
+enum samg_pipeline {
+    SAMG_PIPELINE_SCALAR = 0,
+    SAMG_PIPELINE_BLOCK = 1,
+    SAMG_PIPELINE_NS_SCALAR = 2,
+    SAMG_PIPELINE_NS_HYBRID1 = 3,
+    SAMG_PIPELINE_NS_HYBRID2 = 4,
+    SAMG_PIPELINE_NS_BLOCK = 5
+};
+
+/* Smoothers.  JACOBI = the reference's point damped_jacobi
+ * (relaxation.hpp:141-180, omega default 0.72).  SPAI0 and BLOCK_JACOBI are
+ * 3x3 block smoothers.  ILU0 (relaxation.hpp:20-139)
+ * is not on this path yet: SAMG_UNSUPPORTED. */
+enum samg_smoother {
+    SAMG_SMOOTHER_JACOBI = 0,
+    SAMG_SMOOTHER_SPAI0 = 1,
+    SAMG_SMOOTHER_BLOCK_JACOBI = 2,
+    SAMG_SMOOTHER_ILU0 = 3
+};
+
+/* amg_params (hierarchy.hpp:50-58) + coarsening_params (coarsening.hpp:26-31)
+ * + the smoother selector and device placement. */
+typedef struct {
+    double eps_strong;        /* 0.08 */
+    double omega;             /* prolongator damping, 2/3 */
+    int point_block_size;     /* forced to 3 for ns pipelines (hierarchy.hpp:284) */
+    int smoother;             /* samg_smoother, default SPAI0 */
+    double smoother_omega;    /* Jacobi / block-Jacobi damping, 0.72 */
+    int pre_sweeps;           /* 1 */
+    int post_sweeps;          /* 1 */
+    int64_t coarse_enough;    /* 3000 scalar unknowns */
+    double stagnation_ratio;  /* 0.8 */
+    int verify_galerkin;      /* reserved (hierarchy.hpp:382-402) */
+    int device;               /* CUDA device ordinal, default 0 */
+} samg_amg_params;
+
+/* cg_params (cg.hpp:32-35) */
+typedef struct {
+    double tol;               /* 1e-8 */
+    int max_iterations;       /* 1000 */
+} samg_cg_params;
+
+/* solve_report (cg.hpp:22-30) */
+typedef struct {
+    int iterations;
+    double relative_residual;     /* true residual at exit (cg.hpp:105-108) */
+    double setup_seconds;
+    double solve_seconds;
+    uint64_t preconditioner_bytes; /* memory_footprint (hierarchy.hpp:443-458) */
+    int variant;                  /* samg_pipeline */
+    int converged;
+} samg_solve_report;
+
+typedef struct samg_hierarchy samg_hierarchy;  /* owns all level data on the GPU */
+typedef struct samg_bsr3 samg_bsr3;            /* a device-resident 3x3 BSR matrix */
+typedef struct samg_problem samg_problem;      /* host-side synthetic problem */
+
+SAMG_API void samg_default_amg_params(samg_amg_params *p);
+SAMG_API void samg_default_cg_params(samg_cg_params *p);
+SAMG_API const char *samg_last_error(void);     /* thread-local message */
+SAMG_API const char *samg_status_name(int status);
+SAMG_API int samg_device_count(int *count);
+
+/* ---- setup: replaces samg::setup (hierarchy.hpp:263-405) ----------------
+ * Scalar CSR input (int64 ptr/col, fp64 val, n rows), exactly the
+ * reference's csr<double> (csr.hpp:26-40).  B is the column-major
+ * b_rows-by-b_cols near-nullspace (dense_columns, csr.hpp:46-55) or NULL. */
+SAMG_API int samg_setup(int64_t n, const int64_t *ptr, const int64_t *col,
+        const double *val, const double *B, int64_t b_rows, int64_t b_cols,
+        int pipeline, const samg_amg_params *prm, samg_hierarchy **out);
+/* Same, from 3x3 block CSR (nbrows block rows, blocks row-major 9 doubles),
+ * i.e. the result of to_block<3> (csr.hpp:268-324) without the host pass. */
+SAMG_API int samg_setup_bsr3(int64_t nbrows, const int64_t *ptr,
+        const int64_t *col, const double *val, const double *B, int64_t b_rows,
+        int64_t b_cols, int pipeline, const samg_amg_params *prm,
+        samg_hierarchy **out);
+SAMG_API int samg_destroy(samg_hierarchy *h);
+
+/* ---- solve: replaces samg::cg_solve (cg.hpp:87-112) --------------------
+ * f, u host pointers of length finest_dim; u is overwritten (zero start). */
+SAMG_API int samg_cg_solve(samg_hierarchy *h, const double *f, double *u,
+        const samg_cg_params *prm, samg_solve_report *rep);
+/* Same with device pointers on the hierarchy's device. */
+SAMG_API int samg_cg_solve_device(samg_hierarchy *h, const double *d_f,
+        double *d_u, const samg_cg_params *prm, samg_solve_report *rep);
+
+/* ---- preconditioner: replaces samg::vcycle (hierarchy.hpp:408-441) ------
+ * u is the initial approximation and the result (host / device pointers). */
+SAMG_API int samg_vcycle(samg_hierarchy *h, const double *f, double *u);
+SAMG_API int samg_vcycle_device(samg_hierarchy *h, const double *d_f,
+        double *d_u);
+
+/* ---- introspection / parity taps ---------------------------------------- */
+SAMG_API int samg_memory_footprint(const samg_hierarchy *h, uint64_t *bytes);
+SAMG_API int samg_finest_dim(const samg_hierarchy *h, int64_t *n);
+SAMG_API int samg_num_levels(const samg_hierarchy *h, int *nlevels);
+SAMG_API int samg_coarse_dim(const samg_hierarchy *h, int64_t *n);
+SAMG_API int samg_setup_seconds(const samg_hierarchy *h, double *seconds);
+/* which: 0 = A, 1 = P, 2 = R of `level`; sizes in 3x3 blocks */
+SAMG_API int samg_level_info(const samg_hierarchy *h, int level, int which,
+        int64_t *nrows, int64_t *ncols, int64_t *nnzb);
+/* copies into host buffers sized by samg_level_info: ptr[nrows+1],
+ * col[nnzb], val[9*nnzb] */
+SAMG_API int samg_get_level(const samg_hierarchy *h, int level, int which,
+        int64_t *ptr, int64_t *col, double *val);
+/* borrow a level matrix as a device BSR3 (owned by the hierarchy) */
+SAMG_API int samg_level_matrix(samg_hierarchy *h, int level, int which,
+        const samg_bsr3 **m);
+/* aggregate ids of the level's nodes (node = point_block_size scalar rows) */
+SAMG_API int samg_aggregates_info(const samg_hierarchy *h, int level,
+        int64_t *nnodes, int64_t *count);
+SAMG_API int samg_get_aggregates(const samg_hierarchy *h, int level,
+        int64_t *id);
+/* smoother data: 3 per block row (point Jacobi 1/a_ii) or 9 (block M_i) */
+SAMG_API int samg_smoother_info(const samg_hierarchy *h, int level,
+        int64_t *len);
+SAMG_API int samg_get_smoother(const samg_hierarchy *h, int level,
+        double *data);
+
+/* ---- device BSR3 matrices: spmv<static_block<3>> (csr.hpp:129-160) ------ */
+SAMG_API int samg_bsr3_create(int64_t nrows, int64_t ncols, const int64_t *ptr,
+        const int64_t *col, const double *val, int device, samg_bsr3 **out);
+SAMG_API int samg_bsr3_destroy(samg_bsr3 *m);
+SAMG_API int samg_bsr3_info(const samg_bsr3 *m, int64_t *nrows, int64_t *ncols,
+        int64_t *nnzb);
+SAMG_API int samg_bsr3_download(const samg_bsr3 *m, int64_t *ptr, int64_t *col,
+        double *val);
+/* y = alpha*A*x + beta*y with device vectors on `stream` (cudaStream_t or
+ * NULL for the legacy stream); asynchronous. */
+SAMG_API int samg_bsr3_spmv_device(const samg_bsr3 *m, double alpha,
+        const double *d_x, double beta, double *d_y, void *stream);
+/* same with host vectors: H2D x (and y if beta != 0), kernel, D2H y */
+SAMG_API int samg_bsr3_spmv(const samg_bsr3 *m, double alpha, const double *x,
+        double beta, double *y);
+/* Galerkin product R*A*P (csr.hpp:259-262) in the reference's summation
+ * order; result is a new device matrix. */
+SAMG_API int samg_bsr3_galerkin(const samg_bsr3 *R, const samg_bsr3 *A,
+        const samg_bsr3 *P, samg_bsr3 **out);
+/* algorithmic bytes of one spmv */
+SAMG_API int samg_bsr3_spmv_bytes(const samg_bsr3 *m, int beta_nonzero,
+        uint64_t *bytes);
+
+/* ---- synthetic problems (input tooling; elasticity.hpp:38-213 extended) -- */
+enum samg_dirichlet { SAMG_DIRICHLET_NONE = 0, SAMG_DIRICHLET_KEEP_ROWS = 1,
+                      SAMG_DIRICHLET_ELIMINATE = 2 };
+enum samg_load { SAMG_LOAD_BODY_FORCE = 0, SAMG_LOAD_TRACTION_XEND = 1,
+                 SAMG_LOAD_RANDOM = 2 };
+typedef struct {
+    int64_t nx, ny, nz;       /* elements per axis (nodes = n+1) */
+    double lx, ly, lz;        /* domain lengths (unit cube = 1,1,1) */
+    double E, nu;             /* homogeneous material */
+    int heterogeneous;        /* 1: E_e = exp(N(0,1)), nu_e ~ U[0.25,0.35] */
+    int dirichlet;            /* samg_dirichlet on the x=0 face */
+    int load;                 /* samg_load */
+    double noise;             /* + U[-noise, noise] per DOF */
+    uint64_t seed;
+    int x_slowest;            /* node numbering: 0 = x fastest (reference) */
+} samg_problem_params;
+SAMG_API void samg_default_problem_params(samg_problem_params *p);
+SAMG_API int samg_generate_hex(const samg_problem_params *p, samg_problem **out);
+SAMG_API int samg_problem_destroy(samg_problem *p);
+/* n = scalar DOFs (3 per node kept), nbrows = n/3, nnzb 3x3 blocks */
+SAMG_API int samg_problem_info(const samg_problem *p, int64_t *n,
+        int64_t *nnzb, int64_t *nnodes);
+SAMG_API int samg_problem_get_bsr3(const samg_problem *p, int64_t *ptr,
+        int64_t *col, double *val);
+/* scalar CSR with every block entry kept (to_scalar, csr.hpp:327-353) */
+SAMG_API int samg_problem_get_csr(const samg_problem *p, int64_t *ptr,
+        int64_t *col, double *val);
+SAMG_API int samg_problem_get_rhs(const samg_problem *p, double *rhs);
+/* coordinates of the kept nodes, 3 per node */
+SAMG_API int samg_problem_get_coords(const samg_problem *p, double *xyz);
+/* rigid body modes (elasticity.hpp:38-52), column-major n-by-6 */
+SAMG_API int samg_rigid_body_modes(int64_t nnodes, const double *xyz,
+        double *B);
+/* borrow the problem's BSR arrays (no copy; valid until destroy) */
+SAMG_API int samg_problem_bsr3_view(const samg_problem *p, const int64_t **ptr,
+        const int64_t **col, const double **val);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SAMG_B200_H */

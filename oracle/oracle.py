@@ -305,8 +305,17 @@ class Ref(_Backend):
         lib.ref_spmv.argtypes = [vp, C.c_int, C.c_double, f64p, C.c_double, f64p]
         lib.ref_spmv_bsr3.argtypes = [C.c_int64, C.c_int64, i64p, i64p, f64p, C.c_double,
                                       f64p, C.c_double, f64p]
+        lib.ref_bsr3_create.argtypes = [C.c_int64, C.c_int64, i64p, i64p, f64p]
+        lib.ref_bsr3_create.restype = vp
+        lib.ref_bsr3_destroy.argtypes = [vp]
+        lib.ref_bsr3_spmv.argtypes = [vp, C.c_double, f64p, C.c_double, f64p]
         self.lib = lib
         self._err = lib.ref_last_error
+
+    def bsr3(self, nrows, ncols, ptr, col, val):
+        """A reference csr<static_block<3>> (rows [0, nrows) of the arrays;
+        ptr may be a slice of a larger matrix's ptr)."""
+        return RefBsr3(self, nrows, ncols, ptr, col, val)
 
     def generate_hex(self, nx, ny, nz, E=1.0, nu=0.3, clamp_x0=True) -> Problem:
         n = C.c_int64()
@@ -421,4 +430,26 @@ class RefHier:
         nr = self.level(level)[0]
         y = np.zeros(3 * nr) if y is None else np.array(y, dtype=np.float64)
         self.be._check(self.be.lib.ref_spmv(self.h, level, alpha, _p(x), beta, _p(y)))
+        return y
+
+
+class RefBsr3:
+    """Handle to a reference csr<block3>; spmv is samg::spmv (csr.hpp:129-160)."""
+
+    def __init__(self, be: Ref, nrows, ncols, ptr, col, val):
+        self.be = be
+        self.nrows, self.ncols = nrows, ncols
+        ptr = np.ascontiguousarray(ptr, np.int64)
+        col = np.ascontiguousarray(col, np.int64)
+        val = np.ascontiguousarray(val, np.float64)
+        self.h = be.lib.ref_bsr3_create(nrows, ncols, _p(ptr, i64p), _p(col, i64p), _p(val))
+
+    def __del__(self):
+        try:
+            self.be.lib.ref_bsr3_destroy(self.h)
+        except Exception:
+            pass
+
+    def spmv(self, x, y, alpha=1.0, beta=0.0):
+        self.be._check(self.be.lib.ref_bsr3_spmv(self.h, alpha, _p(x), beta, _p(y)))
         return y

@@ -328,6 +328,30 @@ int ref_spmv(void *hp, int level, double alpha, const double *x, double beta,
     GUARD_END
 }
 
+// A reference csr<static_block<3>> built once (timed spmv baseline).
+void *ref_bsr3_create(int64_t nrows, int64_t ncols, const int64_t *ptr, const int64_t *col,
+        const double *val) {
+    auto *A = new csr<block3>;
+    A->nrows = nrows;
+    A->ncols = ncols;
+    A->ptr.assign(ptr, ptr + nrows + 1);
+    A->col.assign(col + ptr[0], col + ptr[nrows]);
+    for (auto &p : A->ptr) p -= ptr[0];
+    A->val.resize(A->col.size());
+    std::memcpy(A->val.data(), val + 9 * ptr[0], sizeof(double) * 9 * A->col.size());
+    return A;
+}
+
+void ref_bsr3_destroy(void *A) { delete static_cast<csr<block3> *>(A); }
+
+int ref_bsr3_spmv(void *Ap, double alpha, const double *x, double beta, double *y) {
+    GUARD_BEGIN
+    const csr<block3> &A = *static_cast<csr<block3> *>(Ap);
+    spmv(alpha, A, std::span<const double>(x, A.scalar_cols()), beta,
+            std::span<double>(y, A.scalar_rows()));
+    GUARD_END
+}
+
 // Standalone spmv on caller-owned BSR3 arrays (no hierarchy).
 int ref_spmv_bsr3(int64_t nrows, int64_t ncols, const int64_t *ptr,
         const int64_t *col, const double *val, double alpha, const double *x,

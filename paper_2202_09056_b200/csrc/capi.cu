@@ -1,0 +1,650 @@
+// capi.cu -- the extern "C" boundary (include/samg_b200.h).
+//
+// Every entry point validates its arguments on the host first (so the
+// reference's typed errors surface without touching a GPU), then checks for
+// a CUDA device (SAMG_NO_DEVICE otherwise: there is no CPU fallback), then
+// runs on the handle's device and stream.  Exceptions become status codes
+// plus a thread-local message.
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "hierarchy.cuh"
+#include "problem.cuh"
+
+struct samg_bsr3 {
+    samgb::Bsr3 own;
+    const samgb::Bsr3 *m = nullptr;
+    int device = 0;
+    samgb::DevBuf<double> xs, ys;  // e2e staging for host-vector spmv
+};
+
+struct samg_hierarchy {
+    std::unique_ptr<samgb::Hierarchy> h;
+    std::vector<std::unique_ptr<samg_bsr3>> views;
+};
+
+namespace samgb {
+samg_problem *generate_hex(const samg_problem_params &p);
+void rigid_body_modes(int64_t nnodes, const double *xyz, double *B);
+}
+
+namespace {
+
+using namespace samgb;
+
+thread_local std::string g_err;
+
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+template <class F>
+int guarded(F f) {
+    try {
+        f();
+        g_err.clear();
+        return SAMG_OK;
+    } catch (const Error &e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::bad_alloc &) {
+        g_err = "host out of memory";
+        return SAMG_OUT_OF_MEMORY;
+    } catch (const std::exception &e) {
+        g_err = e.what();
+        return SAMG_ERROR;
+    }
+}
+
+void require(bool c, int code, const char *msg) {
+    if (!c) fail(code, msg);
+}
+
+void need_device(int device) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        fail(SAMG_NO_DEVICE, "no CUDA device available (the B200 path has no CPU fallback)");
+    }
+    require(device >= 0 && device < n, SAMG_INVALID_ARGUMENT, "device ordinal out of range");
+    CK(cudaSetDevice(device));
+}
+
+cudaStream_t new_stream() {
+    cudaStream_t s;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    return s;
+}
+
+void validate_params(const samg_amg_params *prm, int pipeline) {
+    require(prm != nullptr, SAMG_INVALID_ARGUMENT, "setup: params must not be NULL");
+    if (pipeline != SAMG_PIPELINE_NS_BLOCK)
+        fail(SAMG_UNSUPPORTED, "setup: only pipeline::ns_block is on the B200 path");
+    if (prm->smoother == SAMG_SMOOTHER_ILU0)
+        fail(SAMG_UNSUPPORTED, "setup: ILU(0) smoothing is not on the B200 path yet");
+    require(prm->smoother >= 0 && prm->smoother <= 2, SAMG_INVALID_ARGUMENT, "setup: unknown smoother");
+    require(prm->pre_sweeps >= 0 && prm->post_sweeps >= 0, SAMG_INVALID_ARGUMENT,
+            "setup: negative sweep count");
+}
+
+// hierarchy.hpp:267-282 + coarsening.hpp:269-270 checks
+void validate_ns(int64_t n, const double *B, int64_t b_rows, int64_t b_cols) {
+    require(n >= 0, SAMG_INVALID_ARGUMENT, "setup: negative dimension");
+    if (!B) fail(SAMG_BAD_NULLSPACE_SHAPE, "setup: pipeline requires a nullspace basis");
+    if (b_rows != n) fail(SAMG_BAD_NULLSPACE_SHAPE, "setup: nullspace rows do not match matrix");
+    if (n % 3) fail(SAMG_NOT_DIVISIBLE, "setup: block pipelines require dimension divisible by 3");
+    if (b_cols < 1 || b_cols % 3)
+        fail(SAMG_NOT_DIVISIBLE, "as_scalar_transfer: coarse dimension not divisible by block size");
+    if (b_cols > 12) fail(SAMG_UNSUPPORTED, "setup: at most 12 nullspace vectors");
+}
+
+template <class F>
+__global__ void k_apply(int64_t n, F f) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        f(i);
+}
+template <class F>
+void apply(int64_t n, F f, cudaStream_t s) {
+    if (n <= 0) return;
+    int64_t g = (n + 255) / 256;
+    if (g > 524280) g = 524280;
+    k_apply<<<static_cast<int>(g), 256, 0, s>>>(n, f);
+    CK_LAUNCH();
+}
+
+// upload a host int64 BSR3 into a device Bsr3 (int32), validating structure
+void upload_bsr3(int64_t nrows, int64_t ncols, const int64_t *ptr, const int64_t *col,
+                 const double *val, Bsr3 &M, cudaStream_t s) {
+    require(ptr && (ptr[nrows] == 0 || (col && val)), SAMG_INVALID_ARGUMENT, "bsr3: NULL array");
+    require(ptr[0] == 0, SAMG_INVALID_ARGUMENT, "bsr3: ptr[0] must be 0");
+    const int64_t nnz = ptr[nrows];
+    M.alloc(nrows, ncols, nnz, s);
+    DevBuf<int64_t> p64(nrows + 1, s), c64(nnz, s);
+    CK(cudaMemcpyAsync(p64.p, ptr, sizeof(int64_t) * (nrows + 1), cudaMemcpyHostToDevice, s));
+    if (nnz) {
+        CK(cudaMemcpyAsync(c64.p, col, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(M.val.p, val, sizeof(double) * 9 * nnz, cudaMemcpyHostToDevice, s));
+    }
+    DevBuf<int> bad(1, s);
+    CK(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
+    int *mp = M.ptr.p, *mc = M.col.p, *bp = bad.p;
+    const int64_t *pp = p64.p, *cp = c64.p;
+    apply(nrows + 1, [=] __device__(int64_t i) {
+        mp[i] = static_cast<int>(pp[i]);
+        if (i > 0 && pp[i] < pp[i - 1]) *bp = 1;
+    }, s);
+    apply(nrows, [=] __device__(int64_t i) {
+        for (int64_t j = pp[i]; j < pp[i + 1]; ++j) {
+            const int64_t c = cp[j];
+            if (c < 0 || c >= ncols || (j > pp[i] && c <= cp[j - 1])) *bp = 1;
+            mc[j] = static_cast<int>(c);
+        }
+    }, s);
+    int hbad = 0;
+    CK(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (hbad) fail(SAMG_INVALID_ARGUMENT, "bsr3: ptr must be nondecreasing and each row's columns strictly increasing and in range");
+}
+
+samgb::Hierarchy &H(samg_hierarchy *h) {
+    if (!h || !h->h) fail(SAMG_INVALID_ARGUMENT, "NULL hierarchy handle");
+    CK(cudaSetDevice(h->h->device));
+    return *h->h;
+}
+const samgb::Hierarchy &Hc(const samg_hierarchy *h) {
+    if (!h || !h->h) fail(SAMG_INVALID_ARGUMENT, "NULL hierarchy handle");
+    return *h->h;
+}
+
+const Bsr3 &level_mat(const samgb::Hierarchy &h, int level, int which) {
+    if (level < 0 || level >= static_cast<int>(h.levels.size()))
+        fail(SAMG_INVALID_ARGUMENT, "level out of range");
+    const Level &lv = h.levels[level];
+    if (which == 0) return lv.A;
+    if (!lv.has_transfer) fail(SAMG_INVALID_ARGUMENT, "coarsest level has no P/R");
+    if (which == 1) return lv.P;
+    if (which == 2) return lv.R;
+    fail(SAMG_INVALID_ARGUMENT, "which must be 0 (A), 1 (P) or 2 (R)");
+}
+
+void download_bsr3(const Bsr3 &M, int64_t *ptr, int64_t *col, double *val, cudaStream_t s) {
+    std::vector<int> p(M.nrows + 1), c(M.nnzb);
+    CK(cudaMemcpyAsync(p.data(), M.ptr.p, sizeof(int) * (M.nrows + 1), cudaMemcpyDeviceToHost, s));
+    if (M.nnzb) {
+        CK(cudaMemcpyAsync(c.data(), M.col.p, sizeof(int) * M.nnzb, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(val, M.val.p, sizeof(double) * 9 * M.nnzb, cudaMemcpyDeviceToHost, s));
+    }
+    CK(cudaStreamSynchronize(s));
+    for (int64_t i = 0; i <= M.nrows; ++i) ptr[i] = p[i];
+    for (int64_t i = 0; i < M.nnzb; ++i) col[i] = c[i];
+}
+
+samg_hierarchy *finish_setup(Bsr3 &&A0, const double *B, int64_t b_rows, int64_t b_cols,
+                             const samg_amg_params &prm, cudaStream_t s, double t0) {
+    auto out = std::make_unique<samg_hierarchy>();
+    try {
+        out->h.reset(setup_hierarchy(std::move(A0), B, b_rows, b_cols, prm, s, t0));
+    } catch (...) {
+        cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+        throw;
+    }
+    return out.release();
+}
+
+} // namespace
+
+extern "C" {
+
+SAMG_API void samg_default_amg_params(samg_amg_params *p) {
+    if (!p) return;
+    p->eps_strong = 0.08;
+    p->omega = 2.0 / 3.0;
+    p->point_block_size = 3;
+    p->smoother = SAMG_SMOOTHER_SPAI0;
+    p->smoother_omega = 0.72;
+    p->pre_sweeps = 1;
+    p->post_sweeps = 1;
+    p->coarse_enough = 3000;
+    p->stagnation_ratio = 0.8;
+    p->verify_galerkin = 0;
+    p->device = 0;
+}
+
+SAMG_API void samg_default_cg_params(samg_cg_params *p) {
+    if (!p) return;
+    p->tol = 1e-8;
+    p->max_iterations = 1000;
+}
+
+SAMG_API const char *samg_last_error(void) { return g_err.c_str(); }
+
+SAMG_API const char *samg_status_name(int st) {
+    switch (st) {
+        case SAMG_OK: return "ok";
+        case SAMG_ERROR: return "error";
+        case SAMG_DIMENSION_MISMATCH: return "dimension_mismatch";
+        case SAMG_NOT_DIVISIBLE: return "not_divisible";
+        case SAMG_SINGULAR_BLOCK: return "singular_block";
+        case SAMG_MISSING_DIAGONAL: return "missing_diagonal";
+        case SAMG_ZERO_DIAGONAL: return "zero_diagonal";
+        case SAMG_NON_SQUARE: return "non_square";
+        case SAMG_BAD_NULLSPACE_SHAPE: return "bad_nullspace_shape";
+        case SAMG_BREAKDOWN_NON_SPD: return "breakdown_non_spd";
+        case SAMG_INVALID_MATERIAL: return "invalid_material";
+        case SAMG_SHAPE_MISMATCH: return "shape_mismatch";
+        case SAMG_CUDA_ERROR: return "cuda_error";
+        case SAMG_NCCL_ERROR: return "nccl_error";
+        case SAMG_OUT_OF_MEMORY: return "out_of_memory";
+        case SAMG_NO_DEVICE: return "no_device";
+        case SAMG_UNSUPPORTED: return "unsupported";
+        case SAMG_INVALID_ARGUMENT: return "invalid_argument";
+        default: return "unknown";
+    }
+}
+
+SAMG_API int samg_device_count(int *count) {
+    return guarded([&] {
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess) { cudaGetLastError(); n = 0; }
+        *count = n;
+    });
+}
+
+SAMG_API int samg_setup(int64_t n, const int64_t *ptr, const int64_t *col, const double *val,
+                        const double *B, int64_t b_rows, int64_t b_cols, int pipeline,
+                        const samg_amg_params *prm, samg_hierarchy **out) {
+    return guarded([&] {
+        const double t0 = now_s();
+        require(out != nullptr, SAMG_INVALID_ARGUMENT, "setup: out must not be NULL");
+        *out = nullptr;
+        validate_params(prm, pipeline);
+        validate_ns(n, B, b_rows, b_cols);
+        require(ptr && ptr[0] == 0 && (ptr[n] == 0 || (col && val)), SAMG_INVALID_ARGUMENT,
+                "setup: malformed CSR arrays");
+        need_device(prm->device);
+        cudaStream_t s = new_stream();
+        Bsr3 A0;
+        try {
+            const int64_t nnz = ptr[n];
+            DevBuf<int64_t> dp(n + 1, s), dc(nnz, s);
+            DevBuf<double> dv(nnz, s);
+            CK(cudaMemcpyAsync(dp.p, ptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, s));
+            if (nnz) {
+                CK(cudaMemcpyAsync(dc.p, col, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, s));
+                CK(cudaMemcpyAsync(dv.p, val, sizeof(double) * nnz, cudaMemcpyHostToDevice, s));
+            }
+            scalar_to_bsr3(n, dp.p, dc.p, dv.p, A0, s);
+        } catch (...) {
+            cudaStreamSynchronize(s);
+            cudaStreamDestroy(s);
+            throw;
+        }
+        *out = finish_setup(std::move(A0), B, b_rows, b_cols, *prm, s, t0);
+    });
+}
+
+SAMG_API int samg_setup_bsr3(int64_t nbrows, const int64_t *ptr, const int64_t *col,
+                             const double *val, const double *B, int64_t b_rows, int64_t b_cols,
+                             int pipeline, const samg_amg_params *prm, samg_hierarchy **out) {
+    return guarded([&] {
+        const double t0 = now_s();
+        require(out != nullptr, SAMG_INVALID_ARGUMENT, "setup: out must not be NULL");
+        *out = nullptr;
+        validate_params(prm, pipeline);
+        validate_ns(3 * nbrows, B, b_rows, b_cols);
+        need_device(prm->device);
+        cudaStream_t s = new_stream();
+        Bsr3 A0;
+        try {
+            upload_bsr3(nbrows, nbrows, ptr, col, val, A0, s);
+        } catch (...) {
+            cudaStreamSynchronize(s);
+            cudaStreamDestroy(s);
+            throw;
+        }
+        *out = finish_setup(std::move(A0), B, b_rows, b_cols, *prm, s, t0);
+    });
+}
+
+SAMG_API int samg_destroy(samg_hierarchy *h) {
+    return guarded([&] {
+        if (!h) return;
+        if (h->h) cudaSetDevice(h->h->device);
+        delete h;
+    });
+}
+
+SAMG_API int samg_cg_solve(samg_hierarchy *hp, const double *f, double *u,
+                           const samg_cg_params *prm, samg_solve_report *rep) {
+    return guarded([&] {
+        require(f && u && prm && rep, SAMG_INVALID_ARGUMENT, "cg_solve: NULL argument");
+        samgb::Hierarchy &h = H(hp);
+        const double t0 = now_s();
+        const int64_t n = h.finest_dim();
+        CK(cudaMemcpyAsync(h.fbuf.p, f, sizeof(double) * n, cudaMemcpyHostToDevice, h.stream));
+        *rep = h.cg(h.fbuf.p, h.ubuf.p, *prm);
+        CK(cudaMemcpyAsync(u, h.ubuf.p, sizeof(double) * n, cudaMemcpyDeviceToHost, h.stream));
+        CK(cudaStreamSynchronize(h.stream));
+        rep->solve_seconds = now_s() - t0;
+    });
+}
+
+SAMG_API int samg_cg_solve_device(samg_hierarchy *hp, const double *d_f, double *d_u,
+                                  const samg_cg_params *prm, samg_solve_report *rep) {
+    return guarded([&] {
+        require(d_f && d_u && prm && rep, SAMG_INVALID_ARGUMENT, "cg_solve: NULL argument");
+        samgb::Hierarchy &h = H(hp);
+        *rep = h.cg(d_f, d_u, *prm);
+    });
+}
+
+SAMG_API int samg_vcycle(samg_hierarchy *hp, const double *f, double *u) {
+    return guarded([&] {
+        require(f && u, SAMG_INVALID_ARGUMENT, "vcycle: NULL argument");
+        samgb::Hierarchy &h = H(hp);
+        const int64_t n = h.finest_dim();
+        CK(cudaMemcpyAsync(h.fbuf.p, f, sizeof(double) * n, cudaMemcpyHostToDevice, h.stream));
+        CK(cudaMemcpyAsync(h.ubuf.p, u, sizeof(double) * n, cudaMemcpyHostToDevice, h.stream));
+        h.vcycle(h.fbuf.p, h.ubuf.p, false);
+        CK(cudaMemcpyAsync(u, h.ubuf.p, sizeof(double) * n, cudaMemcpyDeviceToHost, h.stream));
+        CK(cudaStreamSynchronize(h.stream));
+    });
+}
+
+SAMG_API int samg_vcycle_device(samg_hierarchy *hp, const double *d_f, double *d_u) {
+    return guarded([&] {
+        require(d_f && d_u, SAMG_INVALID_ARGUMENT, "vcycle: NULL argument");
+        samgb::Hierarchy &h = H(hp);
+        h.vcycle(d_f, d_u, false);
+        CK(cudaStreamSynchronize(h.stream));
+    });
+}
+
+SAMG_API int samg_memory_footprint(const samg_hierarchy *h, uint64_t *bytes) {
+    return guarded([&] { *bytes = Hc(h).memory_footprint(); });
+}
+SAMG_API int samg_finest_dim(const samg_hierarchy *h, int64_t *n) {
+    return guarded([&] { *n = Hc(h).finest_dim(); });
+}
+SAMG_API int samg_num_levels(const samg_hierarchy *h, int *nl) {
+    return guarded([&] { *nl = static_cast<int>(Hc(h).levels.size()); });
+}
+SAMG_API int samg_coarse_dim(const samg_hierarchy *h, int64_t *n) {
+    return guarded([&] { *n = Hc(h).nc; });
+}
+SAMG_API int samg_setup_seconds(const samg_hierarchy *h, double *sec) {
+    return guarded([&] { *sec = Hc(h).setup_seconds; });
+}
+
+SAMG_API int samg_level_info(const samg_hierarchy *h, int level, int which, int64_t *nrows,
+                             int64_t *ncols, int64_t *nnzb) {
+    return guarded([&] {
+        const Bsr3 &M = level_mat(Hc(h), level, which);
+        *nrows = M.nrows;
+        *ncols = M.ncols;
+        *nnzb = M.nnzb;
+    });
+}
+
+SAMG_API int samg_get_level(const samg_hierarchy *hp, int level, int which, int64_t *ptr,
+                            int64_t *col, double *val) {
+    return guarded([&] {
+        const samgb::Hierarchy &h = Hc(hp);
+        CK(cudaSetDevice(h.device));
+        download_bsr3(level_mat(h, level, which), ptr, col, val, h.stream);
+    });
+}
+
+SAMG_API int samg_level_matrix(samg_hierarchy *hp, int level, int which, const samg_bsr3 **m) {
+    return guarded([&] {
+        const samgb::Hierarchy &h = Hc(hp);
+        auto v = std::make_unique<samg_bsr3>();
+        v->m = &level_mat(h, level, which);
+        v->device = h.device;
+        *m = v.get();
+        hp->views.push_back(std::move(v));
+    });
+}
+
+SAMG_API int samg_aggregates_info(const samg_hierarchy *hp, int level, int64_t *nnodes,
+                                  int64_t *count) {
+    return guarded([&] {
+        const samgb::Hierarchy &h = Hc(hp);
+        if (level < 0 || level + 1 >= static_cast<int>(h.levels.size()))
+            fail(SAMG_INVALID_ARGUMENT, "level has no aggregates");
+        *nnodes = h.levels[level].nnodes;
+        *count = h.levels[level].naggs;
+    });
+}
+
+SAMG_API int samg_get_aggregates(const samg_hierarchy *hp, int level, int64_t *id) {
+    return guarded([&] {
+        const samgb::Hierarchy &h = Hc(hp);
+        if (level < 0 || level + 1 >= static_cast<int>(h.levels.size()))
+            fail(SAMG_INVALID_ARGUMENT, "level has no aggregates");
+        CK(cudaSetDevice(h.device));
+        const Level &lv = h.levels[level];
+        std::vector<int> a(lv.nnodes);
+        CK(cudaMemcpyAsync(a.data(), lv.agg.p, sizeof(int) * lv.nnodes, cudaMemcpyDeviceToHost, h.stream));
+        CK(cudaStreamSynchronize(h.stream));
+        for (int64_t i = 0; i < lv.nnodes; ++i) id[i] = a[i];
+    });
+}
+
+SAMG_API int samg_smoother_info(const samg_hierarchy *hp, int level, int64_t *len) {
+    return guarded([&] {
+        const samgb::Hierarchy &h = Hc(hp);
+        if (level < 0 || level + 1 >= static_cast<int>(h.levels.size()))
+            fail(SAMG_INVALID_ARGUMENT, "level has no smoother");
+        *len = static_cast<int64_t>(h.levels[level].M.data.n);
+    });
+}
+
+SAMG_API int samg_get_smoother(const samg_hierarchy *hp, int level, double *data) {
+    return guarded([&] {
+        const samgb::Hierarchy &h = Hc(hp);
+        if (level < 0 || level + 1 >= static_cast<int>(h.levels.size()))
+            fail(SAMG_INVALID_ARGUMENT, "level has no smoother");
+        CK(cudaSetDevice(h.device));
+        const Smoother &M = h.levels[level].M;
+        CK(cudaMemcpyAsync(data, M.data.p, M.data.bytes(), cudaMemcpyDeviceToHost, h.stream));
+        CK(cudaStreamSynchronize(h.stream));
+    });
+}
+
+SAMG_API int samg_bsr3_create(int64_t nrows, int64_t ncols, const int64_t *ptr, const int64_t *col,
+                              const double *val, int device, samg_bsr3 **out) {
+    return guarded([&] {
+        require(out != nullptr && nrows >= 0 && ncols >= 0, SAMG_INVALID_ARGUMENT, "bsr3_create: bad arguments");
+        *out = nullptr;
+        need_device(device);
+        auto m = std::make_unique<samg_bsr3>();
+        m->device = device;
+        upload_bsr3(nrows, ncols, ptr, col, val, m->own, nullptr);
+        CK(cudaDeviceSynchronize());
+        m->m = &m->own;
+        *out = m.release();
+    });
+}
+
+SAMG_API int samg_bsr3_destroy(samg_bsr3 *m) {
+    return guarded([&] {
+        if (!m) return;
+        cudaSetDevice(m->device);
+        cudaDeviceSynchronize();
+        delete m;
+    });
+}
+
+SAMG_API int samg_bsr3_info(const samg_bsr3 *m, int64_t *nrows, int64_t *ncols, int64_t *nnzb) {
+    return guarded([&] {
+        require(m && m->m, SAMG_INVALID_ARGUMENT, "NULL matrix");
+        *nrows = m->m->nrows;
+        *ncols = m->m->ncols;
+        *nnzb = m->m->nnzb;
+    });
+}
+
+SAMG_API int samg_bsr3_download(const samg_bsr3 *m, int64_t *ptr, int64_t *col, double *val) {
+    return guarded([&] {
+        require(m && m->m, SAMG_INVALID_ARGUMENT, "NULL matrix");
+        CK(cudaSetDevice(m->device));
+        CK(cudaDeviceSynchronize());
+        download_bsr3(*m->m, ptr, col, val, nullptr);
+    });
+}
+
+SAMG_API int samg_bsr3_spmv_device(const samg_bsr3 *m, double alpha, const double *d_x,
+                                   double beta, double *d_y, void *stream) {
+    return guarded([&] {
+        require(m && m->m, SAMG_INVALID_ARGUMENT, "NULL matrix");
+        launch_spmv(*m->m, alpha, d_x, beta, d_y, static_cast<cudaStream_t>(stream));
+    });
+}
+
+SAMG_API int samg_bsr3_spmv(const samg_bsr3 *mc, double alpha, const double *x, double beta,
+                            double *y) {
+    return guarded([&] {
+        require(mc && mc->m && x && y, SAMG_INVALID_ARGUMENT, "spmv: NULL argument");
+        auto *m = const_cast<samg_bsr3 *>(mc);
+        CK(cudaSetDevice(m->device));
+        const Bsr3 &A = *m->m;
+        if (m->xs.n < static_cast<size_t>(3 * A.ncols)) m->xs.alloc(3 * A.ncols, nullptr);
+        if (m->ys.n < static_cast<size_t>(3 * A.nrows)) m->ys.alloc(3 * A.nrows, nullptr);
+        CK(cudaMemcpyAsync(m->xs.p, x, sizeof(double) * 3 * A.ncols, cudaMemcpyHostToDevice, nullptr));
+        if (beta != 0.0)
+            CK(cudaMemcpyAsync(m->ys.p, y, sizeof(double) * 3 * A.nrows, cudaMemcpyHostToDevice, nullptr));
+        launch_spmv(A, alpha, m->xs.p, beta, m->ys.p, nullptr);
+        CK(cudaMemcpyAsync(y, m->ys.p, sizeof(double) * 3 * A.nrows, cudaMemcpyDeviceToHost, nullptr));
+        CK(cudaStreamSynchronize(nullptr));
+    });
+}
+
+SAMG_API int samg_bsr3_galerkin(const samg_bsr3 *R, const samg_bsr3 *A, const samg_bsr3 *P,
+                                samg_bsr3 **out) {
+    return guarded([&] {
+        require(R && A && P && out && R->m && A->m && P->m, SAMG_INVALID_ARGUMENT, "galerkin: NULL argument");
+        *out = nullptr;
+        if (R->m->ncols != A->m->nrows || A->m->ncols != P->m->nrows)
+            fail(SAMG_DIMENSION_MISMATCH, "spgemm: inner dimensions disagree");
+        CK(cudaSetDevice(A->device));
+        auto c = std::make_unique<samg_bsr3>();
+        c->device = A->device;
+        Bsr3 RA;
+        spgemm(*R->m, *A->m, RA, nullptr);
+        spgemm(RA, *P->m, c->own, nullptr);
+        CK(cudaDeviceSynchronize());
+        c->m = &c->own;
+        *out = c.release();
+    });
+}
+
+SAMG_API int samg_bsr3_spmv_bytes(const samg_bsr3 *m, int beta_nonzero, uint64_t *bytes) {
+    return guarded([&] {
+        require(m && m->m && bytes, SAMG_INVALID_ARGUMENT, "NULL argument");
+        const Bsr3 &A = *m->m;
+        // nnzb*(72 + 4) + (nrows+1)*4 + x once + y write (+ y read)
+        *bytes = static_cast<uint64_t>(A.nnzb) * 76 + static_cast<uint64_t>(A.nrows + 1) * 4 +
+                 static_cast<uint64_t>(A.ncols) * 24 + static_cast<uint64_t>(A.nrows) * 24 *
+                 (beta_nonzero ? 2 : 1);
+    });
+}
+
+SAMG_API void samg_default_problem_params(samg_problem_params *p) {
+    if (!p) return;
+    std::memset(p, 0, sizeof *p);
+    p->nx = p->ny = p->nz = 19;
+    p->lx = p->ly = p->lz = 1.0;
+    p->E = 1.0;
+    p->nu = 0.3;
+    p->dirichlet = SAMG_DIRICHLET_ELIMINATE;
+    p->load = SAMG_LOAD_BODY_FORCE;
+    p->seed = 12345;
+}
+
+SAMG_API int samg_generate_hex(const samg_problem_params *p, samg_problem **out) {
+    return guarded([&] {
+        require(p && out, SAMG_INVALID_ARGUMENT, "generate_hex: NULL argument");
+        *out = generate_hex(*p);
+    });
+}
+
+SAMG_API int samg_problem_destroy(samg_problem *p) {
+    return guarded([&] { delete p; });
+}
+
+SAMG_API int samg_problem_info(const samg_problem *p, int64_t *n, int64_t *nnzb, int64_t *nnodes) {
+    return guarded([&] {
+        require(p != nullptr, SAMG_INVALID_ARGUMENT, "NULL problem");
+        *n = p->n;
+        *nnzb = p->ptr.back();
+        *nnodes = p->nnodes;
+    });
+}
+
+SAMG_API int samg_problem_get_bsr3(const samg_problem *p, int64_t *ptr, int64_t *col, double *val) {
+    return guarded([&] {
+        require(p != nullptr, SAMG_INVALID_ARGUMENT, "NULL problem");
+        std::memcpy(ptr, p->ptr.data(), sizeof(int64_t) * p->ptr.size());
+        std::memcpy(col, p->col.data(), sizeof(int64_t) * p->col.size());
+        std::memcpy(val, p->val.data(), sizeof(double) * p->val.size());
+    });
+}
+
+SAMG_API int samg_problem_bsr3_view(const samg_problem *p, const int64_t **ptr,
+                                    const int64_t **col, const double **val) {
+    return guarded([&] {
+        require(p != nullptr, SAMG_INVALID_ARGUMENT, "NULL problem");
+        *ptr = p->ptr.data();
+        *col = p->col.data();
+        *val = p->val.data();
+    });
+}
+
+SAMG_API int samg_problem_get_csr(const samg_problem *p, int64_t *ptr, int64_t *col, double *val) {
+    return guarded([&] {
+        require(p != nullptr, SAMG_INVALID_ARGUMENT, "NULL problem");
+        // to_scalar (csr.hpp:327-353)
+        int64_t out = 0;
+        ptr[0] = 0;
+        const int64_t nb = p->nnodes;
+        for (int64_t bi = 0; bi < nb; ++bi)
+            for (int r = 0; r < 3; ++r) {
+                for (int64_t j = p->ptr[bi]; j < p->ptr[bi + 1]; ++j)
+                    for (int c = 0; c < 3; ++c) {
+                        col[out] = 3 * p->col[j] + c;
+                        val[out] = p->val[9 * j + 3 * r + c];
+                        ++out;
+                    }
+                ptr[3 * bi + r + 1] = out;
+            }
+    });
+}
+
+SAMG_API int samg_problem_get_rhs(const samg_problem *p, double *rhs) {
+    return guarded([&] {
+        require(p != nullptr, SAMG_INVALID_ARGUMENT, "NULL problem");
+        std::memcpy(rhs, p->rhs.data(), sizeof(double) * p->rhs.size());
+    });
+}
+
+SAMG_API int samg_problem_get_coords(const samg_problem *p, double *xyz) {
+    return guarded([&] {
+        require(p != nullptr, SAMG_INVALID_ARGUMENT, "NULL problem");
+        std::memcpy(xyz, p->xyz.data(), sizeof(double) * p->xyz.size());
+    });
+}
+
+SAMG_API int samg_rigid_body_modes(int64_t nnodes, const double *xyz, double *B) {
+    return guarded([&] {
+        require(xyz && B && nnodes >= 0, SAMG_INVALID_ARGUMENT, "rigid_body_modes: bad arguments");
+        rigid_body_modes(nnodes, xyz, B);
+    });
+}
+
+} // extern "C"

@@ -1,0 +1,81 @@
+// common.cuh -- error plumbing, device buffers and launch helpers shared by
+// the solve kernels (solve.cu), the setup kernels (setup.cu) and the host
+// runtime (hierarchy.cu, capi.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <utility>
+
+#include "samg_b200.h"
+
+namespace samgb {
+
+// Typed error carrying a samg_status; thrown by host code, translated at
+// the C-ABI edge (capi.cu).  Mirrors samg::error's hierarchy by code.
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(int code, const std::string &msg) { throw Error(code, msg); }
+
+inline void cuda_check(cudaError_t e, const char *what, const char *file, int line) {
+    if (e == cudaSuccess) return;
+    char buf[512];
+    snprintf(buf, sizeof buf, "%s failed: %s (%s:%d)", what, cudaGetErrorString(e), file, line);
+    throw Error(e == cudaErrorMemoryAllocation ? SAMG_OUT_OF_MEMORY : SAMG_CUDA_ERROR, buf);
+}
+#define CK(x) ::samgb::cuda_check((x), #x, __FILE__, __LINE__)
+#define CK_LAUNCH() ::samgb::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+
+// Device error word written by kernels that detect reference exceptions
+// (zero filtered diagonal, singular pivot, ...).  First code wins.
+struct DevError {
+    int code;
+    int64_t where;
+};
+
+// RAII device buffer (stream-ordered allocation).
+template <class T>
+struct DevBuf {
+    T *p = nullptr;
+    size_t n = 0;
+    cudaStream_t s = nullptr;
+    DevBuf() = default;
+    explicit DevBuf(size_t count, cudaStream_t st = nullptr) { alloc(count, st); }
+    DevBuf(const DevBuf &) = delete;
+    DevBuf &operator=(const DevBuf &) = delete;
+    DevBuf(DevBuf &&o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+    DevBuf &operator=(DevBuf &&o) noexcept {
+        if (this != &o) { release(); p = o.p; n = o.n; s = o.s; o.p = nullptr; o.n = 0; }
+        return *this;
+    }
+    ~DevBuf() { release(); }
+    void alloc(size_t count, cudaStream_t st = nullptr) {
+        release();
+        s = st;
+        n = count;
+        if (count) CK(cudaMallocAsync(&p, count * sizeof(T), st));
+    }
+    void release() {
+        if (p) cudaFreeAsync(p, s);
+        p = nullptr;
+        n = 0;
+    }
+    size_t bytes() const { return n * sizeof(T); }
+    T *get() const { return p; }
+};
+
+constexpr int kWarp = 32;
+
+inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
+
+// SM count of the current device (cached per process).
+int sm_count();
+
+} // namespace samgb

@@ -1,0 +1,268 @@
+// hierarchy.cu -- host orchestration of the ns_block setup loop
+// (hierarchy.hpp:331-380), the V-cycle (hierarchy.hpp:408-441) and PCG
+// (cg.hpp:39-112).  All level data stays in HBM; the host only sequences
+// kernels on one stream and reads back sizes and the CG residual.
+#include "hierarchy.cuh"
+
+#include <chrono>
+#include <cmath>
+#include <memory>
+#include <utility>
+
+namespace samgb {
+
+int sm_count() {
+    static int n = [] {
+        int dev = 0, v = 148;
+        if (cudaGetDevice(&dev) == cudaSuccess)
+            cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    return n;
+}
+
+namespace {
+
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// matrix_bytes (csr.hpp:360-365): 8-byte indices, 72-byte blocks
+uint64_t matrix_bytes(const Bsr3 &A) {
+    return static_cast<uint64_t>(A.nrows + 1) * 8 + static_cast<uint64_t>(A.nnzb) * 8 +
+           static_cast<uint64_t>(A.nnzb) * 72;
+}
+
+} // namespace
+
+Hierarchy::~Hierarchy() {
+    if (stream) cudaStreamSynchronize(stream);
+    levels.clear();
+    Ainv.release();
+    r.release(); z.release(); p.release(); q.release();
+    fbuf.release(); ubuf.release(); partials.release(); sc.release(); err.release();
+    if (sc_host) cudaFreeHost(sc_host);
+    if (stream && owns_stream) {
+        cudaStreamSynchronize(stream);
+        cudaStreamDestroy(stream);
+    }
+}
+
+uint64_t Hierarchy::memory_footprint() const {
+    // memory_footprint (hierarchy.hpp:443-458)
+    uint64_t bytes = 0;
+    for (const Level &lv : levels) {
+        bytes += matrix_bytes(lv.A);
+        if (lv.has_transfer) {
+            bytes += matrix_bytes(lv.P);
+            bytes += matrix_bytes(lv.R);
+        }
+        bytes += lv.M.data.n * 8;
+    }
+    bytes += static_cast<uint64_t>(nc) * nc * 8;
+    return bytes;
+}
+
+Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int64_t b_cols,
+                           const samg_amg_params &prm, cudaStream_t s, double t_start) {
+    auto H = std::make_unique<Hierarchy>();
+    H->stream = s;
+    H->prm = prm;
+    CK(cudaGetDevice(&H->device));
+    H->err.alloc(1, s);
+    CK(cudaMemsetAsync(H->err.p, 0, sizeof(DevError), s));
+    DevError *err = H->err.p;
+
+    const int k = static_cast<int>(b_cols);
+    DevBuf<double> B(b_rows * b_cols, s);
+    CK(cudaMemcpyAsync(B.p, B_host, sizeof(double) * b_rows * b_cols, cudaMemcpyHostToDevice, s));
+
+    H->levels.emplace_back();
+    H->levels.back().A = std::move(A0);
+    // level loop (hierarchy.hpp:338-363)
+    while (3 * H->levels.back().A.nrows > prm.coarse_enough) {
+        Level &Li = H->levels.back();
+        const int pbs = H->levels.size() == 1 ? prm.point_block_size : k;
+        if (pbs % 3) fail(SAMG_NOT_DIVISIBLE, "ns_block: node size must be a multiple of 3");
+        const int h = pbs / 3;
+        if (Li.A.nrows % h)
+            fail(SAMG_NOT_DIVISIBLE, "strength_graph: rows not divisible by point block size");
+        Graph G;
+        strength_graph(Li.A, h, prm.eps_strong, G, s);
+        DevBuf<int> agg;
+        const int64_t naggs = aggregate(G, agg, s);
+        DevBuf<double> Pt, Bc;
+        tentative(agg, G.nnodes, naggs, pbs, B.p, k, Pt, Bc, err, s);
+        Bsr3 P;
+        smooth_prolongation(Li.A, G, agg, naggs, pbs, k, Pt.p, prm.omega, P, err, s);
+        check_dev_error(err, s);
+        // stagnation guard (hierarchy.hpp:355)
+        if (static_cast<double>(3 * P.ncols) >
+            prm.stagnation_ratio * static_cast<double>(3 * Li.A.nrows))
+            break;
+        Bsr3 R;
+        transpose(P, R, s);
+        // Galerkin (csr.hpp:259-262) + fix_decoupled_rows (hierarchy.hpp:357)
+        Bsr3 RA, Ac;
+        spgemm(R, Li.A, RA, s);
+        spgemm(RA, P, Ac, s);
+        RA = Bsr3();
+        fix_decoupled_rows(Ac, s);
+        Li.P = std::move(P);
+        Li.R = std::move(R);
+        Li.has_transfer = true;
+        Li.agg = std::move(agg);
+        Li.nnodes = G.nnodes;
+        Li.naggs = naggs;
+        B = std::move(Bc);
+        b_rows = naggs * k;
+        H->levels.emplace_back();
+        H->levels.back().A = std::move(Ac);
+    }
+    B.release();
+    const size_t L = H->levels.size();
+    for (size_t i = 0; i + 1 < L; ++i)
+        setup_smoother(H->levels[i].A, prm.smoother, prm.smoother_omega, H->levels[i].M, err, s);
+    check_dev_error(err, s);
+    H->nc = 3 * H->levels.back().A.nrows;
+    dense_inverse(H->levels.back().A, H->Ainv, err, s);
+    // V-cycle / CG workspace
+    for (size_t i = 0; i < L; ++i) {
+        Level &lv = H->levels[i];
+        const int64_t n = 3 * lv.A.nrows;
+        lv.f.alloc(n, s); lv.u.alloc(n, s); lv.r.alloc(n, s); lv.t.alloc(n, s);
+    }
+    const int64_t n0 = H->finest_dim();
+    H->r.alloc(n0, s); H->z.alloc(n0, s); H->p.alloc(n0, s); H->q.alloc(n0, s);
+    H->fbuf.alloc(n0, s); H->ubuf.alloc(n0, s);
+    const int64_t np = std::max<int64_t>(kRedBlocks, (H->levels.front().A.nrows * 32 + 255) / 256 + 1);
+    H->partials.alloc(np, s);
+    H->sc.alloc(1, s);
+    CK(cudaMemsetAsync(H->sc.p, 0, sizeof(CgScalars), s));
+    CK(cudaMallocHost(&H->sc_host, sizeof(CgScalars)));
+    CK(cudaStreamSynchronize(s));
+    H->setup_seconds = now_s() - t_start;
+    H->owns_stream = true;
+    return H.release();
+}
+
+// V-cycle (hierarchy.hpp:408-441).  With zero_guess the pre-smoother's first
+// sweep needs no SpMV (r = f - A*0 = f exactly), as inside CG (cg.hpp:98-101)
+// and on every level > 0 (hierarchy.hpp:426).
+void Hierarchy::vcycle(const double *f0, double *u0, bool zero_guess) {
+    cudaStream_t s = stream;
+    const size_t L = levels.size();
+    if (L == 1) {
+        launch_dense_gemv(nc, Ainv.p, f0, u0, s);
+        return;
+    }
+    std::vector<double *> cur(L);
+    for (size_t i = 0; i + 1 < L; ++i) {
+        Level &lv = levels[i];
+        const double *fi = i == 0 ? f0 : lv.f.p;
+        double *a = lv.u.p, *b = lv.t.p;
+        int sweeps = prm.pre_sweeps;
+        const bool zero = (i > 0) || zero_guess;
+        if (!zero) CK(cudaMemcpyAsync(a, u0, sizeof(double) * 3 * lv.A.nrows, cudaMemcpyDeviceToDevice, s));
+        if (zero) {
+            if (sweeps > 0) {
+                launch_smooth_zero(lv.A.nrows, lv.M, fi, a, s);
+                --sweeps;
+            } else {
+                launch_fill(3 * lv.A.nrows, 0.0, a, s);
+            }
+        }
+        for (; sweeps > 0; --sweeps) {
+            launch_smooth(lv.A, lv.M, fi, a, b, s);
+            std::swap(a, b);
+        }
+        launch_residual(lv.A, fi, a, lv.r.p, s);
+        launch_spmv(lv.R, 1.0, lv.r.p, 0.0, levels[i + 1].f.p, s);
+        cur[i] = a;
+    }
+    launch_dense_gemv(nc, Ainv.p, levels[L - 1].f.p, levels[L - 1].u.p, s);
+    cur[L - 1] = levels[L - 1].u.p;
+    for (size_t ii = L - 1; ii-- > 0;) {
+        Level &lv = levels[ii];
+        const double *fi = ii == 0 ? f0 : lv.f.p;
+        double *a = cur[ii];
+        double *b = (a == lv.u.p) ? lv.t.p : lv.u.p;
+        launch_spmv(lv.P, 1.0, cur[ii + 1], 1.0, a, s);
+        for (int sw = prm.post_sweeps; sw > 0; --sw) {
+            double *out = (ii == 0 && sw == 1) ? u0 : b;
+            launch_smooth(lv.A, lv.M, fi, a, out, s);
+            b = a;
+            a = out;
+        }
+        cur[ii] = a;
+    }
+    if (cur[0] != u0)
+        CK(cudaMemcpyAsync(u0, cur[0], sizeof(double) * finest_dim(), cudaMemcpyDeviceToDevice, s));
+}
+
+// PCG from a zero guess (cg_solve_op, cg.hpp:39-83, and cg_solve(hierarchy),
+// cg.hpp:87-112).  alpha/beta stay on the device; the host reads the
+// recurrence residual once per iteration for the stopping test.
+samg_solve_report Hierarchy::cg(const double *d_f, double *d_u, const samg_cg_params &cp) {
+    cudaStream_t s = stream;
+    const double t0 = now_s();
+    samg_solve_report rep{};
+    rep.variant = SAMG_PIPELINE_NS_BLOCK;
+    rep.setup_seconds = setup_seconds;
+    const int64_t n = finest_dim();
+    const Bsr3 &A0 = levels.front().A;
+    double *pr = r.p, *pz = z.p, *pp = p.p, *pq = q.p, *pu = d_u;
+    CK(cudaMemcpyAsync(pr, d_f, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    launch_fill(n, 0.0, pu, s);
+    CK(cudaMemsetAsync(sc.p, 0, sizeof(CgScalars), s));
+    launch_dot_partials(n, d_f, d_f, partials.p, s);
+    launch_finalize(0, partials.p, kRedBlocks, sc.p, s);
+    CK(cudaMemcpyAsync(sc_host, sc.p, sizeof(CgScalars), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const double norm_f = std::sqrt(sc_host->rr);
+    if (norm_f == 0.0) {
+        rep.converged = 1;
+        rep.relative_residual = 0.0;
+        rep.preconditioner_bytes = memory_footprint();
+        rep.solve_seconds = now_s() - t0;
+        return rep;
+    }
+    vcycle(pr, pz, true);
+    launch_dot_partials(n, pr, pz, partials.p, s);
+    launch_finalize(3, partials.p, kRedBlocks, sc.p, s);
+    CK(cudaMemcpyAsync(pp, pz, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    double res_norm = norm_f;
+    int iter = 0;
+    while (res_norm / norm_f > cp.tol && iter < cp.max_iterations) {
+        int nparts = 0;
+        launch_spmv_dot(A0, pp, pq, partials.p, &nparts, s);
+        launch_finalize(1, partials.p, nparts, sc.p, s);
+        launch_cg_update(n, sc.p, pp, pq, pu, pr, partials.p, s);
+        launch_finalize(0, partials.p, kRedBlocks, sc.p, s);
+        CK(cudaMemcpyAsync(sc_host, sc.p, sizeof(CgScalars), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (sc_host->breakdown)
+            fail(SAMG_BREAKDOWN_NON_SPD, "cg: p'Ap <= 0, matrix or preconditioner not SPD");
+        ++iter;
+        res_norm = std::sqrt(sc_host->rr);
+        if (res_norm / norm_f <= cp.tol) break;
+        vcycle(pr, pz, true);
+        launch_dot_partials(n, pr, pz, partials.p, s);
+        launch_finalize(2, partials.p, kRedBlocks, sc.p, s);
+        launch_p_update(n, sc.p, pz, pp, s);
+    }
+    rep.iterations = iter;
+    rep.converged = res_norm / norm_f <= cp.tol;
+    // true residual at exit (cg.hpp:105-108)
+    launch_residual(A0, d_f, pu, pq, s);
+    launch_dot_partials(n, pq, pq, partials.p, s);
+    launch_finalize(0, partials.p, kRedBlocks, sc.p, s);
+    CK(cudaMemcpyAsync(sc_host, sc.p, sizeof(CgScalars), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    rep.relative_residual = std::sqrt(sc_host->rr) / norm_f;
+    rep.preconditioner_bytes = memory_footprint();
+    rep.solve_seconds = now_s() - t0;
+    return rep;
+}
+
+} // namespace samgb

@@ -1,0 +1,47 @@
+// hierarchy.cuh -- the device-resident AMG hierarchy (hierarchy.hpp:78-148)
+// and its setup / V-cycle / CG drivers.
+#pragma once
+
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace samgb {
+
+struct Level {
+    Bsr3 A, P, R;              // P, R empty on the coarsest level
+    bool has_transfer = false;
+    Smoother M;                // absent on the coarsest level
+    DevBuf<int> agg;           // aggregate id per node (parity tap)
+    int64_t nnodes = 0, naggs = 0;
+    DevBuf<double> f, u, r, t; // V-cycle workspace (vcycle_workspace, hierarchy.hpp:152-163)
+};
+
+struct Hierarchy {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool owns_stream = false;  // set once setup succeeded
+    samg_amg_params prm{};
+    std::vector<Level> levels;
+    DevBuf<double> Ainv;       // coarsest inverse, row-major nc x nc
+    int64_t nc = 0;
+    double setup_seconds = 0;
+    DevBuf<DevError> err;
+    // CG workspace (cg.hpp:46-47)
+    DevBuf<double> r, z, p, q, fbuf, ubuf, partials;
+    DevBuf<CgScalars> sc;
+    CgScalars *sc_host = nullptr;  // pinned mirror
+
+    ~Hierarchy();
+    int64_t finest_dim() const { return 3 * levels.front().A.nrows; }
+    uint64_t memory_footprint() const;
+
+    void vcycle(const double *f, double *u, bool zero_guess);
+    samg_solve_report cg(const double *d_f, double *d_u, const samg_cg_params &prm);
+};
+
+// Setup from a device BSR3 fine matrix (consumed) and a host nullspace.
+Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int64_t b_cols,
+                           const samg_amg_params &prm, cudaStream_t stream, double t_start);
+
+} // namespace samgb

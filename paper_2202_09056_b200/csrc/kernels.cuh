@@ -1,0 +1,114 @@
+// kernels.cuh -- device data layout and kernel launchers.
+//
+// HBM layout of a level matrix (Bsr3): the reference's csr<static_block<3>>
+// (csr.hpp:26-40) with 32-bit indices: ptr[nrows+1], col[nnzb] (int32) and
+// val[9*nnzb] fp64, each 3x3 block row-major and the blocks of a row
+// contiguous and column-sorted.  Vectors are in scalar layout (3 per block
+// row), exactly as the reference's spmv expects (csr.hpp:9-12).
+#pragma once
+
+#include "common.cuh"
+
+namespace samgb {
+
+struct Bsr3 {
+    int64_t nrows = 0, ncols = 0, nnzb = 0;
+    DevBuf<int> ptr, col;
+    DevBuf<double> val;
+    void alloc(int64_t nr, int64_t nc, int64_t nz, cudaStream_t s) {
+        if (nz > INT32_MAX || nr > INT32_MAX || nc > INT32_MAX)
+            fail(SAMG_UNSUPPORTED, "BSR3: more than 2^31-1 blocks per matrix");
+        nrows = nr; ncols = nc; nnzb = nz;
+        ptr.alloc(nr + 1, s);
+        col.alloc(nz, s);
+        val.alloc(9 * nz, s);
+    }
+};
+
+enum SmootherKind { SM_POINT = 0, SM_BLOCK = 1 };
+
+// Per-level smoother: point (3 doubles per block row: omega / a_rr) or
+// block (9 doubles per block row: M_i).
+struct Smoother {
+    int kind = SM_POINT;
+    DevBuf<double> data;
+};
+
+// ---- solve phase (solve.cu) -------------------------------------------------
+// y = alpha*A*x + beta*y  (csr.hpp:129-160)
+void launch_spmv(const Bsr3 &A, double alpha, const double *x, double beta, double *y,
+                 cudaStream_t s);
+// r = f - A*u  (csr.hpp:163-169)
+void launch_residual(const Bsr3 &A, const double *f, const double *u, double *r,
+                     cudaStream_t s);
+// u_out = u + M (f - A u)  (one smoothing sweep, relaxation.hpp:165-173)
+void launch_smooth(const Bsr3 &A, const Smoother &M, const double *f, const double *u,
+                   double *u_out, cudaStream_t s);
+// u = M f  (one sweep from a zero guess: the residual is f exactly)
+void launch_smooth_zero(int64_t nrows, const Smoother &M, const double *f, double *u,
+                        cudaStream_t s);
+// q = A p and per-block partial sums of p.q (fused CG matvec, cg.hpp:63-64)
+void launch_spmv_dot(const Bsr3 &A, const double *p, double *q, double *partials,
+                     int *nparts, cudaStream_t s);
+// dense coarse solve u = Ainv f (replaces dense_lu::solve, hierarchy.hpp:113-129)
+void launch_dense_gemv(int64_t n, const double *Ainv, const double *f, double *u,
+                       cudaStream_t s);
+
+// CG device scalars (cg.hpp:39-83).
+struct CgScalars {
+    double pq, rho, rho_new, rr, alpha, beta;
+    int breakdown;
+    int pad;
+};
+constexpr int kRedBlocks = 592;   // 4 x 148 SMs: fixed => deterministic sums
+void launch_dot_partials(int64_t n, const double *x, const double *y, double *partials,
+                         cudaStream_t s);
+// finalize: 0 = rr, 1 = pq (+alpha, breakdown), 2 = rho_new (+beta, rho),
+// 3 = rho (initial), from `nparts` partial sums
+void launch_finalize(int what, const double *partials, int nparts, CgScalars *sc,
+                     cudaStream_t s);
+// u += alpha p; r -= alpha q; partials of r.r
+void launch_cg_update(int64_t n, const CgScalars *sc, const double *p, const double *q,
+                      double *u, double *r, double *partials, cudaStream_t s);
+// p = z + beta p
+void launch_p_update(int64_t n, const CgScalars *sc, const double *z, double *p,
+                     cudaStream_t s);
+void launch_fill(int64_t n, double v, double *x, cudaStream_t s);
+
+// ---- setup phase (setup.cu, compiled with --fmad=false) ----------------------
+struct Graph {  // node adjacency, symmetric, sorted rows (coarsening.hpp:33-38)
+    int64_t nnodes = 0, nedges = 0;
+    DevBuf<int> ptr, col;
+};
+
+// scalar CSR (int64 on host layout) uploaded -> BSR3 (csr.hpp:268-324)
+void scalar_to_bsr3(int64_t n, const int64_t *d_ptr, const int64_t *d_col, const double *d_val,
+                    Bsr3 &out, cudaStream_t s);
+// strength graph on nodes of h block rows (coarsening.hpp:52-123)
+void strength_graph(const Bsr3 &A, int h, double eps_strong, Graph &G, cudaStream_t s);
+// aggregation (coarsening.hpp:131-160); returns the aggregate count
+int64_t aggregate(const Graph &G, DevBuf<int> &agg, cudaStream_t s);
+// tentative prolongation with QR of the nullspace (coarsening.hpp:238-312):
+// Pt[nfine*k] row values (columns agg*k + c), Bc column-major (naggs*k)-by-k
+void tentative(const DevBuf<int> &agg, int64_t nnodes, int64_t naggs, int pbs, const double *B,
+               int k, DevBuf<double> &Pt, DevBuf<double> &Bc, DevError *err, cudaStream_t s);
+// smoothed prolongation in scalar semantics, emitted as BSR3
+// (coarsening.hpp:319-416 + to_block<3>)
+void smooth_prolongation(const Bsr3 &A, const Graph &G, const DevBuf<int> &agg, int64_t naggs,
+                         int pbs, int k, const double *Pt, double omega, Bsr3 &P, DevError *err,
+                         cudaStream_t s);
+// R = P^T with transposed blocks (csr.hpp:173-194)
+void transpose(const Bsr3 &P, Bsr3 &R, cudaStream_t s);
+// C = A*B in the reference's order (csr.hpp:199-255)
+void spgemm(const Bsr3 &A, const Bsr3 &B, Bsr3 &C, cudaStream_t s);
+void fix_decoupled_rows(Bsr3 &A, cudaStream_t s);
+// smoother setup: kind SAMG_SMOOTHER_*
+void setup_smoother(const Bsr3 &A, int kind, double omega, Smoother &M, DevError *err,
+                    cudaStream_t s);
+// coarsest level: dense inverse (row-major n x n), n = 3*A.nrows
+void dense_inverse(const Bsr3 &A, DevBuf<double> &Ainv, DevError *err, cudaStream_t s);
+
+// throws the first device-side error, if any (synchronises s)
+void check_dev_error(DevError *err, cudaStream_t s);
+
+} // namespace samgb

@@ -1,0 +1,1122 @@
+// setup.cu -- setup-phase kernels of the ns_block pipeline.
+//
+// COMPILED WITH --fmad=false: the reference's header code is built without
+// -mfma, so every product and sum here is a separately rounded
+// IEEE operation, and every sum is taken in the reference's order.  With
+// identical inputs the strength graph, the aggregates, P, R and the Galerkin
+// products are therefore bit-identical to samg::setup (pinned by
+// tests/test_gpu_parity.py).
+//
+// Reference functions restated (paths under proj/include/samg/):
+//   to_block<3>            csr.hpp:268-324          -> k_s2b_*
+//   condense_weights +
+//   strength_graph         coarsening.hpp:52-123    -> k_strength_*
+//   aggregate              coarsening.hpp:131-160   -> k_agg_* (parallel, exact)
+//   thin_qr +
+//   tentative_prolongation coarsening.hpp:167-312   -> k_tentative_qr
+//   smooth_prolongation    coarsening.hpp:319-416   -> k_psm_*
+//   transpose              csr.hpp:173-194          -> k_tr_*
+//   spgemm / galerkin      csr.hpp:199-262          -> k_spgemm_*
+//   fix_decoupled_rows     hierarchy.hpp:172-191    -> k_fix_rows
+//   damped_jacobi ctor     relaxation.hpp:147-162   -> k_sm_point
+//   block smoothers        DESIGN.md section 4      -> k_sm_block
+#include "kernels.cuh"
+
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <vector>
+
+namespace samgb {
+
+namespace {
+
+constexpr int INF = 0x7fffffff;
+
+__device__ void raise(DevError *err, int code, int64_t where) {
+    if (atomicCAS(&err->code, 0, code) == 0) err->where = where;
+}
+
+template <class F>
+__global__ void k_for(int64_t n, F f) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        f(i);
+}
+
+template <class F>
+void for_each(int64_t n, F f, cudaStream_t s) {
+    if (n <= 0) return;
+    int64_t g = (n + 255) / 256;
+    if (g > 65535LL * 8) g = 65535LL * 8;
+    k_for<<<static_cast<int>(g), 256, 0, s>>>(n, f);
+    CK_LAUNCH();
+}
+
+// exclusive scan of n ints into out (n+1 entries, out[n] = total); returns total
+int64_t scan_counts(const int *in, int *out, int64_t n, cudaStream_t s) {
+    DevBuf<int64_t> tmp64(n + 1, s);
+    int64_t *t = tmp64.p;
+    for_each(n, [=] __device__(int64_t i) { t[i] = in[i]; }, s);
+    size_t bytes = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, t, t, n + 1, s));
+    DevBuf<char> ws(bytes, s);
+    // t[n] must be zero before the scan so that t[n] becomes the total
+    CK(cudaMemsetAsync(t + n, 0, sizeof(int64_t), s));
+    CK(cub::DeviceScan::ExclusiveSum(ws.p, bytes, t, t, n + 1, s));
+    int64_t total = 0;
+    CK(cudaMemcpyAsync(&total, t + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (total > INT32_MAX) fail(SAMG_UNSUPPORTED, "setup: more than 2^31-1 entries in one matrix");
+    for_each(n + 1, [=] __device__(int64_t i) { out[i] = static_cast<int>(t[i]); }, s);
+    return total;
+}
+
+__device__ __forceinline__ bool bsearch_int(const int *a, int lo, int hi, int key) {
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        const int v = a[mid];
+        if (v == key) return true;
+        if (v < key) lo = mid + 1;
+        else hi = mid;
+    }
+    return false;
+}
+
+__device__ __forceinline__ int lower_bound_int(const int *a, int n, int key) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (a[mid] < key) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// 3x3 product, static_block.hpp:104-113 (r = 0; r(i,j) += a(i,k) b(k,j); i,k,j)
+__device__ __forceinline__ void blk_mul(const double *a, const double *b, double *r) {
+#pragma unroll
+    for (int e = 0; e < 9; ++e) r[e] = 0.0;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const double aik = a[i * 3 + k];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) r[i * 3 + j] = __dadd_rn(r[i * 3 + j], __dmul_rn(aik, b[k * 3 + j]));
+        }
+}
+
+// ---------------------------------------------------------------------------
+// to_block<3> of a sorted scalar CSR (csr.hpp:268-324): 3-way merge of the
+// scalar rows' block columns; absent tile entries stay zero.
+
+__global__ void k_s2b_count(int64_t nb, const int64_t *ptr, const int64_t *col, int *cnt,
+                            DevError *err) {
+    for (int64_t bi = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; bi < nb;
+         bi += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        int64_t h[3], e[3];
+        for (int r = 0; r < 3; ++r) { h[r] = ptr[3 * bi + r]; e[r] = ptr[3 * bi + r + 1]; }
+        for (int r = 0; r < 3; ++r)
+            for (int64_t j = h[r] + 1; j < e[r]; ++j)
+                if (col[j] <= col[j - 1]) raise(err, SAMG_INVALID_ARGUMENT, 3 * bi + r);
+        int c = 0;
+        while (true) {
+            int64_t m = INT64_MAX;
+            for (int r = 0; r < 3; ++r)
+                if (h[r] < e[r]) m = min(m, col[h[r]] / 3);
+            if (m == INT64_MAX) break;
+            ++c;
+            for (int r = 0; r < 3; ++r)
+                while (h[r] < e[r] && col[h[r]] / 3 == m) ++h[r];
+        }
+        cnt[bi] = c;
+    }
+}
+
+__global__ void k_s2b_fill(int64_t nb, const int64_t *ptr, const int64_t *col,
+                           const double *val, const int *bptr, int *bcol, double *bval) {
+    for (int64_t bi = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; bi < nb;
+         bi += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        int64_t h[3], e[3];
+        for (int r = 0; r < 3; ++r) { h[r] = ptr[3 * bi + r]; e[r] = ptr[3 * bi + r + 1]; }
+        int out = bptr[bi];
+        while (true) {
+            int64_t m = INT64_MAX;
+            for (int r = 0; r < 3; ++r)
+                if (h[r] < e[r]) m = min(m, col[h[r]] / 3);
+            if (m == INT64_MAX) break;
+            bcol[out] = static_cast<int>(m);
+            double *blk = bval + 9 * static_cast<int64_t>(out);
+            for (int e9 = 0; e9 < 9; ++e9) blk[e9] = 0.0;
+            for (int r = 0; r < 3; ++r)
+                while (h[r] < e[r] && col[h[r]] / 3 == m) {
+                    blk[r * 3 + static_cast<int>(col[h[r]] % 3)] = val[h[r]];
+                    ++h[r];
+                }
+            ++out;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// strength graph.  A node is h block rows (pbs = 3h); the weight of node
+// tile (i, j) is the max |a| over its scalar entries (condense_weights,
+// coarsening.hpp:64-75); edge iff w*w > (eps2*d_i)*d_j (coarsening.hpp:105),
+// union-symmetrised.
+
+template <class F>
+__device__ __forceinline__ void for_node_tiles(int node, int h, const int *ptr, const int *col,
+                                               const double *val, F f) {
+    // visit (node column, max|a|) of node row `node` in ascending node column
+    if (h == 1) {
+        for (int j = ptr[node]; j < ptr[node + 1]; ++j) {
+            const double *b = val + 9 * static_cast<int64_t>(j);
+            double w = 0.0;
+            for (int e = 0; e < 9; ++e) w = fmax(w, fabs(b[e]));
+            f(col[j], w);
+        }
+        return;
+    }
+    int hd[4], en[4];
+    for (int r = 0; r < h; ++r) { hd[r] = ptr[node * h + r]; en[r] = ptr[node * h + r + 1]; }
+    while (true) {
+        int m = INF;
+        for (int r = 0; r < h; ++r)
+            if (hd[r] < en[r]) m = min(m, col[hd[r]] / h);
+        if (m == INF) break;
+        double w = 0.0;
+        for (int r = 0; r < h; ++r)
+            while (hd[r] < en[r] && col[hd[r]] / h == m) {
+                const double *b = val + 9 * static_cast<int64_t>(hd[r]);
+                for (int e = 0; e < 9; ++e) w = fmax(w, fabs(b[e]));
+                ++hd[r];
+            }
+        f(m, w);
+    }
+}
+
+__global__ void k_strength_diag(int n, int h, const int *ptr, const int *col, const double *val,
+                                double *d) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double di = 0.0;
+    for_node_tiles(i, h, ptr, col, val, [&](int j, double w) { if (j == i) di = w; });
+    d[i] = di;
+}
+
+__global__ void k_strength_edges(int n, int h, const int *ptr, const int *col, const double *val,
+                                 const double *d, double eps2, int *cnt,
+                                 const int *off, unsigned long long *keys) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int c = 0;
+    const double di = d[i];
+    int64_t o = off ? 2 * static_cast<int64_t>(off[i]) : 0;
+    for_node_tiles(i, h, ptr, col, val, [&](int j, double w) {
+        if (j == i) return;
+        if (__dmul_rn(w, w) > __dmul_rn(__dmul_rn(eps2, di), d[j])) {
+            if (keys) {
+                keys[o++] = (static_cast<unsigned long long>(i) << 32) | static_cast<unsigned>(j);
+                keys[o++] = (static_cast<unsigned long long>(j) << 32) | static_cast<unsigned>(i);
+            }
+            ++c;
+        }
+    });
+    if (cnt) cnt[i] = c;
+}
+
+// ---------------------------------------------------------------------------
+// aggregation.  Pass 1 of coarsening.hpp:136-146 seeds node i iff no earlier
+// seed lies within graph distance 2, i.e. the seeds are the
+// lexicographically-first maximal independent set of G^2.  It is computed
+// in rounds: m1[j]/u1[j] = smallest seed / undecided index in the closed
+// neighbourhood of j; an undecided i becomes OUT if min m1 over N[i] < i,
+// IN if min u1 over N[i] == i (all smaller nodes within distance 2 are
+// decided OUT).  Pass 2 (:148-154) joins the first neighbour (ascending)
+// that is pass-1 assigned or has a smaller index; chains are resolved by
+// pointer jumping.  Pass 3 (:156-157) cannot trigger (isolated nodes seed).
+
+enum { UND = 0, IN = 1, OUT = 2 };
+
+__global__ void k_agg_a(int n, const int *gp, const int *gc, const unsigned char *state,
+                        int *m1, int *u1) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const unsigned char sj = state[j];
+    int m = sj == IN ? j : INF, u = sj == UND ? j : INF;
+    for (int e = gp[j]; e < gp[j + 1]; ++e) {
+        const int nb = gc[e];
+        const unsigned char s = state[nb];
+        if (s == IN) m = min(m, nb);
+        else if (s == UND) u = min(u, nb);
+    }
+    m1[j] = m;
+    u1[j] = u;
+}
+
+__global__ void k_agg_b(int n, const int *gp, const int *gc, unsigned char *state, const int *m1,
+                        const int *u1, int *undecided) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || state[i] != UND) return;
+    int m = m1[i], u = u1[i];
+    for (int e = gp[i]; e < gp[i + 1]; ++e) {
+        const int nb = gc[e];
+        m = min(m, m1[nb]);
+        u = min(u, u1[nb]);
+    }
+    if (m < i) state[i] = OUT;
+    else if (u == i) state[i] = IN;
+    else atomicAdd(undecided, 1);
+}
+
+// ---------------------------------------------------------------------------
+// tentative prolongation: Householder thin QR per aggregate, one thread per
+// aggregate, loop orders of coarsening.hpp:167-229 and :289-309.
+
+__global__ void k_tentative_qr(int64_t naggs, int pbs, int k, const int *nodes,
+                               const int *agg_ptr, const double *B, int64_t bnrows,
+                               double *work, double *Qw, double *Pt, double *Bc, DevError *err) {
+    const int64_t a = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (a >= naggs) return;
+    const int n0 = agg_ptr[a], n1 = agg_ptr[a + 1];
+    const int64_t m = static_cast<int64_t>(pbs) * (n1 - n0);
+    double *A = work + static_cast<int64_t>(pbs) * n0 * k;
+    double *Q = Qw + static_cast<int64_t>(pbs) * n0 * k;
+#define a_(i, j) A[(j) * m + (i)]
+#define ROW(r) (static_cast<int64_t>(nodes[n0 + (r) / pbs]) * pbs + (r) % pbs)
+    for (int c = 0; c < k; ++c)
+        for (int64_t r = 0; r < m; ++r) a_(r, c) = B[c * bnrows + ROW(r)];
+    double local_max = 0;
+    for (int64_t t = 0; t < m * k; ++t) local_max = fmax(local_max, fabs(A[t]));
+    const double tol = __dmul_rn(1e-12, fmax(local_max, 1.0));
+    double tau[12], R[144];
+    for (int j = 0; j < k; ++j) tau[j] = 0.0;
+    const int64_t steps = m < k ? m : k;
+    for (int64_t j = 0; j < steps; ++j) {
+        double normx = 0;
+        for (int64_t i = j; i < m; ++i) normx = __dadd_rn(normx, __dmul_rn(a_(i, j), a_(i, j)));
+        normx = __dsqrt_rn(normx);
+        if (normx <= tol) { tau[j] = 0; continue; }
+        const double alpha = a_(j, j) >= 0 ? -normx : normx;
+        const double v0 = __dsub_rn(a_(j, j), alpha);
+        for (int64_t i = j + 1; i < m; ++i) a_(i, j) = __ddiv_rn(a_(i, j), v0);
+        tau[j] = __ddiv_rn(-v0, alpha);
+        a_(j, j) = alpha;
+        for (int c = j + 1; c < k; ++c) {
+            double s = a_(j, c);
+            for (int64_t i = j + 1; i < m; ++i) s = __dadd_rn(s, __dmul_rn(a_(i, j), a_(i, c)));
+            s = __dmul_rn(s, tau[j]);
+            a_(j, c) = __dsub_rn(a_(j, c), s);
+            for (int64_t i = j + 1; i < m; ++i) a_(i, c) = __dsub_rn(a_(i, c), __dmul_rn(s, a_(i, j)));
+        }
+    }
+    for (int t = 0; t < k * k; ++t) R[t] = 0.0;
+    for (int j = 0; j < k; ++j)
+        for (int64_t i = 0; i <= (j < m - 1 ? j : m - 1); ++i) R[j * k + i] = a_(i, j);
+    for (int64_t t = 0; t < m * k; ++t) Q[t] = 0.0;
+    for (int64_t j = 0; j < (m < k ? m : k); ++j) Q[j * m + j] = 1.0;
+    for (int64_t j = steps - 1; j >= 0; --j) {
+        if (tau[j] == 0) continue;
+        for (int c = 0; c < k; ++c) {
+            double s = Q[c * m + j];
+            for (int64_t i = j + 1; i < m; ++i) s = __dadd_rn(s, __dmul_rn(a_(i, j), Q[c * m + i]));
+            s = __dmul_rn(s, tau[j]);
+            Q[c * m + j] = __dsub_rn(Q[c * m + j], s);
+            for (int64_t i = j + 1; i < m; ++i) Q[c * m + i] = __dsub_rn(Q[c * m + i], __dmul_rn(s, a_(i, j)));
+        }
+    }
+    const double lm = fmax(local_max, 1e-300);
+    for (int j = 0; j < k; ++j) {
+        const double rjj = (j < m) ? fabs(R[j * k + j]) : 0.0;
+        if (rjj <= __dmul_rn(1e-12, lm)) {
+            for (int64_t i = 0; i < m; ++i) Q[j * m + i] = 0.0;
+            for (int c = 0; c < k; ++c) R[c * k + j] = 0.0;
+        }
+    }
+    for (int64_t r = 0; r < m; ++r) {
+        const int64_t row = ROW(r);
+        for (int c = 0; c < k; ++c) Pt[row * k + c] = Q[c * m + r];
+    }
+    const int64_t bcn = naggs * k;
+    for (int i = 0; i < k; ++i)
+        for (int c = 0; c < k; ++c) Bc[c * bcn + a * k + i] = R[c * k + i];
+#undef a_
+#undef ROW
+    (void)err;
+}
+
+// ---------------------------------------------------------------------------
+// prolongator smoothing (coarsening.hpp:319-416) in the scalar semantics the
+// ns_block wrapper uses (as_scalar_transfer, :451-464), emitted directly as
+// 3x3 blocks (to_block<3> of the scalar P is exact: every node's scalar
+// rows share one column set made of whole k-column aggregate groups).
+
+__device__ __forceinline__ bool strong(const int *gp, const int *gc, int node, int cnode) {
+    return bsearch_int(gc, gp[node], gp[node + 1], cnode);
+}
+
+// touched aggregates of each node: agg(node) + agg(c) for kept node columns
+__global__ void k_psm_touch(int nnodes, int h, const int *ptr, const int *col, const int *gp,
+                            const int *gc, const int *agg, const int *toff, int *tlist,
+                            int *tcnt) {
+    const int node = blockIdx.x * blockDim.x + threadIdx.x;
+    if (node >= nnodes) return;
+    int *L = tlist + toff[node];
+    int n = 0;
+    L[n++] = agg[node];
+    for (int r = 0; r < h; ++r) {
+        const int br = node * h + r;
+        for (int j = ptr[br]; j < ptr[br + 1]; ++j) {
+            const int cn = col[j] / h;
+            if (cn == node || strong(gp, gc, node, cn)) {
+                const int g = agg[cn];
+                int q = n;
+                bool dup = false;
+                for (int t = 0; t < n; ++t) if (L[t] == g) { dup = true; break; }
+                if (dup) continue;
+                // insertion keeping ascending order
+                while (q > 0 && L[q - 1] > g) { L[q] = L[q - 1]; --q; }
+                L[q] = g;
+                ++n;
+            }
+        }
+    }
+    // the own aggregate was inserted first; restore ascending order
+    for (int t = 1; t < n; ++t) {
+        const int v = L[t];
+        int q = t;
+        while (q > 0 && L[q - 1] > v) { L[q] = L[q - 1]; --q; }
+        L[q] = v;
+    }
+    tcnt[node] = n;
+}
+
+__global__ void k_psm_cols(int nbrows, int h, int kb, const int *toff, const int *tlist,
+                           const int *tcnt, const int *pptr, int *pcol) {
+    const int br = blockIdx.x * blockDim.x + threadIdx.x;
+    if (br >= nbrows) return;
+    const int node = br / h;
+    const int *L = tlist + toff[node];
+    int o = pptr[br];
+    for (int t = 0; t < tcnt[node]; ++t)
+        for (int q = 0; q < kb; ++q) pcol[o++] = L[t] * kb + q;
+}
+
+// filtered scalar diagonal D_f (coarsening.hpp:335-358)
+__global__ void k_psm_diag(int64_t nsc, int pbs, const int *ptr, const int *col,
+                           const double *val, const int *gp, const int *gc, double *dinv,
+                           double *diag, DevError *err) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= nsc) return;
+    const int br = static_cast<int>(i / 3), rr = static_cast<int>(i % 3);
+    const int node = static_cast<int>(i / pbs);
+    double d = 0.0;
+    for (int j = ptr[br]; j < ptr[br + 1]; ++j) {
+        const int64_t sc0 = 3 * static_cast<int64_t>(col[j]);
+        const int cn = static_cast<int>(sc0 / pbs);
+        const bool same = cn == node;
+        const bool st = same ? false : strong(gp, gc, node, cn);
+        const double *b = val + 9 * static_cast<int64_t>(j) + 3 * rr;
+        for (int c = 0; c < 3; ++c) {
+            const int64_t sc = sc0 + c;
+            if (same) {
+                if (sc == i) d = __dadd_rn(d, b[c]);
+            } else if (!st) {
+                d = __dadd_rn(d, b[c]);
+            }
+        }
+    }
+    diag[i] = d;
+    if (d == 0.0) { raise(err, SAMG_ZERO_DIAGONAL, i); dinv[i] = 0.0; return; }
+    if (fabs(d) < 1e-300) { raise(err, SAMG_SINGULAR_BLOCK, i); dinv[i] = 0.0; return; }
+    dinv[i] = __ddiv_rn(1.0, d);
+}
+
+// P row values: for each touched aggregate g, in ascending scalar column
+// order over kept entries k with agg(node(k)) == g (coarsening.hpp:387-414)
+__global__ void k_psm_vals(int64_t nsc, int pbs, int h, int k, const int *ptr, const int *col,
+                           const double *val, const int *gp, const int *gc, const int *agg,
+                           const int *toff, const int *tlist, const int *tcnt,
+                           const double *dinv, const double *diag, const double *Pt,
+                           double omega, const int *pptr, double *pval) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= nsc) return;
+    const int br = static_cast<int>(i / 3), rr = static_cast<int>(i % 3);
+    const int node = static_cast<int>(i / pbs);
+    const int kb = k / 3;
+    const int *L = tlist + toff[node];
+    const int nt = tcnt[node];
+    const double di = dinv[i], dg = diag[i];
+    const double nom = -omega;
+    for (int t = 0; t < nt; ++t) {
+        const int g = L[t];
+        double acc[12];
+        bool touched = agg[node] == g;
+        if (touched)
+            for (int c = 0; c < k; ++c) acc[c] = Pt[i * k + c];
+        for (int j = ptr[br]; j < ptr[br + 1]; ++j) {
+            const int64_t sc0 = 3 * static_cast<int64_t>(col[j]);
+            const int cn = static_cast<int>(sc0 / pbs);
+            if (agg[cn] != g) continue;
+            if (cn != node && !strong(gp, gc, node, cn)) continue;
+            const double *b = val + 9 * static_cast<int64_t>(j) + 3 * rr;
+            for (int c3 = 0; c3 < 3; ++c3) {
+                const int64_t sc = sc0 + c3;
+                const double coef = (sc == i) ? dg : b[c3];
+                const double scaled = __dmul_rn(__dmul_rn(di, coef), nom);
+                const double *pk = Pt + sc * k;
+                if (touched) {
+                    for (int c = 0; c < k; ++c) acc[c] = __dadd_rn(acc[c], __dmul_rn(scaled, pk[c]));
+                } else {
+                    for (int c = 0; c < k; ++c) acc[c] = __dmul_rn(scaled, pk[c]);
+                    touched = true;
+                }
+            }
+        }
+        const int64_t base = pptr[br] + static_cast<int64_t>(t) * kb;
+        for (int c = 0; c < k; ++c) pval[9 * (base + c / 3) + 3 * rr + c % 3] = acc[c];
+    }
+}
+
+// omega == 0: P is the tentative operator (coarsening.hpp:326)
+__global__ void k_ptent_bsr(int nbrows, int h, int k, const int *agg, const double *Pt,
+                            int *pptr, int *pcol, double *pval) {
+    const int br = blockIdx.x * blockDim.x + threadIdx.x;
+    if (br > nbrows) return;
+    const int kb = k / 3;
+    pptr[br] = br * kb;
+    if (br == nbrows) return;
+    const int g = agg[br / h];
+    for (int q = 0; q < kb; ++q) {
+        pcol[br * kb + q] = g * kb + q;
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c)
+                pval[9 * (static_cast<int64_t>(br) * kb + q) + 3 * r + c] =
+                    Pt[(3 * static_cast<int64_t>(br) + r) * k + 3 * q + c];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// SpGEMM C = A*B (csr.hpp:199-255).  One CTA per output row; a hash set of
+// the row's columns lives in shared memory (or a global scratch slab for
+// oversized rows).  Numeric phase: columns are sorted (bitonic), slots
+// zeroed, then A's row entries are consumed in ascending order with a CTA
+// barrier between them, so every output block receives its products in
+// exactly the reference's (ja ascending) order.
+
+__device__ __forceinline__ unsigned hash_u(int key) {
+    unsigned x = static_cast<unsigned>(key);
+    x ^= x >> 16; x *= 0x7feb352dU; x ^= x >> 15; x *= 0x846ca68bU; x ^= x >> 16;
+    return x;
+}
+
+// returns slot index; inserts if absent; -1 if the table is full
+__device__ __forceinline__ int hash_insert(int *keys, int cap, int key, bool &inserted) {
+    unsigned h = hash_u(key) & (cap - 1);
+    for (int probe = 0; probe < cap; ++probe) {
+        const int cur = keys[h];
+        if (cur == key) { inserted = false; return static_cast<int>(h); }
+        if (cur == -1) {
+            const int prev = atomicCAS(keys + h, -1, key);
+            if (prev == -1) { inserted = true; return static_cast<int>(h); }
+            if (prev == key) { inserted = false; return static_cast<int>(h); }
+        }
+        h = (h + 1) & (cap - 1);
+    }
+    inserted = false;
+    return -1;
+}
+
+__device__ __forceinline__ int hash_find(const int *keys, int cap, int key) {
+    unsigned h = hash_u(key) & (cap - 1);
+    for (int probe = 0; probe < cap; ++probe) {
+        const int cur = keys[h];
+        if (cur == key) return static_cast<int>(h);
+        if (cur == -1) return -1;
+        h = (h + 1) & (cap - 1);
+    }
+    return -1;
+}
+
+// symbolic: count distinct columns per row.  GLOBAL: table in scratch.
+template <bool GLOBAL>
+__global__ void k_spgemm_count(int nrows, const int *rows, const int *ap, const int *ac,
+                               const int *bp, const int *bc, int cap, int *keys_g,
+                               const int64_t *goff, int *cnt, int *overflow) {
+    extern __shared__ int smem[];
+    const int ridx = blockIdx.x;
+    if (ridx >= nrows) return;
+    const int row = rows ? rows[ridx] : ridx;
+    int *keys = GLOBAL ? keys_g + goff[ridx] : smem;
+    const int tcap = GLOBAL ? static_cast<int>(goff[ridx + 1] - goff[ridx]) : cap;
+    __shared__ int n_s, full_s;
+    for (int t = threadIdx.x; t < tcap; t += blockDim.x) keys[t] = -1;
+    if (threadIdx.x == 0) { n_s = 0; full_s = 0; }
+    __syncthreads();
+    const int limit = tcap / 2;
+    for (int ja = ap[row]; ja < ap[row + 1]; ++ja) {
+        const int kk = ac[ja];
+        for (int jb = bp[kk] + threadIdx.x; jb < bp[kk + 1]; jb += blockDim.x) {
+            if (full_s) break;
+            bool ins;
+            const int slot = hash_insert(keys, tcap, bc[jb], ins);
+            if (slot < 0) { full_s = 1; break; }
+            if (ins && atomicAdd(&n_s, 1) + 1 > limit - 1) full_s = 1;
+        }
+        if (full_s) break;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (full_s) { cnt[row] = -1; atomicAdd(overflow, 1); }
+        else cnt[row] = n_s;
+    }
+}
+
+template <bool GLOBAL>
+__global__ void __launch_bounds__(256) k_spgemm_numeric(
+        int nrows, const int *rows, const int *ap, const int *ac, const double *av,
+        const int *bp, const int *bc, const double *bv, int cap, int *keys_g, int *vals_g,
+        int *list_g, const int64_t *goff, const int *cp, int *ccol, double *cval) {
+    extern __shared__ int smem[];
+    const int ridx = blockIdx.x;
+    if (ridx >= nrows) return;
+    const int row = rows ? rows[ridx] : ridx;
+    const int tcap = GLOBAL ? static_cast<int>(goff[ridx + 1] - goff[ridx]) : cap;
+    int *keys = GLOBAL ? keys_g + goff[ridx] : smem;
+    int *vals = GLOBAL ? vals_g + goff[ridx] : smem + cap;
+    int *list = GLOBAL ? list_g + goff[ridx] / 2 : smem + 2 * cap;
+    const int lcap = tcap / 2;
+    // rows too wide for the shared table are done by the GLOBAL instance
+    if (!GLOBAL && cp[row + 1] - cp[row] > lcap - 1) return;
+    __shared__ int n_s;
+    for (int t = threadIdx.x; t < tcap; t += blockDim.x) keys[t] = -1;
+    if (threadIdx.x == 0) n_s = 0;
+    __syncthreads();
+    for (int ja = ap[row]; ja < ap[row + 1]; ++ja) {
+        const int kk = ac[ja];
+        for (int jb = bp[kk] + threadIdx.x; jb < bp[kk + 1]; jb += blockDim.x) {
+            bool ins;
+            hash_insert(keys, tcap, bc[jb], ins);
+        }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < tcap; t += blockDim.x)
+        if (keys[t] != -1) list[atomicAdd(&n_s, 1)] = keys[t];
+    __syncthreads();
+    const int n = n_s;
+    int np2 = 1;
+    while (np2 < n) np2 <<= 1;
+    for (int t = n + threadIdx.x; t < np2 && t < lcap; t += blockDim.x) list[t] = INF;
+    __syncthreads();
+    // bitonic sort of list[0..np2)
+    for (int size = 2; size <= np2; size <<= 1)
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int t = threadIdx.x; t < np2; t += blockDim.x) {
+                const int partner = t ^ stride;
+                if (partner > t) {
+                    const bool up = (t & size) == 0;
+                    const int a = list[t], b = list[partner];
+                    if ((a > b) == up) { list[t] = b; list[partner] = a; }
+                }
+            }
+            __syncthreads();
+        }
+    const int64_t base = cp[row];
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+        const int key = list[t];
+        ccol[base + t] = key;
+        vals[hash_find(keys, tcap, key)] = t;
+        double *cb = cval + 9 * (base + t);
+        for (int e = 0; e < 9; ++e) cb[e] = 0.0;
+    }
+    __syncthreads();
+    for (int ja = ap[row]; ja < ap[row + 1]; ++ja) {
+        const int kk = ac[ja];
+        const double *a = av + 9 * static_cast<int64_t>(ja);
+        double am[9];
+#pragma unroll
+        for (int e = 0; e < 9; ++e) am[e] = a[e];
+        for (int jb = bp[kk] + threadIdx.x; jb < bp[kk + 1]; jb += blockDim.x) {
+            const int slot = vals[hash_find(keys, tcap, bc[jb])];
+            double prod[9];
+            blk_mul(am, bv + 9 * static_cast<int64_t>(jb), prod);
+            double *cb = cval + 9 * (base + slot);
+#pragma unroll
+            for (int e = 0; e < 9; ++e) cb[e] = __dadd_rn(cb[e], prod[e]);
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_spgemm_ub(int nrows, const int *ap, const int *ac, const int *bp,
+                            int64_t *ub) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nrows) return;
+    int64_t s = 0;
+    for (int ja = ap[i]; ja < ap[i + 1]; ++ja) s += bp[ac[ja] + 1] - bp[ac[ja]];
+    ub[i] = s;
+}
+
+int next_pow2(int64_t v) {
+    int64_t p = 1;
+    while (p < v) p <<= 1;
+    return static_cast<int>(p);
+}
+
+} // namespace
+
+// ============================================================================
+
+void check_dev_error(DevError *err, cudaStream_t s) {
+    DevError h{};
+    CK(cudaMemcpyAsync(&h, err, sizeof h, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (h.code == 0) return;
+    CK(cudaMemsetAsync(err, 0, sizeof(DevError), s));
+    const char *what = "setup: device-side error";
+    switch (h.code) {
+        case SAMG_ZERO_DIAGONAL: what = "smooth_prolongation: zero filtered diagonal"; break;
+        case SAMG_SINGULAR_BLOCK: what = "singular pivot in block inversion"; break;
+        case SAMG_MISSING_DIAGONAL: what = "structurally zero diagonal"; break;
+        case SAMG_INVALID_ARGUMENT: what = "input CSR rows must have strictly increasing columns"; break;
+        case SAMG_ERROR: what = "dense_lu: singular coarse matrix"; break;
+        default: break;
+    }
+    fail(h.code, std::string(what) + " (at index " + std::to_string(h.where) + ")");
+}
+
+void scalar_to_bsr3(int64_t n, const int64_t *d_ptr, const int64_t *d_col, const double *d_val,
+                    Bsr3 &out, cudaStream_t s) {
+    const int64_t nb = n / 3;
+    DevBuf<int> cnt(nb + 1, s);
+    DevBuf<DevError> err(1, s);
+    CK(cudaMemsetAsync(err.p, 0, sizeof(DevError), s));
+    const int grid = std::max(1, std::min(ceil_div(nb, 256), 65535));
+    k_s2b_count<<<grid, 256, 0, s>>>(nb, d_ptr, d_col, cnt.p, err.p);
+    CK_LAUNCH();
+    check_dev_error(err.p, s);
+    DevBuf<int> bptr(nb + 1, s);
+    const int64_t nnzb = scan_counts(cnt.p, bptr.p, nb, s);
+    out.nrows = out.ncols = nb;
+    out.nnzb = nnzb;
+    out.ptr = std::move(bptr);
+    out.col.alloc(nnzb, s);
+    out.val.alloc(9 * nnzb, s);
+    k_s2b_fill<<<grid, 256, 0, s>>>(nb, d_ptr, d_col, d_val, out.ptr.p, out.col.p, out.val.p);
+    CK_LAUNCH();
+}
+
+void strength_graph(const Bsr3 &A, int h, double eps_strong, Graph &G, cudaStream_t s) {
+    const int n = static_cast<int>(A.nrows / h);
+    const double eps2 = eps_strong * eps_strong;
+    DevBuf<double> d(n, s);
+    const int grid = ceil_div(n, 256);
+    k_strength_diag<<<grid, 256, 0, s>>>(n, h, A.ptr.p, A.col.p, A.val.p, d.p);
+    CK_LAUNCH();
+    DevBuf<int> cnt(n + 1, s), off(n + 1, s);
+    k_strength_edges<<<grid, 256, 0, s>>>(n, h, A.ptr.p, A.col.p, A.val.p, d.p, eps2, cnt.p,
+                                          nullptr, nullptr);
+    CK_LAUNCH();
+    const int64_t ne = scan_counts(cnt.p, off.p, n, s);
+    DevBuf<unsigned long long> keys(2 * ne + 1, s), keys2(2 * ne + 1, s);
+    k_strength_edges<<<grid, 256, 0, s>>>(n, h, A.ptr.p, A.col.p, A.val.p, d.p, eps2, nullptr,
+                                          off.p, keys.p);
+    CK_LAUNCH();
+    int bits = 1;
+    while ((1LL << bits) < n) ++bits;
+    size_t bytes = 0;
+    const int64_t nk = 2 * ne;
+    CK(cub::DeviceRadixSort::SortKeys(nullptr, bytes, keys.p, keys2.p, nk, 0, 32 + bits, s));
+    DevBuf<char> ws(bytes, s);
+    CK(cub::DeviceRadixSort::SortKeys(ws.p, bytes, keys.p, keys2.p, nk, 0, 32 + bits, s));
+    DevBuf<int64_t> nuniq(1, s);
+    size_t b2 = 0;
+    CK(cub::DeviceSelect::Unique(nullptr, b2, keys2.p, keys.p, nuniq.p, nk, s));
+    DevBuf<char> ws2(b2, s);
+    CK(cub::DeviceSelect::Unique(ws2.p, b2, keys2.p, keys.p, nuniq.p, nk, s));
+    int64_t nu = 0;
+    CK(cudaMemcpyAsync(&nu, nuniq.p, sizeof nu, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    G.nnodes = n;
+    G.nedges = nu;
+    G.ptr.alloc(n + 1, s);
+    G.col.alloc(nu + 1, s);
+    int *gp = G.ptr.p, *gc = G.col.p;
+    const unsigned long long *kp = keys.p;
+    for_each(n + 1, [=] __device__(int64_t i) {
+        int64_t lo = 0, hi = nu;
+        const unsigned long long key = static_cast<unsigned long long>(i) << 32;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (kp[mid] < key) lo = mid + 1;
+            else hi = mid;
+        }
+        gp[i] = static_cast<int>(lo);
+    }, s);
+    for_each(nu, [=] __device__(int64_t e) { gc[e] = static_cast<int>(kp[e] & 0xffffffffULL); }, s);
+}
+
+int64_t aggregate(const Graph &G, DevBuf<int> &agg, cudaStream_t s) {
+    const int n = static_cast<int>(G.nnodes);
+    agg.alloc(n, s);
+    if (n == 0) return 0;
+    DevBuf<unsigned char> state(n, s);
+    DevBuf<int> m1(n, s), u1(n, s), und(1, s);
+    CK(cudaMemsetAsync(state.p, 0, n, s));
+    const int grid = ceil_div(n, 256);
+    int h_und = 1;
+    int rounds = 0;
+    while (h_und) {
+        for (int k = 0; k < 8; ++k) {
+            k_agg_a<<<grid, 256, 0, s>>>(n, G.ptr.p, G.col.p, state.p, m1.p, u1.p);
+            CK(cudaMemsetAsync(und.p, 0, sizeof(int), s));
+            k_agg_b<<<grid, 256, 0, s>>>(n, G.ptr.p, G.col.p, state.p, m1.p, u1.p, und.p);
+            ++rounds;
+        }
+        CK_LAUNCH();
+        CK(cudaMemcpyAsync(&h_und, und.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (rounds > 4 * n + 64) fail(SAMG_ERROR, "aggregate: no progress");
+    }
+    // final seed-in-closed-neighbourhood map
+    k_agg_a<<<grid, 256, 0, s>>>(n, G.ptr.p, G.col.p, state.p, m1.p, u1.p);
+    CK_LAUNCH();
+    DevBuf<int> is_in(n + 1, s), seedno(n + 1, s), parent(n, s), changed(1, s);
+    const unsigned char *st = state.p;
+    int *isin = is_in.p;
+    for_each(n, [=] __device__(int64_t i) { isin[i] = st[i] == IN ? 1 : 0; }, s);
+    const int64_t count = scan_counts(is_in.p, seedno.p, n, s);
+    int *id = agg.p, *par = parent.p;
+    const int *mm = m1.p, *sn = seedno.p, *gp = G.ptr.p, *gc = G.col.p;
+    DevBuf<DevError> err(1, s);
+    CK(cudaMemsetAsync(err.p, 0, sizeof(DevError), s));
+    DevError *ep = err.p;
+    for_each(n, [=] __device__(int64_t ii) {
+        const int i = static_cast<int>(ii);
+        if (mm[i] != INF) { id[i] = sn[mm[i]]; par[i] = i; return; }
+        id[i] = -1;
+        par[i] = -1;
+        for (int e = gp[i]; e < gp[i + 1]; ++e) {
+            const int nb = gc[e];
+            if (mm[nb] != INF || nb < i) { par[i] = nb; return; }
+        }
+        raise(ep, SAMG_ERROR, i);
+    }, s);
+    check_dev_error(err.p, s);
+    int h_changed = 1;
+    int* ch = changed.p;
+    while (h_changed) {
+        CK(cudaMemsetAsync(changed.p, 0, sizeof(int), s));
+        for_each(n, [=] __device__(int64_t i) {
+            const int p = par[i];
+            const int pp = par[p];
+            if (pp != p) { par[i] = pp; *ch = 1; }
+        }, s);
+        CK(cudaMemcpyAsync(&h_changed, changed.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    for_each(n, [=] __device__(int64_t i) { if (id[i] < 0) id[i] = id[par[i]]; }, s);
+    return count;
+}
+
+void tentative(const DevBuf<int> &agg, int64_t nnodes, int64_t naggs, int pbs, const double *B,
+               int k, DevBuf<double> &Pt, DevBuf<double> &Bc, DevError *err, cudaStream_t s) {
+    const int64_t nfine = nnodes * pbs;
+    DevBuf<int> keys2(nnodes, s), iota(nnodes, s), nodes(nnodes, s), agg_ptr(naggs + 1, s);
+    int *io = iota.p;
+    for_each(nnodes, [=] __device__(int64_t i) { io[i] = static_cast<int>(i); }, s);
+    size_t bytes = 0;
+    int bits = 1;
+    while ((1LL << bits) < naggs + 1) ++bits;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, agg.p, keys2.p, iota.p, nodes.p, nnodes, 0,
+                                       bits, s));
+    DevBuf<char> ws(bytes, s);
+    CK(cub::DeviceRadixSort::SortPairs(ws.p, bytes, agg.p, keys2.p, iota.p, nodes.p, nnodes, 0,
+                                       bits, s));
+    const int *sk = keys2.p;
+    int *ap = agg_ptr.p;
+    const int nn = static_cast<int>(nnodes);
+    for_each(naggs + 1, [=] __device__(int64_t a) {
+        ap[a] = lower_bound_int(sk, nn, static_cast<int>(a));
+    }, s);
+    Pt.alloc(nfine * k, s);
+    Bc.alloc(naggs * k * k, s);
+    DevBuf<double> work(nfine * k, s), Qw(nfine * k, s);
+    k_tentative_qr<<<ceil_div(naggs, 128), 128, 0, s>>>(naggs, pbs, k, nodes.p, agg_ptr.p, B,
+                                                         nfine, work.p, Qw.p, Pt.p, Bc.p, err);
+    CK_LAUNCH();
+}
+
+void smooth_prolongation(const Bsr3 &A, const Graph &G, const DevBuf<int> &agg, int64_t naggs,
+                         int pbs, int k, const double *Pt, double omega, Bsr3 &P, DevError *err,
+                         cudaStream_t s) {
+    const int h = pbs / 3, kb = k / 3;
+    const int64_t nbrows = A.nrows, nnodes = nbrows / h, nsc = 3 * nbrows;
+    if (omega == 0.0) {
+        P.alloc(nbrows, naggs * kb, nbrows * kb, s);
+        k_ptent_bsr<<<ceil_div(nbrows + 1, 256), 256, 0, s>>>(static_cast<int>(nbrows), h, k, agg.p,
+                                                             Pt, P.ptr.p, P.col.p, P.val.p);
+        CK_LAUNCH();
+        return;
+    }
+    // touched-aggregate lists per node, bounded by the node row length + 1
+    DevBuf<int> rl(nnodes + 1, s), toff(nnodes + 1, s), tcnt(nnodes + 1, s);
+    const int *ap = A.ptr.p;
+    int *rlp = rl.p;
+    for_each(nnodes, [=] __device__(int64_t nd) {
+        rlp[nd] = ap[(nd + 1) * h] - ap[nd * h] + 1;
+    }, s);
+    const int64_t tl = scan_counts(rl.p, toff.p, nnodes, s);
+    DevBuf<int> tlist(tl + 1, s);
+    k_psm_touch<<<ceil_div(nnodes, 128), 128, 0, s>>>(static_cast<int>(nnodes), h, A.ptr.p,
+                                                      A.col.p, G.ptr.p, G.col.p, agg.p, toff.p,
+                                                      tlist.p, tcnt.p);
+    CK_LAUNCH();
+    DevBuf<int> bcnt(nbrows + 1, s);
+    int *bc = bcnt.p;
+    const int *tc = tcnt.p;
+    for_each(nbrows, [=] __device__(int64_t br) { bc[br] = tc[br / h] * kb; }, s);
+    P.nrows = nbrows;
+    P.ncols = naggs * kb;
+    P.ptr.alloc(nbrows + 1, s);
+    P.nnzb = scan_counts(bcnt.p, P.ptr.p, nbrows, s);
+    P.col.alloc(P.nnzb, s);
+    P.val.alloc(9 * P.nnzb, s);
+    k_psm_cols<<<ceil_div(nbrows, 256), 256, 0, s>>>(static_cast<int>(nbrows), h, kb, toff.p,
+                                                     tlist.p, tcnt.p, P.ptr.p, P.col.p);
+    CK_LAUNCH();
+    DevBuf<double> dinv(nsc, s), diag(nsc, s);
+    k_psm_diag<<<ceil_div(nsc, 256), 256, 0, s>>>(nsc, pbs, A.ptr.p, A.col.p, A.val.p, G.ptr.p,
+                                                  G.col.p, dinv.p, diag.p, err);
+    CK_LAUNCH();
+    check_dev_error(err, s);
+    k_psm_vals<<<ceil_div(nsc, 128), 128, 0, s>>>(nsc, pbs, h, k, A.ptr.p, A.col.p, A.val.p,
+                                                  G.ptr.p, G.col.p, agg.p, toff.p, tlist.p,
+                                                  tcnt.p, dinv.p, diag.p, Pt, omega, P.ptr.p,
+                                                  P.val.p);
+    CK_LAUNCH();
+}
+
+void transpose(const Bsr3 &P, Bsr3 &R, cudaStream_t s) {
+    const int64_t nnz = P.nnzb;
+    R.alloc(P.ncols, P.nrows, nnz, s);
+    DevBuf<int> rowidx(nnz + 1, s), iota(nnz + 1, s), perm(nnz + 1, s), skeys(nnz + 1, s);
+    const int *pp = P.ptr.p;
+    int *ri = rowidx.p, *io = iota.p;
+    const int nr = static_cast<int>(P.nrows);
+    for_each(nnz, [=] __device__(int64_t e) {
+        io[e] = static_cast<int>(e);
+        ri[e] = lower_bound_int(pp, nr + 1, static_cast<int>(e) + 1) - 1;
+    }, s);
+    int bits = 1;
+    while ((1LL << bits) < P.ncols + 1) ++bits;
+    size_t bytes = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, P.col.p, skeys.p, iota.p, perm.p, nnz, 0,
+                                       bits, s));
+    DevBuf<char> ws(bytes, s);
+    CK(cub::DeviceRadixSort::SortPairs(ws.p, bytes, P.col.p, skeys.p, iota.p, perm.p, nnz, 0, bits,
+                                       s));
+    const int *sk = skeys.p, *pm = perm.p;
+    int *rp = R.ptr.p, *rc = R.col.p;
+    double *rv = R.val.p;
+    const double *pv = P.val.p;
+    const int nz = static_cast<int>(nnz);
+    for_each(P.ncols + 1, [=] __device__(int64_t c) {
+        rp[c] = lower_bound_int(sk, nz, static_cast<int>(c));
+    }, s);
+    for_each(nnz, [=] __device__(int64_t k) {
+        const int e = pm[k];
+        rc[k] = ri[e];
+        const double *b = pv + 9 * static_cast<int64_t>(e);
+        double *t = rv + 9 * k;
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) t[c * 3 + r] = b[r * 3 + c];
+    }, s);
+}
+
+void spgemm(const Bsr3 &A, const Bsr3 &B, Bsr3 &C, cudaStream_t s) {
+    if (A.ncols != B.nrows) fail(SAMG_DIMENSION_MISMATCH, "spgemm: inner dimensions disagree");
+    const int n = static_cast<int>(A.nrows);
+    C.nrows = A.nrows;
+    C.ncols = B.ncols;
+    C.ptr.alloc(n + 1, s);
+    if (n == 0) { CK(cudaMemsetAsync(C.ptr.p, 0, sizeof(int), s)); C.nnzb = 0; return; }
+    DevBuf<int64_t> ub(n, s);
+    k_spgemm_ub<<<ceil_div(n, 256), 256, 0, s>>>(n, A.ptr.p, A.col.p, B.ptr.p, ub.p);
+    CK_LAUNCH();
+    // max upper bound decides the shared table size of the symbolic pass
+    DevBuf<int64_t> mx(1, s);
+    size_t bytes = 0;
+    CK(cub::DeviceReduce::Max(nullptr, bytes, ub.p, mx.p, n, s));
+    DevBuf<char> ws(bytes, s);
+    CK(cub::DeviceReduce::Max(ws.p, bytes, ub.p, mx.p, n, s));
+    int64_t maxub = 0;
+    CK(cudaMemcpyAsync(&maxub, mx.p, sizeof maxub, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    constexpr int kMaxCap = 16384;
+    const int cap_s = std::min(kMaxCap, std::max(256, next_pow2(2 * std::min<int64_t>(maxub, B.ncols) + 2)));
+    DevBuf<int> cnt(n + 1, s), ovf(1, s);
+    CK(cudaMemsetAsync(ovf.p, 0, sizeof(int), s));
+    CK(cudaFuncSetAttribute(k_spgemm_count<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            kMaxCap * 4));
+    k_spgemm_count<false><<<n, 256, cap_s * 4, s>>>(n, nullptr, A.ptr.p, A.col.p, B.ptr.p, B.col.p,
+                                                   cap_s, nullptr, nullptr, cnt.p, ovf.p);
+    CK_LAUNCH();
+    int novf = 0;
+    CK(cudaMemcpyAsync(&novf, ovf.p, sizeof novf, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    // rows whose distinct count exceeds the shared table: global slabs
+    DevBuf<int> orows;
+    DevBuf<int64_t> goff;
+    DevBuf<int> gkeys, gvals, glist;
+    if (novf) {
+        std::vector<int> hcnt(n);
+        std::vector<int64_t> hub(n);
+        CK(cudaMemcpyAsync(hcnt.data(), cnt.p, sizeof(int) * n, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(hub.data(), ub.p, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        std::vector<int> rows;
+        std::vector<int64_t> off{0};
+        for (int i = 0; i < n; ++i)
+            if (hcnt[i] < 0) {
+                rows.push_back(i);
+                off.push_back(off.back() + next_pow2(2 * std::min<int64_t>(hub[i], B.ncols) + 2));
+            }
+        orows.alloc(rows.size(), s);
+        goff.alloc(off.size(), s);
+        CK(cudaMemcpyAsync(orows.p, rows.data(), sizeof(int) * rows.size(), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(goff.p, off.data(), sizeof(int64_t) * off.size(), cudaMemcpyHostToDevice, s));
+        gkeys.alloc(off.back(), s);
+        gvals.alloc(off.back(), s);
+        glist.alloc(off.back() / 2 + 1, s);
+        k_spgemm_count<true><<<static_cast<int>(rows.size()), 256, 0, s>>>(
+            static_cast<int>(rows.size()), orows.p, A.ptr.p, A.col.p, B.ptr.p, B.col.p, 0, gkeys.p,
+            goff.p, cnt.p, ovf.p);
+        CK_LAUNCH();
+    }
+    C.nnzb = scan_counts(cnt.p, C.ptr.p, n, s);
+    C.col.alloc(C.nnzb, s);
+    C.val.alloc(9 * C.nnzb, s);
+    // numeric: table sized by the actual max row count
+    DevBuf<int> mc(1, s);
+    size_t b3 = 0;
+    CK(cub::DeviceReduce::Max(nullptr, b3, cnt.p, mc.p, n, s));
+    DevBuf<char> ws3(b3, s);
+    CK(cub::DeviceReduce::Max(ws3.p, b3, cnt.p, mc.p, n, s));
+    int maxc = 0;
+    CK(cudaMemcpyAsync(&maxc, mc.p, sizeof maxc, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const int cap_n = std::min(kMaxCap, std::max(256, next_pow2(2 * static_cast<int64_t>(maxc) + 2)));
+    const size_t smem_n = static_cast<size_t>(cap_n) * 4 * 2 + static_cast<size_t>(cap_n / 2) * 4;
+    CK(cudaFuncSetAttribute(k_spgemm_numeric<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            kMaxCap * 10));
+    k_spgemm_numeric<false><<<n, 256, smem_n, s>>>(n, nullptr, A.ptr.p, A.col.p, A.val.p,
+                                                  B.ptr.p, B.col.p, B.val.p, cap_n, nullptr,
+                                                  nullptr, nullptr, nullptr, C.ptr.p, C.col.p,
+                                                  C.val.p);
+    CK_LAUNCH();
+    if (novf) {
+        const int nr = static_cast<int>(orows.n);
+        k_spgemm_numeric<true><<<nr, 256, 0, s>>>(nr, orows.p, A.ptr.p, A.col.p, A.val.p, B.ptr.p,
+                                                 B.col.p, B.val.p, 0, gkeys.p, gvals.p, glist.p,
+                                                 goff.p, C.ptr.p, C.col.p, C.val.p);
+        CK_LAUNCH();
+    }
+}
+
+void fix_decoupled_rows(Bsr3 &A, cudaStream_t s) {
+    const int *ap = A.ptr.p, *ac = A.col.p;
+    double *av = A.val.p;
+    for_each(A.nrows, [=] __device__(int64_t i) {
+        int dg = -1;
+        for (int j = ap[i]; j < ap[i + 1]; ++j)
+            if (ac[j] == i) { dg = j; break; }
+        for (int r = 0; r < 3; ++r) {
+            bool zero_row = true;
+            for (int j = ap[i]; zero_row && j < ap[i + 1]; ++j)
+                for (int c = 0; c < 3; ++c)
+                    if (av[9 * static_cast<int64_t>(j) + 3 * r + c] != 0.0) { zero_row = false; break; }
+            if (zero_row && dg >= 0) av[9 * static_cast<int64_t>(dg) + 4 * r] = 1.0;
+        }
+    }, s);
+}
+
+void setup_smoother(const Bsr3 &A, int kind, double omega, Smoother &M, DevError *err,
+                    cudaStream_t s) {
+    const int *ap = A.ptr.p, *ac = A.col.p;
+    const double *av = A.val.p;
+    DevError *ep = err;
+    if (kind == SAMG_SMOOTHER_JACOBI) {
+        // relaxation.hpp:147-162; the damping is folded in (omega * (1/d)),
+        // the same first product as relaxation.hpp:172
+        M.kind = SM_POINT;
+        M.data.alloc(3 * A.nrows, s);
+        double *m = M.data.p;
+        for_each(A.nrows, [=] __device__(int64_t i) {
+            int dg = -1;
+            for (int j = ap[i]; j < ap[i + 1]; ++j) if (ac[j] == i) { dg = j; break; }
+            for (int r = 0; r < 3; ++r) {
+                const double d = dg >= 0 ? av[9 * static_cast<int64_t>(dg) + 4 * r] : 0.0;
+                if (d == 0.0) { raise(ep, SAMG_ZERO_DIAGONAL, 3 * i + r); m[3 * i + r] = 0.0; continue; }
+                m[3 * i + r] = __dmul_rn(omega, __ddiv_rn(1.0, d));
+            }
+        }, s);
+        return;
+    }
+    M.kind = SM_BLOCK;
+    M.data.alloc(9 * A.nrows, s);
+    double *m = M.data.p;
+    const bool spai = kind == SAMG_SMOOTHER_SPAI0;
+    for_each(A.nrows, [=] __device__(int64_t i) {
+        int dg = -1;
+        double den = 0.0;
+        for (int j = ap[i]; j < ap[i + 1]; ++j) {
+            if (ac[j] == i) dg = j;
+            const double *b = av + 9 * static_cast<int64_t>(j);
+            for (int e = 0; e < 9; ++e) den = __dadd_rn(den, __dmul_rn(b[e], b[e]));
+        }
+        double *Mi = m + 9 * i;
+        if (dg < 0) { raise(ep, SAMG_MISSING_DIAGONAL, i); return; }
+        const double *a = av + 9 * static_cast<int64_t>(dg);
+        if (spai) {
+            if (den == 0.0) { raise(ep, SAMG_ZERO_DIAGONAL, i); return; }
+            for (int e = 0; e < 9; ++e) Mi[e] = __ddiv_rn(a[e], den);
+            return;
+        }
+        // inverse (static_block.hpp:155-194)
+        double lu[9];
+        int piv[3];
+        for (int e = 0; e < 9; ++e) lu[e] = a[e];
+        for (int k = 0; k < 3; ++k) {
+            int p = k;
+            for (int r = k + 1; r < 3; ++r)
+                if (fabs(lu[r * 3 + k]) > fabs(lu[p * 3 + k])) p = r;
+            piv[k] = p;
+            if (p != k)
+                for (int j = 0; j < 3; ++j) { const double t = lu[k * 3 + j]; lu[k * 3 + j] = lu[p * 3 + j]; lu[p * 3 + j] = t; }
+            if (fabs(lu[k * 3 + k]) < 1e-300) { raise(ep, SAMG_SINGULAR_BLOCK, i); return; }
+            const double d = __ddiv_rn(1.0, lu[k * 3 + k]);
+            for (int r = k + 1; r < 3; ++r) {
+                const double l = __dmul_rn(lu[r * 3 + k], d);
+                lu[r * 3 + k] = l;
+                for (int j = k + 1; j < 3; ++j) lu[r * 3 + j] = __dsub_rn(lu[r * 3 + j], __dmul_rn(l, lu[k * 3 + j]));
+            }
+        }
+        for (int c = 0; c < 3; ++c) {
+            double x[3] = {0.0, 0.0, 0.0};
+            x[c] = 1.0;
+            for (int k = 0; k < 3; ++k)
+                if (piv[k] != k) { const double t = x[k]; x[k] = x[piv[k]]; x[piv[k]] = t; }
+            for (int r = 1; r < 3; ++r)
+                for (int j = 0; j < r; ++j) x[r] = __dsub_rn(x[r], __dmul_rn(lu[r * 3 + j], x[j]));
+            for (int r = 2; r >= 0; --r) {
+                for (int j = r + 1; j < 3; ++j) x[r] = __dsub_rn(x[r], __dmul_rn(lu[r * 3 + j], x[j]));
+                x[r] = __ddiv_rn(x[r], lu[r * 3 + r]);
+            }
+            for (int r = 0; r < 3; ++r) Mi[r * 3 + c] = __dmul_rn(omega, x[r]);
+        }
+    }, s);
+}
+
+} // namespace samgb

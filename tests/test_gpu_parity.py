@@ -1,0 +1,241 @@
+"""GPU parity: the B200 path (through the C-ABI) against the reference.
+
+The checker is oracle/_ref (the unmodified reference library compiled from
+/root/reference, shipped as a built .so) and oracle/libsamg_oracle.so (the
+C restatement).  Bars (BASELINE.json north_star):
+  * aggregates bit-exact per level,
+  * hierarchy matrices within 1e-11 relative Frobenius (here: bit-exact,
+    because the setup kernels reproduce the reference's operation order),
+  * CG iterations within +-1 of the reference count at rtol 1e-8,
+  * final solution within 1e-7 relative.
+"""
+import numpy as np
+import pytest
+
+from oracle.oracle import Params, SM_BLOCK_JACOBI, SM_JACOBI, SM_SPAI0
+
+pytestmark = pytest.mark.gpu
+
+SM = {"spai0": SM_SPAI0, "jacobi": SM_JACOBI, "block_jacobi": SM_BLOCK_JACOBI}
+
+
+def make_problem(pb, nx, ny=None, nz=None, **kw):
+    ny = nx if ny is None else ny
+    nz = nx if nz is None else nz
+    return pb.generate_hex(nx=nx, ny=ny, nz=nz, **kw)
+
+
+def rel_fro(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def compare_hierarchies(h, hr, orc_h=None, smoother="spai0", omega=0.72):
+    assert h.nlevels == hr.nlevels
+    for l in range(h.nlevels):
+        for w in (0, 1, 2):
+            if w and l == h.nlevels - 1:
+                continue
+            g, r = h.level(l, w), hr.level(l, w)
+            assert g[0] == r[0] and g[1] == r[1], (l, w)
+            np.testing.assert_array_equal(g[2], r[2], err_msg=f"ptr l={l} w={w}")
+            np.testing.assert_array_equal(g[3], r[3], err_msg=f"col l={l} w={w}")
+            # bit-exact values (north_star bar: 1e-11 relative Frobenius)
+            assert rel_fro(g[4], r[4]) <= 1e-11, (l, w, rel_fro(g[4], r[4]))
+            np.testing.assert_array_equal(g[4], r[4], err_msg=f"val l={l} w={w}")
+        if l < h.nlevels - 1:
+            ga, gc = h.aggregates(l)
+            ra, rc = hr.aggregates(l)
+            assert gc == rc
+            np.testing.assert_array_equal(ga, ra)
+            if orc_h is not None:
+                sm_o = orc_h.smoother(l)
+                sm_g = h.smoother(l)
+                if smoother == "jacobi":
+                    sm_o = omega * sm_o
+                np.testing.assert_array_equal(sm_g, sm_o)
+    assert h.coarse_dim == hr.coarse_dim
+    assert h.memory_footprint() == hr.memory_footprint
+
+
+CASES = [
+    # (name, problem kwargs, smoother, smoother_omega, coarse_enough)
+    ("cube4_keep_spai0", dict(nx=4, dirichlet="keep_rows"), "spai0", 0.72, 100),
+    ("cube6_keep_jacobi", dict(nx=6, dirichlet="keep_rows"), "jacobi", 0.72, 100),
+    ("cube6_free_bjac", dict(nx=6, dirichlet="eliminate"), "block_jacobi", 0.5, 100),
+    ("box975_free_traction", dict(nx=9, ny=7, nz=5, dirichlet="eliminate", load="traction_xend"),
+     "spai0", 0.72, 150),
+    ("cube7_hetero_jacobi05", dict(nx=7, dirichlet="eliminate", heterogeneous=True, load="random",
+                                   seed=7), "jacobi", 0.5, 120),
+    ("beam_xslow", dict(nx=12, ny=4, nz=4, lx=3.0, dirichlet="eliminate", load="traction_xend",
+                        x_slowest=True), "spai0", 0.72, 120),
+    ("cube8_keep_noise", dict(nx=8, dirichlet="keep_rows", noise=0.01, seed=3), "spai0", 0.72, 300),
+]
+
+
+@pytest.mark.parametrize("name,kw,smoother,omega,ce", CASES, ids=[c[0] for c in CASES])
+def test_setup_and_solve_parity(gpu, ref, orc, name, kw, smoother, omega, ce):
+    pb = gpu
+    p = make_problem(pb, **kw)
+    A = p.csr()
+    B = p.nullspace()
+    prm = pb.AmgParams(smoother=smoother, smoother_omega=omega, coarse_enough=ce)
+    h = pb.setup(A, B, "ns_block", prm)
+    rp = Params(smoother=SM[smoother], smoother_omega=omega, coarse_enough=ce)
+    hr = ref.setup(A[0], A[1], A[2], A[3], B, rp)
+    ho = orc.setup(A[0], A[1], A[2], A[3], B, rp)
+    assert h.nlevels >= 2
+    compare_hierarchies(h, hr, ho, smoother, omega)
+
+    f = p.rhs
+    u, rep = h.cg_solve(f)
+    ur, rr = hr.cg_solve(f)
+    assert rep["converged"] == rr["converged"]
+    assert abs(rep["iterations"] - rr["iterations"]) <= 1, (rep, rr)
+    if rr["converged"]:
+        assert rep["relative_residual"] <= 1e-8 * 1.01
+        assert rel_fro(u, ur) <= 1e-7
+    assert rep["preconditioner_bytes"] == hr.memory_footprint
+
+    # V-cycle from a nonzero initial approximation (hierarchy.hpp:408)
+    rng = np.random.default_rng(5)
+    u0 = rng.uniform(-1, 1, f.size)
+    vg = h.vcycle(f, u0)
+    vo = ho.vcycle(f)  # oracle V-cycle from zero
+    vz = h.vcycle(f)
+    assert rel_fro(vz, vo) <= 1e-12
+    assert np.all(np.isfinite(vg))
+
+
+def test_vcycle_linear_and_deterministic(gpu):
+    pb = gpu
+    p = make_problem(pb, 6, dirichlet="eliminate")
+    h = pb.setup(p.csr(), p.nullspace(), "ns_block", pb.AmgParams(coarse_enough=100))
+    rng = np.random.default_rng(109)
+    f = rng.uniform(-1, 1, p.n)
+    u1 = h.vcycle(f)
+    u2 = h.vcycle(2.0 * f)
+    assert np.abs(u2 - 2.0 * u1).max() <= 1e-12 * np.abs(u1).max()
+    np.testing.assert_array_equal(h.vcycle(f), u1)
+    a, ra = h.cg_solve(p.rhs)
+    b, rb = h.cg_solve(p.rhs)
+    np.testing.assert_array_equal(a, b)
+    assert ra["iterations"] == rb["iterations"]
+
+
+def test_zero_rhs(gpu):
+    pb = gpu
+    p = make_problem(pb, 4, dirichlet="eliminate")
+    h = pb.setup(p.csr(), p.nullspace(), "ns_block", pb.AmgParams(coarse_enough=60))
+    u, rep = h.cg_solve(np.zeros(p.n))
+    assert rep["converged"] and rep["iterations"] == 0
+    assert not u.any()
+
+
+def test_single_level_direct_solve(gpu, ref):
+    """coarse_enough >= n: degenerate hierarchy, the V-cycle is the direct
+    solve (hierarchy.hpp:416-419) and CG converges in one iteration."""
+    pb = gpu
+    p = make_problem(pb, 3, dirichlet="eliminate")
+    h = pb.setup(p.csr(), p.nullspace(), "ns_block", pb.AmgParams(coarse_enough=10**6))
+    assert h.nlevels == 1
+    u, rep = h.cg_solve(p.rhs)
+    assert rep["converged"] and rep["iterations"] == 1
+    A = p.csr()
+    hr = ref.setup(A[0], A[1], A[2], A[3], p.nullspace(), Params(coarse_enough=10**6))
+    ur, rr = hr.cg_solve(p.rhs)
+    assert rr["iterations"] == 1
+    assert rel_fro(u, ur) <= 1e-10
+
+
+def test_breakdown_on_indefinite(gpu):
+    pb = gpu
+    p = make_problem(pb, 4, dirichlet="eliminate")
+    n, ptr, col, val = p.csr()
+    with pytest.raises(pb.BreakdownNonSpd):
+        h = pb.setup((n, ptr, col, -val), p.nullspace(), "ns_block", pb.AmgParams(coarse_enough=60))
+        h.cg_solve(p.rhs)
+
+
+def test_zero_diagonal_rejected(gpu):
+    pb = gpu
+    p = make_problem(pb, 4, dirichlet="eliminate")
+    val = p.val.copy()
+    # zero the diagonal block's (0,0) entry of row 0: point Jacobi must throw
+    d = np.where(p.col[p.ptr[0]:p.ptr[1]] == 0)[0][0]
+    val[d, 0, 0] = 0.0
+    with pytest.raises(pb.ZeroDiagonal):
+        pb.setup_bsr3(p.nbrows, p.ptr, p.col, val.reshape(-1), p.nullspace(), "ns_block",
+                      pb.AmgParams(smoother="jacobi", coarse_enough=60))
+
+
+def test_unsupported_pipelines(gpu):
+    pb = gpu
+    p = make_problem(pb, 3, dirichlet="eliminate")
+    for pl in ("scalar", "block", "ns_scalar", "ns_hybrid1", "ns_hybrid2"):
+        with pytest.raises(pb.Unsupported):
+            pb.setup(p.csr(), p.nullspace(), pl)
+    with pytest.raises(pb.Unsupported):
+        pb.setup(p.csr(), p.nullspace(), "ns_block", pb.AmgParams(smoother="ilu0"))
+
+
+def test_spmv_matches_reference(gpu, ref):
+    pb = gpu
+    p = make_problem(pb, 19, dirichlet="eliminate")
+    rng = np.random.default_rng(11)
+    x = rng.uniform(-1, 1, p.n)
+    y0 = rng.uniform(-1, 1, p.n)
+    A = pb.Bsr3.from_host(p.nbrows, p.nbrows, p.ptr, p.col, p.val.reshape(-1))
+    for alpha, beta in ((1.0, 0.0), (-1.0, 1.0), (0.5, -2.0)):
+        yg = A.spmv(x, alpha, beta, y0)
+        yr = ref.spmv_bsr3(p.nbrows, p.nbrows, p.ptr, p.col, p.val.reshape(-1), x, alpha, beta, y0)
+        assert np.abs(yg - yr).max() <= 1e-13 * np.abs(yr).max()
+    nr, nc, ptr, col, val = A.download()
+    np.testing.assert_array_equal(ptr, p.ptr)
+    np.testing.assert_array_equal(col, p.col)
+    np.testing.assert_array_equal(val, p.val)
+
+
+def test_galerkin_random_triples(gpu, orc):
+    """acceptance.cpp:297-332 (criterion 9) restated: random block triples,
+    GPU Galerkin vs the reference order, bit-exact."""
+    pb = gpu
+    rng = np.random.default_rng(223)
+
+    def rand_bsr(nr, nc, dens):
+        mask = rng.random((nr, nc)) < dens
+        ptr = np.concatenate([[0], np.cumsum(mask.sum(1))]).astype(np.int64)
+        col = np.nonzero(mask)[1].astype(np.int64)
+        val = rng.uniform(-1, 1, (col.size, 3, 3))
+        return nr, nc, ptr, col, val
+
+    for trial in range(40):
+        nb = int(rng.integers(2, 40))
+        mb = max(1, nb // 2)
+        R = rand_bsr(mb, nb, 0.3)
+        A = rand_bsr(nb, nb, 0.3)
+        P = rand_bsr(nb, mb, 0.3)
+        dR, dA, dP = (pb.Bsr3.from_host(m[0], m[1], m[2], m[3], m[4].reshape(-1)) for m in (R, A, P))
+        C = pb.Bsr3.galerkin(dR, dA, dP).download()
+        Co = orc.galerkin_bsr3(R, A, P)
+        assert C[0] == Co[0] and C[1] == Co[1]
+        np.testing.assert_array_equal(C[2], Co[2])
+        np.testing.assert_array_equal(C[3], Co[3])
+        np.testing.assert_array_equal(C[4], Co[4])
+
+
+@pytest.mark.slow
+def test_c0_full_size_parity(gpu, ref):
+    """BASELINE config 0: 20x20x20 nodes, E=1, nu=0.3, x=0 clamped, body
+    force + U[-0.01,0.01] noise, SPAI0; both Dirichlet forms."""
+    pb = gpu
+    for dirichlet in ("eliminate", "keep_rows"):
+        p = make_problem(pb, 19, dirichlet=dirichlet, noise=0.01, seed=2022)
+        A, B = p.csr(), p.nullspace()
+        h = pb.setup(A, B, "ns_block", pb.AmgParams(smoother="spai0"))
+        hr = ref.setup(A[0], A[1], A[2], A[3], B, Params(smoother=SM_SPAI0))
+        compare_hierarchies(h, hr)
+        u, rep = h.cg_solve(p.rhs)
+        ur, rr = hr.cg_solve(p.rhs)
+        assert rep["converged"] and rr["converged"]
+        assert abs(rep["iterations"] - rr["iterations"]) <= 1, (rep, rr)
+        assert rel_fro(u, ur) <= 1e-7
