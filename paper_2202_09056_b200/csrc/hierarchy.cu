@@ -6,6 +6,8 @@
 
 #include <chrono>
 #include <cmath>
+#include <cstddef>
+#include <cstdlib>
 #include <memory>
 #include <utility>
 
@@ -42,6 +44,8 @@ Hierarchy::~Hierarchy() {
     r.release(); z.release(); p.release(); q.release();
     fbuf.release(); ubuf.release(); partials.release(); sc.release(); err.release();
     if (sc_host) cudaFreeHost(sc_host);
+    if (sc_stage) cudaFreeHost(sc_stage);
+    if (cg_exec) cudaGraphExecDestroy(cg_exec);
     if (stream && owns_stream) {
         cudaStreamSynchronize(stream);
         cudaStreamDestroy(stream);
@@ -140,6 +144,7 @@ Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int6
     H->sc.alloc(1, s);
     CK(cudaMemsetAsync(H->sc.p, 0, sizeof(CgScalars), s));
     CK(cudaMallocHost(&H->sc_host, sizeof(CgScalars)));
+    CK(cudaMallocHost(&H->sc_stage, sizeof(CgScalars)));
     CK(cudaStreamSynchronize(s));
     H->setup_seconds = now_s() - t_start;
     H->owns_stream = true;
@@ -200,10 +205,53 @@ void Hierarchy::vcycle(const double *f0, double *u0, bool zero_guess) {
         CK(cudaMemcpyAsync(u0, cur[0], sizeof(double) * finest_dim(), cudaMemcpyDeviceToDevice, s));
 }
 
+// One CG iteration (cg.hpp:63-77) on the internal buffers, as recorded into
+// the body of the graph's while node.  The loop condition is set by
+// k_finalize_loop right after ||r|| is known; the V-cycle and p update that
+// follow in the same pass are then unused on the last pass (u and r are
+// final before them).
+void Hierarchy::build_cg_graph() {
+    cudaStream_t s = stream;
+    const int64_t n = finest_dim();
+    const Bsr3 &A0 = levels.front().A;
+    cudaGraph_t g;
+    CK(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle h;
+    CK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams np{};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = h;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t wnode;
+    CK(cudaGraphAddNode(&wnode, g, nullptr, 0, &np));
+    cudaGraph_t body = np.conditional.phGraph_out[0];
+    CK(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    int nparts = 0;
+    launch_spmv_dot(A0, p.p, q.p, partials.p, &nparts, s);
+    launch_finalize(1, partials.p, nparts, sc.p, s);
+    launch_cg_update(n, sc.p, p.p, q.p, ubuf.p, r.p, partials.p, s);
+    launch_finalize_loop(partials.p, kRedBlocks, sc.p, h, s);
+    vcycle(r.p, z.p, true);
+    launch_dot_partials(n, r.p, z.p, partials.p, s);
+    launch_finalize(2, partials.p, kRedBlocks, sc.p, s);
+    launch_p_update(n, sc.p, z.p, p.p, s);
+    cudaGraph_t captured = body;
+    CK(cudaStreamEndCapture(s, &captured));
+    CK(cudaGraphInstantiate(&cg_exec, g, 0));
+    CK(cudaGraphDestroy(g));
+}
+
 // PCG from a zero guess (cg_solve_op, cg.hpp:39-83, and cg_solve(hierarchy),
-// cg.hpp:87-112).  alpha/beta stay on the device; the host reads the
-// recurrence residual once per iteration for the stopping test.
+// cg.hpp:87-112).  alpha/beta stay on the device.  By default the whole
+// iteration loop runs as one CUDA graph with a device-side while condition
+// (no host round trip per iteration); SAMG_CG_GRAPH=0 selects the host loop
+// that reads ||r|| back every iteration.
 samg_solve_report Hierarchy::cg(const double *d_f, double *d_u, const samg_cg_params &cp) {
+    static const bool use_graph = [] {
+        const char *e = std::getenv("SAMG_CG_GRAPH");
+        return !(e && e[0] == '0');
+    }();
     cudaStream_t s = stream;
     const double t0 = now_s();
     samg_solve_report rep{};
@@ -211,7 +259,7 @@ samg_solve_report Hierarchy::cg(const double *d_f, double *d_u, const samg_cg_pa
     rep.setup_seconds = setup_seconds;
     const int64_t n = finest_dim();
     const Bsr3 &A0 = levels.front().A;
-    double *pr = r.p, *pz = z.p, *pp = p.p, *pq = q.p, *pu = d_u;
+    double *pr = r.p, *pz = z.p, *pp = p.p, *pq = q.p, *pu = ubuf.p;
     CK(cudaMemcpyAsync(pr, d_f, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
     launch_fill(n, 0.0, pu, s);
     CK(cudaMemsetAsync(sc.p, 0, sizeof(CgScalars), s));
@@ -221,6 +269,9 @@ samg_solve_report Hierarchy::cg(const double *d_f, double *d_u, const samg_cg_pa
     CK(cudaStreamSynchronize(s));
     const double norm_f = std::sqrt(sc_host->rr);
     if (norm_f == 0.0) {
+        if (pu != d_u)
+            CK(cudaMemcpyAsync(d_u, pu, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+        CK(cudaStreamSynchronize(s));
         rep.converged = 1;
         rep.relative_residual = 0.0;
         rep.preconditioner_bytes = memory_footprint();
@@ -233,7 +284,26 @@ samg_solve_report Hierarchy::cg(const double *d_f, double *d_u, const samg_cg_pa
     CK(cudaMemcpyAsync(pp, pz, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
     double res_norm = norm_f;
     int iter = 0;
-    while (res_norm / norm_f > cp.tol && iter < cp.max_iterations) {
+    if (use_graph && norm_f / norm_f > cp.tol && cp.max_iterations > 0) {
+        sc_stage->norm_f = norm_f;
+        sc_stage->tol = cp.tol;
+        sc_stage->breakdown = 0;
+        sc_stage->iter = 0;
+        sc_stage->max_iter = cp.max_iterations;
+        const size_t off = offsetof(CgScalars, norm_f);
+        CK(cudaMemcpyAsync(reinterpret_cast<char *>(sc.p) + off,
+                           reinterpret_cast<char *>(sc_stage) + off, sizeof(CgScalars) - off,
+                           cudaMemcpyHostToDevice, s));
+        if (!cg_exec) build_cg_graph();
+        CK(cudaGraphLaunch(cg_exec, s));
+        CK(cudaMemcpyAsync(sc_host, sc.p, sizeof(CgScalars), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (sc_host->breakdown)
+            fail(SAMG_BREAKDOWN_NON_SPD, "cg: p'Ap <= 0, matrix or preconditioner not SPD");
+        iter = sc_host->iter;
+        res_norm = std::sqrt(sc_host->rr);
+    }
+    while (!use_graph && res_norm / norm_f > cp.tol && iter < cp.max_iterations) {
         int nparts = 0;
         launch_spmv_dot(A0, pp, pq, partials.p, &nparts, s);
         launch_finalize(1, partials.p, nparts, sc.p, s);
@@ -258,6 +328,8 @@ samg_solve_report Hierarchy::cg(const double *d_f, double *d_u, const samg_cg_pa
     launch_dot_partials(n, pq, pq, partials.p, s);
     launch_finalize(0, partials.p, kRedBlocks, sc.p, s);
     CK(cudaMemcpyAsync(sc_host, sc.p, sizeof(CgScalars), cudaMemcpyDeviceToHost, s));
+    if (pu != d_u)
+        CK(cudaMemcpyAsync(d_u, pu, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
     CK(cudaStreamSynchronize(s));
     rep.relative_residual = std::sqrt(sc_host->rr) / norm_f;
     rep.preconditioner_bytes = memory_footprint();

@@ -31,6 +31,9 @@ struct Hierarchy {
     DevBuf<double> r, z, p, q, fbuf, ubuf, partials;
     DevBuf<CgScalars> sc;
     CgScalars *sc_host = nullptr;  // pinned mirror
+    CgScalars *sc_stage = nullptr; // pinned staging for loop parameters
+    cudaGraphExec_t cg_exec = nullptr;  // device-resident CG loop (while node)
+    void build_cg_graph();
 
     ~Hierarchy();
     int64_t finest_dim() const { return 3 * levels.front().A.nrows; }

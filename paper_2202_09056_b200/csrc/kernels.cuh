@@ -50,16 +50,24 @@ void launch_smooth_zero(int64_t nrows, const Smoother &M, const double *f, doubl
 // q = A p and per-block partial sums of p.q (fused CG matvec, cg.hpp:63-64)
 void launch_spmv_dot(const Bsr3 &A, const double *p, double *q, double *partials,
                      int *nparts, cudaStream_t s);
+// leading dimension of the dense coarse inverse (even, for 16-byte loads)
+inline int64_t dense_ld(int64_t n) { return (n + 1) & ~static_cast<int64_t>(1); }
 // dense coarse solve u = Ainv f (replaces dense_lu::solve, hierarchy.hpp:113-129)
 void launch_dense_gemv(int64_t n, const double *Ainv, const double *f, double *u,
                        cudaStream_t s);
 
 // CG device scalars (cg.hpp:39-83).
 struct CgScalars {
-    double pq, rho, rho_new, rr, alpha, beta;
-    int breakdown;
-    int pad;
+    double pq, rho, rho_new, rr, alpha, beta, norm_f, tol;
+    int breakdown, iter, max_iter, pad;
 };
+// device-side loop control of the graph-resident CG (cg.hpp:62-72):
+// finalize r.r, ++iter, continue iff ||r||/||f|| > tol && iter < max && !breakdown
+void launch_finalize_loop(const double *partials, int nparts, CgScalars *sc,
+                          cudaGraphConditionalHandle h, cudaStream_t s);
+// resets iter/breakdown and sets the loop condition before the first pass
+// (norm_f, tol, max_iter already in sc)
+void launch_cg_loop_init(CgScalars *sc, cudaGraphConditionalHandle h, cudaStream_t s);
 constexpr int kRedBlocks = 592;   // 4 x 148 SMs: fixed => deterministic sums
 void launch_dot_partials(int64_t n, const double *x, const double *y, double *partials,
                          cudaStream_t s);
