@@ -71,6 +71,13 @@ void need_device(int device) {
     }
     require(device >= 0 && device < n, SAMG_INVALID_ARGUMENT, "device ordinal out of range");
     CK(cudaSetDevice(device));
+    // keep stream-ordered allocations cached across syncs (setup allocates
+    // and frees per level; returning memory to the driver each time costs
+    // tens of milliseconds per setup)
+    cudaMemPool_t pool;
+    CK(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;
+    CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
 }
 
 cudaStream_t new_stream() {

@@ -90,14 +90,30 @@ __global__ void __launch_bounds__(kPT) k_panel_gj(int64_t n, int64_t k0, int bk,
             pidx[blockIdx.x] = wi[0];
         }
         grid.sync();
-        // b. global pivot (same in every CTA), read pivot row and row k
-        if (threadIdx.x == 0) {
+        // b. global pivot (same in every CTA): block-parallel reduction of
+        //    the per-CTA candidates, then read pivot row and row k
+        {
             double bv = -1.0;
             int64_t bix = n;
-            for (unsigned c = 0; c < gridDim.x; ++c)
-                if (pval[c] > bv || (pval[c] == bv && pidx[c] < bix)) { bv = pval[c]; bix = pidx[c]; }
-            s_p = bix;
-            s_v = bix < n ? Pn[bix * 2 * kB + q] : 0.0;
+            for (unsigned c = threadIdx.x; c < gridDim.x; c += blockDim.x) {
+                const double v = pval[c];
+                const int64_t i = pidx[c];
+                if (v > bv || (v == bv && i < bix)) { bv = v; bix = i; }
+            }
+            for (int off = 16; off >= 1; off >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
+                const int64_t oi = __shfl_xor_sync(0xffffffffu, bix, off);
+                if (ov > bv || (ov == bv && oi < bix)) { bv = ov; bix = oi; }
+            }
+            __syncthreads();
+            if (lane == 0) { wv[w] = bv; wi[w] = bix; }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                for (int t = 1; t < kPT / 32; ++t)
+                    if (wv[t] > wv[0] || (wv[t] == wv[0] && wi[t] < wi[0])) { wv[0] = wv[t]; wi[0] = wi[t]; }
+                s_p = wi[0];
+                s_v = wi[0] < n ? Pn[wi[0] * 2 * kB + q] : 0.0;
+            }
         }
         __syncthreads();
         const int64_t p = s_p;

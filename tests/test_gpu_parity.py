@@ -239,3 +239,14 @@ def test_c0_full_size_parity(gpu, ref):
         assert rep["converged"] and rr["converged"]
         assert abs(rep["iterations"] - rr["iterations"]) <= 1, (rep, rr)
         assert rel_fro(u, ur) <= 1e-7
+
+
+def test_cpp_shim_program(gpu):
+    """include/samg_b200.hpp used exactly like the reference's C++ API."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(gpu.LIB_PATH), "csrc", "build", "shim_test")
+    assert os.path.exists(exe), "shim_test not built (run __graft_entry__.build())"
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert out.stdout.startswith("ok")
