@@ -86,7 +86,9 @@ Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int6
     // level loop (hierarchy.hpp:338-363)
     while (3 * H->levels.back().A.nrows > prm.coarse_enough) {
         Level &Li = H->levels.back();
-        const int pbs = H->levels.size() == 1 ? prm.point_block_size : k;
+        // ns pipelines force point_block_size = 3 on the fine level
+        // (hierarchy.hpp:284-285), then use the nullspace width (:351-353)
+        const int pbs = H->levels.size() == 1 ? 3 : k;
         if (pbs % 3) fail(SAMG_NOT_DIVISIBLE, "ns_block: node size must be a multiple of 3");
         const int h = pbs / 3;
         if (Li.A.nrows % h)

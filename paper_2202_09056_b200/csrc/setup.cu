@@ -649,6 +649,144 @@ __global__ void __launch_bounds__(256) k_spgemm_numeric(
     }
 }
 
+// Warp-per-row variants (8 rows per CTA) for rows with at most kWCap/2-1
+// distinct columns: same hash, same bitonic sort, same in-order
+// accumulation, __syncwarp instead of the CTA barrier, so 8 rows progress
+// concurrently.  Results are bit-identical to the CTA kernels.
+constexpr int kWCap = 1024;
+constexpr int kWPB = 8;
+
+__global__ void __launch_bounds__(256) k_spgemm_wcount(int nrows, const int *ap, const int *ac,
+                                                       const int *bp, const int *bc, int *cnt) {
+    __shared__ int keys_all[kWPB][kWCap];
+    __shared__ int n_all[kWPB];
+    const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int row = blockIdx.x * kWPB + w;
+    if (row >= nrows) return;  // whole warp
+    int *keys = keys_all[w];
+    for (int t = lane; t < kWCap; t += 32) keys[t] = -1;
+    if (lane == 0) n_all[w] = 0;
+    __syncwarp();
+    bool full = false;
+    for (int ja = ap[row]; ja < ap[row + 1]; ++ja) {
+        const int kk = ac[ja];
+        for (int jb = bp[kk] + lane; jb < bp[kk + 1] && !full; jb += 32) {
+            bool ins;
+            const int slot = hash_insert(keys, kWCap, bc[jb], ins);
+            if (slot < 0 || (ins && atomicAdd(n_all + w, 1) + 1 > kWCap / 2 - 1)) full = true;
+        }
+        if (__any_sync(0xffffffffu, full)) { full = true; break; }
+    }
+    __syncwarp();
+    if (lane == 0) cnt[row] = full ? -1 : n_all[w];
+}
+
+__global__ void __launch_bounds__(256) k_spgemm_wnumeric(
+        int nrows, const int *ap, const int *ac, const double *av, const int *bp, const int *bc,
+        const double *bv, const int *cp, int *ccol, double *cval) {
+    extern __shared__ int wsm[];
+    const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int row = blockIdx.x * kWPB + w;
+    if (row >= nrows) return;
+    const int n = cp[row + 1] - cp[row];
+    if (n > kWCap / 2 - 1) return;  // wide row: CTA kernel
+    int *keys = wsm + w * (kWCap * 5 / 2);
+    int *vals = keys + kWCap;
+    int *list = vals + kWCap;
+    for (int t = lane; t < kWCap; t += 32) keys[t] = -1;
+    __syncwarp();
+    for (int ja = ap[row]; ja < ap[row + 1]; ++ja) {
+        const int kk = ac[ja];
+        for (int jb = bp[kk] + lane; jb < bp[kk + 1]; jb += 32) {
+            bool ins;
+            hash_insert(keys, kWCap, bc[jb], ins);
+        }
+    }
+    __syncwarp();
+    // deterministic compaction: ballot over the table in slot order
+    int out = 0;
+    for (int t0 = 0; t0 < kWCap; t0 += 32) {
+        const int key = keys[t0 + lane];
+        const unsigned m = __ballot_sync(0xffffffffu, key != -1);
+        if (key != -1) list[out + __popc(m & ((1u << lane) - 1u))] = key;
+        out += __popc(m);
+    }
+    int np2 = 1;
+    while (np2 < n) np2 <<= 1;
+    for (int t = n + lane; t < np2; t += 32) list[t] = INF;
+    __syncwarp();
+    for (int size = 2; size <= np2; size <<= 1)
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int t = lane; t < np2; t += 32) {
+                const int partner = t ^ stride;
+                if (partner > t) {
+                    const bool up = (t & size) == 0;
+                    const int a = list[t], b = list[partner];
+                    if ((a > b) == up) { list[t] = b; list[partner] = a; }
+                }
+            }
+            __syncwarp();
+        }
+    const int64_t base = cp[row];
+    for (int t = lane; t < n; t += 32) {
+        const int key = list[t];
+        ccol[base + t] = key;
+        vals[hash_find(keys, kWCap, key)] = t;
+        double *cb = cval + 9 * (base + t);
+        for (int e = 0; e < 9; ++e) cb[e] = 0.0;
+    }
+    __syncwarp();
+    // In-order accumulation.  The operands of step ja+1 (A block, this lane's
+    // first B entry and its column) are loaded while step ja accumulates, so
+    // the L2 latency is off the sequential chain; B rows longer than 32
+    // entries finish their extra chunks unpipelined in the same step.
+    const int ja0 = ap[row], jend = ap[row + 1];
+    double am[9], bm[9];
+    int cc = -1, jbc = -1, kend = 0;
+    auto fetch = [&](int ja, double *a_, double *b_, int &c_, int &jb_, int &kend_) {
+        const int kk = ac[ja];
+        const double *a = av + 9 * static_cast<int64_t>(ja);
+#pragma unroll
+        for (int e = 0; e < 9; ++e) a_[e] = a[e];
+        jb_ = bp[kk] + lane;
+        kend_ = bp[kk + 1];
+        c_ = -1;
+        if (jb_ < kend_) {
+            c_ = bc[jb_];
+            const double *b = bv + 9 * static_cast<int64_t>(jb_);
+#pragma unroll
+            for (int e = 0; e < 9; ++e) b_[e] = b[e];
+        }
+    };
+    if (ja0 < jend) fetch(ja0, am, bm, cc, jbc, kend);
+    for (int ja = ja0; ja < jend; ++ja) {
+        double an[9], bn[9];
+        int cn = -1, jbn = -1, kendn = 0;
+        if (ja + 1 < jend) fetch(ja + 1, an, bn, cn, jbn, kendn);
+        if (cc >= 0) {
+            const int slot = vals[hash_find(keys, kWCap, cc)];
+            double prod[9];
+            blk_mul(am, bm, prod);
+            double *cb = cval + 9 * (base + slot);
+#pragma unroll
+            for (int e = 0; e < 9; ++e) cb[e] = __dadd_rn(cb[e], prod[e]);
+            for (int jb = jbc + 32; jb < kend; jb += 32) {
+                const int sl = vals[hash_find(keys, kWCap, bc[jb])];
+                blk_mul(am, bv + 9 * static_cast<int64_t>(jb), prod);
+                double *cb2 = cval + 9 * (base + sl);
+#pragma unroll
+                for (int e = 0; e < 9; ++e) cb2[e] = __dadd_rn(cb2[e], prod[e]);
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int e = 0; e < 9; ++e) { am[e] = an[e]; bm[e] = bn[e]; }
+        cc = cn;
+        jbc = jbn;
+        kend = kendn;
+    }
+}
+
 __global__ void k_spgemm_ub(int nrows, const int *ap, const int *ac, const int *bp,
                             int64_t *ub) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -958,11 +1096,34 @@ void spgemm(const Bsr3 &A, const Bsr3 &B, Bsr3 &C, cudaStream_t s) {
     const int cap_s = std::min(kMaxCap, std::max(256, next_pow2(2 * std::min<int64_t>(maxub, B.ncols) + 2)));
     DevBuf<int> cnt(n + 1, s), ovf(1, s);
     CK(cudaMemsetAsync(ovf.p, 0, sizeof(int), s));
-    CK(cudaFuncSetAttribute(k_spgemm_count<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            kMaxCap * 4));
-    k_spgemm_count<false><<<n, 256, cap_s * 4, s>>>(n, nullptr, A.ptr.p, A.col.p, B.ptr.p, B.col.p,
-                                                   cap_s, nullptr, nullptr, cnt.p, ovf.p);
+    // 1. warp-per-row symbolic pass; rows above kWCap/2-1 columns -> wide list
+    k_spgemm_wcount<<<ceil_div(n, kWPB), 256, 0, s>>>(n, A.ptr.p, A.col.p, B.ptr.p, B.col.p, cnt.p);
     CK_LAUNCH();
+    DevBuf<int> wide(n, s), nwide_d(1, s);
+    CK(cudaMemsetAsync(nwide_d.p, 0, sizeof(int), s));
+    {
+        int *cc = cnt.p, *wl = wide.p, *nw = nwide_d.p;
+        for_each(n, [=] __device__(int64_t i) {
+            if (cc[i] < 0) wl[atomicAdd(nw, 1)] = static_cast<int>(i);
+        }, s);
+    }
+    int nwide = 0;
+    CK(cudaMemcpyAsync(&nwide, nwide_d.p, sizeof nwide, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (nwide) {
+        // sort the wide list so the CTA passes visit rows in a fixed order
+        std::vector<int> hw(nwide);
+        CK(cudaMemcpyAsync(hw.data(), wide.p, sizeof(int) * nwide, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        std::sort(hw.begin(), hw.end());
+        CK(cudaMemcpyAsync(wide.p, hw.data(), sizeof(int) * nwide, cudaMemcpyHostToDevice, s));
+        CK(cudaFuncSetAttribute(k_spgemm_count<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kMaxCap * 4));
+        k_spgemm_count<false><<<nwide, 256, cap_s * 4, s>>>(nwide, wide.p, A.ptr.p, A.col.p, B.ptr.p,
+                                                           B.col.p, cap_s, nullptr, nullptr, cnt.p,
+                                                           ovf.p);
+        CK_LAUNCH();
+    }
     int novf = 0;
     CK(cudaMemcpyAsync(&novf, ovf.p, sizeof novf, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -1009,13 +1170,24 @@ void spgemm(const Bsr3 &A, const Bsr3 &B, Bsr3 &C, cudaStream_t s) {
     CK(cudaStreamSynchronize(s));
     const int cap_n = std::min(kMaxCap, std::max(256, next_pow2(2 * static_cast<int64_t>(maxc) + 2)));
     const size_t smem_n = static_cast<size_t>(cap_n) * 4 * 2 + static_cast<size_t>(cap_n / 2) * 4;
-    CK(cudaFuncSetAttribute(k_spgemm_numeric<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            kMaxCap * 10));
-    k_spgemm_numeric<false><<<n, 256, smem_n, s>>>(n, nullptr, A.ptr.p, A.col.p, A.val.p,
-                                                  B.ptr.p, B.col.p, B.val.p, cap_n, nullptr,
-                                                  nullptr, nullptr, nullptr, C.ptr.p, C.col.p,
-                                                  C.val.p);
+    // 2. warp-per-row numeric pass for the narrow rows
+    const size_t smem_w = static_cast<size_t>(kWPB) * kWCap * 5 / 2 * sizeof(int);
+    CK(cudaFuncSetAttribute(k_spgemm_wnumeric, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(smem_w)));
+    k_spgemm_wnumeric<<<ceil_div(n, kWPB), 256, smem_w, s>>>(n, A.ptr.p, A.col.p, A.val.p, B.ptr.p,
+                                                             B.col.p, B.val.p, C.ptr.p, C.col.p,
+                                                             C.val.p);
     CK_LAUNCH();
+    // 3. CTA-per-row numeric pass for the wide rows
+    if (nwide) {
+        CK(cudaFuncSetAttribute(k_spgemm_numeric<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kMaxCap * 10));
+        k_spgemm_numeric<false><<<nwide, 256, smem_n, s>>>(nwide, wide.p, A.ptr.p, A.col.p, A.val.p,
+                                                          B.ptr.p, B.col.p, B.val.p, cap_n, nullptr,
+                                                          nullptr, nullptr, nullptr, C.ptr.p, C.col.p,
+                                                          C.val.p);
+        CK_LAUNCH();
+    }
     if (novf) {
         const int nr = static_cast<int>(orows.n);
         k_spgemm_numeric<true><<<nr, 256, 0, s>>>(nr, orows.p, A.ptr.p, A.col.p, A.val.p, B.ptr.p,
