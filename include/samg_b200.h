@@ -194,6 +194,45 @@ SAMG_API int samg_bsr3_galerkin(const samg_bsr3 *R, const samg_bsr3 *A,
 SAMG_API int samg_bsr3_spmv_bytes(const samg_bsr3 *m, int beta_nonzero,
         uint64_t *bytes);
 
+/* ---- row-partitioned operator for multi-GPU runs ---
+ * One process per GPU; rank r owns block rows [row_starts[r], row_starts[r+1])
+ * of a global BSR3 matrix.  The halo plan is built on the host (no GPU
+ * needed); the caller's transport (NCCL / gloo) moves the data:
+ *   1. samg_dist_create with the rank's rows (global column ids);
+ *   2. send every recv peer the global ids of its ghost segment
+ *      (samg_dist_recv_plan + samg_dist_ghosts), receive the peers' lists
+ *      and hand them to samg_dist_set_send;
+ *   3. per SpMV: samg_dist_pack(x) -> send buffers to the send peers,
+ *      receive into x_ext[3*nloc + 3*offset ...], samg_dist_spmv(interior)
+ *      may run while the halo is in flight, then samg_dist_spmv(boundary).
+ * y equals the single-GPU spmv bit-for-bit (same per-row block order). */
+typedef struct samg_dist samg_dist;
+SAMG_API int samg_dist_create(int64_t row0, int64_t row1, const int64_t *ptr,
+        const int64_t *col, const double *val, int nranks,
+        const int64_t *row_starts, int rank, samg_dist **out);
+SAMG_API int samg_dist_destroy(samg_dist *d);
+SAMG_API int samg_dist_info(const samg_dist *d, int64_t *nloc, int64_t *nghost,
+        int64_t *ninterior, int64_t *nboundary, int *nrecv_peers,
+        int *nsend_peers);
+SAMG_API int samg_dist_recv_plan(const samg_dist *d, int *peers,
+        int64_t *counts, int64_t *offsets);
+SAMG_API int samg_dist_ghosts(const samg_dist *d, int64_t *global_ids);
+SAMG_API int samg_dist_set_send(samg_dist *d, int npeers, const int *peers,
+        const int64_t *counts, const int64_t *global_ids);
+SAMG_API int samg_dist_send_plan(const samg_dist *d, int *peers,
+        int64_t *counts, int64_t *offsets, int64_t *local_rows);
+/* the renumbered local matrix (columns: owned [0,nloc), ghosts nloc+g) */
+SAMG_API int samg_dist_local_matrix(const samg_dist *d, int64_t *ptr,
+        int64_t *col, double *val);
+/* upload to `device`; group = lanes per row (0 = auto, or 4/8/16/32 to match
+ * the single-GPU kernel exactly) */
+SAMG_API int samg_dist_to_device(samg_dist *d, int device, int group);
+SAMG_API int samg_dist_pack(const samg_dist *d, const double *d_x,
+        double *d_sendbuf, void *stream);
+/* part: 0 = interior rows, 1 = boundary rows, 2 = all rows */
+SAMG_API int samg_dist_spmv(const samg_dist *d, int part, double alpha,
+        const double *d_xext, double beta, double *d_y, void *stream);
+
 /* ---- synthetic problems (input tooling; elasticity.hpp:38-213 extended) -- */
 enum samg_dirichlet { SAMG_DIRICHLET_NONE = 0, SAMG_DIRICHLET_KEEP_ROWS = 1,
                       SAMG_DIRICHLET_ELIMINATE = 2 };
@@ -209,6 +248,8 @@ typedef struct {
     double noise;             /* + U[-noise, noise] per DOF */
     uint64_t seed;
     int x_slowest;            /* node numbering: 0 = x fastest (reference) */
+    int64_t node_begin;       /* if node_end > node_begin: only the rows of */
+    int64_t node_end;         /* nodes [begin, end), global column ids     */
 } samg_problem_params;
 SAMG_API void samg_default_problem_params(samg_problem_params *p);
 SAMG_API int samg_generate_hex(const samg_problem_params *p, samg_problem **out);

@@ -72,7 +72,8 @@ class ProblemParamsC(C.Structure):
                 ("lx", C.c_double), ("ly", C.c_double), ("lz", C.c_double),
                 ("E", C.c_double), ("nu", C.c_double), ("heterogeneous", C.c_int),
                 ("dirichlet", C.c_int), ("load", C.c_int), ("noise", C.c_double),
-                ("seed", C.c_uint64), ("x_slowest", C.c_int)]
+                ("seed", C.c_uint64), ("x_slowest", C.c_int),
+                ("node_begin", C.c_int64), ("node_end", C.c_int64)]
 
 
 # (name, argtypes) of every exported function; restype int unless noted
@@ -121,6 +122,19 @@ PROTOTYPES = {
     "samg_problem_get_coords": ([vp, f64p], C.c_int),
     "samg_rigid_body_modes": ([i64, f64p, f64p], C.c_int),
     "samg_problem_bsr3_view": ([vp, C.POINTER(i64p), C.POINTER(i64p), C.POINTER(f64p)], C.c_int),
+    "samg_dist_create": ([i64, i64, i64p, i64p, f64p, C.c_int, i64p, C.c_int, C.POINTER(vp)],
+                         C.c_int),
+    "samg_dist_destroy": ([vp], C.c_int),
+    "samg_dist_info": ([vp, i64p, i64p, i64p, i64p, C.POINTER(C.c_int), C.POINTER(C.c_int)],
+                       C.c_int),
+    "samg_dist_recv_plan": ([vp, C.POINTER(C.c_int), i64p, i64p], C.c_int),
+    "samg_dist_ghosts": ([vp, i64p], C.c_int),
+    "samg_dist_set_send": ([vp, C.c_int, C.POINTER(C.c_int), i64p, i64p], C.c_int),
+    "samg_dist_send_plan": ([vp, C.POINTER(C.c_int), i64p, i64p, i64p], C.c_int),
+    "samg_dist_local_matrix": ([vp, i64p, i64p, f64p], C.c_int),
+    "samg_dist_to_device": ([vp, C.c_int, C.c_int], C.c_int),
+    "samg_dist_pack": ([vp, vp, vp, vp], C.c_int),
+    "samg_dist_spmv": ([vp, C.c_int, C.c_double, vp, C.c_double, vp, vp], C.c_int),
 }
 
 

@@ -296,13 +296,19 @@ class ProblemParams:
     noise: float = 0.0
     seed: int = 12345
     x_slowest: bool = False
+    node_begin: int = 0            # node_end > node_begin: rows of that node
+    node_end: int = 0              # range only (global column ids)
 
     def c(self) -> ProblemParamsC:
         d = {"none": 0, "keep_rows": 1, "eliminate": 2}[self.dirichlet]
         ld = {"body_force": 0, "traction_xend": 1, "random": 2}[self.load]
         return ProblemParamsC(self.nx, self.ny, self.nz, self.lx, self.ly, self.lz, self.E,
                               self.nu, int(self.heterogeneous), d, ld, self.noise, self.seed,
-                              int(self.x_slowest))
+                              int(self.x_slowest), self.node_begin, self.node_end)
+
+    def total_nodes(self) -> int:
+        kx = self.nx + (0 if self.dirichlet == "eliminate" else 1)
+        return kx * (self.ny + 1) * (self.nz + 1)
 
 
 @dataclass

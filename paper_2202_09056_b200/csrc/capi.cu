@@ -13,6 +13,7 @@
 
 #include "hierarchy.cuh"
 #include "problem.cuh"
+#include "dist.cuh"
 
 struct samg_bsr3 {
     samgb::Bsr3 own;
@@ -30,6 +31,7 @@ namespace samgb {
 samg_problem *generate_hex(const samg_problem_params &p);
 void rigid_body_modes(int64_t nnodes, const double *xyz, double *B);
 }
+
 
 namespace {
 
@@ -510,6 +512,8 @@ SAMG_API int samg_bsr3_spmv_device(const samg_bsr3 *m, double alpha, const doubl
                                    double beta, double *d_y, void *stream) {
     return guarded([&] {
         require(m && m->m, SAMG_INVALID_ARGUMENT, "NULL matrix");
+        require(reinterpret_cast<uintptr_t>(d_x) % 16 == 0, SAMG_INVALID_ARGUMENT,
+                "spmv: x must be 16-byte aligned (the kernel gathers x with 16-byte loads)");
         launch_spmv(*m->m, alpha, d_x, beta, d_y, static_cast<cudaStream_t>(stream));
     });
 }
@@ -651,6 +655,111 @@ SAMG_API int samg_rigid_body_modes(int64_t nnodes, const double *xyz, double *B)
     return guarded([&] {
         require(xyz && B && nnodes >= 0, SAMG_INVALID_ARGUMENT, "rigid_body_modes: bad arguments");
         rigid_body_modes(nnodes, xyz, B);
+    });
+}
+
+SAMG_API int samg_dist_create(int64_t row0, int64_t row1, const int64_t *ptr, const int64_t *col,
+                              const double *val, int nranks, const int64_t *row_starts, int rank,
+                              samg_dist **out) {
+    return guarded([&] {
+        require(out && ptr && row_starts && row1 >= row0, SAMG_INVALID_ARGUMENT, "dist_create: bad arguments");
+        require(ptr[row1 - row0] == ptr[0] || (col && val), SAMG_INVALID_ARGUMENT, "dist_create: NULL arrays");
+        *out = dist_create(row0, row1, ptr, col, val, nranks, row_starts, rank);
+    });
+}
+
+SAMG_API int samg_dist_destroy(samg_dist *d) {
+    return guarded([&] {
+        if (d && d->device >= 0) { cudaSetDevice(d->device); cudaDeviceSynchronize(); }
+        delete d;
+    });
+}
+
+SAMG_API int samg_dist_info(const samg_dist *d, int64_t *nloc, int64_t *nghost, int64_t *ninterior,
+                            int64_t *nboundary, int *nrecv, int *nsend) {
+    return guarded([&] {
+        require(d != nullptr, SAMG_INVALID_ARGUMENT, "NULL dist");
+        *nloc = d->nloc;
+        *nghost = d->nghost;
+        *ninterior = static_cast<int64_t>(d->interior.size());
+        *nboundary = static_cast<int64_t>(d->boundary.size());
+        *nrecv = static_cast<int>(d->recv_peers.size());
+        *nsend = static_cast<int>(d->send_peers.size());
+    });
+}
+
+SAMG_API int samg_dist_recv_plan(const samg_dist *d, int *peers, int64_t *counts, int64_t *offsets) {
+    return guarded([&] {
+        require(d != nullptr, SAMG_INVALID_ARGUMENT, "NULL dist");
+        for (size_t p = 0; p < d->recv_peers.size(); ++p) {
+            peers[p] = d->recv_peers[p];
+            counts[p] = d->recv_counts[p];
+            offsets[p] = d->recv_offsets[p];
+        }
+    });
+}
+
+SAMG_API int samg_dist_ghosts(const samg_dist *d, int64_t *ids) {
+    return guarded([&] {
+        require(d != nullptr, SAMG_INVALID_ARGUMENT, "NULL dist");
+        std::copy(d->ghost.begin(), d->ghost.end(), ids);
+    });
+}
+
+SAMG_API int samg_dist_set_send(samg_dist *d, int npeers, const int *peers, const int64_t *counts,
+                                const int64_t *ids) {
+    return guarded([&] {
+        require(d != nullptr && npeers >= 0, SAMG_INVALID_ARGUMENT, "dist_set_send: bad arguments");
+        dist_set_send(d, npeers, peers, counts, ids);
+    });
+}
+
+SAMG_API int samg_dist_send_plan(const samg_dist *d, int *peers, int64_t *counts, int64_t *offsets,
+                                 int64_t *local_rows) {
+    return guarded([&] {
+        require(d != nullptr && d->send_set, SAMG_INVALID_ARGUMENT, "dist: send plan not set");
+        for (size_t p = 0; p < d->send_peers.size(); ++p) {
+            peers[p] = d->send_peers[p];
+            counts[p] = d->send_counts[p];
+            offsets[p] = d->send_offsets[p];
+        }
+        if (local_rows) std::copy(d->send_idx.begin(), d->send_idx.end(), local_rows);
+    });
+}
+
+SAMG_API int samg_dist_local_matrix(const samg_dist *d, int64_t *ptr, int64_t *col, double *val) {
+    return guarded([&] {
+        require(d != nullptr, SAMG_INVALID_ARGUMENT, "NULL dist");
+        std::copy(d->ptr.begin(), d->ptr.end(), ptr);  // ptr[nloc] = nnzb
+        if (col) std::copy(d->col.begin(), d->col.end(), col);
+        if (val) std::copy(d->val.begin(), d->val.end(), val);
+    });
+}
+
+SAMG_API int samg_dist_to_device(samg_dist *d, int device, int group) {
+    return guarded([&] {
+        require(d != nullptr, SAMG_INVALID_ARGUMENT, "NULL dist");
+        require(d->send_set || d->nranks == 1, SAMG_INVALID_ARGUMENT, "dist: set the send plan first");
+        need_device(device);
+        dist_to_device(d, device, group);
+    });
+}
+
+SAMG_API int samg_dist_pack(const samg_dist *d, const double *x, double *buf, void *stream) {
+    return guarded([&] {
+        require(d && d->device >= 0, SAMG_INVALID_ARGUMENT, "dist: not on a device");
+        dist_pack(d, x, buf, static_cast<cudaStream_t>(stream));
+    });
+}
+
+SAMG_API int samg_dist_spmv(const samg_dist *d, int part, double alpha, const double *xext,
+                            double beta, double *y, void *stream) {
+    return guarded([&] {
+        require(d && d->device >= 0, SAMG_INVALID_ARGUMENT, "dist: not on a device");
+        require(part >= 0 && part <= 2, SAMG_INVALID_ARGUMENT, "dist: part must be 0, 1 or 2");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        if (part == 0 || part == 2) dist_spmv(d, 0, alpha, xext, beta, y, s);
+        if (part == 1 || part == 2) dist_spmv(d, 1, alpha, xext, beta, y, s);
     });
 }
 

@@ -120,7 +120,14 @@ samg_problem *generate_hex(const samg_problem_params &p) {
         return p.x_slowest ? k + mz * (j + my * ii) : ii + kx * (j + my * k);
     };
     auto constrained = [&](int64_t i) { return keep && i == 0; };
-    const int64_t nnodes = kx * my * mz;
+    const int64_t nnodes_all = kx * my * mz;
+    // optional row range [node_begin, node_end): one rank's slab of a
+    // row-partitioned problem (global column ids)
+    const bool ranged = p.node_end > p.node_begin;
+    const int64_t nb = ranged ? p.node_begin : 0, ne = ranged ? p.node_end : nnodes_all;
+    if (nb < 0 || ne > nnodes_all)
+        fail(SAMG_INVALID_ARGUMENT, "generate_hex: node range outside the grid");
+    const int64_t nnodes = ne - nb;
 
     auto *pb = new samg_problem;
     pb->nnodes = nnodes;
@@ -170,18 +177,18 @@ samg_problem *generate_hex(const samg_problem_params &p) {
     };
 
     std::vector<int64_t> cnt(nnodes + 1, 0);
-    parallel_for(nnodes, [&](int64_t n) {
+    parallel_for(nnodes, [&](int64_t L) {
         int64_t i, j, k;
-        ijk_of(n, i, j, k);
-        if (constrained(i)) { cnt[n + 1] = 1; return; }
+        ijk_of(nb + L, i, j, k);
+        if (constrained(i)) { cnt[L + 1] = 1; return; }
         int64_t c = 0;
         for_nbrs(i, j, k, [&](int di, int dj, int dk) {
             const int64_t a = i + di, b = j + dj, d = k + dk;
             if (inside(a, b, d) && !constrained(a)) ++c;
         });
-        cnt[n + 1] = c;
+        cnt[L + 1] = c;
     });
-    for (int64_t n = 0; n < nnodes; ++n) cnt[n + 1] += cnt[n];
+    for (int64_t L = 0; L < nnodes; ++L) cnt[L + 1] += cnt[L];
     const int64_t nnzb = cnt[nnodes];
     pb->ptr = cnt;
     pb->col.resize(nnzb);
@@ -189,13 +196,14 @@ samg_problem *generate_hex(const samg_problem_params &p) {
     pb->rhs.assign(3 * nnodes, 0.0);
     pb->xyz.resize(3 * nnodes);
 
-    parallel_for(nnodes, [&](int64_t n) {
+    parallel_for(nnodes, [&](int64_t L) {
+        const int64_t n = nb + L;
         int64_t i, j, k;
         ijk_of(n, i, j, k);
-        pb->xyz[3 * n] = i * hx;
-        pb->xyz[3 * n + 1] = j * hy;
-        pb->xyz[3 * n + 2] = k * hz;
-        int64_t o = pb->ptr[n];
+        pb->xyz[3 * L] = i * hx;
+        pb->xyz[3 * L + 1] = j * hy;
+        pb->xyz[3 * L + 2] = k * hz;
+        int64_t o = pb->ptr[L];
         if (constrained(i)) {
             pb->col[o] = n;
             double *blk = &pb->val[9 * o];
@@ -227,7 +235,7 @@ samg_problem *generate_hex(const samg_problem_params &p) {
             ++o;
         });
         // loads
-        double *f = &pb->rhs[3 * n];
+        double *f = &pb->rhs[3 * L];
         if (p.load == SAMG_LOAD_BODY_FORCE) {
             const double nodal_force = -hx * hy * hz / 8.0;  // elasticity.hpp:189
             for (int64_t ez = k - 1; ez <= k; ++ez)

@@ -141,7 +141,8 @@ Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int6
     const int64_t n0 = H->finest_dim();
     H->r.alloc(n0, s); H->z.alloc(n0, s); H->p.alloc(n0, s); H->q.alloc(n0, s);
     H->fbuf.alloc(n0, s); H->ubuf.alloc(n0, s);
-    const int64_t np = std::max<int64_t>(kRedBlocks, (H->levels.front().A.nrows * 32 + 255) / 256 + 1);
+    // one partial per CTA of any fused reduction (<= 148*8 CTAs)
+    const int64_t np = 4096;
     H->partials.alloc(np, s);
     H->sc.alloc(1, s);
     CK(cudaMemsetAsync(H->sc.p, 0, sizeof(CgScalars), s));
@@ -156,13 +157,16 @@ Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int6
 // V-cycle (hierarchy.hpp:408-441).  With zero_guess the pre-smoother's first
 // sweep needs no SpMV (r = f - A*0 = f exactly), as inside CG (cg.hpp:98-101)
 // and on every level > 0 (hierarchy.hpp:426).
-void Hierarchy::vcycle(const double *f0, double *u0, bool zero_guess) {
+// With fuse_rz (inside CG) the last level-0 sweep also forms r.z and
+// finishes the CG beta update; returns whether it did.
+bool Hierarchy::vcycle(const double *f0, double *u0, bool zero_guess, bool fuse_rz) {
     cudaStream_t s = stream;
     const size_t L = levels.size();
     if (L == 1) {
         launch_dense_gemv(nc, Ainv.p, f0, u0, s);
-        return;
+        return false;
     }
+    bool fused = false;
     std::vector<double *> cur(L);
     for (size_t i = 0; i + 1 < L; ++i) {
         Level &lv = levels[i];
@@ -196,8 +200,14 @@ void Hierarchy::vcycle(const double *f0, double *u0, bool zero_guess) {
         double *b = (a == lv.u.p) ? lv.t.p : lv.u.p;
         launch_spmv(lv.P, 1.0, cur[ii + 1], 1.0, a, s);
         for (int sw = prm.post_sweeps; sw > 0; --sw) {
-            double *out = (ii == 0 && sw == 1) ? u0 : b;
-            launch_smooth(lv.A, lv.M, fi, a, out, s);
+            const bool last0 = ii == 0 && sw == 1;
+            double *out = last0 ? u0 : b;
+            if (last0 && fuse_rz) {
+                launch_smooth_dot(lv.A, lv.M, fi, a, out, partials.p, sc.p, s);
+                fused = true;
+            } else {
+                launch_smooth(lv.A, lv.M, fi, a, out, s);
+            }
             b = a;
             a = out;
         }
@@ -205,6 +215,7 @@ void Hierarchy::vcycle(const double *f0, double *u0, bool zero_guess) {
     }
     if (cur[0] != u0)
         CK(cudaMemcpyAsync(u0, cur[0], sizeof(double) * finest_dim(), cudaMemcpyDeviceToDevice, s));
+    return fused;
 }
 
 // One CG iteration (cg.hpp:63-77) on the internal buffers, as recorded into
@@ -229,14 +240,9 @@ void Hierarchy::build_cg_graph() {
     CK(cudaGraphAddNode(&wnode, g, nullptr, 0, &np));
     cudaGraph_t body = np.conditional.phGraph_out[0];
     CK(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-    int nparts = 0;
-    launch_spmv_dot(A0, p.p, q.p, partials.p, &nparts, s);
-    launch_finalize(1, partials.p, nparts, sc.p, s);
-    launch_cg_update(n, sc.p, p.p, q.p, ubuf.p, r.p, partials.p, s);
-    launch_finalize_loop(partials.p, kRedBlocks, sc.p, h, s);
-    vcycle(r.p, z.p, true);
-    launch_dot_partials(n, r.p, z.p, partials.p, s);
-    launch_finalize(2, partials.p, kRedBlocks, sc.p, s);
+    launch_spmv_dot(A0, p.p, q.p, partials.p, sc.p, s);
+    launch_cg_update(n, sc.p, p.p, q.p, ubuf.p, r.p, partials.p, CG_RR_LOOP, h, s);
+    if (!vcycle(r.p, z.p, true, true)) launch_dot(n, r.p, z.p, partials.p, sc.p, CG_RZ, s);
     launch_p_update(n, sc.p, z.p, p.p, s);
     cudaGraph_t captured = body;
     CK(cudaStreamEndCapture(s, &captured));
@@ -265,8 +271,7 @@ samg_solve_report Hierarchy::cg(const double *d_f, double *d_u, const samg_cg_pa
     CK(cudaMemcpyAsync(pr, d_f, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
     launch_fill(n, 0.0, pu, s);
     CK(cudaMemsetAsync(sc.p, 0, sizeof(CgScalars), s));
-    launch_dot_partials(n, d_f, d_f, partials.p, s);
-    launch_finalize(0, partials.p, kRedBlocks, sc.p, s);
+    launch_dot(n, pr, pr, partials.p, sc.p, CG_RR, s);  // r = f (internal, aligned)
     CK(cudaMemcpyAsync(sc_host, sc.p, sizeof(CgScalars), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     const double norm_f = std::sqrt(sc_host->rr);
@@ -280,9 +285,8 @@ samg_solve_report Hierarchy::cg(const double *d_f, double *d_u, const samg_cg_pa
         rep.solve_seconds = now_s() - t0;
         return rep;
     }
-    vcycle(pr, pz, true);
-    launch_dot_partials(n, pr, pz, partials.p, s);
-    launch_finalize(3, partials.p, kRedBlocks, sc.p, s);
+    vcycle(pr, pz, true, false);
+    launch_dot(n, pr, pz, partials.p, sc.p, CG_RHO, s);
     CK(cudaMemcpyAsync(pp, pz, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
     double res_norm = norm_f;
     int iter = 0;
@@ -292,6 +296,7 @@ samg_solve_report Hierarchy::cg(const double *d_f, double *d_u, const samg_cg_pa
         sc_stage->breakdown = 0;
         sc_stage->iter = 0;
         sc_stage->max_iter = cp.max_iterations;
+        sc_stage->ticket = 0;
         const size_t off = offsetof(CgScalars, norm_f);
         CK(cudaMemcpyAsync(reinterpret_cast<char *>(sc.p) + off,
                            reinterpret_cast<char *>(sc_stage) + off, sizeof(CgScalars) - off,
@@ -306,11 +311,8 @@ samg_solve_report Hierarchy::cg(const double *d_f, double *d_u, const samg_cg_pa
         res_norm = std::sqrt(sc_host->rr);
     }
     while (!use_graph && res_norm / norm_f > cp.tol && iter < cp.max_iterations) {
-        int nparts = 0;
-        launch_spmv_dot(A0, pp, pq, partials.p, &nparts, s);
-        launch_finalize(1, partials.p, nparts, sc.p, s);
-        launch_cg_update(n, sc.p, pp, pq, pu, pr, partials.p, s);
-        launch_finalize(0, partials.p, kRedBlocks, sc.p, s);
+        launch_spmv_dot(A0, pp, pq, partials.p, sc.p, s);
+        launch_cg_update(n, sc.p, pp, pq, pu, pr, partials.p, CG_RR, 0, s);
         CK(cudaMemcpyAsync(sc_host, sc.p, sizeof(CgScalars), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         if (sc_host->breakdown)
@@ -318,17 +320,14 @@ samg_solve_report Hierarchy::cg(const double *d_f, double *d_u, const samg_cg_pa
         ++iter;
         res_norm = std::sqrt(sc_host->rr);
         if (res_norm / norm_f <= cp.tol) break;
-        vcycle(pr, pz, true);
-        launch_dot_partials(n, pr, pz, partials.p, s);
-        launch_finalize(2, partials.p, kRedBlocks, sc.p, s);
+        if (!vcycle(pr, pz, true, true)) launch_dot(n, pr, pz, partials.p, sc.p, CG_RZ, s);
         launch_p_update(n, sc.p, pz, pp, s);
     }
     rep.iterations = iter;
     rep.converged = res_norm / norm_f <= cp.tol;
     // true residual at exit (cg.hpp:105-108)
     launch_residual(A0, d_f, pu, pq, s);
-    launch_dot_partials(n, pq, pq, partials.p, s);
-    launch_finalize(0, partials.p, kRedBlocks, sc.p, s);
+    launch_dot(n, pq, pq, partials.p, sc.p, CG_RR, s);
     CK(cudaMemcpyAsync(sc_host, sc.p, sizeof(CgScalars), cudaMemcpyDeviceToHost, s));
     if (pu != d_u)
         CK(cudaMemcpyAsync(d_u, pu, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));

@@ -39,7 +39,7 @@ struct Hierarchy {
     int64_t finest_dim() const { return 3 * levels.front().A.nrows; }
     uint64_t memory_footprint() const;
 
-    void vcycle(const double *f, double *u, bool zero_guess);
+    bool vcycle(const double *f, double *u, bool zero_guess, bool fuse_rz = false);
     samg_solve_report cg(const double *d_f, double *d_u, const samg_cg_params &prm);
 };
 

@@ -47,9 +47,6 @@ void launch_smooth(const Bsr3 &A, const Smoother &M, const double *f, const doub
 // u = M f  (one sweep from a zero guess: the residual is f exactly)
 void launch_smooth_zero(int64_t nrows, const Smoother &M, const double *f, double *u,
                         cudaStream_t s);
-// q = A p and per-block partial sums of p.q (fused CG matvec, cg.hpp:63-64)
-void launch_spmv_dot(const Bsr3 &A, const double *p, double *q, double *partials,
-                     int *nparts, cudaStream_t s);
 // leading dimension of the dense coarse inverse (even, for 16-byte loads)
 inline int64_t dense_ld(int64_t n) { return (n + 1) & ~static_cast<int64_t>(1); }
 // dense coarse solve u = Ainv f (replaces dense_lu::solve, hierarchy.hpp:113-129)
@@ -59,25 +56,29 @@ void launch_dense_gemv(int64_t n, const double *Ainv, const double *f, double *u
 // CG device scalars (cg.hpp:39-83).
 struct CgScalars {
     double pq, rho, rho_new, rr, alpha, beta, norm_f, tol;
-    int breakdown, iter, max_iter, pad;
+    int breakdown, iter, max_iter;
+    unsigned ticket;  // last-CTA counter of the fused reductions
 };
-// device-side loop control of the graph-resident CG (cg.hpp:62-72):
-// finalize r.r, ++iter, continue iff ||r||/||f|| > tol && iter < max && !breakdown
-void launch_finalize_loop(const double *partials, int nparts, CgScalars *sc,
-                          cudaGraphConditionalHandle h, cudaStream_t s);
-// resets iter/breakdown and sets the loop condition before the first pass
-// (norm_f, tol, max_iter already in sc)
-void launch_cg_loop_init(CgScalars *sc, cudaGraphConditionalHandle h, cudaStream_t s);
+// What a fused reduction finishes (cg.hpp:58-77).  Every reduction writes
+// one partial per CTA; the last CTA sums them in index order (deterministic)
+// and applies: RR: rr; PQ: pq, alpha = rho/pq, breakdown if pq <= 0;
+// RZ: beta = rz/rho, rho = rz; RHO: rho; RR_LOOP: rr, ++iter and the graph
+// loop condition ||r||/||f|| > tol && iter < max && !breakdown.
+enum { CG_RR = 0, CG_PQ = 1, CG_RZ = 2, CG_RHO = 3, CG_RR_LOOP = 4 };
 constexpr int kRedBlocks = 592;   // 4 x 148 SMs: fixed => deterministic sums
-void launch_dot_partials(int64_t n, const double *x, const double *y, double *partials,
-                         cudaStream_t s);
-// finalize: 0 = rr, 1 = pq (+alpha, breakdown), 2 = rho_new (+beta, rho),
-// 3 = rho (initial), from `nparts` partial sums
-void launch_finalize(int what, const double *partials, int nparts, CgScalars *sc,
-                     cudaStream_t s);
-// u += alpha p; r -= alpha q; partials of r.r
-void launch_cg_update(int64_t n, const CgScalars *sc, const double *p, const double *q,
-                      double *u, double *r, double *partials, cudaStream_t s);
+// q = A p fused with p.q (cg.hpp:63-64) -> PQ
+void launch_spmv_dot(const Bsr3 &A, const double *p, double *q, double *partials,
+                     CgScalars *sc, cudaStream_t s);
+// last post-smoothing sweep of the V-cycle fused with r.z (cg.hpp:73-75) -> RZ
+void launch_smooth_dot(const Bsr3 &A, const Smoother &M, const double *f, const double *u,
+                       double *u_out, double *partials, CgScalars *sc, cudaStream_t s);
+// x.y -> what
+void launch_dot(int64_t n, const double *x, const double *y, double *partials, CgScalars *sc,
+                int what, cudaStream_t s);
+// u += alpha p; r -= alpha q fused with r.r -> RR or RR_LOOP
+void launch_cg_update(int64_t n, CgScalars *sc, const double *p, const double *q, double *u,
+                      double *r, double *partials, int what, cudaGraphConditionalHandle h,
+                      cudaStream_t s);
 // p = z + beta p
 void launch_p_update(int64_t n, const CgScalars *sc, const double *z, double *p,
                      cudaStream_t s);

@@ -1,22 +1,26 @@
 // solve.cu -- solve-phase kernels: 3x3-BSR SpMV family (spmv, residual,
 // fused smoother sweep, fused CG matvec+dot), coarse dense GEMV and the CG
-// vector kernels with deterministic reductions.
+// vector kernels with deterministic, launch-free reductions.
 //
 // All of these are HBM-bandwidth bound (18 flop per 76 B of matrix; DESIGN.md
-// section 3).  A group of G lanes (G in {4,8,16,32}, chosen per matrix from
-// its blocks per row) owns one block row.  Default (variant 1): lane l
-// accumulates whole 3x3 blocks beg+l, beg+l+G, ... with 16-byte loads, so
-// the row's 72-byte blocks stream as contiguous, coalesced bytes; col[] is
-// read once per block and x[3c..3c+2] is a gather that hits L1/L2
-// (structured meshes keep the column window small).  Variant 0 (row units:
-// lane l handles scalar row l%3 of every block) is kept for comparison
-// (SAMG_SPMV_VARIANT=0).  The three row sums are combined with a width-G
-// butterfly and the epilogue (spmv / residual / smoother sweep / CG dot) is
-// fused on lanes 0..2.
-#include "kernels.cuh"
+// section 5).  A group of G lanes owns one block row; G in {1,...,128} is
+// chosen per matrix (choose_group): ~7 blocks per lane, widened until the
+// matrix fills 148 SMs (coarse levels, restriction).  Default kernel
+// (variant 1): lane l accumulates whole 3x3 blocks beg+l, beg+l+G, ... with
+// 16-byte loads, so the row's 72-byte blocks stream as contiguous, coalesced
+// bytes; col[] is read once per block and x[3c..3c+2] is a gather that hits
+// L1/L2 (structured meshes keep the column window small).  Variant 0 (row
+// units: lane l handles scalar row l%3 of every block, G in {8,16,32}) is kept
+// for comparison (SAMG_SPMV_VARIANT=0).  The three row sums are combined with
+// a width-G butterfly (plus shared memory for G > 32) and the epilogue
+// (spmv / residual / smoother sweep / CG dot) is fused.
+#include <cuda/atomic>
 
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
+
+#include "kernels.cuh"
 
 namespace samgb {
 
@@ -24,49 +28,61 @@ namespace {
 
 __device__ __forceinline__ double ld_stream(const double *p) { return __ldcs(p); }
 
+__device__ __forceinline__ double2 ldg2(const double *p) {
+    return __ldg(reinterpret_cast<const double2 *>(p));
+}
+
+// Sum three values over the G lanes of a group; every lane gets the totals.
+// G > 32 spans G/32 warps of the 256-thread CTA (shared memory, CTA barrier:
+// every thread of the CTA must call it).
 template <int G>
 __device__ __forceinline__ void group_reduce3(double &v0, double &v1, double &v2) {
+    constexpr int W = G < 32 ? G : 32;
 #pragma unroll
-    for (int off = G / 2; off >= 1; off >>= 1) {
-        v0 += __shfl_xor_sync(0xffffffffu, v0, off, G);
-        v1 += __shfl_xor_sync(0xffffffffu, v1, off, G);
-        v2 += __shfl_xor_sync(0xffffffffu, v2, off, G);
+    for (int off = W / 2; off >= 1; off >>= 1) {
+        v0 += __shfl_xor_sync(0xffffffffu, v0, off, W);
+        v1 += __shfl_xor_sync(0xffffffffu, v1, off, W);
+        v2 += __shfl_xor_sync(0xffffffffu, v2, off, W);
+    }
+    if constexpr (G > 32) {
+        __shared__ double red[3][8];
+        const int w = threadIdx.x / 32;
+        if (threadIdx.x % 32 == 0) { red[0][w] = v0; red[1][w] = v1; red[2][w] = v2; }
+        __syncthreads();
+        const int g0 = (threadIdx.x / G) * (G / 32);
+        v0 = v1 = v2 = 0.0;
+#pragma unroll
+        for (int k = 0; k < G / 32; ++k) { v0 += red[0][g0 + k]; v1 += red[1][g0 + k]; v2 += red[2][g0 + k]; }
+        __syncthreads();
     }
 }
 
-// Row-unit accumulation shared by every BSR3 kernel.  Returns the three row
-// sums (A x)_row in every lane of the group.
+// Variant 0: row units (G in {8,16,32}, U = G - G%3 active lanes).
 template <int G>
-__device__ __forceinline__ void bsr3_row_sums(int row, int nrows, int lane,
+__device__ __forceinline__ void row_sums_units(int row, bool valid, int lane,
         const int *__restrict__ ptr, const int *__restrict__ col,
         const double *__restrict__ val, const double *__restrict__ x,
         double &s0, double &s1, double &s2) {
     constexpr int U = G - G % 3;
     double s = 0.0, t2 = 0.0;
-    if (row < nrows && lane < U) {
+    if (valid && lane < U) {
         const int beg = __ldg(ptr + row), end = __ldg(ptr + row + 1);
         const int nu = 3 * (end - beg);
         const double *v = val + 9 * static_cast<size_t>(beg);
         const int *cc = col + beg;
         int t = lane;
         for (; t + U < nu; t += 2 * U) {
-            const int b0 = t / 3, b1 = (t + U) / 3;
-            const int c0 = __ldg(cc + b0), c1 = __ldg(cc + b1);
-            const double a0 = ld_stream(v + 3 * t), a1 = ld_stream(v + 3 * t + 1),
-                         a2 = ld_stream(v + 3 * t + 2);
-            const double d0 = ld_stream(v + 3 * (t + U)), d1 = ld_stream(v + 3 * (t + U) + 1),
-                         d2 = ld_stream(v + 3 * (t + U) + 2);
+            const int c0 = __ldg(cc + t / 3), c1 = __ldg(cc + (t + U) / 3);
             const double *x0 = x + 3 * c0, *x1 = x + 3 * c1;
-            s = fma(a0, __ldg(x0), s);
-            s = fma(a1, __ldg(x0 + 1), s);
-            s = fma(a2, __ldg(x0 + 2), s);
-            t2 = fma(d0, __ldg(x1), t2);
-            t2 = fma(d1, __ldg(x1 + 1), t2);
-            t2 = fma(d2, __ldg(x1 + 2), t2);
+            s = fma(ld_stream(v + 3 * t), __ldg(x0), s);
+            s = fma(ld_stream(v + 3 * t + 1), __ldg(x0 + 1), s);
+            s = fma(ld_stream(v + 3 * t + 2), __ldg(x0 + 2), s);
+            t2 = fma(ld_stream(v + 3 * (t + U)), __ldg(x1), t2);
+            t2 = fma(ld_stream(v + 3 * (t + U) + 1), __ldg(x1 + 1), t2);
+            t2 = fma(ld_stream(v + 3 * (t + U) + 2), __ldg(x1 + 2), t2);
         }
         if (t < nu) {
-            const int c0 = __ldg(cc + t / 3);
-            const double *x0 = x + 3 * c0;
+            const double *x0 = x + 3 * __ldg(cc + t / 3);
             s = fma(ld_stream(v + 3 * t), __ldg(x0), s);
             s = fma(ld_stream(v + 3 * t + 1), __ldg(x0 + 1), s);
             s = fma(ld_stream(v + 3 * t + 2), __ldg(x0 + 2), s);
@@ -80,23 +96,18 @@ __device__ __forceinline__ void bsr3_row_sums(int row, int nrows, int lane,
     group_reduce3<G>(s0, s1, s2);
 }
 
-// Block-per-lane accumulation: lane l of the group handles whole blocks
-// j = beg+l, beg+l+G, ...  A block (72 B) is read with four 16-byte loads
+// Variant 1: block per lane.  A block (72 B) is read with four 16-byte loads
 // plus one 8-byte load whose offsets depend only on the parity of j (block j
 // starts 16-byte aligned iff j is even), so every lane runs the same
 // instruction sequence; x[3c..3c+2] likewise with one 16-byte + one 8-byte
-// load.  Per block: 1 col + 5 value + 2 x loads (vs 21 scalar loads).
-__device__ __forceinline__ double2 ldg2(const double *p) {
-    return __ldg(reinterpret_cast<const double2 *>(p));
-}
-
+// load.  Per block: 1 col + 5 value + 2 x loads.
 template <int G>
-__device__ __forceinline__ void bsr3_row_sums_blk(int row, int nrows, int lane,
+__device__ __forceinline__ void row_sums_blocks(int row, bool valid, int lane,
         const int *__restrict__ ptr, const int *__restrict__ col,
         const double *__restrict__ val, const double *__restrict__ x,
         double &s0, double &s1, double &s2) {
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    if (row < nrows) {
+    if (valid) {
         const int beg = __ldg(ptr + row), end = __ldg(ptr + row + 1);
 #pragma unroll 2
         for (int j = beg + lane; j < end; j += G) {
@@ -123,76 +134,118 @@ __device__ __forceinline__ void bsr3_row_sums_blk(int row, int nrows, int lane,
     group_reduce3<G>(s0, s1, s2);
 }
 
-int spmv_variant() {
-    static const int v = [] {
-        const char *e = std::getenv("SAMG_SPMV_VARIANT");
-        return e ? std::atoi(e) : 1;
-    }();
-    return v;
-}
-
 template <int G, int V>
-__device__ __forceinline__ void row_sums(int row, int nrows, int lane, const int *__restrict__ ptr,
+__device__ __forceinline__ void row_sums(int row, bool valid, int lane, const int *__restrict__ ptr,
         const int *__restrict__ col, const double *__restrict__ val,
         const double *__restrict__ x, double &s0, double &s1, double &s2) {
-    if constexpr (V == 1) bsr3_row_sums_blk<G>(row, nrows, lane, ptr, col, val, x, s0, s1, s2);
-    else bsr3_row_sums<G>(row, nrows, lane, ptr, col, val, x, s0, s1, s2);
+    if constexpr (V == 0) row_sums_units<G>(row, valid, lane, ptr, col, val, x, s0, s1, s2);
+    else row_sums_blocks<G>(row, valid, lane, ptr, col, val, x, s0, s1, s2);
 }
 
 __device__ __forceinline__ double pick3(int c, double a, double b, double d) {
     return c == 0 ? a : (c == 1 ? b : d);
 }
 
+// Run the epilogue for the three components of `row`: lanes 0..2 in
+// parallel, or lane 0 for all three when G < 3.  Returns sum over the
+// handled components of epi's dot contribution (0 if none).
+template <int G, class Epi>
+__device__ __forceinline__ double epilogue(const Epi &epi, int row, int lane, double s0, double s1,
+                                           double s2) {
+    double d = 0.0;
+    if constexpr (G >= 3) {
+        if (lane < 3) d = epi(row, lane, s0, s1, s2);
+    } else {
+        if (lane == 0)
+            for (int c = 0; c < 3; ++c) d += epi(row, c, s0, s1, s2);
+    }
+    return d;
+}
+
 struct EpiSpmv {
     double alpha, beta;
     double *y;
-    __device__ void operator()(int row, int c, double s0, double s1, double s2) const {
+    __device__ double operator()(int row, int c, double s0, double s1, double s2) const {
         double *yi = y + 3 * static_cast<size_t>(row) + c;
         const double s = pick3(c, s0, s1, s2);
         *yi = alpha * s + (beta == 0.0 ? 0.0 : beta * *yi);
+        return 0.0;
     }
 };
 
 struct EpiResidual {
     const double *f;
     double *r;
-    __device__ void operator()(int row, int c, double s0, double s1, double s2) const {
+    __device__ double operator()(int row, int c, double s0, double s1, double s2) const {
         const size_t i = 3 * static_cast<size_t>(row) + c;
         r[i] = f[i] - pick3(c, s0, s1, s2);
+        return 0.0;
     }
 };
 
-struct EpiSmoothPoint {  // u_out = u + (omega/a_cc) * (f - A u)
+// u_out = u + (omega/a_cc) * (f - A u); returns f*u_out (for r.z)
+struct EpiSmoothPoint {
     const double *f, *u, *m;
     double *out;
-    __device__ void operator()(int row, int c, double s0, double s1, double s2) const {
+    __device__ double operator()(int row, int c, double s0, double s1, double s2) const {
         const size_t i = 3 * static_cast<size_t>(row) + c;
-        out[i] = u[i] + m[i] * (f[i] - pick3(c, s0, s1, s2));
+        const double fi = f[i];
+        const double o = u[i] + m[i] * (fi - pick3(c, s0, s1, s2));
+        out[i] = o;
+        return fi * o;
     }
 };
 
-struct EpiSmoothBlock {  // u_out = u + M_row (f - A u)_row
+// u_out = u + M_row (f - A u)_row; returns f*u_out
+struct EpiSmoothBlock {
     const double *f, *u, *m;
     double *out;
-    __device__ void operator()(int row, int c, double s0, double s1, double s2) const {
+    __device__ double operator()(int row, int c, double s0, double s1, double s2) const {
         const size_t b = 3 * static_cast<size_t>(row);
         const double r0 = f[b] - s0, r1 = f[b + 1] - s1, r2 = f[b + 2] - s2;
         const double *M = m + 9 * static_cast<size_t>(row) + 3 * c;
-        out[b + c] = u[b + c] + (M[0] * r0 + M[1] * r1 + M[2] * r2);
+        const double o = u[b + c] + (M[0] * r0 + M[1] * r1 + M[2] * r2);
+        out[b + c] = o;
+        return f[b + c] * o;
     }
 };
 
-// V = 0: row units; V = 1: block per lane; V = 2: block per lane with the
-// register budget capped for 6 resident CTAs (48 warps) per SM.
+// q = A p; returns p*q (CG p'Ap)
+struct EpiDot {
+    const double *p;
+    double *q;
+    __device__ double operator()(int row, int c, double s0, double s1, double s2) const {
+        const size_t i = 3 * static_cast<size_t>(row) + c;
+        const double qi = pick3(c, s0, s1, s2);
+        q[i] = qi;
+        return p[i] * qi;
+    }
+};
+
 template <int G, int V, class Epi>
-__global__ void __launch_bounds__(256, V == 2 ? 6 : 1) k_bsr3(int nrows,
+__global__ void __launch_bounds__(256) k_bsr3(int nrows, const int *__restrict__ ptr,
+        const int *__restrict__ col, const double *__restrict__ val,
+        const double *__restrict__ x, Epi epi) {
+    const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int row = gtid / G, lane = threadIdx.x % G;
+    const bool valid = row < nrows;
+    double s0, s1, s2;
+    row_sums<G, V>(row, valid, lane, ptr, col, val, x, s0, s1, s2);
+    if (valid) epilogue<G>(epi, row, lane, s0, s1, s2);
+}
+
+// Same over an explicit row list (interior / boundary rows of a partition).
+template <int G, class Epi>
+__global__ void __launch_bounds__(256) k_bsr3_rows(int nlist, const int *__restrict__ rows,
         const int *__restrict__ ptr, const int *__restrict__ col,
         const double *__restrict__ val, const double *__restrict__ x, Epi epi) {
     const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
-    const int row = gtid / G, lane = threadIdx.x % G;
+    const int g = gtid / G, lane = threadIdx.x % G;
+    const bool valid = g < nlist;
+    const int row = valid ? __ldg(rows + g) : 0;
     double s0, s1, s2;
-    row_sums<G, (V == 0 ? 0 : 1)>(row, nrows, lane, ptr, col, val, x, s0, s1, s2);
-    if (row < nrows && lane < 3) epi(row, lane, s0, s1, s2);
+    row_sums<G, 1>(row, valid, lane, ptr, col, val, x, s0, s1, s2);
+    if (valid) epilogue<G>(epi, row, lane, s0, s1, s2);
 }
 
 __device__ __forceinline__ double block_sum(double v) {
@@ -213,31 +266,89 @@ __device__ __forceinline__ double block_sum(double v) {
     return t;  // valid in thread 0
 }
 
-// fused CG matvec q = A p with p.q: grid-stride over row groups with a fixed
-// grid, so the partial sums (one per CTA) are few and their order fixed.
-constexpr int kDotCtas = 148 * 8;
+// CG scalar updates (cg.hpp:58-77) applied to a finished dot product s.
+__device__ void cg_apply(int what, double s, CgScalars *sc, cudaGraphConditionalHandle h) {
+    switch (what) {
+        case CG_RR: sc->rr = s; break;
+        case CG_PQ:
+            sc->pq = s;
+            if (!(s > 0.0)) sc->breakdown = 1;
+            sc->alpha = sc->rho / s;
+            break;
+        case CG_RZ:
+            sc->rho_new = s;
+            sc->beta = s / sc->rho;
+            sc->rho = s;
+            break;
+        case CG_RHO: sc->rho = s; break;
+        case CG_RR_LOOP: {
+            sc->rr = s;
+            const int it = sc->iter + 1;
+            sc->iter = it;
+            const bool go = (sqrt(s) / sc->norm_f > sc->tol) && it < sc->max_iter && !sc->breakdown;
+            cudaGraphSetConditional(h, go ? 1u : 0u);
+            break;
+        }
+        default: break;
+    }
+}
 
-template <int G, int V>
-__global__ void __launch_bounds__(256) k_bsr3_dot(int nrows, const int *__restrict__ ptr,
+// Deterministic grid-wide reduction without a second launch: every CTA
+// writes its partial, the last CTA to arrive (ticket) sums all partials in
+// index order and applies the CG update.
+__device__ void grid_finish(double d, double *partials, CgScalars *sc, int what,
+                            cudaGraphConditionalHandle h) {
+    __shared__ bool last;
+    d = block_sum(d);
+    if (threadIdx.x == 0) {
+        // release: the partial is visible before the ticket (no L1 flush,
+        // unlike __threadfence, so co-resident CTAs keep their cached x)
+        __stcg(partials + blockIdx.x, d);
+        cuda::atomic_ref<unsigned, cuda::thread_scope_device> t(sc->ticket);
+        last = t.fetch_add(1u, cuda::memory_order_release) == gridDim.x - 1;
+        if (last) cuda::atomic_thread_fence(cuda::memory_order_acquire, cuda::thread_scope_device);
+    }
+    __syncthreads();
+    if (!last) return;
+    double s = 0.0;
+    for (unsigned i = threadIdx.x; i < gridDim.x; i += blockDim.x) s += __ldcg(partials + i);
+    s = block_sum(s);
+    if (threadIdx.x == 0) {
+        sc->ticket = 0;
+        cg_apply(what, s, sc, h);
+    }
+}
+
+// SpMV-family kernel whose epilogue also yields a dot product, finished by
+// grid_finish: q = A p with p.q (CG), or the last smoothing sweep with r.z.
+// Grid-stride over row groups with a fixed grid so partials are few.
+template <int G, class Epi>
+__global__ void __launch_bounds__(256) k_bsr3_reduce(int nrows, const int *__restrict__ ptr,
         const int *__restrict__ col, const double *__restrict__ val,
-        const double *__restrict__ p, double *__restrict__ q, double *__restrict__ partials) {
+        const double *__restrict__ x, Epi epi, double *__restrict__ partials, CgScalars *sc,
+        int what) {
     const int groups = gridDim.x * (blockDim.x / G);
     const int lane = threadIdx.x % G;
     double d = 0.0;
     const int nit = (nrows + groups - 1) / groups;
     for (int it = 0; it < nit; ++it) {
         const int row = (blockIdx.x * blockDim.x + threadIdx.x) / G + it * groups;
+        const bool valid = row < nrows;
         double s0, s1, s2;
-        row_sums<G, (V == 0 ? 0 : 1)>(row, nrows, lane, ptr, col, val, p, s0, s1, s2);
-        if (row < nrows && lane < 3) {
-            const size_t i = 3 * static_cast<size_t>(row) + lane;
-            const double qi = pick3(lane, s0, s1, s2);
-            q[i] = qi;
-            d = fma(p[i], qi, d);
-        }
+        row_sums<G, 1>(row, valid, lane, ptr, col, val, x, s0, s1, s2);
+        if (valid) d += epilogue<G>(epi, row, lane, s0, s1, s2);
     }
-    d = block_sum(d);
-    if (threadIdx.x == 0) partials[blockIdx.x] = d;
+    grid_finish(d, partials, sc, what, 0);
+}
+
+constexpr int kReduceCtas = 148 * 8;
+
+int spmv_variant() {
+    static const int v = [] {
+        const char *e = std::getenv("SAMG_SPMV_VARIANT");
+        return e ? std::atoi(e) : 1;
+    }();
+    return v;
 }
 
 int choose_group(const Bsr3 &A) {
@@ -245,49 +356,43 @@ int choose_group(const Bsr3 &A) {
         const char *e = std::getenv("SAMG_SPMV_GROUP");
         return e ? std::atoi(e) : 0;
     }();
-    if (forced == 4 || forced == 8 || forced == 16 || forced == 32) return forced;
     const double bpr = A.nrows ? static_cast<double>(A.nnzb) / A.nrows : 0.0;
-    if (spmv_variant() >= 1) {
-        // ~7 blocks per lane: enough independent loads per thread to cover
-        // HBM latency, several rows per warp (measured on C1, fine rows of
-        // ~26 blocks: G=4 5.9 TB/s, G=8 5.2, G=16 4.8, G=32 4.2; profiles/)
-        static const double per_lane = [] {
-            const char *e = std::getenv("SAMG_SPMV_BLOCKS_PER_LANE");
-            return e ? std::atof(e) : 7.0;
-        }();
-        const double want = bpr / per_lane;
-        if (want > 16.0) return 32;
-        if (want > 8.0) return 16;
-        if (want > 4.0) return 8;
-        return 4;
+    if (spmv_variant() == 0) {
+        if (forced == 8 || forced == 16 || forced == 32) return forced;
+        return 3.0 * bpr >= 45.0 ? 32 : (3.0 * bpr >= 12.0 ? 16 : 8);
     }
-    if (3.0 * bpr >= 45.0) return 32;
-    if (3.0 * bpr >= 12.0) return 16;
-    return 8;
+    if (forced >= 1 && forced <= 128 && (forced & (forced - 1)) == 0) return forced;
+    // ~7 blocks per lane: enough independent loads per thread to cover HBM
+    // latency, several rows per warp (measured on C1, fine rows of ~26
+    // blocks: G=4 5.9 TB/s, G=8 5.2, G=16 4.8, G=32 4.2; profiles/)
+    static const double per_lane = [] {
+        const char *e = std::getenv("SAMG_SPMV_BLOCKS_PER_LANE");
+        return e ? std::atof(e) : 7.0;
+    }();
+    const double want = bpr / per_lane;
+    int G = 1;
+    while (G < 32 && G < want) G *= 2;
+    // small (coarse-level / restriction) matrices cannot fill 148 SMs:
+    // spend more lanes per row to shorten the serial chains instead
+    // (R1 of C1: 3 822 rows; 8 lanes -> 40 us, 32 lanes -> ~6 us)
+    while (G < 128 && A.nrows * G < 148LL * 1024) G *= 2;
+    return G;
 }
 
-#define SAMG_DISPATCH_G(G, V, ...)                                  \
-    if ((V) == 1) {                                                 \
-        switch (G) {                                                \
-            case 32: { constexpr int GG = 32, VV = 1; __VA_ARGS__; } break; \
-            case 16: { constexpr int GG = 16, VV = 1; __VA_ARGS__; } break; \
-            case 8: { constexpr int GG = 8, VV = 1; __VA_ARGS__; } break;   \
-            default: { constexpr int GG = 4, VV = 1; __VA_ARGS__; } break;  \
-        }                                                           \
-    } else if ((V) == 2) {                                          \
-        switch (G) {                                                \
-            case 32: { constexpr int GG = 32, VV = 2; __VA_ARGS__; } break; \
-            case 16: { constexpr int GG = 16, VV = 2; __VA_ARGS__; } break; \
-            case 8: { constexpr int GG = 8, VV = 2; __VA_ARGS__; } break;   \
-            default: { constexpr int GG = 4, VV = 2; __VA_ARGS__; } break;  \
-        }                                                           \
-    } else {                                                        \
-        switch (G) {                                                \
-            case 32: { constexpr int GG = 32, VV = 0; __VA_ARGS__; } break; \
-            case 16: { constexpr int GG = 16, VV = 0; __VA_ARGS__; } break; \
-            default: { constexpr int GG = 8, VV = 0; __VA_ARGS__; } break;  \
-        }                                                           \
+// Calls f(std::integral_constant<int, G>) for the runtime G.
+template <class F>
+void dispatch_group(int G, F f) {
+    switch (G) {
+        case 1: f(std::integral_constant<int, 1>{}); break;
+        case 2: f(std::integral_constant<int, 2>{}); break;
+        case 4: f(std::integral_constant<int, 4>{}); break;
+        case 8: f(std::integral_constant<int, 8>{}); break;
+        case 16: f(std::integral_constant<int, 16>{}); break;
+        case 32: f(std::integral_constant<int, 32>{}); break;
+        case 64: f(std::integral_constant<int, 64>{}); break;
+        default: f(std::integral_constant<int, 128>{}); break;
     }
+}
 
 template <class Epi>
 void launch_rows(const Bsr3 &A, const double *x, Epi epi, cudaStream_t s) {
@@ -295,8 +400,39 @@ void launch_rows(const Bsr3 &A, const double *x, Epi epi, cudaStream_t s) {
     const int G = choose_group(A);
     const int grid = ceil_div(A.nrows * static_cast<int64_t>(G), 256);
     const int n = static_cast<int>(A.nrows);
-    SAMG_DISPATCH_G(G, spmv_variant(),
-        (k_bsr3<GG, VV><<<grid, 256, 0, s>>>(n, A.ptr.p, A.col.p, A.val.p, x, epi)));
+    if (spmv_variant() == 0) {
+        if (G == 32) k_bsr3<32, 0><<<grid, 256, 0, s>>>(n, A.ptr.p, A.col.p, A.val.p, x, epi);
+        else if (G == 16) k_bsr3<16, 0><<<grid, 256, 0, s>>>(n, A.ptr.p, A.col.p, A.val.p, x, epi);
+        else k_bsr3<8, 0><<<grid, 256, 0, s>>>(n, A.ptr.p, A.col.p, A.val.p, x, epi);
+    } else {
+        dispatch_group(G, [&](auto g) {
+            constexpr int GG = decltype(g)::value;
+            k_bsr3<GG, 1><<<grid, 256, 0, s>>>(n, A.ptr.p, A.col.p, A.val.p, x, epi);
+        });
+    }
+    CK_LAUNCH();
+}
+
+template <class Epi>
+void launch_reduce(const Bsr3 &A, const double *x, Epi epi, double *partials, CgScalars *sc,
+                   int what, cudaStream_t s) {
+    const int G = choose_group(A);
+    const int n = static_cast<int>(A.nrows);
+    dispatch_group(G, [&](auto g) {
+        constexpr int GG = decltype(g)::value;
+        // persistent grid = exactly one wave of resident CTAs (a second,
+        // partial wave cost ~15% on C1's fine level)
+        static const int resident = [] {
+            int occ = 0, dev = 0, sms = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bsr3_reduce<GG, Epi>, 256, 0);
+            return std::max(1, occ) * sms;
+        }();
+        const int grid = std::max(1, std::min({kReduceCtas, resident,
+                                               ceil_div(A.nrows * static_cast<int64_t>(GG), 256)}));
+        k_bsr3_reduce<GG><<<grid, 256, 0, s>>>(n, A.ptr.p, A.col.p, A.val.p, x, epi, partials, sc, what);
+    });
     CK_LAUNCH();
 }
 
@@ -307,24 +443,28 @@ __global__ void k_smooth_zero_point(int64_t n, const double *__restrict__ m,
         u[i] = m[i] * f[i];
 }
 
+// u = M f for 3x3 M: one thread per block row (72 B of M, 24 B of f, 24 B of u)
 __global__ void k_smooth_zero_block(int64_t nrows, const double *__restrict__ m,
         const double *__restrict__ f, double *__restrict__ u) {
-    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < 3 * nrows;
-         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t row = e / 3;
-        const int c = static_cast<int>(e - 3 * row);
-        const double *M = m + 9 * row + 3 * c;
-        const double *fr = f + 3 * row;
-        u[e] = M[0] * fr[0] + M[1] * fr[1] + M[2] * fr[2];
+    for (int64_t row = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; row < nrows;
+         row += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double *M = m + 9 * row;
+        const double f0 = f[3 * row], f1 = f[3 * row + 1], f2 = f[3 * row + 2];
+        double Mv[9];
+#pragma unroll
+        for (int e = 0; e < 9; ++e) Mv[e] = __ldcs(M + e);
+        u[3 * row] = Mv[0] * f0 + Mv[1] * f1 + Mv[2] * f2;
+        u[3 * row + 1] = Mv[3] * f0 + Mv[4] * f1 + Mv[5] * f2;
+        u[3 * row + 2] = Mv[6] * f0 + Mv[7] * f1 + Mv[8] * f2;
     }
 }
 
 // u = Ainv f, Ainv row-major with an even leading dimension (zero padded):
-// one warp per row, 16-byte loads, 4 in flight per lane.
-__global__ void k_dense_gemv(int n, int64_t ld, const double *__restrict__ A,
+// one 128-thread CTA per row, 16-byte loads, 4 in flight per thread.
+__global__ void __launch_bounds__(128) k_dense_gemv(int n, int64_t ld, const double *__restrict__ A,
         const double *__restrict__ f, double *__restrict__ u) {
-    const int row = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
-    if (row >= n) return;
+    __shared__ double red[4];
+    const int row = blockIdx.x;
     const double2 *a = reinterpret_cast<const double2 *>(A + static_cast<size_t>(row) * ld);
     const int n2 = static_cast<int>(ld / 2);
     double s = 0.0, t = 0.0;
@@ -332,17 +472,17 @@ __global__ void k_dense_gemv(int n, int64_t ld, const double *__restrict__ A,
         const int j = 2 * j2;
         return make_double2(__ldg(f + j), j + 1 < n ? __ldg(f + j + 1) : 0.0);
     };
-    int j2 = lane;
-    for (; j2 + 96 < n2; j2 += 128) {
-        const double2 a0 = __ldcs(a + j2), a1 = __ldcs(a + j2 + 32), a2 = __ldcs(a + j2 + 64),
-                      a3 = __ldcs(a + j2 + 96);
-        const double2 f0 = fpair(j2), f1 = fpair(j2 + 32), f2 = fpair(j2 + 64), f3 = fpair(j2 + 96);
+    int j2 = threadIdx.x;
+    for (; j2 + 384 < n2; j2 += 512) {
+        const double2 a0 = __ldcs(a + j2), a1 = __ldcs(a + j2 + 128), a2 = __ldcs(a + j2 + 256),
+                      a3 = __ldcs(a + j2 + 384);
+        const double2 f0 = fpair(j2), f1 = fpair(j2 + 128), f2 = fpair(j2 + 256), f3 = fpair(j2 + 384);
         s = fma(a0.x, f0.x, s); t = fma(a0.y, f0.y, t);
         s = fma(a1.x, f1.x, s); t = fma(a1.y, f1.y, t);
         s = fma(a2.x, f2.x, s); t = fma(a2.y, f2.y, t);
         s = fma(a3.x, f3.x, s); t = fma(a3.y, f3.y, t);
     }
-    for (; j2 < n2; j2 += 32) {
+    for (; j2 < n2; j2 += 128) {
         const double2 a0 = __ldcs(a + j2);
         const double2 f0 = fpair(j2);
         s = fma(a0.x, f0.x, s); t = fma(a0.y, f0.y, t);
@@ -350,90 +490,75 @@ __global__ void k_dense_gemv(int n, int64_t ld, const double *__restrict__ A,
     s += t;
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    if (lane == 0) u[row] = s;
+    if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) u[row] = (red[0] + red[1]) + (red[2] + red[3]);
 }
 
+// Vector kernels: 2 elements per thread per step (16-byte loads; the
+// vectors are cudaMalloc'd, so 16-byte aligned), grid-stride, tail handled
+// by thread 0.
 __global__ void __launch_bounds__(256) k_dot(int64_t n, const double *__restrict__ x,
-        const double *__restrict__ y, double *__restrict__ partials) {
-    double s = 0.0;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        s = fma(x[i], y[i], s);
-    s = block_sum(s);
-    if (threadIdx.x == 0) partials[blockIdx.x] = s;
+        const double *__restrict__ y, double *__restrict__ partials, CgScalars *sc, int what) {
+    const int64_t n2 = n / 2;
+    const double2 *x2 = reinterpret_cast<const double2 *>(x), *y2 = reinterpret_cast<const double2 *>(y);
+    double s = 0.0, t = 0.0;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n2;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double2 a = x2[i], b = y2[i];
+        s = fma(a.x, b.x, s);
+        t = fma(a.y, b.y, t);
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) s = fma(x[n - 1], y[n - 1], s);
+    grid_finish(s + t, partials, sc, what, 0);
 }
 
-__global__ void __launch_bounds__(256) k_cg_update(int64_t n, const CgScalars *__restrict__ sc,
+// u += alpha p; r -= alpha q; r.r (cg.hpp:68-71), finished in place
+__global__ void __launch_bounds__(256) k_cg_update(int64_t n, CgScalars *sc,
         const double *__restrict__ p, const double *__restrict__ q, double *__restrict__ u,
-        double *__restrict__ r, double *__restrict__ partials) {
+        double *__restrict__ r, double *__restrict__ partials, int what,
+        cudaGraphConditionalHandle h) {
     const double a = sc->alpha;
-    double s = 0.0;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+    const int64_t n2 = n / 2;
+    const double2 *p2 = reinterpret_cast<const double2 *>(p), *q2 = reinterpret_cast<const double2 *>(q);
+    double2 *u2 = reinterpret_cast<double2 *>(u), *r2 = reinterpret_cast<double2 *>(r);
+    double s = 0.0, t = 0.0;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n2;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        u[i] = fma(a, p[i], u[i]);
-        const double ri = fma(-a, q[i], r[i]);
-        r[i] = ri;
+        const double2 pp = p2[i], qq = q2[i], uu = u2[i], rr = r2[i];
+        u2[i] = make_double2(fma(a, pp.x, uu.x), fma(a, pp.y, uu.y));
+        const double ra = fma(-a, qq.x, rr.x), rb = fma(-a, qq.y, rr.y);
+        r2[i] = make_double2(ra, rb);
+        s = fma(ra, ra, s);
+        t = fma(rb, rb, t);
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        u[n - 1] = fma(a, p[n - 1], u[n - 1]);
+        const double ri = fma(-a, q[n - 1], r[n - 1]);
+        r[n - 1] = ri;
         s = fma(ri, ri, s);
     }
-    s = block_sum(s);
-    if (threadIdx.x == 0) partials[blockIdx.x] = s;
+    grid_finish(s + t, partials, sc, what, h);
 }
 
 __global__ void k_p_update(int64_t n, const CgScalars *__restrict__ sc,
         const double *__restrict__ z, double *__restrict__ p) {
     const double b = sc->beta;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        p[i] = fma(b, p[i], z[i]);
+    const int64_t n2 = n / 2;
+    const double2 *z2 = reinterpret_cast<const double2 *>(z);
+    double2 *p2 = reinterpret_cast<double2 *>(p);
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n2;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double2 zz = z2[i], pp = p2[i];
+        p2[i] = make_double2(fma(b, pp.x, zz.x), fma(b, pp.y, zz.y));
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) p[n - 1] = fma(b, p[n - 1], z[n - 1]);
 }
 
 __global__ void k_fill(int64_t n, double v, double *x) {
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
         x[i] = v;
-}
-
-__global__ void __launch_bounds__(256) k_finalize(int what, const double *__restrict__ partials,
-        int nparts, CgScalars *sc) {
-    double s = 0.0;
-    for (int i = threadIdx.x; i < nparts; i += blockDim.x) s += partials[i];
-    s = block_sum(s);
-    if (threadIdx.x != 0) return;
-    switch (what) {
-        case 0: sc->rr = s; break;
-        case 1:
-            sc->pq = s;
-            if (!(s > 0.0)) sc->breakdown = 1;
-            sc->alpha = sc->rho / s;
-            break;
-        case 2:
-            sc->rho_new = s;
-            sc->beta = s / sc->rho;
-            sc->rho = s;
-            break;
-        default: sc->rho = s; break;
-    }
-}
-
-__global__ void __launch_bounds__(256) k_finalize_loop(const double *__restrict__ partials,
-        int nparts, CgScalars *sc, cudaGraphConditionalHandle h) {
-    double s = 0.0;
-    for (int i = threadIdx.x; i < nparts; i += blockDim.x) s += partials[i];
-    s = block_sum(s);
-    if (threadIdx.x != 0) return;
-    sc->rr = s;
-    const int it = sc->iter + 1;
-    sc->iter = it;
-    const bool go = (sqrt(s) / sc->norm_f > sc->tol) && it < sc->max_iter && !sc->breakdown;
-    cudaGraphSetConditional(h, go ? 1u : 0u);
-}
-
-// norm_f / tol / max_iter are written by the host before the graph launch
-__global__ void k_cg_loop_init(CgScalars *sc, cudaGraphConditionalHandle h) {
-    sc->iter = 0;
-    sc->breakdown = 0;
-    // loop condition before the first pass: res_norm = norm_f (cg.hpp:60-62)
-    cudaGraphSetConditional(h, (1.0 > sc->tol && 0 < sc->max_iter) ? 1u : 0u);
 }
 
 int vec_grid(int64_t n) {
@@ -446,6 +571,21 @@ int vec_grid(int64_t n) {
 void launch_spmv(const Bsr3 &A, double alpha, const double *x, double beta, double *y,
                  cudaStream_t s) {
     launch_rows(A, x, EpiSpmv{alpha, beta, y}, s);
+}
+
+// y[rows] = alpha*A[rows,:]*x + beta*y[rows]; group 0 = choose from A
+void launch_spmv_rows(const Bsr3 &A, const int *rows, int64_t nlist, int group, double alpha,
+                      const double *x, double beta, double *y, cudaStream_t s) {
+    if (nlist == 0) return;
+    const int G = (group >= 1 && group <= 128 && (group & (group - 1)) == 0) ? group : choose_group(A);
+    const int grid = ceil_div(nlist * static_cast<int64_t>(G), 256);
+    const int n = static_cast<int>(nlist);
+    const EpiSpmv epi{alpha, beta, y};
+    dispatch_group(G, [&](auto g) {
+        constexpr int GG = decltype(g)::value;
+        k_bsr3_rows<GG><<<grid, 256, 0, s>>>(n, rows, A.ptr.p, A.col.p, A.val.p, x, epi);
+    });
+    CK_LAUNCH();
 }
 
 void launch_residual(const Bsr3 &A, const double *f, const double *u, double *r,
@@ -462,62 +602,47 @@ void launch_smooth(const Bsr3 &A, const Smoother &M, const double *f, const doub
 void launch_smooth_zero(int64_t nrows, const Smoother &M, const double *f, double *u,
                         cudaStream_t s) {
     if (nrows == 0) return;
-    const int grid = vec_grid(3 * nrows);
-    if (M.kind == SM_POINT) k_smooth_zero_point<<<grid, 256, 0, s>>>(3 * nrows, M.data.p, f, u);
-    else k_smooth_zero_block<<<grid, 256, 0, s>>>(nrows, M.data.p, f, u);
+    if (M.kind == SM_POINT) k_smooth_zero_point<<<vec_grid(3 * nrows), 256, 0, s>>>(3 * nrows, M.data.p, f, u);
+    else k_smooth_zero_block<<<vec_grid(nrows), 256, 0, s>>>(nrows, M.data.p, f, u);
     CK_LAUNCH();
 }
 
-void launch_spmv_dot(const Bsr3 &A, const double *p, double *q, double *partials, int *nparts,
-                     cudaStream_t s) {
-    const int G = choose_group(A);
-    const int grid = std::max(1, std::min(kDotCtas, ceil_div(A.nrows * static_cast<int64_t>(G), 256)));
-    const int n = static_cast<int>(A.nrows);
-    SAMG_DISPATCH_G(G, spmv_variant(),
-        (k_bsr3_dot<GG, VV><<<grid, 256, 0, s>>>(n, A.ptr.p, A.col.p, A.val.p, p, q, partials)));
-    CK_LAUNCH();
-    *nparts = grid;
+void launch_spmv_dot(const Bsr3 &A, const double *p, double *q, double *partials,
+                     CgScalars *sc, cudaStream_t s) {
+    launch_reduce(A, p, EpiDot{p, q}, partials, sc, CG_PQ, s);
+}
+
+void launch_smooth_dot(const Bsr3 &A, const Smoother &M, const double *f, const double *u,
+                       double *u_out, double *partials, CgScalars *sc, cudaStream_t s) {
+    if (M.kind == SM_POINT)
+        launch_reduce(A, u, EpiSmoothPoint{f, u, M.data.p, u_out}, partials, sc, CG_RZ, s);
+    else
+        launch_reduce(A, u, EpiSmoothBlock{f, u, M.data.p, u_out}, partials, sc, CG_RZ, s);
 }
 
 void launch_dense_gemv(int64_t n, const double *Ainv, const double *f, double *u,
                        cudaStream_t s) {
     if (n == 0) return;
-    k_dense_gemv<<<ceil_div(n * 32, 256), 256, 0, s>>>(static_cast<int>(n), dense_ld(n), Ainv, f, u);
+    k_dense_gemv<<<static_cast<int>(n), 128, 0, s>>>(static_cast<int>(n), dense_ld(n), Ainv, f, u);
     CK_LAUNCH();
 }
 
-void launch_dot_partials(int64_t n, const double *x, const double *y, double *partials,
-                         cudaStream_t s) {
-    k_dot<<<kRedBlocks, 256, 0, s>>>(n, x, y, partials);
+void launch_dot(int64_t n, const double *x, const double *y, double *partials, CgScalars *sc,
+                int what, cudaStream_t s) {
+    k_dot<<<vec_grid(n / 2 + 1), 256, 0, s>>>(n, x, y, partials, sc, what);
     CK_LAUNCH();
 }
 
-void launch_finalize(int what, const double *partials, int nparts, CgScalars *sc,
-                     cudaStream_t s) {
-    k_finalize<<<1, 256, 0, s>>>(what, partials, nparts, sc);
-    CK_LAUNCH();
-}
-
-void launch_finalize_loop(const double *partials, int nparts, CgScalars *sc,
-                          cudaGraphConditionalHandle h, cudaStream_t s) {
-    k_finalize_loop<<<1, 256, 0, s>>>(partials, nparts, sc, h);
-    CK_LAUNCH();
-}
-
-void launch_cg_loop_init(CgScalars *sc, cudaGraphConditionalHandle h, cudaStream_t s) {
-    k_cg_loop_init<<<1, 1, 0, s>>>(sc, h);
-    CK_LAUNCH();
-}
-
-void launch_cg_update(int64_t n, const CgScalars *sc, const double *p, const double *q,
-                      double *u, double *r, double *partials, cudaStream_t s) {
-    k_cg_update<<<kRedBlocks, 256, 0, s>>>(n, sc, p, q, u, r, partials);
+void launch_cg_update(int64_t n, CgScalars *sc, const double *p, const double *q, double *u,
+                      double *r, double *partials, int what, cudaGraphConditionalHandle h,
+                      cudaStream_t s) {
+    k_cg_update<<<vec_grid(n / 2 + 1), 256, 0, s>>>(n, sc, p, q, u, r, partials, what, h);
     CK_LAUNCH();
 }
 
 void launch_p_update(int64_t n, const CgScalars *sc, const double *z, double *p,
                      cudaStream_t s) {
-    k_p_update<<<vec_grid(n), 256, 0, s>>>(n, sc, z, p);
+    k_p_update<<<vec_grid(n / 2 + 1), 256, 0, s>>>(n, sc, z, p);
     CK_LAUNCH();
 }
 

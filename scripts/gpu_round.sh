@@ -1,6 +1,5 @@
-./paper_2202_09056_b200/csrc/build/shim_test; echo shim rc=$?
-python -m pytest tests -m gpu -q 2>&1 | tail -5
-python bench.py --no-cpu-baseline --steps 500 > gpurun_out/bench4.json 2> gpurun_out/bench4.err; echo bench rc=$?
-SMALL="python bench.py --steps 20 --warmup 5 --amg-repeats 1 --no-cpu-baseline"
-$SMALL > gpurun_out/plain.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches4.csv $SMALL > gpurun_out/ncu_launch.log 2>&1; echo ncu1 rc=$?
+python -m pytest tests -m gpu -q -x 2>&1 | tail -4
+python bench.py --no-cpu-baseline --steps 1000 > gpurun_out/bench7.json 2> gpurun_out/bench7.err; echo bench rc=$?; tail -3 gpurun_out/bench7.err
+python scripts/spmv_variants.py --amg-repeats 2 2>&1 | head -4
+SAMG_CG_GRAPH=0 python scripts/profile_solve.py 5 > gpurun_out/ps.log 2>&1 && \
+SAMG_CG_GRAPH=0 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"k_bsr3|k_smooth|k_dense|k_cg|k_p_update|k_dot|k_fill" --csv --log-file gpurun_out/solve_launches3.csv python scripts/profile_solve.py 5 > gpurun_out/ncu_solve.log 2>&1; echo rc=$?
