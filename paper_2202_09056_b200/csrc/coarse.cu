@@ -19,6 +19,9 @@
 // so the n^3 work streams W once per panel instead of once per column.
 #include <cooperative_groups.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace cg = cooperative_groups;
@@ -245,7 +248,14 @@ void dense_inverse(const Bsr3 &A, DevBuf<double> &Ainv, DevError *err, cudaStrea
     CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
     if (!coop) fail(SAMG_UNSUPPORTED, "dense coarse solve needs cooperative launch");
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_panel_gj, kPT, 0));
-    const int pgrid = static_cast<int>(std::min<int64_t>(nsm * std::max(per_sm, 1), (n + 15) / 16));
+    // panel CTAs: fewer CTAs make the two grid barriers per column cheaper,
+    // more CTAs spread the row updates (SAMG_GJ_CTAS overrides)
+    static const int64_t gj_ctas = [] {
+        const char *e = std::getenv("SAMG_GJ_CTAS");
+        return e ? std::atoll(e) : 128;
+    }();
+    const int pgrid = static_cast<int>(std::max<int64_t>(
+        1, std::min<int64_t>({static_cast<int64_t>(nsm) * std::max(per_sm, 1), (n + 15) / 16, gj_ctas})));
     DevBuf<double> pval(pgrid, s);
     DevBuf<int64_t> pidx(pgrid, s), piv(kB, s);
     CK(cudaMemsetAsync(W.p, 0, W.bytes(), s));

@@ -165,17 +165,24 @@ __global__ void k_s2b_fill(int64_t nb, const int64_t *ptr, const int64_t *col,
 // coarsening.hpp:64-75); edge iff w*w > (eps2*d_i)*d_j (coarsening.hpp:105),
 // union-symmetrised.
 
+// per-block max|a| over its 9 entries (read once, coalesced)
+__global__ void k_block_maxabs(int64_t nnzb, const double *val, double *wblk) {
+    for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < nnzb;
+         j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double *b = val + 9 * j;
+        double w = 0.0;
+        for (int e = 0; e < 9; ++e) w = fmax(w, fabs(b[e]));
+        wblk[j] = w;
+    }
+}
+
 template <class F>
 __device__ __forceinline__ void for_node_tiles(int node, int h, const int *ptr, const int *col,
-                                               const double *val, F f) {
-    // visit (node column, max|a|) of node row `node` in ascending node column
+                                               const double *wblk, F f) {
+    // visit (node column, max|a|) of node row `node` in ascending node column;
+    // wblk[j] = max|a| of block j (max is order-independent: exact)
     if (h == 1) {
-        for (int j = ptr[node]; j < ptr[node + 1]; ++j) {
-            const double *b = val + 9 * static_cast<int64_t>(j);
-            double w = 0.0;
-            for (int e = 0; e < 9; ++e) w = fmax(w, fabs(b[e]));
-            f(col[j], w);
-        }
+        for (int j = ptr[node]; j < ptr[node + 1]; ++j) f(col[j], wblk[j]);
         return;
     }
     int hd[4], en[4];
@@ -188,8 +195,7 @@ __device__ __forceinline__ void for_node_tiles(int node, int h, const int *ptr, 
         double w = 0.0;
         for (int r = 0; r < h; ++r)
             while (hd[r] < en[r] && col[hd[r]] / h == m) {
-                const double *b = val + 9 * static_cast<int64_t>(hd[r]);
-                for (int e = 0; e < 9; ++e) w = fmax(w, fabs(b[e]));
+                w = fmax(w, wblk[hd[r]]);
                 ++hd[r];
             }
         f(m, w);
@@ -271,79 +277,121 @@ __global__ void k_agg_b(int n, const int *gp, const int *gc, unsigned char *stat
 }
 
 // ---------------------------------------------------------------------------
-// tentative prolongation: Householder thin QR per aggregate, one thread per
-// aggregate, loop orders of coarsening.hpp:167-229 and :289-309.
+// tentative prolongation: Householder thin QR per aggregate, loop orders of
+// coarsening.hpp:167-229 and :289-309.  A group of 16 lanes owns one
+// aggregate: every sum over rows i stays sequential on one lane (lane 0 for
+// the column norm, lane c for column c's dot products), so the result is
+// bit-identical to the sequential reference; the k <= 12 column updates and
+// all elementwise work run in parallel across the lanes.
 
-__global__ void k_tentative_qr(int64_t naggs, int pbs, int k, const int *nodes,
-                               const int *agg_ptr, const double *B, int64_t bnrows,
-                               double *work, double *Qw, double *Pt, double *Bc, DevError *err) {
-    const int64_t a = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (a >= naggs) return;
+constexpr int kQrLanes = 16;
+
+__global__ void __launch_bounds__(256) k_tentative_qr(int64_t naggs, int pbs, int k,
+        const int *nodes, const int *agg_ptr, const double *B, int64_t bnrows, double *work,
+        double *Qw, double *Pt, double *Bc) {
+    __shared__ double Rs[256 / kQrLanes][144];
+    const int64_t a = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / kQrLanes;
+    const int lane = threadIdx.x % kQrLanes;
+    const int base = (threadIdx.x % 32) & ~(kQrLanes - 1);
+    const unsigned mask = 0xffffu << base;
+    if (a >= naggs) return;  // whole group
+    double *R = Rs[threadIdx.x / kQrLanes];
     const int n0 = agg_ptr[a], n1 = agg_ptr[a + 1];
     const int64_t m = static_cast<int64_t>(pbs) * (n1 - n0);
     double *A = work + static_cast<int64_t>(pbs) * n0 * k;
     double *Q = Qw + static_cast<int64_t>(pbs) * n0 * k;
 #define a_(i, j) A[(j) * m + (i)]
 #define ROW(r) (static_cast<int64_t>(nodes[n0 + (r) / pbs]) * pbs + (r) % pbs)
-    for (int c = 0; c < k; ++c)
-        for (int64_t r = 0; r < m; ++r) a_(r, c) = B[c * bnrows + ROW(r)];
     double local_max = 0;
-    for (int64_t t = 0; t < m * k; ++t) local_max = fmax(local_max, fabs(A[t]));
+    for (int64_t t = lane; t < m * k; t += kQrLanes) {
+        const int64_t c = t / m, r = t - c * m;
+        const double v = B[c * bnrows + ROW(r)];
+        A[t] = v;
+        local_max = fmax(local_max, fabs(v));
+    }
+    for (int off = kQrLanes / 2; off >= 1; off >>= 1)
+        local_max = fmax(local_max, __shfl_xor_sync(mask, local_max, off, kQrLanes));
+    __syncwarp(mask);
     const double tol = __dmul_rn(1e-12, fmax(local_max, 1.0));
-    double tau[12], R[144];
-    for (int j = 0; j < k; ++j) tau[j] = 0.0;
+    double tau[12];
+    for (int j = 0; j < 12; ++j) tau[j] = 0.0;
     const int64_t steps = m < k ? m : k;
     for (int64_t j = 0; j < steps; ++j) {
-        double normx = 0;
-        for (int64_t i = j; i < m; ++i) normx = __dadd_rn(normx, __dmul_rn(a_(i, j), a_(i, j)));
-        normx = __dsqrt_rn(normx);
-        if (normx <= tol) { tau[j] = 0; continue; }
-        const double alpha = a_(j, j) >= 0 ? -normx : normx;
-        const double v0 = __dsub_rn(a_(j, j), alpha);
-        for (int64_t i = j + 1; i < m; ++i) a_(i, j) = __ddiv_rn(a_(i, j), v0);
+        double normx = 0, alpha = 0, v0 = 0;
+        int skip = 0;
+        if (lane == 0) {
+            for (int64_t i = j; i < m; ++i) normx = __dadd_rn(normx, __dmul_rn(a_(i, j), a_(i, j)));
+            normx = __dsqrt_rn(normx);
+            skip = normx <= tol;
+            if (!skip) {
+                alpha = a_(j, j) >= 0 ? -normx : normx;
+                v0 = __dsub_rn(a_(j, j), alpha);
+            }
+        }
+        skip = __shfl_sync(mask, skip, base);
+        if (skip) continue;  // tau[j] stays 0
+        alpha = __shfl_sync(mask, alpha, base);
+        v0 = __shfl_sync(mask, v0, base);
         tau[j] = __ddiv_rn(-v0, alpha);
-        a_(j, j) = alpha;
-        for (int c = j + 1; c < k; ++c) {
+        for (int64_t i = j + 1 + lane; i < m; i += kQrLanes) a_(i, j) = __ddiv_rn(a_(i, j), v0);
+        __syncwarp(mask);
+        if (lane == 0) a_(j, j) = alpha;
+        const int c = lane;
+        if (c > j && c < k) {
             double s = a_(j, c);
             for (int64_t i = j + 1; i < m; ++i) s = __dadd_rn(s, __dmul_rn(a_(i, j), a_(i, c)));
             s = __dmul_rn(s, tau[j]);
             a_(j, c) = __dsub_rn(a_(j, c), s);
             for (int64_t i = j + 1; i < m; ++i) a_(i, c) = __dsub_rn(a_(i, c), __dmul_rn(s, a_(i, j)));
         }
+        __syncwarp(mask);
     }
-    for (int t = 0; t < k * k; ++t) R[t] = 0.0;
-    for (int j = 0; j < k; ++j)
-        for (int64_t i = 0; i <= (j < m - 1 ? j : m - 1); ++i) R[j * k + i] = a_(i, j);
-    for (int64_t t = 0; t < m * k; ++t) Q[t] = 0.0;
-    for (int64_t j = 0; j < (m < k ? m : k); ++j) Q[j * m + j] = 1.0;
+    for (int t = lane; t < k * k; t += kQrLanes) {
+        const int j = t / k, i = t - j * k;  // R[j*k + i] = a(i, j) for i <= min(j, m-1)
+        R[t] = (i <= j && i < m) ? a_(i, j) : 0.0;
+    }
+    for (int64_t t = lane; t < m * k; t += kQrLanes) {
+        const int64_t c = t / m, r = t - c * m;
+        Q[t] = (r == c) ? 1.0 : 0.0;
+    }
+    __syncwarp(mask);
     for (int64_t j = steps - 1; j >= 0; --j) {
         if (tau[j] == 0) continue;
-        for (int c = 0; c < k; ++c) {
+        const int c = lane;
+        if (c < k) {
             double s = Q[c * m + j];
             for (int64_t i = j + 1; i < m; ++i) s = __dadd_rn(s, __dmul_rn(a_(i, j), Q[c * m + i]));
             s = __dmul_rn(s, tau[j]);
             Q[c * m + j] = __dsub_rn(Q[c * m + j], s);
             for (int64_t i = j + 1; i < m; ++i) Q[c * m + i] = __dsub_rn(Q[c * m + i], __dmul_rn(s, a_(i, j)));
         }
+        __syncwarp(mask);
     }
+    // rank-deficient columns (coarsening.hpp:222-228): lane j tests column j
     const double lm = fmax(local_max, 1e-300);
-    for (int j = 0; j < k; ++j) {
+    const int j = lane;
+    bool drop = false;
+    if (j < k) {
         const double rjj = (j < m) ? fabs(R[j * k + j]) : 0.0;
-        if (rjj <= __dmul_rn(1e-12, lm)) {
-            for (int64_t i = 0; i < m; ++i) Q[j * m + i] = 0.0;
-            for (int c = 0; c < k; ++c) R[c * k + j] = 0.0;
-        }
+        drop = rjj <= __dmul_rn(1e-12, lm);
     }
-    for (int64_t r = 0; r < m; ++r) {
-        const int64_t row = ROW(r);
-        for (int c = 0; c < k; ++c) Pt[row * k + c] = Q[c * m + r];
+    __syncwarp(mask);
+    if (drop) {
+        for (int64_t i = 0; i < m; ++i) Q[j * m + i] = 0.0;
+        for (int c = 0; c < k; ++c) R[c * k + j] = 0.0;
+    }
+    __syncwarp(mask);
+    for (int64_t t = lane; t < m * k; t += kQrLanes) {
+        const int64_t r = t / k, c = t - r * k;
+        Pt[ROW(r) * k + c] = Q[c * m + r];
     }
     const int64_t bcn = naggs * k;
-    for (int i = 0; i < k; ++i)
-        for (int c = 0; c < k; ++c) Bc[c * bcn + a * k + i] = R[c * k + i];
+    for (int t = lane; t < k * k; t += kQrLanes) {
+        const int c = t / k, i = t - c * k;
+        Bc[c * bcn + a * k + i] = R[c * k + i];
+    }
 #undef a_
 #undef ROW
-    (void)err;
 }
 
 // ---------------------------------------------------------------------------
@@ -848,17 +896,19 @@ void scalar_to_bsr3(int64_t n, const int64_t *d_ptr, const int64_t *d_col, const
 void strength_graph(const Bsr3 &A, int h, double eps_strong, Graph &G, cudaStream_t s) {
     const int n = static_cast<int>(A.nrows / h);
     const double eps2 = eps_strong * eps_strong;
-    DevBuf<double> d(n, s);
+    DevBuf<double> d(n, s), wblk(A.nnzb + 1, s);
     const int grid = ceil_div(n, 256);
-    k_strength_diag<<<grid, 256, 0, s>>>(n, h, A.ptr.p, A.col.p, A.val.p, d.p);
+    k_block_maxabs<<<std::max(1, std::min(ceil_div(A.nnzb, 256), 65535)), 256, 0, s>>>(A.nnzb, A.val.p,
+                                                                                    wblk.p);
+    k_strength_diag<<<grid, 256, 0, s>>>(n, h, A.ptr.p, A.col.p, wblk.p, d.p);
     CK_LAUNCH();
     DevBuf<int> cnt(n + 1, s), off(n + 1, s);
-    k_strength_edges<<<grid, 256, 0, s>>>(n, h, A.ptr.p, A.col.p, A.val.p, d.p, eps2, cnt.p,
+    k_strength_edges<<<grid, 256, 0, s>>>(n, h, A.ptr.p, A.col.p, wblk.p, d.p, eps2, cnt.p,
                                           nullptr, nullptr);
     CK_LAUNCH();
     const int64_t ne = scan_counts(cnt.p, off.p, n, s);
     DevBuf<unsigned long long> keys(2 * ne + 1, s), keys2(2 * ne + 1, s);
-    k_strength_edges<<<grid, 256, 0, s>>>(n, h, A.ptr.p, A.col.p, A.val.p, d.p, eps2, nullptr,
+    k_strength_edges<<<grid, 256, 0, s>>>(n, h, A.ptr.p, A.col.p, wblk.p, d.p, eps2, nullptr,
                                           off.p, keys.p);
     CK_LAUNCH();
     int bits = 1;
@@ -981,8 +1031,10 @@ void tentative(const DevBuf<int> &agg, int64_t nnodes, int64_t naggs, int pbs, c
     Pt.alloc(nfine * k, s);
     Bc.alloc(naggs * k * k, s);
     DevBuf<double> work(nfine * k, s), Qw(nfine * k, s);
-    k_tentative_qr<<<ceil_div(naggs, 128), 128, 0, s>>>(naggs, pbs, k, nodes.p, agg_ptr.p, B,
-                                                         nfine, work.p, Qw.p, Pt.p, Bc.p, err);
+    k_tentative_qr<<<ceil_div(naggs * kQrLanes, 256), 256, 0, s>>>(naggs, pbs, k, nodes.p,
+                                                                   agg_ptr.p, B, nfine, work.p,
+                                                                   Qw.p, Pt.p, Bc.p);
+    (void)err;
     CK_LAUNCH();
 }
 
