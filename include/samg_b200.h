@@ -233,6 +233,30 @@ SAMG_API int samg_dist_pack(const samg_dist *d, const double *d_x,
 SAMG_API int samg_dist_spmv(const samg_dist *d, int part, double alpha,
         const double *d_xext, double beta, double *d_y, void *stream);
 
+/* ---- multi-GPU solve (one process per GPU, NCCL) ----
+ * Every rank passes the same global fine matrix and nullspace; the
+ * hierarchy is built on every rank (bit-identical), then each rank keeps its
+ * rows of the levels with >= min_rows*nranks block rows (fine block rows
+ * row_starts[rank]..row_starts[rank+1]; coarse rows follow the aggregates'
+ * seeds), the smaller levels are replicated.  The V-cycle exchanges halos
+ * with ncclSend/ncclRecv and CG all-reduces its dot products.  f and u are
+ * the rank's rows (3 per block row).  Obtain the NCCL id on rank 0 with
+ * samg_nccl_unique_id and broadcast it with your own transport. */
+typedef struct samg_dhierarchy samg_dhierarchy;
+SAMG_API int samg_nccl_unique_id(unsigned char id[128]);
+SAMG_API int samg_dsetup(const unsigned char id[128], int nranks, int rank,
+        int64_t nbrows, const int64_t *ptr, const int64_t *col,
+        const double *val, const double *B, int64_t b_rows, int64_t b_cols,
+        const int64_t *row_starts, int64_t min_rows, int pipeline,
+        const samg_amg_params *prm, samg_dhierarchy **out);
+SAMG_API int samg_ddestroy(samg_dhierarchy *h);
+SAMG_API int samg_dinfo(const samg_dhierarchy *h, int64_t *row0,
+        int64_t *row1, int *nlevels, int *dist_levels, double *setup_seconds);
+SAMG_API int samg_dcg_solve_device(samg_dhierarchy *h, const double *d_f,
+        double *d_u, const samg_cg_params *prm, samg_solve_report *rep);
+SAMG_API int samg_dcg_solve(samg_dhierarchy *h, const double *f, double *u,
+        const samg_cg_params *prm, samg_solve_report *rep);
+
 /* ---- synthetic problems (input tooling; elasticity.hpp:38-213 extended) -- */
 enum samg_dirichlet { SAMG_DIRICHLET_NONE = 0, SAMG_DIRICHLET_KEEP_ROWS = 1,
                       SAMG_DIRICHLET_ELIMINATE = 2 };

@@ -135,6 +135,13 @@ PROTOTYPES = {
     "samg_dist_to_device": ([vp, C.c_int, C.c_int], C.c_int),
     "samg_dist_pack": ([vp, vp, vp, vp], C.c_int),
     "samg_dist_spmv": ([vp, C.c_int, C.c_double, vp, C.c_double, vp, vp], C.c_int),
+    "samg_nccl_unique_id": ([C.POINTER(C.c_ubyte)], C.c_int),
+    "samg_dsetup": ([C.POINTER(C.c_ubyte), C.c_int, C.c_int, i64, i64p, i64p, f64p, f64p, i64,
+                     i64, i64p, i64, C.c_int, C.POINTER(AmgParamsC), C.POINTER(vp)], C.c_int),
+    "samg_ddestroy": ([vp], C.c_int),
+    "samg_dinfo": ([vp, i64p, i64p, C.POINTER(C.c_int), C.POINTER(C.c_int), f64p], C.c_int),
+    "samg_dcg_solve_device": ([vp, vp, vp, C.POINTER(CgParamsC), C.POINTER(ReportC)], C.c_int),
+    "samg_dcg_solve": ([vp, f64p, f64p, C.POINTER(CgParamsC), C.POINTER(ReportC)], C.c_int),
 }
 
 

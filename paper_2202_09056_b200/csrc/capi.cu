@@ -30,7 +30,22 @@ struct samg_hierarchy {
 namespace samgb {
 samg_problem *generate_hex(const samg_problem_params &p);
 void rigid_body_modes(int64_t nnodes, const double *xyz, double *B);
+struct DHierarchy;
+DHierarchy *dsetup_all(const unsigned char *id, int nranks, int rank, Bsr3 &&A0,
+                       const double *B, int64_t b_rows, int64_t b_cols,
+                       const int64_t *row_starts, int64_t min_rows, const samg_amg_params &prm,
+                       cudaStream_t s, double t0);
+void ddelete(DHierarchy *d);
+samg_solve_report dcg(DHierarchy *d, const double *f, double *u, const samg_cg_params &cp,
+                      bool host);
+void dinfo(const DHierarchy *d, int64_t *row0, int64_t *row1, int *nlevels, int *dist_levels,
+           double *setup_s);
+void nccl_unique_id(unsigned char *out);
 }
+
+struct samg_dhierarchy {
+    samgb::DHierarchy *d = nullptr;
+};
 
 
 namespace {
@@ -655,6 +670,74 @@ SAMG_API int samg_rigid_body_modes(int64_t nnodes, const double *xyz, double *B)
     return guarded([&] {
         require(xyz && B && nnodes >= 0, SAMG_INVALID_ARGUMENT, "rigid_body_modes: bad arguments");
         rigid_body_modes(nnodes, xyz, B);
+    });
+}
+
+SAMG_API int samg_nccl_unique_id(unsigned char id[128]) {
+    return guarded([&] {
+        require(id != nullptr, SAMG_INVALID_ARGUMENT, "NULL id");
+        nccl_unique_id(id);
+    });
+}
+
+SAMG_API int samg_dsetup(const unsigned char id[128], int nranks, int rank, int64_t nbrows,
+                         const int64_t *ptr, const int64_t *col, const double *val,
+                         const double *B, int64_t b_rows, int64_t b_cols,
+                         const int64_t *row_starts, int64_t min_rows, int pipeline,
+                         const samg_amg_params *prm, samg_dhierarchy **out) {
+    return guarded([&] {
+        const double t0 = now_s();
+        require(out && id && nranks >= 1 && rank >= 0 && rank < nranks, SAMG_INVALID_ARGUMENT,
+                "dsetup: bad arguments");
+        *out = nullptr;
+        validate_params(prm, pipeline);
+        validate_ns(3 * nbrows, B, b_rows, b_cols);
+        need_device(prm->device);
+        cudaStream_t s = new_stream();
+        try {
+            Bsr3 A0;
+            upload_bsr3(nbrows, nbrows, ptr, col, val, A0, s);
+            auto h = std::make_unique<samg_dhierarchy>();
+            h->d = dsetup_all(id, nranks, rank, std::move(A0), B, b_rows, b_cols, row_starts,
+                              min_rows > 0 ? min_rows : 4096, *prm, s, t0);
+            *out = h.release();
+        } catch (...) {
+            cudaStreamSynchronize(s);
+            cudaStreamDestroy(s);
+            throw;
+        }
+    });
+}
+
+SAMG_API int samg_ddestroy(samg_dhierarchy *h) {
+    return guarded([&] {
+        if (!h) return;
+        ddelete(h->d);
+        delete h;
+    });
+}
+
+SAMG_API int samg_dinfo(const samg_dhierarchy *h, int64_t *row0, int64_t *row1, int *nlevels,
+                        int *dist_levels, double *setup_s) {
+    return guarded([&] {
+        require(h && h->d, SAMG_INVALID_ARGUMENT, "NULL hierarchy");
+        dinfo(h->d, row0, row1, nlevels, dist_levels, setup_s);
+    });
+}
+
+SAMG_API int samg_dcg_solve_device(samg_dhierarchy *h, const double *d_f, double *d_u,
+                                   const samg_cg_params *prm, samg_solve_report *rep) {
+    return guarded([&] {
+        require(h && h->d && d_f && d_u && prm && rep, SAMG_INVALID_ARGUMENT, "dcg: NULL argument");
+        *rep = dcg(h->d, d_f, d_u, *prm, false);
+    });
+}
+
+SAMG_API int samg_dcg_solve(samg_dhierarchy *h, const double *f, double *u,
+                            const samg_cg_params *prm, samg_solve_report *rep) {
+    return guarded([&] {
+        require(h && h->d && f && u && prm && rep, SAMG_INVALID_ARGUMENT, "dcg: NULL argument");
+        *rep = dcg(h->d, f, u, *prm, true);
     });
 }
 

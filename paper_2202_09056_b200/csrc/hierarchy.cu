@@ -96,7 +96,8 @@ Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int6
         Graph G;
         strength_graph(Li.A, h, prm.eps_strong, G, s);
         DevBuf<int> agg;
-        const int64_t naggs = aggregate(G, agg, s);
+        DevBuf<int> seedno;
+        const int64_t naggs = aggregate(G, agg, s, &seedno);
         DevBuf<double> Pt, Bc;
         tentative(agg, G.nnodes, naggs, pbs, B.p, k, Pt, Bc, err, s);
         Bsr3 P;
@@ -120,6 +121,7 @@ Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int6
         Li.agg = std::move(agg);
         Li.nnodes = G.nnodes;
         Li.naggs = naggs;
+        Li.seedno = std::move(seedno);
         B = std::move(Bc);
         b_rows = naggs * k;
         H->levels.emplace_back();
@@ -160,20 +162,27 @@ Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int6
 // With fuse_rz (inside CG) the last level-0 sweep also forms r.z and
 // finishes the CG beta update; returns whether it did.
 bool Hierarchy::vcycle(const double *f0, double *u0, bool zero_guess, bool fuse_rz) {
+    return vcycle_from(0, f0, u0, zero_guess, fuse_rz);
+}
+
+// The V-cycle restricted to levels start..L-1 (f0, u0 live on level
+// `start`); the multi-GPU driver runs the replicated coarse levels this way.
+bool Hierarchy::vcycle_from(size_t start, const double *f0, double *u0, bool zero_guess,
+                            bool fuse_rz) {
     cudaStream_t s = stream;
     const size_t L = levels.size();
-    if (L == 1) {
+    if (start + 1 >= L) {
         launch_dense_gemv(nc, Ainv.p, f0, u0, s);
         return false;
     }
     bool fused = false;
     std::vector<double *> cur(L);
-    for (size_t i = 0; i + 1 < L; ++i) {
+    for (size_t i = start; i + 1 < L; ++i) {
         Level &lv = levels[i];
-        const double *fi = i == 0 ? f0 : lv.f.p;
+        const double *fi = i == start ? f0 : lv.f.p;
         double *a = lv.u.p, *b = lv.t.p;
         int sweeps = prm.pre_sweeps;
-        const bool zero = (i > 0) || zero_guess;
+        const bool zero = (i > start) || zero_guess;
         if (!zero) CK(cudaMemcpyAsync(a, u0, sizeof(double) * 3 * lv.A.nrows, cudaMemcpyDeviceToDevice, s));
         if (zero) {
             if (sweeps > 0) {
@@ -193,14 +202,14 @@ bool Hierarchy::vcycle(const double *f0, double *u0, bool zero_guess, bool fuse_
     }
     launch_dense_gemv(nc, Ainv.p, levels[L - 1].f.p, levels[L - 1].u.p, s);
     cur[L - 1] = levels[L - 1].u.p;
-    for (size_t ii = L - 1; ii-- > 0;) {
+    for (size_t ii = L - 1; ii-- > start;) {
         Level &lv = levels[ii];
-        const double *fi = ii == 0 ? f0 : lv.f.p;
+        const double *fi = ii == start ? f0 : lv.f.p;
         double *a = cur[ii];
         double *b = (a == lv.u.p) ? lv.t.p : lv.u.p;
         launch_spmv(lv.P, 1.0, cur[ii + 1], 1.0, a, s);
         for (int sw = prm.post_sweeps; sw > 0; --sw) {
-            const bool last0 = ii == 0 && sw == 1;
+            const bool last0 = ii == start && sw == 1;
             double *out = last0 ? u0 : b;
             if (last0 && fuse_rz) {
                 launch_smooth_dot(lv.A, lv.M, fi, a, out, partials.p, sc.p, s);
@@ -213,8 +222,9 @@ bool Hierarchy::vcycle(const double *f0, double *u0, bool zero_guess, bool fuse_
         }
         cur[ii] = a;
     }
-    if (cur[0] != u0)
-        CK(cudaMemcpyAsync(u0, cur[0], sizeof(double) * finest_dim(), cudaMemcpyDeviceToDevice, s));
+    if (cur[start] != u0)
+        CK(cudaMemcpyAsync(u0, cur[start], sizeof(double) * 3 * levels[start].A.nrows,
+                           cudaMemcpyDeviceToDevice, s));
     return fused;
 }
 

@@ -13,6 +13,8 @@ struct Level {
     bool has_transfer = false;
     Smoother M;                // absent on the coarsest level
     DevBuf<int> agg;           // aggregate id per node (parity tap)
+    DevBuf<int> seedno;        // #pass-1 seeds before each node (nnodes+1):
+                               // aggregate ids are assigned in seed order
     int64_t nnodes = 0, naggs = 0;
     DevBuf<double> f, u, r, t; // V-cycle workspace (vcycle_workspace, hierarchy.hpp:152-163)
 };
@@ -40,6 +42,8 @@ struct Hierarchy {
     uint64_t memory_footprint() const;
 
     bool vcycle(const double *f, double *u, bool zero_guess, bool fuse_rz = false);
+    bool vcycle_from(size_t start, const double *f, double *u, bool zero_guess,
+                     bool fuse_rz = false);
     samg_solve_report cg(const double *d_f, double *d_u, const samg_cg_params &prm);
 };
 

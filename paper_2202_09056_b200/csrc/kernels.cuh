@@ -55,7 +55,9 @@ void launch_dense_gemv(int64_t n, const double *Ainv, const double *f, double *u
 
 // CG device scalars (cg.hpp:39-83).
 struct CgScalars {
-    double pq, rho, rho_new, rr, alpha, beta, norm_f, tol;
+    double pq, rho, rho_new, rr, alpha, beta;
+    double tmp;  // raw local sum (CG_STORE) awaiting a cross-rank allreduce
+    double norm_f, tol;
     int breakdown, iter, max_iter;
     unsigned ticket;  // last-CTA counter of the fused reductions
 };
@@ -64,14 +66,18 @@ struct CgScalars {
 // and applies: RR: rr; PQ: pq, alpha = rho/pq, breakdown if pq <= 0;
 // RZ: beta = rz/rho, rho = rz; RHO: rho; RR_LOOP: rr, ++iter and the graph
 // loop condition ||r||/||f|| > tol && iter < max && !breakdown.
-enum { CG_RR = 0, CG_PQ = 1, CG_RZ = 2, CG_RHO = 3, CG_RR_LOOP = 4 };
+// STORE: only tmp = s (multi-GPU: allreduce tmp, then launch_cg_finish).
+enum { CG_RR = 0, CG_PQ = 1, CG_RZ = 2, CG_RHO = 3, CG_RR_LOOP = 4, CG_STORE = 5 };
+// apply `what` to sc->tmp (after the allreduce of the partial sums)
+void launch_cg_finish(CgScalars *sc, int what, cudaStream_t s);
 constexpr int kRedBlocks = 592;   // 4 x 148 SMs: fixed => deterministic sums
 // q = A p fused with p.q (cg.hpp:63-64) -> PQ
 void launch_spmv_dot(const Bsr3 &A, const double *p, double *q, double *partials,
-                     CgScalars *sc, cudaStream_t s);
+                     CgScalars *sc, cudaStream_t s, int what = CG_PQ);
 // last post-smoothing sweep of the V-cycle fused with r.z (cg.hpp:73-75) -> RZ
 void launch_smooth_dot(const Bsr3 &A, const Smoother &M, const double *f, const double *u,
-                       double *u_out, double *partials, CgScalars *sc, cudaStream_t s);
+                       double *u_out, double *partials, CgScalars *sc, cudaStream_t s,
+                       int what = CG_RZ);
 // x.y -> what
 void launch_dot(int64_t n, const double *x, const double *y, double *partials, CgScalars *sc,
                 int what, cudaStream_t s);
@@ -96,7 +102,8 @@ void scalar_to_bsr3(int64_t n, const int64_t *d_ptr, const int64_t *d_col, const
 // strength graph on nodes of h block rows (coarsening.hpp:52-123)
 void strength_graph(const Bsr3 &A, int h, double eps_strong, Graph &G, cudaStream_t s);
 // aggregation (coarsening.hpp:131-160); returns the aggregate count
-int64_t aggregate(const Graph &G, DevBuf<int> &agg, cudaStream_t s);
+// seedno (optional out): #pass-1 seeds before each node, nnodes+1 entries
+int64_t aggregate(const Graph &G, DevBuf<int> &agg, cudaStream_t s, DevBuf<int> *seedno = nullptr);
 // tentative prolongation with QR of the nullspace (coarsening.hpp:238-312):
 // Pt[nfine*k] row values (columns agg*k + c), Bc column-major (naggs*k)-by-k
 void tentative(const DevBuf<int> &agg, int64_t nnodes, int64_t naggs, int pbs, const double *B,

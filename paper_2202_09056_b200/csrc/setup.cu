@@ -945,7 +945,7 @@ void strength_graph(const Bsr3 &A, int h, double eps_strong, Graph &G, cudaStrea
     for_each(nu, [=] __device__(int64_t e) { gc[e] = static_cast<int>(kp[e] & 0xffffffffULL); }, s);
 }
 
-int64_t aggregate(const Graph &G, DevBuf<int> &agg, cudaStream_t s) {
+int64_t aggregate(const Graph &G, DevBuf<int> &agg, cudaStream_t s, DevBuf<int> *seedno_out) {
     const int n = static_cast<int>(G.nnodes);
     agg.alloc(n, s);
     if (n == 0) return 0;
@@ -1005,6 +1005,7 @@ int64_t aggregate(const Graph &G, DevBuf<int> &agg, cudaStream_t s) {
         CK(cudaStreamSynchronize(s));
     }
     for_each(n, [=] __device__(int64_t i) { if (id[i] < 0) id[i] = id[par[i]]; }, s);
+    if (seedno_out) *seedno_out = std::move(seedno);
     return count;
 }
 

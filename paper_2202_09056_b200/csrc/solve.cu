@@ -281,6 +281,7 @@ __device__ void cg_apply(int what, double s, CgScalars *sc, cudaGraphConditional
             sc->rho = s;
             break;
         case CG_RHO: sc->rho = s; break;
+        case CG_STORE: sc->tmp = s; break;
         case CG_RR_LOOP: {
             sc->rr = s;
             const int it = sc->iter + 1;
@@ -561,6 +562,8 @@ __global__ void k_fill(int64_t n, double v, double *x) {
         x[i] = v;
 }
 
+__global__ void k_cg_finish(CgScalars *sc, int what) { cg_apply(what, sc->tmp, sc, 0); }
+
 int vec_grid(int64_t n) {
     const int64_t g = (n + 255) / 256;
     return static_cast<int>(g < kRedBlocks ? (g > 0 ? g : 1) : kRedBlocks);
@@ -608,16 +611,16 @@ void launch_smooth_zero(int64_t nrows, const Smoother &M, const double *f, doubl
 }
 
 void launch_spmv_dot(const Bsr3 &A, const double *p, double *q, double *partials,
-                     CgScalars *sc, cudaStream_t s) {
-    launch_reduce(A, p, EpiDot{p, q}, partials, sc, CG_PQ, s);
+                     CgScalars *sc, cudaStream_t s, int what) {
+    launch_reduce(A, p, EpiDot{p, q}, partials, sc, what, s);
 }
 
 void launch_smooth_dot(const Bsr3 &A, const Smoother &M, const double *f, const double *u,
-                       double *u_out, double *partials, CgScalars *sc, cudaStream_t s) {
+                       double *u_out, double *partials, CgScalars *sc, cudaStream_t s, int what) {
     if (M.kind == SM_POINT)
-        launch_reduce(A, u, EpiSmoothPoint{f, u, M.data.p, u_out}, partials, sc, CG_RZ, s);
+        launch_reduce(A, u, EpiSmoothPoint{f, u, M.data.p, u_out}, partials, sc, what, s);
     else
-        launch_reduce(A, u, EpiSmoothBlock{f, u, M.data.p, u_out}, partials, sc, CG_RZ, s);
+        launch_reduce(A, u, EpiSmoothBlock{f, u, M.data.p, u_out}, partials, sc, what, s);
 }
 
 void launch_dense_gemv(int64_t n, const double *Ainv, const double *f, double *u,
@@ -643,6 +646,11 @@ void launch_cg_update(int64_t n, CgScalars *sc, const double *p, const double *q
 void launch_p_update(int64_t n, const CgScalars *sc, const double *z, double *p,
                      cudaStream_t s) {
     k_p_update<<<vec_grid(n / 2 + 1), 256, 0, s>>>(n, sc, z, p);
+    CK_LAUNCH();
+}
+
+void launch_cg_finish(CgScalars *sc, int what, cudaStream_t s) {
+    k_cg_finish<<<1, 1, 0, s>>>(sc, what);
     CK_LAUNCH();
 }
 

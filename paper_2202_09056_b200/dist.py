@@ -175,3 +175,89 @@ class Halo:
         for p, c, o in zip(self.rpeers, self.rcounts, self.roffs):
             ops.append(dist.P2POp(dist.irecv, self.x_ext[base + 3 * o:base + 3 * (o + c)], p))
         return dist.batch_isend_irecv(ops) if ops else []
+
+
+def _load_torch_nccl():
+    """The library resolves NCCL at first use from the libnccl.so.2 already in
+    the process (nccl_shim.cuh); importing torch first makes that torch's own
+    copy, so both share one NCCL."""
+    import torch  # noqa: F401
+
+
+def nccl_unique_id() -> bytes:
+    _load_torch_nccl()
+    buf = (C.c_ubyte * 128)()
+    check(lib.samg_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+class DistHierarchy:
+    """Multi-GPU ns_block hierarchy (samg_dsetup): every rank passes the same
+    global problem; the solve runs on the rank's rows with NCCL halos.  The
+    NCCL id is created on rank 0 and broadcast with torch.distributed."""
+
+    def __init__(self, nbrows, ptr, col, val, B, rank, nranks, dist=None, row_starts=None,
+                 min_rows=4096, prm=None, uid=None):
+        from .api import AmgParams, _nullspace
+        prm = prm or AmgParams()
+        _load_torch_nccl()
+        if uid is None:
+            obj = [nccl_unique_id() if rank == 0 else None]
+            if dist is not None and nranks > 1:
+                dist.broadcast_object_list(obj, src=0)
+            uid = obj[0]
+        idbuf = (C.c_ubyte * 128).from_buffer_copy(uid)
+        ptr, col = _i64(ptr), _i64(col)
+        val = np.ascontiguousarray(val, dtype=np.float64)
+        Bv, brows, k = _nullspace(B, 3 * nbrows)
+        rs = None if row_starts is None else _i64(row_starts)
+        pc = prm.c()
+        h = vp()
+        check(lib.samg_dsetup(idbuf, nranks, rank, nbrows, ptr.ctypes.data_as(i64p),
+                              col.ctypes.data_as(i64p), val.ctypes.data_as(f64p),
+                              Bv.ctypes.data_as(f64p), brows, k,
+                              rs.ctypes.data_as(i64p) if rs is not None else None, min_rows, 5,
+                              C.byref(pc), C.byref(h)))
+        self.h = h
+        self.rank, self.nranks = rank, nranks
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            try:
+                lib.samg_ddestroy(self.h)
+            except Exception:
+                pass
+            self.h = None
+
+    def close(self):
+        self.__del__()
+
+    def info(self):
+        r0, r1 = C.c_int64(), C.c_int64()
+        nl, dl = C.c_int(), C.c_int()
+        ss = C.c_double()
+        check(lib.samg_dinfo(self.h, C.byref(r0), C.byref(r1), C.byref(nl), C.byref(dl),
+                             C.byref(ss)))
+        return dict(row0=r0.value, row1=r1.value, nlevels=nl.value, dist_levels=dl.value,
+                    setup_seconds=ss.value)
+
+    def cg_solve(self, f_local, prm=None):
+        from ._lib import CgParamsC, ReportC
+        from .api import CgParams, _report
+        prm = prm or CgParams()
+        f = np.ascontiguousarray(f_local, dtype=np.float64)
+        u = np.zeros_like(f)
+        rep = ReportC()
+        cp = CgParamsC(prm.tol, prm.max_iterations)
+        check(lib.samg_dcg_solve(self.h, f.ctypes.data_as(f64p), u.ctypes.data_as(f64p),
+                                 C.byref(cp), C.byref(rep)))
+        return u, _report(rep)
+
+    def cg_solve_device(self, f_ptr, u_ptr, prm=None):
+        from ._lib import CgParamsC, ReportC
+        from .api import CgParams, _report
+        prm = prm or CgParams()
+        rep = ReportC()
+        cp = CgParamsC(prm.tol, prm.max_iterations)
+        check(lib.samg_dcg_solve_device(self.h, f_ptr, u_ptr, C.byref(cp), C.byref(rep)))
+        return _report(rep)

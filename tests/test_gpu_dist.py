@@ -80,3 +80,28 @@ def test_emulated_ranks_match_global_spmv(gpu, ref, world):
     yr = ref.spmv_bsr3(full.nbrows, full.nbrows, full.ptr, full.col, full.val.reshape(-1), x)
     assert np.abs(y - yg).max() <= 1e-14 * np.abs(yg).max()
     assert np.abs(y - yr).max() <= 1e-13 * np.abs(yr).max()
+
+
+@pytest.mark.parametrize("min_rows", [1, 10**7])
+def test_multi_gpu_solver_single_rank(gpu, min_rows):
+    """samg_dsetup / samg_dcg_solve on one rank (NCCL communicator of size
+    1): the partitioned V-cycle (all levels partitioned, or only the fine
+    one) must reproduce the single-GPU solve."""
+    from paper_2202_09056_b200.dist import DistHierarchy
+    pb = gpu
+    p = pb.generate_hex(nx=10, ny=8, nz=7, dirichlet="eliminate", load="traction_xend")
+    prm = pb.AmgParams(coarse_enough=150)
+    h = pb.setup_bsr3(p.nbrows, p.ptr, p.col, p.val.reshape(-1), p.nullspace(), "ns_block", prm)
+    u1, r1 = h.cg_solve(p.rhs)
+    dh = DistHierarchy(p.nbrows, p.ptr, p.col, p.val.reshape(-1), p.nullspace(), 0, 1,
+                       min_rows=min_rows, prm=prm)
+    inf = dh.info()
+    assert inf["row0"] == 0 and inf["row1"] == p.nbrows
+    assert 1 <= inf["dist_levels"] <= inf["nlevels"] - 1
+    if min_rows == 1:
+        assert inf["dist_levels"] == inf["nlevels"] - 1
+    u2, r2 = dh.cg_solve(p.rhs)
+    assert r2["converged"] and r1["converged"]
+    assert abs(r1["iterations"] - r2["iterations"]) <= 1
+    assert np.linalg.norm(u1 - u2) <= 1e-10 * np.linalg.norm(u1)
+    assert r2["relative_residual"] <= 1e-8 * 1.01
