@@ -241,7 +241,11 @@ SAMG_API int samg_dist_spmv(const samg_dist *d, int part, double alpha,
  * seeds), the smaller levels are replicated.  The V-cycle exchanges halos
  * with ncclSend/ncclRecv and CG all-reduces its dot products.  f and u are
  * the rank's rows (3 per block row).  Obtain the NCCL id on rank 0 with
- * samg_nccl_unique_id and broadcast it with your own transport. */
+ * samg_nccl_unique_id and broadcast it with your own transport.
+ * id == NULL emulates all nranks in the calling process on one GPU (no
+ * NCCL): every halo / all-reduce / gather becomes a device copy with the
+ * same offsets and counts, and f and u are the global vectors.  This is the
+ * single-GPU check of the partition and halo plans. */
 typedef struct samg_dhierarchy samg_dhierarchy;
 SAMG_API int samg_nccl_unique_id(unsigned char id[128]);
 SAMG_API int samg_dsetup(const unsigned char id[128], int nranks, int rank,

@@ -687,7 +687,7 @@ SAMG_API int samg_dsetup(const unsigned char id[128], int nranks, int rank, int6
                          const samg_amg_params *prm, samg_dhierarchy **out) {
     return guarded([&] {
         const double t0 = now_s();
-        require(out && id && nranks >= 1 && rank >= 0 && rank < nranks, SAMG_INVALID_ARGUMENT,
+        require(out && nranks >= 1 && rank >= 0 && rank < nranks, SAMG_INVALID_ARGUMENT,
                 "dsetup: bad arguments");
         *out = nullptr;
         validate_params(prm, pipeline);

@@ -8,16 +8,22 @@
 //     partition follows the aggregation: aggregate g belongs to the rank that
 //     owns its pass-1 seed node, and aggregate ids are numbered in seed order
 //     (coarsening.hpp:136-146), so every rank's coarse rows are contiguous;
-//   * levels l >= Ld (fewer than min_rows * nranks block rows) are replicated:
-//     f_Ld is gathered on every rank (grouped ncclBroadcast) and the coarse
-//     V-cycle runs redundantly, so the prolongation into level Ld-1 needs no
-//     halo.
+//   * levels l >= Ld (fewer than min_rows * nranks block rows, or a rank
+//     would own none) are replicated: f_Ld is gathered on every rank (grouped
+//     ncclBroadcast) and the coarse V-cycle runs redundantly, so the
+//     prolongation into level Ld-1 needs no halo.
 // Every local SpMV reads a halo-extended vector: owned entries first, then
 // the ghosts sorted by global id (grouped by owner).  Because all ranks hold
 // all matrices, each rank derives both sides of every halo plan locally (no
 // plan exchange).  A halo exchange is pack kernel + grouped ncclSend/ncclRecv
 // on the solve stream.  CG dot products are local fused reductions (the same
 // kernels as on one GPU, in STORE mode) + a one-double ncclAllReduce.
+//
+// The same code drives an *emulated* group (comm == nullptr): all ranks'
+// slices live in one process on one GPU and every communication step is
+// carried out, rank by rank in lock step, as device copies with exactly the
+// offsets and counts the NCCL calls use.  No kernel waits on another rank;
+// this is how the partition and halo plans are verified on a single GPU.
 #include "nccl_shim.cuh"
 
 #include <algorithm>
@@ -40,12 +46,26 @@ inline void nccl_check(ncclResult_t r, const char *what) {
 
 namespace {
 
+constexpr int kMaxEmulated = 16;
+
 __global__ void k_pack3(int64_t n, const int *idx, const double *x, double *buf) {
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < 3 * n;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t k = e / 3;
         buf[e] = x[3 * static_cast<int64_t>(idx[k]) + (e - 3 * k)];
     }
+}
+
+struct ScSet {
+    CgScalars *p[kMaxEmulated];
+    int n;
+};
+
+// emulated all-reduce of CgScalars::tmp (sum in rank order)
+__global__ void k_sum_tmp(ScSet s) {
+    double t = 0;
+    for (int i = 0; i < s.n; ++i) t += s.p[i]->tmp;
+    for (int i = 0; i < s.n; ++i) s.p[i]->tmp = t;
 }
 
 std::vector<int> download_int(const DevBuf<int> &b, size_t n, cudaStream_t s) {
@@ -59,6 +79,10 @@ int owner(const std::vector<int64_t> &starts, int64_t g) {
     return static_cast<int>(std::upper_bound(starts.begin(), starts.end(), g) - starts.begin()) - 1;
 }
 
+void d2d(double *dst, const double *src, int64_t n, cudaStream_t s) {
+    if (n > 0) CK(cudaMemcpyAsync(dst, src, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+}
+
 } // namespace
 
 // Halo plan of one local matrix: ghosts of its column space.
@@ -69,22 +93,24 @@ struct HaloPlan {
     DevBuf<int> send_idx;
     DevBuf<double> sendbuf;
 
-    void exchange(double *xext, ncclComm_t comm, cudaStream_t s) const {
+    void pack(const double *xext, cudaStream_t s) const {
         const int64_t ns = send_idx.n;
-        if (ns) {
-            int64_t g = (3 * ns + 255) / 256;
-            if (g > 4096) g = 4096;
-            k_pack3<<<static_cast<int>(g), 256, 0, s>>>(ns, send_idx.p, xext, sendbuf.p);
-            CK_LAUNCH();
-        }
+        if (!ns) return;
+        int64_t g = (3 * ns + 255) / 256;
+        if (g > 4096) g = 4096;
+        k_pack3<<<static_cast<int>(g), 256, 0, s>>>(ns, send_idx.p, xext, sendbuf.p);
+        CK_LAUNCH();
+    }
+
+    void post(double *xext, ncclComm_t comm, cudaStream_t s) const {
         if (send_peers.empty() && recv_peers.empty()) return;
         NK(nccl().GroupStart());
         for (size_t p = 0; p < send_peers.size(); ++p)
             NK(nccl().Send(sendbuf.p + 3 * send_offsets[p], 3 * send_counts[p], ncclDouble,
-                        send_peers[p], comm, s));
+                           send_peers[p], comm, s));
         for (size_t p = 0; p < recv_peers.size(); ++p)
             NK(nccl().Recv(xext + 3 * (nloc + recv_offsets[p]), 3 * recv_counts[p], ncclDouble,
-                        recv_peers[p], comm, s));
+                           recv_peers[p], comm, s));
         NK(nccl().GroupEnd());
     }
 };
@@ -167,133 +193,207 @@ void build_local(const std::vector<int> &hptr, const std::vector<int> &hcol, con
 }
 
 struct DLevel {
-    std::vector<int64_t> fstarts, cstarts;  // partitions of this level and the next
     LocalMat A, R, P;
-    bool next_replicated = false;
     Smoother M;
     DevBuf<double> f, uA, rR, t, uP;  // f, t: 3*nloc; uA/rR/uP: halo-extended
 };
 
-struct DHierarchy {
-    int rank = 0, nranks = 1, device = 0;
-    ncclComm_t comm = nullptr;
-    std::unique_ptr<Hierarchy> H;
+// The slices one rank owns.
+struct DRank {
+    int rank = 0;
+    int64_t row0 = 0, nloc0 = 0;
     std::vector<DLevel> dl;
-    size_t Ld = 0;
-    std::vector<int64_t> ld_starts;     // partition of level Ld (gather pieces)
-    DevBuf<double> fLd, uLd;            // replicated level-Ld vectors
+    DevBuf<double> fLd, uLd;  // replicated level-Ld vectors
     DevBuf<double> r, z, pext, q, u, uext;
     DevBuf<CgScalars> sc;
-    CgScalars *sc_host = nullptr;
     DevBuf<double> partials;
-    int64_t nloc0 = 0;
+};
+
+struct DHierarchy {
+    int nranks = 1, device = 0;
+    ncclComm_t comm = nullptr;   // nullptr: every rank emulated in this process
+    std::unique_ptr<Hierarchy> H;
+    size_t Ld = 0;
+    std::vector<std::vector<int64_t>> starts;  // partition of levels 0..Ld
+    std::vector<DRank> ranks;    // the ranks this process drives
+    CgScalars *sc_host = nullptr;
 
     ~DHierarchy() {
         if (H && H->stream) cudaStreamSynchronize(H->stream);
-        dl.clear();
+        ranks.clear();
         if (sc_host) cudaFreeHost(sc_host);
         if (comm) nccl().CommDestroy(comm);
     }
 
     cudaStream_t stream() const { return H->stream; }
+    bool emulated() const { return comm == nullptr; }
+
+    // Halo exchange of the level-l operator selected by `which` (0 A, 1 R,
+    // 2 P) into the extended vector `vec` of every driven rank.
+    template <class Vec>
+    void exchange(size_t l, int which, Vec vec) {
+        cudaStream_t s = stream();
+        auto plan = [&](DRank &R) -> const HaloPlan & {
+            DLevel &L = R.dl[l];
+            return which == 0 ? L.A.plan : which == 1 ? L.R.plan : L.P.plan;
+        };
+        for (DRank &R : ranks) plan(R).pack(vec(R), s);
+        if (!emulated()) {
+            plan(ranks[0]).post(vec(ranks[0]), comm, s);
+            return;
+        }
+        for (DRank &R : ranks) {
+            const HaloPlan &pl = plan(R);
+            double *x = vec(R);
+            for (size_t k = 0; k < pl.recv_peers.size(); ++k) {
+                const HaloPlan &ql = plan(ranks[pl.recv_peers[k]]);
+                const auto it = std::find(ql.send_peers.begin(), ql.send_peers.end(), R.rank);
+                if (it == ql.send_peers.end()) fail(SAMG_ERROR, "dsolve: unmatched halo receive");
+                const size_t i = it - ql.send_peers.begin();
+                if (ql.send_counts[i] != pl.recv_counts[k])
+                    fail(SAMG_ERROR, "dsolve: halo send/receive counts differ");
+                d2d(x + 3 * (pl.nloc + pl.recv_offsets[k]), ql.sendbuf.p + 3 * ql.send_offsets[i],
+                    3 * pl.recv_counts[k], s);
+            }
+        }
+    }
 
     // the sum over ranks of sc->tmp, then the CG update `what`
     void allreduce_finish(int what) {
         cudaStream_t s = stream();
-        double *t = reinterpret_cast<double *>(reinterpret_cast<char *>(sc.p) + offsetof(CgScalars, tmp));
-        NK(nccl().AllReduce(t, t, 1, ncclDouble, ncclSum, comm, s));
-        launch_cg_finish(sc.p, what, s);
+        if (!emulated()) {
+            double *t = reinterpret_cast<double *>(reinterpret_cast<char *>(ranks[0].sc.p) +
+                                                   offsetof(CgScalars, tmp));
+            NK(nccl().AllReduce(t, t, 1, ncclDouble, ncclSum, comm, s));
+        } else if (ranks.size() > 1) {
+            ScSet set{};
+            set.n = static_cast<int>(ranks.size());
+            for (int i = 0; i < set.n; ++i) set.p[i] = ranks[i].sc.p;
+            k_sum_tmp<<<1, 1, 0, s>>>(set);
+            CK_LAUNCH();
+        }
+        for (DRank &R : ranks) launch_cg_finish(R.sc.p, what, s);
     }
 
-    void vcycle(const double *f0, double *z0);
+    // every rank's piece of f_Ld to every rank
+    void gather_coarse() {
+        cudaStream_t s = stream();
+        const std::vector<int64_t> &st = starts[Ld];
+        if (!emulated()) {
+            double *f = ranks[0].fLd.p;
+            NK(nccl().GroupStart());
+            for (int q = 0; q < nranks; ++q) {
+                const int64_t o = 3 * st[q], c = 3 * (st[q + 1] - st[q]);
+                if (c) NK(nccl().Broadcast(f + o, f + o, c, ncclDouble, q, comm, s));
+            }
+            NK(nccl().GroupEnd());
+            return;
+        }
+        for (DRank &R : ranks)
+            for (const DRank &Q : ranks)
+                if (Q.rank != R.rank)
+                    d2d(R.fLd.p + 3 * st[Q.rank], Q.fLd.p + 3 * st[Q.rank],
+                        3 * (st[Q.rank + 1] - st[Q.rank]), s);
+    }
+
+    void vcycle();
     samg_solve_report cg(const double *d_f, double *d_u, const samg_cg_params &cp);
 };
 
-// Distributed V-cycle (hierarchy.hpp:408-441) from a zero guess.
-void DHierarchy::vcycle(const double *f0, double *z0) {
+// Distributed V-cycle (hierarchy.hpp:408-441) from a zero guess: z = M^-1 r
+// on every driven rank.
+void DHierarchy::vcycle() {
     cudaStream_t s = stream();
     const int pre = H->prm.pre_sweeps, post = H->prm.post_sweeps;
+    auto fin = [&](DRank &R, size_t l) -> const double * { return l == 0 ? R.r.p : R.dl[l].f.p; };
     for (size_t l = 0; l < Ld; ++l) {
-        DLevel &L = dl[l];
-        const int64_t nl = L.A.A.nrows;
-        const double *f = l == 0 ? f0 : L.f.p;
-        if (pre > 0) launch_smooth_zero(nl, L.M, f, L.uA.p, s);
-        else launch_fill(3 * nl, 0.0, L.uA.p, s);
+        for (DRank &R : ranks) {
+            DLevel &L = R.dl[l];
+            if (pre > 0) launch_smooth_zero(L.A.A.nrows, L.M, fin(R, l), L.uA.p, s);
+            else launch_fill(3 * L.A.A.nrows, 0.0, L.uA.p, s);
+        }
         for (int sw = 1; sw < pre; ++sw) {
-            L.A.plan.exchange(L.uA.p, comm, s);
-            launch_smooth(L.A.A, L.M, f, L.uA.p, L.t.p, s);
-            CK(cudaMemcpyAsync(L.uA.p, L.t.p, sizeof(double) * 3 * nl, cudaMemcpyDeviceToDevice, s));
+            exchange(l, 0, [&](DRank &R) { return R.dl[l].uA.p; });
+            for (DRank &R : ranks) {
+                DLevel &L = R.dl[l];
+                launch_smooth(L.A.A, L.M, fin(R, l), L.uA.p, L.t.p, s);
+                d2d(L.uA.p, L.t.p, 3 * L.A.A.nrows, s);
+            }
         }
-        L.A.plan.exchange(L.uA.p, comm, s);
-        launch_residual(L.A.A, f, L.uA.p, L.rR.p, s);
-        L.R.plan.exchange(L.rR.p, comm, s);
-        double *fc = (l + 1 < Ld) ? dl[l + 1].f.p : fLd.p + 3 * ld_starts[rank];
-        launch_spmv(L.R.A, 1.0, L.rR.p, 0.0, fc, s);
+        exchange(l, 0, [&](DRank &R) { return R.dl[l].uA.p; });
+        for (DRank &R : ranks) {
+            DLevel &L = R.dl[l];
+            launch_residual(L.A.A, fin(R, l), L.uA.p, L.rR.p, s);
+        }
+        exchange(l, 1, [&](DRank &R) { return R.dl[l].rR.p; });
+        for (DRank &R : ranks) {
+            DLevel &L = R.dl[l];
+            double *fc = (l + 1 < Ld) ? R.dl[l + 1].f.p : R.fLd.p + 3 * starts[Ld][R.rank];
+            launch_spmv(L.R.A, 1.0, L.rR.p, 0.0, fc, s);
+        }
     }
-    // gather f_Ld on every rank, coarse levels redundantly
-    NK(nccl().GroupStart());
-    for (int q = 0; q < nranks; ++q) {
-        const int64_t o = 3 * ld_starts[q], c = 3 * (ld_starts[q + 1] - ld_starts[q]);
-        if (c) NK(nccl().Broadcast(fLd.p + o, fLd.p + o, c, ncclDouble, q, comm, s));
-    }
-    NK(nccl().GroupEnd());
-    H->vcycle_from(Ld, fLd.p, uLd.p, true, false);
+    gather_coarse();
+    for (DRank &R : ranks) H->vcycle_from(Ld, R.fLd.p, R.uLd.p, true, false);
     for (size_t l = Ld; l-- > 0;) {
-        DLevel &L = dl[l];
-        const int64_t nl = L.A.A.nrows;
-        const double *f = l == 0 ? f0 : L.f.p;
-        const double *uc;
-        if (L.next_replicated) {
-            uc = uLd.p;
-        } else {
+        const bool next_replicated = l + 1 == Ld;
+        if (!next_replicated) {
             // level l+1's result (in its t or uA) -> local part of uP, then halo
-            const DLevel &N = dl[l + 1];
-            const double *src = post > 0 ? N.t.p : N.uA.p;
-            CK(cudaMemcpyAsync(L.uP.p, src, sizeof(double) * 3 * N.A.A.nrows,
-                               cudaMemcpyDeviceToDevice, s));
-            L.P.plan.exchange(L.uP.p, comm, s);
-            uc = L.uP.p;
+            for (DRank &R : ranks) {
+                const DLevel &N = R.dl[l + 1];
+                d2d(R.dl[l].uP.p, post > 0 ? N.t.p : N.uA.p, 3 * N.A.A.nrows, s);
+            }
+            exchange(l, 2, [&](DRank &R) { return R.dl[l].uP.p; });
         }
-        launch_spmv(L.P.A, 1.0, uc, 1.0, L.uA.p, s);
+        for (DRank &R : ranks) {
+            DLevel &L = R.dl[l];
+            launch_spmv(L.P.A, 1.0, next_replicated ? R.uLd.p : L.uP.p, 1.0, L.uA.p, s);
+        }
         for (int sw = 0; sw < post; ++sw) {
-            L.A.plan.exchange(L.uA.p, comm, s);
-            double *out = (l == 0 && sw == post - 1) ? z0 : L.t.p;
-            launch_smooth(L.A.A, L.M, f, L.uA.p, out, s);
-            if (sw + 1 < post)
-                CK(cudaMemcpyAsync(L.uA.p, out, sizeof(double) * 3 * nl, cudaMemcpyDeviceToDevice, s));
+            exchange(l, 0, [&](DRank &R) { return R.dl[l].uA.p; });
+            for (DRank &R : ranks) {
+                DLevel &L = R.dl[l];
+                double *out = (l == 0 && sw == post - 1) ? R.z.p : L.t.p;
+                launch_smooth(L.A.A, L.M, fin(R, l), L.uA.p, out, s);
+                if (sw + 1 < post) d2d(L.uA.p, out, 3 * L.A.A.nrows, s);
+            }
         }
         if (l == 0 && post == 0)
-            CK(cudaMemcpyAsync(z0, L.uA.p, sizeof(double) * 3 * nl, cudaMemcpyDeviceToDevice, s));
+            for (DRank &R : ranks) d2d(R.z.p, R.dl[0].uA.p, 3 * R.nloc0, s);
     }
 }
 
-// PCG (cg.hpp:39-112) on the row-partitioned fine level; host reads ||r||
-// once per iteration (identical decisions on every rank: all-reduced).
+// PCG (cg.hpp:39-112) on the row-partitioned fine level; the host reads the
+// (all-reduced, identical on every rank) scalars once per iteration.  d_f /
+// d_u are the rank's slices, or the global vectors of an emulated group.
 samg_solve_report DHierarchy::cg(const double *d_f, double *d_u, const samg_cg_params &cp) {
     cudaStream_t s = stream();
     const auto t0 = std::chrono::steady_clock::now();
     samg_solve_report rep{};
     rep.variant = SAMG_PIPELINE_NS_BLOCK;
     rep.setup_seconds = H->setup_seconds;
-    const int64_t n = 3 * nloc0;
-    const LocalMat &A0 = dl[0].A;
-    CK(cudaMemcpyAsync(r.p, d_f, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
-    launch_fill(n, 0.0, u.p, s);
-    CK(cudaMemsetAsync(sc.p, 0, sizeof(CgScalars), s));
+    const int64_t base0 = emulated() ? ranks[0].row0 : 0;
+    auto off = [&](const DRank &R) { return 3 * (R.row0 - base0); };
+    for (DRank &R : ranks) {
+        d2d(R.r.p, d_f + off(R), 3 * R.nloc0, s);
+        launch_fill(3 * R.nloc0, 0.0, R.u.p, s);
+        CK(cudaMemsetAsync(R.sc.p, 0, sizeof(CgScalars), s));
+    }
     auto read = [&] {
-        CK(cudaMemcpyAsync(sc_host, sc.p, sizeof(CgScalars), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(sc_host, ranks[0].sc.p, sizeof(CgScalars), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
     };
-    launch_dot(n, r.p, r.p, partials.p, sc.p, CG_STORE, s);
-    allreduce_finish(CG_RR);
+    auto dots = [&](auto x, auto y, int what) {
+        for (DRank &R : ranks) launch_dot(3 * R.nloc0, x(R), y(R), R.partials.p, R.sc.p, CG_STORE, s);
+        allreduce_finish(what);
+    };
+    dots([](DRank &R) { return R.r.p; }, [](DRank &R) { return R.r.p; }, CG_RR);
     read();
     const double norm_f = std::sqrt(sc_host->rr);
     auto finish = [&](double res) {
         rep.relative_residual = res;
         rep.preconditioner_bytes = H->memory_footprint();
         rep.solve_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-        if (d_u != u.p)
-            CK(cudaMemcpyAsync(d_u, u.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+        for (DRank &R : ranks) d2d(d_u + off(R), R.u.p, 3 * R.nloc0, s);
         CK(cudaStreamSynchronize(s));
     };
     if (norm_f == 0.0) {
@@ -301,17 +401,23 @@ samg_solve_report DHierarchy::cg(const double *d_f, double *d_u, const samg_cg_p
         finish(0.0);
         return rep;
     }
-    vcycle(r.p, z.p);
-    launch_dot(n, r.p, z.p, partials.p, sc.p, CG_STORE, s);
-    allreduce_finish(CG_RHO);
-    CK(cudaMemcpyAsync(pext.p, z.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    auto precondition = [&] {
+        vcycle();
+        dots([](DRank &R) { return R.r.p; }, [](DRank &R) { return R.z.p; }, CG_RZ);
+    };
+    vcycle();
+    dots([](DRank &R) { return R.r.p; }, [](DRank &R) { return R.z.p; }, CG_RHO);
+    for (DRank &R : ranks) d2d(R.pext.p, R.z.p, 3 * R.nloc0, s);
     double res_norm = norm_f;
     int iter = 0;
     while (res_norm / norm_f > cp.tol && iter < cp.max_iterations) {
-        A0.plan.exchange(pext.p, comm, s);
-        launch_spmv_dot(A0.A, pext.p, q.p, partials.p, sc.p, s, CG_STORE);
+        exchange(0, 0, [](DRank &R) { return R.pext.p; });
+        for (DRank &R : ranks)
+            launch_spmv_dot(R.dl[0].A.A, R.pext.p, R.q.p, R.partials.p, R.sc.p, s, CG_STORE);
         allreduce_finish(CG_PQ);
-        launch_cg_update(n, sc.p, pext.p, q.p, u.p, r.p, partials.p, CG_STORE, 0, s);
+        for (DRank &R : ranks)
+            launch_cg_update(3 * R.nloc0, R.sc.p, R.pext.p, R.q.p, R.u.p, R.r.p, R.partials.p,
+                             CG_STORE, 0, s);
         allreduce_finish(CG_RR);
         read();
         if (sc_host->breakdown)
@@ -319,97 +425,108 @@ samg_solve_report DHierarchy::cg(const double *d_f, double *d_u, const samg_cg_p
         ++iter;
         res_norm = std::sqrt(sc_host->rr);
         if (res_norm / norm_f <= cp.tol) break;
-        vcycle(r.p, z.p);
-        launch_dot(n, r.p, z.p, partials.p, sc.p, CG_STORE, s);
-        allreduce_finish(CG_RZ);
-        launch_p_update(n, sc.p, z.p, pext.p, s);
+        precondition();
+        for (DRank &R : ranks) launch_p_update(3 * R.nloc0, R.sc.p, R.z.p, R.pext.p, s);
     }
     rep.iterations = iter;
     rep.converged = res_norm / norm_f <= cp.tol;
     // true residual (cg.hpp:105-108)
-    CK(cudaMemcpyAsync(uext.p, u.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
-    A0.plan.exchange(uext.p, comm, s);
-    launch_residual(A0.A, d_f, uext.p, q.p, s);
-    launch_dot(n, q.p, q.p, partials.p, sc.p, CG_STORE, s);
-    allreduce_finish(CG_RR);
+    for (DRank &R : ranks) d2d(R.uext.p, R.u.p, 3 * R.nloc0, s);
+    exchange(0, 0, [](DRank &R) { return R.uext.p; });
+    for (DRank &R : ranks) launch_residual(R.dl[0].A.A, d_f + off(R), R.uext.p, R.q.p, s);
+    dots([](DRank &R) { return R.q.p; }, [](DRank &R) { return R.q.p; }, CG_RR);
     read();
     finish(std::sqrt(sc_host->rr) / norm_f);
     return rep;
 }
 
-// Build the distributed hierarchy from a full (redundant) single-GPU one.
-DHierarchy *dsetup(std::unique_ptr<Hierarchy> H, ncclComm_t comm, int nranks, int rank,
-                   const std::vector<int64_t> &row_starts, int64_t min_rows) {
+// Build the distributed hierarchy from a full (redundant) single-GPU one for
+// the ranks `mine` (one rank with NCCL, all of them when emulated).
+DHierarchy *dsetup(std::unique_ptr<Hierarchy> H, ncclComm_t comm, int nranks,
+                   const std::vector<int> &mine, const std::vector<int64_t> &row_starts,
+                   int64_t min_rows) {
     auto D = std::make_unique<DHierarchy>();
-    D->rank = rank;
     D->nranks = nranks;
-    D->comm = comm;
     D->device = H->device;
     cudaStream_t s = H->stream;
     const size_t L = H->levels.size();
-    // number of partitioned levels: all levels with a transfer operator that
-    // are large enough (the coarsest level is always replicated)
     if (L < 2) fail(SAMG_UNSUPPORTED, "multi-GPU solve needs at least two levels");
-    size_t Ld = 0;
-    while (Ld + 1 < L && H->levels[Ld].A.nrows >= min_rows * nranks) ++Ld;
-    Ld = std::max<size_t>(Ld, 1);  // the fine level is always partitioned
-    D->Ld = Ld;
-    std::vector<int64_t> fst = row_starts;
-    for (size_t l = 0; l < Ld; ++l) {
-        Level &lv = H->levels[l];
-        DLevel dlv;
-        dlv.fstarts = fst;
-        // coarse partition through the seeds of the aggregation
+    // partition chain: level l+1's rows follow the seeds of level l's aggregation
+    std::vector<std::vector<int64_t>> st{row_starts};
+    size_t Ld = 1;  // the fine level is always partitioned
+    for (size_t l = 0; l + 1 < L; ++l) {
+        const Level &lv = H->levels[l];
         const int h = l == 0 ? 1 : 2;  // block rows per node (pbs 3 / 6)
         const int64_t kb = lv.naggs ? lv.P.ncols / lv.naggs : 2;
-        std::vector<int> seedno = download_int(lv.seedno, lv.nnodes + 1, s);
+        const std::vector<int> seedno = download_int(lv.seedno, lv.nnodes + 1, s);
         std::vector<int64_t> cst(nranks + 1);
-        for (int q = 0; q <= nranks; ++q) cst[q] = kb * seedno[fst[q] / h];
-        dlv.cstarts = cst;
-        dlv.next_replicated = l + 1 >= Ld;
-        std::vector<int> ap = download_int(lv.A.ptr, lv.A.nrows + 1, s);
-        std::vector<int> ac = download_int(lv.A.col, lv.A.nnzb, s);
-        build_local(ap, ac, lv.A.val.p, fst, fst, rank, false, lv.A.ncols, dlv.A, s);
-        std::vector<int> rp = download_int(lv.R.ptr, lv.R.nrows + 1, s);
-        std::vector<int> rc = download_int(lv.R.col, lv.R.nnzb, s);
-        build_local(rp, rc, lv.R.val.p, cst, fst, rank, false, lv.R.ncols, dlv.R, s);
-        std::vector<int> pp = download_int(lv.P.ptr, lv.P.nrows + 1, s);
-        std::vector<int> pc = download_int(lv.P.col, lv.P.nnzb, s);
-        build_local(pp, pc, lv.P.val.p, fst, cst, rank, dlv.next_replicated, lv.P.ncols, dlv.P, s);
-        // smoother rows
-        const int per = lv.M.kind == SM_POINT ? 3 : 9;
-        const int64_t f0 = fst[rank], nl = fst[rank + 1] - f0;
-        dlv.M.kind = lv.M.kind;
-        dlv.M.data.alloc(per * nl + 1, s);
-        if (nl)
-            CK(cudaMemcpyAsync(dlv.M.data.p, lv.M.data.p + per * f0, sizeof(double) * per * nl,
-                               cudaMemcpyDeviceToDevice, s));
-        dlv.f.alloc(3 * nl + 3, s);
-        dlv.t.alloc(3 * nl + 3, s);
-        dlv.uA.alloc(3 * (dlv.A.plan.nloc + dlv.A.plan.nghost) + 3, s);
-        dlv.rR.alloc(3 * (dlv.R.plan.nloc + dlv.R.plan.nghost) + 3, s);
-        if (!dlv.next_replicated) dlv.uP.alloc(3 * (dlv.P.plan.nloc + dlv.P.plan.nghost) + 3, s);
-        D->dl.push_back(std::move(dlv));
-        fst = cst;
+        for (int q = 0; q <= nranks; ++q) cst[q] = kb * seedno[st[l][q] / h];
+        st.push_back(cst);
+        // level l+1 is partitioned too if it is not the coarsest, large
+        // enough, and gives every rank at least one row
+        bool part = l + 2 < L && H->levels[l + 1].A.nrows >= min_rows * nranks;
+        for (int q = 0; q < nranks && part; ++q) part = cst[q + 1] > cst[q];
+        if (!part) break;
+        Ld = l + 2;
     }
-    D->ld_starts = fst;  // partition of level Ld (from the last partitioned level)
+    D->Ld = Ld;
+    D->starts = st;
+    D->ranks.resize(mine.size());
+    for (size_t i = 0; i < mine.size(); ++i) {
+        DRank &R = D->ranks[i];
+        R.rank = mine[i];
+        R.row0 = row_starts[R.rank];
+        R.nloc0 = row_starts[R.rank + 1] - R.row0;
+        R.dl.resize(Ld);
+    }
+    for (size_t l = 0; l < Ld; ++l) {
+        Level &lv = H->levels[l];
+        const std::vector<int64_t> &fst = st[l], &cst = st[l + 1];
+        const bool next_replicated = l + 1 == Ld;
+        const std::vector<int> ap = download_int(lv.A.ptr, lv.A.nrows + 1, s);
+        const std::vector<int> ac = download_int(lv.A.col, lv.A.nnzb, s);
+        const std::vector<int> rp = download_int(lv.R.ptr, lv.R.nrows + 1, s);
+        const std::vector<int> rc = download_int(lv.R.col, lv.R.nnzb, s);
+        const std::vector<int> pp = download_int(lv.P.ptr, lv.P.nrows + 1, s);
+        const std::vector<int> pc = download_int(lv.P.col, lv.P.nnzb, s);
+        const int per = lv.M.kind == SM_POINT ? 3 : 9;
+        for (DRank &R : D->ranks) {
+            DLevel &dlv = R.dl[l];
+            build_local(ap, ac, lv.A.val.p, fst, fst, R.rank, false, lv.A.ncols, dlv.A, s);
+            build_local(rp, rc, lv.R.val.p, cst, fst, R.rank, false, lv.R.ncols, dlv.R, s);
+            build_local(pp, pc, lv.P.val.p, fst, cst, R.rank, next_replicated, lv.P.ncols, dlv.P, s);
+            const int64_t f0 = fst[R.rank], nl = fst[R.rank + 1] - f0;
+            dlv.M.kind = lv.M.kind;
+            dlv.M.data.alloc(per * nl + 1, s);
+            if (nl)
+                CK(cudaMemcpyAsync(dlv.M.data.p, lv.M.data.p + per * f0, sizeof(double) * per * nl,
+                                   cudaMemcpyDeviceToDevice, s));
+            dlv.f.alloc(3 * nl + 3, s);
+            dlv.t.alloc(3 * nl + 3, s);
+            dlv.uA.alloc(3 * (dlv.A.plan.nloc + dlv.A.plan.nghost) + 3, s);
+            dlv.rR.alloc(3 * (dlv.R.plan.nloc + dlv.R.plan.nghost) + 3, s);
+            if (!next_replicated) dlv.uP.alloc(3 * (dlv.P.plan.nloc + dlv.P.plan.nghost) + 3, s);
+        }
+    }
     const int64_t nLd = H->levels[Ld].A.nrows;
-    D->fLd.alloc(3 * nLd + 3, s);
-    D->uLd.alloc(3 * nLd + 3, s);
-    D->nloc0 = row_starts[rank + 1] - row_starts[rank];
-    const int64_t n = 3 * D->nloc0;
-    const LocalMat &A0 = D->dl[0].A;
-    D->r.alloc(n + 3, s);
-    D->z.alloc(n + 3, s);
-    D->q.alloc(n + 3, s);
-    D->u.alloc(n + 3, s);
-    D->pext.alloc(3 * (A0.plan.nloc + A0.plan.nghost) + 3, s);
-    D->uext.alloc(3 * (A0.plan.nloc + A0.plan.nghost) + 3, s);
-    D->partials.alloc(4096, s);
-    D->sc.alloc(1, s);
+    for (DRank &R : D->ranks) {
+        const int64_t n = 3 * R.nloc0;
+        const LocalMat &A0 = R.dl[0].A;
+        R.fLd.alloc(3 * nLd + 3, s);
+        R.uLd.alloc(3 * nLd + 3, s);
+        R.r.alloc(n + 3, s);
+        R.z.alloc(n + 3, s);
+        R.q.alloc(n + 3, s);
+        R.u.alloc(n + 3, s);
+        R.pext.alloc(3 * (A0.plan.nloc + A0.plan.nghost) + 3, s);
+        R.uext.alloc(3 * (A0.plan.nloc + A0.plan.nghost) + 3, s);
+        R.partials.alloc(4096, s);
+        R.sc.alloc(1, s);
+    }
     CK(cudaMallocHost(&D->sc_host, sizeof(CgScalars)));
     CK(cudaStreamSynchronize(s));
     D->H = std::move(H);
+    D->comm = comm;
     return D.release();
 }
 
@@ -418,30 +535,43 @@ DHierarchy *dsetup(std::unique_ptr<Hierarchy> H, ncclComm_t comm, int nranks, in
 // ---- entry points used by capi.cu ------------------------------------------
 namespace samgb {
 
+// id == nullptr: emulate all nranks in this process (no NCCL).
 DHierarchy *dsetup_all(const unsigned char *id, int nranks, int rank, Bsr3 &&A0,
                        const double *B, int64_t b_rows, int64_t b_cols,
                        const int64_t *row_starts, int64_t min_rows, const samg_amg_params &prm,
                        cudaStream_t s, double t0) {
-    std::unique_ptr<Hierarchy> H(setup_hierarchy(std::move(A0), B, b_rows, b_cols, prm, s, t0));
-    const int64_t nb = H->levels.front().A.nrows;
+    if (!id && nranks > kMaxEmulated) fail(SAMG_INVALID_ARGUMENT, "dsetup: at most 16 emulated ranks");
+    const int64_t nb = A0.nrows;
     std::vector<int64_t> st(nranks + 1);
     if (row_starts) {
         st.assign(row_starts, row_starts + nranks + 1);
         if (st[0] != 0 || st[nranks] != nb)
             fail(SAMG_INVALID_ARGUMENT, "dsetup: row_starts must span [0, nbrows]");
-        for (int q = 0; q < nranks; ++q)
-            if (st[q + 1] < st[q]) fail(SAMG_INVALID_ARGUMENT, "dsetup: row_starts must be nondecreasing");
     } else {
         for (int q = 0; q <= nranks; ++q) st[q] = nb * q / nranks;
     }
-    ncclUniqueId uid;
-    std::memcpy(&uid, id, sizeof uid);
-    ncclComm_t comm;
-    NK(nccl().CommInitRank(&comm, nranks, uid, rank));
+    for (int q = 0; q < nranks; ++q)
+        if (st[q + 1] <= st[q]) fail(SAMG_INVALID_ARGUMENT, "dsetup: every rank needs at least one block row");
+    std::unique_ptr<Hierarchy> H(setup_hierarchy(std::move(A0), B, b_rows, b_cols, prm, s, t0));
+    H->owns_stream = false;  // the caller destroys s if anything below throws
+    std::vector<int> mine;
+    if (id) {
+        mine.push_back(rank);
+    } else {
+        for (int q = 0; q < nranks; ++q) mine.push_back(q);
+    }
+    ncclComm_t comm = nullptr;
+    if (id) {
+        ncclUniqueId uid;
+        std::memcpy(&uid, id, sizeof uid);
+        NK(nccl().CommInitRank(&comm, nranks, uid, rank));
+    }
     try {
-        return dsetup(std::move(H), comm, nranks, rank, st, min_rows);
+        DHierarchy *d = dsetup(std::move(H), comm, nranks, mine, st, min_rows);
+        d->H->owns_stream = true;
+        return d;
     } catch (...) {
-        nccl().CommDestroy(comm);
+        if (comm) nccl().CommDestroy(comm);
         throw;
     }
 }
@@ -454,7 +584,8 @@ samg_solve_report dcg(DHierarchy *d, const double *f, double *u, const samg_cg_p
     if (!host) return d->cg(f, u, cp);
     const auto t0 = std::chrono::steady_clock::now();
     cudaStream_t s = d->stream();
-    const int64_t n = 3 * d->nloc0;
+    int64_t n = 0;
+    for (const DRank &R : d->ranks) n += 3 * R.nloc0;
     DevBuf<double> df(n + 1, s), du(n + 1, s);
     CK(cudaMemcpyAsync(df.p, f, sizeof(double) * n, cudaMemcpyHostToDevice, s));
     samg_solve_report rep = d->cg(df.p, du.p, cp);
@@ -466,8 +597,8 @@ samg_solve_report dcg(DHierarchy *d, const double *f, double *u, const samg_cg_p
 
 void dinfo(const DHierarchy *d, int64_t *row0, int64_t *row1, int *nlevels, int *dist_levels,
            double *setup_s) {
-    *row0 = d->dl[0].fstarts[d->rank];
-    *row1 = d->dl[0].fstarts[d->rank + 1];
+    *row0 = d->ranks.front().row0;
+    *row1 = d->ranks.back().row0 + d->ranks.back().nloc0;
     *nlevels = static_cast<int>(d->H->levels.size());
     *dist_levels = static_cast<int>(d->Ld);
     *setup_s = d->H->setup_seconds;

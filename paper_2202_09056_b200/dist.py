@@ -194,19 +194,27 @@ def nccl_unique_id() -> bytes:
 class DistHierarchy:
     """Multi-GPU ns_block hierarchy (samg_dsetup): every rank passes the same
     global problem; the solve runs on the rank's rows with NCCL halos.  The
-    NCCL id is created on rank 0 and broadcast with torch.distributed."""
+    NCCL id is created on rank 0 and broadcast with torch.distributed.
+
+    ``emulate=True`` drives all ``nranks`` slices from this process on one
+    GPU without NCCL (the halo, all-reduce and gather steps become device
+    copies); f and u are then the global vectors."""
 
     def __init__(self, nbrows, ptr, col, val, B, rank, nranks, dist=None, row_starts=None,
-                 min_rows=4096, prm=None, uid=None):
+                 min_rows=4096, prm=None, uid=None, emulate=False):
         from .api import AmgParams, _nullspace
         prm = prm or AmgParams()
-        _load_torch_nccl()
-        if uid is None:
-            obj = [nccl_unique_id() if rank == 0 else None]
-            if dist is not None and nranks > 1:
-                dist.broadcast_object_list(obj, src=0)
-            uid = obj[0]
-        idbuf = (C.c_ubyte * 128).from_buffer_copy(uid)
+        idbuf = None
+        if emulate:
+            rank = 0
+        else:
+            _load_torch_nccl()
+            if uid is None:
+                obj = [nccl_unique_id() if rank == 0 else None]
+                if dist is not None and nranks > 1:
+                    dist.broadcast_object_list(obj, src=0)
+                uid = obj[0]
+            idbuf = (C.c_ubyte * 128).from_buffer_copy(uid)
         ptr, col = _i64(ptr), _i64(col)
         val = np.ascontiguousarray(val, dtype=np.float64)
         Bv, brows, k = _nullspace(B, 3 * nbrows)

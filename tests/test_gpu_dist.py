@@ -105,3 +105,59 @@ def test_multi_gpu_solver_single_rank(gpu, min_rows):
     assert abs(r1["iterations"] - r2["iterations"]) <= 1
     assert np.linalg.norm(u1 - u2) <= 1e-10 * np.linalg.norm(u1)
     assert r2["relative_residual"] <= 1e-8 * 1.01
+
+
+EMU_CASES = [
+    # world, min_rows, (pre, post), smoother, uneven row split
+    (2, 1, (1, 1), "spai0", False),
+    (3, 1, (1, 1), "spai0", True),
+    (4, 8, (2, 2), "spai0", False),
+    (5, 1, (1, 1), "jacobi", True),
+    (2, 1, (1, 1), "block_jacobi", False),
+    (3, 10**7, (1, 1), "spai0", False),
+]
+
+
+@pytest.mark.parametrize("world,min_rows,sweeps,smoother,uneven", EMU_CASES)
+def test_emulated_multi_gpu_solver(gpu, world, min_rows, sweeps, smoother, uneven):
+    """samg_dsetup with id=NULL: all `world` row slices of the partitioned
+    hierarchy driven from one process, every NCCL step replaced by device
+    copies with the same offsets/counts.  The partitioned PCG must reproduce
+    the single-GPU solve (same hierarchy; only dot-product and SpMV
+    summation order differ)."""
+    from paper_2202_09056_b200.dist import DistHierarchy
+    pb = gpu
+    p = pb.generate_hex(nx=16, ny=8, nz=8, dirichlet="eliminate", load="traction_xend")
+    prm = pb.AmgParams(coarse_enough=60, smoother=smoother, smoother_omega=0.5,
+                       pre_sweeps=sweeps[0], post_sweeps=sweeps[1])
+    h = pb.setup_bsr3(p.nbrows, p.ptr, p.col, p.val.reshape(-1), p.nullspace(), "ns_block", prm)
+    u1, r1 = h.cg_solve(p.rhs)
+    rs = None
+    if uneven:
+        cuts = np.cumsum([1] + [2 * k + 1 for k in range(world - 1)])
+        rs = np.concatenate([[0], np.round(p.nbrows * cuts / cuts[-1] * 0.999).astype(np.int64)])
+        rs[-1] = p.nbrows
+    dh = DistHierarchy(p.nbrows, p.ptr, p.col, p.val.reshape(-1), p.nullspace(), 0, world,
+                       row_starts=rs, min_rows=min_rows, prm=prm, emulate=True)
+    inf = dh.info()
+    assert inf["row0"] == 0 and inf["row1"] == p.nbrows
+    if min_rows == 1:
+        assert inf["dist_levels"] >= 2
+    if min_rows >= 10**7:
+        assert inf["dist_levels"] == 1
+    u2, r2 = dh.cg_solve(p.rhs)
+    assert r1["converged"] and r2["converged"]
+    assert abs(r1["iterations"] - r2["iterations"]) <= 1
+    assert np.linalg.norm(u1 - u2) <= 1e-9 * np.linalg.norm(u1)
+    assert r2["relative_residual"] <= 1e-8 * 1.01
+
+
+def test_emulated_rejects_empty_rank(gpu):
+    from paper_2202_09056_b200._lib import InvalidArgument
+    from paper_2202_09056_b200.dist import DistHierarchy
+    pb = gpu
+    p = pb.generate_hex(nx=6, ny=4, nz=4, dirichlet="eliminate")
+    with pytest.raises(InvalidArgument):
+        DistHierarchy(p.nbrows, p.ptr, p.col, p.val.reshape(-1), p.nullspace(), 0, 2,
+                      row_starts=[0, 0, p.nbrows], prm=pb.AmgParams(coarse_enough=30),
+                      emulate=True)
