@@ -411,6 +411,7 @@ def run_b200_dist(args, rank, world, local, dist):
     te = torch.tensor([e2e_t], device=dev, dtype=torch.float64)
     dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_val = total_bytes / float(te.item()) / 1e9
+    amg = run_dist_amg(args, rank, world, local, dist) if args.amg_repeats > 0 else None
     peak, peak_src = peaks()
     gb_rank = nbytes / (ms_per * 1e-3) / 1e9
     if rank == 0:
@@ -436,8 +437,62 @@ def run_b200_dist(args, rank, world, local, dist):
             "gpu_launches": 3 * args.steps,
             "clocks": clk.summary(),
             "cpu_baseline": None,
-            "amg": None,
+            "amg": amg,
         }))
+
+
+def run_dist_amg(args, rank, world, local, dist):
+    """Multi-GPU AMG on the C1 problem (strong scaling): every rank builds the
+    same hierarchy (samg_dsetup), keeps its rows of the large levels and runs
+    the partitioned PCG with NCCL halos / all-reduces (dsolve.cu)."""
+    import torch
+
+    import paper_2202_09056_b200 as pb
+    from paper_2202_09056_b200.dist import DistHierarchy
+    dev = torch.device("cuda", local)
+    p = make_problem(pb)
+    B = p.nullspace()
+    prm = pb.AmgParams(smoother="spai0", device=local)
+    setups, solves, rep, dh = [], [], None, None
+
+    def tmax(x):
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for it in range(args.amg_repeats + 1):  # first round: untimed warm-up
+        if dh is not None:
+            dh.close()
+        dist.barrier()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        dh = DistHierarchy(p.nbrows, p.ptr, p.col, p.val.reshape(-1), B, rank, world, dist=dist,
+                           prm=prm)
+        torch.cuda.synchronize(dev)
+        ts = tmax(time.perf_counter() - t0)
+        inf = dh.info()
+        r0, r1 = inf["row0"], inf["row1"]
+        f_d = torch.from_numpy(np.ascontiguousarray(p.rhs[3 * r0:3 * r1])).to(dev)
+        u_d = torch.zeros_like(f_d)
+        dist.barrier()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        rep = dh.cg_solve_device(f_d.data_ptr(), u_d.data_ptr(),
+                                 pb.CgParams(max_iterations=2) if it == 0 else None)
+        torch.cuda.synchronize(dev)
+        tv = tmax(time.perf_counter() - t0)
+        if it > 0:
+            setups.append(ts)
+            solves.append(tv)
+    out = {"setup_s": statistics.median(setups), "solve_s": statistics.median(solves),
+           "setup_s_all": setups, "solve_s_all": solves, "iterations": rep["iterations"],
+           "relative_residual": rep["relative_residual"], "converged": rep["converged"],
+           "levels": inf["nlevels"], "partitioned_levels": inf["dist_levels"],
+           "problem": "C1 (strong scaling: same global problem on every N)",
+           "timing": "wall clock around setup / solve, max over ranks",
+           "smoother": "spai0", "input": "host BSR3 upload inside setup_s"}
+    dh.close()
+    return out
 
 
 def main():
