@@ -325,7 +325,7 @@ def run_b200(args, rank, world, local, dist):
                        "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
             "roofline": {"bound": "hbm", "achieved": gbs_rank, "peak": peak, "unit": "GB/s",
                          "frac": gbs_rank / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "k_bsr3<G,EpiSpmv> (solve.cu)"},
+                         "kernel": "k_bsr3_tma<8,8,2,false,EpiSpmv> (solve.cu, TMA-fed)"},
             "e2e": {"value": e2e_val, "unit": "GB/s", "h2d_bytes_per_step": 8 * p.n,
                     "d2h_bytes_per_step": 8 * p.n,
                     "path": "samg_bsr3_spmv (C-ABI, pinned host x/y)"},

@@ -342,12 +342,194 @@ __global__ void __launch_bounds__(256) k_bsr3_reduce(int nrows, const int *__res
     grid_finish(d, partials, sc, what, 0);
 }
 
+// ---- TMA-fed persistent variant (variant 3) ---------------------------------
+// The fine-level matrix stream is the whole cost of the SpMV.  Here it is
+// moved by the copy engine instead of by per-thread loads: a persistent CTA
+// (one per SM) walks chunks of RPC = 256/G consecutive block rows; one
+// producer lane issues 1-D bulk copies (cp.async.bulk, completion counted on
+// an mbarrier) of the chunk's contiguous val / col / ptr bytes into an
+// S-stage shared-memory ring, while 8 consumer warps compute the previous
+// chunks from shared memory (x is gathered from L2, as before).  Bytes in
+// flight per SM are set by the ring size, not by registers.  A chunk that
+// does not fit a stage, or would read past the arrays' ends, is computed
+// straight from global memory.
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *b, unsigned n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t *b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+                 "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, unsigned parity) {
+    unsigned done;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done) : "r"(smem_u32(b)), "r"(parity) : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+struct TmaHdr {
+    int p0, direct, voff, coff;  // first block, fallback flag, block p0's offset (doubles / ints)
+};
+
+struct TmaCfg {
+    int nrows, nchunks, stages;
+    unsigned vcap, ccap, pcap;  // stage layout: val | col | ptr (bytes)
+    long long nnzb;
+};
+
+constexpr int kTmaHdrBytes = 1024;  // barriers + headers of up to 16 stages
+
+template <int G, int TW, int NT, bool kReduce, class Epi>
+__global__ void __launch_bounds__(32 * (TW * NT + 1), 1) k_bsr3_tma(TmaCfg cfg, const int *__restrict__ ptr,
+        const int *__restrict__ col, const double *__restrict__ val,
+        const double *__restrict__ x, Epi epi, double *partials, CgScalars *sc, int what) {
+    static_assert(G >= 1 && G <= 32, "TMA variant: at most one warp per row");
+    constexpr int RPC = 32 * TW / G;  // rows per chunk: one team of TW warps per chunk
+    extern __shared__ __align__(128) unsigned char sm[];
+    const int S = cfg.stages;
+    uint64_t *full = reinterpret_cast<uint64_t *>(sm);
+    uint64_t *empty = full + 16;
+    TmaHdr *hdr = reinterpret_cast<TmaHdr *>(sm + 256);
+    unsigned char *data = sm + kTmaHdrBytes;
+    const unsigned stage_bytes = cfg.vcap + cfg.ccap + cfg.pcap;
+    const int warp = threadIdx.x / 32, lane32 = threadIdx.x % 32;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, TW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    double d = 0.0;
+    if (warp == TW * NT) {
+        // producer warp: the 32 lanes fetch the row bounds of 32 upcoming
+        // chunks at once, lane 0 issues the copies in order
+        int st = 0;
+        unsigned ph = 0;
+        for (int c0 = blockIdx.x; c0 < cfg.nchunks; c0 += 32 * gridDim.x) {
+            const int cl = c0 + lane32 * gridDim.x;
+            int b0 = 0, b1 = 0;
+            if (cl < cfg.nchunks) {
+                const int r0 = cl * RPC, r1 = min(r0 + RPC, cfg.nrows);
+                b0 = __ldg(ptr + r0);
+                b1 = __ldg(ptr + r1);
+            }
+            for (int i = 0; i < 32; ++i) {
+                const int c = c0 + i * gridDim.x;
+                const int p0 = __shfl_sync(0xffffffffu, b0, i), p1 = __shfl_sync(0xffffffffu, b1, i);
+                if (c >= cfg.nchunks) break;
+                if (lane32 == 0) {
+                    mbar_wait(empty + st, ph ^ 1);
+                    const int r0 = c * RPC;
+                    const long long vb = (72LL * p0) & ~15LL, ve = (72LL * p1 + 15) & ~15LL;
+                    const long long cb = (4LL * p0) & ~15LL, ce = (4LL * p1 + 15) & ~15LL;
+                    const long long pe = 4LL * (r0 + RPC + 4);
+                    const bool direct = ve - vb > cfg.vcap || ce - cb > cfg.ccap ||
+                                        ve > 72LL * cfg.nnzb || ce > 4LL * cfg.nnzb ||
+                                        r0 + RPC + 4 > cfg.nrows + 1 || p1 == p0;
+                    hdr[st] = TmaHdr{p0, direct ? 1 : 0, static_cast<int>((72LL * p0 - vb) / 8),
+                                     static_cast<int>((4LL * p0 - cb) / 4)};
+                    if (!direct) {
+                        unsigned char *sv = data + static_cast<size_t>(st) * stage_bytes;
+                        mbar_arrive_tx(full + st, static_cast<unsigned>((ve - vb) + (ce - cb) +
+                                                                        (pe - 4LL * r0)));
+                        bulk_g2s(sv, reinterpret_cast<const char *>(val) + vb,
+                                 static_cast<unsigned>(ve - vb), full + st);
+                        bulk_g2s(sv + cfg.vcap, reinterpret_cast<const char *>(col) + cb,
+                                 static_cast<unsigned>(ce - cb), full + st);
+                        bulk_g2s(sv + cfg.vcap + cfg.ccap, ptr + r0,
+                                 static_cast<unsigned>(pe - 4LL * r0), full + st);
+                    } else {
+                        mbar_arrive(full + st);
+                    }
+                }
+                if (++st == S) { st = 0; ph ^= 1; }
+            }
+        }
+    } else {
+        // NT teams of TW consumer warps take the CTA's chunks in turn, so NT
+        // chunks are computed concurrently while the ring fills
+        const int team = warp / TW, tt = threadIdx.x - 32 * TW * team;
+        const int lane = tt % G, grp = tt / G;
+        for (int i = team, c = blockIdx.x + team * gridDim.x; c < cfg.nchunks;
+             i += NT, c += NT * gridDim.x) {
+            const int st = i % S;
+            const unsigned ph = (i / S) & 1;
+            mbar_wait(full + st, ph);
+            const TmaHdr h = hdr[st];
+            const int row = c * RPC + grp;
+            const bool valid = row < cfg.nrows;
+            double s0, s1, s2;
+            if (h.direct) {
+                row_sums_blocks<G>(row, valid, lane, ptr, col, val, x, s0, s1, s2);
+            } else {
+                const unsigned char *sv = data + static_cast<size_t>(st) * stage_bytes;
+                const double *svd = reinterpret_cast<const double *>(sv);
+                const int *svc = reinterpret_cast<const int *>(sv + cfg.vcap);
+                const int *svp = reinterpret_cast<const int *>(sv + cfg.vcap + cfg.ccap);
+                double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+                if (valid) {
+                    const int beg = svp[grp] - h.p0, end = svp[grp + 1] - h.p0;
+#pragma unroll 2
+                    for (int k = beg + lane; k < end; k += G) {
+                        const int c3 = svc[k + h.coff];
+                        const int o = 9 * k + h.voff;
+                        const double *v = svd + o;
+                        const int odd = o & 1;
+                        const double2 q0 = *reinterpret_cast<const double2 *>(v + odd),
+                                      q1 = *reinterpret_cast<const double2 *>(v + odd + 2),
+                                      q2 = *reinterpret_cast<const double2 *>(v + odd + 4),
+                                      q3 = *reinterpret_cast<const double2 *>(v + odd + 6);
+                        const double e = v[odd ? 0 : 8];
+                        const double *xp = x + 3 * static_cast<size_t>(c3);
+                        const int xo = c3 & 1;
+                        const double2 xq = ldg2(xp + xo);
+                        const double xe = __ldg(xp + (xo ? 0 : 2));
+                        const double x0 = xo ? xe : xq.x, x1 = xo ? xq.x : xq.y, x2 = xo ? xq.y : xe;
+                        const double b0 = odd ? e : q0.x, b1 = odd ? q0.x : q0.y, b2 = odd ? q0.y : q1.x;
+                        const double b3 = odd ? q1.x : q1.y, b4 = odd ? q1.y : q2.x, b5 = odd ? q2.x : q2.y;
+                        const double b6 = odd ? q2.y : q3.x, b7 = odd ? q3.x : q3.y, b8 = odd ? q3.y : e;
+                        a0 = fma(b0, x0, a0); a0 = fma(b1, x1, a0); a0 = fma(b2, x2, a0);
+                        a1 = fma(b3, x0, a1); a1 = fma(b4, x1, a1); a1 = fma(b5, x2, a1);
+                        a2 = fma(b6, x0, a2); a2 = fma(b7, x1, a2); a2 = fma(b8, x2, a2);
+                    }
+                }
+                s0 = a0; s1 = a1; s2 = a2;
+                group_reduce3<G>(s0, s1, s2);
+            }
+            __syncwarp();
+            if (lane32 == 0) mbar_arrive(empty + st);
+            if (valid) {
+                const double t = epilogue<G>(epi, row, lane, s0, s1, s2);
+                if constexpr (kReduce) d += t;
+            }
+        }
+    }
+    if constexpr (kReduce) grid_finish(d, partials, sc, what, 0);
+}
+
 constexpr int kReduceCtas = 148 * 8;
 
 int spmv_variant() {
     static const int v = [] {
         const char *e = std::getenv("SAMG_SPMV_VARIANT");
-        return e ? std::atoi(e) : 1;
+        return e ? std::atoi(e) : 3;
     }();
     return v;
 }
@@ -395,9 +577,104 @@ void dispatch_group(int G, F f) {
     }
 }
 
+int env_int(const char *name, int dflt) {
+    const char *e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
+}
+
+// Variant 3 launch; false if the matrix does not suit it (then the caller
+// uses the register-streaming kernel).
+template <int G_, int TW_, int NT_>
+struct TmaShape {
+    static constexpr int G = G_, TW = TW_, NT = NT_;
+};
+
+// (lanes per row, warps per team, teams); SAMG_TMA_CFG selects one
+constexpr int kTmaShapes[][3] = {{8, 8, 2}, {8, 4, 3}, {8, 4, 4}, {16, 4, 4}, {16, 8, 3}, {8, 8, 1}};
+
+template <class F>
+void dispatch_tma_shape(int k, F f) {
+    switch (k) {
+        case 1: f(TmaShape<8, 4, 3>{}); break;
+        case 2: f(TmaShape<8, 4, 4>{}); break;
+        case 3: f(TmaShape<16, 4, 4>{}); break;
+        case 4: f(TmaShape<16, 8, 3>{}); break;
+        case 5: f(TmaShape<8, 8, 1>{}); break;
+        default: f(TmaShape<8, 8, 2>{}); break;
+    }
+}
+
+template <bool kReduce, class Epi>
+bool launch_tma(const Bsr3 &A, const double *x, Epi epi, double *partials, CgScalars *sc,
+                int what, cudaStream_t s) {
+    if (A.nrows < 8 || A.nnzb == 0) return false;
+    if ((reinterpret_cast<uintptr_t>(A.val.p) | reinterpret_cast<uintptr_t>(A.col.p) |
+         reinterpret_cast<uintptr_t>(A.ptr.p)) & 15)
+        return false;
+    static const int shape = std::min(std::max(env_int("SAMG_TMA_CFG", 0), 0), 5);
+    static const int budget = env_int("SAMG_TMA_SMEM", 226000);
+    const int G = kTmaShapes[shape][0], TW = kTmaShapes[shape][1], NT = kTmaShapes[shape][2];
+    const double bpr = static_cast<double>(A.nnzb) / A.nrows;
+    const int rpc = 32 * TW / G;
+    auto up = [](long long b) { return static_cast<unsigned>((b + 127) / 128 * 128); };
+    const long long est = static_cast<long long>(std::ceil(bpr * 1.1)) + 1;
+    TmaCfg cfg{};
+    cfg.nrows = static_cast<int>(A.nrows);
+    cfg.nchunks = static_cast<int>((A.nrows + rpc - 1) / rpc);
+    cfg.nnzb = A.nnzb;
+    cfg.vcap = up(rpc * est * 72 + 16);
+    cfg.ccap = up(rpc * est * 4 + 16);
+    cfg.pcap = up(4LL * (rpc + 4));
+    const long long stage = cfg.vcap + cfg.ccap + cfg.pcap;
+    cfg.stages = static_cast<int>(std::min<long long>(16, (budget - kTmaHdrBytes) / stage));
+    if (cfg.stages < NT + 1) return false;
+    const int smem = kTmaHdrBytes + static_cast<int>(cfg.stages * stage);
+    static int sms = [] {
+        int dev = 0, n = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        return n;
+    }();
+    // one persistent CTA per SM only pays off when every CTA streams many
+    // chunks (C1: fine level 8 064 chunks -> TMA; level 1: 645 -> variant 1)
+    static const int min_chunks_per_sm = env_int("SAMG_TMA_MIN_CHUNKS", 16);
+    if (cfg.nchunks < min_chunks_per_sm * sms) return false;
+    bool ok = false;
+    dispatch_tma_shape(shape, [&](auto sh) {
+        using Sh = decltype(sh);
+        auto kern = k_bsr3_tma<Sh::G, Sh::TW, Sh::NT, kReduce, Epi>;
+        const int threads = 32 * (Sh::TW * Sh::NT + 1);
+        // opt in to the largest dynamic size next to the static shared
+        // memory of the reduction helpers
+        static const int max_dyn = [&] {
+            int dev = 0, optin = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+            cudaFuncAttributes fa{};
+            cudaFuncGetAttributes(&fa, kern);
+            const int m = optin - static_cast<int>(fa.sharedSizeBytes);
+            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, m) !=
+                cudaSuccess) {
+                cudaGetLastError();
+                return 0;
+            }
+            return m;
+        }();
+        if (smem > max_dyn) return;
+        int occ = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
+        const int grid = std::max(1, std::min(cfg.nchunks, std::max(1, occ) * sms));
+        kern<<<grid, threads, smem, s>>>(cfg, A.ptr.p, A.col.p, A.val.p, x, epi, partials, sc, what);
+        ok = true;
+    });
+    if (ok) CK_LAUNCH();
+    return ok;
+}
+
 template <class Epi>
 void launch_rows(const Bsr3 &A, const double *x, Epi epi, cudaStream_t s) {
     if (A.nrows == 0) return;
+    if (spmv_variant() == 3 && launch_tma<false>(A, x, epi, nullptr, nullptr, 0, s)) return;
     const int G = choose_group(A);
     const int grid = ceil_div(A.nrows * static_cast<int64_t>(G), 256);
     const int n = static_cast<int>(A.nrows);
@@ -417,6 +694,7 @@ void launch_rows(const Bsr3 &A, const double *x, Epi epi, cudaStream_t s) {
 template <class Epi>
 void launch_reduce(const Bsr3 &A, const double *x, Epi epi, double *partials, CgScalars *sc,
                    int what, cudaStream_t s) {
+    if (spmv_variant() == 3 && launch_tma<true>(A, x, epi, partials, sc, what, s)) return;
     const int G = choose_group(A);
     const int n = static_cast<int>(A.nrows);
     dispatch_group(G, [&](auto g) {
