@@ -191,6 +191,11 @@ SAMG_API int samg_bsr3_spmv(const samg_bsr3 *m, double alpha, const double *x,
 SAMG_API int samg_bsr3_galerkin(const samg_bsr3 *R, const samg_bsr3 *A,
         const samg_bsr3 *P, samg_bsr3 **out);
 /* algorithmic bytes of one spmv */
+/* coarsest-level direct solver on its own: inv (host, n x n row-major,
+ * n = 3*nrows) = A^-1 by the device's in-place blocked Gauss-Jordan with the
+ * reference's partial pivoting (dense_lu, hierarchy.hpp:86-129); a pivot
+ * below 1e-300 returns SAMG_ERROR ("singular"). */
+SAMG_API int samg_bsr3_dense_inverse(const samg_bsr3 *m, double *inv);
 SAMG_API int samg_bsr3_spmv_bytes(const samg_bsr3 *m, int beta_nonzero,
         uint64_t *bytes);
 

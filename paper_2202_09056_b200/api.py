@@ -122,6 +122,14 @@ class Bsr3:
         check(lib.samg_bsr3_spmv_bytes(self.h, int(beta_nonzero), C.byref(b)))
         return b.value
 
+    def dense_inverse(self) -> np.ndarray:
+        """A^-1 as a dense host array (the coarsest-level solver, coarse.cu)."""
+        nr, nc, _ = self.shape
+        n = 3 * nr
+        out = np.zeros((n, n))
+        check(lib.samg_bsr3_dense_inverse(self.h, out.ctypes.data_as(f64p)))
+        return out
+
     @staticmethod
     def galerkin(R: "Bsr3", A: "Bsr3", P: "Bsr3") -> "Bsr3":
         h = vp()

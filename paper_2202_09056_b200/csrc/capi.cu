@@ -148,10 +148,10 @@ void upload_bsr3(int64_t nrows, int64_t ncols, const int64_t *ptr, const int64_t
     const int64_t nnz = ptr[nrows];
     M.alloc(nrows, ncols, nnz, s);
     DevBuf<int64_t> p64(nrows + 1, s), c64(nnz, s);
-    CK(cudaMemcpyAsync(p64.p, ptr, sizeof(int64_t) * (nrows + 1), cudaMemcpyHostToDevice, s));
+    h2d(p64.p, ptr, sizeof(int64_t) * (nrows + 1), s);
     if (nnz) {
-        CK(cudaMemcpyAsync(c64.p, col, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(M.val.p, val, sizeof(double) * 9 * nnz, cudaMemcpyHostToDevice, s));
+        h2d(c64.p, col, sizeof(int64_t) * nnz, s);
+        h2d(M.val.p, val, sizeof(double) * 9 * nnz, s);
     }
     DevBuf<int> bad(1, s);
     CK(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
@@ -297,10 +297,10 @@ SAMG_API int samg_setup(int64_t n, const int64_t *ptr, const int64_t *col, const
             const int64_t nnz = ptr[n];
             DevBuf<int64_t> dp(n + 1, s), dc(nnz, s);
             DevBuf<double> dv(nnz, s);
-            CK(cudaMemcpyAsync(dp.p, ptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, s));
+            h2d(dp.p, ptr, sizeof(int64_t) * (n + 1), s);
             if (nnz) {
-                CK(cudaMemcpyAsync(dc.p, col, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, s));
-                CK(cudaMemcpyAsync(dv.p, val, sizeof(double) * nnz, cudaMemcpyHostToDevice, s));
+                h2d(dc.p, col, sizeof(int64_t) * nnz, s);
+                h2d(dv.p, val, sizeof(double) * nnz, s);
             }
             scalar_to_bsr3(n, dp.p, dc.p, dv.p, A0, s);
         } catch (...) {
@@ -350,7 +350,7 @@ SAMG_API int samg_cg_solve(samg_hierarchy *hp, const double *f, double *u,
         samgb::Hierarchy &h = H(hp);
         const double t0 = now_s();
         const int64_t n = h.finest_dim();
-        CK(cudaMemcpyAsync(h.fbuf.p, f, sizeof(double) * n, cudaMemcpyHostToDevice, h.stream));
+        h2d(h.fbuf.p, f, sizeof(double) * n, h.stream);
         *rep = h.cg(h.fbuf.p, h.ubuf.p, *prm);
         CK(cudaMemcpyAsync(u, h.ubuf.p, sizeof(double) * n, cudaMemcpyDeviceToHost, h.stream));
         CK(cudaStreamSynchronize(h.stream));
@@ -372,8 +372,8 @@ SAMG_API int samg_vcycle(samg_hierarchy *hp, const double *f, double *u) {
         require(f && u, SAMG_INVALID_ARGUMENT, "vcycle: NULL argument");
         samgb::Hierarchy &h = H(hp);
         const int64_t n = h.finest_dim();
-        CK(cudaMemcpyAsync(h.fbuf.p, f, sizeof(double) * n, cudaMemcpyHostToDevice, h.stream));
-        CK(cudaMemcpyAsync(h.ubuf.p, u, sizeof(double) * n, cudaMemcpyHostToDevice, h.stream));
+        h2d(h.fbuf.p, f, sizeof(double) * n, h.stream);
+        h2d(h.ubuf.p, u, sizeof(double) * n, h.stream);
         h.vcycle(h.fbuf.p, h.ubuf.p, false);
         CK(cudaMemcpyAsync(u, h.ubuf.p, sizeof(double) * n, cudaMemcpyDeviceToHost, h.stream));
         CK(cudaStreamSynchronize(h.stream));
@@ -542,9 +542,9 @@ SAMG_API int samg_bsr3_spmv(const samg_bsr3 *mc, double alpha, const double *x, 
         const Bsr3 &A = *m->m;
         if (m->xs.n < static_cast<size_t>(3 * A.ncols)) m->xs.alloc(3 * A.ncols, nullptr);
         if (m->ys.n < static_cast<size_t>(3 * A.nrows)) m->ys.alloc(3 * A.nrows, nullptr);
-        CK(cudaMemcpyAsync(m->xs.p, x, sizeof(double) * 3 * A.ncols, cudaMemcpyHostToDevice, nullptr));
+        h2d(m->xs.p, x, sizeof(double) * 3 * A.ncols, nullptr);
         if (beta != 0.0)
-            CK(cudaMemcpyAsync(m->ys.p, y, sizeof(double) * 3 * A.nrows, cudaMemcpyHostToDevice, nullptr));
+            h2d(m->ys.p, y, sizeof(double) * 3 * A.nrows, nullptr);
         launch_spmv(A, alpha, m->xs.p, beta, m->ys.p, nullptr);
         CK(cudaMemcpyAsync(y, m->ys.p, sizeof(double) * 3 * A.nrows, cudaMemcpyDeviceToHost, nullptr));
         CK(cudaStreamSynchronize(nullptr));
@@ -567,6 +567,25 @@ SAMG_API int samg_bsr3_galerkin(const samg_bsr3 *R, const samg_bsr3 *A, const sa
         CK(cudaDeviceSynchronize());
         c->m = &c->own;
         *out = c.release();
+    });
+}
+
+SAMG_API int samg_bsr3_dense_inverse(const samg_bsr3 *m, double *inv) {
+    return guarded([&] {
+        require(m && m->m && inv, SAMG_INVALID_ARGUMENT, "dense_inverse: NULL argument");
+        const Bsr3 &A = *m->m;
+        if (A.nrows != A.ncols) fail(SAMG_NON_SQUARE, "dense_lu: matrix must be square");
+        CK(cudaSetDevice(m->device));
+        cudaStream_t s = nullptr;
+        DevBuf<DevError> err(1, s);
+        CK(cudaMemsetAsync(err.p, 0, sizeof(DevError), s));
+        DevBuf<double> Ainv;
+        dense_inverse(A, Ainv, err.p, s);
+        const int64_t n = 3 * A.nrows, ld = dense_ld(n);
+        if (n)
+            CK(cudaMemcpy2DAsync(inv, sizeof(double) * n, Ainv.p, sizeof(double) * ld,
+                                 sizeof(double) * n, n, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
     });
 }
 

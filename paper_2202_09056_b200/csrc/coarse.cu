@@ -9,18 +9,26 @@
 // rows (first index on ties); a pivot below 1e-300 raises samg::error
 // ("dense_lu: singular coarse matrix").
 //
-// Blocked Gauss-Jordan on W = [A | I] (n x 2n, row-major), panel width kB:
-//  1. the panel's kB columns (Y) plus an accumulator Z (n x kB) are reduced
-//     by one cooperative kernel, 2 grid barriers per column (pivot search;
-//     pivot-row broadcast), rows of Y/Z swapped physically;
-//  2. the panel's row swaps are applied to the trailing columns of W;
-//  3. the trailing columns get the rank-kB update
-//     W[:, J] += (Z - E_K) W[K, J]  (one FP64 tiled GEMM),
-// so the n^3 work streams W once per panel instead of once per column.
+// In-place blocked Gauss-Jordan on X (n x n, row-major, even leading
+// dimension), panels of kB columns K = [k0, k0+kB):
+//  1. panel: the n x kB panel is reduced column by column (pivot search, row
+//     swap, elimination; the panel columns are replaced by the columns of the
+//     accumulated transform Z) by ONE thread-block cluster of up to 16 CTAs
+//     that holds the panel in shared memory: the per-column pivot search and
+//     row broadcast go through distributed shared memory with two cluster
+//     barriers per column (instead of grid-wide barriers through L2);
+//  2. the panel's row swaps are applied to the other columns and the kB
+//     pivot rows are copied out (Rk);
+//  3. every other column gets the rank-kB update X[:, J] += (Z - E_K) Rk,
+//     an FP64 tensor-core GEMM (mma.sync m8n8k4 f64, 64x64 tiles).
+// Finally the column permutation implied by the row swaps is undone (gather
+// into the output).  Work 2 n^3 (no identity half), X streamed once per panel.
 #include <cooperative_groups.h>
 
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
+#include <vector>
 
 #include "kernels.cuh"
 
@@ -30,208 +38,607 @@ namespace samgb {
 
 namespace {
 
-constexpr int kB = 32;          // panel width
-constexpr int kPT = 256;        // panel kernel threads per CTA
+constexpr int kPT = 256;            // panel kernel threads per CTA
+constexpr int kMaxB = 64;           // max panel width
+constexpr int kMaxCluster = 16;
 
-// scatter A (BSR3) into W = [A | I], row-major n x 2n (to_dense, csr.hpp:370-382)
+// scatter A (BSR3) into X (row-major, leading dimension ld; to_dense,
+// csr.hpp:370-382)
 __global__ void k_scatter(int nrows, const int *ptr, const int *col, const double *val,
-                          int64_t n, double *W) {
+                          int64_t ld, double *X) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nrows) return;
-    const int64_t ld = 2 * n;
-    for (int r = 0; r < 3; ++r) W[(3 * static_cast<int64_t>(i) + r) * ld + n + 3 * i + r] = 1.0;
     for (int j = ptr[i]; j < ptr[i + 1]; ++j)
         for (int r = 0; r < 3; ++r)
             for (int c = 0; c < 3; ++c)
-                W[(3 * static_cast<int64_t>(i) + r) * ld + 3 * static_cast<int64_t>(col[j]) + c] =
+                X[(3 * static_cast<int64_t>(i) + r) * ld + 3 * static_cast<int64_t>(col[j]) + c] =
                     val[9 * static_cast<int64_t>(j) + 3 * r + c];
 }
 
-__global__ void k_panel_load(int64_t n, int64_t k0, int bk, const double *W, double *Pn) {
-    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n * 2 * kB;
-         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t i = e / (2 * kB);
-        const int q = static_cast<int>(e - i * 2 * kB);
-        Pn[e] = (q < bk) ? W[i * 2 * n + k0 + q] : 0.0;
-    }
+__device__ __forceinline__ bool better(double v, int64_t i, double bv, int64_t bi) {
+    return v > bv || (v == bv && i < bi);
 }
 
-// Gauss-Jordan on the n x (Y | Z) panel; rows split into contiguous ranges
-// per CTA.  piv[q] = pivot row of panel column q.
-__global__ void __launch_bounds__(kPT) k_panel_gj(int64_t n, int64_t k0, int bk, double *Pn,
-                                                   double *pval, int64_t *pidx, int64_t *piv,
-                                                   DevError *err) {
-    cg::grid_group grid = cg::this_grid();
-    __shared__ double prow[2 * kB], krow[2 * kB], rk[2 * kB], fs[64];
+// In-place Gauss-Jordan on the panel X[:, k0:k0+bk] by one cluster.  CTA r
+// of the cluster holds rows [r*R, min(n, (r+1)*R)) in shared memory
+// (row-major, kB doubles per row).  piv[q] = pivot row of column k0+q.
+__global__ void __launch_bounds__(kPT) k_panel_cluster(int64_t n, int64_t ld, int64_t k0, int bk,
+                                                        int kB, int R, double *X, int64_t *piv,
+                                                        DevError *err) {
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ __align__(16) double S[];  // R x kB
+    __shared__ double cand_v;
+    __shared__ int64_t cand_i;
     __shared__ double wv[kPT / 32];
     __shared__ int64_t wi[kPT / 32];
+    __shared__ double prow[kMaxB], krow[kMaxB], r[kMaxB];
     __shared__ int64_t s_p;
     __shared__ double s_v;
-    const int64_t per = (n + gridDim.x - 1) / gridDim.x;
-    const int64_t r0 = blockIdx.x * per, r1 = min(n, r0 + per);
+    const int rank = static_cast<int>(cl.block_rank()), C = static_cast<int>(cl.num_blocks());
+    const int64_t r0 = static_cast<int64_t>(rank) * R, r1 = min(n, r0 + R);
+    const int nr = r1 > r0 ? static_cast<int>(r1 - r0) : 0;
     const int lane = threadIdx.x % 32, w = threadIdx.x / 32;
+    for (int e = threadIdx.x; e < nr * kB; e += kPT) {
+        const int i = e / kB, q = e - i * kB;
+        S[e] = q < bk ? X[(r0 + i) * ld + k0 + q] : 0.0;
+    }
+    __syncthreads();
     for (int q = 0; q < bk; ++q) {
         const int64_t k = k0 + q;
-        // a. local argmax of |Y[i][q]| over own rows i >= k
+        // a. local argmax of |X[i][k]| over own rows i >= k
         double best = -1.0;
         int64_t bi = n;
-        for (int64_t i = max(r0, k) + threadIdx.x; i < r1; i += blockDim.x) {
-            const double v = fabs(Pn[i * 2 * kB + q]);
+        for (int64_t i = max(r0, k) + threadIdx.x; i < r1; i += kPT) {
+            const double v = fabs(S[(i - r0) * kB + q]);
             if (v > best) { best = v; bi = i; }
         }
         for (int off = 16; off >= 1; off >>= 1) {
             const double ov = __shfl_xor_sync(0xffffffffu, best, off);
             const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, off);
-            if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+            if (better(ov, oi, best, bi)) { best = ov; bi = oi; }
         }
         if (lane == 0) { wv[w] = best; wi[w] = bi; }
         __syncthreads();
         if (threadIdx.x == 0) {
+            double bv = wv[0];
+            int64_t bix = wi[0];
             for (int t = 1; t < kPT / 32; ++t)
-                if (wv[t] > wv[0] || (wv[t] == wv[0] && wi[t] < wi[0])) { wv[0] = wv[t]; wi[0] = wi[t]; }
-            pval[blockIdx.x] = wv[0];
-            pidx[blockIdx.x] = wi[0];
+                if (better(wv[t], wi[t], bv, bix)) { bv = wv[t]; bix = wi[t]; }
+            cand_v = bv;
+            cand_i = bix;
         }
-        grid.sync();
-        // b. global pivot (same in every CTA): block-parallel reduction of
-        //    the per-CTA candidates, then read pivot row and row k
-        {
+        cl.sync();  // candidates of every CTA visible
+        // b. global pivot, identical in every CTA
+        if (w == 0) {
             double bv = -1.0;
             int64_t bix = n;
-            for (unsigned c = threadIdx.x; c < gridDim.x; c += blockDim.x) {
-                const double v = pval[c];
-                const int64_t i = pidx[c];
-                if (v > bv || (v == bv && i < bix)) { bv = v; bix = i; }
+            if (lane < C) {
+                bv = *cl.map_shared_rank(&cand_v, lane);
+                bix = *cl.map_shared_rank(&cand_i, lane);
             }
             for (int off = 16; off >= 1; off >>= 1) {
                 const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
                 const int64_t oi = __shfl_xor_sync(0xffffffffu, bix, off);
-                if (ov > bv || (ov == bv && oi < bix)) { bv = ov; bix = oi; }
+                if (better(ov, oi, bv, bix)) { bv = ov; bix = oi; }
             }
-            __syncthreads();
-            if (lane == 0) { wv[w] = bv; wi[w] = bix; }
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                for (int t = 1; t < kPT / 32; ++t)
-                    if (wv[t] > wv[0] || (wv[t] == wv[0] && wi[t] < wi[0])) { wv[0] = wv[t]; wi[0] = wi[t]; }
-                s_p = wi[0];
-                s_v = wi[0] < n ? Pn[wi[0] * 2 * kB + q] : 0.0;
-            }
+            if (lane == 0) s_p = bix;
         }
         __syncthreads();
         const int64_t p = s_p;
+        // c. rows p and k from their owners (distributed shared memory)
+        if (threadIdx.x < 2 * kB && p < n) {
+            const bool isp = threadIdx.x < kB;
+            const int t = isp ? threadIdx.x : threadIdx.x - kB;
+            const int64_t row = isp ? p : k;
+            const int owner = static_cast<int>(row / R);
+            const double *src = cl.map_shared_rank(S, owner) + (row - static_cast<int64_t>(owner) * R) * kB;
+            (isp ? prow : krow)[t] = src[t];
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) s_v = p < n ? prow[q] : 0.0;
+        __syncthreads();
         const double v = s_v;
         if (!(fabs(v) >= 1e-300)) {
-            if (blockIdx.x == 0 && threadIdx.x == 0 && atomicCAS(&err->code, 0, SAMG_ERROR) == 0)
-                err->where = k;
-            return;  // uniform across the grid
+            if (rank == 0 && threadIdx.x == 0) {
+                if (atomicCAS(&err->code, 0, SAMG_ERROR) == 0) err->where = k;
+                for (int t = q; t < bk; ++t) piv[t] = k0 + t;  // keep later kernels in bounds
+            }
+            cl.sync();  // uniform exit: nobody reads this CTA's memory afterwards
+            return;
         }
-        for (int t = threadIdx.x; t < 2 * kB; t += blockDim.x) {
-            prow[t] = Pn[p * 2 * kB + t];
-            krow[t] = Pn[k * 2 * kB + t];
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            prow[kB + q] = 1.0;  // Z column q starts as e_k (after the swap)
-            if (blockIdx.x == 0) piv[q] = p;
-        }
-        __syncthreads();
         const double inv = 1.0 / v;
-        for (int t = threadIdx.x; t < 2 * kB; t += blockDim.x) rk[t] = prow[t] * inv;
-        grid.sync();  // everyone has read rows p and k
-        // c. eliminate column q from own rows (rows k and p swapped), in
-        //    chunks of 64 rows: multipliers first, then the 2*kB updates
-        for (int64_t c0 = r0; c0 < r1; c0 += 64) {
-            const int nr = static_cast<int>(r1 - c0 < 64 ? r1 - c0 : 64);
-            for (int t = threadIdx.x; t < nr; t += blockDim.x) {
-                const int64_t i = c0 + t;
-                fs[t] = (i == k) ? 0.0 : (i == p ? krow[q] : Pn[i * 2 * kB + q]);
+        for (int t = threadIdx.x; t < kB; t += kPT) r[t] = (t == q ? 1.0 : prow[t]) * inv;
+        if (rank == 0 && threadIdx.x == 0) piv[q] = p;
+        cl.sync();  // everyone has read rows p and k before they change
+        // d. eliminate column q from own rows (rows k and p swapped); the
+        //    column becomes column k of the transform.  A warp owns a row, so
+        //    the multiplier is read before any lane overwrites it.
+        for (int il = w; il < nr; il += kPT / 32) {
+            const int64_t i = r0 + il;
+            double *row = S + static_cast<int64_t>(il) * kB;
+            const double f = (i == p) ? krow[q] : row[q];
+            __syncwarp();
+            for (int t = lane; t < kB; t += 32) {
+                if (i == k) {
+                    row[t] = r[t];
+                } else {
+                    const double old = (i == p) ? krow[t] : row[t];
+                    row[t] = (t == q) ? -f * inv : fma(-f, r[t], old);
+                }
             }
-            __syncthreads();
-            for (int e = threadIdx.x; e < nr * 2 * kB; e += blockDim.x) {
-                const int r = e / (2 * kB), t = e % (2 * kB);
-                const int64_t i = c0 + r;
-                double *dst = Pn + i * 2 * kB + t;
-                if (i == k) *dst = rk[t];
-                else *dst = fma(-fs[r], rk[t], i == p ? krow[t] : *dst);
-            }
-            __syncthreads();
         }
+        __syncthreads();
+    }
+    for (int e = threadIdx.x; e < nr * kB; e += kPT) {
+        const int i = e / kB, q = e - i * kB;
+        if (q < bk) X[(r0 + i) * ld + k0 + q] = S[e];
+    }
+    cl.sync();  // keep shared memory alive until every remote read is done
+}
+
+// Register-resident variant (default): panel width 32 = warp width.  A
+// cluster of C CTAs x 16 warps holds the n x 32 panel in registers: CTA c
+// owns rows [c*R, (c+1)*R), warp w of it rows w, w+16, ... (RPW at most),
+// lane t column t.  No cluster barrier per column: every CTA PUSHES its best
+// pivot candidate and that row into slot [rank] of every CTA's shared
+// memory, and the owner of row k pushes row k, with st.async whose bytes
+// complete a transaction count on the receiver's mbarrier (double-buffered
+// by column parity).  Each CTA waits only for its own mbarrier, then finds
+// the pivot and reads rows p and k locally and eliminates in registers.
+// Reuse of a buffer two columns later is safe: a CTA pushes column q+2 only
+// after receiving every CTA's column-q+1 push, which each sends only after
+// finishing its column-q reads.
+constexpr int kRB = 32, kMaxRW = 32;
+
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t a, int rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_async(uint32_t raddr, double v, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];"
+                 ::"r"(raddr), "l"(__double_as_longlong(v)), "r"(rbar) : "memory");
+}
+__device__ __forceinline__ void st_async2(uint32_t raddr, double v, long long i, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];"
+                 ::"r"(raddr), "l"(__double_as_longlong(v)), "l"(i), "r"(rbar) : "memory");
+}
+__device__ __forceinline__ void mbar_init_cta(uint64_t *b, unsigned cnt) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t *b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)),
+                 "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t *b, unsigned parity) {
+    unsigned done;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done) : "r"(smem_addr(b)), "r"(parity) : "memory");
+    } while (!done);
+}
+
+struct __align__(16) Cand {
+    double v;
+    long long i;
+};
+
+template <int RPW>
+__device__ __forceinline__ double pick_reg(const double (&val)[RPW], int j) {
+    double x = 0.0;
+#pragma unroll
+    for (int t = 0; t < RPW; ++t)
+        if (t == j) x = val[t];
+    return x;
+}
+
+template <int RPW>
+__device__ __forceinline__ void set_reg(double (&val)[RPW], int j, double x) {
+#pragma unroll
+    for (int t = 0; t < RPW; ++t)
+        if (t == j) val[t] = x;
+}
+
+// Exact warp argmax of v >= 0 (v < 0: no candidate) with the smallest index
+// on ties, via integer reductions on the IEEE bits (monotone for v >= 0).
+__device__ __forceinline__ void warp_argmax(double v, int idx, double &bv, int &bi) {
+    const unsigned long long b = v >= 0.0 ? static_cast<unsigned long long>(__double_as_longlong(v)) : 0ull;
+    const unsigned hi = static_cast<unsigned>(b >> 32), lo = static_cast<unsigned>(b);
+    const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+    const bool top = hi == mh && lo == ml;
+    bi = static_cast<int>(__reduce_min_sync(0xffffffffu, top ? static_cast<unsigned>(idx) : 0x7fffffffu));
+    bv = __longlong_as_double(static_cast<long long>((static_cast<unsigned long long>(mh) << 32) | ml));
+}
+
+template <int RPW, int kRW>
+__global__ void __launch_bounds__(kRW * 32, 1) k_panel_reg(int n, int64_t ld, int k0, int bk, int R,
+                                                            double *X, int64_t *piv, DevError *err) {
+    cg::cluster_group cl = cg::this_cluster();
+    __shared__ Cand cand[2][kMaxCluster];                       // pushed by CTA [src]
+    __shared__ __align__(16) double crow[2][kMaxCluster][kRB];  // their candidate rows
+    __shared__ __align__(16) double rowk[2][kRB];               // row k, from its owner
+    __shared__ uint64_t bar[2];
+    __shared__ double wv[kRW];
+    __shared__ int wi[kRW], s_b;
+    const int rank = static_cast<int>(cl.block_rank()), C = static_cast<int>(cl.num_blocks());
+    const int r0 = rank * R, r1 = min(n, r0 + R);
+    const int lane = threadIdx.x % 32, w = threadIdx.x / 32;
+    const int rw0 = r0 + w;  // row of slot j: rw0 + kRW * j
+    const int jend = r1 > rw0 ? (r1 - rw0 + kRW - 1) / kRW : 0;  // own slots [0, jend)
+    const unsigned tx = static_cast<unsigned>(C * (sizeof(Cand) + kRB * sizeof(double)) + kRB * sizeof(double));
+    if (threadIdx.x == 0) {
+        mbar_init_cta(&bar[0], 1);
+        mbar_init_cta(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    double val[RPW];  // rows past r1 stay zero through every update
+#pragma unroll
+    for (int j = 0; j < RPW; ++j)
+        val[j] = (j < jend && lane < bk) ? X[static_cast<int64_t>(rw0 + kRW * j) * ld + k0 + lane] : 0.0;
+    cl.sync();  // every CTA's barriers initialised before anyone pushes
+    for (int q = 0; q < bk; ++q) {
+        const int k = k0 + q;
+        const int buf = q & 1;
+        if (threadIdx.x == 0) mbar_expect(&bar[buf], tx);
+        // 1. the warp's candidate: lane q holds column q of the warp's rows
+        //    (slots jmin.. are rows >= k; ascending rows: first on ties)
+        const int jmin = k > rw0 ? (k - rw0 + kRW - 1) / kRW : 0;
+        double best = -1.0;
+        int bj = -1;
+        if (lane == q) {
+#pragma unroll
+            for (int j = 0; j < RPW; ++j) {
+                const double a = fabs(val[j]);
+                if (j >= jmin && j < jend && a > best) { best = a; bj = j; }
+            }
+        }
+        best = __shfl_sync(0xffffffffu, best, q);
+        bj = __shfl_sync(0xffffffffu, bj, q);
+        if (lane == 0) { wv[w] = best; wi[w] = bj >= 0 ? rw0 + kRW * bj : n; }
+        if (k >= r0 && k < r1 && (k - r0) % kRW == w) {  // the owner of row k pushes it
+            const double x = pick_reg(val, (k - rw0) / kRW);
+            const uint32_t la = smem_addr(&rowk[buf][lane]), lb = smem_addr(&bar[buf]);
+            for (int c = 0; c < C; ++c) st_async(mapa(la, c), x, mapa(lb, c));
+        }
+        __syncthreads();
+        if (w == 0) {  // the CTA's candidate, to every CTA (one lane per destination)
+            double bv;
+            int bx;
+            warp_argmax(lane < kRW ? wv[lane] : -1.0, lane < kRW ? wi[lane] : n, bv, bx);
+            if (bx >= n) bv = -1.0;
+            if (lane == 0) s_b = bx;
+            if (lane < C)
+                st_async2(mapa(smem_addr(&cand[buf][rank]), lane), bv, bx, mapa(smem_addr(&bar[buf]), lane));
+        }
+        __syncthreads();
+        const int cb = s_b;
+        if (cb < n ? (cb - r0) % kRW == w : w == 0) {  // its warp pushes the row (warp 0 if none)
+            const double x = cb < n ? pick_reg(val, (cb - rw0) / kRW) : 0.0;
+            const uint32_t la = smem_addr(&crow[buf][rank][lane]), lb = smem_addr(&bar[buf]);
+            for (int c = 0; c < C; ++c) st_async(mapa(la, c), x, mapa(lb, c));
+        }
+        mbar_wait_cluster(&bar[buf], (q >> 1) & 1);
+        // 2. global pivot (identical in every warp of every CTA), local reads
+        double gv;
+        int p;
+        warp_argmax(lane < C ? cand[buf][lane].v : -1.0, lane < C ? static_cast<int>(cand[buf][lane].i) : n,
+                    gv, p);
+        const double v = p < n ? crow[buf][p / R][q] : 0.0;
+        if (!(fabs(v) >= 1e-300)) {
+            if (rank == 0 && threadIdx.x == 0) {
+                if (atomicCAS(&err->code, 0, SAMG_ERROR) == 0) err->where = k;
+                for (int t = q; t < bk; ++t) piv[t] = k0 + t;  // keep later kernels in bounds
+            }
+            break;  // uniform across the cluster
+        }
+        const double inv = 1.0 / v;
+        const double rl = (lane == q ? 1.0 : crow[buf][p / R][lane]) * inv;
+        const double kq = rowk[buf][q], kl = rowk[buf][lane];
+        if (rank == 0 && threadIdx.x == 0) piv[q] = p;
+        // 3. eliminate column q in registers; column q becomes column k of
+        //    the transform.  Rows p and k (exchanged) are fixed up after.
+        const bool lq = lane == q;
+#pragma unroll
+        for (int j = 0; j < RPW; ++j) {
+            const double f = __shfl_sync(0xffffffffu, val[j], q);
+            val[j] = lq ? -f * inv : fma(-f, rl, val[j]);
+        }
+        if (p >= r0 && p < r1 && (p - r0) % kRW == w)
+            set_reg(val, (p - rw0) / kRW, lq ? -kq * inv : fma(-kq, rl, kl));
+        if (k >= r0 && k < r1 && (k - r0) % kRW == w) set_reg(val, (k - rw0) / kRW, rl);
+    }
+#pragma unroll
+    for (int j = 0; j < RPW; ++j)
+        if (j < jend && lane < bk) X[static_cast<int64_t>(rw0 + kRW * j) * ld + k0 + lane] = val[j];
+    cl.sync();  // no CTA exits while pushes to it may still be in flight
+}
+
+// The panel's row swaps, applied to the columns outside the panel (the
+// panel kernel already swapped inside it), are composed into at most 2*bk
+// row moves "row dst[i] receives old row src[i]" by one warp (lane l keeps
+// list slots l and l+32; a find is one ballot), then executed as a gather
+// into T and a scatter from T -- independent loads instead of bk dependent
+// swaps per column.  mv[0] = m, mv[1..64] = dst, mv[65..128] = src.
+constexpr int kMv = 2 * kMaxB;
+
+__global__ void k_moves_build(int64_t k0, int bk, const int64_t *piv, int64_t *mv) {
+    const int lane = threadIdx.x;
+    int64_t d[kMv / 32], sr[kMv / 32];
+#pragma unroll
+    for (int u = 0; u < kMv / 32; ++u) d[u] = sr[u] = -1;
+    int m = 0;
+    const int64_t pv0 = lane < bk ? piv[lane] : -1, pv1 = lane + 32 < bk ? piv[lane + 32] : -1;
+    auto find = [&](int64_t r) {
+        int at = -1;
+#pragma unroll
+        for (int u = 0; u < kMv / 32; ++u) {
+            const unsigned b = __ballot_sync(0xffffffffu, d[u] == r);
+            if (b && at < 0) at = u * 32 + __ffs(b) - 1;
+        }
+        if (at < 0) {
+            at = m++;
+            if (lane == at % 32) {
+#pragma unroll
+                for (int u = 0; u < kMv / 32; ++u)
+                    if (u == at / 32) { d[u] = r; sr[u] = r; }
+            }
+        }
+        return at;
+    };
+    auto get_src = [&](int at) {
+        int64_t x = -1;
+#pragma unroll
+        for (int u = 0; u < kMv / 32; ++u)
+            if (u == at / 32) x = sr[u];
+        return __shfl_sync(0xffffffffu, x, at % 32);
+    };
+    auto set_src = [&](int at, int64_t v) {
+        if (lane == at % 32) {
+#pragma unroll
+            for (int u = 0; u < kMv / 32; ++u)
+                if (u == at / 32) sr[u] = v;
+        }
+    };
+    for (int q = 0; q < bk; ++q) {
+        const int64_t a = k0 + q;
+        const int64_t b = __shfl_sync(0xffffffffu, q < 32 ? pv0 : pv1, q % 32);
+        if (a == b) continue;
+        const int ia = find(a), ib = find(b);
+        const int64_t sa = get_src(ia), sb = get_src(ib);
+        set_src(ia, sb);
+        set_src(ib, sa);
+    }
+    if (lane == 0) mv[0] = m;
+#pragma unroll
+    for (int u = 0; u < kMv / 32; ++u) {
+        mv[1 + u * 32 + lane] = d[u];
+        mv[1 + kMv + u * 32 + lane] = sr[u];
     }
 }
 
-// apply the panel's row swaps, in order, to columns [j0, 2n)
-__global__ void k_apply_swaps(int64_t n, int64_t j0, int64_t k0, int bk, const int64_t *piv,
-                              double *W) {
-    const int64_t ld = 2 * n;
-    for (int64_t j = j0 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < ld;
-         j += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        for (int q = 0; q < bk; ++q) {
-            const int64_t a = k0 + q, b = piv[q];
-            if (a != b) {
-                const double t = W[a * ld + j];
-                W[a * ld + j] = W[b * ld + j];
-                W[b * ld + j] = t;
-            }
-        }
-}
-
-__global__ void k_copy_rk(int64_t n, int64_t j0, int64_t k0, int bk, const double *W, double *Rk) {
-    const int64_t m = 2 * n - j0;
-    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < bk * m;
+__global__ void k_moves_gather(int64_t n, int64_t ld, const int64_t *__restrict__ mv,
+                               const double *__restrict__ X, double *__restrict__ T) {
+    const int64_t m = mv[0];
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < m * n;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t q = e / m, j = e - q * m;
-        Rk[q * m + j] = W[(k0 + q) * 2 * n + j0 + j];
+        const int64_t i = e / n, j = e - i * n;
+        T[e] = X[mv[1 + kMv + i] * ld + j];
     }
 }
 
-// W[i][j0 + j] += sum_q (Z[i][q] - delta(i, k0+q)) * Rk[q][j]; 64x64 tiles,
-// 256 threads x (4x4) outputs, K = bk <= 32 staged in shared memory.
-__global__ void __launch_bounds__(256) k_trailing(int64_t n, int64_t j0, int64_t k0, int bk,
-                                                  const double *Pn, const double *Rk, double *W) {
-    __shared__ double As[kB][64 + 1];
-    __shared__ double Bs[kB][64];
-    const int64_t m = 2 * n - j0;
-    const int64_t i0 = blockIdx.y * 64, jj0 = blockIdx.x * 64;
-    for (int t = threadIdx.x; t < kB * 64; t += 256) {
-        const int q = t / 64, r = t % 64;
-        const int64_t i = i0 + r;
-        double a = 0.0;
-        if (q < bk && i < n) a = Pn[i * 2 * kB + kB + q] - (i == k0 + q ? 1.0 : 0.0);
-        As[q][r] = a;
-        const int64_t j = jj0 + r;
-        Bs[q][r] = (q < bk && j < m) ? Rk[q * m + j] : 0.0;
+// scatter the moved rows back (outside the panel) and copy the pivot rows
+// Rk[q][j] = X[k0+q][j] (zero inside the panel): (bk + m) x n elements
+__global__ void k_moves_apply(int64_t n, int64_t ld, int64_t k0, int bk,
+                              const int64_t *__restrict__ mv, const double *__restrict__ T,
+                              double *__restrict__ X, double *__restrict__ Rk) {
+    __shared__ int slot[kMaxB];
+    const int64_t m = mv[0];
+    for (int q = threadIdx.x; q < bk; q += blockDim.x) {
+        slot[q] = -1;
+        for (int i = 0; i < m; ++i)
+            if (mv[1 + i] == k0 + q) slot[q] = i;
     }
     __syncthreads();
-    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-    double acc[4][4] = {};
-    for (int q = 0; q < bk; ++q) {
-        double a[4], b[4];
-        for (int u = 0; u < 4; ++u) { a[u] = As[q][ty + 16 * u]; b[u] = Bs[q][tx + 16 * u]; }
-        for (int u = 0; u < 4; ++u)
-            for (int v = 0; v < 4; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
-    }
-    for (int u = 0; u < 4; ++u) {
-        const int64_t i = i0 + ty + 16 * u;
-        if (i >= n) continue;
-        for (int v = 0; v < 4; ++v) {
-            const int64_t j = jj0 + tx + 16 * v;
-            if (j < m) W[i * 2 * n + j0 + j] += acc[u][v];
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < (bk + m) * n;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = e / n, j = e - r * n;
+        const bool in_panel = j >= k0 && j < k0 + bk;
+        if (r < bk) {
+            const int sl = slot[r];
+            Rk[e] = in_panel ? 0.0 : (sl >= 0 ? T[sl * n + j] : X[(k0 + r) * ld + j]);
+        } else if (!in_panel) {
+            const int64_t i = r - bk;
+            X[mv[1 + i] * ld + j] = T[i * n + j];
         }
     }
 }
 
-__global__ void k_copy_right(int64_t n, int64_t ld, const double *W, double *Ainv) {
+__device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
+
+// X[i][j] += sum_q (Z[i][q] - delta(i, k0+q)) Rk[q][j] for every column j
+// outside the panel (Z = X[:, K]).  64x64 tile per CTA, 4 warps x 32x32,
+// FP64 tensor-core MMA (m8n8k4), K staged in shared memory 32 at a time.
+constexpr int kTT = 64, kTP = 4, kKC = 32, kTThreads = 256;  // tile, smem pad, K chunk
+__global__ void __launch_bounds__(kTThreads, 2) k_trailing(int64_t n, int64_t ld, int64_t k0, int bk,
+                                                           const double *__restrict__ Rk, double *X) {
+    __shared__ double As[kKC][kTT + kTP];  // As[q][r] = Z[i0+r][kc+q] - delta
+    __shared__ double Bs[kKC][kTT + kTP];  // Bs[q][c] = Rk[kc+q][j0+c]
+    const int64_t i0 = static_cast<int64_t>(blockIdx.y) * kTT, j0 = static_cast<int64_t>(blockIdx.x) * kTT;
+    const int lane = threadIdx.x % 32, wid = threadIdx.x / 32;
+    const int g = lane >> 2, t = lane & 3;
+    const int wm = (wid >> 2) * 32, wn = (wid & 3) * 16;  // 2 x 4 warps of 32 x 16
+    double acc[4][2][2] = {};
+    // the output tile's current values, requested first so their (DRAM)
+    // latency overlaps the operand loads and the MMAs
+    double2 xo[4][2];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) {
+            const int64_t i = i0 + wm + mi * 8 + g, j = j0 + wn + ni * 8 + 2 * t;
+            xo[mi][ni] = (i < n && j < n) ? *reinterpret_cast<const double2 *>(X + i * ld + j)
+                                          : make_double2(0.0, 0.0);
+        }
+    for (int kc = 0; kc < bk; kc += kKC) {
+        const int kn = min(kKC, bk - kc), kq = (kn + 3) & ~3;  // rows kn..kq of the stage are zero
+        if (kc) __syncthreads();
+        // all loads of the stage in flight at once (the panel columns are
+        // never written by this kernel: read-only path)
+        constexpr int kPer = kKC * kTT / kTThreads;
+        double la[kPer], lb[kPer];
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            const int e = threadIdx.x + kTThreads * u;
+            const int rr = e / kKC, q = e - rr * kKC;  // consecutive threads: one row's columns
+            const int64_t i = i0 + rr;
+            la[u] = (q < kn && i < n) ? __ldg(X + i * ld + k0 + kc + q) - (i == k0 + kc + q ? 1.0 : 0.0) : 0.0;
+            const int qb = e / kTT, c = e - qb * kTT;
+            const int64_t j = j0 + c;
+            lb[u] = (qb < kn && j < n) ? __ldg(Rk + (kc + qb) * n + j) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            const int e = threadIdx.x + kTThreads * u;
+            As[e % kKC][e / kKC] = la[u];
+            Bs[e / kTT][e % kTT] = lb[u];
+        }
+        __syncthreads();
+        for (int k = 0; k < kq; k += 4) {
+            double a[4], b[2];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi) a[mi] = As[k + t][wm + mi * 8 + g];
+#pragma unroll
+            for (int ni = 0; ni < 2; ++ni) b[ni] = Bs[k + t][wn + ni * 8 + g];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+        }
+    }
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) {
+        const int64_t i = i0 + wm + mi * 8 + g;
+        if (i >= n) continue;
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) {
+            const int64_t j = j0 + wn + ni * 8 + 2 * t;  // even: 16-byte aligned pair
+            if (j >= n) continue;
+            double2 *dst = reinterpret_cast<double2 *>(X + i * ld + j);
+            double2 v = xo[mi][ni];
+            const bool p0 = !(j >= k0 && j < k0 + bk), p1 = !(j + 1 >= k0 && j + 1 < k0 + bk);
+            if (p0) v.x += acc[mi][ni][0];
+            if (p1 && j + 1 < n) v.y += acc[mi][ni][1];
+            *dst = v;
+        }
+    }
+}
+
+__global__ void k_gather_cols(int64_t n, int64_t ld, const int64_t *perm, const double *X,
+                              double *Ainv) {
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n * ld;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t i = e / ld, j = e - i * ld;
-        Ainv[e] = j < n ? W[i * 2 * n + n + j] : 0.0;
+        Ainv[e] = j < n ? X[i * ld + perm[j]] : 0.0;
     }
+}
+
+__global__ void k_copy_piv(int bk, const int64_t *piv, int64_t *dst) {
+    if (threadIdx.x < bk) dst[threadIdx.x] = piv[threadIdx.x];
 }
 
 int grid_for(int64_t work) {
     const int64_t g = (work + 255) / 256;
     return static_cast<int>(g < 8192 ? (g > 0 ? g : 1) : 8192);
+}
+
+struct PanelPlan {
+    bool reg;      // register-resident kernel (k_panel_reg<rpw, nw>) or shared-memory one
+    int kB, C, R, rpw, smem, nw;
+};
+
+int cluster_limit(const void *kern, int threads, int smem) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(kMaxCluster);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at{};
+    at.id = cudaLaunchAttributeClusterDimension;
+    at.val.clusterDim.x = kMaxCluster;
+    at.val.clusterDim.y = 1;
+    at.val.clusterDim.z = 1;
+    cfg.attrs = &at;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    const bool ok = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                        cudaSuccess &&
+                    cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg) == cudaSuccess &&
+                    nclusters >= 1;
+    cudaGetLastError();
+    return ok ? kMaxCluster : 8;
+}
+
+// (rows per warp, warps per CTA) instantiations of k_panel_reg
+template <class F>
+void dispatch_rpw(int rpw, int nw, F f) {
+    using std::integral_constant;
+    if (nw == 32) {
+        if (rpw <= 4) f(integral_constant<int, 4>{}, integral_constant<int, 32>{});
+        else if (rpw <= 6) f(integral_constant<int, 6>{}, integral_constant<int, 32>{});
+        else f(integral_constant<int, 8>{}, integral_constant<int, 32>{});
+        return;
+    }
+    if (rpw <= 12) f(integral_constant<int, 12>{}, integral_constant<int, 16>{});
+    else if (rpw <= 16) f(integral_constant<int, 16>{}, integral_constant<int, 16>{});
+    else if (rpw <= 24) f(integral_constant<int, 24>{}, integral_constant<int, 16>{});
+    else f(integral_constant<int, 32>{}, integral_constant<int, 16>{});
+}
+
+PanelPlan plan_panel(int64_t n) {
+    static int reg_cluster = -1, smem_cluster = -1, smem_cap = 0;
+    if (reg_cluster < 0) {
+        int dev = 0;
+        CK(cudaGetDevice(&dev));
+        CK(cudaDeviceGetAttribute(&smem_cap, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        smem_cap -= 4096;  // static shared memory of the kernel
+        CK(cudaFuncSetAttribute(k_panel_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap));
+        smem_cluster = cluster_limit(reinterpret_cast<const void *>(k_panel_cluster), kPT, smem_cap);
+        reg_cluster = cluster_limit(reinterpret_cast<const void *>(k_panel_reg<8, 32>), 32 * 32, 0);
+    }
+    static const bool force_smem = [] {
+        const char *e = std::getenv("SAMG_GJ_SMEM_PANEL");
+        return e && e[0] == '1';
+    }();
+    // register panel: 16 warps per CTA (measured faster than 32 on C1: 69 vs 81 us per panel)
+    static const int nw_env = [] {
+        const char *e = std::getenv("SAMG_GJ_WARPS");
+        return e ? std::atoi(e) : 0;
+    }();
+    for (int nw : {16, 32}) {
+        if (nw_env && nw != nw_env) continue;
+        const int C = static_cast<int>(std::min<int64_t>(reg_cluster, std::max<int64_t>(1, (n + 2 * nw - 1) / (2 * nw))));
+        const int64_t R = (n + C - 1) / C;
+        const int64_t rpw = (R + nw - 1) / nw;
+        if (!force_smem && rpw <= (nw == 32 ? 8 : 32))
+            return {true, kRB, C, static_cast<int>(R), static_cast<int>(rpw), 0, nw};
+    }
+    for (int kB = kMaxB; kB >= 8; kB /= 2) {
+        const int C = static_cast<int>(std::min<int64_t>(smem_cluster, std::max<int64_t>(1, (n + 63) / 64)));
+        const int64_t R = (n + C - 1) / C;
+        const int64_t smem = R * kB * static_cast<int64_t>(sizeof(double));
+        if (smem <= smem_cap) return {false, kB, C, static_cast<int>(R), 0, static_cast<int>(smem), 0};
+    }
+    fail(SAMG_UNSUPPORTED, "dense coarse solve: coarsest level too large (" + std::to_string(n) +
+                               " unknowns) for the cluster-resident panel");
 }
 
 } // namespace
@@ -241,44 +648,64 @@ void dense_inverse(const Bsr3 &A, DevBuf<double> &Ainv, DevError *err, cudaStrea
     const int64_t ld = dense_ld(n);
     Ainv.alloc(n * ld, s);
     if (n == 0) return;
-    DevBuf<double> W(2 * n * n, s), Pn(n * 2 * kB, s), Rk(static_cast<int64_t>(kB) * 2 * n, s);
-    int dev = 0, nsm = 148, coop = 0, per_sm = 0;
-    CK(cudaGetDevice(&dev));
-    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
-    if (!coop) fail(SAMG_UNSUPPORTED, "dense coarse solve needs cooperative launch");
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_panel_gj, kPT, 0));
-    // panel CTAs: fewer CTAs make the two grid barriers per column cheaper,
-    // more CTAs spread the row updates (SAMG_GJ_CTAS overrides)
-    static const int64_t gj_ctas = [] {
-        const char *e = std::getenv("SAMG_GJ_CTAS");
-        return e ? std::atoll(e) : 128;
-    }();
-    const int pgrid = static_cast<int>(std::max<int64_t>(
-        1, std::min<int64_t>({static_cast<int64_t>(nsm) * std::max(per_sm, 1), (n + 15) / 16, gj_ctas})));
-    DevBuf<double> pval(pgrid, s);
-    DevBuf<int64_t> pidx(pgrid, s), piv(kB, s);
-    CK(cudaMemsetAsync(W.p, 0, W.bytes(), s));
+    const PanelPlan pp = plan_panel(n);
+    DevBuf<double> X(n * ld, s), Rk(static_cast<int64_t>(pp.kB) * n + 1, s),
+        T(static_cast<int64_t>(2 * pp.kB) * n + 1, s);
+    DevBuf<int64_t> piv(pp.kB, s), piv_all(n, s), perm(n, s), mv(1 + 2 * kMv, s);
+    CK(cudaMemsetAsync(X.p, 0, X.bytes(), s));
     k_scatter<<<ceil_div(A.nrows, 128), 128, 0, s>>>(static_cast<int>(A.nrows), A.ptr.p, A.col.p,
-                                                    A.val.p, n, W.p);
+                                                    A.val.p, ld, X.p);
     CK_LAUNCH();
-    for (int64_t k0 = 0; k0 < n; k0 += kB) {
-        int bk = static_cast<int>(std::min<int64_t>(kB, n - k0));
-        k_panel_load<<<grid_for(n * 2 * kB), 256, 0, s>>>(n, k0, bk, W.p, Pn.p);
-        int64_t nn = n, kk0 = k0;
-        double *pp = Pn.p, *pv = pval.p;
-        int64_t *pi = pidx.p, *pvt = piv.p;
-        DevError *e = err;
-        void *args[] = {&nn, &kk0, &bk, &pp, &pv, &pi, &pvt, &e};
-        CK(cudaLaunchCooperativeKernel(reinterpret_cast<void *>(k_panel_gj), pgrid, kPT, args, 0, s));
-        const int64_t j0 = k0 + bk, m = 2 * n - j0;
-        k_apply_swaps<<<grid_for(m), 256, 0, s>>>(n, j0, k0, bk, piv.p, W.p);
-        k_copy_rk<<<grid_for(bk * m), 256, 0, s>>>(n, j0, k0, bk, W.p, Rk.p);
-        dim3 tg(static_cast<unsigned>((m + 63) / 64), static_cast<unsigned>((n + 63) / 64));
-        k_trailing<<<tg, 256, 0, s>>>(n, j0, k0, bk, Pn.p, Rk.p, W.p);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(pp.C);
+    cfg.blockDim = dim3(pp.reg ? pp.nw * 32 : kPT);
+    cfg.dynamicSmemBytes = pp.smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at{};
+    at.id = cudaLaunchAttributeClusterDimension;
+    at.val.clusterDim.x = pp.C;
+    at.val.clusterDim.y = 1;
+    at.val.clusterDim.z = 1;
+    cfg.attrs = &at;
+    cfg.numAttrs = 1;
+    const dim3 tg(static_cast<unsigned>((n + kTT - 1) / kTT), static_cast<unsigned>((n + kTT - 1) / kTT));
+    for (int64_t k0 = 0; k0 < n; k0 += pp.kB) {
+        const int bk = static_cast<int>(std::min<int64_t>(pp.kB, n - k0));
+        if (pp.reg) {
+            dispatch_rpw(pp.rpw, pp.nw, [&](auto r, auto nw) {
+                constexpr int RPW = decltype(r)::value, NW = decltype(nw)::value;
+                static const bool nonportable = [] {
+                    const bool ok = cudaFuncSetAttribute(k_panel_reg<RPW, NW>,
+                                        cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
+                    cudaGetLastError();
+                    return ok;
+                }();
+                (void)nonportable;
+                CK(cudaLaunchKernelEx(&cfg, k_panel_reg<RPW, NW>, static_cast<int>(n), ld,
+                                      static_cast<int>(k0), bk, pp.R, X.p, piv.p, err));
+            });
+        } else {
+            CK(cudaLaunchKernelEx(&cfg, k_panel_cluster, n, ld, k0, bk, pp.kB, pp.R, X.p, piv.p, err));
+        }
+        k_copy_piv<<<1, kMaxB, 0, s>>>(bk, piv.p, piv_all.p + k0);
+        k_moves_build<<<1, 32, 0, s>>>(k0, bk, piv.p, mv.p);
+        k_moves_gather<<<grid_for(2 * bk * n), 256, 0, s>>>(n, ld, mv.p, X.p, T.p);
+        k_moves_apply<<<grid_for(3 * bk * n), 256, 0, s>>>(n, ld, k0, bk, mv.p, T.p, X.p, Rk.p);
+        k_trailing<<<tg, kTThreads, 0, s>>>(n, ld, k0, bk, Rk.p, X.p);
         CK_LAUNCH();
     }
-    k_copy_right<<<grid_for(n * ld), 256, 0, s>>>(n, ld, W.p, Ainv.p);
+    // column permutation of the in-place algorithm: every swap undone in
+    // reverse order (composed on the host, n steps)
+    std::vector<int64_t> hp(n), hperm(n);
+    CK(cudaMemcpyAsync(hp.data(), piv_all.p, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int64_t j = 0; j < n; ++j) hperm[j] = j;
+    for (int64_t k = n - 1; k >= 0; --k) {
+        const int64_t p = std::min<int64_t>(std::max<int64_t>(hp[k], 0), n - 1);
+        std::swap(hperm[k], hperm[p]);
+    }
+    CK(cudaMemcpyAsync(perm.p, hperm.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
+    k_gather_cols<<<grid_for(n * ld), 256, 0, s>>>(n, ld, perm.p, X.p, Ainv.p);
     CK_LAUNCH();
     check_dev_error(err, s);
 }

@@ -75,6 +75,10 @@ constexpr int kWarp = 32;
 
 inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
 
+// Host -> device copy on stream s; large pageable sources are staged through
+// a pinned buffer pool by parallel host threads (hostcopy.cpp).
+void h2d(void *dst, const void *src, size_t bytes, cudaStream_t s);
+
 // SM count of the current device (cached per process).
 int sm_count();
 

@@ -77,6 +77,21 @@ Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int6
     CK(cudaMemsetAsync(H->err.p, 0, sizeof(DevError), s));
     DevError *err = H->err.p;
 
+    // SAMG_SETUP_TIMING=1: per-phase wall times on stderr (synchronises
+    // after every phase; diagnosis only)
+    static const bool timing = [] {
+        const char *e = std::getenv("SAMG_SETUP_TIMING");
+        return e && e[0] == '1';
+    }();
+    double t_mark = t_start;
+    auto mark = [&](const char *what, size_t level) {
+        if (!timing) return;
+        CK(cudaStreamSynchronize(s));
+        const double t = now_s();
+        std::fprintf(stderr, "setup L%zu %-12s %8.3f ms\n", level, what, 1e3 * (t - t_mark));
+        t_mark = t;
+    };
+    mark("upload", 0);
     const int k = static_cast<int>(b_cols);
     DevBuf<double> B(b_rows * b_cols, s);
     CK(cudaMemcpyAsync(B.p, B_host, sizeof(double) * b_rows * b_cols, cudaMemcpyHostToDevice, s));
@@ -94,27 +109,35 @@ Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int6
         if (Li.A.nrows % h)
             fail(SAMG_NOT_DIVISIBLE, "strength_graph: rows not divisible by point block size");
         Graph G;
+        const size_t lvl = H->levels.size() - 1;
         strength_graph(Li.A, h, prm.eps_strong, G, s);
+        mark("strength", lvl);
         DevBuf<int> agg;
         DevBuf<int> seedno;
         const int64_t naggs = aggregate(G, agg, s, &seedno);
+        mark("aggregate", lvl);
         DevBuf<double> Pt, Bc;
         tentative(agg, G.nnodes, naggs, pbs, B.p, k, Pt, Bc, err, s);
+        mark("tentative", lvl);
         Bsr3 P;
         smooth_prolongation(Li.A, G, agg, naggs, pbs, k, Pt.p, prm.omega, P, err, s);
         check_dev_error(err, s);
+        mark("smooth_P", lvl);
         // stagnation guard (hierarchy.hpp:355)
         if (static_cast<double>(3 * P.ncols) >
             prm.stagnation_ratio * static_cast<double>(3 * Li.A.nrows))
             break;
         Bsr3 R;
         transpose(P, R, s);
+        mark("transpose", lvl);
         // Galerkin (csr.hpp:259-262) + fix_decoupled_rows (hierarchy.hpp:357)
         Bsr3 RA, Ac;
         spgemm(R, Li.A, RA, s);
+        mark("spgemm_RA", lvl);
         spgemm(RA, P, Ac, s);
         RA = Bsr3();
         fix_decoupled_rows(Ac, s);
+        mark("spgemm_RAP", lvl);
         Li.P = std::move(P);
         Li.R = std::move(R);
         Li.has_transfer = true;
@@ -132,8 +155,10 @@ Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int6
     for (size_t i = 0; i + 1 < L; ++i)
         setup_smoother(H->levels[i].A, prm.smoother, prm.smoother_omega, H->levels[i].M, err, s);
     check_dev_error(err, s);
+    mark("smoothers", L - 1);
     H->nc = 3 * H->levels.back().A.nrows;
     dense_inverse(H->levels.back().A, H->Ainv, err, s);
+    mark("dense_inv", L - 1);
     // V-cycle / CG workspace
     for (size_t i = 0; i < L; ++i) {
         Level &lv = H->levels[i];
@@ -151,6 +176,7 @@ Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int6
     CK(cudaMallocHost(&H->sc_host, sizeof(CgScalars)));
     CK(cudaMallocHost(&H->sc_stage, sizeof(CgScalars)));
     CK(cudaStreamSynchronize(s));
+    mark("workspace", L - 1);
     H->setup_seconds = now_s() - t_start;
     H->owns_stream = true;
     return H.release();

@@ -1,0 +1,116 @@
+// hostcopy.cpp -- host->device copies of pageable user arrays.
+//
+// The C-ABI takes plain host pointers (the reference's csr arrays), which
+// are pageable: a direct cudaMemcpyAsync from them runs at ~11 GB/s on the
+// B200 hosts (measured, scripts/h2d_probe.py) versus ~55 GB/s from pinned
+// memory.  Large copies are therefore staged: T host threads each own two
+// pinned chunk buffers, copy their chunks of the source into them
+// (memcpy runs in parallel on the host) and issue the DMA from pinned
+// memory on the caller's stream; a buffer is reused once the event recorded
+// after its DMA has completed.  The pinned pool is allocated on first use
+// and kept for the life of the process.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <exception>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "common.cuh"
+
+namespace samgb {
+
+namespace {
+
+constexpr size_t kChunk = 8u << 20;     // bytes per staging buffer
+constexpr int kThreads = 6;
+constexpr size_t kDirect = 4u << 20;    // below this: plain cudaMemcpyAsync
+
+struct Pool {
+    std::mutex mu;                       // one staged copy at a time
+    bool ready = false;
+    int device = -1;
+    char *buf[kThreads][2] = {};
+    cudaEvent_t ev[kThreads][2] = {};
+
+    void init() {
+        int dev = 0;
+        CK(cudaGetDevice(&dev));
+        if (ready && dev == device) return;
+        release();
+        for (int t = 0; t < kThreads; ++t)
+            for (int b = 0; b < 2; ++b) {
+                CK(cudaHostAlloc(reinterpret_cast<void **>(&buf[t][b]), kChunk, cudaHostAllocPortable));
+                CK(cudaEventCreateWithFlags(&ev[t][b], cudaEventDisableTiming));
+            }
+        device = dev;
+        ready = true;
+    }
+    void release() {
+        for (int t = 0; t < kThreads; ++t)
+            for (int b = 0; b < 2; ++b) {
+                if (buf[t][b]) cudaFreeHost(buf[t][b]);
+                if (ev[t][b]) cudaEventDestroy(ev[t][b]);
+                buf[t][b] = nullptr;
+                ev[t][b] = nullptr;
+            }
+        ready = false;
+    }
+};
+
+Pool &pool() {
+    static Pool *p = new Pool;  // never destroyed: outlives static CUDA teardown
+    return *p;
+}
+
+} // namespace
+
+void h2d(void *dst, const void *src, size_t bytes, cudaStream_t s) {
+    if (bytes == 0) return;
+    cudaPointerAttributes pa{};
+    const bool pinned = cudaPointerGetAttributes(&pa, src) == cudaSuccess &&
+                        (pa.type == cudaMemoryTypeHost || pa.type == cudaMemoryTypeDevice ||
+                         pa.type == cudaMemoryTypeManaged);
+    cudaGetLastError();
+    if (bytes < kDirect || pinned) {
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+        return;
+    }
+    Pool &P = pool();
+    std::lock_guard<std::mutex> lock(P.mu);
+    P.init();
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    const size_t nchunks = (bytes + kChunk - 1) / kChunk;
+    const int T = static_cast<int>(std::min<size_t>(kThreads, nchunks));
+    std::vector<std::exception_ptr> errs(T);
+    auto work = [&](int t) {
+        try {
+            CK(cudaSetDevice(dev));
+            int b = 0;
+            for (size_t c = t; c < nchunks; c += T, b ^= 1) {
+                const size_t off = c * kChunk, n = std::min(kChunk, bytes - off);
+                CK(cudaEventSynchronize(P.ev[t][b]));  // previous DMA from this buffer done
+                std::memcpy(P.buf[t][b], static_cast<const char *>(src) + off, n);
+                CK(cudaMemcpyAsync(static_cast<char *>(dst) + off, P.buf[t][b], n,
+                                   cudaMemcpyHostToDevice, s));
+                CK(cudaEventRecord(P.ev[t][b], s));
+            }
+        } catch (...) {
+            errs[t] = std::current_exception();
+        }
+    };
+    std::vector<std::thread> th;
+    for (int t = 1; t < T; ++t) th.emplace_back(work, t);
+    work(0);
+    for (auto &x : th) x.join();
+    for (auto &e : errs)
+        if (e) std::rethrow_exception(e);
+    // the pinned buffers are reused by the next call only after their
+    // events; the caller's stream already orders the copies before its
+    // next work
+}
+
+} // namespace samgb

@@ -584,23 +584,18 @@ int env_int(const char *name, int dflt) {
 
 // Variant 3 launch; false if the matrix does not suit it (then the caller
 // uses the register-streaming kernel).
-template <int G_, int TW_, int NT_>
+template <int G_>
 struct TmaShape {
-    static constexpr int G = G_, TW = TW_, NT = NT_;
+    static constexpr int G = G_, TW = 8, NT = 2;
 };
 
-// (lanes per row, warps per team, teams); SAMG_TMA_CFG selects one
-constexpr int kTmaShapes[][3] = {{8, 8, 2}, {8, 4, 3}, {8, 4, 4}, {16, 4, 4}, {16, 8, 3}, {8, 8, 1}};
-
 template <class F>
-void dispatch_tma_shape(int k, F f) {
-    switch (k) {
-        case 1: f(TmaShape<8, 4, 3>{}); break;
-        case 2: f(TmaShape<8, 4, 4>{}); break;
-        case 3: f(TmaShape<16, 4, 4>{}); break;
-        case 4: f(TmaShape<16, 8, 3>{}); break;
-        case 5: f(TmaShape<8, 8, 1>{}); break;
-        default: f(TmaShape<8, 8, 2>{}); break;
+void dispatch_tma_shape(int G, F f) {
+    switch (G) {
+        case 4: f(TmaShape<4>{}); break;
+        case 16: f(TmaShape<16>{}); break;
+        case 32: f(TmaShape<32>{}); break;
+        default: f(TmaShape<8>{}); break;
     }
 }
 
@@ -611,10 +606,14 @@ bool launch_tma(const Bsr3 &A, const double *x, Epi epi, double *partials, CgSca
     if ((reinterpret_cast<uintptr_t>(A.val.p) | reinterpret_cast<uintptr_t>(A.col.p) |
          reinterpret_cast<uintptr_t>(A.ptr.p)) & 15)
         return false;
-    static const int shape = std::min(std::max(env_int("SAMG_TMA_CFG", 0), 0), 5);
+    static const int forced_g = env_int("SAMG_TMA_G", 0);
     static const int budget = env_int("SAMG_TMA_SMEM", 226000);
-    const int G = kTmaShapes[shape][0], TW = kTmaShapes[shape][1], NT = kTmaShapes[shape][2];
+    constexpr int TW = 8, NT = 2;  // two teams of 8 consumer warps (measured best on C1)
     const double bpr = static_cast<double>(A.nnzb) / A.nrows;
+    // ~3 blocks per lane (C1 fine level, 26 blocks per row: G = 8)
+    int G = 4;
+    while (G < 32 && 3.3 * G * 1.5 < bpr) G *= 2;
+    if (forced_g == 4 || forced_g == 8 || forced_g == 16 || forced_g == 32) G = forced_g;
     const int rpc = 32 * TW / G;
     auto up = [](long long b) { return static_cast<unsigned>((b + 127) / 128 * 128); };
     const long long est = static_cast<long long>(std::ceil(bpr * 1.1)) + 1;
@@ -636,11 +635,11 @@ bool launch_tma(const Bsr3 &A, const double *x, Epi epi, double *partials, CgSca
         return n;
     }();
     // one persistent CTA per SM only pays off when every CTA streams many
-    // chunks (C1: fine level 8 064 chunks -> TMA; level 1: 645 -> variant 1)
-    static const int min_chunks_per_sm = env_int("SAMG_TMA_MIN_CHUNKS", 16);
+    // chunks (C1: fine level 8 064 chunks, P0 4 032 -> TMA; A1 2 580 -> variant 1)
+    static const int min_chunks_per_sm = env_int("SAMG_TMA_MIN_CHUNKS", 24);
     if (cfg.nchunks < min_chunks_per_sm * sms) return false;
     bool ok = false;
-    dispatch_tma_shape(shape, [&](auto sh) {
+    dispatch_tma_shape(G, [&](auto sh) {
         using Sh = decltype(sh);
         auto kern = k_bsr3_tma<Sh::G, Sh::TW, Sh::NT, kReduce, Epi>;
         const int threads = 32 * (Sh::TW * Sh::NT + 1);
