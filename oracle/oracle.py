@@ -299,6 +299,7 @@ class Ref(_Backend):
         lib.ref_level_matrix.argtypes = [vp, C.c_int, C.c_int, i64p, i64p, C.POINTER(i64p),
                                          C.POINTER(i64p), C.POINTER(f64p)]
         lib.ref_aggregates.argtypes = [vp, C.c_int, i64p, C.POINTER(i64p), i64p]
+        lib.ref_ilu_factors.argtypes = [vp, C.c_int, i64p, i64p, C.POINTER(f64p), C.POINTER(f64p)]
         lib.ref_vcycle.argtypes = [vp, f64p, f64p]
         lib.ref_cg_solve.argtypes = [vp, f64p, f64p, C.c_double, C.c_int, C.POINTER(C.c_int),
                                      f64p, C.POINTER(C.c_int), f64p]
@@ -401,6 +402,15 @@ class RefHier:
         nnz = int(np.ctypeslib.as_array(ptr, shape=(nrows + 1,))[nrows])
         return (nrows, nc.value, _copy(ptr, nrows + 1, np.int64), _copy(col, nnz, np.int64),
                 _copy(val, nnz * 9, np.float64).reshape(-1, 3, 3))
+
+    def ilu(self, l):
+        """[factors (9*nnzb) | inverted pivots (9*nrows)] of level l's ilu0<block3>"""
+        nz, nr = C.c_int64(), C.c_int64()
+        lp, ip = f64p(), f64p()
+        if self.be.lib.ref_ilu_factors(self.h, l, C.byref(nz), C.byref(nr), C.byref(lp), C.byref(ip)):
+            raise KeyError(l)
+        return np.concatenate([np.ctypeslib.as_array(lp, (9 * nz.value,)).copy(),
+                               np.ctypeslib.as_array(ip, (9 * nr.value,)).copy()])
 
     def aggregates(self, l):
         nn, cnt, idp = C.c_int64(), C.c_int64(), i64p()

@@ -261,6 +261,20 @@ int ref_level_matrix(void *hp, int level, int which, int64_t *nrows,
     return 0;
 }
 
+// ilu0<block3> factors and inverted pivots of a level (relaxation.hpp:90-92)
+int ref_ilu_factors(void *hp, int level, int64_t *nnz, int64_t *nrows, const double **lu,
+        const double **inv) {
+    auto *h = static_cast<ref_handle *>(hp);
+    if (level < 0 || level + 1 >= h->H.nlevels()) return 1;
+    const auto *sm = std::get_if<ilu0<block3>>(&h->H.levels[level].smoother);
+    if (!sm) return 1;
+    *nnz = static_cast<int64_t>(sm->factors().val.size());
+    *nrows = static_cast<int64_t>(sm->inverted_pivots().size());
+    *lu = reinterpret_cast<const double *>(sm->factors().val.data());
+    *inv = reinterpret_cast<const double *>(sm->inverted_pivots().data());
+    return 0;
+}
+
 int ref_aggregates(void *hp, int level, int64_t *nnodes, const int64_t **id,
         int64_t *count) {
     auto *h = static_cast<ref_handle *>(hp);

@@ -749,6 +749,81 @@ static void setup_block_smoother(orc_level *L, int kind, double omega) {
     }
 }
 
+/* ilu0<block3> ctor (relaxation.hpp:103-136): IKJ elimination restricted
+ * to A's pattern, L_ik = A_ik * inverse(U_kk), inverted pivots.  The
+ * smoother data is [factors (9*nnz) | inverted pivots (9*nrows)]. */
+static void setup_ilu0(orc_level *L) {
+    const orc_mat *A = &L->A;
+    const int64_t n = A->nrows, nnz = A->ptr[n];
+    if (A->nrows != A->ncols) fail(ORC_NON_SQUARE, "ilu0: matrix must be square");
+    L->sm_len = 9 * (nnz + n);
+    L->sm = xcalloc(L->sm_len, sizeof(double));
+    double *lu = L->sm, *inv = L->sm + 9 * nnz;
+    memcpy(lu, A->val, sizeof(double) * 9 * nnz);
+    int64_t *dpos = xmalloc(sizeof(int64_t) * (n + 1)), *pos = xmalloc(sizeof(int64_t) * (n + 1));
+    for (int64_t i = 0; i < n; ++i) {
+        dpos[i] = -1;
+        pos[i] = -1;
+        for (int64_t j = A->ptr[i]; j < A->ptr[i + 1]; ++j)
+            if (A->col[j] == i) dpos[i] = j;
+    }
+    for (int64_t i = 0; i < n; ++i)
+        if (dpos[i] < 0) fail(ORC_MISSING_DIAGONAL, "ilu0: structurally zero diagonal");
+    for (int64_t i = 0; i < n; ++i) {
+        for (int64_t j = A->ptr[i]; j < A->ptr[i + 1]; ++j) pos[A->col[j]] = j;
+        for (int64_t j = A->ptr[i]; j < dpos[i]; ++j) {
+            const int64_t k = A->col[j];
+            double lik[9], prod[9];
+            blk_mul(lu + 9 * j, inv + 9 * k, lik);
+            memcpy(lu + 9 * j, lik, sizeof lik);
+            for (int64_t l = dpos[k] + 1; l < A->ptr[k + 1]; ++l) {
+                const int64_t q = pos[A->col[l]];
+                if (q < 0) continue;
+                blk_mul(lik, lu + 9 * l, prod);
+                for (int e = 0; e < 9; ++e) lu[9 * q + e] -= prod[e];
+            }
+        }
+        blk_inverse(lu + 9 * dpos[i], inv + 9 * i);
+        for (int64_t j = A->ptr[i]; j < A->ptr[i + 1]; ++j) pos[A->col[j]] = -1;
+    }
+    free(dpos);
+    free(pos);
+}
+
+/* ilu0::solve_in_place (relaxation.hpp:44-88): forward with the unit lower
+ * factor, backward with the upper factor and the inverted pivots. */
+static void ilu0_solve(const orc_level *L, double *r) {
+    const orc_mat *A = &L->A;
+    const int64_t n = A->nrows, nnz = A->ptr[n];
+    const double *lu = L->sm, *inv = L->sm + 9 * nnz;
+    for (int64_t i = 0; i < n; ++i) {
+        double *ri = r + 3 * i;
+        for (int64_t j = A->ptr[i]; j < A->ptr[i + 1] && A->col[j] < i; ++j) {
+            const double *rj = r + 3 * A->col[j], *b = lu + 9 * j;
+            for (int p = 0; p < 3; ++p)
+                for (int q = 0; q < 3; ++q) ri[p] -= b[p * 3 + q] * rj[q];
+        }
+    }
+    for (int64_t i = n - 1; i >= 0; --i) {
+        double *ri = r + 3 * i;
+        int64_t dg = -1;
+        for (int64_t j = A->ptr[i]; j < A->ptr[i + 1]; ++j)
+            if (A->col[j] == i) dg = j;
+        for (int64_t j = dg + 1; j < A->ptr[i + 1]; ++j) {
+            const double *rj = r + 3 * A->col[j], *b = lu + 9 * j;
+            for (int p = 0; p < 3; ++p)
+                for (int q = 0; q < 3; ++q) ri[p] -= b[p * 3 + q] * rj[q];
+        }
+        const double *d = inv + 9 * i;
+        double t[3];
+        for (int p = 0; p < 3; ++p) {
+            t[p] = 0;
+            for (int q = 0; q < 3; ++q) t[p] += d[p * 3 + q] * ri[q];
+        }
+        for (int p = 0; p < 3; ++p) ri[p] = t[p];
+    }
+}
+
 /* dense_lu ctor (hierarchy.hpp:90-111) */
 static void dense_lu_factor(orc_hier *H, const orc_mat *Ac) {
     orc_mat S = to_scalar(Ac);
@@ -870,6 +945,7 @@ int orc_setup_ns_block(int64_t n, const int64_t *ptr, const int64_t *col,
     free(Bi);
     for (int l = 0; l + 1 < H->nlev; ++l) {
         if (prm->smoother == ORC_SM_JACOBI) setup_point_jacobi(&H->lv[l]);
+        else if (prm->smoother == ORC_SM_ILU0) setup_ilu0(&H->lv[l]);
         else setup_block_smoother(&H->lv[l], prm->smoother, prm->smoother_omega);
     }
     dense_lu_factor(H, &H->lv[H->nlev - 1].A);
@@ -921,6 +997,10 @@ uint64_t orc_hier_memory_footprint(const orc_hier *h) {
             bytes += matrix_bytes(&h->lv[l].R);
         }
         bytes += (uint64_t)h->lv[l].sm_len * 8;
+        /* ilu0::bytes (relaxation.hpp:93-95): the factors are a csr, with
+         * its ptr and col arrays */
+        if (h->prm.smoother == ORC_SM_ILU0 && l + 1 < h->nlev)
+            bytes += (uint64_t)(h->lv[l].A.nrows + 1) * 8 + (uint64_t)nnz_of(&h->lv[l].A) * 8;
     }
     bytes += (uint64_t)h->nc * h->nc * 8;
     return bytes;
@@ -932,7 +1012,11 @@ static void apply_smoother(const orc_hier *H, const orc_level *L,
     const int64_t n = L->A.nrows * 3;
     for (int s = 0; s < sweeps; ++s) {
         residual(&L->A, f, u, r);
-        if (H->prm.smoother == ORC_SM_JACOBI) {
+        if (H->prm.smoother == ORC_SM_ILU0) {
+            /* hierarchy.hpp:211-220: r = f - A u; LU d = r; u += d */
+            ilu0_solve(L, r);
+            for (int64_t i = 0; i < n; ++i) u[i] = r[i] + u[i];
+        } else if (H->prm.smoother == ORC_SM_JACOBI) {
             /* damped_jacobi::smooth (relaxation.hpp:165-173) */
             const double w = H->prm.smoother_omega;
             for (int64_t i = 0; i < n; ++i) u[i] += w * L->sm[i] * r[i];

@@ -40,7 +40,7 @@ enum {
 /* Smoother kinds.  JACOBI is the reference's point damped Jacobi
  * (relaxation.hpp:141-180); SPAI0 and BLOCK_JACOBI are the 3x3 block
  * smoothers the reference lacks (definitions in DESIGN.md section 4). */
-enum { ORC_SM_JACOBI = 0, ORC_SM_SPAI0 = 1, ORC_SM_BLOCK_JACOBI = 2 };
+enum { ORC_SM_JACOBI = 0, ORC_SM_SPAI0 = 1, ORC_SM_BLOCK_JACOBI = 2, ORC_SM_ILU0 = 3 };
 
 /* Block CSR, block size b in {1,3}; val holds nnz*b*b doubles, each block
  * row-major (static_block.hpp:19-66, csr.hpp:26-40). */

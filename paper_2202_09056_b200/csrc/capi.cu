@@ -107,9 +107,7 @@ void validate_params(const samg_amg_params *prm, int pipeline) {
     require(prm != nullptr, SAMG_INVALID_ARGUMENT, "setup: params must not be NULL");
     if (pipeline != SAMG_PIPELINE_NS_BLOCK)
         fail(SAMG_UNSUPPORTED, "setup: only pipeline::ns_block is on the B200 path");
-    if (prm->smoother == SAMG_SMOOTHER_ILU0)
-        fail(SAMG_UNSUPPORTED, "setup: ILU(0) smoothing is not on the B200 path yet");
-    require(prm->smoother >= 0 && prm->smoother <= 2, SAMG_INVALID_ARGUMENT, "setup: unknown smoother");
+    require(prm->smoother >= 0 && prm->smoother <= 3, SAMG_INVALID_ARGUMENT, "setup: unknown smoother");
     require(prm->pre_sweeps >= 0 && prm->post_sweeps >= 0, SAMG_INVALID_ARGUMENT,
             "setup: negative sweep count");
 }
@@ -465,7 +463,9 @@ SAMG_API int samg_smoother_info(const samg_hierarchy *hp, int level, int64_t *le
         const samgb::Hierarchy &h = Hc(hp);
         if (level < 0 || level + 1 >= static_cast<int>(h.levels.size()))
             fail(SAMG_INVALID_ARGUMENT, "level has no smoother");
-        *len = static_cast<int64_t>(h.levels[level].M.data.n);
+        const Smoother &M = h.levels[level].M;
+        // ILU(0): [factors (9*nnzb) | inverted pivots (9*nrows)]
+        *len = M.kind == SM_ILU ? 9 * (M.nnzb + M.nrows) : static_cast<int64_t>(M.data.n);
     });
 }
 
@@ -476,7 +476,13 @@ SAMG_API int samg_get_smoother(const samg_hierarchy *hp, int level, double *data
             fail(SAMG_INVALID_ARGUMENT, "level has no smoother");
         CK(cudaSetDevice(h.device));
         const Smoother &M = h.levels[level].M;
-        CK(cudaMemcpyAsync(data, M.data.p, M.data.bytes(), cudaMemcpyDeviceToHost, h.stream));
+        if (M.kind == SM_ILU) {
+            CK(cudaMemcpyAsync(data, M.lu.p, sizeof(double) * 9 * M.nnzb, cudaMemcpyDeviceToHost, h.stream));
+            CK(cudaMemcpyAsync(data + 9 * M.nnzb, M.data.p, sizeof(double) * 9 * M.nrows,
+                               cudaMemcpyDeviceToHost, h.stream));
+        } else {
+            CK(cudaMemcpyAsync(data, M.data.p, M.data.bytes(), cudaMemcpyDeviceToHost, h.stream));
+        }
         CK(cudaStreamSynchronize(h.stream));
     });
 }

@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(kPT) k_panel_cluster(int64_t n, int64_t ld, in
 // Reuse of a buffer two columns later is safe: a CTA pushes column q+2 only
 // after receiving every CTA's column-q+1 push, which each sends only after
 // finishing its column-q reads.
-constexpr int kRB = 32, kMaxRW = 32;
+constexpr int kRB = 32;
 
 __device__ __forceinline__ uint32_t smem_addr(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));

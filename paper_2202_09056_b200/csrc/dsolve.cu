@@ -541,6 +541,8 @@ DHierarchy *dsetup_all(const unsigned char *id, int nranks, int rank, Bsr3 &&A0,
                        const int64_t *row_starts, int64_t min_rows, const samg_amg_params &prm,
                        cudaStream_t s, double t0) {
     if (!id && nranks > kMaxEmulated) fail(SAMG_INVALID_ARGUMENT, "dsetup: at most 16 emulated ranks");
+    if (prm.smoother == SAMG_SMOOTHER_ILU0)
+        fail(SAMG_UNSUPPORTED, "multi-GPU solve: the ILU(0) sweeps are sequential across row partitions");
     const int64_t nb = A0.nrows;
     std::vector<int64_t> st(nranks + 1);
     if (row_starts) {

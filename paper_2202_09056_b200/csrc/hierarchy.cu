@@ -61,7 +61,11 @@ uint64_t Hierarchy::memory_footprint() const {
             bytes += matrix_bytes(lv.P);
             bytes += matrix_bytes(lv.R);
         }
-        bytes += lv.M.data.n * 8;
+        if (lv.M.kind == SM_ILU)  // ilu0::bytes (relaxation.hpp:93-95)
+            bytes += static_cast<uint64_t>(lv.M.nrows + 1) * 8 + static_cast<uint64_t>(lv.M.nnzb) * 80 +
+                     static_cast<uint64_t>(lv.M.nrows) * 72;
+        else
+            bytes += lv.M.data.n * 8;
     }
     bytes += static_cast<uint64_t>(nc) * nc * 8;
     return bytes;

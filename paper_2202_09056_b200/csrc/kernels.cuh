@@ -25,13 +25,20 @@ struct Bsr3 {
     }
 };
 
-enum SmootherKind { SM_POINT = 0, SM_BLOCK = 1 };
+enum SmootherKind { SM_POINT = 0, SM_BLOCK = 1, SM_ILU = 2 };
 
-// Per-level smoother: point (3 doubles per block row: omega / a_rr) or
-// block (9 doubles per block row: M_i).
+// Per-level smoother: point (3 doubles per block row: omega / a_rr), block
+// (9 doubles per block row: M_i) or block ILU(0) (ilu0<block3>,
+// relaxation.hpp:20-139): data = inverted pivots (9 per block row), lu =
+// the factors in A's pattern (9 per block), whose ptr/col are A's.
 struct Smoother {
     int kind = SM_POINT;
     DevBuf<double> data;
+    // ILU(0) only
+    DevBuf<double> lu, tmp;      // factors; scratch vector (3 per block row)
+    DevBuf<int> dpos, flags;     // diagonal position per row; solve flags
+    const int *ptr = nullptr, *col = nullptr;  // A's pattern
+    int64_t nrows = 0, nnzb = 0;
 };
 
 // ---- solve phase (solve.cu) -------------------------------------------------
@@ -121,6 +128,11 @@ void fix_decoupled_rows(Bsr3 &A, cudaStream_t s);
 // smoother setup: kind SAMG_SMOOTHER_*
 void setup_smoother(const Bsr3 &A, int kind, double omega, Smoother &M, DevError *err,
                     cudaStream_t s);
+// block ILU(0) (ilu.cu): factorization, and one smoothing application
+// u_out = u_in + (LU)^-1 (f - A u_in)  (u_in == nullptr: zero guess, r = f)
+void setup_ilu0(const Bsr3 &A, Smoother &M, DevError *err, cudaStream_t s);
+void launch_ilu_smooth(const Bsr3 *A, const Smoother &M, const double *f, const double *u_in,
+                       double *u_out, cudaStream_t s);
 // coarsest level: dense inverse (row-major n x n), n = 3*A.nrows
 void dense_inverse(const Bsr3 &A, DevBuf<double> &Ainv, DevError *err, cudaStream_t s);
 

@@ -1272,6 +1272,10 @@ void setup_smoother(const Bsr3 &A, int kind, double omega, Smoother &M, DevError
     const int *ap = A.ptr.p, *ac = A.col.p;
     const double *av = A.val.p;
     DevError *ep = err;
+    if (kind == SAMG_SMOOTHER_ILU0) {
+        setup_ilu0(A, M, err, s);
+        return;
+    }
     if (kind == SAMG_SMOOTHER_JACOBI) {
         // relaxation.hpp:147-162; the damping is folded in (omega * (1/d)),
         // the same first product as relaxation.hpp:172

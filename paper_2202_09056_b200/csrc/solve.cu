@@ -875,6 +875,7 @@ void launch_residual(const Bsr3 &A, const double *f, const double *u, double *r,
 
 void launch_smooth(const Bsr3 &A, const Smoother &M, const double *f, const double *u,
                    double *u_out, cudaStream_t s) {
+    if (M.kind == SM_ILU) return launch_ilu_smooth(&A, M, f, u, u_out, s);
     if (M.kind == SM_POINT) launch_rows(A, u, EpiSmoothPoint{f, u, M.data.p, u_out}, s);
     else launch_rows(A, u, EpiSmoothBlock{f, u, M.data.p, u_out}, s);
 }
@@ -882,6 +883,7 @@ void launch_smooth(const Bsr3 &A, const Smoother &M, const double *f, const doub
 void launch_smooth_zero(int64_t nrows, const Smoother &M, const double *f, double *u,
                         cudaStream_t s) {
     if (nrows == 0) return;
+    if (M.kind == SM_ILU) return launch_ilu_smooth(nullptr, M, f, nullptr, u, s);
     if (M.kind == SM_POINT) k_smooth_zero_point<<<vec_grid(3 * nrows), 256, 0, s>>>(3 * nrows, M.data.p, f, u);
     else k_smooth_zero_block<<<vec_grid(nrows), 256, 0, s>>>(nrows, M.data.p, f, u);
     CK_LAUNCH();
@@ -894,6 +896,12 @@ void launch_spmv_dot(const Bsr3 &A, const double *p, double *q, double *partials
 
 void launch_smooth_dot(const Bsr3 &A, const Smoother &M, const double *f, const double *u,
                        double *u_out, double *partials, CgScalars *sc, cudaStream_t s, int what) {
+    if (M.kind == SM_ILU) {
+        // f.u_out, as the fused sweeps' epilogues return (r.z inside CG)
+        launch_ilu_smooth(&A, M, f, u, u_out, s);
+        launch_dot(3 * A.nrows, f, u_out, partials, sc, what, s);
+        return;
+    }
     if (M.kind == SM_POINT)
         launch_reduce(A, u, EpiSmoothPoint{f, u, M.data.p, u_out}, partials, sc, what, s);
     else

@@ -12,11 +12,11 @@ C restatement).  Bars (BASELINE.json north_star):
 import numpy as np
 import pytest
 
-from oracle.oracle import Params, SM_BLOCK_JACOBI, SM_JACOBI, SM_SPAI0
+from oracle.oracle import Params, SM_BLOCK_JACOBI, SM_ILU0, SM_JACOBI, SM_SPAI0
 
 pytestmark = pytest.mark.gpu
 
-SM = {"spai0": SM_SPAI0, "jacobi": SM_JACOBI, "block_jacobi": SM_BLOCK_JACOBI}
+SM = {"spai0": SM_SPAI0, "jacobi": SM_JACOBI, "block_jacobi": SM_BLOCK_JACOBI, "ilu0": SM_ILU0}
 
 
 def make_problem(pb, nx, ny=None, nz=None, **kw):
@@ -53,6 +53,8 @@ def compare_hierarchies(h, hr, orc_h=None, smoother="spai0", omega=0.72):
                 if smoother == "jacobi":
                     sm_o = omega * sm_o
                 np.testing.assert_array_equal(sm_g, sm_o)
+            if smoother == "ilu0":  # factors + inverted pivots of ilu0<block3> itself
+                np.testing.assert_array_equal(h.smoother(l), hr.ilu(l))
     assert h.coarse_dim == hr.coarse_dim
     assert h.memory_footprint() == hr.memory_footprint
 
@@ -69,6 +71,14 @@ CASES = [
     ("beam_xslow", dict(nx=12, ny=4, nz=4, lx=3.0, dirichlet="eliminate", load="traction_xend",
                         x_slowest=True), "spai0", 0.72, 120),
     ("cube8_keep_noise", dict(nx=8, dirichlet="keep_rows", noise=0.01, seed=3), "spai0", 0.72, 300),
+    # block ILU(0), the reference's default smoother (relaxation.hpp:20-139)
+    ("cube6_keep_ilu0", dict(nx=6, dirichlet="keep_rows"), "ilu0", 0.72, 100),
+    ("box975_free_ilu0", dict(nx=9, ny=7, nz=5, dirichlet="eliminate", load="traction_xend"),
+     "ilu0", 0.72, 150),
+    ("cube7_hetero_ilu0", dict(nx=7, dirichlet="eliminate", heterogeneous=True, load="random",
+                               seed=7), "ilu0", 0.72, 120),
+    ("beam_xslow_ilu0", dict(nx=16, ny=4, nz=4, lx=4.0, dirichlet="eliminate", load="traction_xend",
+                             x_slowest=True), "ilu0", 0.72, 120),
 ]
 
 
@@ -174,8 +184,6 @@ def test_unsupported_pipelines(gpu):
     for pl in ("scalar", "block", "ns_scalar", "ns_hybrid1", "ns_hybrid2"):
         with pytest.raises(pb.Unsupported):
             pb.setup(p.csr(), p.nullspace(), pl)
-    with pytest.raises(pb.Unsupported):
-        pb.setup(p.csr(), p.nullspace(), "ns_block", pb.AmgParams(smoother="ilu0"))
 
 
 def test_spmv_matches_reference(gpu, ref):
