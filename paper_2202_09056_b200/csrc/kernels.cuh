@@ -37,6 +37,7 @@ struct Smoother {
     // ILU(0) only
     DevBuf<double> lu, tmp;      // factors; scratch vector (3 per block row)
     DevBuf<int> dpos, flags;     // diagonal position per row; solve flags
+    DevBuf<int> order;           // rows in level order: forward (n), backward (n)
     const int *ptr = nullptr, *col = nullptr;  // A's pattern
     int64_t nrows = 0, nnzb = 0;
 };

@@ -36,11 +36,13 @@ CONFIGS = {
                 x_slowest=True), [("spai0", 0.72)]),
     "C4": (dict(nx=199, ny=199, nz=199, dirichlet="eliminate", noise=0.01, seed=2022), [("spai0", 0.72)]),
 }
-SM = {"spai0": 1, "jacobi": 0, "block_jacobi": 2}
+SM = {"spai0": 1, "jacobi": 0, "block_jacobi": 2, "ilu0": 3}
 
 
-def run(name, ref_on, max_it, out):
+def run(name, ref_on, max_it, out, smoother=None):
     kw, smoothers = CONFIGS[name]
+    if smoother:
+        smoothers = [(smoother, 0.72)]
     t0 = time.perf_counter()
     p = pb.generate_hex(**kw)
     tgen = time.perf_counter() - t0
@@ -101,9 +103,10 @@ def main():
     ap.add_argument("--ref", action="store_true")
     ap.add_argument("--max-it", type=int, default=1000)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--smoother", default=None, help="override the configs' smoothers (e.g. ilu0)")
     a = ap.parse_args()
     for c in a.configs:
-        run(c, a.ref, a.max_it, a.out)
+        run(c, a.ref, a.max_it, a.out, a.smoother)
 
 
 if __name__ == "__main__":
