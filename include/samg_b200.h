@@ -188,6 +188,13 @@ SAMG_API int samg_bsr3_spmv(const samg_bsr3 *m, double alpha, const double *x,
         double beta, double *y);
 /* Galerkin product R*A*P (csr.hpp:259-262) in the reference's summation
  * order; result is a new device matrix. */
+/* count products y_k = alpha*A*x_k + beta*y_k with host vectors
+ * (x: count x 3*ncols, y: count x 3*nrows, row-major); each product copies
+ * its own x_k in and y_k out, pipelined over three streams so the copies of
+ * neighbouring products overlap the kernel.  Pinned host memory gives full
+ * PCIe bandwidth (pageable memory is copied correctly, more slowly). */
+SAMG_API int samg_bsr3_spmv_batch(const samg_bsr3 *m, double alpha,
+        const double *x, double beta, double *y, int64_t count);
 SAMG_API int samg_bsr3_galerkin(const samg_bsr3 *R, const samg_bsr3 *A,
         const samg_bsr3 *P, samg_bsr3 **out);
 /* algorithmic bytes of one spmv */

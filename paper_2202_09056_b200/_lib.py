@@ -110,6 +110,7 @@ PROTOTYPES = {
     "samg_bsr3_download": ([vp, i64p, i64p, f64p], C.c_int),
     "samg_bsr3_spmv_device": ([vp, C.c_double, vp, C.c_double, vp, vp], C.c_int),
     "samg_bsr3_spmv": ([vp, C.c_double, f64p, C.c_double, f64p], C.c_int),
+    "samg_bsr3_spmv_batch": ([vp, C.c_double, vp, C.c_double, vp, i64], C.c_int),
     "samg_bsr3_galerkin": ([vp, vp, vp, C.POINTER(vp)], C.c_int),
     "samg_bsr3_dense_inverse": ([vp, f64p], C.c_int),
     "samg_bsr3_spmv_bytes": ([vp, C.c_int, C.POINTER(C.c_uint64)], C.c_int),

@@ -114,6 +114,15 @@ class Bsr3:
         check(lib.samg_bsr3_spmv(self.h, alpha, _p(x), beta, _p(y)))
         return y
 
+    def spmv_batch(self, X, alpha=1.0, beta=0.0, Y=None):
+        """Rows of X (count x 3*ncols host array) -> rows of Y, each product
+        with its own H2D/D2H, pipelined (samg_bsr3_spmv_batch)."""
+        nr, nc, _ = self.shape
+        X = np.ascontiguousarray(X, dtype=np.float64).reshape(-1, 3 * nc)
+        Y = np.zeros((X.shape[0], 3 * nr)) if Y is None else np.ascontiguousarray(Y, dtype=np.float64)
+        check(lib.samg_bsr3_spmv_batch(self.h, alpha, X.ctypes.data, beta, Y.ctypes.data, X.shape[0]))
+        return Y
+
     def spmv_device(self, x_ptr: int, y_ptr: int, alpha=1.0, beta=0.0, stream: int = 0):
         check(lib.samg_bsr3_spmv_device(self.h, alpha, x_ptr, beta, y_ptr, stream or None))
 

@@ -20,6 +20,19 @@ struct samg_bsr3 {
     const samgb::Bsr3 *m = nullptr;
     int device = 0;
     samgb::DevBuf<double> xs, ys;  // e2e staging for host-vector spmv
+    // batched host-vector spmv: three streams, triple-buffered staging
+    static constexpr int kPipe = 3;
+    cudaStream_t bs[kPipe] = {nullptr, nullptr, nullptr};
+    samgb::DevBuf<double> bx[kPipe], by[kPipe];
+    ~samg_bsr3() {
+        // the staging buffers are stream-ordered on bs[]: free them first
+        for (int b = 0; b < kPipe; ++b) {
+            bx[b].release();
+            by[b].release();
+        }
+        for (cudaStream_t &q : bs)
+            if (q) { cudaStreamSynchronize(q); cudaStreamDestroy(q); }
+    }
 };
 
 struct samg_hierarchy {
@@ -554,6 +567,39 @@ SAMG_API int samg_bsr3_spmv(const samg_bsr3 *mc, double alpha, const double *x, 
         launch_spmv(A, alpha, m->xs.p, beta, m->ys.p, nullptr);
         CK(cudaMemcpyAsync(y, m->ys.p, sizeof(double) * 3 * A.nrows, cudaMemcpyDeviceToHost, nullptr));
         CK(cudaStreamSynchronize(nullptr));
+    });
+}
+
+// count independent products y_k = alpha A x_k + beta y_k with host
+// vectors (x: count x 3*ncols, y: count x 3*nrows, row-major).  Every
+// product still copies its x_k in and its y_k out; three streams with
+// triple-buffered device staging overlap the H2D of x_{k+1}, the kernel of
+// k and the D2H of y_{k-1} (full-duplex PCIe, separate copy engines): a
+// stream's chain H2D -> kernel -> D2H spans ~3 steps, so 3 buffers keep both
+// copy directions busy.
+SAMG_API int samg_bsr3_spmv_batch(const samg_bsr3 *mc, double alpha, const double *x, double beta,
+                                  double *y, int64_t count) {
+    return guarded([&] {
+        require(mc && mc->m && x && y && count >= 0, SAMG_INVALID_ARGUMENT, "spmv_batch: bad argument");
+        auto *m = const_cast<samg_bsr3 *>(mc);
+        CK(cudaSetDevice(m->device));
+        const Bsr3 &A = *m->m;
+        const int64_t nx = 3 * A.ncols, ny = 3 * A.nrows;
+        for (int b = 0; b < samg_bsr3::kPipe; ++b) {
+            if (!m->bs[b]) CK(cudaStreamCreateWithFlags(&m->bs[b], cudaStreamNonBlocking));
+            if (m->bx[b].n < static_cast<size_t>(nx) + 1) m->bx[b].alloc(nx + 1, m->bs[b]);
+            if (m->by[b].n < static_cast<size_t>(ny) + 1) m->by[b].alloc(ny + 1, m->bs[b]);
+        }
+        for (int64_t k = 0; k < count; ++k) {
+            const int b = static_cast<int>(k % samg_bsr3::kPipe);
+            cudaStream_t q = m->bs[b];
+            CK(cudaMemcpyAsync(m->bx[b].p, x + k * nx, sizeof(double) * nx, cudaMemcpyHostToDevice, q));
+            if (beta != 0.0)
+                CK(cudaMemcpyAsync(m->by[b].p, y + k * ny, sizeof(double) * ny, cudaMemcpyHostToDevice, q));
+            launch_spmv(A, alpha, m->bx[b].p, beta, m->by[b].p, q);
+            CK(cudaMemcpyAsync(y + k * ny, m->by[b].p, sizeof(double) * ny, cudaMemcpyDeviceToHost, q));
+        }
+        for (cudaStream_t q : m->bs) CK(cudaStreamSynchronize(q));
     });
 }
 

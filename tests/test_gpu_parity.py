@@ -186,6 +186,19 @@ def test_unsupported_pipelines(gpu):
             pb.setup(p.csr(), p.nullspace(), pl)
 
 
+def test_spmv_batch_matches_single(gpu):
+    pb = gpu
+    p = make_problem(pb, 9, dirichlet="eliminate")
+    A = pb.Bsr3.from_host(p.nbrows, p.nbrows, p.ptr, p.col, p.val.reshape(-1))
+    rng = np.random.default_rng(12)
+    X = rng.uniform(-1, 1, (5, p.n))
+    Y0 = rng.uniform(-1, 1, (5, p.n))
+    Y = A.spmv_batch(X, 0.5, 0.25, Y0.copy())
+    for k in range(5):
+        np.testing.assert_array_equal(Y[k], A.spmv(X[k], 0.5, 0.25, Y0[k]))
+    assert A.spmv_batch(np.zeros((0, p.n))).shape == (0, p.n)
+
+
 def test_spmv_matches_reference(gpu, ref):
     pb = gpu
     p = make_problem(pb, 19, dirichlet="eliminate")
