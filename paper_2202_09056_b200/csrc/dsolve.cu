@@ -221,7 +221,7 @@ struct DHierarchy {
     ~DHierarchy() {
         if (H && H->stream) cudaStreamSynchronize(H->stream);
         ranks.clear();
-        if (sc_host) cudaFreeHost(sc_host);
+        pinned_small_free(sc_host);
         if (comm) nccl().CommDestroy(comm);
     }
 
@@ -523,7 +523,7 @@ DHierarchy *dsetup(std::unique_ptr<Hierarchy> H, ncclComm_t comm, int nranks,
         R.partials.alloc(4096, s);
         R.sc.alloc(1, s);
     }
-    CK(cudaMallocHost(&D->sc_host, sizeof(CgScalars)));
+    D->sc_host = static_cast<CgScalars *>(pinned_small_alloc(sizeof(CgScalars)));
     CK(cudaStreamSynchronize(s));
     D->H = std::move(H);
     D->comm = comm;

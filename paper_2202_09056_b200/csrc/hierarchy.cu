@@ -43,8 +43,8 @@ Hierarchy::~Hierarchy() {
     Ainv.release();
     r.release(); z.release(); p.release(); q.release();
     fbuf.release(); ubuf.release(); partials.release(); sc.release(); err.release();
-    if (sc_host) cudaFreeHost(sc_host);
-    if (sc_stage) cudaFreeHost(sc_stage);
+    pinned_small_free(sc_host);
+    pinned_small_free(sc_stage);
     if (cg_exec) cudaGraphExecDestroy(cg_exec);
     if (stream && owns_stream) {
         cudaStreamSynchronize(stream);
@@ -177,8 +177,8 @@ Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int6
     H->partials.alloc(np, s);
     H->sc.alloc(1, s);
     CK(cudaMemsetAsync(H->sc.p, 0, sizeof(CgScalars), s));
-    CK(cudaMallocHost(&H->sc_host, sizeof(CgScalars)));
-    CK(cudaMallocHost(&H->sc_stage, sizeof(CgScalars)));
+    H->sc_host = static_cast<CgScalars *>(pinned_small_alloc(sizeof(CgScalars)));
+    H->sc_stage = static_cast<CgScalars *>(pinned_small_alloc(sizeof(CgScalars)));
     CK(cudaStreamSynchronize(s));
     mark("workspace", L - 1);
     H->setup_seconds = now_s() - t_start;

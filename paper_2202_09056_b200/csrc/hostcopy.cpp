@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <mutex>
@@ -25,7 +26,7 @@ namespace samgb {
 namespace {
 
 constexpr size_t kChunk = 8u << 20;     // bytes per staging buffer
-constexpr int kThreads = 6;
+constexpr int kThreads = 16;  // upper bound; SAMG_H2D_THREADS (default 8) uses fewer
 constexpr size_t kDirect = 4u << 20;    // below this: plain cudaMemcpyAsync
 
 struct Pool {
@@ -84,7 +85,12 @@ void h2d(void *dst, const void *src, size_t bytes, cudaStream_t s) {
     int dev = 0;
     CK(cudaGetDevice(&dev));
     const size_t nchunks = (bytes + kChunk - 1) / kChunk;
-    const int T = static_cast<int>(std::min<size_t>(kThreads, nchunks));
+    static const int threads = [] {
+        const char *e = std::getenv("SAMG_H2D_THREADS");
+        const int v = e ? std::atoi(e) : 8;
+        return std::min(kThreads, std::max(1, v));
+    }();
+    const int T = static_cast<int>(std::min<size_t>(threads, nchunks));
     std::vector<std::exception_ptr> errs(T);
     auto work = [&](int t) {
         try {
@@ -111,6 +117,43 @@ void h2d(void *dst, const void *src, size_t bytes, cudaStream_t s) {
     // the pinned buffers are reused by the next call only after their
     // events; the caller's stream already orders the copies before its
     // next work
+}
+
+// Small pinned objects (CG scalar mirrors, ...): 256-byte slots carved
+// from 1 MB pinned slabs, so a hierarchy setup does not pay cudaMallocHost
+// (~2 ms each) for a few hundred bytes.
+namespace {
+constexpr size_t kSlot = 256, kSlab = 1u << 20;
+struct SmallPool {
+    std::mutex mu;
+    std::vector<void *> free_slots;
+};
+SmallPool &small_pool() {
+    static SmallPool *p = new SmallPool;  // slabs live for the process
+    return *p;
+}
+} // namespace
+
+void *pinned_small_alloc(size_t bytes) {
+    if (bytes > kSlot) fail(SAMG_INVALID_ARGUMENT, "pinned_small_alloc: object too large");
+    SmallPool &P = small_pool();
+    std::lock_guard<std::mutex> lock(P.mu);
+    if (P.free_slots.empty()) {
+        char *slab = nullptr;
+        CK(cudaHostAlloc(reinterpret_cast<void **>(&slab), kSlab, cudaHostAllocPortable));
+        for (size_t o = 0; o < kSlab; o += kSlot) P.free_slots.push_back(slab + o);
+    }
+    void *p = P.free_slots.back();
+    P.free_slots.pop_back();
+    std::memset(p, 0, kSlot);
+    return p;
+}
+
+void pinned_small_free(void *p) {
+    if (!p) return;
+    SmallPool &P = small_pool();
+    std::lock_guard<std::mutex> lock(P.mu);
+    P.free_slots.push_back(p);
 }
 
 } // namespace samgb

@@ -25,6 +25,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 namespace samgb {
@@ -704,13 +705,15 @@ __global__ void __launch_bounds__(256) k_spgemm_numeric(
 constexpr int kWCap = 1024;
 constexpr int kWPB = 8;
 
-__global__ void __launch_bounds__(256) k_spgemm_wcount(int nrows, const int *ap, const int *ac,
-                                                       const int *bp, const int *bc, int *cnt) {
+__global__ void __launch_bounds__(256) k_spgemm_wcount(int nrows, const int *rows, const int *ap,
+                                                       const int *ac, const int *bp, const int *bc,
+                                                       int *cnt) {
     __shared__ int keys_all[kWPB][kWCap];
     __shared__ int n_all[kWPB];
     const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int row = blockIdx.x * kWPB + w;
-    if (row >= nrows) return;  // whole warp
+    const int ridx = blockIdx.x * kWPB + w;
+    if (ridx >= nrows) return;  // whole warp
+    const int row = rows ? rows[ridx] : ridx;
     int *keys = keys_all[w];
     for (int t = lane; t < kWCap; t += 32) keys[t] = -1;
     if (lane == 0) n_all[w] = 0;
@@ -731,11 +734,11 @@ __global__ void __launch_bounds__(256) k_spgemm_wcount(int nrows, const int *ap,
 
 __global__ void __launch_bounds__(256) k_spgemm_wnumeric(
         int nrows, const int *ap, const int *ac, const double *av, const int *bp, const int *bc,
-        const double *bv, const int *cp, int *ccol, double *cval) {
+        const double *bv, const int *cp, const int *mode, int *ccol, double *cval) {
     extern __shared__ int wsm[];
     const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int row = blockIdx.x * kWPB + w;
-    if (row >= nrows) return;
+    if (row >= nrows || mode[row]) return;  // bitmap rows: k_spgemm_bnumeric
     const int n = cp[row + 1] - cp[row];
     if (n > kWCap / 2 - 1) return;  // wide row: CTA kernel
     int *keys = wsm + w * (kWCap * 5 / 2);
@@ -833,6 +836,179 @@ __global__ void __launch_bounds__(256) k_spgemm_wnumeric(
         jbc = jbn;
         kend = kendn;
     }
+}
+
+// ---------------------------------------------------------------------------
+// Window-bitmap SpGEMM (warp per row) for rows whose output columns span a
+// window of at most kWinMax columns -- every row of the AMG Galerkin
+// products on mesh matrices.  The row's column set is a bitmap over
+// [cmin, cmin + W) in shared memory; a per-word prefix popcount gives both
+// the sorted column list (no hashing, no sort) and every product's output
+// slot (one popcount).  Products are accumulated in the reference's ja order
+// into shared memory when the row has <= acc_cap columns (global memory
+// otherwise).  Results are bit-identical to the hash kernels.
+constexpr int kWinMax = 32768;   // columns of the widest window (bits)
+constexpr int kBWPB = 8;         // warps (rows) per CTA
+
+// [cmin, cmax] of row i's products: B rows are column-sorted, so their first
+// and last entries bound them.  Empty row: cmin > cmax.
+__device__ __forceinline__ void row_window(int i, const int *__restrict__ ap, const int *__restrict__ ac,
+                                           const int *__restrict__ bp, const int *__restrict__ bc,
+                                           int &cmin, int &cmax) {
+    const int lane = threadIdx.x & 31;
+    int lo = INT_MAX, hi = -1;
+    for (int ja = ap[i] + lane; ja < ap[i + 1]; ja += 32) {
+        const int kk = ac[ja], b0 = bp[kk], b1 = bp[kk + 1];
+        if (b1 > b0) { lo = min(lo, bc[b0]); hi = max(hi, bc[b1 - 1]); }
+    }
+    cmin = static_cast<int>(__reduce_min_sync(0xffffffffu, static_cast<unsigned>(lo)));
+    cmax = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(hi + 1))) - 1;
+}
+
+// set the bits of row i's product columns; returns the column count
+__device__ int row_bitmap(int i, const int *__restrict__ ap, const int *__restrict__ ac,
+                          const int *__restrict__ bp, const int *__restrict__ bc, int cmin,
+                          int words, unsigned *bm) {
+    const int lane = threadIdx.x & 31;
+    for (int w = lane; w < words; w += 32) bm[w] = 0u;
+    __syncwarp();
+    for (int ja = ap[i]; ja < ap[i + 1]; ++ja) {
+        const int kk = ac[ja];
+        for (int jb = bp[kk] + lane; jb < bp[kk + 1]; jb += 32) {
+            const int c = bc[jb] - cmin;
+            atomicOr(bm + (c >> 5), 1u << (c & 31));
+        }
+    }
+    __syncwarp();
+    int cnt = 0;
+    for (int w = lane; w < words; w += 32) cnt += __popc(bm[w]);
+    return __reduce_add_sync(0xffffffffu, cnt);
+}
+
+// symbolic pass: count = distinct columns, or -2 when the window is too wide
+__global__ void __launch_bounds__(kBWPB * 32) k_spgemm_bcount(int nrows, const int *ap, const int *ac,
+        const int *bp, const int *bc, int win_limit, int *cnt, int *win_lo, int *maxwin) {
+    __shared__ unsigned bm_all[kBWPB][kWinMax / 32];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int row = blockIdx.x * kBWPB + w;
+    if (row >= nrows) return;
+    int cmin, cmax;
+    row_window(row, ap, ac, bp, bc, cmin, cmax);
+    if (cmax < cmin) {  // empty row
+        if (lane == 0) { cnt[row] = 0; win_lo[row] = 0; }
+        return;
+    }
+    const int width = cmax - cmin + 1;
+    if (width > win_limit) {
+        if (lane == 0) cnt[row] = -2;
+        return;
+    }
+    const int c = row_bitmap(row, ap, ac, bp, bc, cmin, (width + 31) >> 5, bm_all[w]);
+    if (lane == 0) {
+        cnt[row] = c;
+        win_lo[row] = cmin;
+        atomicMax(maxwin, width);
+    }
+}
+
+// numeric pass for the bitmap rows (cnt >= 0 from k_spgemm_bcount; rows
+// marked -2 there are skipped here, the hash kernels do them)
+__global__ void __launch_bounds__(kBWPB * 32) k_spgemm_bnumeric(int nrows, const int *ap,
+        const int *ac, const double *av, const int *bp, const int *bc, const double *bv,
+        const int *cp, const int *mode, const int *win_lo, int words, int acc_cap, int *ccol,
+        double *cval) {
+    extern __shared__ __align__(16) unsigned char bsm[];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int row = blockIdx.x * kBWPB + w;
+    if (row >= nrows || mode[row] != 1) return;
+    const size_t per = (2 * static_cast<size_t>(words) * 4 + 15) / 16 * 16 + static_cast<size_t>(acc_cap) * 72;
+    unsigned *bm = reinterpret_cast<unsigned *>(bsm + w * per);
+    int *pre = reinterpret_cast<int *>(bm + words);
+    double *acc_s = reinterpret_cast<double *>(bsm + w * per + (2 * static_cast<size_t>(words) * 4 + 15) / 16 * 16);
+    const int cmin = win_lo[row];
+    const int64_t base = cp[row];
+    const int n = cp[row + 1] - cp[row];
+    if (n == 0) return;
+    row_bitmap(row, ap, ac, bp, bc, cmin, words, bm);
+    // exclusive prefix of the word popcounts: lane l owns words [l*wpl, (l+1)*wpl)
+    const int wpl = (words + 31) / 32;
+    int mine = 0;
+    for (int t = 0; t < wpl; ++t) {
+        const int wd = lane * wpl + t;
+        if (wd < words) mine += __popc(bm[wd]);
+    }
+    int incl = mine;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += v;
+    }
+    int run = incl - mine;
+    for (int t = 0; t < wpl; ++t) {
+        const int wd = lane * wpl + t;
+        if (wd >= words) break;
+        unsigned bits = bm[wd];
+        pre[wd] = run;
+        while (bits) {
+            const int b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            ccol[base + run++] = cmin + (wd << 5) + b;
+        }
+    }
+    const bool in_smem = n <= acc_cap;
+    double *acc = in_smem ? acc_s : cval + 9 * base;
+    for (int e = lane; e < 9 * n; e += 32) acc[e] = 0.0;
+    __syncwarp();
+    auto slot_of = [&](int col) {
+        const int c = col - cmin, wd = c >> 5, b = c & 31;
+        return pre[wd] + __popc(bm[wd] & ((1u << b) - 1u));
+    };
+    // in-order accumulation; operands of step ja+1 fetched during step ja
+    const int ja0 = ap[row], jend = ap[row + 1];
+    double am[9], bmx[9];
+    int cc = -1, jbc = -1, kend = 0;
+    auto fetch = [&](int ja, double *a_, double *b_, int &c_, int &jb_, int &kend_) {
+        const int kk = ac[ja];
+        const double *a = av + 9 * static_cast<int64_t>(ja);
+#pragma unroll
+        for (int e = 0; e < 9; ++e) a_[e] = a[e];
+        jb_ = bp[kk] + lane;
+        kend_ = bp[kk + 1];
+        c_ = -1;
+        if (jb_ < kend_) {
+            c_ = bc[jb_];
+            const double *b = bv + 9 * static_cast<int64_t>(jb_);
+#pragma unroll
+            for (int e = 0; e < 9; ++e) b_[e] = b[e];
+        }
+    };
+    if (ja0 < jend) fetch(ja0, am, bmx, cc, jbc, kend);
+    for (int ja = ja0; ja < jend; ++ja) {
+        double an[9], bn[9];
+        int cn = -1, jbn = -1, kendn = 0;
+        if (ja + 1 < jend) fetch(ja + 1, an, bn, cn, jbn, kendn);
+        if (cc >= 0) {
+            double prod[9];
+            blk_mul(am, bmx, prod);
+            double *cb = acc + 9 * slot_of(cc);
+#pragma unroll
+            for (int e = 0; e < 9; ++e) cb[e] = __dadd_rn(cb[e], prod[e]);
+            for (int jb = jbc + 32; jb < kend; jb += 32) {
+                blk_mul(am, bv + 9 * static_cast<int64_t>(jb), prod);
+                double *cb2 = acc + 9 * slot_of(bc[jb]);
+#pragma unroll
+                for (int e = 0; e < 9; ++e) cb2[e] = __dadd_rn(cb2[e], prod[e]);
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int e = 0; e < 9; ++e) { am[e] = an[e]; bmx[e] = bn[e]; }
+        cc = cn;
+        jbc = jbn;
+        kend = kendn;
+    }
+    if (in_smem)
+        for (int e = lane; e < 9 * n; e += 32) cval[9 * base + e] = acc_s[e];
 }
 
 __global__ void k_spgemm_ub(int nrows, const int *ap, const int *ac, const int *bp,
@@ -1147,10 +1323,42 @@ void spgemm(const Bsr3 &A, const Bsr3 &B, Bsr3 &C, cudaStream_t s) {
     CK(cudaStreamSynchronize(s));
     constexpr int kMaxCap = 16384;
     const int cap_s = std::min(kMaxCap, std::max(256, next_pow2(2 * std::min<int64_t>(maxub, B.ncols) + 2)));
-    DevBuf<int> cnt(n + 1, s), ovf(1, s);
+    DevBuf<int> cnt(n + 1, s), ovf(1, s), winlo(n + 1, s), mode(n + 1, s), maxwin(1, s);
     CK(cudaMemsetAsync(ovf.p, 0, sizeof(int), s));
-    // 1. warp-per-row symbolic pass; rows above kWCap/2-1 columns -> wide list
-    k_spgemm_wcount<<<ceil_div(n, kWPB), 256, 0, s>>>(n, A.ptr.p, A.col.p, B.ptr.p, B.col.p, cnt.p);
+    CK(cudaMemsetAsync(maxwin.p, 0, sizeof(int), s));
+    // 0. window-bitmap symbolic pass (most rows); rows whose product columns
+    //    span more than kWinMax columns are marked -2 for the hash kernels
+    static const int win_env = [] {
+        const char *e = std::getenv("SAMG_SPGEMM_MAXWIN");
+        return e ? std::min(kWinMax, std::atoi(e)) : -1;
+    }();
+    // measured on C1 (profiles/README.md): the bitmap kernels win for
+    // products with short B rows (x P: RAP), the hash kernels for long ones
+    // (x A: RA, whose many lanes per step amortise the hashing)
+    const double b_row = B.nrows ? static_cast<double>(B.nnzb) / B.nrows : 0.0;
+    const int win_limit = win_env >= 0 ? win_env : (b_row <= 16.0 ? kWinMax : 0);
+    k_spgemm_bcount<<<ceil_div(n, kBWPB), kBWPB * 32, 0, s>>>(n, A.ptr.p, A.col.p, B.ptr.p, B.col.p,
+                                                              win_limit, cnt.p, winlo.p, maxwin.p);
+    CK_LAUNCH();
+    DevBuf<int> fb(n, s), nfb_d(1, s);
+    CK(cudaMemsetAsync(nfb_d.p, 0, sizeof(int), s));
+    {
+        int *cc = cnt.p, *md = mode.p, *fl = fb.p, *nf = nfb_d.p;
+        for_each(n, [=] __device__(int64_t i) {
+            md[i] = cc[i] >= 0 ? 1 : 0;
+            if (cc[i] == -2) fl[atomicAdd(nf, 1)] = static_cast<int>(i);
+        }, s);
+    }
+    int hdr[2] = {0, 0};
+    CK(cudaMemcpyAsync(&hdr[0], nfb_d.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&hdr[1], maxwin.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const int nfb = hdr[0], wmax = hdr[1];
+    // 1. warp-per-row hash symbolic pass for those; rows above kWCap/2-1
+    //    columns -> wide list
+    if (nfb)
+        k_spgemm_wcount<<<ceil_div(nfb, kWPB), 256, 0, s>>>(nfb, fb.p, A.ptr.p, A.col.p, B.ptr.p,
+                                                            B.col.p, cnt.p);
     CK_LAUNCH();
     DevBuf<int> wide(n, s), nwide_d(1, s);
     CK(cudaMemsetAsync(nwide_d.p, 0, sizeof(int), s));
@@ -1223,14 +1431,38 @@ void spgemm(const Bsr3 &A, const Bsr3 &B, Bsr3 &C, cudaStream_t s) {
     CK(cudaStreamSynchronize(s));
     const int cap_n = std::min(kMaxCap, std::max(256, next_pow2(2 * static_cast<int64_t>(maxc) + 2)));
     const size_t smem_n = static_cast<size_t>(cap_n) * 4 * 2 + static_cast<size_t>(cap_n / 2) * 4;
-    // 2. warp-per-row numeric pass for the narrow rows
-    const size_t smem_w = static_cast<size_t>(kWPB) * kWCap * 5 / 2 * sizeof(int);
-    CK(cudaFuncSetAttribute(k_spgemm_wnumeric, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(smem_w)));
-    k_spgemm_wnumeric<<<ceil_div(n, kWPB), 256, smem_w, s>>>(n, A.ptr.p, A.col.p, A.val.p, B.ptr.p,
-                                                             B.col.p, B.val.p, C.ptr.p, C.col.p,
-                                                             C.val.p);
-    CK_LAUNCH();
+    // 2a. window-bitmap numeric pass (accumulators in shared memory for rows
+    //     of up to acc_cap columns)
+    if (wmax > 0) {
+        static const int budget = [] {  // shared bytes per warp (rows of one CTA)
+            const char *e = std::getenv("SAMG_SPGEMM_WARP_SMEM");
+            return e ? std::atoi(e) : 20 * 1024;
+        }();
+        const int words = (wmax + 31) / 32;
+        const int bm_bytes = (2 * words * 4 + 15) / 16 * 16;
+        const int acc_cap = std::max(0, std::min(512, (budget - bm_bytes) / 72));
+        const size_t smem_b = static_cast<size_t>(kBWPB) * (bm_bytes + static_cast<size_t>(acc_cap) * 72);
+        static const bool battr = [] {
+            CK(cudaFuncSetAttribute(k_spgemm_bnumeric, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    220 * 1024));
+            return true;
+        }();
+        (void)battr;
+        k_spgemm_bnumeric<<<ceil_div(n, kBWPB), kBWPB * 32, smem_b, s>>>(
+            n, A.ptr.p, A.col.p, A.val.p, B.ptr.p, B.col.p, B.val.p, C.ptr.p, mode.p, winlo.p, words,
+            acc_cap, C.col.p, C.val.p);
+        CK_LAUNCH();
+    }
+    // 2b. warp-per-row hash numeric pass for the other narrow rows
+    if (nfb) {
+        const size_t smem_w = static_cast<size_t>(kWPB) * kWCap * 5 / 2 * sizeof(int);
+        CK(cudaFuncSetAttribute(k_spgemm_wnumeric, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem_w)));
+        k_spgemm_wnumeric<<<ceil_div(n, kWPB), 256, smem_w, s>>>(n, A.ptr.p, A.col.p, A.val.p, B.ptr.p,
+                                                                 B.col.p, B.val.p, C.ptr.p, mode.p,
+                                                                 C.col.p, C.val.p);
+        CK_LAUNCH();
+    }
     // 3. CTA-per-row numeric pass for the wide rows
     if (nwide) {
         CK(cudaFuncSetAttribute(k_spgemm_numeric<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
