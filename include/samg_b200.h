@@ -312,6 +312,28 @@ SAMG_API int samg_rigid_body_modes(int64_t nnodes, const double *xyz,
 SAMG_API int samg_problem_bsr3_view(const samg_problem *p, const int64_t **ptr,
         const int64_t **col, const double **val);
 
+/* ---- on-GPU assembly ----------------------------------------
+ * The same problems assembled directly in device memory (bitwise equal to
+ * samg_generate_hex): 3x3 BSR matrix, right-hand side, node coordinates and
+ * the rigid-body modes (3n x 6, column-major), all device pointers owned by
+ * the handle.  samg_setup_device builds a hierarchy from a device matrix
+ * (copied) and a host or device nullspace. */
+typedef struct samg_dproblem samg_dproblem;
+SAMG_API int samg_generate_hex_device(const samg_problem_params *p, int device,
+        samg_dproblem **out);
+SAMG_API int samg_dproblem_destroy(samg_dproblem *p);
+SAMG_API int samg_dproblem_info(const samg_dproblem *p, int64_t *n,
+        int64_t *nbrows, int64_t *nnzb);
+SAMG_API int samg_dproblem_matrix(const samg_dproblem *p, const samg_bsr3 **A);
+SAMG_API int samg_dproblem_vectors(const samg_dproblem *p, const double **d_rhs,
+        const double **d_nullspace, const double **d_xyz);
+/* host copies of the vectors (any pointer may be NULL) */
+SAMG_API int samg_dproblem_download(const samg_dproblem *p, double *rhs,
+        double *nullspace, double *xyz);
+SAMG_API int samg_setup_device(const samg_bsr3 *A, const double *B,
+        int64_t b_rows, int64_t b_cols, int pipeline,
+        const samg_amg_params *prm, samg_hierarchy **out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -32,17 +32,21 @@ from .api import (  # noqa: F401
     AmgParams,
     Bsr3,
     CgParams,
+    DeviceProblem,
     Hierarchy,
     Problem,
     ProblemParams,
     device_count,
     generate_hex,
+    generate_hex_device,
     rigid_body_modes,
     setup,
     setup_bsr3,
+    setup_device,
 )
 
 __all__ = [
     "setup", "setup_bsr3", "Hierarchy", "AmgParams", "CgParams", "Bsr3", "Problem",
     "ProblemParams", "generate_hex", "rigid_body_modes", "device_count", "SamgError",
+    "DeviceProblem", "generate_hex_device", "setup_device",
 ]

@@ -137,6 +137,13 @@ PROTOTYPES = {
     "samg_dist_to_device": ([vp, C.c_int, C.c_int], C.c_int),
     "samg_dist_pack": ([vp, vp, vp, vp], C.c_int),
     "samg_dist_spmv": ([vp, C.c_int, C.c_double, vp, C.c_double, vp, vp], C.c_int),
+    "samg_generate_hex_device": ([C.POINTER(ProblemParamsC), C.c_int, C.POINTER(vp)], C.c_int),
+    "samg_dproblem_destroy": ([vp], C.c_int),
+    "samg_dproblem_info": ([vp, i64p, i64p, i64p], C.c_int),
+    "samg_dproblem_matrix": ([vp, C.POINTER(vp)], C.c_int),
+    "samg_dproblem_vectors": ([vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)], C.c_int),
+    "samg_dproblem_download": ([vp, f64p, f64p, f64p], C.c_int),
+    "samg_setup_device": ([vp, vp, i64, i64, C.c_int, C.POINTER(AmgParamsC), C.POINTER(vp)], C.c_int),
     "samg_nccl_unique_id": ([C.POINTER(C.c_ubyte)], C.c_int),
     "samg_dsetup": ([C.POINTER(C.c_ubyte), C.c_int, C.c_int, i64, i64p, i64p, f64p, f64p, i64,
                      i64, i64p, i64, C.c_int, C.POINTER(AmgParamsC), C.POINTER(vp)], C.c_int),

@@ -394,6 +394,59 @@ def generate_hex(prm: ProblemParams = ProblemParams(), **kw) -> Problem:
     return Problem(n.value, nn.value, ptr, col, val.reshape(-1, 3, 3), rhs, xyz)
 
 
+class DeviceProblem:
+    """A problem assembled on the GPU (samg_generate_hex_device): the matrix
+    as a device Bsr3 view, rhs / nullspace / coordinates as device pointers."""
+
+    def __init__(self, handle):
+        self.h = handle
+        n, nb, nz = C.c_int64(), C.c_int64(), C.c_int64()
+        check(lib.samg_dproblem_info(handle, C.byref(n), C.byref(nb), C.byref(nz)))
+        self.n, self.nbrows, self.nnzb = n.value, nb.value, nz.value
+        a = vp()
+        check(lib.samg_dproblem_matrix(handle, C.byref(a)))
+        self.A = Bsr3(a, owner=self)
+        r, b, x = vp(), vp(), vp()
+        check(lib.samg_dproblem_vectors(handle, C.byref(r), C.byref(b), C.byref(x)))
+        self.rhs_ptr, self.nullspace_ptr, self.xyz_ptr = r.value, b.value, x.value
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            try:
+                lib.samg_dproblem_destroy(self.h)
+            except Exception:
+                pass
+            self.h = None
+
+    def download(self):
+        """(rhs, nullspace (6 x 3n column-major blocks, flat), xyz) on the host"""
+        rhs, B, xyz = np.zeros(self.n), np.zeros(6 * self.n), np.zeros(self.n)
+        check(lib.samg_dproblem_download(self.h, _p(rhs), _p(B), _p(xyz)))
+        return rhs, B, xyz
+
+
+def generate_hex_device(prm: ProblemParams = ProblemParams(), device: int = 0, **kw) -> DeviceProblem:
+    """generate_hex assembled directly in device memory (bitwise equal)."""
+    if kw:
+        prm = ProblemParams(**{**prm.__dict__, **kw})
+    pc = prm.c()
+    h = vp()
+    check(lib.samg_generate_hex_device(C.byref(pc), device, C.byref(h)))
+    return DeviceProblem(h)
+
+
+def setup_device(A: "Bsr3", B_ptr: int, b_cols: int = 6, pipeline="ns_block",
+                 prm: AmgParams = AmgParams()) -> Hierarchy:
+    """samg_setup_device: hierarchy from a device matrix and a device (or
+    host, by address) nullspace of 3*nrows x b_cols, column-major."""
+    nr, _, _ = A.shape
+    h = vp()
+    pc = prm.c()
+    check(lib.samg_setup_device(A.h, B_ptr, 3 * nr, b_cols, _pipeline(pipeline), C.byref(pc),
+                                C.byref(h)))
+    return Hierarchy(h)
+
+
 def rigid_body_modes(xyz) -> np.ndarray:
     """rigid_body_modes (elasticity.hpp:38-52): column-major (3n x 6), flat."""
     xyz = _f64(xyz)

@@ -42,6 +42,8 @@ struct samg_hierarchy {
 
 namespace samgb {
 samg_problem *generate_hex(const samg_problem_params &p);
+void generate_hex_device(const samg_problem_params &p, Bsr3 &A, DevBuf<double> &rhs,
+                         DevBuf<double> &xyz, DevBuf<double> &B, int64_t &nnodes, cudaStream_t s);
 void rigid_body_modes(int64_t nnodes, const double *xyz, double *B);
 struct DHierarchy;
 DHierarchy *dsetup_all(const unsigned char *id, int nranks, int rank, Bsr3 &&A0,
@@ -55,6 +57,14 @@ void dinfo(const DHierarchy *d, int64_t *row0, int64_t *row1, int *nlevels, int 
            double *setup_s);
 void nccl_unique_id(unsigned char *out);
 }
+
+struct samg_dproblem {
+    int device = 0;
+    samgb::Bsr3 A;
+    samgb::DevBuf<double> rhs, xyz, B;
+    int64_t nnodes = 0;
+    samg_bsr3 view;
+};
 
 struct samg_dhierarchy {
     samgb::DHierarchy *d = nullptr;
@@ -343,6 +353,99 @@ SAMG_API int samg_setup_bsr3(int64_t nbrows, const int64_t *ptr, const int64_t *
             throw;
         }
         *out = finish_setup(std::move(A0), B, b_rows, b_cols, *prm, s, t0);
+    });
+}
+
+// setup from a device-resident matrix (copied, the caller keeps its own);
+// B may be a host or a device pointer
+SAMG_API int samg_setup_device(const samg_bsr3 *A, const double *B, int64_t b_rows, int64_t b_cols,
+                               int pipeline, const samg_amg_params *prm, samg_hierarchy **out) {
+    return guarded([&] {
+        const double t0 = now_s();
+        require(out != nullptr && A && A->m, SAMG_INVALID_ARGUMENT, "setup_device: NULL argument");
+        *out = nullptr;
+        validate_params(prm, pipeline);
+        const Bsr3 &M = *A->m;
+        if (M.nrows != M.ncols) fail(SAMG_NON_SQUARE, "transfer_operators: matrix must be square");
+        validate_ns(3 * M.nrows, B, b_rows, b_cols);
+        need_device(prm->device);
+        require(A->device == prm->device, SAMG_INVALID_ARGUMENT, "setup_device: matrix lives on another device");
+        cudaStream_t s = new_stream();
+        Bsr3 A0;
+        try {
+            A0.alloc(M.nrows, M.ncols, M.nnzb, s);
+            CK(cudaMemcpyAsync(A0.ptr.p, M.ptr.p, sizeof(int) * (M.nrows + 1), cudaMemcpyDeviceToDevice, s));
+            if (M.nnzb) {
+                CK(cudaMemcpyAsync(A0.col.p, M.col.p, sizeof(int) * M.nnzb, cudaMemcpyDeviceToDevice, s));
+                CK(cudaMemcpyAsync(A0.val.p, M.val.p, sizeof(double) * 9 * M.nnzb, cudaMemcpyDeviceToDevice, s));
+            }
+        } catch (...) {
+            cudaStreamSynchronize(s);
+            cudaStreamDestroy(s);
+            throw;
+        }
+        *out = finish_setup(std::move(A0), B, b_rows, b_cols, *prm, s, t0);
+    });
+}
+
+SAMG_API int samg_generate_hex_device(const samg_problem_params *p, int device, samg_dproblem **out) {
+    return guarded([&] {
+        require(p && out, SAMG_INVALID_ARGUMENT, "generate_hex_device: NULL argument");
+        *out = nullptr;
+        need_device(device);
+        auto d = std::make_unique<samg_dproblem>();
+        d->device = device;
+        cudaStream_t s = nullptr;
+        generate_hex_device(*p, d->A, d->rhs, d->xyz, d->B, d->nnodes, s);
+        d->view.m = &d->A;
+        d->view.device = device;
+        *out = d.release();
+    });
+}
+
+SAMG_API int samg_dproblem_destroy(samg_dproblem *p) {
+    return guarded([&] {
+        if (!p) return;
+        cudaSetDevice(p->device);
+        cudaDeviceSynchronize();
+        delete p;
+    });
+}
+
+SAMG_API int samg_dproblem_info(const samg_dproblem *p, int64_t *n, int64_t *nbrows, int64_t *nnzb) {
+    return guarded([&] {
+        require(p && n && nbrows && nnzb, SAMG_INVALID_ARGUMENT, "dproblem_info: NULL argument");
+        *n = 3 * p->nnodes;
+        *nbrows = p->A.nrows;
+        *nnzb = p->A.nnzb;
+    });
+}
+
+SAMG_API int samg_dproblem_matrix(const samg_dproblem *p, const samg_bsr3 **A) {
+    return guarded([&] {
+        require(p && A, SAMG_INVALID_ARGUMENT, "dproblem_matrix: NULL argument");
+        *A = &p->view;
+    });
+}
+
+SAMG_API int samg_dproblem_vectors(const samg_dproblem *p, const double **rhs, const double **B,
+                                   const double **xyz) {
+    return guarded([&] {
+        require(p, SAMG_INVALID_ARGUMENT, "dproblem_vectors: NULL argument");
+        if (rhs) *rhs = p->rhs.p;
+        if (B) *B = p->B.p;
+        if (xyz) *xyz = p->xyz.p;
+    });
+}
+
+SAMG_API int samg_dproblem_download(const samg_dproblem *p, double *rhs, double *B, double *xyz) {
+    return guarded([&] {
+        require(p, SAMG_INVALID_ARGUMENT, "dproblem_download: NULL argument");
+        CK(cudaSetDevice(p->device));
+        const int64_t n = 3 * p->nnodes;
+        if (rhs) CK(cudaMemcpy(rhs, p->rhs.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+        if (B) CK(cudaMemcpy(B, p->B.p, sizeof(double) * 6 * n, cudaMemcpyDeviceToHost));
+        if (xyz) CK(cudaMemcpy(xyz, p->xyz.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
     });
 }
 

@@ -20,70 +20,12 @@
 #include <vector>
 
 #include "common.cuh"
+#include "hexgen.cuh"
 #include "problem.cuh"
 
 namespace samgb {
 
 namespace {
-
-// hex8_stiffness (elasticity.hpp:57-123) for a given isotropic C.
-void hex8_ke(double hx, double hy, double hz, const double C[6][6], double *Ke) {
-    int off[8][3];
-    for (int a = 0; a < 8; ++a) { off[a][0] = a & 1; off[a][1] = (a >> 1) & 1; off[a][2] = (a >> 2) & 1; }
-    const double g = 1.0 / std::sqrt(3.0);
-    const double gp[2] = {-g, g};
-    const double jac[3] = {hx / 2, hy / 2, hz / 2};
-    const double detJ = jac[0] * jac[1] * jac[2];
-    std::fill(Ke, Ke + 576, 0.0);
-    for (int qx = 0; qx < 2; ++qx)
-    for (int qy = 0; qy < 2; ++qy)
-    for (int qz = 0; qz < 2; ++qz) {
-        const double xi = gp[qx], eta = gp[qy], zeta = gp[qz];
-        double dN[8][3];
-        for (int a = 0; a < 8; ++a) {
-            const double sx = off[a][0] ? 1.0 : -1.0, sy = off[a][1] ? 1.0 : -1.0,
-                         sz = off[a][2] ? 1.0 : -1.0;
-            dN[a][0] = 0.125 * sx * (1 + sy * eta) * (1 + sz * zeta) / jac[0];
-            dN[a][1] = 0.125 * (1 + sx * xi) * sy * (1 + sz * zeta) / jac[1];
-            dN[a][2] = 0.125 * (1 + sx * xi) * (1 + sy * eta) * sz / jac[2];
-        }
-        for (int a = 0; a < 8; ++a)
-        for (int b = 0; b < 8; ++b) {
-            double Ba[6][3] = {}, Bb[6][3] = {};
-            auto fill = [](double Bm[6][3], const double d[3]) {
-                Bm[0][0] = d[0]; Bm[1][1] = d[1]; Bm[2][2] = d[2];
-                Bm[3][0] = d[1]; Bm[3][1] = d[0];
-                Bm[4][1] = d[2]; Bm[4][2] = d[1];
-                Bm[5][0] = d[2]; Bm[5][2] = d[0];
-            };
-            fill(Ba, dN[a]);
-            fill(Bb, dN[b]);
-            for (int i = 0; i < 3; ++i)
-            for (int j = 0; j < 3; ++j) {
-                double s = 0;
-                for (int p = 0; p < 6; ++p)
-                for (int q = 0; q < 6; ++q) s += Ba[p][i] * C[p][q] * Bb[q][j];
-                Ke[(3 * a + i) * 24 + (3 * b + j)] += s * detJ;
-            }
-        }
-    }
-}
-
-void iso_C(double lambda, double mu, double C[6][6]) {
-    for (int i = 0; i < 6; ++i) for (int j = 0; j < 6; ++j) C[i][j] = 0.0;
-    for (int i = 0; i < 3; ++i)
-        for (int j = 0; j < 3; ++j) C[i][j] = (i == j) ? lambda + 2 * mu : lambda;
-    for (int i = 3; i < 6; ++i) C[i][i] = mu;
-}
-
-// counter-based uniform in [0,1): splitmix64 of (seed, stream, index)
-double uhash(uint64_t seed, uint64_t stream, uint64_t i) {
-    uint64_t z = seed * 0x9E3779B97F4A7C15ULL + stream * 0xD1B54A32D192ED03ULL + i + 0x632BE59BD9B4E019ULL;
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
-    z ^= z >> 31;
-    return static_cast<double>(z >> 11) * (1.0 / 9007199254740992.0);
-}
 
 template <class F>
 void parallel_for(int64_t n, F f) {
@@ -101,63 +43,81 @@ void parallel_for(int64_t n, F f) {
 
 } // namespace
 
-samg_problem *generate_hex(const samg_problem_params &p) {
+// Validated grid, element matrices and per-element materials of a problem:
+// shared by the host assembly below and the device assembly (assemble.cu),
+// so both use bitwise the same inputs.
+HexSetup hex_prepare(const samg_problem_params &p) {
     if (p.nx < 1 || p.ny < 1 || p.nz < 1)
         fail(SAMG_INVALID_MATERIAL, "generate_hex_elasticity: element counts must be >= 1");
     if (!p.heterogeneous && (!(p.E > 0) || !(p.nu > 0 && p.nu < 0.5)))
         fail(SAMG_INVALID_MATERIAL, "generate_hex_elasticity: need E > 0 and 0 < nu < 0.5");
     if (!(p.lx > 0 && p.ly > 0 && p.lz > 0))
         fail(SAMG_INVALID_MATERIAL, "generate_hex_elasticity: domain lengths must be > 0");
-    const int64_t nx = p.nx, ny = p.ny, nz = p.nz;
-    const int64_t mx = nx + 1, my = ny + 1, mz = nz + 1;
-    const double hx = p.lx / nx, hy = p.ly / ny, hz = p.lz / nz;
-    const bool elim = p.dirichlet == SAMG_DIRICHLET_ELIMINATE;
-    const bool keep = p.dirichlet == SAMG_DIRICHLET_KEEP_ROWS;
-    const int64_t i0 = elim ? 1 : 0;  // first kept x index
-    const int64_t kx = mx - i0;        // kept nodes along x
+    HexSetup h;
+    h.p = p;
+    h.nx = p.nx; h.ny = p.ny; h.nz = p.nz;
+    h.mx = h.nx + 1; h.my = h.ny + 1; h.mz = h.nz + 1;
+    h.hx = p.lx / h.nx; h.hy = p.ly / h.ny; h.hz = p.lz / h.nz;
+    h.elim = p.dirichlet == SAMG_DIRICHLET_ELIMINATE;
+    h.keep = p.dirichlet == SAMG_DIRICHLET_KEEP_ROWS;
+    h.i0 = h.elim ? 1 : 0;
+    h.kx = h.mx - h.i0;
+    h.nnodes_all = h.kx * h.my * h.mz;
+    const bool ranged = p.node_end > p.node_begin;
+    h.nb = ranged ? p.node_begin : 0;
+    h.ne = ranged ? p.node_end : h.nnodes_all;
+    if (h.nb < 0 || h.ne > h.nnodes_all)
+        fail(SAMG_INVALID_ARGUMENT, "generate_hex: node range outside the grid");
+    h.nodal_force = -h.hx * h.hy * h.hz / 8.0;  // elasticity.hpp:189
+    h.traction = -h.hy * h.hz / 4.0;
+    h.Khom.assign(576, 0.0); h.Klam.assign(576, 0.0); h.Kmu.assign(576, 0.0);
+    const int64_t nel = h.nx * h.ny * h.nz;
+    if (!p.heterogeneous) {
+        double C[6][6];
+        iso_C(p.E * p.nu / ((1 + p.nu) * (1 - 2 * p.nu)), p.E / (2 * (1 + p.nu)), C);
+        hex8_ke(h.hx, h.hy, h.hz, C, h.Khom.data());
+    } else {
+        double C[6][6];
+        iso_C(1.0, 0.0, C);
+        hex8_ke(h.hx, h.hy, h.hz, C, h.Klam.data());
+        iso_C(0.0, 1.0, C);
+        hex8_ke(h.hx, h.hy, h.hz, C, h.Kmu.data());
+        h.elam.resize(nel);
+        h.emu.resize(nel);
+        double *el = h.elam.data(), *em = h.emu.data();
+        const uint64_t seed = p.seed;
+        parallel_for(nel, [=](int64_t e) {
+            const double u1 = std::max(uhash(seed, 1, e), 1e-300), u2 = uhash(seed, 2, e);
+            const double g = std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586 * u2);
+            const double E = std::exp(g);
+            const double nu = 0.25 + 0.1 * uhash(seed, 3, e);
+            el[e] = E * nu / ((1 + nu) * (1 - 2 * nu));
+            em[e] = E / (2 * (1 + nu));
+        });
+    }
+    return h;
+}
+
+samg_problem *generate_hex(const samg_problem_params &p) {
+    const HexSetup H = hex_prepare(p);
+    const int64_t nx = H.nx, ny = H.ny, nz = H.nz;
+    const int64_t mx = H.mx, my = H.my, mz = H.mz;
+    const double hx = H.hx, hy = H.hy, hz = H.hz;
+    const bool keep = H.keep;
+    const int64_t i0 = H.i0, kx = H.kx;
     auto node_id = [&](int64_t i, int64_t j, int64_t k) -> int64_t {
         const int64_t ii = i - i0;
         return p.x_slowest ? k + mz * (j + my * ii) : ii + kx * (j + my * k);
     };
     auto constrained = [&](int64_t i) { return keep && i == 0; };
-    const int64_t nnodes_all = kx * my * mz;
-    // optional row range [node_begin, node_end): one rank's slab of a
-    // row-partitioned problem (global column ids)
-    const bool ranged = p.node_end > p.node_begin;
-    const int64_t nb = ranged ? p.node_begin : 0, ne = ranged ? p.node_end : nnodes_all;
-    if (nb < 0 || ne > nnodes_all)
-        fail(SAMG_INVALID_ARGUMENT, "generate_hex: node range outside the grid");
+    const int64_t nb = H.nb, ne = H.ne;
     const int64_t nnodes = ne - nb;
 
     auto *pb = new samg_problem;
     pb->nnodes = nnodes;
     pb->n = 3 * nnodes;
-
-    // element matrices: homogeneous -> one Ke; heterogeneous -> lambda/mu split
-    std::vector<double> Khom(576), Klam(576), Kmu(576);
-    std::vector<double> elam, emu;
-    const int64_t nel = nx * ny * nz;
-    if (!p.heterogeneous) {
-        double C[6][6];
-        iso_C(p.E * p.nu / ((1 + p.nu) * (1 - 2 * p.nu)), p.E / (2 * (1 + p.nu)), C);
-        hex8_ke(hx, hy, hz, C, Khom.data());
-    } else {
-        double C[6][6];
-        iso_C(1.0, 0.0, C);
-        hex8_ke(hx, hy, hz, C, Klam.data());
-        iso_C(0.0, 1.0, C);
-        hex8_ke(hx, hy, hz, C, Kmu.data());
-        elam.resize(nel);
-        emu.resize(nel);
-        parallel_for(nel, [&](int64_t e) {
-            const double u1 = std::max(uhash(p.seed, 1, e), 1e-300), u2 = uhash(p.seed, 2, e);
-            const double g = std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586 * u2);
-            const double E = std::exp(g);
-            const double nu = 0.25 + 0.1 * uhash(p.seed, 3, e);
-            elam[e] = E * nu / ((1 + nu) * (1 - 2 * nu));
-            emu[e] = E / (2 * (1 + nu));
-        });
-    }
+    const std::vector<double> &Khom = H.Khom, &Klam = H.Klam, &Kmu = H.Kmu;
+    const std::vector<double> &elam = H.elam, &emu = H.emu;
 
     // node -> (i,j,k)
     auto ijk_of = [&](int64_t id, int64_t &i, int64_t &j, int64_t &k) {
@@ -237,7 +197,7 @@ samg_problem *generate_hex(const samg_problem_params &p) {
         // loads
         double *f = &pb->rhs[3 * L];
         if (p.load == SAMG_LOAD_BODY_FORCE) {
-            const double nodal_force = -hx * hy * hz / 8.0;  // elasticity.hpp:189
+            const double nodal_force = H.nodal_force;
             for (int64_t ez = k - 1; ez <= k; ++ez)
             for (int64_t ey = j - 1; ey <= j; ++ey)
             for (int64_t ex = i - 1; ex <= i; ++ex)
@@ -245,7 +205,7 @@ samg_problem *generate_hex(const samg_problem_params &p) {
                     f[2] += nodal_force;
         } else if (p.load == SAMG_LOAD_TRACTION_XEND) {
             if (i == nx) {
-                const double q = -hy * hz / 4.0;
+                const double q = H.traction;
                 for (int64_t ez = k - 1; ez <= k; ++ez)
                 for (int64_t ey = j - 1; ey <= j; ++ey)
                     if (ey >= 0 && ez >= 0 && ey < ny && ez < nz) f[2] += q;

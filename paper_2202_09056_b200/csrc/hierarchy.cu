@@ -98,7 +98,8 @@ Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int6
     mark("upload", 0);
     const int k = static_cast<int>(b_cols);
     DevBuf<double> B(b_rows * b_cols, s);
-    CK(cudaMemcpyAsync(B.p, B_host, sizeof(double) * b_rows * b_cols, cudaMemcpyHostToDevice, s));
+    // B may be host (pageable/pinned) or device memory (samg_setup_device)
+    CK(cudaMemcpyAsync(B.p, B_host, sizeof(double) * b_rows * b_cols, cudaMemcpyDefault, s));
 
     H->levels.emplace_back();
     H->levels.back().A = std::move(A0);
