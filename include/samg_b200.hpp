@@ -10,7 +10,8 @@
 // become samg_b200::... with the same argument types and meaning, and the
 // same exception classes (common.hpp:12-28).  Differences:
 // the hierarchy lives in GPU memory (move-only handle); the default smoother
-// is SPAI0 because ILU(0) is not on the B200 path (it throws unsupported);
+// is the reference's, ILU(0) (bit-identical results; its triangular sweeps
+// are latency-bound on a GPU, smoother_kind::spai0 is the fast choice);
 // one hierarchy serves one solve at a time (device workspace is internal).
 #pragma once
 
@@ -114,7 +115,7 @@ enum class smoother_kind { ilu0, jacobi, spai0, block_jacobi };
 
 struct amg_params {
     coarsening_params coarsening;
-    smoother_kind smoother = smoother_kind::spai0;
+    smoother_kind smoother = smoother_kind::ilu0;  // hierarchy.hpp:52
     double smoother_omega = 0.72;  // damped_jacobi default (relaxation.hpp:143)
     int pre_sweeps = 1;
     int post_sweeps = 1;
