@@ -121,50 +121,97 @@ __global__ void k_ilu_dpos(int n, const int *ptr, const int *col, int *dpos, Dev
 }
 
 // IKJ factorization (relaxation.hpp:115-132), a warp per row.
+constexpr int kFMax = 192;  // rows up to this many blocks live in shared memory
+
 __global__ void __launch_bounds__(256) k_ilu_factor(int n, const int *__restrict__ order,
         const int *__restrict__ ptr, const int *__restrict__ col, const int *__restrict__ dpos,
         double *lu, double *inv, int *done, int *counter, DevError *err) {
-    const int lane = threadIdx.x & 31;
+    // per warp: the row's columns and blocks (the IKJ chain then runs in
+    // shared memory: binary searches and updates never touch L2)
+    extern __shared__ __align__(16) unsigned char fsm[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double *srow = reinterpret_cast<double *>(fsm) + static_cast<size_t>(w) * 9 * kFMax;
+    int *scol = reinterpret_cast<int *>(fsm + sizeof(double) * 9 * kFMax * 8) + w * kFMax;
     for (;;) {
         int t = 0;
         if (lane == 0) t = atomicAdd(counter, 1);
         t = __shfl_sync(kFull, t, 0);
         if (t >= n) return;
         const int i = __ldg(order + t);
-        const int b = ptr[i], e = ptr[i + 1], di = dpos[i];
+        const int b = ptr[i], e = ptr[i + 1], di = dpos[i], len = e - b;
+        const bool in_smem = len <= kFMax;
+        double *rv = in_smem ? srow - 9LL * b : lu;   // rv[9j + .] = block j of row i
+        const int *rc = in_smem ? scol - b : col;     // rc[j] = column of block j
+        if (in_smem) {
+            for (int q = lane; q < len; q += 32) scol[q] = col[b + q];
+            for (int q = lane; q < 9 * len; q += 32) srow[q] = lu[9LL * b + q];
+        }
         wait_deps(col, b, di, done);
+        // operands of step j+1 (inverted pivot of row k, first 32 blocks of
+        // its U part) are requested while step j runs: every row k < i is
+        // final once the dependencies are met
+        auto load_step = [&](int j, double (&dv)[3], int &c0, double (&u0v)[9], int &uend) {
+            const int k = rc[j];
+            if (lane < 9) {
+                const double *d = inv + 9LL * k;
+                const int c = lane % 3;
+                dv[0] = __ldcg(d + c); dv[1] = __ldcg(d + 3 + c); dv[2] = __ldcg(d + 6 + c);
+            }
+            const int ub = __ldg(dpos + k) + 1;
+            uend = __ldg(ptr + k + 1);
+            const int l = ub + lane;
+            c0 = -1;
+            if (l < uend) {
+                c0 = __ldg(col + l);
+#pragma unroll
+                for (int q = 0; q < 9; ++q) u0v[q] = __ldcg(lu + 9LL * l + q);
+            }
+        };
+        double dv[3] = {0, 0, 0}, u0v[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+        int c0 = -1, uend = 0;
+        if (b < di) load_step(b, dv, c0, u0v, uend);
         for (int j = b; j < di; ++j) {
-            const int k = col[j];
+            const int k = rc[j];
+            double ndv[3] = {0, 0, 0}, nu0v[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+            int nc0 = -1, nuend = 0;
+            if (j + 1 < di) load_step(j + 1, ndv, nc0, nu0v, nuend);
             // L_ik = A_ik * U_kk^-1 (operator*, static_block.hpp:68-76)
             double le = 0.0;
             if (lane < 9) {
-                const int r = lane / 3, c = lane % 3;
-                const double *a = lu + 9LL * j, *d = inv + 9LL * k;
-                le = __dadd_rn(le, __dmul_rn(a[r * 3 + 0], __ldcg(d + 0 * 3 + c)));
-                le = __dadd_rn(le, __dmul_rn(a[r * 3 + 1], __ldcg(d + 1 * 3 + c)));
-                le = __dadd_rn(le, __dmul_rn(a[r * 3 + 2], __ldcg(d + 2 * 3 + c)));
+                const int r = lane / 3;
+                const double *a = rv + 9LL * j;
+                le = __dadd_rn(le, __dmul_rn(a[r * 3 + 0], dv[0]));
+                le = __dadd_rn(le, __dmul_rn(a[r * 3 + 1], dv[1]));
+                le = __dadd_rn(le, __dmul_rn(a[r * 3 + 2], dv[2]));
             }
             __syncwarp();
-            if (lane < 9) lu[9LL * j + lane] = le;
+            if (lane < 9) rv[9LL * j + lane] = le;
             double lik[9];
 #pragma unroll
-            for (int t = 0; t < 9; ++t) lik[t] = __shfl_sync(kFull, le, t);
+            for (int q = 0; q < 9; ++q) lik[q] = __shfl_sync(kFull, le, q);
             // A_i. -= L_ik * U_k. over the U part of row k that hits row i
-            const int u0 = __ldg(dpos + k) + 1, u1 = __ldg(ptr + k + 1);
-            for (int l = u0 + lane; l < u1; l += 32) {
-                const int c = col[l];
+            const int ub = __ldg(dpos + k) + 1;
+            for (int l = ub + lane; l < uend; l += 32) {
+                int c;
+                double uv[9];
+                if (l == ub + lane) {
+                    c = c0;
+#pragma unroll
+                    for (int q = 0; q < 9; ++q) uv[q] = u0v[q];
+                } else {
+                    c = __ldg(col + l);
+#pragma unroll
+                    for (int q = 0; q < 9; ++q) uv[q] = __ldcg(lu + 9LL * l + q);
+                }
                 int lo = b, hi = e - 1, q = -1;
                 while (lo <= hi) {
-                    const int m = (lo + hi) >> 1, cm = col[m];
+                    const int m = (lo + hi) >> 1, cm = rc[m];
                     if (cm == c) { q = m; break; }
                     if (cm < c) lo = m + 1;
                     else hi = m - 1;
                 }
                 if (q < 0) continue;
-                double uv[9];
-#pragma unroll
-                for (int t = 0; t < 9; ++t) uv[t] = __ldcg(lu + 9LL * l + t);
-                double *dst = lu + 9LL * q;
+                double *dst = rv + 9LL * q;
 #pragma unroll
                 for (int r = 0; r < 3; ++r)
 #pragma unroll
@@ -177,15 +224,23 @@ __global__ void __launch_bounds__(256) k_ilu_factor(int n, const int *__restrict
                     }
             }
             __syncwarp();
+#pragma unroll
+            for (int q = 0; q < 3; ++q) dv[q] = ndv[q];
+#pragma unroll
+            for (int q = 0; q < 9; ++q) u0v[q] = nu0v[q];
+            c0 = nc0;
+            uend = nuend;
         }
+        if (in_smem)
+            for (int q = lane; q < 9 * len; q += 32) lu[9LL * b + q] = srow[q];
         if (lane == 0) {
             double piv[9], out[9];
-            for (int t = 0; t < 9; ++t) piv[t] = lu[9LL * di + t];
+            for (int q = 0; q < 9; ++q) piv[q] = rv[9LL * di + q];
             if (!blk_inverse_ref(piv, out)) {
                 raise_err(err, SAMG_SINGULAR_BLOCK, i);
-                for (int t = 0; t < 9; ++t) out[t] = 0.0;
+                for (int q = 0; q < 9; ++q) out[q] = 0.0;
             }
-            for (int t = 0; t < 9; ++t) inv[9LL * i + t] = out[t];
+            for (int q = 0; q < 9; ++q) inv[9LL * i + q] = out[q];
         }
         __syncwarp();
         if (lane == 0) {
@@ -351,7 +406,13 @@ void setup_ilu0(const Bsr3 &A, Smoother &M, DevError *err, cudaStream_t s) {
     level_orders(A, M.dpos, M.order, s);
     CK(cudaMemcpyAsync(M.lu.p, A.val.p, sizeof(double) * 9 * A.nnzb, cudaMemcpyDeviceToDevice, s));
     CK(cudaMemsetAsync(M.flags.p, 0, sizeof(int) * (2 * A.nrows * kFS + 2), s));
-    k_ilu_factor<<<persistent_grid(reinterpret_cast<const void *>(k_ilu_factor), n), 256, 0, s>>>(
+    constexpr int fsmem = 8 * kFMax * (9 * static_cast<int>(sizeof(double)) + static_cast<int>(sizeof(int)));
+    static const bool fattr = [] {
+        CK(cudaFuncSetAttribute(k_ilu_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem));
+        return true;
+    }();
+    (void)fattr;
+    k_ilu_factor<<<persistent_grid(reinterpret_cast<const void *>(k_ilu_factor), n), 256, fsmem, s>>>(
         n, M.order.p, A.ptr.p, A.col.p, M.dpos.p, M.lu.p, M.data.p, M.flags.p,
         M.flags.p + 2 * static_cast<int64_t>(n) * kFS, err);
     CK_LAUNCH();
