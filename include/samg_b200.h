@@ -50,8 +50,11 @@ enum samg_status {
     SAMG_INVALID_ARGUMENT = 105
 };
 
-/* samg::pipeline (hierarchy.hpp:30).  Only SAMG_PIPELINE_NS_BLOCK is the
- * B200 hot path; the others return SAMG_UNSUPPORTED. */
+/* samg::pipeline (hierarchy.hpp:30).  SAMG_PIPELINE_NS_BLOCK is the B200
+ * hot path; NS_HYBRID2 and NS_HYBRID1 (scalar-space Galerkin, block storage,
+ * hierarchy.hpp:233-330; NS_HYBRID1 without ILU(0), whose scalar smoother
+ * is not on this path) are supported with the same bit-exact parity; SCALAR,
+ * BLOCK and NS_SCALAR return SAMG_UNSUPPORTED. */
 enum samg_pipeline {
     SAMG_PIPELINE_SCALAR = 0,
     SAMG_PIPELINE_BLOCK = 1,

@@ -62,6 +62,7 @@ class Params:
     smoother_omega: float = 0.72
     coarse_enough: int = 3000
     stagnation_ratio: float = 0.8
+    pipeline: int = 5  # samg::pipeline: 3 ns_hybrid1, 4 ns_hybrid2, 5 ns_block
 
 
 class _orc_mat(C.Structure):
@@ -73,7 +74,8 @@ class _orc_params(C.Structure):
     _fields_ = [("eps_strong", C.c_double), ("omega", C.c_double),
                 ("smoother", C.c_int), ("smoother_omega", C.c_double),
                 ("pre_sweeps", C.c_int), ("post_sweeps", C.c_int),
-                ("coarse_enough", C.c_int64), ("stagnation_ratio", C.c_double)]
+                ("coarse_enough", C.c_int64), ("stagnation_ratio", C.c_double),
+                ("pipeline", C.c_int)]
 
 
 class _orc_report(C.Structure):
@@ -162,7 +164,7 @@ class Oracle(_Backend):
     def setup(self, n, ptr, col, val, B, params: Params = Params()):
         pr = _orc_params(params.eps_strong, params.omega, params.smoother,
                          params.smoother_omega, 1, 1, params.coarse_enough,
-                         params.stagnation_ratio)
+                         params.stagnation_ratio, params.pipeline)
         ptr = np.ascontiguousarray(ptr, np.int64)
         col = np.ascontiguousarray(col, np.int64)
         val = np.ascontiguousarray(val, np.float64)
@@ -287,7 +289,7 @@ class Ref(_Backend):
         lib.ref_rigid_body_modes.argtypes = [C.c_int64, f64p, f64p]
         lib.ref_setup.argtypes = [C.c_int64, i64p, i64p, f64p, f64p, C.c_int64, C.c_double,
                                   C.c_double, C.c_int, C.c_double, C.c_int64, C.c_double,
-                                  C.POINTER(vp)]
+                                  C.c_int, C.POINTER(vp)]
         lib.ref_destroy.argtypes = [vp]
         lib.ref_nlevels.argtypes = [vp]
         lib.ref_setup_seconds.argtypes = [vp]
@@ -352,7 +354,7 @@ class Ref(_Backend):
                                        B.size // n, params.eps_strong, params.omega,
                                        params.smoother, params.smoother_omega,
                                        params.coarse_enough, params.stagnation_ratio,
-                                       C.byref(h)))
+                                       params.pipeline, C.byref(h)))
         return RefHier(self, h, n)
 
     def spmv_bsr3(self, nrows, ncols, ptr, col, val, x, alpha=1.0, beta=0.0, y=None):

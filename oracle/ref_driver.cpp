@@ -158,7 +158,7 @@ int ref_rigid_body_modes(int64_t nnodes, const double *xyz, double *B) {
 int ref_setup(int64_t n, const int64_t *ptr, const int64_t *col,
         const double *val, const double *B, int64_t bcols, double eps_strong,
         double omega, int smoother, double smoother_omega,
-        int64_t coarse_enough, double stagnation_ratio, void **out) {
+        int64_t coarse_enough, double stagnation_ratio, int pipeline_id, void **out) {
     GUARD_BEGIN
     scalar_csr A;
     A.nrows = A.ncols = n;
@@ -182,7 +182,10 @@ int ref_setup(int64_t n, const int64_t *ptr, const int64_t *col,
     h->smoother = smoother;
     h->smoother_omega = smoother_omega;
     auto t0 = clk::now();
-    h->H = setup(A, Bd, pipeline::ns_block, prm);
+    // samg::pipeline numbering (hierarchy.hpp:30): 3 ns_hybrid1, 4 ns_hybrid2, 5 ns_block
+    const pipeline pl = pipeline_id == 3 ? pipeline::ns_hybrid1
+                      : pipeline_id == 4 ? pipeline::ns_hybrid2 : pipeline::ns_block;
+    h->H = setup(A, Bd, pl, prm);
     const samg::index L = h->H.nlevels();
     // Smoother override through the public level members.
     h->sm.resize(L);

@@ -71,6 +71,7 @@ void orc_default_params(orc_params *p) {
     p->post_sweeps = 1;
     p->coarse_enough = 3000;       /* hierarchy.hpp:55 */
     p->stagnation_ratio = 0.8;     /* hierarchy.hpp:56 */
+    p->pipeline = ORC_PIPELINE_NS_BLOCK;
 }
 
 /* ------------------------------------------------------------------------ */
@@ -674,16 +675,17 @@ static orc_mat smooth_prolongation(const orc_mat *A, const orc_mat *Pt,
 
 /* fix_decoupled_rows (hierarchy.hpp:172-191), 3x3 blocks */
 static void fix_decoupled_rows(orc_mat *A) {
+    const int b = A->b, bb = b * b;
     for (int64_t i = 0; i < A->nrows; ++i) {
         int64_t dg = -1;
         for (int64_t j = A->ptr[i]; j < A->ptr[i + 1]; ++j)
             if (A->col[j] == i) { dg = j; break; }
-        for (int r = 0; r < 3; ++r) {
+        for (int r = 0; r < b; ++r) {
             int zero_row = 1;
             for (int64_t j = A->ptr[i]; zero_row && j < A->ptr[i + 1]; ++j)
-                for (int c = 0; c < 3; ++c)
-                    if (A->val[j * 9 + r * 3 + c] != 0.0) { zero_row = 0; break; }
-            if (zero_row && dg >= 0) A->val[dg * 9 + r * 3 + r] = 1.0;
+                for (int c = 0; c < b; ++c)
+                    if (A->val[j * bb + r * b + c] != 0.0) { zero_row = 0; break; }
+            if (zero_row && dg >= 0) A->val[dg * bb + r * b + r] = 1.0;
         }
     }
 }
@@ -921,15 +923,28 @@ int orc_setup_ns_block(int64_t n, const int64_t *ptr, const int64_t *col,
         orc_mat Rs = transpose(&Ps);
         if (Ps.ncols % 3) fail(ORC_NOT_DIVISIBLE, "as_scalar_transfer: coarse dimension not divisible by block size");
         orc_mat P = to_block3(&Ps), R = to_block3(&Rs);
-        mat_free(&As); mat_free(&Pt); mat_free(&Ps); mat_free(&Rs);
-        free(G.ptr); free(G.col);
-        /* stagnation guard (hierarchy.hpp:355) */
+        /* stagnation guard (hierarchy.hpp:355; scalar_setup :246) */
         if ((double)(P.ncols * 3) > prm->stagnation_ratio * (double)(Li->A.nrows * 3)) {
+            mat_free(&As); mat_free(&Pt); mat_free(&Ps); mat_free(&Rs);
+            free(G.ptr); free(G.col);
             mat_free(&P); mat_free(&R); free(agg); free(Bc);
             break;
         }
-        orc_mat Ac = galerkin(&R, &Li->A, &P);
-        fix_decoupled_rows(&Ac);
+        orc_mat Ac;
+        if (prm->pipeline == ORC_PIPELINE_NS_HYBRID1 || prm->pipeline == ORC_PIPELINE_NS_HYBRID2) {
+            /* scalar_setup (hierarchy.hpp:233-260): Galerkin and
+             * fix_decoupled_rows on the scalar matrices, stored as blocks
+             * (hierarchy.hpp:318-322) */
+            orc_mat Acs = galerkin(&Rs, &As, &Ps);
+            fix_decoupled_rows(&Acs);
+            Ac = to_block3(&Acs);
+            mat_free(&Acs);
+        } else {
+            Ac = galerkin(&R, &Li->A, &P);
+            fix_decoupled_rows(&Ac);
+        }
+        mat_free(&As); mat_free(&Pt); mat_free(&Ps); mat_free(&Rs);
+        free(G.ptr); free(G.col);
         Li->P = P; Li->R = R; Li->has_transfer = 1;
         Li->agg = agg; Li->nnodes = G.nnodes; Li->naggs = naggs;
         if (H->nlev == cap) {

@@ -64,7 +64,11 @@ typedef struct {
     int pre_sweeps, post_sweeps;
     int64_t coarse_enough;   /* hierarchy.hpp:55 */
     double stagnation_ratio; /* hierarchy.hpp:56 */
+    int pipeline;            /* ORC_PIPELINE_NS_BLOCK or _NS_HYBRID1/2 */
 } orc_params;
+
+/* samg::pipeline values (hierarchy.hpp:30) handled by orc_setup_ns_block */
+enum { ORC_PIPELINE_NS_HYBRID1 = 3, ORC_PIPELINE_NS_HYBRID2 = 4, ORC_PIPELINE_NS_BLOCK = 5 };
 
 typedef struct {
     int iterations;

@@ -49,7 +49,7 @@ struct DHierarchy;
 DHierarchy *dsetup_all(const unsigned char *id, int nranks, int rank, Bsr3 &&A0,
                        const double *B, int64_t b_rows, int64_t b_cols,
                        const int64_t *row_starts, int64_t min_rows, const samg_amg_params &prm,
-                       cudaStream_t s, double t0);
+                       cudaStream_t s, double t0, int pipeline);
 void ddelete(DHierarchy *d);
 samg_solve_report dcg(DHierarchy *d, const double *f, double *u, const samg_cg_params &cp,
                       bool host);
@@ -128,8 +128,14 @@ cudaStream_t new_stream() {
 
 void validate_params(const samg_amg_params *prm, int pipeline) {
     require(prm != nullptr, SAMG_INVALID_ARGUMENT, "setup: params must not be NULL");
-    if (pipeline != SAMG_PIPELINE_NS_BLOCK)
-        fail(SAMG_UNSUPPORTED, "setup: only pipeline::ns_block is on the B200 path");
+    // ns_block, and the hybrids that differ from it only in the Galerkin
+    // arithmetic (scalar order, hierarchy.hpp:233-260) and, for ns_hybrid1,
+    // in scalar smoothers (ilu0<double> is not on the B200 path)
+    if (pipeline != SAMG_PIPELINE_NS_BLOCK && pipeline != SAMG_PIPELINE_NS_HYBRID2 &&
+        pipeline != SAMG_PIPELINE_NS_HYBRID1)
+        fail(SAMG_UNSUPPORTED, "setup: pipelines scalar, block and ns_scalar are not on the B200 path");
+    if (pipeline == SAMG_PIPELINE_NS_HYBRID1 && prm && prm->smoother == SAMG_SMOOTHER_ILU0)
+        fail(SAMG_UNSUPPORTED, "setup: ns_hybrid1 with scalar ILU(0) is not on the B200 path");
     require(prm->smoother >= 0 && prm->smoother <= 3, SAMG_INVALID_ARGUMENT, "setup: unknown smoother");
     require(prm->pre_sweeps >= 0 && prm->post_sweeps >= 0, SAMG_INVALID_ARGUMENT,
             "setup: negative sweep count");
@@ -229,10 +235,10 @@ void download_bsr3(const Bsr3 &M, int64_t *ptr, int64_t *col, double *val, cudaS
 }
 
 samg_hierarchy *finish_setup(Bsr3 &&A0, const double *B, int64_t b_rows, int64_t b_cols,
-                             const samg_amg_params &prm, cudaStream_t s, double t0) {
+                             const samg_amg_params &prm, cudaStream_t s, double t0, int pipeline) {
     auto out = std::make_unique<samg_hierarchy>();
     try {
-        out->h.reset(setup_hierarchy(std::move(A0), B, b_rows, b_cols, prm, s, t0));
+        out->h.reset(setup_hierarchy(std::move(A0), B, b_rows, b_cols, prm, s, t0, pipeline));
     } catch (...) {
         cudaStreamSynchronize(s);
         cudaStreamDestroy(s);
@@ -329,7 +335,7 @@ SAMG_API int samg_setup(int64_t n, const int64_t *ptr, const int64_t *col, const
             cudaStreamDestroy(s);
             throw;
         }
-        *out = finish_setup(std::move(A0), B, b_rows, b_cols, *prm, s, t0);
+        *out = finish_setup(std::move(A0), B, b_rows, b_cols, *prm, s, t0, pipeline);
     });
 }
 
@@ -352,7 +358,7 @@ SAMG_API int samg_setup_bsr3(int64_t nbrows, const int64_t *ptr, const int64_t *
             cudaStreamDestroy(s);
             throw;
         }
-        *out = finish_setup(std::move(A0), B, b_rows, b_cols, *prm, s, t0);
+        *out = finish_setup(std::move(A0), B, b_rows, b_cols, *prm, s, t0, pipeline);
     });
 }
 
@@ -384,7 +390,7 @@ SAMG_API int samg_setup_device(const samg_bsr3 *A, const double *B, int64_t b_ro
             cudaStreamDestroy(s);
             throw;
         }
-        *out = finish_setup(std::move(A0), B, b_rows, b_cols, *prm, s, t0);
+        *out = finish_setup(std::move(A0), B, b_rows, b_cols, *prm, s, t0, pipeline);
     });
 }
 
@@ -873,7 +879,7 @@ SAMG_API int samg_dsetup(const unsigned char id[128], int nranks, int rank, int6
             upload_bsr3(nbrows, nbrows, ptr, col, val, A0, s);
             auto h = std::make_unique<samg_dhierarchy>();
             h->d = dsetup_all(id, nranks, rank, std::move(A0), B, b_rows, b_cols, row_starts,
-                              min_rows > 0 ? min_rows : 4096, *prm, s, t0);
+                              min_rows > 0 ? min_rows : 4096, *prm, s, t0, pipeline);
             *out = h.release();
         } catch (...) {
             cudaStreamSynchronize(s);

@@ -369,7 +369,7 @@ samg_solve_report DHierarchy::cg(const double *d_f, double *d_u, const samg_cg_p
     cudaStream_t s = stream();
     const auto t0 = std::chrono::steady_clock::now();
     samg_solve_report rep{};
-    rep.variant = SAMG_PIPELINE_NS_BLOCK;
+    rep.variant = H->pipeline;
     rep.setup_seconds = H->setup_seconds;
     const int64_t base0 = emulated() ? ranks[0].row0 : 0;
     auto off = [&](const DRank &R) { return 3 * (R.row0 - base0); };
@@ -539,7 +539,7 @@ namespace samgb {
 DHierarchy *dsetup_all(const unsigned char *id, int nranks, int rank, Bsr3 &&A0,
                        const double *B, int64_t b_rows, int64_t b_cols,
                        const int64_t *row_starts, int64_t min_rows, const samg_amg_params &prm,
-                       cudaStream_t s, double t0) {
+                       cudaStream_t s, double t0, int pipeline) {
     if (!id && nranks > kMaxEmulated) fail(SAMG_INVALID_ARGUMENT, "dsetup: at most 16 emulated ranks");
     if (prm.smoother == SAMG_SMOOTHER_ILU0)
         fail(SAMG_UNSUPPORTED, "multi-GPU solve: the ILU(0) sweeps are sequential across row partitions");
@@ -554,7 +554,7 @@ DHierarchy *dsetup_all(const unsigned char *id, int nranks, int rank, Bsr3 &&A0,
     }
     for (int q = 0; q < nranks; ++q)
         if (st[q + 1] <= st[q]) fail(SAMG_INVALID_ARGUMENT, "dsetup: every rank needs at least one block row");
-    std::unique_ptr<Hierarchy> H(setup_hierarchy(std::move(A0), B, b_rows, b_cols, prm, s, t0));
+    std::unique_ptr<Hierarchy> H(setup_hierarchy(std::move(A0), B, b_rows, b_cols, prm, s, t0, pipeline));
     H->owns_stream = false;  // the caller destroys s if anything below throws
     std::vector<int> mine;
     if (id) {

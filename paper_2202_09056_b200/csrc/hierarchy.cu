@@ -72,10 +72,15 @@ uint64_t Hierarchy::memory_footprint() const {
 }
 
 Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int64_t b_cols,
-                           const samg_amg_params &prm, cudaStream_t s, double t_start) {
+                           const samg_amg_params &prm, cudaStream_t s, double t_start, int pipeline) {
     auto H = std::make_unique<Hierarchy>();
     H->stream = s;
     H->prm = prm;
+    H->pipeline = pipeline;
+    // the hybrids run the scalar-space setup (hierarchy.hpp:233-260): the
+    // same transfer operators, the Galerkin product in scalar arithmetic
+    const bool scalar_galerkin =
+        pipeline == SAMG_PIPELINE_NS_HYBRID1 || pipeline == SAMG_PIPELINE_NS_HYBRID2;
     CK(cudaGetDevice(&H->device));
     H->err.alloc(1, s);
     CK(cudaMemsetAsync(H->err.p, 0, sizeof(DevError), s));
@@ -137,9 +142,9 @@ Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int6
         mark("transpose", lvl);
         // Galerkin (csr.hpp:259-262) + fix_decoupled_rows (hierarchy.hpp:357)
         Bsr3 RA, Ac;
-        spgemm(R, Li.A, RA, s);
+        spgemm(R, Li.A, RA, s, scalar_galerkin);
         mark("spgemm_RA", lvl);
-        spgemm(RA, P, Ac, s);
+        spgemm(RA, P, Ac, s, scalar_galerkin);
         RA = Bsr3();
         fix_decoupled_rows(Ac, s);
         mark("spgemm_RAP", lvl);
@@ -304,7 +309,7 @@ samg_solve_report Hierarchy::cg(const double *d_f, double *d_u, const samg_cg_pa
     cudaStream_t s = stream;
     const double t0 = now_s();
     samg_solve_report rep{};
-    rep.variant = SAMG_PIPELINE_NS_BLOCK;
+    rep.variant = pipeline;
     rep.setup_seconds = setup_seconds;
     const int64_t n = finest_dim();
     const Bsr3 &A0 = levels.front().A;

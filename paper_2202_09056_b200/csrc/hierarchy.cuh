@@ -24,6 +24,7 @@ struct Hierarchy {
     cudaStream_t stream = nullptr;
     bool owns_stream = false;  // set once setup succeeded
     samg_amg_params prm{};
+    int pipeline = SAMG_PIPELINE_NS_BLOCK;
     std::vector<Level> levels;
     DevBuf<double> Ainv;       // coarsest inverse, row-major nc x nc
     int64_t nc = 0;
@@ -48,7 +49,9 @@ struct Hierarchy {
 };
 
 // Setup from a device BSR3 fine matrix (consumed) and a host nullspace.
+// pipeline: ns_block, or ns_hybrid1/2 (Galerkin in scalar order)
 Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int64_t b_cols,
-                           const samg_amg_params &prm, cudaStream_t stream, double t_start);
+                           const samg_amg_params &prm, cudaStream_t stream, double t_start,
+                           int pipeline = SAMG_PIPELINE_NS_BLOCK);
 
 } // namespace samgb

@@ -123,8 +123,11 @@ void smooth_prolongation(const Bsr3 &A, const Graph &G, const DevBuf<int> &agg, 
                          cudaStream_t s);
 // R = P^T with transposed blocks (csr.hpp:173-194)
 void transpose(const Bsr3 &P, Bsr3 &R, cudaStream_t s);
-// C = A*B in the reference's order (csr.hpp:199-255)
-void spgemm(const Bsr3 &A, const Bsr3 &B, Bsr3 &C, cudaStream_t s);
+// C = A*B in the reference's order (csr.hpp:199-255): block arithmetic
+// (csr<block3>), or with scalar_order the scalar product of the full-block
+// scalar views (csr<double>: every scalar term added to the accumulator in
+// (ja, q) order) -- the hybrids' scalar Galerkin, hierarchy.hpp:233-260
+void spgemm(const Bsr3 &A, const Bsr3 &B, Bsr3 &C, cudaStream_t s, bool scalar_order = false);
 void fix_decoupled_rows(Bsr3 &A, cudaStream_t s);
 // smoother setup: kind SAMG_SMOOTHER_*
 void setup_smoother(const Bsr3 &A, int kind, double omega, Smoother &M, DevError *err,

@@ -108,6 +108,31 @@ __device__ __forceinline__ void blk_mul(const double *a, const double *b, double
         }
 }
 
+// c += a*b for the SpGEMM accumulators.  Block arithmetic (csr<block3>):
+// the block product first (blk_mul), then added.  Scalar order (csr<double>
+// on the full-block scalar view, csr.hpp:237-243): each scalar term goes
+// straight into the accumulator, terms of one block in q order.
+template <bool kScalar>
+__device__ __forceinline__ void accum_block(const double *a, const double *b, double *c) {
+    if constexpr (kScalar) {
+#pragma unroll
+        for (int p = 0; p < 3; ++p)
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                double t = c[p * 3 + q];
+                t = __dadd_rn(t, __dmul_rn(a[p * 3 + 0], b[0 * 3 + q]));
+                t = __dadd_rn(t, __dmul_rn(a[p * 3 + 1], b[1 * 3 + q]));
+                t = __dadd_rn(t, __dmul_rn(a[p * 3 + 2], b[2 * 3 + q]));
+                c[p * 3 + q] = t;
+            }
+    } else {
+        double prod[9];
+        blk_mul(a, b, prod);
+#pragma unroll
+        for (int e = 0; e < 9; ++e) c[e] = __dadd_rn(c[e], prod[e]);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // to_block<3> of a sorted scalar CSR (csr.hpp:268-324): 3-way merge of the
 // scalar rows' block columns; absent tile entries stay zero.
@@ -622,7 +647,7 @@ __global__ void k_spgemm_count(int nrows, const int *rows, const int *ap, const 
     }
 }
 
-template <bool GLOBAL>
+template <bool GLOBAL, bool kScalar>
 __global__ void __launch_bounds__(256) k_spgemm_numeric(
         int nrows, const int *rows, const int *ap, const int *ac, const double *av,
         const int *bp, const int *bc, const double *bv, int cap, int *keys_g, int *vals_g,
@@ -688,11 +713,7 @@ __global__ void __launch_bounds__(256) k_spgemm_numeric(
         for (int e = 0; e < 9; ++e) am[e] = a[e];
         for (int jb = bp[kk] + threadIdx.x; jb < bp[kk + 1]; jb += blockDim.x) {
             const int slot = vals[hash_find(keys, tcap, bc[jb])];
-            double prod[9];
-            blk_mul(am, bv + 9 * static_cast<int64_t>(jb), prod);
-            double *cb = cval + 9 * (base + slot);
-#pragma unroll
-            for (int e = 0; e < 9; ++e) cb[e] = __dadd_rn(cb[e], prod[e]);
+            accum_block<kScalar>(am, bv + 9 * static_cast<int64_t>(jb), cval + 9 * (base + slot));
         }
         __syncthreads();
     }
@@ -732,6 +753,7 @@ __global__ void __launch_bounds__(256) k_spgemm_wcount(int nrows, const int *row
     if (lane == 0) cnt[row] = full ? -1 : n_all[w];
 }
 
+template <bool kScalar>
 __global__ void __launch_bounds__(256) k_spgemm_wnumeric(
         int nrows, const int *ap, const int *ac, const double *av, const int *bp, const int *bc,
         const double *bv, const int *cp, const int *mode, int *ccol, double *cval) {
@@ -816,17 +838,10 @@ __global__ void __launch_bounds__(256) k_spgemm_wnumeric(
         if (ja + 1 < jend) fetch(ja + 1, an, bn, cn, jbn, kendn);
         if (cc >= 0) {
             const int slot = vals[hash_find(keys, kWCap, cc)];
-            double prod[9];
-            blk_mul(am, bm, prod);
-            double *cb = cval + 9 * (base + slot);
-#pragma unroll
-            for (int e = 0; e < 9; ++e) cb[e] = __dadd_rn(cb[e], prod[e]);
+            accum_block<kScalar>(am, bm, cval + 9 * (base + slot));
             for (int jb = jbc + 32; jb < kend; jb += 32) {
                 const int sl = vals[hash_find(keys, kWCap, bc[jb])];
-                blk_mul(am, bv + 9 * static_cast<int64_t>(jb), prod);
-                double *cb2 = cval + 9 * (base + sl);
-#pragma unroll
-                for (int e = 0; e < 9; ++e) cb2[e] = __dadd_rn(cb2[e], prod[e]);
+                accum_block<kScalar>(am, bv + 9 * static_cast<int64_t>(jb), cval + 9 * (base + sl));
             }
         }
         __syncwarp();
@@ -913,6 +928,7 @@ __global__ void __launch_bounds__(kBWPB * 32) k_spgemm_bcount(int nrows, const i
 
 // numeric pass for the bitmap rows (cnt >= 0 from k_spgemm_bcount; rows
 // marked -2 there are skipped here, the hash kernels do them)
+template <bool kScalar>
 __global__ void __launch_bounds__(kBWPB * 32) k_spgemm_bnumeric(int nrows, const int *ap,
         const int *ac, const double *av, const int *bp, const int *bc, const double *bv,
         const int *cp, const int *mode, const int *win_lo, int words, int acc_cap, int *ccol,
@@ -988,17 +1004,9 @@ __global__ void __launch_bounds__(kBWPB * 32) k_spgemm_bnumeric(int nrows, const
         int cn = -1, jbn = -1, kendn = 0;
         if (ja + 1 < jend) fetch(ja + 1, an, bn, cn, jbn, kendn);
         if (cc >= 0) {
-            double prod[9];
-            blk_mul(am, bmx, prod);
-            double *cb = acc + 9 * slot_of(cc);
-#pragma unroll
-            for (int e = 0; e < 9; ++e) cb[e] = __dadd_rn(cb[e], prod[e]);
-            for (int jb = jbc + 32; jb < kend; jb += 32) {
-                blk_mul(am, bv + 9 * static_cast<int64_t>(jb), prod);
-                double *cb2 = acc + 9 * slot_of(bc[jb]);
-#pragma unroll
-                for (int e = 0; e < 9; ++e) cb2[e] = __dadd_rn(cb2[e], prod[e]);
-            }
+            accum_block<kScalar>(am, bmx, acc + 9 * slot_of(cc));
+            for (int jb = jbc + 32; jb < kend; jb += 32)
+                accum_block<kScalar>(am, bv + 9 * static_cast<int64_t>(jb), acc + 9 * slot_of(bc[jb]));
         }
         __syncwarp();
 #pragma unroll
@@ -1302,7 +1310,9 @@ void transpose(const Bsr3 &P, Bsr3 &R, cudaStream_t s) {
     }, s);
 }
 
-void spgemm(const Bsr3 &A, const Bsr3 &B, Bsr3 &C, cudaStream_t s) {
+namespace {
+template <bool kScalar>
+void spgemm_impl(const Bsr3 &A, const Bsr3 &B, Bsr3 &C, cudaStream_t s) {
     if (A.ncols != B.nrows) fail(SAMG_DIMENSION_MISMATCH, "spgemm: inner dimensions disagree");
     const int n = static_cast<int>(A.nrows);
     C.nrows = A.nrows;
@@ -1443,12 +1453,12 @@ void spgemm(const Bsr3 &A, const Bsr3 &B, Bsr3 &C, cudaStream_t s) {
         const int acc_cap = std::max(0, std::min(512, (budget - bm_bytes) / 72));
         const size_t smem_b = static_cast<size_t>(kBWPB) * (bm_bytes + static_cast<size_t>(acc_cap) * 72);
         static const bool battr = [] {
-            CK(cudaFuncSetAttribute(k_spgemm_bnumeric, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            CK(cudaFuncSetAttribute(k_spgemm_bnumeric<kScalar>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     220 * 1024));
             return true;
         }();
         (void)battr;
-        k_spgemm_bnumeric<<<ceil_div(n, kBWPB), kBWPB * 32, smem_b, s>>>(
+        k_spgemm_bnumeric<kScalar><<<ceil_div(n, kBWPB), kBWPB * 32, smem_b, s>>>(
             n, A.ptr.p, A.col.p, A.val.p, B.ptr.p, B.col.p, B.val.p, C.ptr.p, mode.p, winlo.p, words,
             acc_cap, C.col.p, C.val.p);
         CK_LAUNCH();
@@ -1456,18 +1466,18 @@ void spgemm(const Bsr3 &A, const Bsr3 &B, Bsr3 &C, cudaStream_t s) {
     // 2b. warp-per-row hash numeric pass for the other narrow rows
     if (nfb) {
         const size_t smem_w = static_cast<size_t>(kWPB) * kWCap * 5 / 2 * sizeof(int);
-        CK(cudaFuncSetAttribute(k_spgemm_wnumeric, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CK(cudaFuncSetAttribute(k_spgemm_wnumeric<kScalar>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem_w)));
-        k_spgemm_wnumeric<<<ceil_div(n, kWPB), 256, smem_w, s>>>(n, A.ptr.p, A.col.p, A.val.p, B.ptr.p,
+        k_spgemm_wnumeric<kScalar><<<ceil_div(n, kWPB), 256, smem_w, s>>>(n, A.ptr.p, A.col.p, A.val.p, B.ptr.p,
                                                                  B.col.p, B.val.p, C.ptr.p, mode.p,
                                                                  C.col.p, C.val.p);
         CK_LAUNCH();
     }
     // 3. CTA-per-row numeric pass for the wide rows
     if (nwide) {
-        CK(cudaFuncSetAttribute(k_spgemm_numeric<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CK(cudaFuncSetAttribute(k_spgemm_numeric<false, kScalar>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kMaxCap * 10));
-        k_spgemm_numeric<false><<<nwide, 256, smem_n, s>>>(nwide, wide.p, A.ptr.p, A.col.p, A.val.p,
+        k_spgemm_numeric<false, kScalar><<<nwide, 256, smem_n, s>>>(nwide, wide.p, A.ptr.p, A.col.p, A.val.p,
                                                           B.ptr.p, B.col.p, B.val.p, cap_n, nullptr,
                                                           nullptr, nullptr, nullptr, C.ptr.p, C.col.p,
                                                           C.val.p);
@@ -1475,11 +1485,18 @@ void spgemm(const Bsr3 &A, const Bsr3 &B, Bsr3 &C, cudaStream_t s) {
     }
     if (novf) {
         const int nr = static_cast<int>(orows.n);
-        k_spgemm_numeric<true><<<nr, 256, 0, s>>>(nr, orows.p, A.ptr.p, A.col.p, A.val.p, B.ptr.p,
+        k_spgemm_numeric<true, kScalar><<<nr, 256, 0, s>>>(nr, orows.p, A.ptr.p, A.col.p, A.val.p, B.ptr.p,
                                                  B.col.p, B.val.p, 0, gkeys.p, gvals.p, glist.p,
                                                  goff.p, C.ptr.p, C.col.p, C.val.p);
         CK_LAUNCH();
     }
+}
+
+} // namespace
+
+void spgemm(const Bsr3 &A, const Bsr3 &B, Bsr3 &C, cudaStream_t s, bool scalar_order) {
+    if (scalar_order) spgemm_impl<true>(A, B, C, s);
+    else spgemm_impl<false>(A, B, C, s);
 }
 
 void fix_decoupled_rows(Bsr3 &A, cudaStream_t s) {

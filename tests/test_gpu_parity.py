@@ -79,18 +79,31 @@ CASES = [
                                seed=7), "ilu0", 0.72, 120),
     ("beam_xslow_ilu0", dict(nx=16, ny=4, nz=4, lx=4.0, dirichlet="eliminate", load="traction_xend",
                              x_slowest=True), "ilu0", 0.72, 120),
+    # the hybrid pipelines: scalar-space Galerkin (hierarchy.hpp:233-260)
+    ("box975_hybrid2_spai0", dict(nx=9, ny=7, nz=5, dirichlet="eliminate", load="traction_xend"),
+     "spai0", 0.72, 150, "ns_hybrid2"),
+    ("cube6_keep_hybrid2_ilu0", dict(nx=6, dirichlet="keep_rows"), "ilu0", 0.72, 100, "ns_hybrid2"),
+    ("cube7_hetero_hybrid1_jacobi", dict(nx=7, dirichlet="eliminate", heterogeneous=True,
+                                         load="random", seed=7), "jacobi", 0.5, 120, "ns_hybrid1"),
+    ("beam_hybrid1_bjac", dict(nx=12, ny=4, nz=4, lx=3.0, dirichlet="eliminate",
+                               load="traction_xend", x_slowest=True), "block_jacobi", 0.5, 120,
+     "ns_hybrid1"),
 ]
+PIPE = {"ns_hybrid1": 3, "ns_hybrid2": 4, "ns_block": 5}
 
 
-@pytest.mark.parametrize("name,kw,smoother,omega,ce", CASES, ids=[c[0] for c in CASES])
-def test_setup_and_solve_parity(gpu, ref, orc, name, kw, smoother, omega, ce):
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_setup_and_solve_parity(gpu, ref, orc, case):
+    name, kw, smoother, omega, ce = case[:5]
+    pipeline = case[5] if len(case) > 5 else "ns_block"
     pb = gpu
     p = make_problem(pb, **kw)
     A = p.csr()
     B = p.nullspace()
     prm = pb.AmgParams(smoother=smoother, smoother_omega=omega, coarse_enough=ce)
-    h = pb.setup(A, B, "ns_block", prm)
-    rp = Params(smoother=SM[smoother], smoother_omega=omega, coarse_enough=ce)
+    h = pb.setup(A, B, pipeline, prm)
+    rp = Params(smoother=SM[smoother], smoother_omega=omega, coarse_enough=ce,
+                pipeline=PIPE[pipeline])
     hr = ref.setup(A[0], A[1], A[2], A[3], B, rp)
     ho = orc.setup(A[0], A[1], A[2], A[3], B, rp)
     assert h.nlevels >= 2
@@ -181,9 +194,11 @@ def test_zero_diagonal_rejected(gpu):
 def test_unsupported_pipelines(gpu):
     pb = gpu
     p = make_problem(pb, 3, dirichlet="eliminate")
-    for pl in ("scalar", "block", "ns_scalar", "ns_hybrid1", "ns_hybrid2"):
+    for pl in ("scalar", "block", "ns_scalar"):
         with pytest.raises(pb.Unsupported):
             pb.setup(p.csr(), p.nullspace(), pl)
+    with pytest.raises(pb.Unsupported):  # ilu0<double> is not on the B200 path
+        pb.setup(p.csr(), p.nullspace(), "ns_hybrid1", pb.AmgParams(smoother="ilu0"))
 
 
 def test_spmv_batch_matches_single(gpu):

@@ -193,3 +193,24 @@ def test_breakdown_and_zero_rhs(orc):
     with pytest.raises(OracleError) as e:
         hn.cg_solve(p.rhs)
     assert e.value.code == 9
+
+
+@pytest.mark.parametrize("pipeline", [3, 4])
+def test_hybrid_pipelines_match_reference(orc, ref, pipeline):
+    """ns_hybrid1 / ns_hybrid2 (hierarchy.hpp:233-260, 300-330): the scalar
+    Galerkin path of the restatement equals the reference bit for bit, and
+    differs from ns_block at rounding level (so the test has teeth)."""
+    p = orc.generate_hex(9, 7, 5, 1.0, 0.3, True)
+    n, ptr, col, val = p.n, p.ptr, p.col, p.val
+    B = orc.rigid_body_modes(p.coords)
+    prm = Params(coarse_enough=150, pipeline=pipeline)
+    o = orc.setup(n, ptr, col, val, B, prm)
+    r = ref.setup(n, ptr, col, val, B, prm)
+    assert o.nlevels == r.nlevels >= 3
+    for l in range(o.nlevels):
+        for w in ((0, 1, 2) if l < o.nlevels - 1 else (0,)):
+            np.testing.assert_array_equal(o.level(l, w)[4], r.level(l, w)[4])
+    nb = orc.setup(n, ptr, col, val, B, Params(coarse_enough=150))
+    assert not np.array_equal(nb.level(1)[4], o.level(1)[4])
+    assert o.memory_footprint == r.memory_footprint
+    assert o.cg_solve(p.rhs)[1]["iterations"] == r.cg_solve(p.rhs)[1]["iterations"]
