@@ -168,10 +168,11 @@ class Oracle(_Backend):
         ptr = np.ascontiguousarray(ptr, np.int64)
         col = np.ascontiguousarray(col, np.int64)
         val = np.ascontiguousarray(val, np.float64)
-        B = np.ascontiguousarray(B, np.float64)
+        Bp, bc = (None, 0) if B is None else (_p(B := np.ascontiguousarray(B, np.float64)),
+                                               B.size // n)
         h = vp()
         self._check(self.lib.orc_setup_ns_block(n, _p(ptr, i64p), _p(col, i64p), _p(val),
-                                                _p(B), B.size // n, C.byref(pr), C.byref(h)))
+                                                Bp, bc, C.byref(pr), C.byref(h)))
         return OracleHier(self, h, n)
 
     def spmv_bsr3(self, nrows, ncols, ptr, col, val, x, alpha=1.0, beta=0.0, y=None):
@@ -348,10 +349,11 @@ class Ref(_Backend):
         ptr = np.ascontiguousarray(ptr, np.int64)
         col = np.ascontiguousarray(col, np.int64)
         val = np.ascontiguousarray(val, np.float64)
-        B = np.ascontiguousarray(B, np.float64)
+        Bp, bc = (None, 0) if B is None else (_p(B := np.ascontiguousarray(B, np.float64)),
+                                               B.size // n)
         h = vp()
-        self._check(self.lib.ref_setup(n, _p(ptr, i64p), _p(col, i64p), _p(val), _p(B),
-                                       B.size // n, params.eps_strong, params.omega,
+        self._check(self.lib.ref_setup(n, _p(ptr, i64p), _p(col, i64p), _p(val), Bp,
+                                       bc, params.eps_strong, params.omega,
                                        params.smoother, params.smoother_omega,
                                        params.coarse_enough, params.stagnation_ratio,
                                        params.pipeline, C.byref(h)))

@@ -183,7 +183,8 @@ int ref_setup(int64_t n, const int64_t *ptr, const int64_t *col,
     h->smoother_omega = smoother_omega;
     auto t0 = clk::now();
     // samg::pipeline numbering (hierarchy.hpp:30): 3 ns_hybrid1, 4 ns_hybrid2, 5 ns_block
-    const pipeline pl = pipeline_id == 3 ? pipeline::ns_hybrid1
+    const pipeline pl = pipeline_id == 1 ? pipeline::block
+                      : pipeline_id == 3 ? pipeline::ns_hybrid1
                       : pipeline_id == 4 ? pipeline::ns_hybrid2 : pipeline::ns_block;
     h->H = setup(A, Bd, pl, prm);
     const samg::index L = h->H.nlevels();
@@ -220,9 +221,14 @@ int ref_setup(int64_t n, const int64_t *ptr, const int64_t *col,
     h->agg.resize(L);
     h->agg_count.assign(L, 0);
     for (samg::index l = 0; l + 1 < L; ++l) {
-        scalar_csr S = to_scalar(blk(h->H.levels[l].A));
-        const int pbs = l == 0 ? 3 : static_cast<int>(bcols);
-        adjacency G = strength_graph(S, eps_strong, pbs);
+        adjacency G;
+        if (pl == pipeline::block) {  // block_transfer_operators, coarsening.hpp:471
+            G = strength_graph(blk(h->H.levels[l].A), eps_strong, 1);
+        } else {
+            scalar_csr S = to_scalar(blk(h->H.levels[l].A));
+            const int pbs = l == 0 ? 3 : static_cast<int>(bcols);
+            G = strength_graph(S, eps_strong, pbs);
+        }
         aggregates a = aggregate(G);
         h->agg[l] = a.id;
         h->agg_count[l] = a.count;

@@ -362,9 +362,13 @@ static int cmp_cw(const void *a, const void *b) {
 
 /* strength_graph for scalar matrices with point-block condensation
  * (coarsening.hpp:52-77 condense_weights, :81-123 strength_graph). */
+/* For a block matrix (b = 3, the block pipeline) the node is the block row
+ * and the weight the Frobenius norm of the block (condense_weights,
+ * coarsening.hpp:55-62; fnorm, static_block.hpp:111-115). */
 static orc_adj strength_graph(const orc_mat *A, double eps_strong, int pbs) {
     if (A->nrows != A->ncols)
         fail(ORC_NON_SQUARE, "strength_graph: matrix must be square");
+    if (A->b == 3) pbs = 1;
     if (A->nrows % pbs)
         fail(ORC_NOT_DIVISIBLE, "strength_graph: rows not divisible by point block size");
     const int64_t n = A->nrows / pbs;
@@ -379,7 +383,13 @@ static orc_adj strength_graph(const orc_mat *A, double eps_strong, int pbs) {
             const int64_t i = ni * pbs + r;
             for (int64_t j = A->ptr[i]; j < A->ptr[i + 1]; ++j) {
                 w[nw].c = A->col[j] / pbs;
-                w[nw].w = fabs(A->val[j]);
+                if (A->b == 3) {
+                    double sq = 0;
+                    for (int e = 0; e < 9; ++e) sq += A->val[9 * j + e] * A->val[9 * j + e];
+                    w[nw].w = sqrt(sq);
+                } else {
+                    w[nw].w = fabs(A->val[j]);
+                }
                 ++nw;
             }
         }
@@ -751,6 +761,110 @@ static void setup_block_smoother(orc_level *L, int kind, double omega) {
     }
 }
 
+/* block_transfer_operators (coarsening.hpp:466-499) for the block pipeline:
+ * indicator tentative operator with identity blocks scaled by
+ * 1/sqrt(|aggregate|), smoothed with block diagonal inverses
+ * (smooth_prolongation<block3>, coarsening.hpp:320-411, pbs = 1). */
+static orc_mat block_transfer(const orc_mat *A, const orc_adj *G, const int64_t *agg,
+                              int64_t naggs, double omega) {
+    const int64_t n = A->nrows;
+    int64_t *cnt = xcalloc(naggs + 1, sizeof(int64_t));
+    for (int64_t i = 0; i < n; ++i) cnt[agg[i]]++;
+    double *pv = xmalloc(sizeof(double) * (naggs + 1));
+    for (int64_t g = 0; g < naggs; ++g) pv[g] = 1.0 / sqrt((double)cnt[g]);
+    free(cnt);
+    /* tentative blocks v*I (operator*(double, block): v*1, v*0) */
+    double *ptb = xmalloc(sizeof(double) * 9 * (n + 1));
+    for (int64_t i = 0; i < n; ++i)
+        for (int e = 0; e < 9; ++e) ptb[9 * i + e] = pv[agg[i]] * ((e % 4 == 0) ? 1.0 : 0.0);
+    free(pv);
+    orc_mat P = {n, naggs, 3, xcalloc(n + 1, sizeof(int64_t)), NULL, NULL};
+    if (omega == 0.0) {  /* return P_tent */
+        P.col = xmalloc(sizeof(int64_t) * (n + 1));
+        P.val = ptb;
+        for (int64_t i = 0; i < n; ++i) { P.ptr[i + 1] = i + 1; P.col[i] = agg[i]; }
+        return P;
+    }
+    int64_t *marker = xmalloc(sizeof(int64_t) * (n + 1));
+    for (int64_t i = 0; i < n; ++i) marker[i] = -1;
+    const int64_t nnz = A->ptr[n];
+    char *keep = xcalloc(nnz + 1, 1);
+    double *diag = xcalloc(9 * (n + 1), sizeof(double));
+    for (int64_t i = 0; i < n; ++i) {
+        for (int64_t j = G->ptr[i]; j < G->ptr[i + 1]; ++j) marker[G->col[j]] = i;
+        for (int64_t j = A->ptr[i]; j < A->ptr[i + 1]; ++j) {
+            const int64_t c = A->col[j];
+            if (c == i) {
+                keep[j] = 1;
+                for (int e = 0; e < 9; ++e) diag[9 * i + e] += A->val[9 * j + e];
+            } else if (marker[c] == i) {
+                keep[j] = 1;
+            } else {
+                for (int e = 0; e < 9; ++e) diag[9 * i + e] += A->val[9 * j + e];
+            }
+        }
+    }
+    double *inv = xmalloc(sizeof(double) * 9 * (n + 1));
+    for (int64_t i = 0; i < n; ++i) {
+        int zero = 1;
+        for (int e = 0; e < 9; ++e) if (diag[9 * i + e] != 0.0) zero = 0;
+        if (zero) fail(ORC_ZERO_DIAGONAL, "smooth_prolongation: zero filtered diagonal");
+        blk_inverse(diag + 9 * i, inv + 9 * i);
+    }
+    /* rows: P_tent column first, then kept entries in order; first touch
+     * assigns the product, later touches add it; columns sorted */
+    int64_t cap = 0;
+    for (int64_t i = 0; i < n; ++i) cap += 1 + (A->ptr[i + 1] - A->ptr[i]);
+    P.col = xmalloc(sizeof(int64_t) * (cap + 1));
+    P.val = xmalloc(sizeof(double) * 9 * (cap + 1));
+    int64_t out = 0;
+    int64_t rc[64];
+    double racc[64 * 9];
+    for (int64_t i = 0; i < n; ++i) {
+        int m = 0;
+        rc[m] = agg[i];
+        memcpy(racc, ptb + 9 * i, sizeof(double) * 9);
+        ++m;
+        for (int64_t j = A->ptr[i]; j < A->ptr[i + 1]; ++j) {
+            if (!keep[j]) continue;
+            const int64_t k = A->col[j];
+            const double *coef = (k == i) ? diag + 9 * i : A->val + 9 * j;
+            double scaled[9], prod[9];
+            blk_mul(inv + 9 * i, coef, scaled);
+            for (int e = 0; e < 9; ++e) scaled[e] *= -omega;
+            blk_mul(scaled, ptb + 9 * k, prod);
+            const int64_t c = agg[k];
+            int at = -1;
+            for (int t = 0; t < m; ++t) if (rc[t] == c) { at = t; break; }
+            if (at < 0) {
+                if (m == 64) fail(ORC_ERROR, "block_transfer: row too long");
+                rc[m] = c;
+                memcpy(racc + 9 * m, prod, sizeof prod);
+                ++m;
+            } else {
+                for (int e = 0; e < 9; ++e) racc[9 * at + e] += prod[e];
+            }
+        }
+        /* sort the row's columns (insertion sort, <= 64 entries) */
+        for (int a = 1; a < m; ++a)
+            for (int b2 = a; b2 > 0 && rc[b2 - 1] > rc[b2]; --b2) {
+                int64_t t = rc[b2]; rc[b2] = rc[b2 - 1]; rc[b2 - 1] = t;
+                double tv[9];
+                memcpy(tv, racc + 9 * b2, sizeof tv);
+                memcpy(racc + 9 * b2, racc + 9 * (b2 - 1), sizeof tv);
+                memcpy(racc + 9 * (b2 - 1), tv, sizeof tv);
+            }
+        for (int t = 0; t < m; ++t) {
+            P.col[out] = rc[t];
+            memcpy(P.val + 9 * out, racc + 9 * t, sizeof(double) * 9);
+            ++out;
+        }
+        P.ptr[i + 1] = out;
+    }
+    free(marker); free(keep); free(diag); free(inv); free(ptb);
+    return P;
+}
+
 /* ilu0<block3> ctor (relaxation.hpp:103-136): IKJ elimination restricted
  * to A's pattern, L_ik = A_ik * inverse(U_kk), inverted pivots.  The
  * smoother data is [factors (9*nnz) | inverted pivots (9*nrows)]. */
@@ -896,7 +1010,8 @@ int orc_setup_ns_block(int64_t n, const int64_t *ptr, const int64_t *col,
         const double *val, const double *B, int64_t bcols,
         const orc_params *prm, orc_hier **out) {
     API_BEGIN
-    if (!B) fail(ORC_BAD_NULLSPACE_SHAPE, "setup: pipeline requires a nullspace basis");
+    const int blockp = prm->pipeline == ORC_PIPELINE_BLOCK;
+    if (!B && !blockp) fail(ORC_BAD_NULLSPACE_SHAPE, "setup: pipeline requires a nullspace basis");
     if (n % 3) fail(ORC_NOT_DIVISIBLE, "setup: block pipelines require dimension divisible by 3");
     orc_hier *H = xcalloc(1, sizeof(orc_hier));
     H->prm = *prm;
@@ -905,11 +1020,39 @@ int orc_setup_ns_block(int64_t n, const int64_t *ptr, const int64_t *col,
     orc_mat Ain = {n, n, 1, (int64_t *)ptr, (int64_t *)col, (double *)val};
     H->lv[0].A = to_block3(&Ain);
     H->nlev = 1;
-    double *Bi = xmalloc(sizeof(double) * n * bcols);
-    memcpy(Bi, B, sizeof(double) * n * bcols);
+    double *Bi = NULL;
     int64_t bi_rows = n, k = bcols;
+    if (!blockp) {
+        Bi = xmalloc(sizeof(double) * n * bcols);
+        memcpy(Bi, B, sizeof(double) * n * bcols);
+    }
     while (H->lv[H->nlev - 1].A.nrows * 3 > prm->coarse_enough) {
         orc_level *Li = &H->lv[H->nlev - 1];
+        if (blockp) {
+            /* block pipeline (hierarchy.hpp:340-347): block_transfer_operators */
+            orc_adj G = strength_graph(&Li->A, prm->eps_strong, 1);
+            int64_t *agg = xmalloc(sizeof(int64_t) * (G.nnodes + 1));
+            const int64_t naggs = aggregate(&G, agg);
+            orc_mat P = block_transfer(&Li->A, &G, agg, naggs, prm->omega);
+            orc_mat R = transpose(&P);
+            free(G.ptr); free(G.col);
+            if ((double)(P.ncols * 3) > prm->stagnation_ratio * (double)(Li->A.nrows * 3)) {
+                mat_free(&P); mat_free(&R); free(agg);
+                break;
+            }
+            orc_mat Ac = galerkin(&R, &Li->A, &P);
+            fix_decoupled_rows(&Ac);
+            Li->P = P; Li->R = R; Li->has_transfer = 1;
+            Li->agg = agg; Li->nnodes = G.nnodes; Li->naggs = naggs;
+            if (H->nlev == cap) {
+                cap *= 2;
+                H->lv = realloc(H->lv, sizeof(orc_level) * cap);
+                memset(H->lv + H->nlev, 0, sizeof(orc_level) * (cap - H->nlev));
+            }
+            H->lv[H->nlev].A = Ac;
+            H->nlev++;
+            continue;
+        }
         const int pbs = (H->nlev == 1) ? 3 : (int)k;
         /* as_scalar_transfer: to_scalar -> transfer_operators -> to_block */
         orc_mat As = to_scalar(&Li->A);

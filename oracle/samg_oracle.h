@@ -68,7 +68,8 @@ typedef struct {
 } orc_params;
 
 /* samg::pipeline values (hierarchy.hpp:30) handled by orc_setup_ns_block */
-enum { ORC_PIPELINE_NS_HYBRID1 = 3, ORC_PIPELINE_NS_HYBRID2 = 4, ORC_PIPELINE_NS_BLOCK = 5 };
+enum { ORC_PIPELINE_BLOCK = 1, ORC_PIPELINE_NS_HYBRID1 = 3, ORC_PIPELINE_NS_HYBRID2 = 4,
+       ORC_PIPELINE_NS_BLOCK = 5 };
 
 typedef struct {
     int iterations;
