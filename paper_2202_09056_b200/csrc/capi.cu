@@ -131,9 +131,10 @@ void validate_params(const samg_amg_params *prm, int pipeline) {
     // ns_block, and the hybrids that differ from it only in the Galerkin
     // arithmetic (scalar order, hierarchy.hpp:233-260) and, for ns_hybrid1,
     // in scalar smoothers (ilu0<double> is not on the B200 path)
+    // block: no nullspace, block strength / transfer (hierarchy.hpp:340-347)
     if (pipeline != SAMG_PIPELINE_NS_BLOCK && pipeline != SAMG_PIPELINE_NS_HYBRID2 &&
-        pipeline != SAMG_PIPELINE_NS_HYBRID1)
-        fail(SAMG_UNSUPPORTED, "setup: pipelines scalar, block and ns_scalar are not on the B200 path");
+        pipeline != SAMG_PIPELINE_NS_HYBRID1 && pipeline != SAMG_PIPELINE_BLOCK)
+        fail(SAMG_UNSUPPORTED, "setup: pipelines scalar and ns_scalar are not on the B200 path");
     if (pipeline == SAMG_PIPELINE_NS_HYBRID1 && prm && prm->smoother == SAMG_SMOOTHER_ILU0)
         fail(SAMG_UNSUPPORTED, "setup: ns_hybrid1 with scalar ILU(0) is not on the B200 path");
     require(prm->smoother >= 0 && prm->smoother <= 3, SAMG_INVALID_ARGUMENT, "setup: unknown smoother");
@@ -142,8 +143,12 @@ void validate_params(const samg_amg_params *prm, int pipeline) {
 }
 
 // hierarchy.hpp:267-282 + coarsening.hpp:269-270 checks
-void validate_ns(int64_t n, const double *B, int64_t b_rows, int64_t b_cols) {
+void validate_ns(int64_t n, const double *B, int64_t b_rows, int64_t b_cols, int pipeline) {
     require(n >= 0, SAMG_INVALID_ARGUMENT, "setup: negative dimension");
+    if (pipeline == SAMG_PIPELINE_BLOCK) {  // the block pipeline ignores B
+        if (n % 3) fail(SAMG_NOT_DIVISIBLE, "setup: block pipelines require dimension divisible by 3");
+        return;
+    }
     if (!B) fail(SAMG_BAD_NULLSPACE_SHAPE, "setup: pipeline requires a nullspace basis");
     if (b_rows != n) fail(SAMG_BAD_NULLSPACE_SHAPE, "setup: nullspace rows do not match matrix");
     if (n % 3) fail(SAMG_NOT_DIVISIBLE, "setup: block pipelines require dimension divisible by 3");
@@ -314,7 +319,7 @@ SAMG_API int samg_setup(int64_t n, const int64_t *ptr, const int64_t *col, const
         require(out != nullptr, SAMG_INVALID_ARGUMENT, "setup: out must not be NULL");
         *out = nullptr;
         validate_params(prm, pipeline);
-        validate_ns(n, B, b_rows, b_cols);
+        validate_ns(n, B, b_rows, b_cols, pipeline);
         require(ptr && ptr[0] == 0 && (ptr[n] == 0 || (col && val)), SAMG_INVALID_ARGUMENT,
                 "setup: malformed CSR arrays");
         need_device(prm->device);
@@ -347,7 +352,7 @@ SAMG_API int samg_setup_bsr3(int64_t nbrows, const int64_t *ptr, const int64_t *
         require(out != nullptr, SAMG_INVALID_ARGUMENT, "setup: out must not be NULL");
         *out = nullptr;
         validate_params(prm, pipeline);
-        validate_ns(3 * nbrows, B, b_rows, b_cols);
+        validate_ns(3 * nbrows, B, b_rows, b_cols, pipeline);
         need_device(prm->device);
         cudaStream_t s = new_stream();
         Bsr3 A0;
@@ -373,7 +378,7 @@ SAMG_API int samg_setup_device(const samg_bsr3 *A, const double *B, int64_t b_ro
         validate_params(prm, pipeline);
         const Bsr3 &M = *A->m;
         if (M.nrows != M.ncols) fail(SAMG_NON_SQUARE, "transfer_operators: matrix must be square");
-        validate_ns(3 * M.nrows, B, b_rows, b_cols);
+        validate_ns(3 * M.nrows, B, b_rows, b_cols, pipeline);
         need_device(prm->device);
         require(A->device == prm->device, SAMG_INVALID_ARGUMENT, "setup_device: matrix lives on another device");
         cudaStream_t s = new_stream();
@@ -871,7 +876,7 @@ SAMG_API int samg_dsetup(const unsigned char id[128], int nranks, int rank, int6
                 "dsetup: bad arguments");
         *out = nullptr;
         validate_params(prm, pipeline);
-        validate_ns(3 * nbrows, B, b_rows, b_cols);
+        validate_ns(3 * nbrows, B, b_rows, b_cols, pipeline);
         need_device(prm->device);
         cudaStream_t s = new_stream();
         try {

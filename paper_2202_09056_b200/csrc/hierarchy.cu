@@ -101,16 +101,57 @@ Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int6
         t_mark = t;
     };
     mark("upload", 0);
-    const int k = static_cast<int>(b_cols);
-    DevBuf<double> B(b_rows * b_cols, s);
-    // B may be host (pageable/pinned) or device memory (samg_setup_device)
-    CK(cudaMemcpyAsync(B.p, B_host, sizeof(double) * b_rows * b_cols, cudaMemcpyDefault, s));
+    const bool block = pipeline == SAMG_PIPELINE_BLOCK;  // no nullspace
+    const int k = block ? 0 : static_cast<int>(b_cols);
+    DevBuf<double> B;
+    if (!block) {
+        B.alloc(b_rows * b_cols, s);
+        // B may be host (pageable/pinned) or device memory (samg_setup_device)
+        CK(cudaMemcpyAsync(B.p, B_host, sizeof(double) * b_rows * b_cols, cudaMemcpyDefault, s));
+    }
 
     H->levels.emplace_back();
     H->levels.back().A = std::move(A0);
     // level loop (hierarchy.hpp:338-363)
     while (3 * H->levels.back().A.nrows > prm.coarse_enough) {
         Level &Li = H->levels.back();
+        const size_t lvl = H->levels.size() - 1;
+        if (block) {
+            // block pipeline (hierarchy.hpp:340-347): Frobenius-norm block
+            // strength, block_transfer_operators (coarsening.hpp:471-560)
+            Graph G;
+            strength_graph(Li.A, 1, prm.eps_strong, G, s, true);
+            mark("strength", lvl);
+            DevBuf<int> agg;
+            DevBuf<int> seedno;
+            const int64_t naggs = aggregate(G, agg, s, &seedno);
+            mark("aggregate", lvl);
+            Bsr3 P;
+            block_transfer(Li.A, G, agg, naggs, prm.omega, P, err, s);
+            check_dev_error(err, s);
+            mark("block_P", lvl);
+            if (static_cast<double>(3 * P.ncols) >
+                prm.stagnation_ratio * static_cast<double>(3 * Li.A.nrows))
+                break;
+            Bsr3 R;
+            transpose(P, R, s);
+            Bsr3 RA, Ac;
+            spgemm(R, Li.A, RA, s);
+            spgemm(RA, P, Ac, s);
+            RA = Bsr3();
+            fix_decoupled_rows(Ac, s);
+            mark("galerkin", lvl);
+            Li.P = std::move(P);
+            Li.R = std::move(R);
+            Li.has_transfer = true;
+            Li.agg = std::move(agg);
+            Li.nnodes = G.nnodes;
+            Li.naggs = naggs;
+            Li.seedno = std::move(seedno);
+            H->levels.emplace_back();
+            H->levels.back().A = std::move(Ac);
+            continue;
+        }
         // ns pipelines force point_block_size = 3 on the fine level
         // (hierarchy.hpp:284-285), then use the nullspace width (:351-353)
         const int pbs = H->levels.size() == 1 ? 3 : k;
@@ -119,7 +160,6 @@ Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int6
         if (Li.A.nrows % h)
             fail(SAMG_NOT_DIVISIBLE, "strength_graph: rows not divisible by point block size");
         Graph G;
-        const size_t lvl = H->levels.size() - 1;
         strength_graph(Li.A, h, prm.eps_strong, G, s);
         mark("strength", lvl);
         DevBuf<int> agg;

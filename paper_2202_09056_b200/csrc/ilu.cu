@@ -24,6 +24,7 @@
 #include <cstdlib>
 #include <vector>
 
+#include "block3.cuh"
 #include "kernels.cuh"
 
 namespace samgb {
@@ -72,42 +73,6 @@ __device__ __forceinline__ void wait_deps(const int *col, int b, int e, int *fla
 
 __device__ void raise_err(DevError *err, int code, int64_t where) {
     if (atomicCAS(&err->code, 0, code) == 0) err->where = where;
-}
-
-// inverse (static_block.hpp:119-158); false on a singular pivot
-__device__ bool blk_inverse_ref(const double *a, double *inv) {
-    double lu[9];
-    int piv[3];
-    for (int e = 0; e < 9; ++e) lu[e] = a[e];
-    for (int k = 0; k < 3; ++k) {
-        int p = k;
-        for (int r = k + 1; r < 3; ++r)
-            if (fabs(lu[r * 3 + k]) > fabs(lu[p * 3 + k])) p = r;
-        piv[k] = p;
-        if (p != k)
-            for (int j = 0; j < 3; ++j) { const double t = lu[k * 3 + j]; lu[k * 3 + j] = lu[p * 3 + j]; lu[p * 3 + j] = t; }
-        if (fabs(lu[k * 3 + k]) < 1e-300) return false;
-        const double d = __ddiv_rn(1.0, lu[k * 3 + k]);
-        for (int r = k + 1; r < 3; ++r) {
-            const double l = __dmul_rn(lu[r * 3 + k], d);
-            lu[r * 3 + k] = l;
-            for (int j = k + 1; j < 3; ++j) lu[r * 3 + j] = __dsub_rn(lu[r * 3 + j], __dmul_rn(l, lu[k * 3 + j]));
-        }
-    }
-    for (int c = 0; c < 3; ++c) {
-        double x[3] = {0.0, 0.0, 0.0};
-        x[c] = 1.0;
-        for (int k = 0; k < 3; ++k)
-            if (piv[k] != k) { const double t = x[k]; x[k] = x[piv[k]]; x[piv[k]] = t; }
-        for (int r = 1; r < 3; ++r)
-            for (int j = 0; j < r; ++j) x[r] = __dsub_rn(x[r], __dmul_rn(lu[r * 3 + j], x[j]));
-        for (int r = 2; r >= 0; --r) {
-            for (int j = r + 1; j < 3; ++j) x[r] = __dsub_rn(x[r], __dmul_rn(lu[r * 3 + j], x[j]));
-            x[r] = __ddiv_rn(x[r], lu[r * 3 + r]);
-        }
-        for (int r = 0; r < 3; ++r) inv[r * 3 + c] = x[r];
-    }
-    return true;
 }
 
 __global__ void k_ilu_dpos(int n, const int *ptr, const int *col, int *dpos, DevError *err) {

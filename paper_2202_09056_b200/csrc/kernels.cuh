@@ -107,8 +107,11 @@ struct Graph {  // node adjacency, symmetric, sorted rows (coarsening.hpp:33-38)
 // scalar CSR (int64 on host layout) uploaded -> BSR3 (csr.hpp:268-324)
 void scalar_to_bsr3(int64_t n, const int64_t *d_ptr, const int64_t *d_col, const double *d_val,
                     Bsr3 &out, cudaStream_t s);
-// strength graph on nodes of h block rows (coarsening.hpp:52-123)
-void strength_graph(const Bsr3 &A, int h, double eps_strong, Graph &G, cudaStream_t s);
+// strength graph on nodes of h block rows (coarsening.hpp:52-123); tile
+// weight max|a| of the scalar view, or with fnorm (the block pipeline's
+// csr<block3> strength, pbs 1) the block's Frobenius norm
+void strength_graph(const Bsr3 &A, int h, double eps_strong, Graph &G, cudaStream_t s,
+                    bool fnorm = false);
 // aggregation (coarsening.hpp:131-160); returns the aggregate count
 // seedno (optional out): #pass-1 seeds before each node, nnodes+1 entries
 int64_t aggregate(const Graph &G, DevBuf<int> &agg, cudaStream_t s, DevBuf<int> *seedno = nullptr);
@@ -121,6 +124,11 @@ void tentative(const DevBuf<int> &agg, int64_t nnodes, int64_t naggs, int pbs, c
 void smooth_prolongation(const Bsr3 &A, const Graph &G, const DevBuf<int> &agg, int64_t naggs,
                          int pbs, int k, const double *Pt, double omega, Bsr3 &P, DevError *err,
                          cudaStream_t s);
+// block pipeline transfer (block_transfer_operators, coarsening.hpp:471-560):
+// identity-block tentative scaled by 1/sqrt(|aggregate|), smoothed with the
+// inverse of the lumped filtered block diagonal; P is n-by-naggs blocks
+void block_transfer(const Bsr3 &A, const Graph &G, const DevBuf<int> &agg, int64_t naggs,
+                    double omega, Bsr3 &P, DevError *err, cudaStream_t s);
 // R = P^T with transposed blocks (csr.hpp:173-194)
 void transpose(const Bsr3 &P, Bsr3 &R, cudaStream_t s);
 // C = A*B in the reference's order (csr.hpp:199-255): block arithmetic

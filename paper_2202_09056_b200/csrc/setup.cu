@@ -20,6 +20,7 @@
 //   fix_decoupled_rows     hierarchy.hpp:172-191    -> k_fix_rows
 //   damped_jacobi ctor     relaxation.hpp:147-162   -> k_sm_point
 //   block smoothers        DESIGN.md section 4      -> k_sm_block
+#include "block3.cuh"
 #include "kernels.cuh"
 
 #include <cub/cub.cuh>
@@ -199,6 +200,18 @@ __global__ void k_block_maxabs(int64_t nnzb, const double *val, double *wblk) {
         double w = 0.0;
         for (int e = 0; e < 9; ++e) w = fmax(w, fabs(b[e]));
         wblk[j] = w;
+    }
+}
+
+// per-block Frobenius norm (static_block.hpp:111-115: sum of squares in
+// entry order, then sqrt) -- the block pipeline's strength weight
+__global__ void k_block_fnorm(int64_t nnzb, const double *val, double *wblk) {
+    for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < nnzb;
+         j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double *b = val + 9 * j;
+        double q = 0.0;
+        for (int e = 0; e < 9; ++e) q = __dadd_rn(q, __dmul_rn(b[e], b[e]));
+        wblk[j] = __dsqrt_rn(q);
     }
 }
 
@@ -551,6 +564,98 @@ __global__ void k_psm_vals(int64_t nsc, int pbs, int h, int k, const int *ptr, c
         const int64_t base = pptr[br] + static_cast<int64_t>(t) * kb;
         for (int c = 0; c < k; ++c) pval[9 * (base + c / 3) + 3 * rr + c % 3] = acc[c];
     }
+}
+
+// ---------------------------------------------------------------------------
+// block pipeline transfer (block_transfer_operators, coarsening.hpp:471-560).
+// Tentative: block v_g * I for node i in aggregate g, v_g = 1/sqrt(|g|).
+// Filtered diagonal D_i = sum, in row order, of the diagonal block and every
+// weak off-diagonal block; P row i = the tentative entry first, then for each
+// kept entry k (diagonal or strong) in row order the block
+// ((D_i^-1 * coef) * -omega) * Ptent_k, where coef = D_i on the diagonal;
+// the first contribution to a column assigns, later ones add.
+
+__global__ void k_bt_count(int n, const int *agg, int *cnt) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) atomicAdd(cnt + agg[i], 1);
+}
+
+__global__ void k_bt_scale(int naggs, const int *cnt, double *pv) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < naggs) pv[g] = __ddiv_rn(1.0, __dsqrt_rn(static_cast<double>(cnt[g])));
+}
+
+__device__ __forceinline__ void bt_tent(double v, double *t) {
+    for (int e = 0; e < 9; ++e) t[e] = __dmul_rn(v, (e % 4 == 0) ? 1.0 : 0.0);
+}
+
+// omega == 0: P = P_tent
+__global__ void k_bt_tent(int n, const int *agg, const double *pv, int *pptr, int *pcol,
+                          double *pval) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i > n) return;
+    pptr[i] = i;
+    if (i == n) return;
+    pcol[i] = agg[i];
+    bt_tent(pv[agg[i]], pval + 9 * static_cast<int64_t>(i));
+}
+
+// lumped filtered diagonal and its inverse, a thread per block row
+__global__ void k_bt_diag(int n, const int *ptr, const int *col, const double *val,
+                          const int *gp, const int *gc, double *dg, double *dinv, DevError *err) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double d[9];
+    for (int e = 0; e < 9; ++e) d[e] = 0.0;
+    for (int j = ptr[i]; j < ptr[i + 1]; ++j) {
+        const int c = col[j];
+        if (c != i && strong(gp, gc, i, c)) continue;
+        const double *b = val + 9 * static_cast<int64_t>(j);
+        for (int e = 0; e < 9; ++e) d[e] = __dadd_rn(d[e], b[e]);
+    }
+    bool zero = true;
+    for (int e = 0; e < 9; ++e) {
+        dg[9 * static_cast<int64_t>(i) + e] = d[e];
+        if (d[e] != 0.0) zero = false;
+    }
+    double inv[9];
+    if (zero) { raise(err, SAMG_ZERO_DIAGONAL, i); return; }
+    if (!blk_inverse_ref(d, inv)) { raise(err, SAMG_SINGULAR_BLOCK, i); return; }
+    for (int e = 0; e < 9; ++e) dinv[9 * static_cast<int64_t>(i) + e] = inv[e];
+}
+
+// one thread per P entry (row i, aggregate column g)
+__global__ void k_bt_vals(int64_t nnzb, int n, const int *ptr, const int *col, const double *val,
+                          const int *gp, const int *gc, const int *agg, const double *pv,
+                          const double *dg, const double *dinv, double omega, const int *pptr,
+                          const int *pcol, double *pval) {
+    const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (e >= nnzb) return;
+    const int i = lower_bound_int(pptr, n + 1, static_cast<int>(e) + 1) - 1;
+    const int g = pcol[e];
+    double acc[9], inv[9];
+    bool touched = agg[i] == g;
+    if (touched) bt_tent(pv[g], acc);
+    for (int q = 0; q < 9; ++q) inv[q] = dinv[9 * static_cast<int64_t>(i) + q];
+    const double nom = -omega;
+    for (int j = ptr[i]; j < ptr[i + 1]; ++j) {
+        const int k = col[j];
+        if (agg[k] != g) continue;
+        if (k != i && !strong(gp, gc, i, k)) continue;
+        const double *coef = k == i ? dg + 9 * static_cast<int64_t>(i) : val + 9 * static_cast<int64_t>(j);
+        double sc[9], t[9], prod[9];
+        blk_mul_ref(inv, coef, sc);
+        for (int q = 0; q < 9; ++q) sc[q] = __dmul_rn(sc[q], nom);
+        bt_tent(pv[g], t);
+        blk_mul_ref(sc, t, prod);
+        if (touched) {
+            for (int q = 0; q < 9; ++q) acc[q] = __dadd_rn(acc[q], prod[q]);
+        } else {
+            for (int q = 0; q < 9; ++q) acc[q] = prod[q];
+            touched = true;
+        }
+    }
+    for (int q = 0; q < 9; ++q) pval[9 * e + q] = acc[q];
 }
 
 // omega == 0: P is the tentative operator (coarsening.hpp:326)
@@ -1077,13 +1182,17 @@ void scalar_to_bsr3(int64_t n, const int64_t *d_ptr, const int64_t *d_col, const
     CK_LAUNCH();
 }
 
-void strength_graph(const Bsr3 &A, int h, double eps_strong, Graph &G, cudaStream_t s) {
+void strength_graph(const Bsr3 &A, int h, double eps_strong, Graph &G, cudaStream_t s,
+                    bool fnorm) {
     const int n = static_cast<int>(A.nrows / h);
     const double eps2 = eps_strong * eps_strong;
     DevBuf<double> d(n, s), wblk(A.nnzb + 1, s);
     const int grid = ceil_div(n, 256);
-    k_block_maxabs<<<std::max(1, std::min(ceil_div(A.nnzb, 256), 65535)), 256, 0, s>>>(A.nnzb, A.val.p,
-                                                                                    wblk.p);
+    const int wgrid = std::max(1, std::min(ceil_div(A.nnzb, 256), 65535));
+    if (fnorm)
+        k_block_fnorm<<<wgrid, 256, 0, s>>>(A.nnzb, A.val.p, wblk.p);
+    else
+        k_block_maxabs<<<wgrid, 256, 0, s>>>(A.nnzb, A.val.p, wblk.p);
     k_strength_diag<<<grid, 256, 0, s>>>(n, h, A.ptr.p, A.col.p, wblk.p, d.p);
     CK_LAUNCH();
     DevBuf<int> cnt(n + 1, s), off(n + 1, s);
@@ -1270,6 +1379,51 @@ void smooth_prolongation(const Bsr3 &A, const Graph &G, const DevBuf<int> &agg, 
                                                   G.ptr.p, G.col.p, agg.p, toff.p, tlist.p,
                                                   tcnt.p, dinv.p, diag.p, Pt, omega, P.ptr.p,
                                                   P.val.p);
+    CK_LAUNCH();
+}
+
+void block_transfer(const Bsr3 &A, const Graph &G, const DevBuf<int> &agg, int64_t naggs,
+                    double omega, Bsr3 &P, DevError *err, cudaStream_t s) {
+    const int n = static_cast<int>(A.nrows);
+    DevBuf<int> cnt(naggs + 1, s);
+    DevBuf<double> pv(naggs + 1, s);
+    CK(cudaMemsetAsync(cnt.p, 0, sizeof(int) * (naggs + 1), s));
+    k_bt_count<<<ceil_div(n, 256), 256, 0, s>>>(n, agg.p, cnt.p);
+    k_bt_scale<<<ceil_div(naggs, 256), 256, 0, s>>>(static_cast<int>(naggs), cnt.p, pv.p);
+    CK_LAUNCH();
+    if (omega == 0.0) {
+        P.alloc(n, naggs, n, s);
+        k_bt_tent<<<ceil_div(n + 1, 256), 256, 0, s>>>(n, agg.p, pv.p, P.ptr.p, P.col.p, P.val.p);
+        CK_LAUNCH();
+        return;
+    }
+    // columns: the sorted distinct aggregates of the row's kept entries and
+    // its own (k_psm_touch with one block row per node)
+    DevBuf<int> rl(n + 1, s), toff(n + 1, s), tcnt(n + 1, s);
+    const int *ap = A.ptr.p;
+    int *rlp = rl.p;
+    for_each(n, [=] __device__(int64_t i) { rlp[i] = ap[i + 1] - ap[i] + 1; }, s);
+    const int64_t tl = scan_counts(rl.p, toff.p, n, s);
+    DevBuf<int> tlist(tl + 1, s);
+    k_psm_touch<<<ceil_div(n, 128), 128, 0, s>>>(n, 1, A.ptr.p, A.col.p, G.ptr.p, G.col.p, agg.p,
+                                                 toff.p, tlist.p, tcnt.p);
+    CK_LAUNCH();
+    P.nrows = n;
+    P.ncols = naggs;
+    P.ptr.alloc(n + 1, s);
+    P.nnzb = scan_counts(tcnt.p, P.ptr.p, n, s);
+    P.col.alloc(P.nnzb, s);
+    P.val.alloc(9 * P.nnzb, s);
+    k_psm_cols<<<ceil_div(n, 256), 256, 0, s>>>(n, 1, 1, toff.p, tlist.p, tcnt.p, P.ptr.p,
+                                                P.col.p);
+    DevBuf<double> dg(9 * static_cast<int64_t>(n) + 1, s), dinv(9 * static_cast<int64_t>(n) + 1, s);
+    k_bt_diag<<<ceil_div(n, 128), 128, 0, s>>>(n, A.ptr.p, A.col.p, A.val.p, G.ptr.p, G.col.p,
+                                               dg.p, dinv.p, err);
+    CK_LAUNCH();
+    check_dev_error(err, s);
+    k_bt_vals<<<std::max<int64_t>(1, ceil_div(P.nnzb, 128)), 128, 0, s>>>(
+        P.nnzb, n, A.ptr.p, A.col.p, A.val.p, G.ptr.p, G.col.p, agg.p, pv.p, dg.p, dinv.p, omega,
+        P.ptr.p, P.col.p, P.val.p);
     CK_LAUNCH();
 }
 

@@ -88,8 +88,15 @@ CASES = [
     ("beam_hybrid1_bjac", dict(nx=12, ny=4, nz=4, lx=3.0, dirichlet="eliminate",
                                load="traction_xend", x_slowest=True), "block_jacobi", 0.5, 120,
      "ns_hybrid1"),
+    # the block pipeline: no nullspace, block strength / transfer
+    # (hierarchy.hpp:340-347, coarsening.hpp:471-560)
+    ("box975_block_spai0", dict(nx=9, ny=7, nz=5, dirichlet="eliminate", load="traction_xend"),
+     "spai0", 0.72, 150, "block"),
+    ("cube8_keep_block_ilu0", dict(nx=8, dirichlet="keep_rows"), "ilu0", 0.72, 300, "block"),
+    ("cube7_hetero_block_bjac", dict(nx=7, dirichlet="eliminate", heterogeneous=True,
+                                     load="random", seed=7), "block_jacobi", 0.5, 120, "block"),
 ]
-PIPE = {"ns_hybrid1": 3, "ns_hybrid2": 4, "ns_block": 5}
+PIPE = {"block": 1, "ns_hybrid1": 3, "ns_hybrid2": 4, "ns_block": 5}
 
 
 @pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
@@ -99,7 +106,7 @@ def test_setup_and_solve_parity(gpu, ref, orc, case):
     pb = gpu
     p = make_problem(pb, **kw)
     A = p.csr()
-    B = p.nullspace()
+    B = None if pipeline == "block" else p.nullspace()
     prm = pb.AmgParams(smoother=smoother, smoother_omega=omega, coarse_enough=ce)
     h = pb.setup(A, B, pipeline, prm)
     rp = Params(smoother=SM[smoother], smoother_omega=omega, coarse_enough=ce,
@@ -194,7 +201,7 @@ def test_zero_diagonal_rejected(gpu):
 def test_unsupported_pipelines(gpu):
     pb = gpu
     p = make_problem(pb, 3, dirichlet="eliminate")
-    for pl in ("scalar", "block", "ns_scalar"):
+    for pl in ("scalar", "ns_scalar"):
         with pytest.raises(pb.Unsupported):
             pb.setup(p.csr(), p.nullspace(), pl)
     with pytest.raises(pb.Unsupported):  # ilu0<double> is not on the B200 path
