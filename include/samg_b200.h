@@ -53,8 +53,9 @@ enum samg_status {
 /* samg::pipeline (hierarchy.hpp:30).  SAMG_PIPELINE_NS_BLOCK is the B200
  * hot path; NS_HYBRID2 and NS_HYBRID1 (scalar-space Galerkin, block storage,
  * hierarchy.hpp:233-330; NS_HYBRID1 without ILU(0), whose scalar smoother
- * is not on this path) are supported with the same bit-exact parity; SCALAR,
- * BLOCK and NS_SCALAR return SAMG_UNSUPPORTED. */
+ * is not on this path) are supported with the same bit-exact parity, and so
+ * is BLOCK (no nullspace: B may be NULL and is ignored, hierarchy.hpp:340-347);
+ * SCALAR and NS_SCALAR return SAMG_UNSUPPORTED. */
 enum samg_pipeline {
     SAMG_PIPELINE_SCALAR = 0,
     SAMG_PIPELINE_BLOCK = 1,

@@ -201,8 +201,8 @@ class DistHierarchy:
     copies); f and u are then the global vectors."""
 
     def __init__(self, nbrows, ptr, col, val, B, rank, nranks, dist=None, row_starts=None,
-                 min_rows=4096, prm=None, uid=None, emulate=False):
-        from .api import AmgParams, _nullspace
+                 min_rows=4096, prm=None, uid=None, emulate=False, pipeline="ns_block"):
+        from .api import AmgParams, _nullspace, _pipeline
         prm = prm or AmgParams()
         idbuf = None
         if emulate:
@@ -223,8 +223,9 @@ class DistHierarchy:
         h = vp()
         check(lib.samg_dsetup(idbuf, nranks, rank, nbrows, ptr.ctypes.data_as(i64p),
                               col.ctypes.data_as(i64p), val.ctypes.data_as(f64p),
-                              Bv.ctypes.data_as(f64p), brows, k,
-                              rs.ctypes.data_as(i64p) if rs is not None else None, min_rows, 5,
+                              Bv.ctypes.data_as(f64p) if Bv is not None else None, brows, k,
+                              rs.ctypes.data_as(i64p) if rs is not None else None, min_rows,
+                              _pipeline(pipeline),
                               C.byref(pc), C.byref(h)))
         self.h = h
         self.rank, self.nranks = rank, nranks

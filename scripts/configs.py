@@ -39,22 +39,25 @@ CONFIGS = {
 SM = {"spai0": 1, "jacobi": 0, "block_jacobi": 2, "ilu0": 3}
 
 
-def run(name, ref_on, max_it, out, smoother=None):
+PIPE = {"block": 1, "ns_hybrid1": 3, "ns_hybrid2": 4, "ns_block": 5}
+
+
+def run(name, ref_on, max_it, out, smoother=None, pipeline="ns_block"):
     kw, smoothers = CONFIGS[name]
     if smoother:
         smoothers = [(smoother, 0.72)]
     t0 = time.perf_counter()
     p = pb.generate_hex(**kw)
     tgen = time.perf_counter() - t0
-    B = p.nullspace()
+    B = None if pipeline == "block" else p.nullspace()
     for sm, om in smoothers:
-        rec = {"config": name, "smoother": sm, "omega": om, "unknowns": p.n, "nnzb": p.nnzb,
-               "generate_s": tgen}
+        rec = {"config": name, "pipeline": pipeline, "smoother": sm, "omega": om, "unknowns": p.n,
+               "nnzb": p.nnzb, "generate_s": tgen}
         prm = pb.AmgParams(smoother=sm, smoother_omega=om)
-        h = pb.setup_bsr3(p.nbrows, p.ptr, p.col, p.val.reshape(-1), B, "ns_block", prm)
+        h = pb.setup_bsr3(p.nbrows, p.ptr, p.col, p.val.reshape(-1), B, pipeline, prm)
         h.close()  # warm-up (lazy module loading, memory pool)
         t0 = time.perf_counter()
-        h = pb.setup_bsr3(p.nbrows, p.ptr, p.col, p.val.reshape(-1), B, "ns_block", prm)
+        h = pb.setup_bsr3(p.nbrows, p.ptr, p.col, p.val.reshape(-1), B, pipeline, prm)
         rec["gpu_setup_s"] = time.perf_counter() - t0
         rec["levels_block_rows"] = [h.level_info(l)[0] for l in range(h.nlevels)]
         rec["coarse_dim"] = h.coarse_dim
@@ -68,7 +71,8 @@ def run(name, ref_on, max_it, out, smoother=None):
             ref = Ref()
             n, ptr, col, val = p.csr()
             t0 = time.perf_counter()
-            hr = ref.setup(n, ptr, col, val, B, Params(smoother=SM[sm], smoother_omega=om))
+            hr = ref.setup(n, ptr, col, val, B, Params(smoother=SM[sm], smoother_omega=om,
+                                                         pipeline=PIPE[pipeline]))
             rec["ref_setup_s"] = time.perf_counter() - t0
             same = hr.nlevels == h.nlevels
             agg_same = same
@@ -104,9 +108,10 @@ def main():
     ap.add_argument("--max-it", type=int, default=1000)
     ap.add_argument("--out", default=None)
     ap.add_argument("--smoother", default=None, help="override the configs' smoothers (e.g. ilu0)")
+    ap.add_argument("--pipeline", default="ns_block", choices=sorted(PIPE))
     a = ap.parse_args()
     for c in a.configs:
-        run(c, a.ref, a.max_it, a.out, a.smoother)
+        run(c, a.ref, a.max_it, a.out, a.smoother, a.pipeline)
 
 
 if __name__ == "__main__":

@@ -1,0 +1,32 @@
+"""Small end-to-end exercise of every kernel family for compute-sanitizer:
+setup (all phases incl. the cluster GJ panel) + CG with SPAI0 and ILU(0),
+the TMA SpMV (>= 24 chunks per SM: 50^3 elements), the bitmap/hash SpGEMM,
+the batch SpMV, device assembly and the emulated multi-rank solve."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+
+import paper_2202_09056_b200 as pb  # noqa: E402
+from paper_2202_09056_b200.dist import DistHierarchy  # noqa: E402
+
+p = pb.generate_hex(nx=8, ny=8, nz=8, dirichlet="eliminate", noise=0.01, seed=1)
+for sm in ("spai0", "ilu0"):
+    h = pb.setup(p.csr(), p.nullspace(), "ns_block", pb.AmgParams(smoother=sm, coarse_enough=300))
+    u, rep = h.cg_solve(p.rhs)
+    print(sm, rep["iterations"], flush=True)
+    h.close()
+hh = pb.setup(p.csr(), p.nullspace(), "ns_hybrid2", pb.AmgParams(coarse_enough=300))
+print("hybrid2", hh.cg_solve(p.rhs)[1]["iterations"], flush=True)
+q = pb.generate_hex(nx=50, ny=50, nz=50, dirichlet="eliminate")
+M = pb.Bsr3.from_host(q.nbrows, q.nbrows, q.ptr, q.col, q.val.reshape(-1))
+x = np.ones(q.n)
+print("tma spmv", float(M.spmv(x).sum()), flush=True)
+print("batch", float(M.spmv_batch(np.ones((3, q.n))).sum()), flush=True)
+dp = pb.generate_hex_device(nx=6, ny=5, nz=4, dirichlet="eliminate")
+print("device assembly", dp.nnzb, flush=True)
+dh = DistHierarchy(p.nbrows, p.ptr, p.col, p.val.reshape(-1), p.nullspace(), 0, 3,
+                   min_rows=1, prm=pb.AmgParams(coarse_enough=300), emulate=True)
+print("emulated 3 ranks", dh.cg_solve(p.rhs)[1]["iterations"], flush=True)

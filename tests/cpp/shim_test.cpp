@@ -88,6 +88,14 @@ int main() {
     try { std::vector<double> bad(5); cg_solve(H, bad, u, cg_params{}); } catch (const dimension_mismatch &) { thrown = true; }
     EXPECT(thrown);
 
+    // pipeline::block takes no nullspace (hierarchy.hpp:340-347)
+    hierarchy Hb = setup(A, std::nullopt, pipeline::block, prm);
+    EXPECT(Hb.nlevels() >= 2);
+    std::vector<double> ub(n, 0.0);
+    solve_report rb = cg_solve(Hb, rhs, ub, cg_params{});
+    EXPECT(rb.converged && rb.relative_residual <= 1e-8);
+    EXPECT(rb.variant == pipeline::block);
+
     std::printf("%s: levels=%td iterations=%d relres=%.3e\n", failures ? "FAILED" : "ok",
                 H.nlevels(), rep.iterations, rep.relative_residual);
     return failures ? 1 : 0;

@@ -108,18 +108,20 @@ def test_multi_gpu_solver_single_rank(gpu, min_rows):
 
 
 EMU_CASES = [
-    # world, min_rows, (pre, post), smoother, uneven row split
-    (2, 1, (1, 1), "spai0", False),
-    (3, 1, (1, 1), "spai0", True),
-    (4, 8, (2, 2), "spai0", False),
-    (5, 1, (1, 1), "jacobi", True),
-    (2, 1, (1, 1), "block_jacobi", False),
-    (3, 10**7, (1, 1), "spai0", False),
+    # world, min_rows, (pre, post), smoother, uneven row split, pipeline
+    (2, 1, (1, 1), "spai0", False, "ns_block"),
+    (3, 1, (1, 1), "spai0", True, "ns_block"),
+    (4, 8, (2, 2), "spai0", False, "ns_block"),
+    (5, 1, (1, 1), "jacobi", True, "ns_block"),
+    (2, 1, (1, 1), "block_jacobi", False, "ns_block"),
+    (3, 10**7, (1, 1), "spai0", False, "ns_block"),
+    (3, 1, (1, 1), "spai0", True, "ns_hybrid2"),
+    (2, 1, (1, 1), "spai0", False, "block"),
 ]
 
 
-@pytest.mark.parametrize("world,min_rows,sweeps,smoother,uneven", EMU_CASES)
-def test_emulated_multi_gpu_solver(gpu, world, min_rows, sweeps, smoother, uneven):
+@pytest.mark.parametrize("world,min_rows,sweeps,smoother,uneven,pipeline", EMU_CASES)
+def test_emulated_multi_gpu_solver(gpu, world, min_rows, sweeps, smoother, uneven, pipeline):
     """samg_dsetup with id=NULL: all `world` row slices of the partitioned
     hierarchy driven from one process, every NCCL step replaced by device
     copies with the same offsets/counts.  The partitioned PCG must reproduce
@@ -130,15 +132,16 @@ def test_emulated_multi_gpu_solver(gpu, world, min_rows, sweeps, smoother, uneve
     p = pb.generate_hex(nx=16, ny=8, nz=8, dirichlet="eliminate", load="traction_xend")
     prm = pb.AmgParams(coarse_enough=60, smoother=smoother, smoother_omega=0.5,
                        pre_sweeps=sweeps[0], post_sweeps=sweeps[1])
-    h = pb.setup_bsr3(p.nbrows, p.ptr, p.col, p.val.reshape(-1), p.nullspace(), "ns_block", prm)
+    B = None if pipeline == "block" else p.nullspace()
+    h = pb.setup_bsr3(p.nbrows, p.ptr, p.col, p.val.reshape(-1), B, pipeline, prm)
     u1, r1 = h.cg_solve(p.rhs)
     rs = None
     if uneven:
         cuts = np.cumsum([1] + [2 * k + 1 for k in range(world - 1)])
         rs = np.concatenate([[0], np.round(p.nbrows * cuts / cuts[-1] * 0.999).astype(np.int64)])
         rs[-1] = p.nbrows
-    dh = DistHierarchy(p.nbrows, p.ptr, p.col, p.val.reshape(-1), p.nullspace(), 0, world,
-                       row_starts=rs, min_rows=min_rows, prm=prm, emulate=True)
+    dh = DistHierarchy(p.nbrows, p.ptr, p.col, p.val.reshape(-1), B, 0, world,
+                       row_starts=rs, min_rows=min_rows, prm=prm, emulate=True, pipeline=pipeline)
     inf = dh.info()
     assert inf["row0"] == 0 and inf["row1"] == p.nbrows
     if min_rows == 1:
