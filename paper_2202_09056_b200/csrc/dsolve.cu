@@ -456,7 +456,9 @@ DHierarchy *dsetup(std::unique_ptr<Hierarchy> H, ncclComm_t comm, int nranks,
     size_t Ld = 1;  // the fine level is always partitioned
     for (size_t l = 0; l + 1 < L; ++l) {
         const Level &lv = H->levels[l];
-        const int h = l == 0 ? 1 : 2;  // block rows per node (pbs 3 / 6)
+        // block rows per node: 1 on the fine level (pbs 3) and in the block
+        // pipeline, 2 on ns coarse levels (pbs 6)
+        const int64_t h = lv.nnodes ? lv.A.nrows / lv.nnodes : 1;
         const int64_t kb = lv.naggs ? lv.P.ncols / lv.naggs : 2;
         const std::vector<int> seedno = download_int(lv.seedno, lv.nnodes + 1, s);
         std::vector<int64_t> cst(nranks + 1);
