@@ -7,17 +7,17 @@
 //
 // Both the IKJ factorization and the two triangular sweeps are sequential
 // chains in row order.  They run as "sync-free" persistent kernels: warps
-// take work in increasing row order from an atomic counter and wait only
-// for the rows they depend on (one release/acquire flag per row), so the
-// critical path is the dependency depth of the pattern (~nx+ny+nz row hops
-// for a structured mesh in natural order), not n.
-//  * factorization: a warp per row; lanes split the U part of each pivot row
-//    (distinct targets per step), steps in the reference's j order;
-//  * triangular sweeps: a warp per segment of S consecutive rows, processed
-//    in order with the segment's results kept in shared memory, so the
-//    (frequent) dependency on the preceding rows costs no flag round trip;
-//    lanes 0..2 carry the three row components through the exact
-//    subtraction chain; dependencies outside the segment are awaited on flags.
+// take rows in dependency-level order from an atomic counter and wait only
+// for the rows they depend on, so the critical path is the dependency depth
+// of the pattern (~nx+2ny+4nz row hops for a structured mesh in natural
+// order), not n.
+//  * factorization: a warp per row, one release/acquire flag per row; lanes
+//    split the U part of each pivot row (distinct targets per step), steps
+//    in the reference's j order;
+//  * triangular sweeps: a warp per row, the output value is its own flag
+//    (sentinel-filled vector, relaxed polls); lanes 0..2 carry the three row
+//    components through the exact subtraction chain over the ready prefix
+//    of the dependencies (k_ilu_sweep).
 #include <cuda/atomic>
 
 #include <algorithm>
@@ -218,54 +218,137 @@ __global__ void __launch_bounds__(256) k_ilu_factor(int n, const int *__restrict
 // Triangular sweeps (relaxation.hpp:44-88), level-scheduled and sync-free:
 // a warp per row, rows taken from an atomic counter in LEVEL order (forward:
 // the levels of the unit lower factor's dependency DAG, backward: of the
-// upper factor's), each waiting on the flags of its dependencies.  Lanes
-// 0..2 carry the three components through the exact subtraction chain in
-// the reference's (j, q) order:
+// upper factor's).  Lanes 0..2 carry the three components through the exact
+// subtraction chain in the reference's (j, q) order:
 //   forward  y_i = r_i - sum_{j<i} L_ij y_j            (unit lower factor)
-//   backward x_i = U_ii^-1 (y_i - sum_{j>i} U_ij x_j), in place over y,
+//   backward x_i = U_ii^-1 (y_i - sum_{j>i} U_ij x_j),
 //            then u_out = x (zero guess) or u_in + x  (kernels::axpby(1,x,1,u)).
+//
+// The value is its own flag: the output vector is pre-filled with kSent (all
+// bits set, a NaN payload fp arithmetic never returns) and a dependency is
+// complete once its three components are not kSent.  A hand-off therefore
+// costs one relaxed L2 poll -- no release fence on the producer, no flag
+// load + acquire + data load on the consumer (scripts/micro/value_chain.cu:
+// 0.36 us per hop against 0.98 us for flag + fence).  The factor blocks of
+// the row do not depend on other rows and are staged in shared memory before
+// the first poll; every lane polls its own dependencies and, once one is
+// complete, forms its 9 products (independent of the chain) in place; lanes
+// 0..2 then walk the READY PREFIX of the subtraction chain while later
+// dependencies are still pending.  In natural order the latest forward
+// dependency (row i-1) is the last in the chain, so only a few subtractions
+// follow the hand-off; backward, the latest (row i+1) is the first, and the
+// whole chain of 3 dependent subtractions per dependency follows it.
+constexpr unsigned long long kSent = ~0ull;
+constexpr int kWin = 96;  // dependencies staged per window (3 per lane)
+
+__device__ __forceinline__ unsigned long long ld_poll(const double *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_publish(double *p, double x) {
+    unsigned long long v = static_cast<unsigned long long>(__double_as_longlong(x));
+    if (v == kSent) v = 0x7fffffffffffffffull;  // a NaN input carrying the sentinel bits
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 template <bool kFwd, bool kZero>
 __global__ void __launch_bounds__(256) k_ilu_sweep(int n, const int *__restrict__ order,
         const int *__restrict__ ptr, const int *__restrict__ col, const int *__restrict__ dpos,
-        const double *__restrict__ lu, const double *__restrict__ inv, const double *rin,
-        double *y, const double *u_in, double *u_out, int *flags, int *counter) {
-    __shared__ double stage[8][12 * 32];  // per warp: 32 x 3 values + 32 x 9 block entries
+        const double *__restrict__ lu, const double *__restrict__ inv, const double *src,
+        double *out, const double *u_in, double *u_out, unsigned *counter) {
+    extern __shared__ __align__(16) double ssm[];  // per warp: kWin x 9 block entries (then products)
     const int lane = threadIdx.x & 31;
+    double *bs = ssm + static_cast<size_t>(threadIdx.x >> 5) * kWin * 9;
     for (;;) {
-        int t = 0;
-        if (lane == 0) t = atomicAdd(counter, 1);
+        unsigned t = 0;
+        if (lane == 0) t = atomicAdd(counter, 1u) + 1u;  // counter starts at 0xffffffff
         t = __shfl_sync(kFull, t, 0);
-        if (t >= n) return;
+        if (t >= static_cast<unsigned>(n)) return;
         const int i = __ldg(order + t);
-        const int b = kFwd ? ptr[i] : dpos[i] + 1, e = kFwd ? dpos[i] : ptr[i + 1];
-        wait_deps(col, b, e, flags);
-        // the lanes fetch a chunk of up to 32 dependencies (their values and
-        // the lanes' rows of the factor blocks) in parallel into shared
-        // memory -- one L2 round trip per chunk -- then lanes 0..2 walk the
-        // chunk in order
+        const int b = kFwd ? __ldg(ptr + i) : __ldg(dpos + i) + 1, e = kFwd ? __ldg(dpos + i) : __ldg(ptr + i + 1);
         double acc = 0.0;
-        if (lane < 3) acc = __ldcg((kFwd ? rin : y) + 3LL * i + lane);
-        double *xs = stage[threadIdx.x >> 5], *bs = xs + 3 * 32;
-        for (int c = b; c < e; c += 32) {
-            const int j = c + lane, m = min(32, e - c);
-            if (j < e) {
-                const double *g = y + 3LL * col[j];
-                const double *blk = lu + 9LL * j;
-                xs[3 * lane] = __ldcg(g); xs[3 * lane + 1] = __ldcg(g + 1); xs[3 * lane + 2] = __ldcg(g + 2);
+        if (lane < 3) acc = src[3LL * i + lane];
+        for (int w0 = b; w0 < e; w0 += kWin) {
+            const int m = min(kWin, e - w0);
+            for (int q = lane; q < 9 * m; q += 32) bs[q] = __ldg(lu + 9LL * w0 + q);
+            int kk[3];
+            unsigned pend = 0;
 #pragma unroll
-                for (int q = 0; q < 9; ++q) bs[9 * lane + q] = __ldg(blk + q);
+            for (int s = 0; s < 3; ++s) {
+                const int d = lane + 32 * s;
+                kk[s] = 0;
+                if (d < m) { kk[s] = __ldg(col + w0 + d); pend |= 1u << s; }
             }
-            __syncwarp();
-            if (lane < 3)
-                for (int d = 0; d < m; ++d) {
-                    const double *bl = bs + 9 * d + 3 * lane, *v = xs + 3 * d;
-                    acc = __dsub_rn(acc, __dmul_rn(bl[0], v[0]));
-                    acc = __dsub_rn(acc, __dmul_rn(bl[1], v[1]));
-                    acc = __dsub_rn(acc, __dmul_rn(bl[2], v[2]));
+            __syncwarp();  // the staged blocks are multiplied by their dependency's lane
+            int done = 0;
+            for (;;) {
+#pragma unroll
+                for (int s = 0; s < 3; ++s)
+                    if (pend >> s & 1u) {
+                        const double *g = out + 3LL * kk[s];
+                        const unsigned long long v0 = ld_poll(g), v1 = ld_poll(g + 1), v2 = ld_poll(g + 2);
+                        if (v0 != kSent && v1 != kSent && v2 != kSent) {
+                            // the dependency's 9 products, in place over its
+                            // block: only the subtractions stay sequential
+                            double *bl = bs + 9 * (lane + 32 * s);
+                            const double x0 = __longlong_as_double(static_cast<long long>(v0)),
+                                         x1 = __longlong_as_double(static_cast<long long>(v1)),
+                                         x2 = __longlong_as_double(static_cast<long long>(v2));
+#pragma unroll
+                            for (int r = 0; r < 3; ++r) {
+                                bl[3 * r] = __dmul_rn(bl[3 * r], x0);
+                                bl[3 * r + 1] = __dmul_rn(bl[3 * r + 1], x1);
+                                bl[3 * r + 2] = __dmul_rn(bl[3 * r + 2], x2);
+                            }
+                            pend &= ~(1u << s);
+                        }
+                    }
+                __syncwarp();
+                const unsigned r0 = __ballot_sync(kFull, !(pend & 1u)), r1 = __ballot_sync(kFull, !(pend & 2u)),
+                               r2 = __ballot_sync(kFull, !(pend & 4u));
+                int ready = r0 != kFull ? __ffs(~r0) - 1
+                          : r1 != kFull ? 32 + __ffs(~r1) - 1
+                          : r2 != kFull ? 64 + __ffs(~r2) - 1 : kWin;
+                ready = min(ready, m);
+                if (lane < 3) {
+                    // acc = ((acc - B(r,0) x0) - B(r,1) x1) - B(r,2) x2 per
+                    // dependency, in order (relaxation.hpp:60-66); the
+                    // products of the next 4 dependencies are loaded while
+                    // the current 4 are subtracted (the chain is DADD-latency
+                    // bound, shared-memory latency stays off it)
+                    const double *pr = bs + 3 * lane;
+                    int d = done;
+                    double p[12];
+                    auto load4 = [&](int d0, double (&q)[12]) {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int dd = min(d0 + u, kWin - 1);
+                            q[3 * u] = pr[9 * dd]; q[3 * u + 1] = pr[9 * dd + 1]; q[3 * u + 2] = pr[9 * dd + 2];
+                        }
+                    };
+                    if (d + 4 <= ready) load4(d, p);
+                    while (d + 4 <= ready) {
+                        double q[12];
+                        load4(d + 4, q);
+#pragma unroll
+                        for (int u = 0; u < 12; ++u) acc = __dsub_rn(acc, p[u]);
+#pragma unroll
+                        for (int u = 0; u < 12; ++u) p[u] = q[u];
+                        d += 4;
+                    }
+                    for (; d < ready; ++d) {
+                        acc = __dsub_rn(acc, pr[9 * d]);
+                        acc = __dsub_rn(acc, pr[9 * d + 1]);
+                        acc = __dsub_rn(acc, pr[9 * d + 2]);
+                    }
                 }
-            __syncwarp();
+                done = ready;
+                if (done == m) break;
+            }
+            __syncwarp();  // the window's staging is reused
         }
-        double out = acc;
+        double res = acc;
         if constexpr (!kFwd) {
             const double a0 = __shfl_sync(kFull, acc, 0), a1 = __shfl_sync(kFull, acc, 1),
                          a2 = __shfl_sync(kFull, acc, 2);
@@ -275,23 +358,24 @@ __global__ void __launch_bounds__(256) k_ilu_sweep(int n, const int *__restrict_
                 tt = __dadd_rn(tt, __dmul_rn(d[0], a0));
                 tt = __dadd_rn(tt, __dmul_rn(d[1], a1));
                 tt = __dadd_rn(tt, __dmul_rn(d[2], a2));
-                out = tt;
+                res = tt;
             }
         }
         if (lane < 3) {
-            y[3LL * i + lane] = out;
+            st_publish(out + 3LL * i + lane, res);
             if constexpr (!kFwd)
-                u_out[3LL * i + lane] = kZero ? out : __dadd_rn(out, u_in[3LL * i + lane]);
+                u_out[3LL * i + lane] = kZero ? res : __dadd_rn(res, u_in[3LL * i + lane]);
         }
         __syncwarp();
-        if (lane == 0) st_release(flags + static_cast<int64_t>(i) * kFS, 1);
     }
 }
 
-// Persistent grid: at most SAMG_ILU_CTAS_PER_SM (default 2) CTAs of 8 warps
+constexpr int kSweepSmem = 8 * kWin * 9 * static_cast<int>(sizeof(double));
+
+// Persistent grid: at most SAMG_ILU_CTAS_PER_SM (default 1; the sweeps: 2) CTAs of 8 warps
 // per SM -- the wavefront of a structured mesh offers a few hundred to a
 // few thousand independent rows, more warps would only wait.
-int persistent_grid(const void *kern, int64_t work_warps) {
+int persistent_grid(const void *kern, int64_t work_warps, int smem = 0, int per_sm_cap = 0) {
     static int sms = [] {
         int dev = 0, v = 148;
         cudaGetDevice(&dev);
@@ -303,9 +387,9 @@ int persistent_grid(const void *kern, int64_t work_warps) {
         return e ? std::max(1, std::atoi(e)) : 1;
     }();
     int occ = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
     const int64_t want = (work_warps + 7) / 8;
-    const int64_t cap = static_cast<int64_t>(std::min(std::max(occ, 1), per_sm)) * sms;
+    const int64_t cap = static_cast<int64_t>(std::min(std::max(occ, 1), per_sm_cap ? per_sm_cap : per_sm)) * sms;
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, cap)));
 }
 
@@ -313,7 +397,8 @@ int persistent_grid(const void *kern, int64_t work_warps) {
 // levels < l), from one host pass over the pattern: forward = unit lower
 // factor (row i waits for col < i), backward = upper factor (col > i).
 // Within a level rows keep ascending (forward) / descending (backward) order.
-void level_orders(const Bsr3 &A, const DevBuf<int> &dpos, DevBuf<int> &order, cudaStream_t s) {
+void level_orders(const Bsr3 &A, const DevBuf<int> &dpos, DevBuf<int> &order, int (&depth)[2],
+                  cudaStream_t s) {
     const int n = static_cast<int>(A.nrows);
     std::vector<int> ptr(n + 1), col(A.nnzb), dp(n);
     CK(cudaMemcpyAsync(ptr.data(), A.ptr.p, sizeof(int) * (n + 1), cudaMemcpyDeviceToHost, s));
@@ -321,9 +406,10 @@ void level_orders(const Bsr3 &A, const DevBuf<int> &dpos, DevBuf<int> &order, cu
     CK(cudaMemcpyAsync(dp.data(), dpos.p, sizeof(int) * n, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     std::vector<int> lev(n), ord(2 * static_cast<size_t>(n)), cnt;
-    auto bucket = [&](int *out, bool ascending) {
+    auto bucket = [&](int *out, bool ascending, int &nlev) {
         int maxl = 0;
         for (int i = 0; i < n; ++i) maxl = std::max(maxl, lev[i]);
+        nlev = maxl + 1;
         cnt.assign(maxl + 2, 0);
         for (int i = 0; i < n; ++i) ++cnt[lev[i] + 1];
         for (int l = 0; l <= maxl; ++l) cnt[l + 1] += cnt[l];
@@ -337,13 +423,13 @@ void level_orders(const Bsr3 &A, const DevBuf<int> &dpos, DevBuf<int> &order, cu
         for (int j = ptr[i]; j < dp[i]; ++j) l = std::max(l, lev[col[j]] + 1);
         lev[i] = l;
     }
-    bucket(ord.data(), true);
+    bucket(ord.data(), true, depth[0]);
     for (int i = n - 1; i >= 0; --i) {
         int l = 0;
         for (int j = dp[i] + 1; j < ptr[i + 1]; ++j) l = std::max(l, lev[col[j]] + 1);
         lev[i] = l;
     }
-    bucket(ord.data() + n, false);
+    bucket(ord.data() + n, false, depth[1]);
     order.alloc(2 * static_cast<size_t>(n), s);
     CK(cudaMemcpyAsync(order.p, ord.data(), sizeof(int) * 2 * n, cudaMemcpyHostToDevice, s));
     CK(cudaStreamSynchronize(s));  // host vectors go out of scope
@@ -363,14 +449,15 @@ void setup_ilu0(const Bsr3 &A, Smoother &M, DevError *err, cudaStream_t s) {
     M.lu.alloc(9 * A.nnzb + 1, s);
     M.tmp.alloc(3 * A.nrows + 3, s);
     M.dpos.alloc(A.nrows + 1, s);
-    M.flags.alloc(2 * A.nrows * kFS + 2, s);
+    M.flags.alloc(A.nrows * kFS + 2, s);
+    M.sweep.alloc(6 * A.nrows + 1, s);
     if (n == 0) return;
     k_ilu_dpos<<<ceil_div(n, 256), 256, 0, s>>>(n, A.ptr.p, A.col.p, M.dpos.p, err);
     CK_LAUNCH();
     check_dev_error(err, s);  // no factorization without every diagonal
-    level_orders(A, M.dpos, M.order, s);
+    level_orders(A, M.dpos, M.order, M.depth, s);
     CK(cudaMemcpyAsync(M.lu.p, A.val.p, sizeof(double) * 9 * A.nnzb, cudaMemcpyDeviceToDevice, s));
-    CK(cudaMemsetAsync(M.flags.p, 0, sizeof(int) * (2 * A.nrows * kFS + 2), s));
+    CK(cudaMemsetAsync(M.flags.p, 0, sizeof(int) * (A.nrows * kFS + 2), s));
     constexpr int fsmem = 8 * kFMax * (9 * static_cast<int>(sizeof(double)) + static_cast<int>(sizeof(int)));
     static const bool fattr = [] {
         CK(cudaFuncSetAttribute(k_ilu_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem));
@@ -379,7 +466,7 @@ void setup_ilu0(const Bsr3 &A, Smoother &M, DevError *err, cudaStream_t s) {
     (void)fattr;
     k_ilu_factor<<<persistent_grid(reinterpret_cast<const void *>(k_ilu_factor), n), 256, fsmem, s>>>(
         n, M.order.p, A.ptr.p, A.col.p, M.dpos.p, M.lu.p, M.data.p, M.flags.p,
-        M.flags.p + 2 * static_cast<int64_t>(n) * kFS, err);
+        M.flags.p + static_cast<int64_t>(n) * kFS, err);
     CK_LAUNCH();
 }
 
@@ -387,25 +474,46 @@ void launch_ilu_smooth(const Bsr3 *A, const Smoother &M, const double *f, const 
                        double *u_out, cudaStream_t s) {
     const int n = static_cast<int>(M.nrows);
     if (n == 0) return;
-    const int64_t nf = static_cast<int64_t>(n) * kFS;
-    int *fw = M.flags.p, *bw = M.flags.p + nf, *cnt = M.flags.p + 2 * nf;
-    CK(cudaMemsetAsync(M.flags.p, 0, sizeof(int) * (2 * nf + 2), s));
+    // [y | x | two row counters]: sentinel-filled by one memset (the counters
+    // start at 0xffffffff, see k_ilu_sweep)
+    double *y = M.sweep.p, *x = M.sweep.p + 3LL * n;
+    unsigned *cnt = reinterpret_cast<unsigned *>(M.sweep.p + 6LL * n);
+    CK(cudaMemsetAsync(M.sweep.p, 0xff, sizeof(double) * (6LL * n + 1), s));
     const double *rin = f;
     if (u_in) {
         launch_residual(*A, f, u_in, M.tmp.p, s);  // r = f - A u (hierarchy.hpp:213-215)
         rin = M.tmp.p;
     }
-    static const int gf = persistent_grid(reinterpret_cast<const void *>(k_ilu_sweep<true, true>), 1 << 30);
-    const int grid = std::min(gf, (n + 7) / 8);
+    static const int gf = [] {
+        for (const void *k : {reinterpret_cast<const void *>(k_ilu_sweep<true, true>),
+                               reinterpret_cast<const void *>(k_ilu_sweep<false, false>),
+                               reinterpret_cast<const void *>(k_ilu_sweep<false, true>)})
+            CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSweepSmem));
+        const char *e = std::getenv("SAMG_ILU_CTAS_PER_SM");
+        return persistent_grid(reinterpret_cast<const void *>(k_ilu_sweep<true, true>), 1 << 30, kSweepSmem,
+                               e ? 0 : 2);
+    }();
+    // warps for about kAhead dependency levels: a warp spins on the rows it
+    // waits for, and warps far ahead of the wavefront only load L2 (coarse
+    // levels have a few rows per level)
+    static const int ahead = [] {
+        const char *e = std::getenv("SAMG_ILU_AHEAD");
+        return e ? std::max(1, std::atoi(e)) : 16;
+    }();
+    auto grid_for = [&](int depth) {
+        const int64_t warps = (static_cast<int64_t>(ahead) * n + depth - 1) / std::max(depth, 1);
+        return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(gf, (std::min<int64_t>(warps, n) + 7) / 8)));
+    };
+    const int gridf = grid_for(M.depth[0]), gridb = grid_for(M.depth[1]);
     const int *of = M.order.p, *ob = M.order.p + n;
-    k_ilu_sweep<true, true><<<grid, 256, 0, s>>>(n, of, M.ptr, M.col, M.dpos.p, M.lu.p, M.data.p, rin,
-                                                 M.tmp.p, nullptr, nullptr, fw, cnt);
+    k_ilu_sweep<true, true><<<gridf, 256, kSweepSmem, s>>>(n, of, M.ptr, M.col, M.dpos.p, M.lu.p, M.data.p,
+                                                          rin, y, nullptr, nullptr, cnt);
     if (u_in)
-        k_ilu_sweep<false, false><<<grid, 256, 0, s>>>(n, ob, M.ptr, M.col, M.dpos.p, M.lu.p, M.data.p,
-                                                       nullptr, M.tmp.p, u_in, u_out, bw, cnt + 1);
+        k_ilu_sweep<false, false><<<gridb, 256, kSweepSmem, s>>>(n, ob, M.ptr, M.col, M.dpos.p, M.lu.p,
+                                                                M.data.p, y, x, u_in, u_out, cnt + 1);
     else
-        k_ilu_sweep<false, true><<<grid, 256, 0, s>>>(n, ob, M.ptr, M.col, M.dpos.p, M.lu.p, M.data.p,
-                                                      nullptr, M.tmp.p, nullptr, u_out, bw, cnt + 1);
+        k_ilu_sweep<false, true><<<gridb, 256, kSweepSmem, s>>>(n, ob, M.ptr, M.col, M.dpos.p, M.lu.p,
+                                                               M.data.p, y, x, nullptr, u_out, cnt + 1);
     CK_LAUNCH();
 }
 

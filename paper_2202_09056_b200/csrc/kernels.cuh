@@ -36,8 +36,10 @@ struct Smoother {
     DevBuf<double> data;
     // ILU(0) only
     DevBuf<double> lu, tmp;      // factors; scratch vector (3 per block row)
-    DevBuf<int> dpos, flags;     // diagonal position per row; solve flags
+    DevBuf<double> sweep;        // sweep outputs y, x (3 per block row each) + row counters
+    DevBuf<int> dpos, flags;     // diagonal position per row; factorization flags
     DevBuf<int> order;           // rows in level order: forward (n), backward (n)
+    int depth[2] = {1, 1};       // number of forward / backward dependency levels
     const int *ptr = nullptr, *col = nullptr;  // A's pattern
     int64_t nrows = 0, nnzb = 0;
 };
