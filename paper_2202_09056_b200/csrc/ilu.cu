@@ -45,32 +45,6 @@ __device__ __forceinline__ void st_release(int *p, int v) {
     a.store(v, cuda::memory_order_release);
 }
 
-// Wait until every dependency k = col[j], j in [b, e) (all of them finish
-// earlier in the level order) has its flag set.  The lanes test all of them
-// at once; while some are pending a single lane spins on one pending flag
-// (one load in flight per waiting warp), then the warp re-tests.  Ends with
-// an acquire fence.  (Measured on a 27-point 64^3 sweep: 7.7 us per level,
-// against 10.3 us for a one-lane sequential scan, scripts/micro/ilu_trace.cu.)
-__device__ __forceinline__ void wait_deps(const int *col, int b, int e, int *flags) {
-    const int lane = threadIdx.x & 31;
-    for (;;) {
-        int pend = -1;
-        for (int j = b + lane; j < e; j += 32) {
-            const int k = col[j];
-            if (ld_relaxed(flags + static_cast<int64_t>(k) * kFS) == 0) { pend = k; break; }
-        }
-        const unsigned m = __ballot_sync(kFull, pend >= 0);
-        if (!m) break;
-        const int k = __shfl_sync(kFull, pend, __ffs(m) - 1);
-        if (lane == 0)
-            while (ld_relaxed(flags + static_cast<int64_t>(k) * kFS) == 0) {
-            }
-        __syncwarp();
-    }
-    cuda::atomic_thread_fence(cuda::memory_order_acquire, cuda::thread_scope_device);
-    __syncwarp();
-}
-
 __device__ void raise_err(DevError *err, int code, int64_t where) {
     if (atomicCAS(&err->code, 0, code) == 0) err->where = where;
 }
@@ -111,10 +85,30 @@ __global__ void __launch_bounds__(256) k_ilu_factor(int n, const int *__restrict
             for (int q = lane; q < len; q += 32) scol[q] = col[b + q];
             for (int q = lane; q < 9 * len; q += 32) srow[q] = lu[9LL * b + q];
         }
-        wait_deps(col, b, di, done);
+        // Steps run as soon as THEIR pivot row is final, in the reference's
+        // j order: [b, rdy) are known complete (flags seen, then an acquire
+        // fence).  In natural order the latest dependency (k = i-1) is the
+        // last step, so all but the last step overlap the rows before.
+        int rdy = b;
+        auto advance = [&](int j) {  // make dependency j complete, extend rdy
+            for (;;) {
+                const int c = j + lane;
+                const bool ok = c >= di || ld_relaxed(done + static_cast<int64_t>(rc[c]) * kFS) != 0;
+                const unsigned nr = __ballot_sync(kFull, !ok);
+                const int pre = nr ? __ffs(nr) - 1 : 32;
+                if (pre > 0) { rdy = min(di, j + pre); break; }
+                if (lane == 0)
+                    while (ld_relaxed(done + static_cast<int64_t>(rc[j]) * kFS) == 0) {
+                    }
+                __syncwarp();
+            }
+            cuda::atomic_thread_fence(cuda::memory_order_acquire, cuda::thread_scope_device);
+            __syncwarp();
+        };
+        if (in_smem) __syncwarp();  // scol staged
         // operands of step j+1 (inverted pivot of row k, first 32 blocks of
-        // its U part) are requested while step j runs: every row k < i is
-        // final once the dependencies are met
+        // its U part) are requested while step j runs when row k is known
+        // final
         auto load_step = [&](int j, double (&dv)[3], int &c0, double (&u0v)[9], int &uend) {
             const int k = rc[j];
             if (lane < 9) {
@@ -134,12 +128,16 @@ __global__ void __launch_bounds__(256) k_ilu_factor(int n, const int *__restrict
         };
         double dv[3] = {0, 0, 0}, u0v[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
         int c0 = -1, uend = 0;
-        if (b < di) load_step(b, dv, c0, u0v, uend);
+        if (b < di) {
+            advance(b);
+            load_step(b, dv, c0, u0v, uend);
+        }
         for (int j = b; j < di; ++j) {
             const int k = rc[j];
             double ndv[3] = {0, 0, 0}, nu0v[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
             int nc0 = -1, nuend = 0;
-            if (j + 1 < di) load_step(j + 1, ndv, nc0, nu0v, nuend);
+            const bool pre = j + 1 < rdy;
+            if (pre) load_step(j + 1, ndv, nc0, nu0v, nuend);
             // L_ik = A_ik * U_kk^-1 (operator*, static_block.hpp:68-76)
             double le = 0.0;
             if (lane < 9) {
@@ -189,6 +187,10 @@ __global__ void __launch_bounds__(256) k_ilu_factor(int n, const int *__restrict
                     }
             }
             __syncwarp();
+            if (j + 1 < di && !pre) {
+                advance(j + 1);
+                load_step(j + 1, ndv, nc0, nu0v, nuend);
+            }
 #pragma unroll
             for (int q = 0; q < 3; ++q) dv[q] = ndv[q];
 #pragma unroll
