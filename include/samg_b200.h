@@ -67,13 +67,26 @@ enum samg_pipeline {
 
 /* Smoothers.  JACOBI = the reference's point damped_jacobi
  * (relaxation.hpp:141-180, omega default 0.72).  SPAI0 and BLOCK_JACOBI are
- * 3x3 block smoothers.  ILU0 (relaxation.hpp:20-139)
- * is not on this path yet: SAMG_UNSUPPORTED. */
+ * 3x3 block smoothers.  ILU0 = the reference's default
+ * ilu0<block3> (relaxation.hpp:20-139), bit-identical factors and sweeps
+ * (single GPU; the partitioned solver returns SAMG_UNSUPPORTED). */
 enum samg_smoother {
     SAMG_SMOOTHER_JACOBI = 0,
     SAMG_SMOOTHER_SPAI0 = 1,
     SAMG_SMOOTHER_BLOCK_JACOBI = 2,
     SAMG_SMOOTHER_ILU0 = 3
+};
+
+/* Storage precision of the operators the V-cycle streams (an extension: the
+ * reference is fp64 throughout).  FP64 (default) reproduces the reference.
+ * MIXED keeps fp32 copies of A_l, P_l, R_l for the V-cycle's sweeps,
+ * residuals and transfers (vectors, arithmetic, smoother data, the coarse
+ * inverse and CG itself stay fp64; CG's A p and the exit residual read the
+ * fp64 matrix): about half the bytes per V-cycle, a preconditioner that
+ * differs from the fp64 one at fp32 rounding level. */
+enum samg_precision {
+    SAMG_PRECISION_FP64 = 0,
+    SAMG_PRECISION_MIXED = 1
 };
 
 /* amg_params (hierarchy.hpp:50-58) + coarsening_params (coarsening.hpp:26-31)
@@ -90,6 +103,7 @@ typedef struct {
     double stagnation_ratio;  /* 0.8 */
     int verify_galerkin;      /* reserved (hierarchy.hpp:382-402) */
     int device;               /* CUDA device ordinal, default 0 */
+    int vcycle_precision;     /* samg_precision, default FP64 */
 } samg_amg_params;
 
 /* cg_params (cg.hpp:32-35) */
@@ -153,6 +167,10 @@ SAMG_API int samg_memory_footprint(const samg_hierarchy *h, uint64_t *bytes);
 SAMG_API int samg_finest_dim(const samg_hierarchy *h, int64_t *n);
 SAMG_API int samg_num_levels(const samg_hierarchy *h, int *nlevels);
 SAMG_API int samg_coarse_dim(const samg_hierarchy *h, int64_t *n);
+/* coarse solve in use: 0 = explicit inverse (GEMV), 1 = the reference's
+ * dense LU, bit-exact (chosen when the inverse fails its accuracy check,
+ * i.e. for a numerically singular coarse operator) */
+SAMG_API int samg_coarse_solver(const samg_hierarchy *h, int *kind);
 SAMG_API int samg_setup_seconds(const samg_hierarchy *h, double *seconds);
 /* which: 0 = A, 1 = P, 2 = R of `level`; sizes in 3x3 blocks */
 SAMG_API int samg_level_info(const samg_hierarchy *h, int level, int which,

@@ -123,6 +123,7 @@ struct amg_params {
     double stagnation_ratio = 0.8;
     bool verify_galerkin = false;
     int device = 0;
+    bool mixed_precision_vcycle = false;  // extension: fp32 operator copies (samg_precision)
 };
 
 struct cg_params {
@@ -210,6 +211,7 @@ inline samg_amg_params to_c(const amg_params &p) {
     c.stagnation_ratio = p.stagnation_ratio;
     c.verify_galerkin = p.verify_galerkin ? 1 : 0;
     c.device = p.device;
+    c.vcycle_precision = p.mixed_precision_vcycle ? SAMG_PRECISION_MIXED : SAMG_PRECISION_FP64;
     return c;
 }
 } // namespace detail

@@ -53,7 +53,7 @@ class AmgParamsC(C.Structure):
                 ("smoother_omega", C.c_double), ("pre_sweeps", C.c_int),
                 ("post_sweeps", C.c_int), ("coarse_enough", C.c_int64),
                 ("stagnation_ratio", C.c_double), ("verify_galerkin", C.c_int),
-                ("device", C.c_int)]
+                ("device", C.c_int), ("vcycle_precision", C.c_int)]
 
 
 class CgParamsC(C.Structure):
@@ -96,6 +96,7 @@ PROTOTYPES = {
     "samg_finest_dim": ([vp, i64p], C.c_int),
     "samg_num_levels": ([vp, C.POINTER(C.c_int)], C.c_int),
     "samg_coarse_dim": ([vp, i64p], C.c_int),
+    "samg_coarse_solver": ([vp, C.POINTER(C.c_int)], C.c_int),
     "samg_setup_seconds": ([vp, f64p], C.c_int),
     "samg_level_info": ([vp, C.c_int, C.c_int, i64p, i64p, i64p], C.c_int),
     "samg_get_level": ([vp, C.c_int, C.c_int, i64p, i64p, f64p], C.c_int),

@@ -16,6 +16,7 @@ from ._lib import (AmgParamsC, CgParamsC, ProblemParamsC, ReportC, check, f64p, 
 PIPELINES = {"scalar": 0, "block": 1, "ns_scalar": 2, "ns_hybrid1": 3, "ns_hybrid2": 4,
              "ns_block": 5}
 SMOOTHERS = {"jacobi": 0, "spai0": 1, "block_jacobi": 2, "ilu0": 3}
+PRECISIONS = {"fp64": 0, "mixed": 1}
 
 
 def _i64(a):
@@ -48,13 +49,15 @@ class AmgParams:
     coarse_enough: int = 3000
     stagnation_ratio: float = 0.8
     device: int = 0
+    # "fp64" (the reference) or "mixed": fp32 operator copies for the V-cycle
+    vcycle_precision: str = "fp64"
 
     def c(self) -> AmgParamsC:
         return AmgParamsC(self.eps_strong, self.omega, self.point_block_size,
                           SMOOTHERS[self.smoother] if isinstance(self.smoother, str)
                           else int(self.smoother), self.smoother_omega, self.pre_sweeps,
                           self.post_sweeps, self.coarse_enough, self.stagnation_ratio, 0,
-                          self.device)
+                          self.device, PRECISIONS[self.vcycle_precision])
 
 
 @dataclass
@@ -180,6 +183,14 @@ class Hierarchy:
         n = C.c_int64()
         check(lib.samg_coarse_dim(self.h, C.byref(n)))
         return n.value
+
+    @property
+    def coarse_solver(self) -> str:
+        """"inverse" (GEMV with the explicit inverse) or "lu" (the reference's
+        dense LU, bit-exact; numerically singular coarse operators)."""
+        k = C.c_int()
+        check(lib.samg_coarse_solver(self.h, C.byref(k)))
+        return "lu" if k.value == 1 else "inverse"
 
     @property
     def setup_seconds(self) -> float:

@@ -140,6 +140,8 @@ void validate_params(const samg_amg_params *prm, int pipeline) {
     require(prm->smoother >= 0 && prm->smoother <= 3, SAMG_INVALID_ARGUMENT, "setup: unknown smoother");
     require(prm->pre_sweeps >= 0 && prm->post_sweeps >= 0, SAMG_INVALID_ARGUMENT,
             "setup: negative sweep count");
+    require(prm->vcycle_precision == SAMG_PRECISION_FP64 || prm->vcycle_precision == SAMG_PRECISION_MIXED,
+            SAMG_INVALID_ARGUMENT, "setup: unknown vcycle_precision");
 }
 
 // hierarchy.hpp:267-282 + coarsening.hpp:269-270 checks
@@ -269,6 +271,7 @@ SAMG_API void samg_default_amg_params(samg_amg_params *p) {
     p->stagnation_ratio = 0.8;
     p->verify_galerkin = 0;
     p->device = 0;
+    p->vcycle_precision = SAMG_PRECISION_FP64;
 }
 
 SAMG_API void samg_default_cg_params(samg_cg_params *p) {
@@ -525,6 +528,9 @@ SAMG_API int samg_num_levels(const samg_hierarchy *h, int *nl) {
 }
 SAMG_API int samg_coarse_dim(const samg_hierarchy *h, int64_t *n) {
     return guarded([&] { *n = Hc(h).nc; });
+}
+SAMG_API int samg_coarse_solver(const samg_hierarchy *h, int *kind) {
+    return guarded([&] { *kind = Hc(h).coarse_lu ? 1 : 0; });
 }
 SAMG_API int samg_setup_seconds(const samg_hierarchy *h, double *sec) {
     return guarded([&] { *sec = Hc(h).setup_seconds; });
@@ -877,6 +883,8 @@ SAMG_API int samg_dsetup(const unsigned char id[128], int nranks, int rank, int6
         *out = nullptr;
         validate_params(prm, pipeline);
         validate_ns(3 * nbrows, B, b_rows, b_cols, pipeline);
+        if (prm->vcycle_precision != SAMG_PRECISION_FP64)
+            fail(SAMG_UNSUPPORTED, "dsetup: the mixed-precision V-cycle is single-GPU only");
         need_device(prm->device);
         cudaStream_t s = new_stream();
         try {

@@ -543,12 +543,37 @@ __global__ void __launch_bounds__(kTThreads, 2) k_trailing(int64_t n, int64_t ld
     }
 }
 
-__global__ void k_gather_cols(int64_t n, int64_t ld, const int64_t *perm, const double *X,
-                              double *Ainv) {
+// Exact (power-of-two) symmetric equilibration: s_i = 2^-floor(e_i/2) with
+// |a_ii| = m 2^e_i, so S A S has diagonal entries in [1/2, 2) up to the
+// pivot structure, and no entry is rounded.  A coarse operator of a
+// badly scaled hierarchy (e.g. a heterogeneous cantilever whose rank-
+// deficient aggregates leave diagonal entries near 1e28 next to O(0.1)) has
+// cond(A) ~ 1e30 while cond(SAS) is modest; the reference's dense LU solve
+// is backward stable there, an explicit inverse of the unscaled A is not.
+// A^-1 = S (S A S)^-1 S (k_gather_cols).
+__global__ void k_equilibrate(int64_t n, int64_t ld, double *X, double *sc) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const double d = fabs(X[i * ld + i]);
+    int e = 0;
+    if (d > 0.0 && isfinite(d)) frexp(d, &e);
+    sc[i] = ldexp(1.0, -(e / 2));
+}
+
+__global__ void k_scale_sym(int64_t n, int64_t ld, const double *__restrict__ sc, double *X) {
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n * ld;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t i = e / ld, j = e - i * ld;
-        Ainv[e] = j < n ? X[i * ld + perm[j]] : 0.0;
+        if (j < n) X[e] *= sc[i] * sc[j];
+    }
+}
+
+__global__ void k_gather_cols(int64_t n, int64_t ld, const int64_t *perm, const double *X,
+                              const double *__restrict__ sc, double *Ainv) {
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n * ld;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = e / ld, j = e - i * ld;
+        Ainv[e] = j < n ? X[i * ld + perm[j]] * (sc[i] * sc[j]) : 0.0;
     }
 }
 
@@ -655,6 +680,9 @@ void dense_inverse(const Bsr3 &A, DevBuf<double> &Ainv, DevError *err, cudaStrea
     CK(cudaMemsetAsync(X.p, 0, X.bytes(), s));
     k_scatter<<<ceil_div(A.nrows, 128), 128, 0, s>>>(static_cast<int>(A.nrows), A.ptr.p, A.col.p,
                                                     A.val.p, ld, X.p);
+    DevBuf<double> sc(n, s);
+    k_equilibrate<<<ceil_div(n, 256), 256, 0, s>>>(n, ld, X.p, sc.p);
+    k_scale_sym<<<grid_for(n * ld), 256, 0, s>>>(n, ld, sc.p, X.p);
     CK_LAUNCH();
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(pp.C);
@@ -705,7 +733,7 @@ void dense_inverse(const Bsr3 &A, DevBuf<double> &Ainv, DevError *err, cudaStrea
         std::swap(hperm[k], hperm[p]);
     }
     CK(cudaMemcpyAsync(perm.p, hperm.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
-    k_gather_cols<<<grid_for(n * ld), 256, 0, s>>>(n, ld, perm.p, X.p, Ainv.p);
+    k_gather_cols<<<grid_for(n * ld), 256, 0, s>>>(n, ld, perm.p, X.p, sc.p, Ainv.p);
     CK_LAUNCH();
     check_dev_error(err, s);
 }

@@ -9,6 +9,8 @@
 #include <cstddef>
 #include <cstdlib>
 #include <memory>
+#include <string>
+#include <vector>
 #include <utility>
 
 namespace samgb {
@@ -37,10 +39,13 @@ uint64_t matrix_bytes(const Bsr3 &A) {
 
 } // namespace
 
+void choose_coarse_solver(Hierarchy &H, DevError *err, cudaStream_t s);
+
 Hierarchy::~Hierarchy() {
     if (stream) cudaStreamSynchronize(stream);
     levels.clear();
     Ainv.release();
+    lu.X.release(); lu.Lt.release(); lu.perm.release();
     r.release(); z.release(); p.release(); q.release();
     fbuf.release(); ubuf.release(); partials.release(); sc.release(); err.release();
     pinned_small_free(sc_host);
@@ -206,9 +211,22 @@ Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int6
         setup_smoother(H->levels[i].A, prm.smoother, prm.smoother_omega, H->levels[i].M, err, s);
     check_dev_error(err, s);
     mark("smoothers", L - 1);
+    if (prm.vcycle_precision == SAMG_PRECISION_MIXED) {
+        // fp32 value copies of every operator the V-cycle streams (A_l, P_l,
+        // R_l above the coarsest level); CG's q = A p and the true residual
+        // keep reading the fp64 values
+        for (size_t i = 0; i + 1 < L; ++i) {
+            make_lowp(H->levels[i].A, s);
+            make_lowp(H->levels[i].P, s);
+            make_lowp(H->levels[i].R, s);
+        }
+        mark("fp32_copies", L - 1);
+    }
     H->nc = 3 * H->levels.back().A.nrows;
     dense_inverse(H->levels.back().A, H->Ainv, err, s);
     mark("dense_inv", L - 1);
+    choose_coarse_solver(*H, err, s);
+    mark("coarse_check", L - 1);
     // V-cycle / CG workspace
     for (size_t i = 0; i < L; ++i) {
         Level &lv = H->levels[i];
@@ -232,6 +250,53 @@ Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int6
     return H.release();
 }
 
+// The explicit inverse is checked once: x random, b = A_c x (the sparse
+// coarse operator), e = |Ainv b - x| / |x|.  A well-conditioned coarse
+// operator gives e ~ cond * 1e-16; e > 1e-6 means A_c is numerically singular
+// and its solve is decided by rounding -- then (n <= kLuMaxN) the coarse
+// solve switches to the reference's own LU, bit-exact (coarse_lu.cu).
+// SAMG_COARSE_SOLVER=inverse|lu forces either.
+void choose_coarse_solver(Hierarchy &H, DevError *err, cudaStream_t s) {
+    static const int forced = [] {
+        const char *e = std::getenv("SAMG_COARSE_SOLVER");
+        if (!e) return 0;
+        return std::string(e) == "lu" ? 2 : (std::string(e) == "inverse" ? 1 : 0);
+    }();
+    const Bsr3 &Ac = H.levels.back().A;
+    const int64_t n = H.nc;
+    bool use_lu = forced == 2;
+    if (forced == 0 && n > 0 && n <= kLuMaxN) {
+        std::vector<double> hx(n);
+        uint64_t st = 0x9e3779b97f4a7c15ull;
+        for (auto &v : hx) {  // xorshift, uniform in [-1, 1)
+            st ^= st << 13; st ^= st >> 7; st ^= st << 17;
+            v = static_cast<double>(st >> 11) * 0x1.0p-52 - 1.0;
+        }
+        DevBuf<double> x(n, s), b(n, s), y(n, s);
+        CK(cudaMemcpyAsync(x.p, hx.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s));
+        launch_spmv(Ac, 1.0, x.p, 0.0, b.p, s);
+        launch_dense_gemv(n, H.Ainv.p, b.p, y.p, s);
+        std::vector<double> hy(n);
+        CK(cudaMemcpyAsync(hy.data(), y.p, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        double num = 0.0, den = 0.0;
+        for (int64_t i = 0; i < n; ++i) {
+            num += (hy[i] - hx[i]) * (hy[i] - hx[i]);
+            den += hx[i] * hx[i];
+        }
+        use_lu = !(std::sqrt(num / den) <= 1e-6);
+    }
+    if (!use_lu || n > kLuMaxN) return;
+    dense_lu_ref(Ac, H.lu, err, s);
+    H.coarse_lu = true;
+    H.Ainv.release();
+}
+
+void Hierarchy::coarse_solve(const double *f, double *u) {
+    if (coarse_lu) launch_lu_solve(lu, f, u, stream);
+    else launch_dense_gemv(nc, Ainv.p, f, u, stream);
+}
+
 // V-cycle (hierarchy.hpp:408-441).  With zero_guess the pre-smoother's first
 // sweep needs no SpMV (r = f - A*0 = f exactly), as inside CG (cg.hpp:98-101)
 // and on every level > 0 (hierarchy.hpp:426).
@@ -247,8 +312,9 @@ bool Hierarchy::vcycle_from(size_t start, const double *f0, double *u0, bool zer
                             bool fuse_rz) {
     cudaStream_t s = stream;
     const size_t L = levels.size();
+    const bool lowp = prm.vcycle_precision == SAMG_PRECISION_MIXED;
     if (start + 1 >= L) {
-        launch_dense_gemv(nc, Ainv.p, f0, u0, s);
+        coarse_solve(f0, u0);
         return false;
     }
     bool fused = false;
@@ -269,29 +335,29 @@ bool Hierarchy::vcycle_from(size_t start, const double *f0, double *u0, bool zer
             }
         }
         for (; sweeps > 0; --sweeps) {
-            launch_smooth(lv.A, lv.M, fi, a, b, s);
+            launch_smooth(lv.A, lv.M, fi, a, b, s, lowp);
             std::swap(a, b);
         }
-        launch_residual(lv.A, fi, a, lv.r.p, s);
-        launch_spmv(lv.R, 1.0, lv.r.p, 0.0, levels[i + 1].f.p, s);
+        launch_residual(lv.A, fi, a, lv.r.p, s, lowp);
+        launch_spmv(lv.R, 1.0, lv.r.p, 0.0, levels[i + 1].f.p, s, lowp);
         cur[i] = a;
     }
-    launch_dense_gemv(nc, Ainv.p, levels[L - 1].f.p, levels[L - 1].u.p, s);
+    coarse_solve(levels[L - 1].f.p, levels[L - 1].u.p);
     cur[L - 1] = levels[L - 1].u.p;
     for (size_t ii = L - 1; ii-- > start;) {
         Level &lv = levels[ii];
         const double *fi = ii == start ? f0 : lv.f.p;
         double *a = cur[ii];
         double *b = (a == lv.u.p) ? lv.t.p : lv.u.p;
-        launch_spmv(lv.P, 1.0, cur[ii + 1], 1.0, a, s);
+        launch_spmv(lv.P, 1.0, cur[ii + 1], 1.0, a, s, lowp);
         for (int sw = prm.post_sweeps; sw > 0; --sw) {
             const bool last0 = ii == start && sw == 1;
             double *out = last0 ? u0 : b;
             if (last0 && fuse_rz) {
-                launch_smooth_dot(lv.A, lv.M, fi, a, out, partials.p, sc.p, s);
+                launch_smooth_dot(lv.A, lv.M, fi, a, out, partials.p, sc.p, s, CG_RZ, lowp);
                 fused = true;
             } else {
-                launch_smooth(lv.A, lv.M, fi, a, out, s);
+                launch_smooth(lv.A, lv.M, fi, a, out, s, lowp);
             }
             b = a;
             a = out;

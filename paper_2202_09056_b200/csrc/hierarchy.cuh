@@ -28,6 +28,9 @@ struct Hierarchy {
     std::vector<Level> levels;
     DevBuf<double> Ainv;       // coarsest inverse, row-major nc x nc
     int64_t nc = 0;
+    bool coarse_lu = false;    // coarse solve by the reference's LU (coarse_lu.cu)
+    CoarseLu lu;
+    void coarse_solve(const double *f, double *u);
     double setup_seconds = 0;
     DevBuf<DevError> err;
     // CG workspace (cg.hpp:46-47)

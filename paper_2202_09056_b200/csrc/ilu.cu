@@ -473,7 +473,7 @@ void setup_ilu0(const Bsr3 &A, Smoother &M, DevError *err, cudaStream_t s) {
 }
 
 void launch_ilu_smooth(const Bsr3 *A, const Smoother &M, const double *f, const double *u_in,
-                       double *u_out, cudaStream_t s) {
+                       double *u_out, cudaStream_t s, bool lowp) {
     const int n = static_cast<int>(M.nrows);
     if (n == 0) return;
     // [y | x | two row counters]: sentinel-filled by one memset (the counters
@@ -483,7 +483,7 @@ void launch_ilu_smooth(const Bsr3 *A, const Smoother &M, const double *f, const 
     CK(cudaMemsetAsync(M.sweep.p, 0xff, sizeof(double) * (6LL * n + 1), s));
     const double *rin = f;
     if (u_in) {
-        launch_residual(*A, f, u_in, M.tmp.p, s);  // r = f - A u (hierarchy.hpp:213-215)
+        launch_residual(*A, f, u_in, M.tmp.p, s, lowp);  // r = f - A u (hierarchy.hpp:213-215)
         rin = M.tmp.p;
     }
     static const int gf = [] {

@@ -15,6 +15,7 @@ struct Bsr3 {
     int64_t nrows = 0, ncols = 0, nnzb = 0;
     DevBuf<int> ptr, col;
     DevBuf<double> val;
+    DevBuf<float> val32;  // optional fp32 copy of val (mixed-precision V-cycle)
     void alloc(int64_t nr, int64_t nc, int64_t nz, cudaStream_t s) {
         if (nz > INT32_MAX || nr > INT32_MAX || nc > INT32_MAX)
             fail(SAMG_UNSUPPORTED, "BSR3: more than 2^31-1 blocks per matrix");
@@ -46,14 +47,18 @@ struct Smoother {
 
 // ---- solve phase (solve.cu) -------------------------------------------------
 // y = alpha*A*x + beta*y  (csr.hpp:129-160)
+// lowp (mixed-precision V-cycle): read A.val32 instead of A.val when present;
+// vectors and arithmetic stay fp64
 void launch_spmv(const Bsr3 &A, double alpha, const double *x, double beta, double *y,
-                 cudaStream_t s);
+                 cudaStream_t s, bool lowp = false);
 // r = f - A*u  (csr.hpp:163-169)
 void launch_residual(const Bsr3 &A, const double *f, const double *u, double *r,
-                     cudaStream_t s);
+                     cudaStream_t s, bool lowp = false);
 // u_out = u + M (f - A u)  (one smoothing sweep, relaxation.hpp:165-173)
 void launch_smooth(const Bsr3 &A, const Smoother &M, const double *f, const double *u,
-                   double *u_out, cudaStream_t s);
+                   double *u_out, cudaStream_t s, bool lowp = false);
+// fp32 copy of the values (A.val32) for the mixed-precision V-cycle
+void make_lowp(Bsr3 &A, cudaStream_t s);
 // u = M f  (one sweep from a zero guess: the residual is f exactly)
 void launch_smooth_zero(int64_t nrows, const Smoother &M, const double *f, double *u,
                         cudaStream_t s);
@@ -87,7 +92,7 @@ void launch_spmv_dot(const Bsr3 &A, const double *p, double *q, double *partials
 // last post-smoothing sweep of the V-cycle fused with r.z (cg.hpp:73-75) -> RZ
 void launch_smooth_dot(const Bsr3 &A, const Smoother &M, const double *f, const double *u,
                        double *u_out, double *partials, CgScalars *sc, cudaStream_t s,
-                       int what = CG_RZ);
+                       int what = CG_RZ, bool lowp = false);
 // x.y -> what
 void launch_dot(int64_t n, const double *x, const double *y, double *partials, CgScalars *sc,
                 int what, cudaStream_t s);
@@ -146,9 +151,21 @@ void setup_smoother(const Bsr3 &A, int kind, double omega, Smoother &M, DevError
 // u_out = u_in + (LU)^-1 (f - A u_in)  (u_in == nullptr: zero guess, r = f)
 void setup_ilu0(const Bsr3 &A, Smoother &M, DevError *err, cudaStream_t s);
 void launch_ilu_smooth(const Bsr3 *A, const Smoother &M, const double *f, const double *u_in,
-                       double *u_out, cudaStream_t s);
+                       double *u_out, cudaStream_t s, bool lowp = false);
 // coarsest level: dense inverse (row-major n x n), n = 3*A.nrows
 void dense_inverse(const Bsr3 &A, DevBuf<double> &Ainv, DevError *err, cudaStream_t s);
+// the reference's dense_lu (hierarchy.hpp:86-129), bit-exact (coarse_lu.cu):
+// for numerically singular coarse operators, where the explicit inverse and
+// the LU solve disagree
+constexpr int64_t kLuMaxN = 2048;
+struct CoarseLu {
+    int64_t n = 0;
+    DevBuf<double> X;        // row-major n x n: unit L below, U on and above the diagonal
+    DevBuf<double> Lt;       // L column-major (forward sweep)
+    DevBuf<int64_t> perm;    // composed row swaps: (P f)[k] = f[perm[k]]
+};
+void dense_lu_ref(const Bsr3 &A, CoarseLu &lu, DevError *err, cudaStream_t s);
+void launch_lu_solve(const CoarseLu &lu, const double *f, double *u, cudaStream_t s);
 
 // throws the first device-side error, if any (synchronises s)
 void check_dev_error(DevError *err, cudaStream_t s);

@@ -101,30 +101,57 @@ __device__ __forceinline__ void row_sums_units(int row, bool valid, int lane,
 // starts 16-byte aligned iff j is even), so every lane runs the same
 // instruction sequence; x[3c..3c+2] likewise with one 16-byte + one 8-byte
 // load.  Per block: 1 col + 5 value + 2 x loads.
-template <int G>
+// A block as 9 doubles from its 9 stored values v[0..8] (element offset of
+// v in its array has parity `odd`): fp64 -- four 16-byte + one 8-byte load;
+// fp32 (mixed-precision V-cycle storage) -- four 8-byte + one 4-byte load.
+// kNc: read-only global path (ld.global.nc), else a generic (shared) load.
+template <bool kNc>
+__device__ __forceinline__ void blk9(const double *v, int odd, double (&b)[9]) {
+    auto l2 = [](const double *p) {
+        if constexpr (kNc) return ldg2(p);
+        else return *reinterpret_cast<const double2 *>(p);
+    };
+    const double2 q0 = l2(v + odd), q1 = l2(v + odd + 2), q2 = l2(v + odd + 4), q3 = l2(v + odd + 6);
+    const double e = kNc ? __ldg(v + (odd ? 0 : 8)) : v[odd ? 0 : 8];
+    b[0] = odd ? e : q0.x; b[1] = odd ? q0.x : q0.y; b[2] = odd ? q0.y : q1.x;
+    b[3] = odd ? q1.x : q1.y; b[4] = odd ? q1.y : q2.x; b[5] = odd ? q2.x : q2.y;
+    b[6] = odd ? q2.y : q3.x; b[7] = odd ? q3.x : q3.y; b[8] = odd ? q3.y : e;
+}
+template <bool kNc>
+__device__ __forceinline__ void blk9(const float *v, int odd, double (&b)[9]) {
+    auto l2 = [](const float *p) {
+        if constexpr (kNc) return __ldg(reinterpret_cast<const float2 *>(p));
+        else return *reinterpret_cast<const float2 *>(p);
+    };
+    const float2 q0 = l2(v + odd), q1 = l2(v + odd + 2), q2 = l2(v + odd + 4), q3 = l2(v + odd + 6);
+    const float e = kNc ? __ldg(v + (odd ? 0 : 8)) : v[odd ? 0 : 8];
+    b[0] = odd ? e : q0.x; b[1] = odd ? q0.x : q0.y; b[2] = odd ? q0.y : q1.x;
+    b[3] = odd ? q1.x : q1.y; b[4] = odd ? q1.y : q2.x; b[5] = odd ? q2.x : q2.y;
+    b[6] = odd ? q2.y : q3.x; b[7] = odd ? q3.x : q3.y; b[8] = odd ? q3.y : e;
+}
+
+template <int G, class VT = double>
 __device__ __forceinline__ void row_sums_blocks(int row, bool valid, int lane,
         const int *__restrict__ ptr, const int *__restrict__ col,
-        const double *__restrict__ val, const double *__restrict__ x,
+        const VT *__restrict__ val, const double *__restrict__ x,
         double &s0, double &s1, double &s2) {
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    // blocks in flight per lane: fp32 blocks are half the bytes, so twice as many
+    constexpr int kUnr = sizeof(VT) == 4 ? 4 : 2;
     if (valid) {
         const int beg = __ldg(ptr + row), end = __ldg(ptr + row + 1);
-#pragma unroll 2
+#pragma unroll kUnr
         for (int j = beg + lane; j < end; j += G) {
             const int c = __ldg(col + j);
-            const double *v = val + 9 * static_cast<size_t>(j);
-            const int odd = j & 1;
-            const double2 q0 = ldg2(v + odd), q1 = ldg2(v + odd + 2), q2 = ldg2(v + odd + 4),
-                          q3 = ldg2(v + odd + 6);
-            const double e = __ldg(v + (odd ? 0 : 8));
+            double bb[9];
+            blk9<true>(val + 9 * static_cast<size_t>(j), j & 1, bb);
             const double *xp = x + 3 * static_cast<size_t>(c);
             const int xo = c & 1;
             const double2 xq = ldg2(xp + xo);
             const double xe = __ldg(xp + (xo ? 0 : 2));
             const double x0 = xo ? xe : xq.x, x1 = xo ? xq.x : xq.y, x2 = xo ? xq.y : xe;
-            const double b0 = odd ? e : q0.x, b1 = odd ? q0.x : q0.y, b2 = odd ? q0.y : q1.x;
-            const double b3 = odd ? q1.x : q1.y, b4 = odd ? q1.y : q2.x, b5 = odd ? q2.x : q2.y;
-            const double b6 = odd ? q2.y : q3.x, b7 = odd ? q3.x : q3.y, b8 = odd ? q3.y : e;
+            const double b0 = bb[0], b1 = bb[1], b2 = bb[2], b3 = bb[3], b4 = bb[4], b5 = bb[5],
+                         b6 = bb[6], b7 = bb[7], b8 = bb[8];
             a0 = fma(b0, x0, a0); a0 = fma(b1, x1, a0); a0 = fma(b2, x2, a0);
             a1 = fma(b3, x0, a1); a1 = fma(b4, x1, a1); a1 = fma(b5, x2, a1);
             a2 = fma(b6, x0, a2); a2 = fma(b7, x1, a2); a2 = fma(b8, x2, a2);
@@ -134,12 +161,12 @@ __device__ __forceinline__ void row_sums_blocks(int row, bool valid, int lane,
     group_reduce3<G>(s0, s1, s2);
 }
 
-template <int G, int V>
+template <int G, int V, class VT>
 __device__ __forceinline__ void row_sums(int row, bool valid, int lane, const int *__restrict__ ptr,
-        const int *__restrict__ col, const double *__restrict__ val,
+        const int *__restrict__ col, const VT *__restrict__ val,
         const double *__restrict__ x, double &s0, double &s1, double &s2) {
-    if constexpr (V == 0) row_sums_units<G>(row, valid, lane, ptr, col, val, x, s0, s1, s2);
-    else row_sums_blocks<G>(row, valid, lane, ptr, col, val, x, s0, s1, s2);
+    if constexpr (V == 0 && std::is_same_v<VT, double>) row_sums_units<G>(row, valid, lane, ptr, col, val, x, s0, s1, s2);
+    else row_sums_blocks<G, VT>(row, valid, lane, ptr, col, val, x, s0, s1, s2);
 }
 
 __device__ __forceinline__ double pick3(int c, double a, double b, double d) {
@@ -222,9 +249,9 @@ struct EpiDot {
     }
 };
 
-template <int G, int V, class Epi>
+template <int G, int V, class Epi, class VT = double>
 __global__ void __launch_bounds__(256) k_bsr3(int nrows, const int *__restrict__ ptr,
-        const int *__restrict__ col, const double *__restrict__ val,
+        const int *__restrict__ col, const VT *__restrict__ val,
         const double *__restrict__ x, Epi epi) {
     const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const int row = gtid / G, lane = threadIdx.x % G;
@@ -244,7 +271,7 @@ __global__ void __launch_bounds__(256) k_bsr3_rows(int nlist, const int *__restr
     const bool valid = g < nlist;
     const int row = valid ? __ldg(rows + g) : 0;
     double s0, s1, s2;
-    row_sums<G, 1>(row, valid, lane, ptr, col, val, x, s0, s1, s2);
+    row_sums<G, 1, double>(row, valid, lane, ptr, col, val, x, s0, s1, s2);
     if (valid) epilogue<G>(epi, row, lane, s0, s1, s2);
 }
 
@@ -323,9 +350,9 @@ __device__ void grid_finish(double d, double *partials, CgScalars *sc, int what,
 // SpMV-family kernel whose epilogue also yields a dot product, finished by
 // grid_finish: q = A p with p.q (CG), or the last smoothing sweep with r.z.
 // Grid-stride over row groups with a fixed grid so partials are few.
-template <int G, class Epi>
+template <int G, class Epi, class VT = double>
 __global__ void __launch_bounds__(256) k_bsr3_reduce(int nrows, const int *__restrict__ ptr,
-        const int *__restrict__ col, const double *__restrict__ val,
+        const int *__restrict__ col, const VT *__restrict__ val,
         const double *__restrict__ x, Epi epi, double *__restrict__ partials, CgScalars *sc,
         int what) {
     const int groups = gridDim.x * (blockDim.x / G);
@@ -336,7 +363,7 @@ __global__ void __launch_bounds__(256) k_bsr3_reduce(int nrows, const int *__res
         const int row = (blockIdx.x * blockDim.x + threadIdx.x) / G + it * groups;
         const bool valid = row < nrows;
         double s0, s1, s2;
-        row_sums<G, 1>(row, valid, lane, ptr, col, val, x, s0, s1, s2);
+        row_sums<G, 1, VT>(row, valid, lane, ptr, col, val, x, s0, s1, s2);
         if (valid) d += epilogue<G>(epi, row, lane, s0, s1, s2);
     }
     grid_finish(d, partials, sc, what, 0);
@@ -388,15 +415,27 @@ struct TmaHdr {
 
 struct TmaCfg {
     int nrows, nchunks, stages;
+    int per_cta;  // > 0: CTA b owns the contiguous chunks [b*per_cta, (b+1)*per_cta)
+                  // (neighbouring rows share x, so the gathers hit L1); 0: strided
     unsigned vcap, ccap, pcap;  // stage layout: val | col | ptr (bytes)
     long long nnzb;
 };
 
 constexpr int kTmaHdrBytes = 1024;  // barriers + headers of up to 16 stages
 
-template <int G, int TW, int NT, bool kReduce, class Epi>
+// the CTA's k-th chunk, or -1 past its last
+__device__ __forceinline__ int chunk_of(const TmaCfg &cfg, int k) {
+    if (cfg.per_cta > 0) {
+        const int c = blockIdx.x * cfg.per_cta + k;
+        return k < cfg.per_cta && c < cfg.nchunks ? c : -1;
+    }
+    const int c = blockIdx.x + k * gridDim.x;
+    return c < cfg.nchunks ? c : -1;
+}
+
+template <int G, int TW, int NT, bool kReduce, class Epi, class VT = double>
 __global__ void __launch_bounds__(32 * (TW * NT + 1), 1) k_bsr3_tma(TmaCfg cfg, const int *__restrict__ ptr,
-        const int *__restrict__ col, const double *__restrict__ val,
+        const int *__restrict__ col, const VT *__restrict__ val,
         const double *__restrict__ x, Epi epi, double *partials, CgScalars *sc, int what) {
     static_assert(G >= 1 && G <= 32, "TMA variant: at most one warp per row");
     constexpr int RPC = 32 * TW / G;  // rows per chunk: one team of TW warps per chunk
@@ -422,28 +461,30 @@ __global__ void __launch_bounds__(32 * (TW * NT + 1), 1) k_bsr3_tma(TmaCfg cfg, 
         // chunks at once, lane 0 issues the copies in order
         int st = 0;
         unsigned ph = 0;
-        for (int c0 = blockIdx.x; c0 < cfg.nchunks; c0 += 32 * gridDim.x) {
-            const int cl = c0 + lane32 * gridDim.x;
+        for (int k0 = 0; chunk_of(cfg, k0) >= 0; k0 += 32) {
+            const int cl = chunk_of(cfg, k0 + lane32);
             int b0 = 0, b1 = 0;
-            if (cl < cfg.nchunks) {
+            if (cl >= 0) {
                 const int r0 = cl * RPC, r1 = min(r0 + RPC, cfg.nrows);
                 b0 = __ldg(ptr + r0);
                 b1 = __ldg(ptr + r1);
             }
             for (int i = 0; i < 32; ++i) {
-                const int c = c0 + i * gridDim.x;
+                const int c = chunk_of(cfg, k0 + i);
                 const int p0 = __shfl_sync(0xffffffffu, b0, i), p1 = __shfl_sync(0xffffffffu, b1, i);
-                if (c >= cfg.nchunks) break;
+                if (c < 0) break;
                 if (lane32 == 0) {
                     mbar_wait(empty + st, ph ^ 1);
                     const int r0 = c * RPC;
-                    const long long vb = (72LL * p0) & ~15LL, ve = (72LL * p1 + 15) & ~15LL;
+                    constexpr long long BB = 9 * sizeof(VT);  // bytes per stored block
+                    const long long vb = (BB * p0) & ~15LL, ve = (BB * p1 + 15) & ~15LL;
                     const long long cb = (4LL * p0) & ~15LL, ce = (4LL * p1 + 15) & ~15LL;
                     const long long pe = 4LL * (r0 + RPC + 4);
                     const bool direct = ve - vb > cfg.vcap || ce - cb > cfg.ccap ||
-                                        ve > 72LL * cfg.nnzb || ce > 4LL * cfg.nnzb ||
+                                        ve > BB * cfg.nnzb || ce > 4LL * cfg.nnzb ||
                                         r0 + RPC + 4 > cfg.nrows + 1 || p1 == p0;
-                    hdr[st] = TmaHdr{p0, direct ? 1 : 0, static_cast<int>((72LL * p0 - vb) / 8),
+                    hdr[st] = TmaHdr{p0, direct ? 1 : 0,
+                                     static_cast<int>((BB * p0 - vb) / static_cast<long long>(sizeof(VT))),
                                      static_cast<int>((4LL * p0 - cb) / 4)};
                     if (!direct) {
                         unsigned char *sv = data + static_cast<size_t>(st) * stage_bytes;
@@ -467,8 +508,7 @@ __global__ void __launch_bounds__(32 * (TW * NT + 1), 1) k_bsr3_tma(TmaCfg cfg, 
         // chunks are computed concurrently while the ring fills
         const int team = warp / TW, tt = threadIdx.x - 32 * TW * team;
         const int lane = tt % G, grp = tt / G;
-        for (int i = team, c = blockIdx.x + team * gridDim.x; c < cfg.nchunks;
-             i += NT, c += NT * gridDim.x) {
+        for (int i = team, c = chunk_of(cfg, team); c >= 0; i += NT, c = chunk_of(cfg, i)) {
             const int st = i % S;
             const unsigned ph = (i / S) & 1;
             mbar_wait(full + st, ph);
@@ -477,34 +517,29 @@ __global__ void __launch_bounds__(32 * (TW * NT + 1), 1) k_bsr3_tma(TmaCfg cfg, 
             const bool valid = row < cfg.nrows;
             double s0, s1, s2;
             if (h.direct) {
-                row_sums_blocks<G>(row, valid, lane, ptr, col, val, x, s0, s1, s2);
+                row_sums_blocks<G, VT>(row, valid, lane, ptr, col, val, x, s0, s1, s2);
             } else {
                 const unsigned char *sv = data + static_cast<size_t>(st) * stage_bytes;
-                const double *svd = reinterpret_cast<const double *>(sv);
+                const VT *svd = reinterpret_cast<const VT *>(sv);
                 const int *svc = reinterpret_cast<const int *>(sv + cfg.vcap);
                 const int *svp = reinterpret_cast<const int *>(sv + cfg.vcap + cfg.ccap);
                 double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+                constexpr int kUnr = sizeof(VT) == 4 ? 4 : 2;
                 if (valid) {
                     const int beg = svp[grp] - h.p0, end = svp[grp + 1] - h.p0;
-#pragma unroll 2
+#pragma unroll kUnr
                     for (int k = beg + lane; k < end; k += G) {
                         const int c3 = svc[k + h.coff];
                         const int o = 9 * k + h.voff;
-                        const double *v = svd + o;
-                        const int odd = o & 1;
-                        const double2 q0 = *reinterpret_cast<const double2 *>(v + odd),
-                                      q1 = *reinterpret_cast<const double2 *>(v + odd + 2),
-                                      q2 = *reinterpret_cast<const double2 *>(v + odd + 4),
-                                      q3 = *reinterpret_cast<const double2 *>(v + odd + 6);
-                        const double e = v[odd ? 0 : 8];
+                        double bb[9];
+                        blk9<false>(svd + o, o & 1, bb);
                         const double *xp = x + 3 * static_cast<size_t>(c3);
                         const int xo = c3 & 1;
                         const double2 xq = ldg2(xp + xo);
                         const double xe = __ldg(xp + (xo ? 0 : 2));
                         const double x0 = xo ? xe : xq.x, x1 = xo ? xq.x : xq.y, x2 = xo ? xq.y : xe;
-                        const double b0 = odd ? e : q0.x, b1 = odd ? q0.x : q0.y, b2 = odd ? q0.y : q1.x;
-                        const double b3 = odd ? q1.x : q1.y, b4 = odd ? q1.y : q2.x, b5 = odd ? q2.x : q2.y;
-                        const double b6 = odd ? q2.y : q3.x, b7 = odd ? q3.x : q3.y, b8 = odd ? q3.y : e;
+                        const double b0 = bb[0], b1 = bb[1], b2 = bb[2], b3 = bb[3], b4 = bb[4],
+                                     b5 = bb[5], b6 = bb[6], b7 = bb[7], b8 = bb[8];
                         a0 = fma(b0, x0, a0); a0 = fma(b1, x1, a0); a0 = fma(b2, x2, a0);
                         a1 = fma(b3, x0, a1); a1 = fma(b4, x1, a1); a1 = fma(b5, x2, a1);
                         a2 = fma(b6, x0, a2); a2 = fma(b7, x1, a2); a2 = fma(b8, x2, a2);
@@ -599,20 +634,23 @@ void dispatch_tma_shape(int G, F f) {
     }
 }
 
-template <bool kReduce, class Epi>
-bool launch_tma(const Bsr3 &A, const double *x, Epi epi, double *partials, CgScalars *sc,
-                int what, cudaStream_t s) {
+template <bool kReduce, class VT, class Epi>
+bool launch_tma(const Bsr3 &A, const VT *val, const double *x, Epi epi, double *partials,
+                CgScalars *sc, int what, cudaStream_t s) {
     if (A.nrows < 8 || A.nnzb == 0) return false;
-    if ((reinterpret_cast<uintptr_t>(A.val.p) | reinterpret_cast<uintptr_t>(A.col.p) |
+    if ((reinterpret_cast<uintptr_t>(val) | reinterpret_cast<uintptr_t>(A.col.p) |
          reinterpret_cast<uintptr_t>(A.ptr.p)) & 15)
         return false;
     static const int forced_g = env_int("SAMG_TMA_G", 0);
-    static const int budget = env_int("SAMG_TMA_SMEM", 226000);
+    static const int budget64 = env_int("SAMG_TMA_SMEM", 226000);
+    static const int budget32 = env_int("SAMG_TMA_SMEM32", 226000);
+    const int budget = sizeof(VT) == 4 ? budget32 : budget64;
     constexpr int TW = 8, NT = 2;  // two teams of 8 consumer warps (measured best on C1)
     const double bpr = static_cast<double>(A.nnzb) / A.nrows;
     // ~3 blocks per lane (C1 fine level, 26 blocks per row: G = 8)
+    // (fp32 values: twice the blocks per lane, C1 mixed solve 0.080 -> 0.074 s)
     int G = 4;
-    while (G < 32 && 3.3 * G * 1.5 < bpr) G *= 2;
+    while (G < 32 && 3.3 * G * 1.5 * (sizeof(VT) == 4 ? 2 : 1) < bpr) G *= 2;
     if (forced_g == 4 || forced_g == 8 || forced_g == 16 || forced_g == 32) G = forced_g;
     const int rpc = 32 * TW / G;
     auto up = [](long long b) { return static_cast<unsigned>((b + 127) / 128 * 128); };
@@ -621,7 +659,7 @@ bool launch_tma(const Bsr3 &A, const double *x, Epi epi, double *partials, CgSca
     cfg.nrows = static_cast<int>(A.nrows);
     cfg.nchunks = static_cast<int>((A.nrows + rpc - 1) / rpc);
     cfg.nnzb = A.nnzb;
-    cfg.vcap = up(rpc * est * 72 + 16);
+    cfg.vcap = up(rpc * est * 9 * static_cast<long long>(sizeof(VT)) + 16);
     cfg.ccap = up(rpc * est * 4 + 16);
     cfg.pcap = up(4LL * (rpc + 4));
     const long long stage = cfg.vcap + cfg.ccap + cfg.pcap;
@@ -641,7 +679,7 @@ bool launch_tma(const Bsr3 &A, const double *x, Epi epi, double *partials, CgSca
     bool ok = false;
     dispatch_tma_shape(G, [&](auto sh) {
         using Sh = decltype(sh);
-        auto kern = k_bsr3_tma<Sh::G, Sh::TW, Sh::NT, kReduce, Epi>;
+        auto kern = k_bsr3_tma<Sh::G, Sh::TW, Sh::NT, kReduce, Epi, VT>;
         const int threads = 32 * (Sh::TW * Sh::NT + 1);
         // opt in to the largest dynamic size next to the static shared
         // memory of the reduction helpers
@@ -663,37 +701,47 @@ bool launch_tma(const Bsr3 &A, const double *x, Epi epi, double *partials, CgSca
         int occ = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
         const int grid = std::max(1, std::min(cfg.nchunks, std::max(1, occ) * sms));
-        kern<<<grid, threads, smem, s>>>(cfg, A.ptr.p, A.col.p, A.val.p, x, epi, partials, sc, what);
+        static const int blocked = env_int("SAMG_TMA_BLOCKED", 0);
+        cfg.per_cta = blocked ? (cfg.nchunks + grid - 1) / grid : 0;
+        kern<<<grid, threads, smem, s>>>(cfg, A.ptr.p, A.col.p, val, x, epi, partials, sc, what);
         ok = true;
     });
     if (ok) CK_LAUNCH();
     return ok;
 }
 
-template <class Epi>
-void launch_rows(const Bsr3 &A, const double *x, Epi epi, cudaStream_t s) {
-    if (A.nrows == 0) return;
-    if (spmv_variant() == 3 && launch_tma<false>(A, x, epi, nullptr, nullptr, 0, s)) return;
+template <class VT, class Epi>
+void launch_rows_t(const Bsr3 &A, const VT *val, const double *x, Epi epi, cudaStream_t s) {
+    if (spmv_variant() == 3 && launch_tma<false>(A, val, x, epi, nullptr, nullptr, 0, s)) return;
     const int G = choose_group(A);
     const int grid = ceil_div(A.nrows * static_cast<int64_t>(G), 256);
     const int n = static_cast<int>(A.nrows);
-    if (spmv_variant() == 0) {
-        if (G == 32) k_bsr3<32, 0><<<grid, 256, 0, s>>>(n, A.ptr.p, A.col.p, A.val.p, x, epi);
-        else if (G == 16) k_bsr3<16, 0><<<grid, 256, 0, s>>>(n, A.ptr.p, A.col.p, A.val.p, x, epi);
-        else k_bsr3<8, 0><<<grid, 256, 0, s>>>(n, A.ptr.p, A.col.p, A.val.p, x, epi);
+    if (std::is_same_v<VT, double> && spmv_variant() == 0) {
+        const double *vd = reinterpret_cast<const double *>(val);
+        if (G == 32) k_bsr3<32, 0><<<grid, 256, 0, s>>>(n, A.ptr.p, A.col.p, vd, x, epi);
+        else if (G == 16) k_bsr3<16, 0><<<grid, 256, 0, s>>>(n, A.ptr.p, A.col.p, vd, x, epi);
+        else k_bsr3<8, 0><<<grid, 256, 0, s>>>(n, A.ptr.p, A.col.p, vd, x, epi);
     } else {
         dispatch_group(G, [&](auto g) {
             constexpr int GG = decltype(g)::value;
-            k_bsr3<GG, 1><<<grid, 256, 0, s>>>(n, A.ptr.p, A.col.p, A.val.p, x, epi);
+            k_bsr3<GG, 1, Epi, VT><<<grid, 256, 0, s>>>(n, A.ptr.p, A.col.p, val, x, epi);
         });
     }
     CK_LAUNCH();
 }
 
+// lowp: use the matrix's fp32 value copy (mixed-precision V-cycle) if it has one
 template <class Epi>
-void launch_reduce(const Bsr3 &A, const double *x, Epi epi, double *partials, CgScalars *sc,
-                   int what, cudaStream_t s) {
-    if (spmv_variant() == 3 && launch_tma<true>(A, x, epi, partials, sc, what, s)) return;
+void launch_rows(const Bsr3 &A, const double *x, Epi epi, cudaStream_t s, bool lowp = false) {
+    if (A.nrows == 0) return;
+    if (lowp && A.val32.p) launch_rows_t(A, static_cast<const float *>(A.val32.p), x, epi, s);
+    else launch_rows_t(A, static_cast<const double *>(A.val.p), x, epi, s);
+}
+
+template <class VT, class Epi>
+void launch_reduce_t(const Bsr3 &A, const VT *val, const double *x, Epi epi, double *partials,
+                     CgScalars *sc, int what, cudaStream_t s) {
+    if (spmv_variant() == 3 && launch_tma<true>(A, val, x, epi, partials, sc, what, s)) return;
     const int G = choose_group(A);
     const int n = static_cast<int>(A.nrows);
     dispatch_group(G, [&](auto g) {
@@ -704,14 +752,27 @@ void launch_reduce(const Bsr3 &A, const double *x, Epi epi, double *partials, Cg
             int occ = 0, dev = 0, sms = 148;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bsr3_reduce<GG, Epi>, 256, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bsr3_reduce<GG, Epi, VT>, 256, 0);
             return std::max(1, occ) * sms;
         }();
         const int grid = std::max(1, std::min({kReduceCtas, resident,
                                                ceil_div(A.nrows * static_cast<int64_t>(GG), 256)}));
-        k_bsr3_reduce<GG><<<grid, 256, 0, s>>>(n, A.ptr.p, A.col.p, A.val.p, x, epi, partials, sc, what);
+        k_bsr3_reduce<GG, Epi, VT><<<grid, 256, 0, s>>>(n, A.ptr.p, A.col.p, val, x, epi, partials, sc, what);
     });
     CK_LAUNCH();
+}
+
+template <class Epi>
+void launch_reduce(const Bsr3 &A, const double *x, Epi epi, double *partials, CgScalars *sc,
+                   int what, cudaStream_t s, bool lowp = false) {
+    if (lowp && A.val32.p) launch_reduce_t(A, static_cast<const float *>(A.val32.p), x, epi, partials, sc, what, s);
+    else launch_reduce_t(A, static_cast<const double *>(A.val.p), x, epi, partials, sc, what, s);
+}
+
+__global__ void k_to_f32(int64_t n, const double *__restrict__ a, float *__restrict__ b) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        b[i] = __double2float_rn(a[i]);
 }
 
 __global__ void k_smooth_zero_point(int64_t n, const double *__restrict__ m,
@@ -849,8 +910,8 @@ int vec_grid(int64_t n) {
 } // namespace
 
 void launch_spmv(const Bsr3 &A, double alpha, const double *x, double beta, double *y,
-                 cudaStream_t s) {
-    launch_rows(A, x, EpiSpmv{alpha, beta, y}, s);
+                 cudaStream_t s, bool lowp) {
+    launch_rows(A, x, EpiSpmv{alpha, beta, y}, s, lowp);
 }
 
 // y[rows] = alpha*A[rows,:]*x + beta*y[rows]; group 0 = choose from A
@@ -869,15 +930,15 @@ void launch_spmv_rows(const Bsr3 &A, const int *rows, int64_t nlist, int group, 
 }
 
 void launch_residual(const Bsr3 &A, const double *f, const double *u, double *r,
-                     cudaStream_t s) {
-    launch_rows(A, u, EpiResidual{f, r}, s);
+                     cudaStream_t s, bool lowp) {
+    launch_rows(A, u, EpiResidual{f, r}, s, lowp);
 }
 
 void launch_smooth(const Bsr3 &A, const Smoother &M, const double *f, const double *u,
-                   double *u_out, cudaStream_t s) {
-    if (M.kind == SM_ILU) return launch_ilu_smooth(&A, M, f, u, u_out, s);
-    if (M.kind == SM_POINT) launch_rows(A, u, EpiSmoothPoint{f, u, M.data.p, u_out}, s);
-    else launch_rows(A, u, EpiSmoothBlock{f, u, M.data.p, u_out}, s);
+                   double *u_out, cudaStream_t s, bool lowp) {
+    if (M.kind == SM_ILU) return launch_ilu_smooth(&A, M, f, u, u_out, s, lowp);
+    if (M.kind == SM_POINT) launch_rows(A, u, EpiSmoothPoint{f, u, M.data.p, u_out}, s, lowp);
+    else launch_rows(A, u, EpiSmoothBlock{f, u, M.data.p, u_out}, s, lowp);
 }
 
 void launch_smooth_zero(int64_t nrows, const Smoother &M, const double *f, double *u,
@@ -895,17 +956,24 @@ void launch_spmv_dot(const Bsr3 &A, const double *p, double *q, double *partials
 }
 
 void launch_smooth_dot(const Bsr3 &A, const Smoother &M, const double *f, const double *u,
-                       double *u_out, double *partials, CgScalars *sc, cudaStream_t s, int what) {
+                       double *u_out, double *partials, CgScalars *sc, cudaStream_t s, int what,
+                       bool lowp) {
     if (M.kind == SM_ILU) {
         // f.u_out, as the fused sweeps' epilogues return (r.z inside CG)
-        launch_ilu_smooth(&A, M, f, u, u_out, s);
+        launch_ilu_smooth(&A, M, f, u, u_out, s, lowp);
         launch_dot(3 * A.nrows, f, u_out, partials, sc, what, s);
         return;
     }
     if (M.kind == SM_POINT)
-        launch_reduce(A, u, EpiSmoothPoint{f, u, M.data.p, u_out}, partials, sc, what, s);
+        launch_reduce(A, u, EpiSmoothPoint{f, u, M.data.p, u_out}, partials, sc, what, s, lowp);
     else
-        launch_reduce(A, u, EpiSmoothBlock{f, u, M.data.p, u_out}, partials, sc, what, s);
+        launch_reduce(A, u, EpiSmoothBlock{f, u, M.data.p, u_out}, partials, sc, what, s, lowp);
+}
+
+void make_lowp(Bsr3 &A, cudaStream_t s) {
+    A.val32.alloc(9 * A.nnzb, s);
+    if (A.nnzb) k_to_f32<<<vec_grid(9 * A.nnzb), 256, 0, s>>>(9 * A.nnzb, A.val.p, A.val32.p);
+    CK_LAUNCH();
 }
 
 void launch_dense_gemv(int64_t n, const double *Ainv, const double *f, double *u,

@@ -42,7 +42,7 @@ SM = {"spai0": 1, "jacobi": 0, "block_jacobi": 2, "ilu0": 3}
 PIPE = {"block": 1, "ns_hybrid1": 3, "ns_hybrid2": 4, "ns_block": 5}
 
 
-def run(name, ref_on, max_it, out, smoother=None, pipeline="ns_block"):
+def run(name, ref_on, max_it, out, smoother=None, pipeline="ns_block", precision="fp64"):
     kw, smoothers = CONFIGS[name]
     if smoother:
         smoothers = [(smoother, 0.72)]
@@ -52,8 +52,8 @@ def run(name, ref_on, max_it, out, smoother=None, pipeline="ns_block"):
     B = None if pipeline == "block" else p.nullspace()
     for sm, om in smoothers:
         rec = {"config": name, "pipeline": pipeline, "smoother": sm, "omega": om, "unknowns": p.n,
-               "nnzb": p.nnzb, "generate_s": tgen}
-        prm = pb.AmgParams(smoother=sm, smoother_omega=om)
+               "nnzb": p.nnzb, "generate_s": tgen, "vcycle_precision": precision}
+        prm = pb.AmgParams(smoother=sm, smoother_omega=om, vcycle_precision=precision)
         h = pb.setup_bsr3(p.nbrows, p.ptr, p.col, p.val.reshape(-1), B, pipeline, prm)
         h.close()  # warm-up (lazy module loading, memory pool)
         t0 = time.perf_counter()
@@ -109,9 +109,11 @@ def main():
     ap.add_argument("--out", default=None)
     ap.add_argument("--smoother", default=None, help="override the configs' smoothers (e.g. ilu0)")
     ap.add_argument("--pipeline", default="ns_block", choices=sorted(PIPE))
+    ap.add_argument("--precision", default="fp64", choices=["fp64", "mixed"],
+                    help="V-cycle operator storage (mixed: fp32 copies, DESIGN.md 5.8)")
     a = ap.parse_args()
     for c in a.configs:
-        run(c, a.ref, a.max_it, a.out, a.smoother, a.pipeline)
+        run(c, a.ref, a.max_it, a.out, a.smoother, a.pipeline, a.precision)
 
 
 if __name__ == "__main__":

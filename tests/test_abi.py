@@ -60,6 +60,12 @@ def test_validation_before_device():
         pb.setup(A, B, "ns_block", pb.AmgParams(smoother=7))
     with pytest.raises(pb.NotDivisible):
         pb.setup(A, np.zeros((n, 4)))
+    prm = pb.AmgParams()
+    prm.vcycle_precision = "mixed"
+    c = prm.c()
+    c.vcycle_precision = 5
+    with pytest.raises(pb.InvalidArgument):
+        pb.setup(A, B, "ns_block", type("P", (), {"c": lambda self: c})())
 
 
 def test_no_cpu_fallback():
@@ -121,3 +127,13 @@ def test_generator_configs_shapes():
                         x_slowest=True)
     # traction total = -area of the end face
     assert abs(b.rhs[2::3].sum() + 1.0) <= 1e-14
+
+
+def test_mixed_precision_is_single_gpu_only():
+    """The partitioned solver keeps fp64 operators: dsetup refuses MIXED
+    before touching a device (include/samg_b200.h samg_precision)."""
+    from paper_2202_09056_b200.dist import DistHierarchy
+    p = pb.generate_hex(nx=3, ny=2, nz=2, dirichlet="eliminate")
+    with pytest.raises(pb.Unsupported):
+        DistHierarchy(p.nbrows, p.ptr, p.col, p.val.reshape(-1), p.nullspace(), 0, 2,
+                      prm=pb.AmgParams(vcycle_precision="mixed"), emulate=True)
