@@ -323,6 +323,30 @@ def run_b200(args, rank, world, local, dist):
             "runs": times,
             "what": "samg_generate_hex_device + samg_setup_device + samg_cg_solve_device "
                     "(last of three runs)"}
+        # the same problem with the reference's default smoother (block
+        # ILU(0), bit-identical) and with the mixed-precision V-cycle
+        variants = {}
+        for key, vprm in (("ilu0", pb.AmgParams(smoother="ilu0", device=local)),
+                          ("spai0_mixed", pb.AmgParams(smoother="spai0", device=local,
+                                                       vcycle_precision="mixed"))):
+            st, sv, vr = [], [], None
+            for it in range(1 + args.amg_repeats):  # first run: untimed warm-up
+                torch.cuda.synchronize(dev)
+                t0 = time.perf_counter()
+                hv = pb.setup_bsr3(p.nbrows, p.ptr, p.col, p.val.reshape(-1), B, "ns_block", vprm)
+                torch.cuda.synchronize(dev)
+                t1 = time.perf_counter()
+                vr = hv.cg_solve_device(f_d.data_ptr(), u_d.data_ptr())
+                torch.cuda.synchronize(dev)
+                t2 = time.perf_counter()
+                hv.close()
+                if it:
+                    st.append(t1 - t0)
+                    sv.append(t2 - t1)
+            variants[key] = {"setup_s": statistics.median(st), "solve_s": statistics.median(sv),
+                             "iterations": vr["iterations"], "converged": vr["converged"],
+                             "relative_residual": vr["relative_residual"]}
+        amg["variants"] = variants
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
