@@ -378,7 +378,9 @@ def run_b200(args, rank, world, local, dist):
             "e2e": {"value": e2e_val, "unit": "GB/s", "h2d_bytes_per_step": 8 * p.n,
                     "d2h_bytes_per_step": 8 * p.n,
                     "path": "samg_bsr3_spmv_batch (C-ABI): per step H2D of its own x and D2H of "
-                            "its y from/to pinned host memory, steps pipelined over three streams"},
+                            "its y from/to pinned host memory, steps pipelined over per-engine "
+                            "streams (H2D / SpMV / D2H, 4 staging slots), the SpMV on 96 of 148 "
+                            "SMs to leave HBM headroom for the PCIe DMA"},
             "gpu_launches": args.steps,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,

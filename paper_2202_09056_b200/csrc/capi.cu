@@ -20,15 +20,22 @@ struct samg_bsr3 {
     const samgb::Bsr3 *m = nullptr;
     int device = 0;
     samgb::DevBuf<double> xs, ys;  // e2e staging for host-vector spmv
-    // batched host-vector spmv: three streams, triple-buffered staging
-    static constexpr int kPipe = 3;
-    cudaStream_t bs[kPipe] = {nullptr, nullptr, nullptr};
+    // batched host-vector spmv: one stream per engine (H2D copies, kernels,
+    // D2H copies) over kPipe staging slots, ordered by events only where a
+    // slot is reused, so both copy directions stream back to back
+    static constexpr int kPipe = 4;
+    cudaStream_t bs[3] = {nullptr, nullptr, nullptr};  // h2d, kernel, d2h
+    cudaEvent_t ev_h[kPipe] = {}, ev_k[kPipe] = {}, ev_d[kPipe] = {};
     samgb::DevBuf<double> bx[kPipe], by[kPipe];
     ~samg_bsr3() {
-        // the staging buffers are stream-ordered on bs[]: free them first
+        // the staging buffers are stream-ordered on bs[1]: free them first
+        for (cudaStream_t &q : bs)
+            if (q) cudaStreamSynchronize(q);
         for (int b = 0; b < kPipe; ++b) {
             bx[b].release();
             by[b].release();
+            for (cudaEvent_t e : {ev_h[b], ev_k[b], ev_d[b]})
+                if (e) cudaEventDestroy(e);
         }
         for (cudaStream_t &q : bs)
             if (q) { cudaStreamSynchronize(q); cudaStreamDestroy(q); }
@@ -697,6 +704,24 @@ SAMG_API int samg_bsr3_spmv(const samg_bsr3 *mc, double alpha, const double *x, 
 // k and the D2H of y_{k-1} (full-duplex PCIe, separate copy engines): a
 // stream's chain H2D -> kernel -> D2H spans ~3 steps, so 3 buffers keep both
 // copy directions busy.
+// CTAs of the SpMV inside the host-vector pipeline (SAMG_BATCH_CTAS; 0 = one
+// per SM).  With the SpMV on every SM the kernel saturates HBM and starves
+// the concurrent PCIe DMA in both directions (H2D 116 -> 177 us, the SpMV
+// 85 -> 115 us per step, scripts/e2e_timeline.py); on 96 of 148 SMs the
+// SpMV still keeps up and the copies run at the duplex PCIe rate: C1 e2e
+// 2 900 -> 3 920 GB/s-equivalent (scripts/e2e_sweep.sh).
+static int batch_cta_cap() {
+    static const int v = [] {
+        const char *e = std::getenv("SAMG_BATCH_CTAS");
+        if (e) return std::atoi(e);
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        return std::max(1, sms * 96 / 148);
+    }();
+    return v;
+}
+
 SAMG_API int samg_bsr3_spmv_batch(const samg_bsr3 *mc, double alpha, const double *x, double beta,
                                   double *y, int64_t count) {
     return guarded([&] {
@@ -705,19 +730,35 @@ SAMG_API int samg_bsr3_spmv_batch(const samg_bsr3 *mc, double alpha, const doubl
         CK(cudaSetDevice(m->device));
         const Bsr3 &A = *m->m;
         const int64_t nx = 3 * A.ncols, ny = 3 * A.nrows;
-        for (int b = 0; b < samg_bsr3::kPipe; ++b) {
-            if (!m->bs[b]) CK(cudaStreamCreateWithFlags(&m->bs[b], cudaStreamNonBlocking));
-            if (m->bx[b].n < static_cast<size_t>(nx) + 1) m->bx[b].alloc(nx + 1, m->bs[b]);
-            if (m->by[b].n < static_cast<size_t>(ny) + 1) m->by[b].alloc(ny + 1, m->bs[b]);
+        constexpr int P = samg_bsr3::kPipe;
+        for (cudaStream_t &q : m->bs)
+            if (!q) CK(cudaStreamCreateWithFlags(&q, cudaStreamNonBlocking));
+        cudaStream_t sh = m->bs[0], sk = m->bs[1], sd = m->bs[2];
+        for (int b = 0; b < P; ++b) {
+            for (cudaEvent_t *e : {&m->ev_h[b], &m->ev_k[b], &m->ev_d[b]})
+                if (!*e) CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+            if (m->bx[b].n < static_cast<size_t>(nx) + 1) m->bx[b].alloc(nx + 1, sk);
+            if (m->by[b].n < static_cast<size_t>(ny) + 1) m->by[b].alloc(ny + 1, sk);
         }
+        CK(cudaStreamSynchronize(sk));  // staging allocations visible to the copy streams
         for (int64_t k = 0; k < count; ++k) {
-            const int b = static_cast<int>(k % samg_bsr3::kPipe);
-            cudaStream_t q = m->bs[b];
-            CK(cudaMemcpyAsync(m->bx[b].p, x + k * nx, sizeof(double) * nx, cudaMemcpyHostToDevice, q));
+            const int b = static_cast<int>(k % P);
+            // x slot b: free once kernel k-P has read it
+            if (k >= P) CK(cudaStreamWaitEvent(sh, m->ev_k[b], 0));
+            CK(cudaMemcpyAsync(m->bx[b].p, x + k * nx, sizeof(double) * nx, cudaMemcpyHostToDevice, sh));
             if (beta != 0.0)
-                CK(cudaMemcpyAsync(m->by[b].p, y + k * ny, sizeof(double) * ny, cudaMemcpyHostToDevice, q));
-            launch_spmv(A, alpha, m->bx[b].p, beta, m->by[b].p, q);
-            CK(cudaMemcpyAsync(y + k * ny, m->by[b].p, sizeof(double) * ny, cudaMemcpyDeviceToHost, q));
+                CK(cudaMemcpyAsync(m->by[b].p, y + k * ny, sizeof(double) * ny, cudaMemcpyHostToDevice, sh));
+            CK(cudaEventRecord(m->ev_h[b], sh));
+            // kernel k: its x has arrived, and y slot b has been copied out (step k-P)
+            CK(cudaStreamWaitEvent(sk, m->ev_h[b], 0));
+            if (k >= P) CK(cudaStreamWaitEvent(sk, m->ev_d[b], 0));
+            set_spmv_cta_cap(batch_cta_cap());
+            launch_spmv(A, alpha, m->bx[b].p, beta, m->by[b].p, sk);
+            set_spmv_cta_cap(-1);
+            CK(cudaEventRecord(m->ev_k[b], sk));
+            CK(cudaStreamWaitEvent(sd, m->ev_k[b], 0));
+            CK(cudaMemcpyAsync(y + k * ny, m->by[b].p, sizeof(double) * ny, cudaMemcpyDeviceToHost, sd));
+            CK(cudaEventRecord(m->ev_d[b], sd));
         }
         for (cudaStream_t q : m->bs) CK(cudaStreamSynchronize(q));
     });

@@ -57,6 +57,9 @@ void launch_residual(const Bsr3 &A, const double *f, const double *u, double *r,
 // u_out = u + M (f - A u)  (one smoothing sweep, relaxation.hpp:165-173)
 void launch_smooth(const Bsr3 &A, const Smoother &M, const double *f, const double *u,
                    double *u_out, cudaStream_t s, bool lowp = false);
+// cap on the persistent SpMV's CTAs for this host thread (-1: default /
+// SAMG_TMA_CTAS, 0: one per SM)
+void set_spmv_cta_cap(int ctas);
 // fp32 copy of the values (A.val32) for the mixed-precision V-cycle
 void make_lowp(Bsr3 &A, cudaStream_t s);
 // u = M f  (one sweep from a zero guess: the residual is f exactly)

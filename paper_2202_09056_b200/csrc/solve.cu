@@ -634,6 +634,15 @@ void dispatch_tma_shape(int G, F f) {
     }
 }
 
+// CTA cap for the persistent SpMV (0 = one per SM): the host-vector
+// pipeline leaves HBM headroom for the concurrent PCIe copies this way
+thread_local int g_tma_cta_cap = -1;
+int tma_cta_cap() {
+    if (g_tma_cta_cap >= 0) return g_tma_cta_cap;
+    static const int env = env_int("SAMG_TMA_CTAS", 0);
+    return env;
+}
+
 template <bool kReduce, class VT, class Epi>
 bool launch_tma(const Bsr3 &A, const VT *val, const double *x, Epi epi, double *partials,
                 CgScalars *sc, int what, cudaStream_t s) {
@@ -700,7 +709,8 @@ bool launch_tma(const Bsr3 &A, const VT *val, const double *x, Epi epi, double *
         if (smem > max_dyn) return;
         int occ = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
-        const int grid = std::max(1, std::min(cfg.nchunks, std::max(1, occ) * sms));
+        int grid = std::max(1, std::min(cfg.nchunks, std::max(1, occ) * sms));
+        if (tma_cta_cap() > 0) grid = std::min(grid, tma_cta_cap());
         static const int blocked = env_int("SAMG_TMA_BLOCKED", 0);
         cfg.per_cta = blocked ? (cfg.nchunks + grid - 1) / grid : 0;
         kern<<<grid, threads, smem, s>>>(cfg, A.ptr.p, A.col.p, val, x, epi, partials, sc, what);
@@ -908,6 +918,8 @@ int vec_grid(int64_t n) {
 }
 
 } // namespace
+
+void set_spmv_cta_cap(int ctas) { g_tma_cta_cap = ctas; }
 
 void launch_spmv(const Bsr3 &A, double alpha, const double *x, double beta, double *y,
                  cudaStream_t s, bool lowp) {
