@@ -549,6 +549,9 @@ def run_dist_amg(args, rank, world, local, dist):
 
 def main():
     args = parse()
+    # NCCL's own log lines ("NCCL version ...") go to stderr: stdout carries
+    # exactly one JSON line
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     rank, world, local, dist = dist_init(args)
     try:
         if args.impl == "reference":

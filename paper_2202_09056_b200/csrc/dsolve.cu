@@ -34,6 +34,8 @@
 #include <memory>
 #include <vector>
 
+#include <cub/cub.cuh>
+
 #include "hierarchy.cuh"
 
 namespace samgb {
@@ -68,16 +70,7 @@ __global__ void k_sum_tmp(ScSet s) {
     for (int i = 0; i < s.n; ++i) s.p[i]->tmp = t;
 }
 
-std::vector<int> download_int(const DevBuf<int> &b, size_t n, cudaStream_t s) {
-    std::vector<int> h(n);
-    if (n) CK(cudaMemcpyAsync(h.data(), b.p, sizeof(int) * n, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    return h;
-}
 
-int owner(const std::vector<int64_t> &starts, int64_t g) {
-    return static_cast<int>(std::upper_bound(starts.begin(), starts.end(), g) - starts.begin()) - 1;
-}
 
 void d2d(double *dst, const double *src, int64_t n, cudaStream_t s) {
     if (n > 0) CK(cudaMemcpyAsync(dst, src, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
@@ -122,74 +115,144 @@ struct LocalMat {
     HaloPlan plan;
 };
 
-// Build rank r's slice of the matrix (host structure hptr/hcol, device
-// values dval) whose rows are partitioned by row_starts and whose column
-// space is partitioned by col_starts.
-void build_local(const std::vector<int> &hptr, const std::vector<int> &hcol, const double *dval,
-                 const std::vector<int64_t> &row_starts, const std::vector<int64_t> &col_starts,
-                 int rank, bool global_cols, int64_t ncols_global, LocalMat &out, cudaStream_t s) {
+// ---- slicing on the device -------------------------------------------------
+__global__ void k_gather_ptr(int n, const int64_t *idx, const int *ptr, int *out) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < n) out[q] = ptr[idx[q]];
+}
+// flag[c - lo] = 1 for every column c of cols[0, n) with (inside ? lo <= c < hi : c outside [lo, hi))
+__global__ void k_mark_cols(int64_t n, const int *cols, int64_t lo, int64_t hi, bool inside, int *flag) {
+    for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < n;
+         j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t c = cols[j];
+        const bool in = c >= lo && c < hi;
+        if (in == inside) flag[inside ? c - lo : c] = 1;
+    }
+}
+// out[scan[k]] = k for flagged k (the flagged positions in ascending order)
+__global__ void k_compact(int64_t n, const int *flag, const int *scan, int *out) {
+    for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        if (flag[k]) out[scan[k]] = static_cast<int>(k);
+}
+__global__ void k_rebase_ptr(int64_t n, const int *ptr, int base, int *out) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        out[i] = ptr[i] - base;
+}
+// owned column c -> c - c0; ghost -> nloc + (rank of c among the ghosts)
+__global__ void k_renumber(int64_t n, const int *cols, int64_t c0, int64_t c1, int64_t nloc,
+                           const int *gscan, bool global_cols, int *out) {
+    for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < n;
+         j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t c = cols[j];
+        out[j] = static_cast<int>(global_cols ? c : (c >= c0 && c < c1 ? c - c0 : nloc + gscan[c]));
+    }
+}
+
+int grid_of(int64_t n) { return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(4096, (n + 255) / 256))); }
+
+// exclusive scan of flag[0, n) into scan[0, n] (scan[n] = total), on s
+int64_t scan_flags(const int *flag, int *scan, int64_t n, cudaStream_t s) {
+    size_t bytes = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, flag, scan, n + 1, s));
+    DevBuf<char> ws(bytes + 1, s);
+    CK(cub::DeviceScan::ExclusiveSum(ws.p, bytes, flag, scan, n + 1, s));
+    int total = 0;
+    CK(cudaMemcpyAsync(&total, scan + n, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return total;
+}
+
+// Rank r's slice of the (device, global) matrix G whose rows are partitioned
+// by row_starts and whose column space is partitioned by col_starts: rows
+// [r0, r1) with columns renumbered into the halo-extended vector (owned
+// first, then the ghosts in ascending global id, i.e. grouped by owner), the
+// receive plan (ghost counts per owner) and the send plan (the owned columns
+// every other rank's slice reads, ascending).  All on the device: flag
+// arrays + scans, O(nnz + ncols) per rank, a few scalars to the host.
+void build_local(const Bsr3 &G, const std::vector<int64_t> &row_starts,
+                 const std::vector<int64_t> &col_starts, int rank, bool global_cols,
+                 LocalMat &out, cudaStream_t s) {
     const int nranks = static_cast<int>(row_starts.size()) - 1;
+    // the row bounds of every rank's slice
+    std::vector<int> bnd(nranks + 1);
+    {
+        DevBuf<int64_t> ridx(nranks + 1, s);
+        DevBuf<int> rb(nranks + 1, s);
+        CK(cudaMemcpyAsync(ridx.p, row_starts.data(), sizeof(int64_t) * (nranks + 1), cudaMemcpyHostToDevice, s));
+        k_gather_ptr<<<1, 32, 0, s>>>(nranks + 1, ridx.p, G.ptr.p, rb.p);
+        CK(cudaMemcpyAsync(bnd.data(), rb.p, sizeof(int) * (nranks + 1), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    }
     const int64_t r0 = row_starts[rank], r1 = row_starts[rank + 1];
     const int64_t c0 = col_starts[rank], c1 = col_starts[rank + 1];
-    const int64_t nl = r1 - r0, base = hptr[r0], nnz = hptr[r1] - base;
+    const int64_t nl = r1 - r0, base = bnd[rank], nnz = bnd[rank + 1] - base;
+    const int64_t ncg = G.ncols;
     HaloPlan &pl = out.plan;
-    std::vector<int64_t> ghost;
+    DevBuf<int> gscan;
     if (!global_cols) {
-        for (int64_t j = base; j < base + nnz; ++j)
-            if (hcol[j] < c0 || hcol[j] >= c1) ghost.push_back(hcol[j]);
-        std::sort(ghost.begin(), ghost.end());
-        ghost.erase(std::unique(ghost.begin(), ghost.end()), ghost.end());
         pl.nloc = c1 - c0;
-        pl.nghost = static_cast<int64_t>(ghost.size());
-        for (int64_t k = 0; k < pl.nghost;) {
-            const int q = owner(col_starts, ghost[k]);
-            int64_t e = k;
-            while (e < pl.nghost && ghost[e] < col_starts[q + 1]) ++e;
-            pl.recv_peers.push_back(q);
-            pl.recv_counts.push_back(e - k);
-            pl.recv_offsets.push_back(k);
-            k = e;
+        // ghosts: flags over the global column space, scanned
+        DevBuf<int> gflag(ncg + 1, s);
+        gscan.alloc(ncg + 1, s);
+        CK(cudaMemsetAsync(gflag.p, 0, sizeof(int) * (ncg + 1), s));
+        if (nnz) k_mark_cols<<<grid_of(nnz), 256, 0, s>>>(nnz, G.col.p + base, c0, c1, false, gflag.p);
+        pl.nghost = scan_flags(gflag.p, gscan.p, ncg, s);
+        // receive plan: ghosts per owner = scan differences at the owners' bounds
+        std::vector<int> at(nranks + 1);
+        {
+            DevBuf<int64_t> cidx(nranks + 1, s);
+            DevBuf<int> cv(nranks + 1, s);
+            CK(cudaMemcpyAsync(cidx.p, col_starts.data(), sizeof(int64_t) * (nranks + 1), cudaMemcpyHostToDevice, s));
+            k_gather_ptr<<<1, 32, 0, s>>>(nranks + 1, cidx.p, gscan.p, cv.p);
+            CK(cudaMemcpyAsync(at.data(), cv.p, sizeof(int) * (nranks + 1), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
         }
-        // send side: what every other rank's slice reads from my columns
-        std::vector<int> sidx;
-        std::vector<int64_t> need;
+        for (int q = 0; q < nranks; ++q)
+            if (at[q + 1] > at[q]) {
+                pl.recv_peers.push_back(q);
+                pl.recv_counts.push_back(at[q + 1] - at[q]);
+                pl.recv_offsets.push_back(at[q]);
+            }
+        // send plan: for every other rank, the owned columns its rows read
+        const int64_t nown = c1 - c0;
+        DevBuf<int> sflag(nown + 1, s), sscan(nown + 1, s);
+        std::vector<DevBuf<int>> parts;
+        int64_t total = 0;
         for (int q = 0; q < nranks; ++q) {
             if (q == rank) continue;
-            need.clear();
-            for (int64_t j = hptr[row_starts[q]]; j < hptr[row_starts[q + 1]]; ++j)
-                if (hcol[j] >= c0 && hcol[j] < c1) need.push_back(hcol[j]);
-            if (need.empty()) continue;
-            std::sort(need.begin(), need.end());
-            need.erase(std::unique(need.begin(), need.end()), need.end());
+            const int64_t qb = bnd[q], qn = bnd[q + 1] - bnd[q];
+            if (!qn || !nown) continue;
+            CK(cudaMemsetAsync(sflag.p, 0, sizeof(int) * (nown + 1), s));
+            k_mark_cols<<<grid_of(qn), 256, 0, s>>>(qn, G.col.p + qb, c0, c1, true, sflag.p);
+            const int64_t cnt = scan_flags(sflag.p, sscan.p, nown, s);
+            if (!cnt) continue;
+            parts.emplace_back(cnt, s);
+            k_compact<<<grid_of(nown), 256, 0, s>>>(nown, sflag.p, sscan.p, parts.back().p);
             pl.send_peers.push_back(q);
-            pl.send_counts.push_back(static_cast<int64_t>(need.size()));
-            pl.send_offsets.push_back(static_cast<int64_t>(sidx.size()));
-            for (int64_t g : need) sidx.push_back(static_cast<int>(g - c0));
+            pl.send_counts.push_back(cnt);
+            pl.send_offsets.push_back(total);
+            total += cnt;
         }
-        pl.send_idx.alloc(sidx.size(), s);
-        if (!sidx.empty())
-            CK(cudaMemcpyAsync(pl.send_idx.p, sidx.data(), sizeof(int) * sidx.size(),
-                               cudaMemcpyHostToDevice, s));
-        pl.sendbuf.alloc(3 * sidx.size() + 3, s);
+        pl.send_idx.alloc(total, s);
+        for (size_t k = 0; k < parts.size(); ++k)
+            CK(cudaMemcpyAsync(pl.send_idx.p + pl.send_offsets[k], parts[k].p, sizeof(int) * pl.send_counts[k],
+                               cudaMemcpyDeviceToDevice, s));
+        pl.sendbuf.alloc(3 * total + 3, s);
     } else {
-        pl.nloc = ncols_global;
+        pl.nloc = ncg;
     }
     Bsr3 &A = out.A;
-    A.alloc(nl, global_cols ? ncols_global : pl.nloc + pl.nghost, nnz, s);
-    std::vector<int> p32(nl + 1), c32(nnz);
-    for (int64_t i = 0; i <= nl; ++i) p32[i] = static_cast<int>(hptr[r0 + i] - base);
-    for (int64_t j = 0; j < nnz; ++j) {
-        const int64_t c = hcol[base + j];
-        if (global_cols || (c >= c0 && c < c1)) c32[j] = static_cast<int>(global_cols ? c : c - c0);
-        else c32[j] = static_cast<int>(pl.nloc + (std::lower_bound(ghost.begin(), ghost.end(), c) - ghost.begin()));
-    }
-    CK(cudaMemcpyAsync(A.ptr.p, p32.data(), sizeof(int) * (nl + 1), cudaMemcpyHostToDevice, s));
+    A.alloc(nl, global_cols ? ncg : pl.nloc + pl.nghost, nnz, s);
+    k_rebase_ptr<<<grid_of(nl + 1), 256, 0, s>>>(nl + 1, G.ptr.p + r0, static_cast<int>(base), A.ptr.p);
     if (nnz) {
-        CK(cudaMemcpyAsync(A.col.p, c32.data(), sizeof(int) * nnz, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(A.val.p, dval + 9 * base, sizeof(double) * 9 * nnz,
-                           cudaMemcpyDeviceToDevice, s));
+        k_renumber<<<grid_of(nnz), 256, 0, s>>>(nnz, G.col.p + base, c0, c1, pl.nloc, gscan.p, global_cols,
+                                               A.col.p);
+        CK(cudaMemcpyAsync(A.val.p, G.val.p + 9 * base, sizeof(double) * 9 * nnz, cudaMemcpyDeviceToDevice, s));
     }
-    CK(cudaStreamSynchronize(s));  // host vectors above go out of scope
+    CK_LAUNCH();
+    CK(cudaStreamSynchronize(s));  // the temporaries above are freed on s
 }
 
 struct DLevel {
@@ -460,9 +523,20 @@ DHierarchy *dsetup(std::unique_ptr<Hierarchy> H, ncclComm_t comm, int nranks,
         // pipeline, 2 on ns coarse levels (pbs 6)
         const int64_t h = lv.nnodes ? lv.A.nrows / lv.nnodes : 1;
         const int64_t kb = lv.naggs ? lv.P.ncols / lv.naggs : 2;
-        const std::vector<int> seedno = download_int(lv.seedno, lv.nnodes + 1, s);
+        // seedno at the partition bounds only (nranks + 1 values)
+        std::vector<int64_t> nidx(nranks + 1);
+        for (int q = 0; q <= nranks; ++q) nidx[q] = st[l][q] / h;
+        std::vector<int> sn(nranks + 1);
+        {
+            DevBuf<int64_t> di(nranks + 1, s);
+            DevBuf<int> dv(nranks + 1, s);
+            CK(cudaMemcpyAsync(di.p, nidx.data(), sizeof(int64_t) * (nranks + 1), cudaMemcpyHostToDevice, s));
+            k_gather_ptr<<<1, 32, 0, s>>>(nranks + 1, di.p, lv.seedno.p, dv.p);
+            CK(cudaMemcpyAsync(sn.data(), dv.p, sizeof(int) * (nranks + 1), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+        }
         std::vector<int64_t> cst(nranks + 1);
-        for (int q = 0; q <= nranks; ++q) cst[q] = kb * seedno[st[l][q] / h];
+        for (int q = 0; q <= nranks; ++q) cst[q] = kb * sn[q];
         st.push_back(cst);
         // level l+1 is partitioned too if it is not the coarsest, large
         // enough, and gives every rank at least one row
@@ -485,18 +559,12 @@ DHierarchy *dsetup(std::unique_ptr<Hierarchy> H, ncclComm_t comm, int nranks,
         Level &lv = H->levels[l];
         const std::vector<int64_t> &fst = st[l], &cst = st[l + 1];
         const bool next_replicated = l + 1 == Ld;
-        const std::vector<int> ap = download_int(lv.A.ptr, lv.A.nrows + 1, s);
-        const std::vector<int> ac = download_int(lv.A.col, lv.A.nnzb, s);
-        const std::vector<int> rp = download_int(lv.R.ptr, lv.R.nrows + 1, s);
-        const std::vector<int> rc = download_int(lv.R.col, lv.R.nnzb, s);
-        const std::vector<int> pp = download_int(lv.P.ptr, lv.P.nrows + 1, s);
-        const std::vector<int> pc = download_int(lv.P.col, lv.P.nnzb, s);
         const int per = lv.M.kind == SM_POINT ? 3 : 9;
         for (DRank &R : D->ranks) {
             DLevel &dlv = R.dl[l];
-            build_local(ap, ac, lv.A.val.p, fst, fst, R.rank, false, lv.A.ncols, dlv.A, s);
-            build_local(rp, rc, lv.R.val.p, cst, fst, R.rank, false, lv.R.ncols, dlv.R, s);
-            build_local(pp, pc, lv.P.val.p, fst, cst, R.rank, next_replicated, lv.P.ncols, dlv.P, s);
+            build_local(lv.A, fst, fst, R.rank, false, dlv.A, s);
+            build_local(lv.R, cst, fst, R.rank, false, dlv.R, s);
+            build_local(lv.P, fst, cst, R.rank, next_replicated, dlv.P, s);
             const int64_t f0 = fst[R.rank], nl = fst[R.rank + 1] - f0;
             dlv.M.kind = lv.M.kind;
             dlv.M.data.alloc(per * nl + 1, s);
