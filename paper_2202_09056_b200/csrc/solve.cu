@@ -590,6 +590,9 @@ int choose_group(const Bsr3 &A) {
     const double want = bpr / per_lane;
     int G = 1;
     while (G < 32 && G < want) G *= 2;
+    // long rows (C1's A1, ~102 blocks): a full warp per row beats two rows
+    // per warp (33.8 vs 35.7 us, scripts/solve_sweep.sh)
+    if (bpr >= 64.0 && G < 32 && forced == 0) G = 32;
     // small (coarse-level / restriction) matrices cannot fill 148 SMs:
     // spend more lanes per row to shorten the serial chains instead
     // (R1 of C1: 3 822 rows; 8 lanes -> 40 us, 32 lanes -> ~6 us)
@@ -810,9 +813,14 @@ __global__ void k_smooth_zero_block(int64_t nrows, const double *__restrict__ m,
 
 // u = Ainv f, Ainv row-major with an even leading dimension (zero padded):
 // one 128-thread CTA per row, 16-byte loads, 4 in flight per thread.
-__global__ void __launch_bounds__(128) k_dense_gemv(int n, int64_t ld, const double *__restrict__ A,
+// One 64-thread CTA per row: 2 922 rows at C1 fit in one wave (32 resident
+// CTAs per SM; 128-thread CTAs needed 1.23 waves, 20.4 us -> see profiles/),
+// eight 16-byte loads in flight per thread.
+constexpr int kGemvThreads = 64;
+__global__ void __launch_bounds__(kGemvThreads) k_dense_gemv(int n, int64_t ld, const double *__restrict__ A,
         const double *__restrict__ f, double *__restrict__ u) {
-    __shared__ double red[4];
+    constexpr int T = kGemvThreads;
+    __shared__ double red[T / 32];
     const int row = blockIdx.x;
     const double2 *a = reinterpret_cast<const double2 *>(A + static_cast<size_t>(row) * ld);
     const int n2 = static_cast<int>(ld / 2);
@@ -822,16 +830,18 @@ __global__ void __launch_bounds__(128) k_dense_gemv(int n, int64_t ld, const dou
         return make_double2(__ldg(f + j), j + 1 < n ? __ldg(f + j + 1) : 0.0);
     };
     int j2 = threadIdx.x;
-    for (; j2 + 384 < n2; j2 += 512) {
-        const double2 a0 = __ldcs(a + j2), a1 = __ldcs(a + j2 + 128), a2 = __ldcs(a + j2 + 256),
-                      a3 = __ldcs(a + j2 + 384);
-        const double2 f0 = fpair(j2), f1 = fpair(j2 + 128), f2 = fpair(j2 + 256), f3 = fpair(j2 + 384);
-        s = fma(a0.x, f0.x, s); t = fma(a0.y, f0.y, t);
-        s = fma(a1.x, f1.x, s); t = fma(a1.y, f1.y, t);
-        s = fma(a2.x, f2.x, s); t = fma(a2.y, f2.y, t);
-        s = fma(a3.x, f3.x, s); t = fma(a3.y, f3.y, t);
+    for (; j2 + 7 * T < n2; j2 += 8 * T) {
+        double2 av[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) av[k] = __ldcs(a + j2 + k * T);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const double2 fk = fpair(j2 + k * T);
+            s = fma(av[k].x, fk.x, s);
+            t = fma(av[k].y, fk.y, t);
+        }
     }
-    for (; j2 < n2; j2 += 128) {
+    for (; j2 < n2; j2 += T) {
         const double2 a0 = __ldcs(a + j2);
         const double2 f0 = fpair(j2);
         s = fma(a0.x, f0.x, s); t = fma(a0.y, f0.y, t);
@@ -841,7 +851,7 @@ __global__ void __launch_bounds__(128) k_dense_gemv(int n, int64_t ld, const dou
     for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
     if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = s;
     __syncthreads();
-    if (threadIdx.x == 0) u[row] = (red[0] + red[1]) + (red[2] + red[3]);
+    if (threadIdx.x == 0) u[row] = red[0] + red[1];
 }
 
 // Vector kernels: 2 elements per thread per step (16-byte loads; the
@@ -991,7 +1001,7 @@ void make_lowp(Bsr3 &A, cudaStream_t s) {
 void launch_dense_gemv(int64_t n, const double *Ainv, const double *f, double *u,
                        cudaStream_t s) {
     if (n == 0) return;
-    k_dense_gemv<<<static_cast<int>(n), 128, 0, s>>>(static_cast<int>(n), dense_ld(n), Ainv, f, u);
+    k_dense_gemv<<<static_cast<int>(n), kGemvThreads, 0, s>>>(static_cast<int>(n), dense_ld(n), Ainv, f, u);
     CK_LAUNCH();
 }
 
