@@ -106,6 +106,36 @@ Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int6
         t_mark = t;
     };
     mark("upload", 0);
+    // Grow the stream-ordered pool once to the setup's working set (the
+    // level-0 Galerkin intermediate R*A alone is ~1.1x A_0): growing it piece
+    // by piece inside the level loop maps fresh physical memory per
+    // allocation (C4: 0.1-0.5 s per Galerkin allocation).  The pool keeps it
+    // (release threshold = max), so later setups reuse it.
+    {
+        static const double factor = [] {
+            const char *e = std::getenv("SAMG_POOL_RESERVE");
+            return e ? std::atof(e) : 2.5;
+        }();
+        const double a_bytes = static_cast<double>(A0.nnzb) * 76.0 + 4.0 * A0.nrows;
+        if (factor > 0.0 && a_bytes * factor > 64.0 * (1 << 20)) {
+            cudaMemPool_t pool;
+            CK(cudaDeviceGetDefaultMemPool(&pool, H->device));
+            uint64_t reserved = 0, used = 0;
+            CK(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
+            CK(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
+            size_t free_b = 0, total_b = 0;
+            CK(cudaMemGetInfo(&free_b, &total_b));
+            const double want = std::min(a_bytes * factor, 0.7 * static_cast<double>(free_b + (reserved - used)));
+            if (want > static_cast<double>(reserved - used)) {
+                void *tmp = nullptr;
+                if (cudaMallocAsync(&tmp, static_cast<size_t>(want), s) == cudaSuccess)
+                    CK(cudaFreeAsync(tmp, s));
+                else
+                    cudaGetLastError();
+            }
+        }
+        mark("pool", 0);
+    }
     const bool block = pipeline == SAMG_PIPELINE_BLOCK;  // no nullspace
     const int k = block ? 0 : static_cast<int>(b_cols);
     DevBuf<double> B;
@@ -140,10 +170,8 @@ Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int6
                 break;
             Bsr3 R;
             transpose(P, R, s);
-            Bsr3 RA, Ac;
-            spgemm(R, Li.A, RA, s);
-            spgemm(RA, P, Ac, s);
-            RA = Bsr3();
+            Bsr3 Ac;
+            galerkin(R, Li.A, P, Ac, s);
             fix_decoupled_rows(Ac, s);
             mark("galerkin", lvl);
             Li.P = std::move(P);
@@ -186,13 +214,10 @@ Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int6
         transpose(P, R, s);
         mark("transpose", lvl);
         // Galerkin (csr.hpp:259-262) + fix_decoupled_rows (hierarchy.hpp:357)
-        Bsr3 RA, Ac;
-        spgemm(R, Li.A, RA, s, scalar_galerkin);
-        mark("spgemm_RA", lvl);
-        spgemm(RA, P, Ac, s, scalar_galerkin);
-        RA = Bsr3();
+        Bsr3 Ac;
+        galerkin(R, Li.A, P, Ac, s, scalar_galerkin);
         fix_decoupled_rows(Ac, s);
-        mark("spgemm_RAP", lvl);
+        mark("galerkin", lvl);
         Li.P = std::move(P);
         Li.R = std::move(R);
         Li.has_transfer = true;

@@ -146,6 +146,9 @@ void transpose(const Bsr3 &P, Bsr3 &R, cudaStream_t s);
 // scalar views (csr<double>: every scalar term added to the accumulator in
 // (ja, q) order) -- the hybrids' scalar Galerkin, hierarchy.hpp:233-260
 void spgemm(const Bsr3 &A, const Bsr3 &B, Bsr3 &C, cudaStream_t s, bool scalar_order = false);
+// A_c = (R A) P with R = P^T exactly (the hierarchy's transfer operators)
+void galerkin(const Bsr3 &R, const Bsr3 &A, const Bsr3 &P, Bsr3 &Ac, cudaStream_t s,
+              bool scalar_order = false);
 void fix_decoupled_rows(Bsr3 &A, cudaStream_t s);
 // smoother setup: kind SAMG_SMOOTHER_*
 void setup_smoother(const Bsr3 &A, int kind, double omega, Smoother &M, DevError *err,

@@ -25,7 +25,12 @@
 
 #include <cub/cub.cuh>
 
+// the pattern-only (kCols) instances return before the accumulation loops
+#pragma nv_diag_suppress 128
+
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -752,7 +757,7 @@ __global__ void k_spgemm_count(int nrows, const int *rows, const int *ap, const 
     }
 }
 
-template <bool GLOBAL, bool kScalar>
+template <bool GLOBAL, bool kScalar, bool kCols = false>
 __global__ void __launch_bounds__(256) k_spgemm_numeric(
         int nrows, const int *rows, const int *ap, const int *ac, const double *av,
         const int *bp, const int *bc, const double *bv, int cap, int *keys_g, int *vals_g,
@@ -802,6 +807,10 @@ __global__ void __launch_bounds__(256) k_spgemm_numeric(
             __syncthreads();
         }
     const int64_t base = cp[row];
+    if constexpr (kCols) {  // pattern only: values come from k_spgemm_pull
+        for (int t = threadIdx.x; t < n; t += blockDim.x) ccol[base + t] = list[t];
+        return;
+    }
     for (int t = threadIdx.x; t < n; t += blockDim.x) {
         const int key = list[t];
         ccol[base + t] = key;
@@ -858,7 +867,7 @@ __global__ void __launch_bounds__(256) k_spgemm_wcount(int nrows, const int *row
     if (lane == 0) cnt[row] = full ? -1 : n_all[w];
 }
 
-template <bool kScalar>
+template <bool kScalar, bool kCols = false>
 __global__ void __launch_bounds__(256) k_spgemm_wnumeric(
         int nrows, const int *ap, const int *ac, const double *av, const int *bp, const int *bc,
         const double *bv, const int *cp, const int *mode, int *ccol, double *cval) {
@@ -906,6 +915,10 @@ __global__ void __launch_bounds__(256) k_spgemm_wnumeric(
             __syncwarp();
         }
     const int64_t base = cp[row];
+    if constexpr (kCols) {  // pattern only: values come from k_spgemm_pull
+        for (int t = lane; t < n; t += 32) ccol[base + t] = list[t];
+        return;
+    }
     for (int t = lane; t < n; t += 32) {
         const int key = list[t];
         ccol[base + t] = key;
@@ -1033,7 +1046,7 @@ __global__ void __launch_bounds__(kBWPB * 32) k_spgemm_bcount(int nrows, const i
 
 // numeric pass for the bitmap rows (cnt >= 0 from k_spgemm_bcount; rows
 // marked -2 there are skipped here, the hash kernels do them)
-template <bool kScalar>
+template <bool kScalar, bool kCols = false>
 __global__ void __launch_bounds__(kBWPB * 32) k_spgemm_bnumeric(int nrows, const int *ap,
         const int *ac, const double *av, const int *bp, const int *bc, const double *bv,
         const int *cp, const int *mode, const int *win_lo, int words, int acc_cap, int *ccol,
@@ -1076,6 +1089,7 @@ __global__ void __launch_bounds__(kBWPB * 32) k_spgemm_bnumeric(int nrows, const
             ccol[base + run++] = cmin + (wd << 5) + b;
         }
     }
+    if constexpr (kCols) return;  // pattern only: values come from k_spgemm_pull
     const bool in_smem = n <= acc_cap;
     double *acc = in_smem ? acc_s : cval + 9 * base;
     for (int e = lane; e < 9 * n; e += 32) acc[e] = 0.0;
@@ -1122,6 +1136,120 @@ __global__ void __launch_bounds__(kBWPB * 32) k_spgemm_bnumeric(int nrows, const
     }
     if (in_smem)
         for (int e = lane; e < 9 * n; e += 32) cval[9 * base + e] = acc_s[e];
+}
+
+// ---------------------------------------------------------------------------
+// Pull (inner-product) numeric pass over a known output pattern.  Output
+// block (i, c) = sum over the entries of B's column c in ascending row j of
+// A(i, j) * B(j, c), restricted to the j present in A's row i.  The reference
+// accumulates (i, c) over A's row entries in ascending column order
+// (csr.hpp:231-243), i.e. ascending j as well, so every output block gets
+// the same terms in the same order as in the row-by-row (push) kernels --
+// bit-identical -- but no output depends on another: no in-order chain along
+// the row, no shared or global accumulators, every thread owns its outputs.
+// A's row i is a shared-memory hash (column -> position); B's columns come
+// from BCols (A itself for a structurally symmetric level matrix, through the
+// transpose positions; R = P^T for P, through its block transposes).
+struct BCols {
+    const int *cp = nullptr, *ri = nullptr, *pos = nullptr;
+    const double *val = nullptr;
+    bool tr = false;  // stored block is B(j, c)^T (R's blocks for P)
+};
+
+template <bool kScalar, bool kTr, int NT, int BATCH>
+__global__ void __launch_bounds__(NT) k_spgemm_pull(int nrows, int tcap, const int *__restrict__ ap,
+        const int *__restrict__ ac, const double *__restrict__ av, BCols bc,
+        const int *__restrict__ mode, const int *__restrict__ cp, const int *__restrict__ ccol,
+        double *__restrict__ cval) {
+    extern __shared__ int psm[];
+    int *keys = psm, *vals = psm + tcap;
+    const int row = blockIdx.x;
+    if (row >= nrows || mode[row] == 2) return;  // 2: global-table rows (k_spgemm_numeric<true>)
+    const int64_t base = cp[row];
+    const int n = cp[row + 1] - cp[row];
+    if (n == 0) return;
+    for (int t = threadIdx.x; t < tcap; t += NT) keys[t] = -1;
+    __syncthreads();
+    const int a0 = ap[row], na = ap[row + 1] - a0;
+    for (int t = threadIdx.x; t < na; t += NT) {
+        bool ins;
+        const int slot = hash_insert(keys, tcap, ac[a0 + t], ins);
+        vals[slot] = t;
+    }
+    __syncthreads();
+    const int *__restrict__ bcp = bc.cp;
+    const int *__restrict__ bri = bc.ri;
+    const int *__restrict__ bpos = bc.pos;
+    const double *__restrict__ bval = bc.val;
+    for (int t = threadIdx.x; t < n; t += NT) {
+        const int c = ccol[base + t];
+        double acc[9];
+#pragma unroll
+        for (int e = 0; e < 9; ++e) acc[e] = 0.0;
+        const int e1 = bcp[c + 1];
+        // batches of BATCH column entries: the index loads, then the B blocks
+        // of the hits are issued together (memory-level parallelism), then
+        // the hits are accumulated in ascending row order
+        for (int e = bcp[c]; e < e1; e += BATCH) {
+            int ja[BATCH], qq[BATCH];
+#pragma unroll
+            for (int u = 0; u < BATCH; ++u) {
+                const int ee = e + u;
+                const bool in = ee < e1;
+                const int j = in ? bri[ee] : -1;
+                qq[u] = in ? (bpos ? bpos[ee] : ee) : 0;
+                ja[u] = j;
+            }
+#pragma unroll
+            for (int u = 0; u < BATCH; ++u) {
+                const int slot = ja[u] >= 0 ? hash_find(keys, tcap, ja[u]) : -1;
+                ja[u] = slot >= 0 ? vals[slot] : -1;
+            }
+            double bm[BATCH][9];
+#pragma unroll
+            for (int u = 0; u < BATCH; ++u)
+                if (ja[u] >= 0) {
+                    const double *b = bval + 9 * static_cast<int64_t>(qq[u]);
+#pragma unroll
+                    for (int q = 0; q < 9; ++q) bm[u][q] = b[q];
+                }
+#pragma unroll
+            for (int u = 0; u < BATCH; ++u)
+                if (ja[u] >= 0) {
+                    const double *a = av + 9 * static_cast<int64_t>(a0 + ja[u]);
+                    double am[9], bt[9];
+#pragma unroll
+                    for (int q = 0; q < 9; ++q) am[q] = a[q];
+#pragma unroll
+                    for (int r = 0; r < 3; ++r)
+#pragma unroll
+                        for (int q = 0; q < 3; ++q) bt[r * 3 + q] = kTr ? bm[u][q * 3 + r] : bm[u][r * 3 + q];
+                    accum_block<kScalar>(am, bt, acc);
+                }
+        }
+        double *o = cval + 9 * (base + t);
+#pragma unroll
+        for (int q = 0; q < 9; ++q) o[q] = acc[q];
+    }
+}
+
+// Transpose positions of a structurally symmetric BSR pattern: for entry e =
+// (i, j), tpos[e] = the index of entry (j, i); *bad = 1 if one is missing.
+__global__ void k_tpos(int nrows, const int *__restrict__ ptr, const int *__restrict__ col,
+                       int *__restrict__ tpos, int *bad) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nrows) return;
+    for (int e = ptr[i]; e < ptr[i + 1]; ++e) {
+        const int j = col[e];
+        int lo = ptr[j], hi = ptr[j + 1] - 1, found = -1;
+        while (lo <= hi) {
+            const int mid = (lo + hi) >> 1, v = col[mid];
+            if (v == i) { found = mid; break; }
+            if (v < i) lo = mid + 1; else hi = mid - 1;
+        }
+        tpos[e] = found;
+        if (found < 0) *bad = 1;
+    }
 }
 
 __global__ void k_spgemm_ub(int nrows, const int *ap, const int *ac, const int *bp,
@@ -1465,10 +1593,32 @@ void transpose(const Bsr3 &P, Bsr3 &R, cudaStream_t s) {
 }
 
 namespace {
+__global__ void k_max_row_len(int nrows, const int *ptr, int *mx) {
+    int v = 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nrows; i += gridDim.x * blockDim.x)
+        v = max(v, ptr[i + 1] - ptr[i]);
+    v = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(v)));
+    if ((threadIdx.x & 31) == 0) atomicMax(mx, v);
+}
+
 template <bool kScalar>
-void spgemm_impl(const Bsr3 &A, const Bsr3 &B, Bsr3 &C, cudaStream_t s) {
+void spgemm_impl(const Bsr3 &A, const Bsr3 &B, Bsr3 &C, cudaStream_t s, const BCols *bcols) {
     if (A.ncols != B.nrows) fail(SAMG_DIMENSION_MISMATCH, "spgemm: inner dimensions disagree");
     const int n = static_cast<int>(A.nrows);
+    // SAMG_SPGEMM_TIMING=1: sub-phase wall times on stderr (diagnosis only)
+    static const bool timing = [] {
+        const char *e = std::getenv("SAMG_SPGEMM_TIMING");
+        return e && e[0] == '1';
+    }();
+    auto t_last = std::chrono::steady_clock::now();
+    auto mark = [&](const char *what) {
+        if (!timing) return;
+        CK(cudaStreamSynchronize(s));
+        const auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "  spgemm %8d rows %-10s %8.3f ms\n", n, what,
+                     std::chrono::duration<double, std::milli>(t - t_last).count());
+        t_last = t;
+    };
     C.nrows = A.nrows;
     C.ncols = B.ncols;
     C.ptr.alloc(n + 1, s);
@@ -1581,9 +1731,11 @@ void spgemm_impl(const Bsr3 &A, const Bsr3 &B, Bsr3 &C, cudaStream_t s) {
             goff.p, cnt.p, ovf.p);
         CK_LAUNCH();
     }
+    mark("symbolic");
     C.nnzb = scan_counts(cnt.p, C.ptr.p, n, s);
     C.col.alloc(C.nnzb, s);
     C.val.alloc(9 * C.nnzb, s);
+    mark("alloc");
     // numeric: table sized by the actual max row count
     DevBuf<int> mc(1, s);
     size_t b3 = 0;
@@ -1594,6 +1746,26 @@ void spgemm_impl(const Bsr3 &A, const Bsr3 &B, Bsr3 &C, cudaStream_t s) {
     CK(cudaMemcpyAsync(&maxc, mc.p, sizeof maxc, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     const int cap_n = std::min(kMaxCap, std::max(256, next_pow2(2 * static_cast<int64_t>(maxc) + 2)));
+    // pull numeric (k_spgemm_pull) when B's columns are available and A's
+    // longest row fits a shared-memory hash; the row kernels then only write
+    // the pattern (kCols)
+    static const bool pull_env = [] {
+        const char *e = std::getenv("SAMG_SPGEMM_PULL");
+        return !e || e[0] != '0';
+    }();
+    int tcap = 0;
+    if (bcols && pull_env) {
+        DevBuf<int> mxa(1, s);
+        CK(cudaMemsetAsync(mxa.p, 0, sizeof(int), s));
+        k_max_row_len<<<std::min(1184, ceil_div(n, 256)), 256, 0, s>>>(n, A.ptr.p, mxa.p);
+        CK_LAUNCH();
+        int maxa = 0;
+        CK(cudaMemcpyAsync(&maxa, mxa.p, sizeof maxa, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        tcap = std::max(64, next_pow2(2 * static_cast<int64_t>(maxa) + 2));
+        if (tcap > 16384) tcap = 0;  // 128 KB of hash: use the row kernels
+    }
+    const bool pull = tcap > 0;
     const size_t smem_n = static_cast<size_t>(cap_n) * 4 * 2 + static_cast<size_t>(cap_n / 2) * 4;
     // 2a. window-bitmap numeric pass (accumulators in shared memory for rows
     //     of up to acc_cap columns)
@@ -1612,29 +1784,43 @@ void spgemm_impl(const Bsr3 &A, const Bsr3 &B, Bsr3 &C, cudaStream_t s) {
             return true;
         }();
         (void)battr;
-        k_spgemm_bnumeric<kScalar><<<ceil_div(n, kBWPB), kBWPB * 32, smem_b, s>>>(
-            n, A.ptr.p, A.col.p, A.val.p, B.ptr.p, B.col.p, B.val.p, C.ptr.p, mode.p, winlo.p, words,
-            acc_cap, C.col.p, C.val.p);
+        static const bool battr2 = [] {
+            CK(cudaFuncSetAttribute(k_spgemm_bnumeric<kScalar, true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+            return true;
+        }();
+        (void)battr2;
+        if (pull)
+            k_spgemm_bnumeric<kScalar, true><<<ceil_div(n, kBWPB), kBWPB * 32, smem_b, s>>>(
+                n, A.ptr.p, A.col.p, A.val.p, B.ptr.p, B.col.p, B.val.p, C.ptr.p, mode.p, winlo.p, words,
+                acc_cap, C.col.p, C.val.p);
+        else
+            k_spgemm_bnumeric<kScalar><<<ceil_div(n, kBWPB), kBWPB * 32, smem_b, s>>>(
+                n, A.ptr.p, A.col.p, A.val.p, B.ptr.p, B.col.p, B.val.p, C.ptr.p, mode.p, winlo.p, words,
+                acc_cap, C.col.p, C.val.p);
         CK_LAUNCH();
     }
+    mark("bnumeric");
     // 2b. warp-per-row hash numeric pass for the other narrow rows
     if (nfb) {
         const size_t smem_w = static_cast<size_t>(kWPB) * kWCap * 5 / 2 * sizeof(int);
-        CK(cudaFuncSetAttribute(k_spgemm_wnumeric<kScalar>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        auto kw = pull ? k_spgemm_wnumeric<kScalar, true> : k_spgemm_wnumeric<kScalar>;
+        CK(cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem_w)));
-        k_spgemm_wnumeric<kScalar><<<ceil_div(n, kWPB), 256, smem_w, s>>>(n, A.ptr.p, A.col.p, A.val.p, B.ptr.p,
-                                                                 B.col.p, B.val.p, C.ptr.p, mode.p,
-                                                                 C.col.p, C.val.p);
+        kw<<<ceil_div(n, kWPB), 256, smem_w, s>>>(n, A.ptr.p, A.col.p, A.val.p, B.ptr.p,
+                                                  B.col.p, B.val.p, C.ptr.p, mode.p,
+                                                  C.col.p, C.val.p);
         CK_LAUNCH();
     }
+    mark("wnumeric");
     // 3. CTA-per-row numeric pass for the wide rows
     if (nwide) {
-        CK(cudaFuncSetAttribute(k_spgemm_numeric<false, kScalar>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                kMaxCap * 10));
-        k_spgemm_numeric<false, kScalar><<<nwide, 256, smem_n, s>>>(nwide, wide.p, A.ptr.p, A.col.p, A.val.p,
-                                                          B.ptr.p, B.col.p, B.val.p, cap_n, nullptr,
-                                                          nullptr, nullptr, nullptr, C.ptr.p, C.col.p,
-                                                          C.val.p);
+        auto kn = pull ? k_spgemm_numeric<false, kScalar, true> : k_spgemm_numeric<false, kScalar>;
+        CK(cudaFuncSetAttribute(kn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxCap * 10));
+        kn<<<nwide, 256, smem_n, s>>>(nwide, wide.p, A.ptr.p, A.col.p, A.val.p,
+                                      B.ptr.p, B.col.p, B.val.p, cap_n, nullptr,
+                                      nullptr, nullptr, nullptr, C.ptr.p, C.col.p,
+                                      C.val.p);
         CK_LAUNCH();
     }
     if (novf) {
@@ -1643,14 +1829,78 @@ void spgemm_impl(const Bsr3 &A, const Bsr3 &B, Bsr3 &C, cudaStream_t s) {
                                                  B.col.p, B.val.p, 0, gkeys.p, gvals.p, glist.p,
                                                  goff.p, C.ptr.p, C.col.p, C.val.p);
         CK_LAUNCH();
+        if (pull) {  // these rows are complete: the pull pass skips them
+            int *md = mode.p;
+            const int *orw = orows.p;
+            for_each(nr, [=] __device__(int64_t k) { md[orw[k]] = 2; }, s);
+        }
+    }
+    mark("wide");
+    if (pull) {
+        const int smem_p = tcap * 8;
+        // few rows (coarse levels: long rows, many outputs each): more
+        // threads per row
+        const bool wide_cta = n < 148 * 16;
+        // batch: measured on C4 (scripts/setup_phases.py): 1 for the fine
+        // level's 601 526 rows (88 / 100 ms vs 122 / 139 with 4: occupancy),
+        // 4 for level 1's 78 162 (37 / 57 ms vs 40 / 83 with 1)
+        static const int batch_env = [] {
+            const char *e = std::getenv("SAMG_PULL_BATCH");
+            return e ? std::atoi(e) : 0;
+        }();
+        const int batch = batch_env > 0 ? batch_env : (n >= 16384 && n < 200000 ? 4 : 1);
+        using KP = decltype(&k_spgemm_pull<kScalar, true, 128, 1>);
+        KP kp;
+        auto pick = [&](auto bt) {
+            constexpr int BT = decltype(bt)::value;
+            kp = wide_cta ? (bcols->tr ? k_spgemm_pull<kScalar, true, 256, BT> : k_spgemm_pull<kScalar, false, 256, BT>)
+                          : (bcols->tr ? k_spgemm_pull<kScalar, true, 128, BT> : k_spgemm_pull<kScalar, false, 128, BT>);
+        };
+        if (batch >= 4) pick(std::integral_constant<int, 4>{});
+        else if (batch == 2) pick(std::integral_constant<int, 2>{});
+        else pick(std::integral_constant<int, 1>{});
+        if (smem_p > 48 * 1024)
+            CK(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_p));
+        kp<<<n, wide_cta ? 256 : 128, smem_p, s>>>(n, tcap, A.ptr.p, A.col.p, A.val.p, *bcols, mode.p,
+                                                   C.ptr.p, C.col.p, C.val.p);
+        CK_LAUNCH();
+        mark("pull");
     }
 }
 
 } // namespace
 
 void spgemm(const Bsr3 &A, const Bsr3 &B, Bsr3 &C, cudaStream_t s, bool scalar_order) {
-    if (scalar_order) spgemm_impl<true>(A, B, C, s);
-    else spgemm_impl<false>(A, B, C, s);
+    if (scalar_order) spgemm_impl<true>(A, B, C, s, nullptr);
+    else spgemm_impl<false>(A, B, C, s, nullptr);
+}
+
+// Galerkin product A_c = (R A) P (csr.hpp:259-262), both products with the
+// pull numeric pass: B = A through its transpose positions when A's pattern
+// is symmetric (every level matrix: R = P^T), B = P through R's blocks.
+void galerkin(const Bsr3 &R, const Bsr3 &A, const Bsr3 &P, Bsr3 &Ac, cudaStream_t s,
+              bool scalar_order) {
+    Bsr3 RA;
+    {
+        DevBuf<int> tpos(std::max<int64_t>(1, A.nnzb), s), bad(1, s);
+        CK(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
+        if (A.nrows)
+            k_tpos<<<ceil_div(A.nrows, 256), 256, 0, s>>>(static_cast<int>(A.nrows), A.ptr.p, A.col.p,
+                                                          tpos.p, bad.p);
+        CK_LAUNCH();
+        int hbad = 0;
+        CK(cudaMemcpyAsync(&hbad, bad.p, sizeof hbad, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        BCols ba;
+        ba.cp = A.ptr.p; ba.ri = A.col.p; ba.pos = tpos.p; ba.val = A.val.p; ba.tr = false;
+        const BCols *pa = (hbad || A.nrows != A.ncols) ? nullptr : &ba;
+        if (scalar_order) spgemm_impl<true>(R, A, RA, s, pa);
+        else spgemm_impl<false>(R, A, RA, s, pa);
+    }
+    BCols bp;
+    bp.cp = R.ptr.p; bp.ri = R.col.p; bp.pos = nullptr; bp.val = R.val.p; bp.tr = true;
+    if (scalar_order) spgemm_impl<true>(RA, P, Ac, s, &bp);
+    else spgemm_impl<false>(RA, P, Ac, s, &bp);
 }
 
 void fix_decoupled_rows(Bsr3 &A, cudaStream_t s) {
