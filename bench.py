@@ -50,6 +50,21 @@ def parse():
     return ap.parse_args()
 
 
+_OUT_FD = None
+
+
+def emit(line):
+    """The one JSON line, on the real stdout (fd 1 is pointed at stderr for
+    the rest of the run, so library log lines such as NCCL's version banner
+    cannot land on stdout)."""
+    data = (json.dumps(line) + "\n").encode()
+    if _OUT_FD is None:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_OUT_FD, data)
+
+
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -203,7 +218,7 @@ def run_reference(args, rank, world, dist):
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "amg": amg,
     }
-    print(json.dumps(line))
+    emit(line)
 
 
 def run_b200(args, rank, world, local, dist):
@@ -388,7 +403,7 @@ def run_b200(args, rank, world, local, dist):
             "cpu_baseline": cpu,
             "amg": amg,
         }
-        print(json.dumps(line))
+        emit(line)
 
 
 def run_b200_dist(args, rank, world, local, dist):
@@ -469,7 +484,7 @@ def run_b200_dist(args, rank, world, local, dist):
     peak, peak_src = peaks()
     gb_rank = nbytes / (ms_per * 1e-3) / 1e9
     if rank == 0:
-        print(json.dumps({
+        emit({
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -542,6 +557,7 @@ def run_dist_amg(args, rank, world, local, dist):
            "setup_s_all": setups, "solve_s_all": solves, "iterations": rep["iterations"],
            "relative_residual": rep["relative_residual"], "converged": rep["converged"],
            "levels": inf["nlevels"], "partitioned_levels": inf["dist_levels"],
+           "sliced_galerkin_levels": inf["sliced_levels"],
            "problem": "C1 (strong scaling: same global problem on every N)",
            "timing": "wall clock around setup / solve, max over ranks",
            "smoother": "spai0", "input": "host BSR3 upload inside setup_s"}
@@ -554,6 +570,10 @@ def main():
     # NCCL's own log lines ("NCCL version ...") go to stderr: stdout carries
     # exactly one JSON line
     os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    global _OUT_FD
+    sys.stdout.flush()
+    _OUT_FD = os.dup(1)
+    os.dup2(2, 1)
     rank, world, local, dist = dist_init(args)
     try:
         if args.impl == "reference":

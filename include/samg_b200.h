@@ -290,6 +290,16 @@ SAMG_API int samg_dsetup(const unsigned char id[128], int nranks, int rank,
 SAMG_API int samg_ddestroy(samg_dhierarchy *h);
 SAMG_API int samg_dinfo(const samg_dhierarchy *h, int64_t *row0,
         int64_t *row1, int *nlevels, int *dist_levels, double *setup_seconds);
+/* Number of levels whose Galerkin product the setup formed row-sliced across
+ * the ranks (each rank its own coarse rows, then assembled on every rank;
+ * SAMG_DIST_SLICED_GALERKIN=0 disables it).  No reference counterpart. */
+SAMG_API int samg_dsliced_levels(const samg_dhierarchy *h, int *sliced_levels);
+/* Parity taps on the distributed hierarchy's global level matrices (every
+ * rank holds them): as samg_level_info / samg_get_level. */
+SAMG_API int samg_dlevel_info(const samg_dhierarchy *h, int level, int which,
+        int64_t *nrows, int64_t *ncols, int64_t *nnzb);
+SAMG_API int samg_dget_level(const samg_dhierarchy *h, int level, int which,
+        int64_t *ptr, int64_t *col, double *val);
 SAMG_API int samg_dcg_solve_device(samg_dhierarchy *h, const double *d_f,
         double *d_u, const samg_cg_params *prm, samg_solve_report *rep);
 SAMG_API int samg_dcg_solve(samg_dhierarchy *h, const double *f, double *u,

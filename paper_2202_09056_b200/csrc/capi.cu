@@ -63,6 +63,8 @@ samg_solve_report dcg(DHierarchy *d, const double *f, double *u, const samg_cg_p
 void dinfo(const DHierarchy *d, int64_t *row0, int64_t *row1, int *nlevels, int *dist_levels,
            double *setup_s);
 void nccl_unique_id(unsigned char *out);
+int dsliced_levels(const DHierarchy *d);
+const Hierarchy &dfull(const DHierarchy *d);
 }
 
 struct samg_dproblem {
@@ -956,6 +958,34 @@ SAMG_API int samg_dinfo(const samg_dhierarchy *h, int64_t *row0, int64_t *row1, 
     return guarded([&] {
         require(h && h->d, SAMG_INVALID_ARGUMENT, "NULL hierarchy");
         dinfo(h->d, row0, row1, nlevels, dist_levels, setup_s);
+    });
+}
+
+SAMG_API int samg_dsliced_levels(const samg_dhierarchy *h, int *sliced_levels) {
+    return guarded([&] {
+        require(h && h->d && sliced_levels, SAMG_INVALID_ARGUMENT, "NULL argument");
+        *sliced_levels = dsliced_levels(h->d);
+    });
+}
+
+SAMG_API int samg_dlevel_info(const samg_dhierarchy *h, int level, int which, int64_t *nrows,
+                              int64_t *ncols, int64_t *nnzb) {
+    return guarded([&] {
+        require(h && h->d, SAMG_INVALID_ARGUMENT, "NULL hierarchy");
+        const Bsr3 &M = level_mat(dfull(h->d), level, which);
+        *nrows = M.nrows;
+        *ncols = M.ncols;
+        *nnzb = M.nnzb;
+    });
+}
+
+SAMG_API int samg_dget_level(const samg_dhierarchy *h, int level, int which, int64_t *ptr,
+                             int64_t *col, double *val) {
+    return guarded([&] {
+        require(h && h->d, SAMG_INVALID_ARGUMENT, "NULL hierarchy");
+        const samgb::Hierarchy &H = dfull(h->d);
+        CK(cudaSetDevice(H.device));
+        download_bsr3(level_mat(H, level, which), ptr, col, val, H.stream);
     });
 }
 

@@ -116,6 +116,16 @@ struct LocalMat {
 };
 
 // ---- slicing on the device -------------------------------------------------
+__global__ void k_rebase(int64_t n, const int *in, int o, int *out) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        out[i] = in[i] + o;
+}
+void for_each_rebase(int64_t n, const int *in, int o, int *out, cudaStream_t s) {
+    if (n <= 0) return;
+    k_rebase<<<static_cast<int>(std::min<int64_t>(4096, (n + 255) / 256)), 256, 0, s>>>(n, in, o, out);
+    CK_LAUNCH();
+}
 __global__ void k_gather_ptr(int n, const int64_t *idx, const int *ptr, int *out) {
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q < n) out[q] = ptr[idx[q]];
@@ -277,6 +287,7 @@ struct DHierarchy {
     ncclComm_t comm = nullptr;   // nullptr: every rank emulated in this process
     std::unique_ptr<Hierarchy> H;
     size_t Ld = 0;
+    int sliced_levels = 0;       // levels whose Galerkin product was row-sliced (DistSlicer)
     std::vector<std::vector<int64_t>> starts;  // partition of levels 0..Ld
     std::vector<DRank> ranks;    // the ranks this process drives
     CgScalars *sc_host = nullptr;
@@ -605,6 +616,102 @@ DHierarchy *dsetup(std::unique_ptr<Hierarchy> H, ncclComm_t comm, int nranks,
 // ---- entry points used by capi.cu ------------------------------------------
 namespace samgb {
 
+// Row-sliced Galerkin product for the multi-GPU setup.  Every rank runs the
+// (deterministic) setup on the whole matrix, except for the dominant step:
+// rank q forms only the coarse rows it will own, [cst[q], cst[q+1]) -- the
+// same partition chain dsetup derives from the aggregation seeds -- as
+// (R[cst[q]:cst[q+1]] A) P, and the rows are then assembled on every rank
+// (one all-reduce of the block counts, then grouped in-place ncclBroadcasts
+// of each rank's ptr / col / val piece).  Every output row is computed by
+// exactly the kernels of the single-GPU product, so A_c is bit-identical to
+// it.  Levels below min_rows * nranks coarse rows are formed redundantly.
+// Emulated group (comm == nullptr): the pieces of all ranks are formed one
+// after the other and assembled by device copies (verification on one GPU).
+struct DistSlicer : GalerkinSlicer {
+    ncclComm_t comm = nullptr;
+    int nranks = 1, rank = 0;
+    int64_t min_rows = 4096;
+    std::vector<int64_t> st;  // fine row starts of the current level
+    bool active = true;
+    int sliced_levels = 0;
+
+    bool galerkin(size_t, const Bsr3 &A, const int *seedno, int64_t nnodes, int64_t naggs,
+                  const Bsr3 &R, const Bsr3 &P, Bsr3 &Ac, bool scalar_order, cudaStream_t s) override {
+        if (!active || nnodes == 0 || naggs == 0) return active = false;
+        const int64_t h = A.nrows / nnodes, kb = P.ncols / naggs;
+        std::vector<int64_t> nidx(nranks + 1);
+        for (int q = 0; q <= nranks; ++q) nidx[q] = st[q] / h;
+        std::vector<int> sn(nranks + 1);
+        {
+            DevBuf<int64_t> di(nranks + 1, s);
+            DevBuf<int> dv(nranks + 1, s);
+            CK(cudaMemcpyAsync(di.p, nidx.data(), sizeof(int64_t) * (nranks + 1), cudaMemcpyHostToDevice, s));
+            k_gather_ptr<<<1, 32, 0, s>>>(nranks + 1, di.p, seedno, dv.p);
+            CK(cudaMemcpyAsync(sn.data(), dv.p, sizeof(int) * (nranks + 1), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+        }
+        std::vector<int64_t> cst(nranks + 1);
+        for (int q = 0; q <= nranks; ++q) cst[q] = kb * sn[q];
+        bool slice = R.nrows >= min_rows * nranks && cst[nranks] == R.nrows;
+        for (int q = 0; q < nranks && slice; ++q) slice = cst[q + 1] > cst[q];
+        if (!slice) return active = false;
+        st = cst;  // the next level's fine partition
+        ++sliced_levels;
+        std::vector<int> mine;
+        if (comm) mine.push_back(rank);
+        else for (int q = 0; q < nranks; ++q) mine.push_back(q);
+        // each driven rank's piece
+        std::vector<Bsr3> piece(nranks);
+        std::vector<int64_t> cnt(nranks, 0);
+        for (int q : mine) {
+            Bsr3 Rs;
+            slice_rows(R, cst[q], cst[q + 1], Rs, s);
+            galerkin_rows(Rs, A, P, R, piece[q], s, scalar_order);
+            cnt[q] = piece[q].nnzb;
+        }
+        if (comm) {  // block counts of every rank (an all-gather as a sum)
+            DevBuf<int64_t> dc(nranks, s);
+            CK(cudaMemcpyAsync(dc.p, cnt.data(), sizeof(int64_t) * nranks, cudaMemcpyHostToDevice, s));
+            NK(nccl().AllReduce(dc.p, dc.p, nranks, ncclInt64, ncclSum, comm, s));
+            CK(cudaMemcpyAsync(cnt.data(), dc.p, sizeof(int64_t) * nranks, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+        }
+        std::vector<int64_t> off(nranks + 1, 0);
+        for (int q = 0; q < nranks; ++q) off[q + 1] = off[q] + cnt[q];
+        Ac.alloc(R.nrows, P.ncols, off[nranks], s);
+        for (int q : mine) {  // own pieces into place, ptr rebased
+            const int *pp = piece[q].ptr.p;
+            int *ap = Ac.ptr.p + cst[q];
+            const int o = static_cast<int>(off[q]);
+            const int64_t nr = cst[q + 1] - cst[q] + (q == nranks - 1 ? 1 : 0);
+            for_each_rebase(nr, pp, o, ap, s);
+            if (cnt[q]) {
+                CK(cudaMemcpyAsync(Ac.col.p + off[q], piece[q].col.p, sizeof(int) * cnt[q],
+                                   cudaMemcpyDeviceToDevice, s));
+                CK(cudaMemcpyAsync(Ac.val.p + 9 * off[q], piece[q].val.p, sizeof(double) * 9 * cnt[q],
+                                   cudaMemcpyDeviceToDevice, s));
+            }
+            piece[q] = Bsr3();
+        }
+        if (comm) {
+            NK(nccl().GroupStart());
+            for (int q = 0; q < nranks; ++q) {
+                const int64_t nr = cst[q + 1] - cst[q] + (q == nranks - 1 ? 1 : 0);
+                int *pq = Ac.ptr.p + cst[q];
+                NK(nccl().Broadcast(pq, pq, nr, ncclInt32, q, comm, s));
+                if (cnt[q]) {
+                    int *cq = Ac.col.p + off[q];
+                    double *vq = Ac.val.p + 9 * off[q];
+                    NK(nccl().Broadcast(cq, cq, cnt[q], ncclInt32, q, comm, s));
+                    NK(nccl().Broadcast(vq, vq, 9 * cnt[q], ncclDouble, q, comm, s));
+                }
+            }
+            NK(nccl().GroupEnd());
+        }
+        return true;
+    }
+};
+
 // id == nullptr: emulate all nranks in this process (no NCCL).
 DHierarchy *dsetup_all(const unsigned char *id, int nranks, int rank, Bsr3 &&A0,
                        const double *B, int64_t b_rows, int64_t b_cols,
@@ -624,8 +731,6 @@ DHierarchy *dsetup_all(const unsigned char *id, int nranks, int rank, Bsr3 &&A0,
     }
     for (int q = 0; q < nranks; ++q)
         if (st[q + 1] <= st[q]) fail(SAMG_INVALID_ARGUMENT, "dsetup: every rank needs at least one block row");
-    std::unique_ptr<Hierarchy> H(setup_hierarchy(std::move(A0), B, b_rows, b_cols, prm, s, t0, pipeline));
-    H->owns_stream = false;  // the caller destroys s if anything below throws
     std::vector<int> mine;
     if (id) {
         mine.push_back(rank);
@@ -639,7 +744,21 @@ DHierarchy *dsetup_all(const unsigned char *id, int nranks, int rank, Bsr3 &&A0,
         NK(nccl().CommInitRank(&comm, nranks, uid, rank));
     }
     try {
+        DistSlicer slicer;
+        slicer.comm = comm;
+        slicer.nranks = nranks;
+        slicer.rank = rank;
+        slicer.min_rows = min_rows;
+        slicer.st = st;
+        static const bool slice_env = [] {
+            const char *e = std::getenv("SAMG_DIST_SLICED_GALERKIN");
+            return !e || e[0] != '0';
+        }();
+        std::unique_ptr<Hierarchy> H(setup_hierarchy(std::move(A0), B, b_rows, b_cols, prm, s, t0,
+                                                     pipeline, slice_env ? &slicer : nullptr));
+        H->owns_stream = false;  // the caller destroys s if anything below throws
         DHierarchy *d = dsetup(std::move(H), comm, nranks, mine, st, min_rows);
+        d->sliced_levels = slicer.sliced_levels;
         d->H->owns_stream = true;
         return d;
     } catch (...) {
@@ -675,6 +794,9 @@ void dinfo(const DHierarchy *d, int64_t *row0, int64_t *row1, int *nlevels, int 
     *dist_levels = static_cast<int>(d->Ld);
     *setup_s = d->H->setup_seconds;
 }
+
+int dsliced_levels(const DHierarchy *d) { return d->sliced_levels; }
+const Hierarchy &dfull(const DHierarchy *d) { return *d->H; }
 
 void nccl_unique_id(unsigned char *out) {
     ncclUniqueId uid;

@@ -77,7 +77,8 @@ uint64_t Hierarchy::memory_footprint() const {
 }
 
 Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int64_t b_cols,
-                           const samg_amg_params &prm, cudaStream_t s, double t_start, int pipeline) {
+                           const samg_amg_params &prm, cudaStream_t s, double t_start, int pipeline,
+                           GalerkinSlicer *slicer) {
     auto H = std::make_unique<Hierarchy>();
     H->stream = s;
     H->prm = prm;
@@ -126,6 +127,9 @@ Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int6
             size_t free_b = 0, total_b = 0;
             CK(cudaMemGetInfo(&free_b, &total_b));
             const double want = std::min(a_bytes * factor, 0.7 * static_cast<double>(free_b + (reserved - used)));
+            if (timing)
+                std::fprintf(stderr, "setup pool: reserved %.2f GB used %.2f GB free %.2f GB want %.2f GB\n",
+                             reserved / 1e9, used / 1e9, free_b / 1e9, want / 1e9);
             if (want > static_cast<double>(reserved - used)) {
                 void *tmp = nullptr;
                 if (cudaMallocAsync(&tmp, static_cast<size_t>(want), s) == cudaSuccess)
@@ -171,7 +175,8 @@ Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int6
             Bsr3 R;
             transpose(P, R, s);
             Bsr3 Ac;
-            galerkin(R, Li.A, P, Ac, s);
+            if (!slicer || !slicer->galerkin(lvl, Li.A, seedno.p, G.nnodes, naggs, R, P, Ac, false, s))
+                galerkin(R, Li.A, P, Ac, s);
             fix_decoupled_rows(Ac, s);
             mark("galerkin", lvl);
             Li.P = std::move(P);
@@ -215,7 +220,9 @@ Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int6
         mark("transpose", lvl);
         // Galerkin (csr.hpp:259-262) + fix_decoupled_rows (hierarchy.hpp:357)
         Bsr3 Ac;
-        galerkin(R, Li.A, P, Ac, s, scalar_galerkin);
+        if (!slicer ||
+            !slicer->galerkin(lvl, Li.A, seedno.p, G.nnodes, naggs, R, P, Ac, scalar_galerkin, s))
+            galerkin(R, Li.A, P, Ac, s, scalar_galerkin);
         fix_decoupled_rows(Ac, s);
         mark("galerkin", lvl);
         Li.P = std::move(P);

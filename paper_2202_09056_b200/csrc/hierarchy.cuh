@@ -51,10 +51,20 @@ struct Hierarchy {
     samg_solve_report cg(const double *d_f, double *d_u, const samg_cg_params &prm);
 };
 
+// Hook for the multi-GPU setup (dsolve.cu): forms A_c = R A P of level `lvl`
+// row-sliced across ranks and returns true, or returns false to let the
+// setup form the plain product.  seedno = the aggregation's seed numbering.
+struct GalerkinSlicer {
+    virtual ~GalerkinSlicer() = default;
+    virtual bool galerkin(size_t lvl, const Bsr3 &A, const int *seedno, int64_t nnodes,
+                          int64_t naggs, const Bsr3 &R, const Bsr3 &P, Bsr3 &Ac, bool scalar_order,
+                          cudaStream_t s) = 0;
+};
+
 // Setup from a device BSR3 fine matrix (consumed) and a host nullspace.
 // pipeline: ns_block, or ns_hybrid1/2 (Galerkin in scalar order)
 Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int64_t b_cols,
                            const samg_amg_params &prm, cudaStream_t stream, double t_start,
-                           int pipeline = SAMG_PIPELINE_NS_BLOCK);
+                           int pipeline = SAMG_PIPELINE_NS_BLOCK, GalerkinSlicer *slicer = nullptr);
 
 } // namespace samgb

@@ -149,6 +149,11 @@ void spgemm(const Bsr3 &A, const Bsr3 &B, Bsr3 &C, cudaStream_t s, bool scalar_o
 // A_c = (R A) P with R = P^T exactly (the hierarchy's transfer operators)
 void galerkin(const Bsr3 &R, const Bsr3 &A, const Bsr3 &P, Bsr3 &Ac, cudaStream_t s,
               bool scalar_order = false);
+// rows of (Rl A) P for a row slice Rl of R (P's columns read through R)
+void galerkin_rows(const Bsr3 &Rl, const Bsr3 &A, const Bsr3 &P, const Bsr3 &R, Bsr3 &Ac,
+                   cudaStream_t s, bool scalar_order = false);
+// rows [r0, r1) of M as a matrix of their own
+void slice_rows(const Bsr3 &M, int64_t r0, int64_t r1, Bsr3 &out, cudaStream_t s);
 void fix_decoupled_rows(Bsr3 &A, cudaStream_t s);
 // smoother setup: kind SAMG_SMOOTHER_*
 void setup_smoother(const Bsr3 &A, int kind, double omega, Smoother &M, DevError *err,

@@ -1880,6 +1880,31 @@ void spgemm(const Bsr3 &A, const Bsr3 &B, Bsr3 &C, cudaStream_t s, bool scalar_o
 // is symmetric (every level matrix: R = P^T), B = P through R's blocks.
 void galerkin(const Bsr3 &R, const Bsr3 &A, const Bsr3 &P, Bsr3 &Ac, cudaStream_t s,
               bool scalar_order) {
+    galerkin_rows(R, A, P, R, Ac, s, scalar_order);
+}
+
+// Rows [r0, r1) of M as a matrix of their own (same columns).
+void slice_rows(const Bsr3 &M, int64_t r0, int64_t r1, Bsr3 &out, cudaStream_t s) {
+    int b[2] = {0, 0};
+    CK(cudaMemcpyAsync(&b[0], M.ptr.p + r0, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&b[1], M.ptr.p + r1, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    out.alloc(r1 - r0, M.ncols, b[1] - b[0], s);
+    const int *mp = M.ptr.p + r0;
+    int *op = out.ptr.p;
+    const int b0 = b[0];
+    for_each(r1 - r0 + 1, [=] __device__(int64_t i) { op[i] = mp[i] - b0; }, s);
+    if (out.nnzb) {
+        CK(cudaMemcpyAsync(out.col.p, M.col.p + b0, sizeof(int) * out.nnzb, cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(out.val.p, M.val.p + 9LL * b0, sizeof(double) * 9 * out.nnzb,
+                           cudaMemcpyDeviceToDevice, s));
+    }
+}
+
+// Rows of the Galerkin product for the rows of Rl (a row slice of R, or R):
+// (Rl A) P, with P's columns read through the full R = P^T.
+void galerkin_rows(const Bsr3 &Rl, const Bsr3 &A, const Bsr3 &P, const Bsr3 &R, Bsr3 &Ac,
+                   cudaStream_t s, bool scalar_order) {
     Bsr3 RA;
     {
         DevBuf<int> tpos(std::max<int64_t>(1, A.nnzb), s), bad(1, s);
@@ -1894,8 +1919,8 @@ void galerkin(const Bsr3 &R, const Bsr3 &A, const Bsr3 &P, Bsr3 &Ac, cudaStream_
         BCols ba;
         ba.cp = A.ptr.p; ba.ri = A.col.p; ba.pos = tpos.p; ba.val = A.val.p; ba.tr = false;
         const BCols *pa = (hbad || A.nrows != A.ncols) ? nullptr : &ba;
-        if (scalar_order) spgemm_impl<true>(R, A, RA, s, pa);
-        else spgemm_impl<false>(R, A, RA, s, pa);
+        if (scalar_order) spgemm_impl<true>(Rl, A, RA, s, pa);
+        else spgemm_impl<false>(Rl, A, RA, s, pa);
     }
     BCols bp;
     bp.cp = R.ptr.p; bp.ri = R.col.p; bp.pos = nullptr; bp.val = R.val.p; bp.tr = true;

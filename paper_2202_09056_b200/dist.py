@@ -247,8 +247,23 @@ class DistHierarchy:
         ss = C.c_double()
         check(lib.samg_dinfo(self.h, C.byref(r0), C.byref(r1), C.byref(nl), C.byref(dl),
                              C.byref(ss)))
+        sl = C.c_int()
+        check(lib.samg_dsliced_levels(self.h, C.byref(sl)))
         return dict(row0=r0.value, row1=r1.value, nlevels=nl.value, dist_levels=dl.value,
-                    setup_seconds=ss.value)
+                    setup_seconds=ss.value, sliced_levels=sl.value)
+
+    def level(self, level, which=0):
+        """(nrows, ncols, ptr, col, val[nnzb,3,3]) of the global A (0), P (1)
+        or R (2) of `level` (every rank holds them)."""
+        import numpy as np
+        nr, nc, nz = C.c_int64(), C.c_int64(), C.c_int64()
+        check(lib.samg_dlevel_info(self.h, level, which, C.byref(nr), C.byref(nc), C.byref(nz)))
+        ptr, col = np.zeros(nr.value + 1, np.int64), np.zeros(nz.value, np.int64)
+        val = np.zeros(9 * nz.value)
+        check(lib.samg_dget_level(self.h, level, which, ptr.ctypes.data_as(C.POINTER(C.c_int64)),
+                                  col.ctypes.data_as(C.POINTER(C.c_int64)),
+                                  val.ctypes.data_as(C.POINTER(C.c_double))))
+        return nr.value, nc.value, ptr, col, val.reshape(-1, 3, 3)
 
     def cg_solve(self, f_local, prm=None):
         from ._lib import CgParamsC, ReportC

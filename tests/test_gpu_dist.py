@@ -164,3 +164,32 @@ def test_emulated_rejects_empty_rank(gpu):
         DistHierarchy(p.nbrows, p.ptr, p.col, p.val.reshape(-1), p.nullspace(), 0, 2,
                       row_starts=[0, 0, p.nbrows], prm=pb.AmgParams(coarse_enough=30),
                       emulate=True)
+
+
+@pytest.mark.parametrize("world,uneven,pipeline", [(2, False, "ns_block"), (3, True, "ns_block"),
+                                                   (4, False, "ns_hybrid2"), (3, False, "block")])
+def test_sliced_galerkin_setup_is_bit_identical(gpu, world, uneven, pipeline):
+    """The multi-GPU setup forms each level's Galerkin product row-sliced
+    (rank q its own coarse rows, then assembled on every rank).  Emulated
+    here rank by rank: every level matrix must be bit-identical to the
+    single-GPU setup's, and the slicing must actually have happened."""
+    from paper_2202_09056_b200.dist import DistHierarchy
+    pb = gpu
+    p = pb.generate_hex(nx=16, ny=8, nz=8, dirichlet="eliminate", load="traction_xend")
+    prm = pb.AmgParams(coarse_enough=60)
+    B = None if pipeline == "block" else p.nullspace()
+    h = pb.setup_bsr3(p.nbrows, p.ptr, p.col, p.val.reshape(-1), B, pipeline, prm)
+    rs = None
+    if uneven:
+        rs = np.array([0, p.nbrows // 5, p.nbrows // 2, p.nbrows], np.int64)
+    dh = DistHierarchy(p.nbrows, p.ptr, p.col, p.val.reshape(-1), B, 0, world, row_starts=rs,
+                       min_rows=1, prm=prm, emulate=True, pipeline=pipeline)
+    inf = dh.info()
+    assert inf["nlevels"] == h.nlevels
+    assert inf["sliced_levels"] >= 1
+    for lvl in range(h.nlevels):
+        for w in ((0, 1, 2) if lvl + 1 < h.nlevels else (0,)):
+            a, b = h.level(lvl, w), dh.level(lvl, w)
+            assert a[0] == b[0] and a[1] == b[1], (lvl, w)
+            for x, y in zip(a[2:], b[2:]):
+                assert np.array_equal(x, y), (lvl, w)
