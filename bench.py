@@ -507,7 +507,7 @@ def run_b200_dist(args, rank, world, local, dist):
             "clocks": clk.summary(),
             "cpu_baseline": None,
             "amg": amg,
-        }))
+        })
 
 
 def run_dist_amg(args, rank, world, local, dist):
