@@ -137,3 +137,14 @@ def test_mixed_precision_is_single_gpu_only():
     with pytest.raises(pb.Unsupported):
         DistHierarchy(p.nbrows, p.ptr, p.col, p.val.reshape(-1), p.nullspace(), 0, 2,
                       prm=pb.AmgParams(vcycle_precision="mixed"), emulate=True)
+
+
+def test_bench_and_entry_compile():
+    """bench.py and __graft_entry__.py are at least valid Python (the driver
+    runs them on the GPU box only)."""
+    import ast
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for f in ("bench.py", "__graft_entry__.py"):
+        with open(os.path.join(root, f)) as fh:
+            ast.parse(fh.read(), f)
