@@ -238,3 +238,26 @@ def test_block_pipeline_matches_reference(orc, ref, nx, ny, nz, ce, sm):
     assert o.memory_footprint == r.memory_footprint
     # +-1: the reference's dot is AVX2-FMA (kernels_avx2.cpp:35-45)
     assert abs(o.cg_solve(p.rhs)[1]["iterations"] - r.cg_solve(p.rhs)[1]["iterations"]) <= 1
+
+
+def test_threaded_reference_spmv_matches_single_thread():
+    """bench.py's multi-threaded reference baseline (the reference's own
+    spmv on row slices, one thread each) computes the same y as one call."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    import paper_2202_09056_b200 as pb
+    from oracle.oracle import Ref
+    p = pb.generate_hex(nx=9, ny=7, nz=8, dirichlet="eliminate", noise=0.01, seed=5)
+    ref = Ref()
+    x = np.random.default_rng(1).uniform(-1, 1, p.n)
+    y1 = np.zeros(p.n)
+    ref.bsr3(p.nbrows, p.nbrows, p.ptr, p.col, p.val.reshape(-1)).spmv(x, y1)
+    cuts = [0, p.nbrows // 3, p.nbrows // 2, p.nbrows]
+    y2 = np.zeros(p.n)
+    for r0, r1 in zip(cuts[:-1], cuts[1:]):
+        ref.bsr3(r1 - r0, p.nbrows, p.ptr[r0:r1 + 1], p.col, p.val.reshape(-1)).spmv(
+            x, y2[3 * r0:3 * r1])
+    assert np.array_equal(y1, y2)
+    times, used = bench.cpu_reference_spmv_threaded(p, 3, 0, steps=2)
+    assert used == 3 and len(times) == 2
