@@ -113,7 +113,22 @@ struct HaloPlan {
 struct LocalMat {
     Bsr3 A;
     HaloPlan plan;
+    // [ia, ib): the longest run of rows that read no ghost column; these
+    // are multiplied while the halo is in flight (slab partitions: all rows
+    // but the first / last node layers)
+    int64_t ia = 0, ib = 0;
 };
+
+// flag[i] = 1 if row i reads a ghost column (>= nloc)
+__global__ void k_ghost_rows(int64_t nrows, const int *ptr, const int *col, int64_t nloc,
+                             unsigned char *flag) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nrows;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        unsigned char g = 0;
+        for (int e = ptr[i]; e < ptr[i + 1]; ++e) g |= col[e] >= nloc;
+        flag[i] = g;
+    }
+}
 
 // ---- slicing on the device -------------------------------------------------
 __global__ void k_rebase(int64_t n, const int *in, int o, int *out) {
@@ -262,8 +277,49 @@ void build_local(const Bsr3 &G, const std::vector<int64_t> &row_starts,
         CK(cudaMemcpyAsync(A.val.p, G.val.p + 9 * base, sizeof(double) * 9 * nnz, cudaMemcpyDeviceToDevice, s));
     }
     CK_LAUNCH();
+    out.ia = out.ib = 0;
+    if (!global_cols && nl > 0) {
+        DevBuf<unsigned char> gf(nl, s);
+        k_ghost_rows<<<grid_of(nl), 256, 0, s>>>(nl, A.ptr.p, A.col.p, pl.nloc, gf.p);
+        CK_LAUNCH();
+        std::vector<unsigned char> hf(nl);
+        CK(cudaMemcpyAsync(hf.data(), gf.p, nl, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        int64_t best = 0, run = 0;
+        for (int64_t i = 0; i < nl; ++i) {
+            run = hf[i] ? 0 : run + 1;
+            if (run > best) { best = run; out.ib = i + 1; out.ia = i + 1 - run; }
+        }
+    }
     CK(cudaStreamSynchronize(s));  // the temporaries above are freed on s
 }
+
+// Rows [r0, r1) of M as a non-owning matrix (ptr offset; col / val shared,
+// so the ptr values stay absolute).  Vectors indexed by row (f, u, out, M)
+// are offset by the caller.
+struct RowView {
+    Bsr3 m;
+    RowView(const Bsr3 &src, int64_t r0, int64_t r1) {
+        m.nrows = r1 - r0;
+        m.ncols = src.ncols;
+        m.nnzb = src.nnzb;  // bounds of the shared arrays (the TMA path's end checks)
+        m.ptr.p = src.ptr.p + r0;
+        m.col.p = src.col.p;
+        m.val.p = src.val.p;
+        m.val32.p = src.val32.p;
+    }
+    RowView(const RowView &) = delete;
+    ~RowView() { m.ptr.p = nullptr; m.col.p = nullptr; m.val.p = nullptr; m.val32.p = nullptr; }
+};
+struct SmootherView {
+    Smoother m;
+    SmootherView(const Smoother &src, int64_t r0) {
+        m.kind = src.kind;
+        m.data.p = src.data.p ? src.data.p + (src.kind == SM_POINT ? 3 : 9) * r0 : nullptr;
+    }
+    SmootherView(const SmootherView &) = delete;
+    ~SmootherView() { m.data.p = nullptr; }
+};
 
 struct DLevel {
     LocalMat A, R, P;
@@ -291,10 +347,16 @@ struct DHierarchy {
     std::vector<std::vector<int64_t>> starts;  // partition of levels 0..Ld
     std::vector<DRank> ranks;    // the ranks this process drives
     CgScalars *sc_host = nullptr;
+    cudaStream_t cs = nullptr;   // halo transfers overlapped with interior rows
+    cudaEvent_t ev_pack = nullptr, ev_halo = nullptr;
 
     ~DHierarchy() {
         if (H && H->stream) cudaStreamSynchronize(H->stream);
+        if (cs) cudaStreamSynchronize(cs);
         ranks.clear();
+        if (ev_pack) cudaEventDestroy(ev_pack);
+        if (ev_halo) cudaEventDestroy(ev_halo);
+        if (cs) cudaStreamDestroy(cs);
         pinned_small_free(sc_host);
         if (comm) nccl().CommDestroy(comm);
     }
@@ -304,30 +366,68 @@ struct DHierarchy {
 
     // Halo exchange of the level-l operator selected by `which` (0 A, 1 R,
     // 2 P) into the extended vector `vec` of every driven rank.
+    LocalMat &local(DRank &R, size_t l, int which) {
+        DLevel &L = R.dl[l];
+        return which == 0 ? L.A : which == 1 ? L.R : L.P;
+    }
+
+    // Halo transfer of already packed send buffers into the ghost segments
+    // of `vec`, on stream cs (NCCL, or device copies when emulated).
     template <class Vec>
-    void exchange(size_t l, int which, Vec vec) {
-        cudaStream_t s = stream();
-        auto plan = [&](DRank &R) -> const HaloPlan & {
-            DLevel &L = R.dl[l];
-            return which == 0 ? L.A.plan : which == 1 ? L.R.plan : L.P.plan;
-        };
-        for (DRank &R : ranks) plan(R).pack(vec(R), s);
+    void transfer(size_t l, int which, Vec vec, cudaStream_t cs) {
         if (!emulated()) {
-            plan(ranks[0]).post(vec(ranks[0]), comm, s);
+            local(ranks[0], l, which).plan.post(vec(ranks[0]), comm, cs);
             return;
         }
         for (DRank &R : ranks) {
-            const HaloPlan &pl = plan(R);
+            const HaloPlan &pl = local(R, l, which).plan;
             double *x = vec(R);
             for (size_t k = 0; k < pl.recv_peers.size(); ++k) {
-                const HaloPlan &ql = plan(ranks[pl.recv_peers[k]]);
+                const HaloPlan &ql = local(ranks[pl.recv_peers[k]], l, which).plan;
                 const auto it = std::find(ql.send_peers.begin(), ql.send_peers.end(), R.rank);
                 if (it == ql.send_peers.end()) fail(SAMG_ERROR, "dsolve: unmatched halo receive");
                 const size_t i = it - ql.send_peers.begin();
                 if (ql.send_counts[i] != pl.recv_counts[k])
                     fail(SAMG_ERROR, "dsolve: halo send/receive counts differ");
                 d2d(x + 3 * (pl.nloc + pl.recv_offsets[k]), ql.sendbuf.p + 3 * ql.send_offsets[i],
-                    3 * pl.recv_counts[k], s);
+                    3 * pl.recv_counts[k], cs);
+            }
+        }
+    }
+
+    // Halo exchange of the level-l operator selected by `which` (0 A, 1 R,
+    // 2 P) into the extended vector `vec` of every driven rank.
+    template <class Vec>
+    void exchange(size_t l, int which, Vec vec) {
+        cudaStream_t s = stream();
+        for (DRank &R : ranks) local(R, l, which).plan.pack(vec(R), s);
+        transfer(l, which, vec, s);
+    }
+
+    // Exchange overlapped with the rows that read no ghost: pack on the solve
+    // stream, the transfer on the comm stream, op(R, r0, r1) on rows [ia, ib)
+    // meanwhile, the remaining rows once the halo has arrived.
+    template <class Vec, class Op>
+    void exchange_overlap(size_t l, int which, Vec vec, Op op) {
+        cudaStream_t s = stream();
+        for (DRank &R : ranks) local(R, l, which).plan.pack(vec(R), s);
+        CK(cudaEventRecord(ev_pack, s));
+        CK(cudaStreamWaitEvent(cs, ev_pack, 0));
+        transfer(l, which, vec, cs);
+        CK(cudaEventRecord(ev_halo, cs));
+        for (DRank &R : ranks) {
+            const LocalMat &M = local(R, l, which);
+            if (M.ib > M.ia) op(R, M.ia, M.ib);
+        }
+        CK(cudaStreamWaitEvent(s, ev_halo, 0));
+        for (DRank &R : ranks) {
+            const LocalMat &M = local(R, l, which);
+            const int64_t n = M.A.nrows;
+            if (M.ib > M.ia) {
+                if (M.ia > 0) op(R, 0, M.ia);
+                if (n > M.ib) op(R, M.ib, n);
+            } else if (n > 0) {
+                op(R, 0, n);
             }
         }
     }
@@ -387,24 +487,28 @@ void DHierarchy::vcycle() {
             else launch_fill(3 * L.A.A.nrows, 0.0, L.uA.p, s);
         }
         for (int sw = 1; sw < pre; ++sw) {
-            exchange(l, 0, [&](DRank &R) { return R.dl[l].uA.p; });
-            for (DRank &R : ranks) {
+            exchange_overlap(l, 0, [&](DRank &R) { return R.dl[l].uA.p; },
+                             [&](DRank &R, int64_t a, int64_t b) {
                 DLevel &L = R.dl[l];
-                launch_smooth(L.A.A, L.M, fin(R, l), L.uA.p, L.t.p, s);
-                d2d(L.uA.p, L.t.p, 3 * L.A.A.nrows, s);
-            }
+                RowView v(L.A.A, a, b);
+                SmootherView m(L.M, a);
+                launch_smooth_split(v.m, m.m, fin(R, l) + 3 * a, L.uA.p, L.uA.p + 3 * a, L.t.p + 3 * a, s);
+            });
+            for (DRank &R : ranks) d2d(R.dl[l].uA.p, R.dl[l].t.p, 3 * R.dl[l].A.A.nrows, s);
         }
-        exchange(l, 0, [&](DRank &R) { return R.dl[l].uA.p; });
-        for (DRank &R : ranks) {
+        exchange_overlap(l, 0, [&](DRank &R) { return R.dl[l].uA.p; },
+                         [&](DRank &R, int64_t a, int64_t b) {
             DLevel &L = R.dl[l];
-            launch_residual(L.A.A, fin(R, l), L.uA.p, L.rR.p, s);
-        }
-        exchange(l, 1, [&](DRank &R) { return R.dl[l].rR.p; });
-        for (DRank &R : ranks) {
+            RowView v(L.A.A, a, b);
+            launch_residual(v.m, fin(R, l) + 3 * a, L.uA.p, L.rR.p + 3 * a, s);
+        });
+        exchange_overlap(l, 1, [&](DRank &R) { return R.dl[l].rR.p; },
+                         [&](DRank &R, int64_t a, int64_t b) {
             DLevel &L = R.dl[l];
             double *fc = (l + 1 < Ld) ? R.dl[l + 1].f.p : R.fLd.p + 3 * starts[Ld][R.rank];
-            launch_spmv(L.R.A, 1.0, L.rR.p, 0.0, fc, s);
-        }
+            RowView v(L.R.A, a, b);
+            launch_spmv(v.m, 1.0, L.rR.p, 0.0, fc + 3 * a, s);
+        });
     }
     gather_coarse();
     for (DRank &R : ranks) H->vcycle_from(Ld, R.fLd.p, R.uLd.p, true, false);
@@ -416,20 +520,30 @@ void DHierarchy::vcycle() {
                 const DLevel &N = R.dl[l + 1];
                 d2d(R.dl[l].uP.p, post > 0 ? N.t.p : N.uA.p, 3 * N.A.A.nrows, s);
             }
-            exchange(l, 2, [&](DRank &R) { return R.dl[l].uP.p; });
-        }
-        for (DRank &R : ranks) {
-            DLevel &L = R.dl[l];
-            launch_spmv(L.P.A, 1.0, next_replicated ? R.uLd.p : L.uP.p, 1.0, L.uA.p, s);
-        }
-        for (int sw = 0; sw < post; ++sw) {
-            exchange(l, 0, [&](DRank &R) { return R.dl[l].uA.p; });
+            exchange_overlap(l, 2, [&](DRank &R) { return R.dl[l].uP.p; },
+                             [&](DRank &R, int64_t a, int64_t b) {
+                DLevel &L = R.dl[l];
+                RowView v(L.P.A, a, b);
+                launch_spmv(v.m, 1.0, L.uP.p, 1.0, L.uA.p + 3 * a, s);
+            });
+        } else {
             for (DRank &R : ranks) {
                 DLevel &L = R.dl[l];
-                double *out = (l == 0 && sw == post - 1) ? R.z.p : L.t.p;
-                launch_smooth(L.A.A, L.M, fin(R, l), L.uA.p, out, s);
-                if (sw + 1 < post) d2d(L.uA.p, out, 3 * L.A.A.nrows, s);
+                launch_spmv(L.P.A, 1.0, R.uLd.p, 1.0, L.uA.p, s);
             }
+        }
+        for (int sw = 0; sw < post; ++sw) {
+            auto out_of = [&](DRank &R) { return (l == 0 && sw == post - 1) ? R.z.p : R.dl[l].t.p; };
+            exchange_overlap(l, 0, [&](DRank &R) { return R.dl[l].uA.p; },
+                             [&](DRank &R, int64_t a, int64_t b) {
+                DLevel &L = R.dl[l];
+                RowView v(L.A.A, a, b);
+                SmootherView m(L.M, a);
+                launch_smooth_split(v.m, m.m, fin(R, l) + 3 * a, L.uA.p, L.uA.p + 3 * a,
+                                    out_of(R) + 3 * a, s);
+            });
+            if (sw + 1 < post)
+                for (DRank &R : ranks) d2d(R.dl[l].uA.p, out_of(R), 3 * R.dl[l].A.A.nrows, s);
         }
         if (l == 0 && post == 0)
             for (DRank &R : ranks) d2d(R.z.p, R.dl[0].uA.p, 3 * R.nloc0, s);
@@ -605,6 +719,9 @@ DHierarchy *dsetup(std::unique_ptr<Hierarchy> H, ncclComm_t comm, int nranks,
         R.sc.alloc(1, s);
     }
     D->sc_host = static_cast<CgScalars *>(pinned_small_alloc(sizeof(CgScalars)));
+    CK(cudaStreamCreateWithFlags(&D->cs, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&D->ev_pack, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&D->ev_halo, cudaEventDisableTiming));
     CK(cudaStreamSynchronize(s));
     D->H = std::move(H);
     D->comm = comm;

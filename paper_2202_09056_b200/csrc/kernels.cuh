@@ -63,6 +63,9 @@ void set_spmv_cta_cap(int ctas);
 // fp32 copy of the values (A.val32) for the mixed-precision V-cycle
 void make_lowp(Bsr3 &A, cudaStream_t s);
 // u = M f  (one sweep from a zero guess: the residual is f exactly)
+// launch_smooth with the gathered x apart from the row-indexed u / f / M / out
+void launch_smooth_split(const Bsr3 &A, const Smoother &M, const double *f, const double *x,
+                         const double *u, double *u_out, cudaStream_t s);
 void launch_smooth_zero(int64_t nrows, const Smoother &M, const double *f, double *u,
                         cudaStream_t s);
 // leading dimension of the dense coarse inverse (even, for 16-byte loads)

@@ -963,6 +963,16 @@ void launch_smooth(const Bsr3 &A, const Smoother &M, const double *f, const doub
     else launch_rows(A, u, EpiSmoothBlock{f, u, M.data.p, u_out}, s, lowp);
 }
 
+// As launch_smooth with the gathered vector x apart from the row-indexed u
+// (a row range of a partitioned level: x is the whole halo-extended vector)
+void launch_smooth_split(const Bsr3 &A, const Smoother &M, const double *f, const double *x,
+                         const double *u, double *u_out, cudaStream_t s) {
+    if (M.kind == SM_ILU) fail(SAMG_UNSUPPORTED, "launch_smooth_split: ILU(0) sweeps are not row-separable");
+    if (A.nrows == 0) return;
+    if (M.kind == SM_POINT) launch_rows(A, x, EpiSmoothPoint{f, u, M.data.p, u_out}, s, false);
+    else launch_rows(A, x, EpiSmoothBlock{f, u, M.data.p, u_out}, s, false);
+}
+
 void launch_smooth_zero(int64_t nrows, const Smoother &M, const double *f, double *u,
                         cudaStream_t s) {
     if (nrows == 0) return;
