@@ -599,9 +599,16 @@ samg_solve_report DHierarchy::cg(const double *d_f, double *d_u, const samg_cg_p
     double res_norm = norm_f;
     int iter = 0;
     while (res_norm / norm_f > cp.tol && iter < cp.max_iterations) {
-        exchange(0, 0, [](DRank &R) { return R.pext.p; });
-        for (DRank &R : ranks)
-            launch_spmv_dot(R.dl[0].A.A, R.pext.p, R.q.p, R.partials.p, R.sc.p, s, CG_STORE);
+        // q = A p overlapped with the halo: the first row range stores its
+        // partial p.q, the others add to it
+        std::vector<int> pieces(ranks.size(), 0);
+        exchange_overlap(0, 0, [](DRank &R) { return R.pext.p; },
+                         [&](DRank &R, int64_t a, int64_t b) {
+            RowView v(R.dl[0].A.A, a, b);
+            int &k = pieces[&R - ranks.data()];
+            launch_spmv_dot_split(v.m, R.pext.p, R.pext.p + 3 * a, R.q.p + 3 * a, R.partials.p,
+                                  R.sc.p, s, k++ == 0 ? CG_STORE : CG_ADD);
+        });
         allreduce_finish(CG_PQ);
         for (DRank &R : ranks)
             launch_cg_update(3 * R.nloc0, R.sc.p, R.pext.p, R.q.p, R.u.p, R.r.p, R.partials.p,

@@ -88,7 +88,10 @@ struct CgScalars {
 // RZ: beta = rz/rho, rho = rz; RHO: rho; RR_LOOP: rr, ++iter and the graph
 // loop condition ||r||/||f|| > tol && iter < max && !breakdown.
 // STORE: only tmp = s (multi-GPU: allreduce tmp, then launch_cg_finish).
-enum { CG_RR = 0, CG_PQ = 1, CG_RZ = 2, CG_RHO = 3, CG_RR_LOOP = 4, CG_STORE = 5 };
+enum { CG_RR = 0, CG_PQ = 1, CG_RZ = 2, CG_RHO = 3, CG_RR_LOOP = 4, CG_STORE = 5, CG_ADD = 6 };
+// q = A x and p.q on a row range (x the whole halo-extended vector)
+void launch_spmv_dot_split(const Bsr3 &A, const double *x, const double *p, double *q,
+                           double *partials, CgScalars *sc, cudaStream_t s, int what);
 // apply `what` to sc->tmp (after the allreduce of the partial sums)
 void launch_cg_finish(CgScalars *sc, int what, cudaStream_t s);
 constexpr int kRedBlocks = 592;   // 4 x 148 SMs: fixed => deterministic sums

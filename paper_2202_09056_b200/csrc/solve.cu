@@ -309,6 +309,7 @@ __device__ void cg_apply(int what, double s, CgScalars *sc, cudaGraphConditional
             break;
         case CG_RHO: sc->rho = s; break;
         case CG_STORE: sc->tmp = s; break;
+        case CG_ADD: sc->tmp += s; break;  // further row ranges of one product
         case CG_RR_LOOP: {
             sc->rr = s;
             const int it = sc->iter + 1;
@@ -985,6 +986,14 @@ void launch_smooth_zero(int64_t nrows, const Smoother &M, const double *f, doubl
 void launch_spmv_dot(const Bsr3 &A, const double *p, double *q, double *partials,
                      CgScalars *sc, cudaStream_t s, int what) {
     launch_reduce(A, p, EpiDot{p, q}, partials, sc, what, s);
+}
+
+// q = A x and p.q on a row range: x the whole halo-extended vector, p / q
+// row-indexed
+void launch_spmv_dot_split(const Bsr3 &A, const double *x, const double *p, double *q,
+                           double *partials, CgScalars *sc, cudaStream_t s, int what) {
+    if (A.nrows == 0) return;
+    launch_reduce(A, x, EpiDot{p, q}, partials, sc, what, s);
 }
 
 void launch_smooth_dot(const Bsr3 &A, const Smoother &M, const double *f, const double *u,
