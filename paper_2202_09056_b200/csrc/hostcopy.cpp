@@ -26,7 +26,7 @@ namespace samgb {
 namespace {
 
 constexpr size_t kChunk = 8u << 20;     // bytes per staging buffer
-constexpr int kThreads = 16;  // upper bound; SAMG_H2D_THREADS (default 8) uses fewer
+constexpr int kThreads = 16;  // upper bound; SAMG_H2D_THREADS (default min(12, cores - 2)) uses fewer
 constexpr size_t kDirect = 4u << 20;    // below this: plain cudaMemcpyAsync
 
 struct Pool {
@@ -85,9 +85,13 @@ void h2d(void *dst, const void *src, size_t bytes, cudaStream_t s) {
     int dev = 0;
     CK(cudaGetDevice(&dev));
     const size_t nchunks = (bytes + kChunk - 1) / kChunk;
+    // default: 12 staging threads, or all but two of the host's (C1 setup
+    // on the 16-thread GPU hosts, scripts/upload_sweep.py: 4 / 8 / 12 / 16
+    // threads -> 89.1 / 80.6 / 76.7 / 77.1 ms)
     static const int threads = [] {
         const char *e = std::getenv("SAMG_H2D_THREADS");
-        const int v = e ? std::atoi(e) : 8;
+        const int hw = static_cast<int>(std::thread::hardware_concurrency());
+        const int v = e ? std::atoi(e) : std::min(12, std::max(1, hw - 2));
         return std::min(kThreads, std::max(1, v));
     }();
     const int T = static_cast<int>(std::min<size_t>(threads, nchunks));
