@@ -1843,12 +1843,14 @@ void spgemm_impl(const Bsr3 &A, const Bsr3 &B, Bsr3 &C, cudaStream_t s, const BC
         const bool wide_cta = n < 148 * 16;
         // batch: measured on C4 (scripts/setup_phases.py): 1 for the fine
         // level's 601 526 rows (88 / 100 ms vs 122 / 139 with 4: occupancy),
-        // 4 for level 1's 78 162 (37 / 57 ms vs 40 / 83 with 1)
+        // 4 for level 1's 78 162 (37 / 57 ms vs 40 / 83 with 1); C1's level
+        // 0 (20 642 rows): 1 (2.3 / 3.0 ms vs 2.8 / 4.0 with 4; ncu: 128
+        // registers, 20 % warps active)
         static const int batch_env = [] {
             const char *e = std::getenv("SAMG_PULL_BATCH");
             return e ? std::atoi(e) : 0;
         }();
-        const int batch = batch_env > 0 ? batch_env : (n >= 16384 && n < 200000 ? 4 : 1);
+        const int batch = batch_env > 0 ? batch_env : (n >= 50000 && n < 200000 ? 4 : 1);
         using KP = decltype(&k_spgemm_pull<kScalar, true, 128, 1>);
         KP kp;
         auto pick = [&](auto bt) {
