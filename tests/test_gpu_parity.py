@@ -427,3 +427,35 @@ def test_c1_full_size_hierarchy_and_properties(gpu, ref):
     u, rep = h.cg_solve(p.rhs)
     assert rep["converged"] and rep["relative_residual"] <= 1.01e-8
     assert abs(rep["iterations"] - 165) <= 1, rep
+
+
+@pytest.mark.slow
+def test_c4_full_size_properties(gpu):
+    """BASELINE config 4 (200^3 nodes, 23.88 M unknowns, 212.8 M blocks),
+    assembled on the GPU: no reference run is affordable (37 GB
+    preconditioner, tens of minutes single-threaded), so size-independent
+    properties: SpMV linearity on the device, the hierarchy's level sizes
+    (profiles/r01_configs_final.jsonl) and CG convergence to rtol 1e-8."""
+    import torch
+    pb = gpu
+    dp = pb.generate_hex_device(pb.ProblemParams(nx=199, ny=199, nz=199, dirichlet="eliminate",
+                                                 noise=0.01, seed=2022), device=0)
+    assert (dp.n, dp.nnzb) == (23880000, 212774380)
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device=dev).manual_seed(5)
+    x = torch.rand(dp.n + 2, dtype=torch.float64, device=dev, generator=g) - 0.5
+    y = torch.rand(dp.n + 2, dtype=torch.float64, device=dev, generator=g) - 0.5
+    z = 2.5 * x - 0.75 * y
+    ax, ay, az = (torch.zeros_like(x) for _ in range(3))
+    for v, out in ((x, ax), (y, ay), (z, az)):
+        dp.A.spmv_device(v.data_ptr(), out.data_ptr())
+    torch.cuda.synchronize()
+    ref = 2.5 * ax[:dp.n] - 0.75 * ay[:dp.n]
+    assert float((az[:dp.n] - ref).abs().max()) <= 1e-12 * float(ref.abs().max())
+    del x, y, z, ax, ay, az
+    h = pb.setup_device(dp.A, dp.nullspace_ptr, 6, "ns_block", pb.AmgParams(smoother="spai0"))
+    assert [h.level_info(l)[0] for l in range(h.nlevels)] == [7960000, 601526, 78162, 8716, 1352, 626]
+    u = torch.zeros(dp.n + 2, dtype=torch.float64, device=dev)
+    rep = h.cg_solve_device(dp.rhs_ptr, u.data_ptr())
+    assert rep["converged"] and rep["relative_residual"] <= 1.01e-8, rep
+    h.close()
