@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--amg-repeats", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c4", action="store_true", help="skip the C4 setup+solve leg")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--force-dist", action="store_true",
                     help="use the row-partitioned (NCCL halo) path even on one GPU")
@@ -152,6 +153,14 @@ def make_problem(pb):
     return pb.generate_hex(**C1)
 
 
+def config_dict(p, world):
+    """The `config` object, identical in both arms (same workload, same sizes)."""
+    return {"workload": WORKLOAD, "unknowns": p.n, "block_rows": p.nbrows, "nnzb": p.nnzb,
+            "spmv_bytes_per_step": spmv_bytes(p),
+            "l2": "no flush: matrix stream 527 MB > 126 MB L2",
+            "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"}
+
+
 def cpu_reference_spmv(p, seconds, steps=None):
     """The reference's spmv<static_block<3>> (csr.hpp:129-160) from
     oracle/_ref on one host core over the C1 matrix: time-bounded sample."""
@@ -223,14 +232,18 @@ def spmv_bytes(p):
 
 
 def run_reference(args, rank, world, dist):
-    """--impl reference: the reference's own CPU path, rank 0 only."""
+    """--impl reference: the reference's own CPU path, rank 0 only.  Nothing
+    of the product is loaded: the problem comes from the repo's host
+    generator as linked into oracle/_ref (bitwise the product's
+    generate_hex, tests/test_abi.py), the rigid-body modes from the
+    reference's own rigid_body_modes (elasticity.hpp:38-52)."""
     if rank != 0:
         return
-    import paper_2202_09056_b200 as pb  # host-only generator (no GPU work)
-    p = make_problem(pb)
+    from oracle.oracle import Params, Ref, SM_SPAI0
+    ref = Ref()
+    p = ref.gen_hex(**C1)
     nbytes = spmv_bytes(p)
-    cores = 1
-    # each step: one full SpMV (23 ms class); bound the run to a few minutes
+    # each step: one full SpMV (5 ms class on all threads); bound the run
     steps = args.steps
     budget = 60.0
     threads = host_threads()
@@ -243,23 +256,22 @@ def run_reference(args, rank, world, dist):
     t1 = statistics.median(cpu_reference_spmv(p, 0, steps=5))
     amg = None
     if os.environ.get("SAMG_BENCH_REF_AMG", "1") == "1":
-        from oracle.oracle import Params, Ref, SM_SPAI0
-        ref = Ref()
         n, ptr, col, val = p.csr()
         B = p.nullspace()
-        t0 = time.perf_counter()
         h = ref.setup(n, ptr, col, val, B, Params(smoother=SM_SPAI0))
-        t_setup = time.perf_counter() - t0
         u, rep = h.cg_solve(p.rhs)
-        amg = {"setup_s": t_setup, "solve_s": rep["solve_seconds"], "iterations": rep["iterations"],
-               "relative_residual": rep["relative_residual"], "levels": h.nlevels,
-               "converged": rep["converged"], "cores": 1}
+        amg = {"setup_s": h.setup_seconds, "solve_s": rep["solve_seconds"],
+               "iterations": rep["iterations"], "relative_residual": rep["relative_residual"],
+               "levels": h.nlevels, "converged": rep["converged"], "cores": 1,
+               "timing": "steady_clock inside oracle/_ref around samg::setup (+ the harness "
+                         "smoother arrays) and around cg_solve_op, as bench.hpp:72-80",
+               "input": "host scalar CSR + host f/u (the reference's own API)"}
     line = {
         "metric": METRIC, "value": gbs, "unit": "GB/s", "impl": "reference",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "unknowns": p.n, "nnzb": p.nnzb},
+        "config": config_dict(p, world),
         "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "reference",
                          "sample": f"{len(times)} x samg::spmv<static_block<3>> over the full C1 "
                                    f"matrix (median), oracle/_ref, {cores} threads on row slices "
@@ -328,30 +340,30 @@ def run_b200(args, rank, world, local, dist):
         e2e_t = float(t.item())
     e2e_val = nbytes / e2e_t / 1e9 * world
 
-    # full AMG setup + solve on the same problem (device-resident after upload)
+    # full AMG setup + solve on the same problem through the drop-in calls a
+    # reference user makes: samg_setup from the host scalar CSR + host B
+    # (hierarchy.hpp:263) and samg_cg_solve with host f / u (cg.hpp:87);
+    # uploads and the D2H of u inside the timed region, wall clock
     amg = None
     if args.amg_repeats > 0:
-        n, ptr, col, val = p.csr()
+        A_csr = p.csr()
         B = p.nullspace()
         prm = pb.AmgParams(smoother="spai0", device=local)
         setups, solves, rep, h = [], [], None, None
-        f_d = torch.from_numpy(p.rhs).to(dev)
-        u_d = torch.zeros_like(f_d)
         # untimed warm-up: lazy module loading of every setup/solve kernel
-        hw = pb.setup_bsr3(p.nbrows, p.ptr, p.col, p.val.reshape(-1), B, "ns_block", prm)
-        hw.cg_solve_device(f_d.data_ptr(), u_d.data_ptr(), pb.CgParams(max_iterations=2))
+        hw = pb.setup(A_csr, B, "ns_block", prm)
+        hw.cg_solve(p.rhs, pb.CgParams(max_iterations=2))
         hw.close()
         for _ in range(args.amg_repeats):
             if h is not None:
                 h.close()
             torch.cuda.synchronize(dev)
             t0 = time.perf_counter()
-            h = pb.setup_bsr3(p.nbrows, p.ptr, p.col, p.val.reshape(-1), B, "ns_block", prm)
+            h = pb.setup(A_csr, B, "ns_block", prm)
             torch.cuda.synchronize(dev)
             setups.append(time.perf_counter() - t0)
             t0 = time.perf_counter()
-            rep = h.cg_solve_device(f_d.data_ptr(), u_d.data_ptr())
-            torch.cuda.synchronize(dev)
+            u_host, rep = h.cg_solve(p.rhs)
             solves.append(time.perf_counter() - t0)
         levels = [h.level_info(l)[0] for l in range(h.nlevels)]
         amg = {"setup_s": statistics.median(setups), "solve_s": statistics.median(solves),
@@ -359,9 +371,32 @@ def run_b200(args, rank, world, local, dist):
                "iterations": rep["iterations"], "relative_residual": rep["relative_residual"],
                "converged": rep["converged"], "levels_block_rows": levels,
                "coarse_dim": h.coarse_dim, "preconditioner_bytes": rep["preconditioner_bytes"],
-               "smoother": "spai0 (M_i = A_ii / sum_j ||A_ij||_F^2)", "input": "host BSR3 upload "
-               "inside setup_s"}
+               "smoother": "spai0 (M_i = A_ii / sum_j ||A_ij||_F^2)",
+               "input": "drop-in C-ABI: samg_setup(host scalar CSR, host B) + "
+                        "samg_cg_solve(host f, host u); H2D / D2H inside the timed region"}
         h.close()
+        # the same with block input (samg_setup_bsr3, host BSR3 upload) and the
+        # solve on device vectors
+        f_d = torch.from_numpy(p.rhs).to(dev)
+        u_d = torch.zeros_like(f_d)
+        st, sv = [], []
+        for it in range(1 + args.amg_repeats):
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            hb = pb.setup_bsr3(p.nbrows, p.ptr, p.col, p.val.reshape(-1), B, "ns_block", prm)
+            torch.cuda.synchronize(dev)
+            t1 = time.perf_counter()
+            repb = hb.cg_solve_device(f_d.data_ptr(), u_d.data_ptr())
+            torch.cuda.synchronize(dev)
+            t2 = time.perf_counter()
+            hb.close()
+            if it:
+                st.append(t1 - t0)
+                sv.append(t2 - t1)
+        amg["bsr3_input"] = {"setup_s": statistics.median(st), "solve_s": statistics.median(sv),
+                             "iterations": repb["iterations"],
+                             "what": "samg_setup_bsr3 (host BSR3 upload inside setup_s) + "
+                                     "samg_cg_solve_device"}
         # fully device-resident pipeline: on-GPU assembly (samg_generate_hex_device),
         # setup from the device matrix, solve on the device right-hand side
         times = []
@@ -415,6 +450,8 @@ def run_b200(args, rank, world, local, dist):
                              "iterations": vr["iterations"], "converged": vr["converged"],
                              "relative_residual": vr["relative_residual"]}
         amg["variants"] = variants
+        if not args.no_c4:
+            amg["c4"] = run_c4(pb, torch, dev, local)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -440,10 +477,7 @@ def run_b200(args, rank, world, local, dist):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "unknowns": p.n, "block_rows": p.nbrows,
-                       "nnzb": p.nnzb, "spmv_bytes_per_step": nbytes,
-                       "l2": "no flush: matrix stream 527 MB > 126 MB L2",
-                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
+            "config": config_dict(p, world),
             "roofline": {"bound": "hbm", "achieved": gbs_rank, "peak": peak, "unit": "GB/s",
                          "frac": gbs_rank / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": "k_bsr3_tma<8,8,2,false,EpiSpmv> (solve.cu, TMA-fed)"},
@@ -459,6 +493,42 @@ def run_b200(args, rank, world, local, dist):
             "amg": amg,
         }
         emit(line)
+
+
+C4 = dict(nx=199, ny=199, nz=199, dirichlet="eliminate", noise=0.01, seed=2022)
+
+
+def run_c4(pb, torch, dev, local):
+    """C4 (200^3-node cube, 23.88 M unknowns, 212.8 M blocks) on one GPU:
+    assembled in HBM (samg_generate_hex_device; the host generator + 16.6 GB
+    upload would dominate), ns_block setup from the device matrix, SPAI0-PCG
+    to 1e-8.  Two runs, the first also warms the memory pool."""
+    prm = pb.AmgParams(smoother="spai0", device=local)
+    runs = []
+    for it in range(2):
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        dp = pb.generate_hex_device(pb.ProblemParams(**C4), device=local)
+        torch.cuda.synchronize(dev)
+        t1 = time.perf_counter()
+        hd = pb.setup_device(dp.A, dp.nullspace_ptr, 6, "ns_block", prm)
+        torch.cuda.synchronize(dev)
+        t2 = time.perf_counter()
+        u_d = torch.zeros(dp.n, dtype=torch.float64, device=dev)
+        rep = hd.cg_solve_device(dp.rhs_ptr, u_d.data_ptr())
+        torch.cuda.synchronize(dev)
+        t3 = time.perf_counter()
+        levels = [hd.level_info(l)[0] for l in range(hd.nlevels)]
+        runs.append({"assemble_s": t1 - t0, "setup_s": t2 - t1, "solve_s": t3 - t2,
+                     "iterations": rep["iterations"], "converged": rep["converged"],
+                     "relative_residual": rep["relative_residual"]})
+        hd.close()
+        del dp, u_d
+    torch.cuda.empty_cache()
+    best = runs[-1]
+    return {**best, "levels_block_rows": levels, "runs": runs, "unknowns": 23880000,
+            "what": "C4 200^3 nodes free-DOF, samg_generate_hex_device + samg_setup_device + "
+                    "samg_cg_solve_device, SPAI0; second run reported (first warms the pool)"}
 
 
 def run_b200_dist(args, rank, world, local, dist):

@@ -101,7 +101,9 @@ typedef struct {
     int post_sweeps;          /* 1 */
     int64_t coarse_enough;    /* 3000 scalar unknowns */
     double stagnation_ratio;  /* 0.8 */
-    int verify_galerkin;      /* reserved (hierarchy.hpp:382-402) */
+    int verify_galerkin;      /* 0; 1: recompute every coarse operator as the
+                                 scalar R A P and fail with SAMG_ERROR on a
+                                 mismatch (hierarchy.hpp:382-401) */
     int device;               /* CUDA device ordinal, default 0 */
     int vcycle_precision;     /* samg_precision, default FP64 */
 } samg_amg_params;

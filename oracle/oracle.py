@@ -65,6 +65,63 @@ class Params:
     pipeline: int = 5  # samg::pipeline: 3 ns_hybrid1, 4 ns_hybrid2, 5 ns_block
 
 
+class _problem_params(C.Structure):
+    """samg_problem_params (include/samg_b200.h), for ref_gen_hex."""
+    _fields_ = [("nx", C.c_int64), ("ny", C.c_int64), ("nz", C.c_int64),
+                ("lx", C.c_double), ("ly", C.c_double), ("lz", C.c_double),
+                ("E", C.c_double), ("nu", C.c_double), ("heterogeneous", C.c_int),
+                ("dirichlet", C.c_int), ("load", C.c_int), ("noise", C.c_double),
+                ("seed", C.c_uint64), ("x_slowest", C.c_int), ("node_begin", C.c_int64),
+                ("node_end", C.c_int64)]
+
+
+_DIRICHLET = {"none": 0, "keep_rows": 1, "eliminate": 2}
+_LOAD = {"body_force": 0, "traction_xend": 1, "random": 2}
+
+
+@dataclass
+class GenProblem:
+    """A BASELINE-config problem from the repo's host generator as compiled
+    into oracle/_ref (same fields as paper_2202_09056_b200.Problem)."""
+    n: int
+    nnodes: int
+    ptr: np.ndarray
+    col: np.ndarray
+    val: np.ndarray          # (nnzb, 3, 3)
+    rhs: np.ndarray
+    xyz: np.ndarray
+    ref: object = None
+
+    @property
+    def nbrows(self):
+        return self.n // 3
+
+    @property
+    def nnzb(self):
+        return int(self.ptr[-1])
+
+    def nullspace(self):
+        """rigid_body_modes (elasticity.hpp:38-52), the reference's own."""
+        return self.ref.rigid_body_modes(self.xyz)
+
+    def csr(self):
+        """Scalar CSR with every block entry kept (to_scalar, csr.hpp:327-353)."""
+        nb = self.nbrows
+        lens = np.diff(self.ptr)
+        ptr = np.zeros(self.n + 1, np.int64)
+        ptr[1:] = np.repeat(3 * lens, 3).cumsum()
+        rows_blocks = np.repeat(np.arange(nb), lens)
+        jpos = np.arange(self.nnzb) - self.ptr[rows_blocks]
+        col = np.empty(9 * self.nnzb, np.int64)
+        val = np.empty(9 * self.nnzb)
+        for r in range(3):
+            base = ptr[3 * rows_blocks + r] + 3 * jpos
+            for c in range(3):
+                col[base + c] = 3 * self.col + c
+                val[base + c] = self.val[:, r, c]
+        return self.n, ptr, col, val
+
+
 class _orc_mat(C.Structure):
     _fields_ = [("nrows", C.c_int64), ("ncols", C.c_int64), ("b", C.c_int),
                 ("ptr", i64p), ("col", i64p), ("val", f64p)]
@@ -288,9 +345,14 @@ class Ref(_Backend):
                                          C.POINTER(i64p), C.POINTER(f64p), C.POINTER(f64p),
                                          C.POINTER(f64p)]
         lib.ref_rigid_body_modes.argtypes = [C.c_int64, f64p, f64p]
+        lib.ref_gen_hex.argtypes = [C.POINTER(_problem_params), i64p, i64p, C.POINTER(i64p),
+                                    C.POINTER(i64p), C.POINTER(f64p), C.POINTER(f64p),
+                                    C.POINTER(f64p)]
+        lib.ref_force_isa.argtypes = [C.c_int]
         lib.ref_setup.argtypes = [C.c_int64, i64p, i64p, f64p, f64p, C.c_int64, C.c_double,
                                   C.c_double, C.c_int, C.c_double, C.c_int64, C.c_double,
                                   C.c_int, C.POINTER(vp)]
+        lib.ref_setup_bsr3.argtypes = lib.ref_setup.argtypes
         lib.ref_destroy.argtypes = [vp]
         lib.ref_nlevels.argtypes = [vp]
         lib.ref_setup_seconds.argtypes = [vp]
@@ -345,6 +407,33 @@ class Ref(_Backend):
         self._check(self.lib.ref_rigid_body_modes(nn, _p(coords), _p(B)))
         return B
 
+    def gen_hex(self, nx=19, ny=19, nz=19, lx=1.0, ly=1.0, lz=1.0, E=1.0, nu=0.3,
+                heterogeneous=False, dirichlet="eliminate", load="body_force", noise=0.0,
+                seed=12345, x_slowest=False, node_begin=0, node_end=0) -> GenProblem:
+        """The repo's BASELINE-config generator (generator.cpp, host-only,
+        linked into oracle/_ref); keywords as paper_2202_09056_b200.ProblemParams."""
+        pc = _problem_params(nx, ny, nz, lx, ly, lz, E, nu, int(heterogeneous),
+                             _DIRICHLET[dirichlet], _LOAD[load], noise, seed, int(x_slowest),
+                             node_begin, node_end)
+        n, nn = C.c_int64(), C.c_int64()
+        ptr, col = i64p(), i64p()
+        val, rhs, xyz = f64p(), f64p(), f64p()
+        self._check(self.lib.ref_gen_hex(C.byref(pc), C.byref(n), C.byref(nn), C.byref(ptr),
+                                         C.byref(col), C.byref(val), C.byref(rhs), C.byref(xyz)))
+        N, NN = n.value, nn.value
+        nnzb = int(np.ctypeslib.as_array(ptr, shape=(NN + 1,))[NN])
+        out = GenProblem(N, NN, _copy(ptr, NN + 1, np.int64), _copy(col, nnzb, np.int64),
+                         _copy(val, 9 * nnzb, np.float64).reshape(-1, 3, 3),
+                         _copy(rhs, N, np.float64), _copy(xyz, 3 * NN, np.float64), self)
+        for p in (ptr, col, val, rhs, xyz):
+            self.lib.ref_free_buf(C.cast(p, vp))
+        return out
+
+    def force_isa(self, avx2: bool) -> bool:
+        """kernels::force_isa (kernels.hpp:25-28) for the CG dot/axpby;
+        returns whether AVX2 is active afterwards."""
+        return bool(self.lib.ref_force_isa(int(avx2)))
+
     def setup(self, n, ptr, col, val, B, params: Params = Params()):
         ptr = np.ascontiguousarray(ptr, np.int64)
         col = np.ascontiguousarray(col, np.int64)
@@ -357,6 +446,23 @@ class Ref(_Backend):
                                        params.smoother, params.smoother_omega,
                                        params.coarse_enough, params.stagnation_ratio,
                                        params.pipeline, C.byref(h)))
+        return RefHier(self, h, n)
+
+    def setup_bsr3(self, nbrows, ptr, col, val, B, params: Params = Params()):
+        """setup() of to_scalar(BSR3 input) (csr.hpp:327-353), formed inside
+        the reference driver."""
+        ptr = np.ascontiguousarray(ptr, np.int64)
+        col = np.ascontiguousarray(col, np.int64)
+        val = np.ascontiguousarray(val, np.float64)
+        n = 3 * nbrows
+        Bp, bc = (None, 0) if B is None else (_p(B := np.ascontiguousarray(B, np.float64)),
+                                               B.size // n)
+        h = vp()
+        self._check(self.lib.ref_setup_bsr3(nbrows, _p(ptr, i64p), _p(col, i64p), _p(val), Bp,
+                                            bc, params.eps_strong, params.omega,
+                                            params.smoother, params.smoother_omega,
+                                            params.coarse_enough, params.stagnation_ratio,
+                                            params.pipeline, C.byref(h)))
         return RefHier(self, h, n)
 
     def spmv_bsr3(self, nrows, ncols, ptr, col, val, x, alpha=1.0, beta=0.0, y=None):

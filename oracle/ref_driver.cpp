@@ -26,6 +26,15 @@
 #include "samg/coarsening.hpp"
 #include "samg/elasticity.hpp"
 #include "samg/hierarchy.hpp"
+#include "samg/kernels.hpp"
+
+// The repo's host problem generator (paper_2202_09056_b200/csrc/generator.cpp,
+// compiled into this library by oracle/Makefile as host-only C++): the
+// reference arm of bench.py and the golden scripts build the BASELINE
+// configs (free-DOF, heterogeneous, cantilever) without loading the product
+// library.  Input tooling only, not on any measured path.
+#include "problem.cuh"
+namespace samgb { samg_problem *generate_hex(const samg_problem_params &p); }
 
 using namespace samg;
 
@@ -146,6 +155,29 @@ int ref_generate_hex(int64_t nx, int64_t ny, int64_t nz, double E, double nu,
     GUARD_END
 }
 
+// The BASELINE-config generator (see the include above): BSR3 arrays,
+// right-hand side and node coordinates, malloc'd (ref_free_buf).
+int ref_gen_hex(const samg_problem_params *p, int64_t *n, int64_t *nnodes, int64_t **ptr,
+        int64_t **col, double **val, double **rhs, double **xyz) {
+    GUARD_BEGIN
+    std::unique_ptr<samg_problem> pb(samgb::generate_hex(*p));
+    *n = pb->n;
+    *nnodes = pb->nnodes;
+    *ptr = dup(pb->ptr);
+    *col = dup(pb->col);
+    *val = dup(pb->val);
+    *rhs = dup(pb->rhs);
+    *xyz = dup(pb->xyz);
+    GUARD_END
+}
+
+// kernels::force_isa (kernels.hpp:25-28): 0 = scalar, 1 = avx2 dot/axpby.
+// Returns the active ISA after the call (1 avx2, 0 scalar).
+int ref_force_isa(int which) {
+    kernels::force_isa(which ? kernels::isa::avx2 : kernels::isa::scalar);
+    return kernels::active_isa() == kernels::isa::avx2 ? 1 : 0;
+}
+
 int ref_rigid_body_modes(int64_t nnodes, const double *xyz, double *B) {
     GUARD_BEGIN
     node_coordinates c;
@@ -155,16 +187,10 @@ int ref_rigid_body_modes(int64_t nnodes, const double *xyz, double *B) {
     GUARD_END
 }
 
-int ref_setup(int64_t n, const int64_t *ptr, const int64_t *col,
-        const double *val, const double *B, int64_t bcols, double eps_strong,
+static void setup_impl(scalar_csr &&A, const double *B, int64_t bcols, double eps_strong,
         double omega, int smoother, double smoother_omega,
         int64_t coarse_enough, double stagnation_ratio, int pipeline_id, void **out) {
-    GUARD_BEGIN
-    scalar_csr A;
-    A.nrows = A.ncols = n;
-    A.ptr.assign(ptr, ptr + n + 1);
-    A.col.assign(col, col + ptr[n]);
-    A.val.assign(val, val + ptr[n]);
+    const int64_t n = A.nrows;
     std::optional<dense_columns> Bd;
     if (B) {
         dense_columns D(n, bcols);
@@ -234,6 +260,44 @@ int ref_setup(int64_t n, const int64_t *ptr, const int64_t *col,
         h->agg_count[l] = a.count;
     }
     *out = h.release();
+}
+
+int ref_setup(int64_t n, const int64_t *ptr, const int64_t *col,
+        const double *val, const double *B, int64_t bcols, double eps_strong,
+        double omega, int smoother, double smoother_omega,
+        int64_t coarse_enough, double stagnation_ratio, int pipeline_id, void **out) {
+    GUARD_BEGIN
+    scalar_csr A;
+    A.nrows = A.ncols = n;
+    A.ptr.assign(ptr, ptr + n + 1);
+    A.col.assign(col, col + ptr[n]);
+    A.val.assign(val, val + ptr[n]);
+    setup_impl(std::move(A), B, bcols, eps_strong, omega, smoother, smoother_omega,
+               coarse_enough, stagnation_ratio, pipeline_id, out);
+    GUARD_END
+}
+
+// The same from a 3x3 BSR input: the scalar CSR the reference's setup takes
+// is formed by its own to_scalar (csr.hpp:327-353, every block entry kept),
+// which is what the host generator's scalar view is -- without holding a
+// second scalar copy on the Python side (C3: 8 GB).
+int ref_setup_bsr3(int64_t nbrows, const int64_t *ptr, const int64_t *col,
+        const double *val, const double *B, int64_t bcols, double eps_strong,
+        double omega, int smoother, double smoother_omega,
+        int64_t coarse_enough, double stagnation_ratio, int pipeline_id, void **out) {
+    GUARD_BEGIN
+    scalar_csr A;
+    {
+        csr<block3> Ab;
+        Ab.nrows = Ab.ncols = nbrows;
+        Ab.ptr.assign(ptr, ptr + nbrows + 1);
+        Ab.col.assign(col, col + ptr[nbrows]);
+        Ab.val.resize(ptr[nbrows]);
+        std::memcpy(Ab.val.data(), val, sizeof(double) * 9 * ptr[nbrows]);
+        A = to_scalar(Ab);
+    }
+    setup_impl(std::move(A), B, bcols, eps_strong, omega, smoother, smoother_omega,
+               coarse_enough, stagnation_ratio, pipeline_id, out);
     GUARD_END
 }
 

@@ -51,12 +51,15 @@ class AmgParams:
     device: int = 0
     # "fp64" (the reference) or "mixed": fp32 operator copies for the V-cycle
     vcycle_precision: str = "fp64"
+    # hierarchy.hpp:382-401: recompute each coarse operator and compare
+    verify_galerkin: bool = False
 
     def c(self) -> AmgParamsC:
         return AmgParamsC(self.eps_strong, self.omega, self.point_block_size,
                           SMOOTHERS[self.smoother] if isinstance(self.smoother, str)
                           else int(self.smoother), self.smoother_omega, self.pre_sweeps,
-                          self.post_sweeps, self.coarse_enough, self.stagnation_ratio, 0,
+                          self.post_sweeps, self.coarse_enough, self.stagnation_ratio,
+                          int(self.verify_galerkin),
                           self.device, PRECISIONS[self.vcycle_precision])
 
 

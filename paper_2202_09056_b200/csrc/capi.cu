@@ -713,15 +713,11 @@ SAMG_API int samg_bsr3_spmv(const samg_bsr3 *mc, double alpha, const double *x, 
 // SpMV still keeps up and the copies run at the duplex PCIe rate: C1 e2e
 // 2 900 -> 3 920 GB/s-equivalent (scripts/e2e_sweep.sh).
 static int batch_cta_cap() {
-    static const int v = [] {
+    static const int env = [] {
         const char *e = std::getenv("SAMG_BATCH_CTAS");
-        if (e) return std::atoi(e);
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        return std::max(1, sms * 96 / 148);
+        return e ? std::atoi(e) : 0;
     }();
-    return v;
+    return env ? env : std::max(1, sm_count() * 96 / 148);
 }
 
 SAMG_API int samg_bsr3_spmv_batch(const samg_bsr3 *mc, double alpha, const double *x, double beta,
@@ -748,8 +744,11 @@ SAMG_API int samg_bsr3_spmv_batch(const samg_bsr3 *mc, double alpha, const doubl
             // x slot b: free once kernel k-P has read it
             if (k >= P) CK(cudaStreamWaitEvent(sh, m->ev_k[b], 0));
             CK(cudaMemcpyAsync(m->bx[b].p, x + k * nx, sizeof(double) * nx, cudaMemcpyHostToDevice, sh));
-            if (beta != 0.0)
+            if (beta != 0.0) {
+                // y slot b: step k-P's result must have been copied out first
+                if (k >= P) CK(cudaStreamWaitEvent(sh, m->ev_d[b], 0));
                 CK(cudaMemcpyAsync(m->by[b].p, y + k * ny, sizeof(double) * ny, cudaMemcpyHostToDevice, sh));
+            }
             CK(cudaEventRecord(m->ev_h[b], sh));
             // kernel k: its x has arrived, and y slot b has been copied out (step k-P)
             CK(cudaStreamWaitEvent(sk, m->ev_h[b], 0));
@@ -795,7 +794,8 @@ SAMG_API int samg_bsr3_dense_inverse(const samg_bsr3 *m, double *inv) {
         DevBuf<DevError> err(1, s);
         CK(cudaMemsetAsync(err.p, 0, sizeof(DevError), s));
         DevBuf<double> Ainv;
-        dense_inverse(A, Ainv, err.p, s);
+        if (!dense_inverse(A, Ainv, err.p, s))
+            fail(SAMG_ERROR, "dense_lu: singular coarse matrix (Gauss-Jordan pivot below 1e-300)");
         const int64_t n = 3 * A.nrows, ld = dense_ld(n);
         if (n)
             CK(cudaMemcpy2DAsync(inv, sizeof(double) * n, Ainv.p, sizeof(double) * ld,

@@ -629,16 +629,22 @@ void dispatch_rpw(int rpw, int nw, F f) {
 }
 
 PanelPlan plan_panel(int64_t n) {
-    static int reg_cluster = -1, smem_cluster = -1, smem_cap = 0;
-    if (reg_cluster < 0) {
-        int dev = 0;
+    // per device: the opt-in and the cluster limits are device attributes
+    static DeviceCache cap_cache, smem_cl_cache, reg_cl_cache;
+    const int smem_cap = cap_cache.get([] {
+        int dev = 0, cap = 0;
         CK(cudaGetDevice(&dev));
-        CK(cudaDeviceGetAttribute(&smem_cap, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-        smem_cap -= 4096;  // static shared memory of the kernel
-        CK(cudaFuncSetAttribute(k_panel_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap));
-        smem_cluster = cluster_limit(reinterpret_cast<const void *>(k_panel_cluster), kPT, smem_cap);
-        reg_cluster = cluster_limit(reinterpret_cast<const void *>(k_panel_reg<8, 32>), 32 * 32, 0);
-    }
+        CK(cudaDeviceGetAttribute(&cap, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        cap -= 4096;  // static shared memory of the kernel
+        CK(cudaFuncSetAttribute(k_panel_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, cap));
+        return cap;
+    });
+    const int smem_cluster = smem_cl_cache.get([&] {
+        return cluster_limit(reinterpret_cast<const void *>(k_panel_cluster), kPT, smem_cap);
+    });
+    const int reg_cluster = reg_cl_cache.get([] {
+        return cluster_limit(reinterpret_cast<const void *>(k_panel_reg<8, 32>), 32 * 32, 0);
+    });
     static const bool force_smem = [] {
         const char *e = std::getenv("SAMG_GJ_SMEM_PANEL");
         return e && e[0] == '1';
@@ -668,11 +674,11 @@ PanelPlan plan_panel(int64_t n) {
 
 } // namespace
 
-void dense_inverse(const Bsr3 &A, DevBuf<double> &Ainv, DevError *err, cudaStream_t s) {
+bool dense_inverse(const Bsr3 &A, DevBuf<double> &Ainv, DevError *err, cudaStream_t s) {
     const int64_t n = 3 * A.nrows;
     const int64_t ld = dense_ld(n);
     Ainv.alloc(n * ld, s);
-    if (n == 0) return;
+    if (n == 0) return true;
     const PanelPlan pp = plan_panel(n);
     DevBuf<double> X(n * ld, s), Rk(static_cast<int64_t>(pp.kB) * n + 1, s),
         T(static_cast<int64_t>(2 * pp.kB) * n + 1, s);
@@ -702,13 +708,13 @@ void dense_inverse(const Bsr3 &A, DevBuf<double> &Ainv, DevError *err, cudaStrea
         if (pp.reg) {
             dispatch_rpw(pp.rpw, pp.nw, [&](auto r, auto nw) {
                 constexpr int RPW = decltype(r)::value, NW = decltype(nw)::value;
-                static const bool nonportable = [] {
+                static DeviceCache nonportable;
+                nonportable.get([] {
                     const bool ok = cudaFuncSetAttribute(k_panel_reg<RPW, NW>,
                                         cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
                     cudaGetLastError();
-                    return ok;
-                }();
-                (void)nonportable;
+                    return ok ? 1 : 0;
+                });
                 CK(cudaLaunchKernelEx(&cfg, k_panel_reg<RPW, NW>, static_cast<int>(n), ld,
                                       static_cast<int>(k0), bk, pp.R, X.p, piv.p, err));
             });
@@ -735,7 +741,15 @@ void dense_inverse(const Bsr3 &A, DevBuf<double> &Ainv, DevError *err, cudaStrea
     CK(cudaMemcpyAsync(perm.p, hperm.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
     k_gather_cols<<<grid_for(n * ld), 256, 0, s>>>(n, ld, perm.p, X.p, sc.p, Ainv.p);
     CK_LAUNCH();
+    DevError h{};
+    CK(cudaMemcpyAsync(&h, err, sizeof h, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (h.code == SAMG_ERROR) {  // pivot below 1e-300: report, let the caller fall back
+        CK(cudaMemsetAsync(err, 0, sizeof(DevError), s));
+        return false;
+    }
     check_dev_error(err, s);
+    return true;
 }
 
 } // namespace samgb

@@ -190,12 +190,12 @@ void launch_lu_solve(const CoarseLu &lu, const double *f, double *u, cudaStream_
     const int n = static_cast<int>(lu.n);
     if (n == 0) return;
     const int smem = 3 * n * static_cast<int>(sizeof(double));
-    static const bool attr = [] {
+    static DeviceCache attr;
+    attr.get([] {
         CK(cudaFuncSetAttribute(k_lu_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 3 * kLuMaxN * static_cast<int>(sizeof(double))));
-        return true;
-    }();
-    (void)attr;
+        return 1;
+    });
     k_lu_solve<<<1, kLuThreads, smem, s>>>(n, lu.n, lu.X.p, lu.Lt.p, lu.perm.p, f, u);
     CK_LAUNCH();
 }

@@ -5,6 +5,8 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
+#include <climits>
 #include <cstdint>
 #include <cstdio>
 #include <stdexcept>
@@ -82,7 +84,29 @@ void h2d(void *dst, const void *src, size_t bytes, cudaStream_t s);
 void *pinned_small_alloc(size_t bytes);
 void pinned_small_free(void *p);
 
-// SM count of the current device (cached per process).
+// Per-device cache of an int computed once per device (function attributes
+// such as the dynamic shared-memory opt-in and cluster limits are per
+// device: a value cached per process would leave a second device's kernels
+// un-opted-in).  Racing first calls on one device both compute f(); harmless.
+constexpr int kMaxDevices = 64;
+struct DeviceCache {
+    std::atomic<int> v[kMaxDevices];
+    DeviceCache() { for (auto &x : v) x.store(INT_MIN, std::memory_order_relaxed); }
+    template <class F>
+    int get(F &&f) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+        std::atomic<int> &slot = v[dev & (kMaxDevices - 1)];
+        int x = slot.load(std::memory_order_acquire);
+        if (x == INT_MIN) {
+            x = f();
+            slot.store(x, std::memory_order_release);
+        }
+        return x;
+    }
+};
+
+// SM count of the current device (cached per device).
 int sm_count();
 
 } // namespace samgb

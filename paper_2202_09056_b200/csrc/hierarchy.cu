@@ -16,13 +16,13 @@
 namespace samgb {
 
 int sm_count() {
-    static int n = [] {
+    static DeviceCache cache;
+    return cache.get([] {
         int dev = 0, v = 148;
         if (cudaGetDevice(&dev) == cudaSuccess)
             cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
         return v;
-    }();
-    return n;
+    });
 }
 
 namespace {
@@ -39,7 +39,7 @@ uint64_t matrix_bytes(const Bsr3 &A) {
 
 } // namespace
 
-void choose_coarse_solver(Hierarchy &H, DevError *err, cudaStream_t s);
+void choose_coarse_solver(Hierarchy &H, DevError *err, cudaStream_t s, bool inverse_ok);
 
 Hierarchy::~Hierarchy() {
     if (stream) cudaStreamSynchronize(stream);
@@ -254,10 +254,26 @@ Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int6
         }
         mark("fp32_copies", L - 1);
     }
+    if (prm.verify_galerkin) {
+        // hierarchy.hpp:382-401: recompute every A_{i+1} as the scalar
+        // Galerkin product of the stored R_i, A_i, P_i (+ fix_decoupled_rows)
+        // and compare on the union pattern, relative squared Frobenius 1e-24
+        for (size_t i = 0; i + 1 < L; ++i) {
+            Bsr3 G;
+            galerkin(H->levels[i].R, H->levels[i].A, H->levels[i].P, G, s, true);
+            fix_decoupled_rows(G, s);
+            double dr[2];
+            union_diff(H->levels[i + 1].A, G, dr, s);
+            if (dr[0] > 1e-24 * dr[1])
+                fail(SAMG_ERROR, "setup: Galerkin consistency check failed on level " +
+                                     std::to_string(i));
+        }
+        mark("verify_galerkin", L - 1);
+    }
     H->nc = 3 * H->levels.back().A.nrows;
-    dense_inverse(H->levels.back().A, H->Ainv, err, s);
+    const bool inverse_ok = dense_inverse(H->levels.back().A, H->Ainv, err, s);
     mark("dense_inv", L - 1);
-    choose_coarse_solver(*H, err, s);
+    choose_coarse_solver(*H, err, s, inverse_ok);
     mark("coarse_check", L - 1);
     // V-cycle / CG workspace
     for (size_t i = 0; i < L; ++i) {
@@ -288,7 +304,7 @@ Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int6
 // and its solve is decided by rounding -- then (n <= kLuMaxN) the coarse
 // solve switches to the reference's own LU, bit-exact (coarse_lu.cu).
 // SAMG_COARSE_SOLVER=inverse|lu forces either.
-void choose_coarse_solver(Hierarchy &H, DevError *err, cudaStream_t s) {
+void choose_coarse_solver(Hierarchy &H, DevError *err, cudaStream_t s, bool inverse_ok) {
     static const int forced = [] {
         const char *e = std::getenv("SAMG_COARSE_SOLVER");
         if (!e) return 0;
@@ -296,8 +312,12 @@ void choose_coarse_solver(Hierarchy &H, DevError *err, cudaStream_t s) {
     }();
     const Bsr3 &Ac = H.levels.back().A;
     const int64_t n = H.nc;
-    bool use_lu = forced == 2;
-    if (forced == 0 && n > 0 && n <= kLuMaxN) {
+    bool use_lu = forced == 2 || !inverse_ok;
+    if (!inverse_ok && n > kLuMaxN)
+        fail(SAMG_ERROR, "dense coarse solve: Gauss-Jordan pivot below 1e-300 and the coarsest "
+                         "level (" + std::to_string(n) + " unknowns) is too large for the LU "
+                         "fallback");
+    if (!use_lu && forced == 0 && n > 0 && n <= kLuMaxN) {
         std::vector<double> hx(n);
         uint64_t st = 0x9e3779b97f4a7c15ull;
         for (auto &v : hx) {  // xorshift, uniform in [-1, 1)

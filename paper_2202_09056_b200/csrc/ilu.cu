@@ -378,12 +378,7 @@ constexpr int kSweepSmem = 8 * kWin * 9 * static_cast<int>(sizeof(double));
 // per SM -- the wavefront of a structured mesh offers a few hundred to a
 // few thousand independent rows, more warps would only wait.
 int persistent_grid(const void *kern, int64_t work_warps, int smem = 0, int per_sm_cap = 0) {
-    static int sms = [] {
-        int dev = 0, v = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-        return v;
-    }();
+    const int sms = sm_count();
     static const int per_sm = [] {
         const char *e = std::getenv("SAMG_ILU_CTAS_PER_SM");
         return e ? std::max(1, std::atoi(e)) : 1;
@@ -461,11 +456,11 @@ void setup_ilu0(const Bsr3 &A, Smoother &M, DevError *err, cudaStream_t s) {
     CK(cudaMemcpyAsync(M.lu.p, A.val.p, sizeof(double) * 9 * A.nnzb, cudaMemcpyDeviceToDevice, s));
     CK(cudaMemsetAsync(M.flags.p, 0, sizeof(int) * (A.nrows * kFS + 2), s));
     constexpr int fsmem = 8 * kFMax * (9 * static_cast<int>(sizeof(double)) + static_cast<int>(sizeof(int)));
-    static const bool fattr = [] {
+    static DeviceCache fattr;
+    fattr.get([] {
         CK(cudaFuncSetAttribute(k_ilu_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem));
-        return true;
-    }();
-    (void)fattr;
+        return 1;
+    });
     k_ilu_factor<<<persistent_grid(reinterpret_cast<const void *>(k_ilu_factor), n), 256, fsmem, s>>>(
         n, M.order.p, A.ptr.p, A.col.p, M.dpos.p, M.lu.p, M.data.p, M.flags.p,
         M.flags.p + static_cast<int64_t>(n) * kFS, err);
@@ -486,7 +481,8 @@ void launch_ilu_smooth(const Bsr3 *A, const Smoother &M, const double *f, const 
         launch_residual(*A, f, u_in, M.tmp.p, s, lowp);  // r = f - A u (hierarchy.hpp:213-215)
         rin = M.tmp.p;
     }
-    static const int gf = [] {
+    static DeviceCache gf_cache;
+    const int gf = gf_cache.get([] {
         for (const void *k : {reinterpret_cast<const void *>(k_ilu_sweep<true, true>),
                                reinterpret_cast<const void *>(k_ilu_sweep<false, false>),
                                reinterpret_cast<const void *>(k_ilu_sweep<false, true>)})
@@ -494,7 +490,7 @@ void launch_ilu_smooth(const Bsr3 *A, const Smoother &M, const double *f, const 
         const char *e = std::getenv("SAMG_ILU_CTAS_PER_SM");
         return persistent_grid(reinterpret_cast<const void *>(k_ilu_sweep<true, true>), 1 << 30, kSweepSmem,
                                e ? 0 : 2);
-    }();
+    });
     // warps for about kAhead dependency levels: a warp spins on the rows it
     // waits for, and warps far ahead of the wavefront only load L2 (coarse
     // levels have a few rows per level)

@@ -161,6 +161,9 @@ void galerkin_rows(const Bsr3 &Rl, const Bsr3 &A, const Bsr3 &P, const Bsr3 &R, 
 // rows [r0, r1) of M as a matrix of their own
 void slice_rows(const Bsr3 &M, int64_t r0, int64_t r1, Bsr3 &out, cudaStream_t s);
 void fix_decoupled_rows(Bsr3 &A, cudaStream_t s);
+// sum over the union pattern of (A - G)^2 and of G^2 (the Galerkin
+// consistency check, hierarchy.hpp:382-401); out[0] = diff, out[1] = ref
+void union_diff(const Bsr3 &A, const Bsr3 &G, double out[2], cudaStream_t s);
 // smoother setup: kind SAMG_SMOOTHER_*
 void setup_smoother(const Bsr3 &A, int kind, double omega, Smoother &M, DevError *err,
                     cudaStream_t s);
@@ -170,7 +173,9 @@ void setup_ilu0(const Bsr3 &A, Smoother &M, DevError *err, cudaStream_t s);
 void launch_ilu_smooth(const Bsr3 *A, const Smoother &M, const double *f, const double *u_in,
                        double *u_out, cudaStream_t s, bool lowp = false);
 // coarsest level: dense inverse (row-major n x n), n = 3*A.nrows
-void dense_inverse(const Bsr3 &A, DevBuf<double> &Ainv, DevError *err, cudaStream_t s);
+// false: a Gauss-Jordan pivot of the equilibrated matrix fell below 1e-300
+// (numerically singular; Ainv is then garbage -- fall back to the LU)
+bool dense_inverse(const Bsr3 &A, DevBuf<double> &Ainv, DevError *err, cudaStream_t s);
 // the reference's dense_lu (hierarchy.hpp:86-129), bit-exact (coarse_lu.cu):
 // for numerically singular coarse operators, where the explicit inverse and
 // the LU solve disagree

@@ -1778,18 +1778,14 @@ void spgemm_impl(const Bsr3 &A, const Bsr3 &B, Bsr3 &C, cudaStream_t s, const BC
         const int bm_bytes = (2 * words * 4 + 15) / 16 * 16;
         const int acc_cap = std::max(0, std::min(512, (budget - bm_bytes) / 72));
         const size_t smem_b = static_cast<size_t>(kBWPB) * (bm_bytes + static_cast<size_t>(acc_cap) * 72);
-        static const bool battr = [] {
+        static DeviceCache battr;
+        battr.get([] {
             CK(cudaFuncSetAttribute(k_spgemm_bnumeric<kScalar>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     220 * 1024));
-            return true;
-        }();
-        (void)battr;
-        static const bool battr2 = [] {
             CK(cudaFuncSetAttribute(k_spgemm_bnumeric<kScalar, true>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-            return true;
-        }();
-        (void)battr2;
+            return 1;
+        });
         if (pull)
             k_spgemm_bnumeric<kScalar, true><<<ceil_div(n, kBWPB), kBWPB * 32, smem_b, s>>>(
                 n, A.ptr.p, A.col.p, A.val.p, B.ptr.p, B.col.p, B.val.p, C.ptr.p, mode.p, winlo.p, words,
@@ -1928,6 +1924,51 @@ void galerkin_rows(const Bsr3 &Rl, const Bsr3 &A, const Bsr3 &P, const Bsr3 &R, 
     bp.cp = R.ptr.p; bp.ri = R.col.p; bp.pos = nullptr; bp.val = R.val.p; bp.tr = true;
     if (scalar_order) spgemm_impl<true>(RA, P, Ac, s, &bp);
     else spgemm_impl<false>(RA, P, Ac, s, &bp);
+}
+
+// thread per block row: merge the two sorted column lists (to_dense of both,
+// compared on the union pattern, hierarchy.hpp:390-396)
+__global__ void k_union_diff(int64_t n, const int *ap, const int *ac, const double *av,
+                             const int *gp, const int *gc, const double *gv, double *acc) {
+    double d = 0.0, r = 0.0;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        int ja = ap[i], jg = gp[i];
+        const int ea = ap[i + 1], eg = gp[i + 1];
+        while (ja < ea || jg < eg) {
+            const int ca = ja < ea ? ac[ja] : INT_MAX, cg = jg < eg ? gc[jg] : INT_MAX;
+            const double *x = ca <= cg ? av + 9LL * ja : nullptr;
+            const double *y = cg <= ca ? gv + 9LL * jg : nullptr;
+            for (int e = 0; e < 9; ++e) {
+                const double a = x ? x[e] : 0.0, g = y ? y[e] : 0.0;
+                d += (a - g) * (a - g);
+                r += g * g;
+            }
+            if (x) ++ja;
+            if (y) ++jg;
+        }
+    }
+    for (int o = 16; o; o >>= 1) {
+        d += __shfl_xor_sync(0xffffffffu, d, o);
+        r += __shfl_xor_sync(0xffffffffu, r, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(acc, d);
+        atomicAdd(acc + 1, r);
+    }
+}
+
+void union_diff(const Bsr3 &A, const Bsr3 &G, double out[2], cudaStream_t s) {
+    if (A.nrows != G.nrows || A.ncols != G.ncols)
+        fail(SAMG_ERROR, "setup: Galerkin consistency check: shapes differ");
+    DevBuf<double> acc(2, s);
+    CK(cudaMemsetAsync(acc.p, 0, 2 * sizeof(double), s));
+    if (A.nrows)
+        k_union_diff<<<std::min(ceil_div(A.nrows, 256), 4 * sm_count()), 256, 0, s>>>(
+            A.nrows, A.ptr.p, A.col.p, A.val.p, G.ptr.p, G.col.p, G.val.p, acc.p);
+    CK_LAUNCH();
+    CK(cudaMemcpyAsync(out, acc.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
 }
 
 void fix_decoupled_rows(Bsr3 &A, cudaStream_t s) {

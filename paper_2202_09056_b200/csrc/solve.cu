@@ -679,12 +679,7 @@ bool launch_tma(const Bsr3 &A, const VT *val, const double *x, Epi epi, double *
     cfg.stages = static_cast<int>(std::min<long long>(16, (budget - kTmaHdrBytes) / stage));
     if (cfg.stages < NT + 1) return false;
     const int smem = kTmaHdrBytes + static_cast<int>(cfg.stages * stage);
-    static int sms = [] {
-        int dev = 0, n = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        return n;
-    }();
+    const int sms = sm_count();
     // one persistent CTA per SM only pays off when every CTA streams many
     // chunks (C1: fine level 8 064 chunks, P0 4 032 -> TMA; A1 2 580 -> variant 1)
     static const int min_chunks_per_sm = env_int("SAMG_TMA_MIN_CHUNKS", 24);
@@ -696,7 +691,8 @@ bool launch_tma(const Bsr3 &A, const VT *val, const double *x, Epi epi, double *
         const int threads = 32 * (Sh::TW * Sh::NT + 1);
         // opt in to the largest dynamic size next to the static shared
         // memory of the reduction helpers
-        static const int max_dyn = [&] {
+        static DeviceCache max_dyn_cache;
+        const int max_dyn = max_dyn_cache.get([&] {
             int dev = 0, optin = 0;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
@@ -709,7 +705,7 @@ bool launch_tma(const Bsr3 &A, const VT *val, const double *x, Epi epi, double *
                 return 0;
             }
             return m;
-        }();
+        });
         if (smem > max_dyn) return;
         int occ = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);

@@ -230,6 +230,82 @@ def test_spmv_batch_matches_single(gpu):
     assert A.spmv_batch(np.zeros((0, p.n))).shape == (0, p.n)
 
 
+def test_spmv_batch_pinned_beta_pipeline(gpu):
+    """Pinned host buffers (asynchronous D2H), more steps than twice the
+    staging slots and beta != 0: a reused y slot must be copied out before
+    the next step's y is copied in (capi.cu samg_bsr3_spmv_batch)."""
+    import torch
+    pb = gpu
+    p = make_problem(pb, 9, dirichlet="eliminate")
+    A = pb.Bsr3.from_host(p.nbrows, p.nbrows, p.ptr, p.col, p.val.reshape(-1))
+    count = 23
+    rng = np.random.default_rng(13)
+    Xh = torch.empty((count, p.n), dtype=torch.float64, pin_memory=True).numpy()
+    Yh = torch.empty((count, p.n), dtype=torch.float64, pin_memory=True).numpy()
+    Xh[:] = rng.uniform(-1, 1, (count, p.n))
+    Y0 = rng.uniform(-1, 1, (count, p.n))
+    Yh[:] = Y0
+    for _ in range(3):  # repeated calls reuse the staging slots as well
+        Yh[:] = Y0
+        A.spmv_batch(Xh, 0.5, 0.25, Yh)
+        for k in range(count):
+            np.testing.assert_array_equal(Yh[k], A.spmv(Xh[k], 0.5, 0.25, Y0[k]))
+
+
+def test_verify_galerkin(gpu):
+    """amg_params::verify_galerkin (hierarchy.hpp:382-401): the setup
+    recomputes every coarse operator as the scalar R A P and compares; a
+    consistent hierarchy passes and is unchanged."""
+    pb = gpu
+    for kw, pl in ((dict(nx=9, ny=7, nz=5, dirichlet="eliminate", load="traction_xend"), "ns_block"),
+                   (dict(nx=6, dirichlet="keep_rows"), "ns_hybrid2"),
+                   (dict(nx=8, dirichlet="keep_rows"), "block")):
+        p = pb.generate_hex(**kw)
+        B = None if pl == "block" else p.nullspace()
+        prm = dict(smoother="spai0", coarse_enough=150)
+        h0 = pb.setup(p.csr(), B, pl, pb.AmgParams(**prm))
+        h1 = pb.setup(p.csr(), B, pl, pb.AmgParams(verify_galerkin=True, **prm))
+        assert h0.nlevels == h1.nlevels >= 2
+        for l in range(h0.nlevels):
+            np.testing.assert_array_equal(h0.level(l)[4], h1.level(l)[4])
+
+
+def test_dense_inverse_singular_is_reported(gpu):
+    """A singular coarse matrix: the Gauss-Jordan pivot check reports
+    samg::error (dense_lu: singular, hierarchy.hpp:100-104) instead of
+    returning garbage."""
+    pb = gpu
+    nb = 4
+    ptr = np.arange(nb + 1, dtype=np.int64)
+    col = np.arange(nb, dtype=np.int64)
+    val = np.zeros((nb, 3, 3))
+    for i in range(nb):
+        val[i] = np.eye(3)
+    val[2] = 0.0  # rows 6..8 all zero
+    A = pb.Bsr3.from_host(nb, nb, ptr, col, val.reshape(-1))
+    with pytest.raises(pb.SamgError):
+        A.dense_inverse()
+
+
+def test_second_device_after_first(gpu):
+    """Function attributes (dynamic shared memory opt-in, cluster limits)
+    are per device: setup + solve on device 1 after device 0 in the same
+    process (skipped with one visible device)."""
+    pb = gpu
+    if pb.device_count() < 2:
+        pytest.skip("needs two visible devices")
+    p = make_problem(pb, 50, dirichlet="eliminate", noise=0.01, seed=2)  # TMA SpMV engages
+    res = []
+    for dev in (0, 1):
+        h = pb.setup_bsr3(p.nbrows, p.ptr, p.col, p.val.reshape(-1), p.nullspace(), "ns_block",
+                          pb.AmgParams(device=dev))
+        u, rep = h.cg_solve(p.rhs)
+        assert rep["converged"], (dev, rep)
+        res.append(u)
+        h.close()
+    assert np.linalg.norm(res[0] - res[1]) <= 1e-12 * np.linalg.norm(res[0])
+
+
 def test_spmv_matches_reference(gpu, ref):
     pb = gpu
     p = make_problem(pb, 19, dirichlet="eliminate")
