@@ -40,6 +40,10 @@ struct Hierarchy {
     CgScalars *sc_stage = nullptr; // pinned staging for loop parameters
     cudaGraphExec_t cg_exec = nullptr;  // device-resident CG loop (while node)
     void build_cg_graph();
+    // keep the dense coarse inverse L2-resident across V-cycles (access
+    // policy window on the solve stream; SAMG_L2_PERSIST=0 disables)
+    size_t l2_window_bytes = 0;
+    void set_l2_residency();
 
     ~Hierarchy();
     int64_t finest_dim() const { return 3 * levels.front().A.nrows; }

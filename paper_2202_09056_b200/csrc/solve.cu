@@ -830,7 +830,7 @@ __global__ void __launch_bounds__(kGemvThreads) k_dense_gemv(int n, int64_t ld, 
     for (; j2 + 7 * T < n2; j2 += 8 * T) {
         double2 av[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) av[k] = __ldcs(a + j2 + k * T);
+        for (int k = 0; k < 8; ++k) av[k] = __ldg(a + j2 + k * T);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             const double2 fk = fpair(j2 + k * T);
@@ -839,7 +839,7 @@ __global__ void __launch_bounds__(kGemvThreads) k_dense_gemv(int n, int64_t ld, 
         }
     }
     for (; j2 < n2; j2 += T) {
-        const double2 a0 = __ldcs(a + j2);
+        const double2 a0 = __ldg(a + j2);
         const double2 f0 = fpair(j2);
         s = fma(a0.x, f0.x, s); t = fma(a0.y, f0.y, t);
     }

@@ -49,8 +49,12 @@ CONFIGS = {
            "spai0", 0.72, 1000),
     "C2": (dict(nx=95, ny=95, nz=95, dirichlet="eliminate", heterogeneous=True,
                 load="random", seed=2022), "jacobi", 0.5, 5000),
+    # C2's ns_block hierarchy has near-singular coarse diagonal blocks (the
+    # reference's block inverse throws singular_block there):
+    # no smoother converges, so C2 is pinned on the hierarchy and on a
+    # fixed number of SPAI0-PCG iterations
     "C2s": (dict(nx=95, ny=95, nz=95, dirichlet="eliminate", heterogeneous=True,
-                 load="random", seed=2022), "spai0", 0.72, 5000),
+                 load="random", seed=2022), "spai0", 0.72, 100),
     "C3": (dict(nx=511, ny=63, nz=63, lx=511 / 63, dirichlet="eliminate",
                 load="traction_xend", x_slowest=True), "spai0", 0.72, 5000),
     "C3i": (dict(nx=511, ny=63, nz=63, lx=511 / 63, dirichlet="eliminate",
@@ -79,8 +83,11 @@ def main():
     ap.add_argument("--smoother", default=None)
     ap.add_argument("--omega", type=float, default=None)
     ap.add_argument("--no-solve", action="store_true")
+    ap.add_argument("--maxit", type=int, default=None,
+                    help="CG iteration cap (C2: a fixed-iteration comparison)")
     args = ap.parse_args()
     kw, sm, om, maxit = CONFIGS[args.config]
+    maxit = args.maxit or maxit
     sm = args.smoother or sm
     om = args.omega if args.omega is not None else om
     ref = Ref()
