@@ -269,19 +269,27 @@ SAMG_API int samg_dist_pack(const samg_dist *d, const double *d_x,
 SAMG_API int samg_dist_spmv(const samg_dist *d, int part, double alpha,
         const double *d_xext, double beta, double *d_y, void *stream);
 
-/* ---- multi-GPU solve (one process per GPU, NCCL) ----
- * Every rank passes the same global fine matrix and nullspace; the
- * hierarchy is built on every rank (bit-identical), then each rank keeps its
- * rows of the levels with >= min_rows*nranks block rows (fine block rows
+/* ---- multi-GPU setup + solve (one process per GPU, NCCL; DESIGN.md s.6) --
+ * The setup is distributed: each rank builds only its rows of the levels
+ * with >= min_rows*nranks block rows (fine block rows
  * row_starts[rank]..row_starts[rank+1]; coarse rows follow the aggregates'
- * seeds), the smaller levels are replicated.  The V-cycle exchanges halos
- * with ncclSend/ncclRecv and CG all-reduces its dot products.  f and u are
- * the rank's rows (3 per block row).  Obtain the NCCL id on rank 0 with
- * samg_nccl_unique_id and broadcast it with your own transport.
- * id == NULL emulates all nranks in the calling process on one GPU (no
- * NCCL): every halo / all-reduce / gather becomes a device copy with the
- * same offsets and counts, and f and u are the global vectors.  This is the
- * single-GPU check of the partition and halo plans. */
+ * seeds: an aggregate belongs to the rank owning its seed node), fetching
+ * from the owners only the halo rows it needs; the node graph of the
+ * strength test is gathered so that every rank aggregates exactly as one
+ * GPU (coarsening.hpp:131-160).  The first level below the threshold is
+ * gathered and the rest set up and solved redundantly.  Every level is
+ * bit-identical to the single-GPU (and reference) hierarchy.  The V-cycle
+ * exchanges halos with ncclSend/ncclRecv and CG all-reduces its dot
+ * products.  f and u are the rank's rows (3 per block row).  Obtain the
+ * NCCL id on rank 0 with samg_nccl_unique_id and broadcast it.
+ * samg_dsetup: every rank passes the global matrix (host), only its rows are
+ * uploaded.  samg_dsetup_local / samg_dsetup_device: each rank passes only
+ * its rows (global column ids; ptr from 0) and its nullspace rows
+ * (3*nloc x b_cols, column-major), from host or device memory.
+ * id == NULL (samg_dsetup only) emulates all nranks in the calling process
+ * on one GPU (no NCCL): every exchange becomes a device copy with the same
+ * offsets and counts, and f and u are the global vectors.  This is the
+ * single-GPU check of the distributed setup and the halo plans. */
 typedef struct samg_dhierarchy samg_dhierarchy;
 SAMG_API int samg_nccl_unique_id(unsigned char id[128]);
 SAMG_API int samg_dsetup(const unsigned char id[128], int nranks, int rank,
@@ -292,12 +300,20 @@ SAMG_API int samg_dsetup(const unsigned char id[128], int nranks, int rank,
 SAMG_API int samg_ddestroy(samg_dhierarchy *h);
 SAMG_API int samg_dinfo(const samg_dhierarchy *h, int64_t *row0,
         int64_t *row1, int *nlevels, int *dist_levels, double *setup_seconds);
-/* Number of levels whose Galerkin product the setup formed row-sliced across
- * the ranks (each rank its own coarse rows, then assembled on every rank;
- * SAMG_DIST_SLICED_GALERKIN=0 disables it).  No reference counterpart. */
-SAMG_API int samg_dsliced_levels(const samg_dhierarchy *h, int *sliced_levels);
-/* Parity taps on the distributed hierarchy's global level matrices (every
- * rank holds them): as samg_level_info / samg_get_level. */
+SAMG_API int samg_dsetup_local(const unsigned char id[128], int nranks, int rank,
+        const int64_t *row_starts, const int64_t *ptr, const int64_t *col,
+        const double *val, const double *B, int64_t b_cols, int64_t min_rows,
+        int pipeline, const samg_amg_params *prm, samg_dhierarchy **out);
+SAMG_API int samg_dsetup_device(const unsigned char id[128], int nranks, int rank,
+        const int64_t *row_starts, const samg_bsr3 *A_local, const double *d_B,
+        int64_t b_cols, int64_t min_rows, int pipeline, const samg_amg_params *prm,
+        samg_dhierarchy **out);
+/* Block rows of A_0 the (first driven) rank held during the setup: its own
+ * rows plus the halo rows it fetched.  No reference counterpart. */
+SAMG_API int samg_dheld_rows(const samg_dhierarchy *h, int64_t *rows);
+/* Parity taps on the distributed hierarchy's level matrices, assembled from
+ * every rank's rows (collective over the ranks for a distributed level):
+ * as samg_level_info / samg_get_level. */
 SAMG_API int samg_dlevel_info(const samg_dhierarchy *h, int level, int which,
         int64_t *nrows, int64_t *ncols, int64_t *nnzb);
 SAMG_API int samg_dget_level(const samg_dhierarchy *h, int level, int which,

@@ -150,7 +150,11 @@ PROTOTYPES = {
                      i64, i64p, i64, C.c_int, C.POINTER(AmgParamsC), C.POINTER(vp)], C.c_int),
     "samg_ddestroy": ([vp], C.c_int),
     "samg_dinfo": ([vp, i64p, i64p, C.POINTER(C.c_int), C.POINTER(C.c_int), f64p], C.c_int),
-    "samg_dsliced_levels": ([vp, C.POINTER(C.c_int)], C.c_int),
+    "samg_dheld_rows": ([vp, i64p], C.c_int),
+    "samg_dsetup_local": ([C.POINTER(C.c_ubyte), C.c_int, C.c_int, i64p, i64p, i64p, f64p, f64p,
+                           i64, i64, C.c_int, C.POINTER(AmgParamsC), C.POINTER(vp)], C.c_int),
+    "samg_dsetup_device": ([C.POINTER(C.c_ubyte), C.c_int, C.c_int, i64p, vp, vp, i64, i64,
+                            C.c_int, C.POINTER(AmgParamsC), C.POINTER(vp)], C.c_int),
     "samg_dlevel_info": ([vp, C.c_int, C.c_int, i64p, i64p, i64p], C.c_int),
     "samg_dget_level": ([vp, C.c_int, C.c_int, i64p, i64p, f64p], C.c_int),
     "samg_dcg_solve_device": ([vp, vp, vp, C.POINTER(CgParamsC), C.POINTER(ReportC)], C.c_int),

@@ -7,6 +7,7 @@
 // plus a thread-local message.
 #include <chrono>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <string>
 #include <vector>
@@ -53,8 +54,8 @@ void generate_hex_device(const samg_problem_params &p, Bsr3 &A, DevBuf<double> &
                          DevBuf<double> &xyz, DevBuf<double> &B, int64_t &nnodes, cudaStream_t s);
 void rigid_body_modes(int64_t nnodes, const double *xyz, double *B);
 struct DHierarchy;
-DHierarchy *dsetup_all(const unsigned char *id, int nranks, int rank, Bsr3 &&A0,
-                       const double *B, int64_t b_rows, int64_t b_cols,
+DHierarchy *dsetup_all(const unsigned char *id, int nranks, int rank, int64_t nbrows,
+                       Bsr3 &&A_rows, const double *B, int64_t b_cols,
                        const int64_t *row_starts, int64_t min_rows, const samg_amg_params &prm,
                        cudaStream_t s, double t0, int pipeline);
 void ddelete(DHierarchy *d);
@@ -63,8 +64,8 @@ samg_solve_report dcg(DHierarchy *d, const double *f, double *u, const samg_cg_p
 void dinfo(const DHierarchy *d, int64_t *row0, int64_t *row1, int *nlevels, int *dist_levels,
            double *setup_s);
 void nccl_unique_id(unsigned char *out);
-int dsliced_levels(const DHierarchy *d);
-const Hierarchy &dfull(const DHierarchy *d);
+int64_t dheld_rows(const DHierarchy *d);
+const Bsr3 &dlevel(DHierarchy *d, int level, int which, Bsr3 &tmp);
 }
 
 struct samg_dproblem {
@@ -677,7 +678,17 @@ SAMG_API int samg_bsr3_spmv_device(const samg_bsr3 *m, double alpha, const doubl
         require(m && m->m, SAMG_INVALID_ARGUMENT, "NULL matrix");
         require(reinterpret_cast<uintptr_t>(d_x) % 16 == 0, SAMG_INVALID_ARGUMENT,
                 "spmv: x must be 16-byte aligned (the kernel gathers x with 16-byte loads)");
-        launch_spmv(*m->m, alpha, d_x, beta, d_y, static_cast<cudaStream_t>(stream));
+        // consecutive standalone SpMVs overlap: the next one's matrix stream
+        // starts under the previous one's tail (programmatic dependent
+        // launch; x is read only once the previous kernel completed)
+        set_spmv_pdl(true);
+        try {
+            launch_spmv(*m->m, alpha, d_x, beta, d_y, static_cast<cudaStream_t>(stream));
+        } catch (...) {
+            set_spmv_pdl(false);
+            throw;
+        }
+        set_spmv_pdl(false);
     });
 }
 
@@ -914,6 +925,36 @@ SAMG_API int samg_nccl_unique_id(unsigned char id[128]) {
     });
 }
 
+namespace {
+// shared tail of the samg_dsetup* entry points: `rows` are this process's
+// input rows (the whole matrix when emulating), B likewise
+void dsetup_entry(const unsigned char *id, int nranks, int rank, int64_t nbrows,
+                  const std::function<void(Bsr3 &, cudaStream_t)> &rows, const double *B,
+                  int64_t b_cols, const int64_t *row_starts, int64_t min_rows, int pipeline,
+                  const samg_amg_params *prm, samg_dhierarchy **out, double t0) {
+    require(out && nranks >= 1 && rank >= 0 && rank < nranks, SAMG_INVALID_ARGUMENT,
+            "dsetup: bad arguments");
+    *out = nullptr;
+    validate_params(prm, pipeline);
+    if (prm->vcycle_precision != SAMG_PRECISION_FP64)
+        fail(SAMG_UNSUPPORTED, "dsetup: the mixed-precision V-cycle is single-GPU only");
+    need_device(prm->device);
+    cudaStream_t s = new_stream();
+    try {
+        Bsr3 A;
+        rows(A, s);
+        auto h = std::make_unique<samg_dhierarchy>();
+        h->d = dsetup_all(id, nranks, rank, nbrows, std::move(A), B, b_cols, row_starts,
+                          min_rows > 0 ? min_rows : 4096, *prm, s, t0, pipeline);
+        *out = h.release();
+    } catch (...) {
+        cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+        throw;
+    }
+}
+}  // namespace
+
 SAMG_API int samg_dsetup(const unsigned char id[128], int nranks, int rank, int64_t nbrows,
                          const int64_t *ptr, const int64_t *col, const double *val,
                          const double *B, int64_t b_rows, int64_t b_cols,
@@ -921,27 +962,74 @@ SAMG_API int samg_dsetup(const unsigned char id[128], int nranks, int rank, int6
                          const samg_amg_params *prm, samg_dhierarchy **out) {
     return guarded([&] {
         const double t0 = now_s();
-        require(out && nranks >= 1 && rank >= 0 && rank < nranks, SAMG_INVALID_ARGUMENT,
+        require(ptr && nranks >= 1 && rank >= 0 && rank < nranks, SAMG_INVALID_ARGUMENT,
                 "dsetup: bad arguments");
-        *out = nullptr;
-        validate_params(prm, pipeline);
         validate_ns(3 * nbrows, B, b_rows, b_cols, pipeline);
-        if (prm->vcycle_precision != SAMG_PRECISION_FP64)
-            fail(SAMG_UNSUPPORTED, "dsetup: the mixed-precision V-cycle is single-GPU only");
-        need_device(prm->device);
-        cudaStream_t s = new_stream();
-        try {
-            Bsr3 A0;
-            upload_bsr3(nbrows, nbrows, ptr, col, val, A0, s);
-            auto h = std::make_unique<samg_dhierarchy>();
-            h->d = dsetup_all(id, nranks, rank, std::move(A0), B, b_rows, b_cols, row_starts,
-                              min_rows > 0 ? min_rows : 4096, *prm, s, t0, pipeline);
-            *out = h.release();
-        } catch (...) {
-            cudaStreamSynchronize(s);
-            cudaStreamDestroy(s);
-            throw;
+        // NCCL: only this rank's rows go to the device (the partition is
+        // row_starts, or the even split)
+        int64_t r0 = 0, r1 = nbrows;
+        if (id) {
+            r0 = row_starts ? row_starts[rank] : nbrows * rank / nranks;
+            r1 = row_starts ? row_starts[rank + 1] : nbrows * (rank + 1) / nranks;
+            require(0 <= r0 && r0 <= r1 && r1 <= nbrows, SAMG_INVALID_ARGUMENT, "dsetup: bad row_starts");
         }
+        std::vector<int64_t> lp(r1 - r0 + 1);
+        for (int64_t i = r0; i <= r1; ++i) lp[i - r0] = ptr[i] - ptr[r0];
+        std::vector<double> Bl;
+        const double *Bp = B;
+        if (id && B && pipeline != SAMG_PIPELINE_BLOCK) {
+            const int64_t n3 = 3 * (r1 - r0);
+            Bl.resize(n3 * b_cols);
+            for (int64_t c = 0; c < b_cols; ++c)
+                std::memcpy(Bl.data() + c * n3, B + c * 3 * nbrows + 3 * r0, sizeof(double) * n3);
+            Bp = Bl.data();
+        }
+        dsetup_entry(id, nranks, rank, nbrows, [&](Bsr3 &A, cudaStream_t s) {
+            upload_bsr3(r1 - r0, nbrows, lp.data(), col + ptr[r0], val + 9 * ptr[r0], A, s);
+        }, Bp, b_cols, row_starts, min_rows, pipeline, prm, out, t0);
+    });
+}
+
+SAMG_API int samg_dsetup_local(const unsigned char id[128], int nranks, int rank,
+                               const int64_t *row_starts, const int64_t *ptr, const int64_t *col,
+                               const double *val, const double *B, int64_t b_cols,
+                               int64_t min_rows, int pipeline, const samg_amg_params *prm,
+                               samg_dhierarchy **out) {
+    return guarded([&] {
+        const double t0 = now_s();
+        require(id && row_starts && ptr && nranks >= 1 && rank >= 0 && rank < nranks,
+                SAMG_INVALID_ARGUMENT, "dsetup_local: bad arguments (NCCL id and row_starts required)");
+        const int64_t nbrows = row_starts[nranks], nl = row_starts[rank + 1] - row_starts[rank];
+        if (pipeline != SAMG_PIPELINE_BLOCK && (!B || b_cols <= 0))
+            fail(SAMG_BAD_NULLSPACE_SHAPE, "dsetup_local: the ns pipelines need the nullspace rows");
+        dsetup_entry(id, nranks, rank, nbrows, [&](Bsr3 &A, cudaStream_t s) {
+            upload_bsr3(nl, nbrows, ptr, col, val, A, s);
+        }, B, b_cols, row_starts, min_rows, pipeline, prm, out, t0);
+    });
+}
+
+SAMG_API int samg_dsetup_device(const unsigned char id[128], int nranks, int rank,
+                                const int64_t *row_starts, const samg_bsr3 *A_local,
+                                const double *d_B, int64_t b_cols, int64_t min_rows, int pipeline,
+                                const samg_amg_params *prm, samg_dhierarchy **out) {
+    return guarded([&] {
+        const double t0 = now_s();
+        require(id && row_starts && A_local && A_local->m && nranks >= 1 && rank >= 0 && rank < nranks,
+                SAMG_INVALID_ARGUMENT, "dsetup_device: bad arguments (NCCL id and row_starts required)");
+        const int64_t nbrows = row_starts[nranks];
+        if (A_local->m->nrows != row_starts[rank + 1] - row_starts[rank] || A_local->m->ncols != nbrows)
+            fail(SAMG_DIMENSION_MISMATCH, "dsetup_device: local rows disagree with row_starts");
+        if (pipeline != SAMG_PIPELINE_BLOCK && (!d_B || b_cols <= 0))
+            fail(SAMG_BAD_NULLSPACE_SHAPE, "dsetup_device: the ns pipelines need the nullspace rows");
+        dsetup_entry(id, nranks, rank, nbrows, [&](Bsr3 &A, cudaStream_t s) {
+            const Bsr3 &M = *A_local->m;
+            A.alloc(M.nrows, M.ncols, M.nnzb, s);
+            CK(cudaMemcpyAsync(A.ptr.p, M.ptr.p, sizeof(int) * (M.nrows + 1), cudaMemcpyDeviceToDevice, s));
+            if (M.nnzb) {
+                CK(cudaMemcpyAsync(A.col.p, M.col.p, sizeof(int) * M.nnzb, cudaMemcpyDeviceToDevice, s));
+                CK(cudaMemcpyAsync(A.val.p, M.val.p, sizeof(double) * 9 * M.nnzb, cudaMemcpyDeviceToDevice, s));
+            }
+        }, d_B, b_cols, row_starts, min_rows, pipeline, prm, out, t0);
     });
 }
 
@@ -961,10 +1049,10 @@ SAMG_API int samg_dinfo(const samg_dhierarchy *h, int64_t *row0, int64_t *row1, 
     });
 }
 
-SAMG_API int samg_dsliced_levels(const samg_dhierarchy *h, int *sliced_levels) {
+SAMG_API int samg_dheld_rows(const samg_dhierarchy *h, int64_t *rows) {
     return guarded([&] {
-        require(h && h->d && sliced_levels, SAMG_INVALID_ARGUMENT, "NULL argument");
-        *sliced_levels = dsliced_levels(h->d);
+        require(h && h->d && rows, SAMG_INVALID_ARGUMENT, "NULL argument");
+        *rows = dheld_rows(h->d);
     });
 }
 
@@ -972,7 +1060,8 @@ SAMG_API int samg_dlevel_info(const samg_dhierarchy *h, int level, int which, in
                               int64_t *ncols, int64_t *nnzb) {
     return guarded([&] {
         require(h && h->d, SAMG_INVALID_ARGUMENT, "NULL hierarchy");
-        const Bsr3 &M = level_mat(dfull(h->d), level, which);
+        Bsr3 tmp;
+        const Bsr3 &M = dlevel(h->d, level, which, tmp);
         *nrows = M.nrows;
         *ncols = M.ncols;
         *nnzb = M.nnzb;
@@ -983,9 +1072,9 @@ SAMG_API int samg_dget_level(const samg_dhierarchy *h, int level, int which, int
                              int64_t *col, double *val) {
     return guarded([&] {
         require(h && h->d, SAMG_INVALID_ARGUMENT, "NULL hierarchy");
-        const samgb::Hierarchy &H = dfull(h->d);
-        CK(cudaSetDevice(H.device));
-        download_bsr3(level_mat(H, level, which), ptr, col, val, H.stream);
+        Bsr3 tmp;
+        const Bsr3 &M = dlevel(h->d, level, which, tmp);
+        download_bsr3(M, ptr, col, val, nullptr);
     });
 }
 

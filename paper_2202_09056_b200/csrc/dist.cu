@@ -87,6 +87,18 @@ samg_dist *dist_create(int64_t row0, int64_t row1, const int64_t *ptr, const int
         (bnd ? d->boundary : d->interior).push_back(static_cast<int>(i));
     }
     d->val.assign(val + 9 * base, val + 9 * (base + nnz));
+    // the longest run of interior rows (slab partitions: all but the first
+    // and last node layers): one contiguous row view, so it streams through
+    // the TMA-fed SpMV like a whole matrix
+    {
+        std::vector<unsigned char> isb(nl, 0);
+        for (int b : d->boundary) isb[b] = 1;
+        int64_t best = 0, run = 0;
+        for (int64_t i = 0; i < nl; ++i) {
+            run = isb[i] ? 0 : run + 1;
+            if (run > best) { best = run; d->ib = i + 1; d->ia = i + 1 - run; }
+        }
+    }
     // recv plan: ghosts grouped by owner (sorted ids + contiguous ranges)
     int64_t k = 0;
     while (k < d->nghost) {
@@ -159,12 +171,22 @@ void dist_pack(const samg_dist *d, const double *x, double *buf, cudaStream_t s)
     CK_LAUNCH();
 }
 
+// part 0: the interior run [ia, ib) (reads no ghost: runs while the halo is
+// in flight); part 1: the other rows [0, ia) and [ib, nloc).  Row views of
+// the local matrix: the same per-row arithmetic as one launch over all rows.
 void dist_spmv(const samg_dist *d, int part, double alpha, const double *xext, double beta,
                double *y, cudaStream_t s) {
-    const DevBuf<int> &rows = part == 0 ? d->d_interior : d->d_boundary;
-    const int64_t n = static_cast<int64_t>(part == 0 ? d->interior.size() : d->boundary.size());
-    if (n == 0) return;
-    launch_spmv_rows(d->A, rows.p, n, d->group, alpha, xext, beta, y, s);
+    auto run = [&](int64_t a, int64_t b) {
+        if (b <= a) return;
+        RowView v(d->A, a, b);
+        launch_spmv(v.m, alpha, xext, beta, y + 3 * a, s);
+    };
+    if (part == 0) {
+        run(d->ia, d->ib);
+    } else {
+        run(0, d->ia);
+        run(d->ib, d->nloc);
+    }
 }
 
 } // namespace samgb

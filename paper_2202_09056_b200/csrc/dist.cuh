@@ -17,6 +17,8 @@ struct samg_dist {
     std::vector<int64_t> recv_counts, recv_offsets, send_counts, send_offsets;
     std::vector<int64_t> send_idx;   // local block rows, per send peer in order
     std::vector<int> interior, boundary;
+    int64_t ia = 0, ib = 0;          // longest run of interior rows (multiplied
+                                     // by one contiguous launch while the halo flies)
     bool send_set = false;
     samgb::Bsr3 A;
     samgb::DevBuf<int> d_interior, d_boundary, d_send_idx;

@@ -1,23 +1,24 @@
 // dsolve.cu -- multi-GPU solve: row-partitioned V-cycle + PCG over NCCL.
 //
-// One process per GPU (rank).  Every rank builds the same hierarchy with the
-// single-GPU setup (deterministic, bit-identical on every rank and to the
-// reference), then keeps only its rows of the large levels:
+// One process per GPU (rank).  The setup is distributed (dsetup.cu): every
+// rank builds only its rows of the large levels,
 //   * level l (l < Ld) is row-partitioned: fine block rows [f0, f1) of A_l,
 //     P_l, the smoother, and coarse block rows [c0, c1) of R_l.  The coarse
 //     partition follows the aggregation: aggregate g belongs to the rank that
 //     owns its pass-1 seed node, and aggregate ids are numbered in seed order
 //     (coarsening.hpp:136-146), so every rank's coarse rows are contiguous;
 //   * levels l >= Ld (fewer than min_rows * nranks block rows, or a rank
-//     would own none) are replicated: f_Ld is gathered on every rank (grouped
-//     ncclBroadcast) and the coarse V-cycle runs redundantly, so the
-//     prolongation into level Ld-1 needs no halo.
+//     would own none) are gathered once and replicated: f_Ld is gathered on
+//     every rank (grouped ncclBroadcast) and the coarse V-cycle runs
+//     redundantly, so the prolongation into level Ld-1 needs no halo.
 // Every local SpMV reads a halo-extended vector: owned entries first, then
-// the ghosts sorted by global id (grouped by owner).  Because all ranks hold
-// all matrices, each rank derives both sides of every halo plan locally (no
-// plan exchange).  A halo exchange is pack kernel + grouped ncclSend/ncclRecv
-// on the solve stream.  CG dot products are local fused reductions (the same
-// kernels as on one GPU, in STORE mode) + a one-double ncclAllReduce.
+// the ghosts sorted by global id (grouped by owner).  The halo plans are
+// derived locally: a rank's ghosts are the columns its rows read outside its
+// range, and what it sends to rank p are the owned entries p's rows read --
+// the rows of the transposed operator (A for A, P for R, R for P) that hold
+// a column in p's row range.  A halo exchange is pack kernel + grouped
+// ncclSend/ncclRecv.  CG dot products are local fused reductions (the same
+// kernels as on one GPU, in STORE mode) + one ncclAllReduce.
 //
 // The same code drives an *emulated* group (comm == nullptr): all ranks'
 // slices live in one process on one GPU and every communication step is
@@ -36,15 +37,10 @@
 
 #include <cub/cub.cuh>
 
+#include "dsetup.cuh"
 #include "hierarchy.cuh"
 
 namespace samgb {
-
-inline void nccl_check(ncclResult_t r, const char *what) {
-    if (r != ncclSuccess)
-        fail(SAMG_NCCL_ERROR, std::string(what) + " failed: " + nccl().GetErrorString(r));
-}
-#define NK(x) ::samgb::nccl_check((x), #x)
 
 namespace {
 
@@ -63,11 +59,14 @@ struct ScSet {
     int n;
 };
 
-// emulated all-reduce of CgScalars::tmp (sum in rank order)
-__global__ void k_sum_tmp(ScSet s) {
-    double t = 0;
-    for (int i = 0; i < s.n; ++i) t += s.p[i]->tmp;
-    for (int i = 0; i < s.n; ++i) s.p[i]->tmp = t;
+// emulated all-reduce of CgScalars::tmp (and tmp2), sums in rank order
+__global__ void k_sum_tmp(ScSet s, int two) {
+    double t = 0, t2 = 0;
+    for (int i = 0; i < s.n; ++i) { t += s.p[i]->tmp; t2 += s.p[i]->tmp2; }
+    for (int i = 0; i < s.n; ++i) {
+        s.p[i]->tmp = t;
+        if (two) s.p[i]->tmp2 = t2;
+    }
 }
 
 
@@ -160,6 +159,16 @@ __global__ void k_compact(int64_t n, const int *flag, const int *scan, int *out)
          k += static_cast<int64_t>(gridDim.x) * blockDim.x)
         if (flag[k]) out[scan[k]] = static_cast<int>(k);
 }
+// flag[x] = 1 if row x of T has a column in [lo, hi)
+__global__ void k_rows_reading(int64_t n, const int *ptr, const int *col, int64_t lo, int64_t hi,
+                               int *flag) {
+    for (int64_t x = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; x < n;
+         x += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        int f = 0;
+        for (int e = ptr[x]; e < ptr[x + 1] && !f; ++e) f = col[e] >= lo && col[e] < hi;
+        flag[x] = f;
+    }
+}
 __global__ void k_rebase_ptr(int64_t n, const int *ptr, int base, int *out) {
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -189,31 +198,25 @@ int64_t scan_flags(const int *flag, int *scan, int64_t n, cudaStream_t s) {
     return total;
 }
 
-// Rank r's slice of the (device, global) matrix G whose rows are partitioned
-// by row_starts and whose column space is partitioned by col_starts: rows
-// [r0, r1) with columns renumbered into the halo-extended vector (owned
-// first, then the ghosts in ascending global id, i.e. grouped by owner), the
-// receive plan (ghost counts per owner) and the send plan (the owned columns
-// every other rank's slice reads, ascending).  All on the device: flag
-// arrays + scans, O(nnz + ncols) per rank, a few scalars to the host.
-void build_local(const Bsr3 &G, const std::vector<int64_t> &row_starts,
-                 const std::vector<int64_t> &col_starts, int rank, bool global_cols,
-                 LocalMat &out, cudaStream_t s) {
+// A rank's local operator from its own rows M (rows [row_starts[rank],
+// row_starts[rank+1]) of the row space, global column ids in the column
+// space partitioned by col_starts): columns renumbered into the
+// halo-extended vector (owned first, then the ghosts in ascending global id,
+// i.e. grouped by owner), the receive plan (ghost counts per owner) and the
+// send plan.  The send plan comes from T, the rank's rows of the transposed
+// operator (its owned column-space entries as rows, global ids of M's row
+// space as columns): peer p reads the owned entries whose T row has a column
+// in p's row range (pattern(T) = pattern(M^T): A is structurally symmetric,
+// R = P^T exactly).  global_cols: keep global columns, no plan (the
+// prolongation from a replicated level).  All on the device: flag arrays +
+// scans, a few scalars to the host.
+void build_local_rows(const Bsr3 &M, const Bsr3 *T, const std::vector<int64_t> &row_starts,
+                      const std::vector<int64_t> &col_starts, int rank, bool global_cols,
+                      LocalMat &out, cudaStream_t s) {
     const int nranks = static_cast<int>(row_starts.size()) - 1;
-    // the row bounds of every rank's slice
-    std::vector<int> bnd(nranks + 1);
-    {
-        DevBuf<int64_t> ridx(nranks + 1, s);
-        DevBuf<int> rb(nranks + 1, s);
-        CK(cudaMemcpyAsync(ridx.p, row_starts.data(), sizeof(int64_t) * (nranks + 1), cudaMemcpyHostToDevice, s));
-        k_gather_ptr<<<1, 32, 0, s>>>(nranks + 1, ridx.p, G.ptr.p, rb.p);
-        CK(cudaMemcpyAsync(bnd.data(), rb.p, sizeof(int) * (nranks + 1), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-    }
-    const int64_t r0 = row_starts[rank], r1 = row_starts[rank + 1];
     const int64_t c0 = col_starts[rank], c1 = col_starts[rank + 1];
-    const int64_t nl = r1 - r0, base = bnd[rank], nnz = bnd[rank + 1] - base;
-    const int64_t ncg = G.ncols;
+    const int64_t nl = M.nrows, nnz = M.nnzb;
+    const int64_t ncg = col_starts[nranks];
     HaloPlan &pl = out.plan;
     DevBuf<int> gscan;
     if (!global_cols) {
@@ -222,7 +225,7 @@ void build_local(const Bsr3 &G, const std::vector<int64_t> &row_starts,
         DevBuf<int> gflag(ncg + 1, s);
         gscan.alloc(ncg + 1, s);
         CK(cudaMemsetAsync(gflag.p, 0, sizeof(int) * (ncg + 1), s));
-        if (nnz) k_mark_cols<<<grid_of(nnz), 256, 0, s>>>(nnz, G.col.p + base, c0, c1, false, gflag.p);
+        if (nnz) k_mark_cols<<<grid_of(nnz), 256, 0, s>>>(nnz, M.col.p, c0, c1, false, gflag.p);
         pl.nghost = scan_flags(gflag.p, gscan.p, ncg, s);
         // receive plan: ghosts per owner = scan differences at the owners' bounds
         std::vector<int> at(nranks + 1);
@@ -240,17 +243,17 @@ void build_local(const Bsr3 &G, const std::vector<int64_t> &row_starts,
                 pl.recv_counts.push_back(at[q + 1] - at[q]);
                 pl.recv_offsets.push_back(at[q]);
             }
-        // send plan: for every other rank, the owned columns its rows read
+        // send plan: for every other rank, the owned entries whose row of T
+        // reads that rank's rows
         const int64_t nown = c1 - c0;
         DevBuf<int> sflag(nown + 1, s), sscan(nown + 1, s);
         std::vector<DevBuf<int>> parts;
         int64_t total = 0;
         for (int q = 0; q < nranks; ++q) {
-            if (q == rank) continue;
-            const int64_t qb = bnd[q], qn = bnd[q + 1] - bnd[q];
-            if (!qn || !nown) continue;
+            if (q == rank || !nown) continue;
             CK(cudaMemsetAsync(sflag.p, 0, sizeof(int) * (nown + 1), s));
-            k_mark_cols<<<grid_of(qn), 256, 0, s>>>(qn, G.col.p + qb, c0, c1, true, sflag.p);
+            k_rows_reading<<<grid_of(nown), 256, 0, s>>>(nown, T->ptr.p, T->col.p, row_starts[q],
+                                                        row_starts[q + 1], sflag.p);
             const int64_t cnt = scan_flags(sflag.p, sscan.p, nown, s);
             if (!cnt) continue;
             parts.emplace_back(cnt, s);
@@ -270,11 +273,11 @@ void build_local(const Bsr3 &G, const std::vector<int64_t> &row_starts,
     }
     Bsr3 &A = out.A;
     A.alloc(nl, global_cols ? ncg : pl.nloc + pl.nghost, nnz, s);
-    k_rebase_ptr<<<grid_of(nl + 1), 256, 0, s>>>(nl + 1, G.ptr.p + r0, static_cast<int>(base), A.ptr.p);
+    CK(cudaMemcpyAsync(A.ptr.p, M.ptr.p, sizeof(int) * (nl + 1), cudaMemcpyDeviceToDevice, s));
     if (nnz) {
-        k_renumber<<<grid_of(nnz), 256, 0, s>>>(nnz, G.col.p + base, c0, c1, pl.nloc, gscan.p, global_cols,
+        k_renumber<<<grid_of(nnz), 256, 0, s>>>(nnz, M.col.p, c0, c1, pl.nloc, gscan.p, global_cols,
                                                A.col.p);
-        CK(cudaMemcpyAsync(A.val.p, G.val.p + 9 * base, sizeof(double) * 9 * nnz, cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(A.val.p, M.val.p, sizeof(double) * 9 * nnz, cudaMemcpyDeviceToDevice, s));
     }
     CK_LAUNCH();
     out.ia = out.ib = 0;
@@ -294,23 +297,6 @@ void build_local(const Bsr3 &G, const std::vector<int64_t> &row_starts,
     CK(cudaStreamSynchronize(s));  // the temporaries above are freed on s
 }
 
-// Rows [r0, r1) of M as a non-owning matrix (ptr offset; col / val shared,
-// so the ptr values stay absolute).  Vectors indexed by row (f, u, out, M)
-// are offset by the caller.
-struct RowView {
-    Bsr3 m;
-    RowView(const Bsr3 &src, int64_t r0, int64_t r1) {
-        m.nrows = r1 - r0;
-        m.ncols = src.ncols;
-        m.nnzb = src.nnzb;  // bounds of the shared arrays (the TMA path's end checks)
-        m.ptr.p = src.ptr.p + r0;
-        m.col.p = src.col.p;
-        m.val.p = src.val.p;
-        m.val32.p = src.val32.p;
-    }
-    RowView(const RowView &) = delete;
-    ~RowView() { m.ptr.p = nullptr; m.col.p = nullptr; m.val.p = nullptr; m.val32.p = nullptr; }
-};
 struct SmootherView {
     Smoother m;
     SmootherView(const Smoother &src, int64_t r0) {
@@ -341,28 +327,48 @@ struct DRank {
 struct DHierarchy {
     int nranks = 1, device = 0;
     ncclComm_t comm = nullptr;   // nullptr: every rank emulated in this process
-    std::unique_ptr<Hierarchy> H;
+    cudaStream_t s = nullptr;    // the solve stream (owned)
+    samg_amg_params prm{};
+    int pipeline = SAMG_PIPELINE_NS_BLOCK;
+    double setup_seconds = 0;
+    uint64_t footprint = 0;      // memory_footprint of the global hierarchy
+    int64_t held_rows0 = 0;      // A_0 rows the setup held on the first driven rank
+    std::unique_ptr<Hierarchy> Hc;  // levels Ld.. (replicated; level Ld = Hc level 0)
     size_t Ld = 0;
-    int sliced_levels = 0;       // levels whose Galerkin product was row-sliced (DistSlicer)
     std::vector<std::vector<int64_t>> starts;  // partition of levels 0..Ld
+    std::vector<int64_t> nrows;  // global block rows of levels 0..Ld
+    std::vector<std::vector<DPiece>> pieces;   // setup rows per level / driven rank (taps)
     std::vector<DRank> ranks;    // the ranks this process drives
     CgScalars *sc_host = nullptr;
     cudaStream_t cs = nullptr;   // halo transfers overlapped with interior rows
     cudaEvent_t ev_pack = nullptr, ev_halo = nullptr;
+    cudaGraphExec_t cg_exec = nullptr;  // PCG loop body (device-side while)
 
     ~DHierarchy() {
-        if (H && H->stream) cudaStreamSynchronize(H->stream);
+        if (s) cudaStreamSynchronize(s);
         if (cs) cudaStreamSynchronize(cs);
+        if (cg_exec) cudaGraphExecDestroy(cg_exec);
         ranks.clear();
+        pieces.clear();
+        Hc.reset();
         if (ev_pack) cudaEventDestroy(ev_pack);
         if (ev_halo) cudaEventDestroy(ev_halo);
         if (cs) cudaStreamDestroy(cs);
+        if (s) cudaStreamDestroy(s);
         pinned_small_free(sc_host);
         if (comm) nccl().CommDestroy(comm);
     }
 
-    cudaStream_t stream() const { return H->stream; }
+    cudaStream_t stream() const { return s; }
     bool emulated() const { return comm == nullptr; }
+    Xport xport() const {
+        Xport x;
+        x.comm = comm;
+        x.nranks = nranks;
+        for (const DRank &R : ranks) x.mine.push_back(R.rank);
+        x.s = s;
+        return x;
+    }
 
     // Halo exchange of the level-l operator selected by `which` (0 A, 1 R,
     // 2 P) into the extended vector `vec` of every driven rank.
@@ -432,22 +438,36 @@ struct DHierarchy {
         }
     }
 
-    // the sum over ranks of sc->tmp, then the CG update `what`
-    void allreduce_finish(int what) {
+    // the sum over ranks of sc->tmp (count 1) or of (tmp, tmp2) (count 2)
+    void allreduce_tmp(int count) {
+        static_assert(offsetof(CgScalars, tmp2) == offsetof(CgScalars, tmp) + sizeof(double),
+                      "tmp, tmp2 are all-reduced as one 2-double buffer");
         cudaStream_t s = stream();
         if (!emulated()) {
             double *t = reinterpret_cast<double *>(reinterpret_cast<char *>(ranks[0].sc.p) +
                                                    offsetof(CgScalars, tmp));
-            NK(nccl().AllReduce(t, t, 1, ncclDouble, ncclSum, comm, s));
+            NK(nccl().AllReduce(t, t, count, ncclDouble, ncclSum, comm, s));
         } else if (ranks.size() > 1) {
             ScSet set{};
             set.n = static_cast<int>(ranks.size());
             for (int i = 0; i < set.n; ++i) set.p[i] = ranks[i].sc.p;
-            k_sum_tmp<<<1, 1, 0, s>>>(set);
+            k_sum_tmp<<<1, 1, 0, s>>>(set, count == 2 ? 1 : 0);
             CK_LAUNCH();
         }
-        for (DRank &R : ranks) launch_cg_finish(R.sc.p, what, s);
     }
+
+    // the sum over ranks of sc->tmp, then the CG update `what`
+    void allreduce_finish(int what) {
+        allreduce_tmp(1);
+        for (DRank &R : ranks) launch_cg_finish(R.sc.p, what, stream());
+    }
+
+    // one CG iteration after the first preconditioner application
+    // (cg.hpp:58-77): q = A p, alpha; u, r update; z = M r; then r.r and
+    // r.z in ONE 2-double all-reduce; beta; p = z + beta p.  rr_what:
+    // CG_RR (host loop) or CG_RR_LOOP (sets the graph loop condition h).
+    void cg_iteration(int rr_what, cudaGraphConditionalHandle h);
+    void build_cg_graph();
 
     // every rank's piece of f_Ld to every rank
     void gather_coarse() {
@@ -474,11 +494,60 @@ struct DHierarchy {
     samg_solve_report cg(const double *d_f, double *d_u, const samg_cg_params &cp);
 };
 
+void DHierarchy::cg_iteration(int rr_what, cudaGraphConditionalHandle h) {
+    cudaStream_t st = stream();
+    // q = A p overlapped with the halo: the first row range stores its
+    // partial p.q, the others add to it
+    std::vector<int> pieces_done(ranks.size(), 0);
+    exchange_overlap(0, 0, [](DRank &R) { return R.pext.p; },
+                     [&](DRank &R, int64_t a, int64_t b) {
+        RowView v(R.dl[0].A.A, a, b);
+        int &k = pieces_done[&R - ranks.data()];
+        launch_spmv_dot_split(v.m, R.pext.p, R.pext.p + 3 * a, R.q.p + 3 * a, R.partials.p,
+                              R.sc.p, st, k++ == 0 ? CG_STORE : CG_ADD);
+    });
+    allreduce_finish(CG_PQ);
+    for (DRank &R : ranks)
+        launch_cg_update(3 * R.nloc0, R.sc.p, R.pext.p, R.q.p, R.u.p, R.r.p, R.partials.p,
+                         CG_STORE, 0, st);
+    vcycle();
+    for (DRank &R : ranks) launch_dot(3 * R.nloc0, R.r.p, R.z.p, R.partials.p, R.sc.p, CG_STORE2, st);
+    allreduce_tmp(2);
+    for (DRank &R : ranks) launch_cg_finish2(R.sc.p, rr_what, h, st);
+    for (DRank &R : ranks) launch_p_update(3 * R.nloc0, R.sc.p, R.z.p, R.pext.p, st);
+}
+
+// The PCG loop as one CUDA graph with a device-side while node, as on one
+// GPU: the halo sends / receives, the all-reduces and the replicated coarse
+// V-cycle are captured with the rest; the loop condition is set on every
+// rank from the same all-reduced r.r, so all ranks leave together.
+void DHierarchy::build_cg_graph() {
+    cudaStream_t st = stream();
+    cudaGraph_t g;
+    CK(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle h;
+    CK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams np{};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = h;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t wnode;
+    CK(cudaGraphAddNode(&wnode, g, nullptr, 0, &np));
+    cudaGraph_t body = np.conditional.phGraph_out[0];
+    CK(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    cg_iteration(CG_RR_LOOP, h);
+    cudaGraph_t captured = body;
+    CK(cudaStreamEndCapture(st, &captured));
+    CK(cudaGraphInstantiate(&cg_exec, g, 0));
+    CK(cudaGraphDestroy(g));
+}
+
 // Distributed V-cycle (hierarchy.hpp:408-441) from a zero guess: z = M^-1 r
 // on every driven rank.
 void DHierarchy::vcycle() {
     cudaStream_t s = stream();
-    const int pre = H->prm.pre_sweeps, post = H->prm.post_sweeps;
+    const int pre = prm.pre_sweeps, post = prm.post_sweeps;
     auto fin = [&](DRank &R, size_t l) -> const double * { return l == 0 ? R.r.p : R.dl[l].f.p; };
     for (size_t l = 0; l < Ld; ++l) {
         for (DRank &R : ranks) {
@@ -511,7 +580,7 @@ void DHierarchy::vcycle() {
         });
     }
     gather_coarse();
-    for (DRank &R : ranks) H->vcycle_from(Ld, R.fLd.p, R.uLd.p, true, false);
+    for (DRank &R : ranks) Hc->vcycle_from(0, R.fLd.p, R.uLd.p, true, false);
     for (size_t l = Ld; l-- > 0;) {
         const bool next_replicated = l + 1 == Ld;
         if (!next_replicated) {
@@ -557,8 +626,8 @@ samg_solve_report DHierarchy::cg(const double *d_f, double *d_u, const samg_cg_p
     cudaStream_t s = stream();
     const auto t0 = std::chrono::steady_clock::now();
     samg_solve_report rep{};
-    rep.variant = H->pipeline;
-    rep.setup_seconds = H->setup_seconds;
+    rep.variant = pipeline;
+    rep.setup_seconds = setup_seconds;
     const int64_t base0 = emulated() ? ranks[0].row0 : 0;
     auto off = [&](const DRank &R) { return 3 * (R.row0 - base0); };
     for (DRank &R : ranks) {
@@ -568,7 +637,7 @@ samg_solve_report DHierarchy::cg(const double *d_f, double *d_u, const samg_cg_p
     }
     auto read = [&] {
         CK(cudaMemcpyAsync(sc_host, ranks[0].sc.p, sizeof(CgScalars), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
+        stream_wait(comm, s);  // polls ncclCommGetAsyncError: a dead peer raises, no hang
     };
     auto dots = [&](auto x, auto y, int what) {
         for (DRank &R : ranks) launch_dot(3 * R.nloc0, x(R), y(R), R.partials.p, R.sc.p, CG_STORE, s);
@@ -579,7 +648,7 @@ samg_solve_report DHierarchy::cg(const double *d_f, double *d_u, const samg_cg_p
     const double norm_f = std::sqrt(sc_host->rr);
     auto finish = [&](double res) {
         rep.relative_residual = res;
-        rep.preconditioner_bytes = H->memory_footprint();
+        rep.preconditioner_bytes = footprint;
         rep.solve_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         for (DRank &R : ranks) d2d(d_u + off(R), R.u.p, 3 * R.nloc0, s);
         CK(cudaStreamSynchronize(s));
@@ -589,39 +658,47 @@ samg_solve_report DHierarchy::cg(const double *d_f, double *d_u, const samg_cg_p
         finish(0.0);
         return rep;
     }
-    auto precondition = [&] {
-        vcycle();
-        dots([](DRank &R) { return R.r.p; }, [](DRank &R) { return R.z.p; }, CG_RZ);
-    };
+    static const bool use_graph = [] {
+        const char *e = std::getenv("SAMG_CG_GRAPH");
+        return !(e && e[0] == '0');
+    }();
     vcycle();
     dots([](DRank &R) { return R.r.p; }, [](DRank &R) { return R.z.p; }, CG_RHO);
     for (DRank &R : ranks) d2d(R.pext.p, R.z.p, 3 * R.nloc0, s);
     double res_norm = norm_f;
     int iter = 0;
-    while (res_norm / norm_f > cp.tol && iter < cp.max_iterations) {
-        // q = A p overlapped with the halo: the first row range stores its
-        // partial p.q, the others add to it
-        std::vector<int> pieces(ranks.size(), 0);
-        exchange_overlap(0, 0, [](DRank &R) { return R.pext.p; },
-                         [&](DRank &R, int64_t a, int64_t b) {
-            RowView v(R.dl[0].A.A, a, b);
-            int &k = pieces[&R - ranks.data()];
-            launch_spmv_dot_split(v.m, R.pext.p, R.pext.p + 3 * a, R.q.p + 3 * a, R.partials.p,
-                                  R.sc.p, s, k++ == 0 ? CG_STORE : CG_ADD);
-        });
-        allreduce_finish(CG_PQ);
-        for (DRank &R : ranks)
-            launch_cg_update(3 * R.nloc0, R.sc.p, R.pext.p, R.q.p, R.u.p, R.r.p, R.partials.p,
-                             CG_STORE, 0, s);
-        allreduce_finish(CG_RR);
-        read();
-        if (sc_host->breakdown)
-            fail(SAMG_BREAKDOWN_NON_SPD, "cg: p'Ap <= 0, matrix or preconditioner not SPD");
-        ++iter;
-        res_norm = std::sqrt(sc_host->rr);
-        if (res_norm / norm_f <= cp.tol) break;
-        precondition();
-        for (DRank &R : ranks) launch_p_update(3 * R.nloc0, R.sc.p, R.z.p, R.pext.p, s);
+    if (cp.max_iterations > 0 && res_norm / norm_f > cp.tol) {
+        for (DRank &R : ranks) {
+            CgScalars *st = sc_host;
+            CK(cudaMemcpyAsync(st, R.sc.p, sizeof(CgScalars), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            st->norm_f = norm_f;
+            st->tol = cp.tol;
+            st->iter = 0;
+            st->max_iter = cp.max_iterations;
+            st->breakdown = 0;
+            st->ticket = 0;
+            CK(cudaMemcpyAsync(R.sc.p, st, sizeof(CgScalars), cudaMemcpyHostToDevice, s));
+            CK(cudaStreamSynchronize(s));
+        }
+        if (use_graph) {
+            if (!cg_exec) build_cg_graph();
+            CK(cudaGraphLaunch(cg_exec, s));
+            read();
+            if (sc_host->breakdown)
+                fail(SAMG_BREAKDOWN_NON_SPD, "cg: p'Ap <= 0, matrix or preconditioner not SPD");
+            iter = sc_host->iter;
+            res_norm = std::sqrt(sc_host->rr);
+        } else {
+            while (res_norm / norm_f > cp.tol && iter < cp.max_iterations) {
+                cg_iteration(CG_RR, 0);
+                read();
+                if (sc_host->breakdown)
+                    fail(SAMG_BREAKDOWN_NON_SPD, "cg: p'Ap <= 0, matrix or preconditioner not SPD");
+                ++iter;
+                res_norm = std::sqrt(sc_host->rr);
+            }
+        }
     }
     rep.iterations = iter;
     rep.converged = res_norm / norm_f <= cp.tol;
@@ -635,73 +712,49 @@ samg_solve_report DHierarchy::cg(const double *d_f, double *d_u, const samg_cg_p
     return rep;
 }
 
-// Build the distributed hierarchy from a full (redundant) single-GPU one for
-// the ranks `mine` (one rank with NCCL, all of them when emulated).
-DHierarchy *dsetup(std::unique_ptr<Hierarchy> H, ncclComm_t comm, int nranks,
-                   const std::vector<int> &mine, const std::vector<int64_t> &row_starts,
-                   int64_t min_rows) {
+// The solve-side structures of the distributed hierarchy: every driven
+// rank's local operators with their halo plans (from the setup's rows).
+DHierarchy *dbuild(DSetup &&S, const Xport &x, const samg_amg_params &prm, int pipeline,
+                   double t0) {
     auto D = std::make_unique<DHierarchy>();
-    D->nranks = nranks;
-    D->device = H->device;
-    cudaStream_t s = H->stream;
-    const size_t L = H->levels.size();
-    if (L < 2) fail(SAMG_UNSUPPORTED, "multi-GPU solve needs at least two levels");
-    // partition chain: level l+1's rows follow the seeds of level l's aggregation
-    std::vector<std::vector<int64_t>> st{row_starts};
-    size_t Ld = 1;  // the fine level is always partitioned
-    for (size_t l = 0; l + 1 < L; ++l) {
-        const Level &lv = H->levels[l];
-        // block rows per node: 1 on the fine level (pbs 3) and in the block
-        // pipeline, 2 on ns coarse levels (pbs 6)
-        const int64_t h = lv.nnodes ? lv.A.nrows / lv.nnodes : 1;
-        const int64_t kb = lv.naggs ? lv.P.ncols / lv.naggs : 2;
-        // seedno at the partition bounds only (nranks + 1 values)
-        std::vector<int64_t> nidx(nranks + 1);
-        for (int q = 0; q <= nranks; ++q) nidx[q] = st[l][q] / h;
-        std::vector<int> sn(nranks + 1);
-        {
-            DevBuf<int64_t> di(nranks + 1, s);
-            DevBuf<int> dv(nranks + 1, s);
-            CK(cudaMemcpyAsync(di.p, nidx.data(), sizeof(int64_t) * (nranks + 1), cudaMemcpyHostToDevice, s));
-            k_gather_ptr<<<1, 32, 0, s>>>(nranks + 1, di.p, lv.seedno.p, dv.p);
-            CK(cudaMemcpyAsync(sn.data(), dv.p, sizeof(int) * (nranks + 1), cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
-        }
-        std::vector<int64_t> cst(nranks + 1);
-        for (int q = 0; q <= nranks; ++q) cst[q] = kb * sn[q];
-        st.push_back(cst);
-        // level l+1 is partitioned too if it is not the coarsest, large
-        // enough, and gives every rank at least one row
-        bool part = l + 2 < L && H->levels[l + 1].A.nrows >= min_rows * nranks;
-        for (int q = 0; q < nranks && part; ++q) part = cst[q + 1] > cst[q];
-        if (!part) break;
-        Ld = l + 2;
-    }
+    D->nranks = x.nranks;
+    CK(cudaGetDevice(&D->device));
+    D->s = x.s;
+    D->comm = x.comm;
+    D->prm = prm;
+    D->pipeline = pipeline;
+    cudaStream_t s = x.s;
+    const size_t Ld = S.Ld();
     D->Ld = Ld;
-    D->starts = st;
-    D->ranks.resize(mine.size());
-    for (size_t i = 0; i < mine.size(); ++i) {
+    D->starts = S.starts;
+    D->nrows = S.nrows;
+    D->footprint = S.footprint;
+    D->held_rows0 = S.held_rows.empty() ? 0 : S.held_rows[0];
+    D->ranks.resize(x.mine.size());
+    const std::vector<int64_t> &row_starts = S.starts[0];
+    for (size_t i = 0; i < x.mine.size(); ++i) {
         DRank &R = D->ranks[i];
-        R.rank = mine[i];
+        R.rank = x.mine[i];
         R.row0 = row_starts[R.rank];
         R.nloc0 = row_starts[R.rank + 1] - R.row0;
         R.dl.resize(Ld);
     }
     for (size_t l = 0; l < Ld; ++l) {
-        Level &lv = H->levels[l];
-        const std::vector<int64_t> &fst = st[l], &cst = st[l + 1];
+        const std::vector<int64_t> &fst = S.starts[l], &cst = S.starts[l + 1];
         const bool next_replicated = l + 1 == Ld;
-        const int per = lv.M.kind == SM_POINT ? 3 : 9;
-        for (DRank &R : D->ranks) {
+        for (size_t i = 0; i < D->ranks.size(); ++i) {
+            DRank &R = D->ranks[i];
+            const DPiece &pc = S.lv[l][i];
             DLevel &dlv = R.dl[l];
-            build_local(lv.A, fst, fst, R.rank, false, dlv.A, s);
-            build_local(lv.R, cst, fst, R.rank, false, dlv.R, s);
-            build_local(lv.P, fst, cst, R.rank, next_replicated, dlv.P, s);
-            const int64_t f0 = fst[R.rank], nl = fst[R.rank + 1] - f0;
-            dlv.M.kind = lv.M.kind;
+            build_local_rows(pc.A, &pc.A, fst, fst, R.rank, false, dlv.A, s);
+            build_local_rows(pc.R, &pc.P, cst, fst, R.rank, false, dlv.R, s);
+            build_local_rows(pc.P, &pc.R, fst, cst, R.rank, next_replicated, dlv.P, s);
+            const int64_t nl = fst[R.rank + 1] - fst[R.rank];
+            const int per = pc.M.kind == SM_POINT ? 3 : 9;
+            dlv.M.kind = pc.M.kind;
             dlv.M.data.alloc(per * nl + 1, s);
             if (nl)
-                CK(cudaMemcpyAsync(dlv.M.data.p, lv.M.data.p + per * f0, sizeof(double) * per * nl,
+                CK(cudaMemcpyAsync(dlv.M.data.p, pc.M.data.p, sizeof(double) * per * nl,
                                    cudaMemcpyDeviceToDevice, s));
             dlv.f.alloc(3 * nl + 3, s);
             dlv.t.alloc(3 * nl + 3, s);
@@ -710,7 +763,7 @@ DHierarchy *dsetup(std::unique_ptr<Hierarchy> H, ncclComm_t comm, int nranks,
             if (!next_replicated) dlv.uP.alloc(3 * (dlv.P.plan.nloc + dlv.P.plan.nghost) + 3, s);
         }
     }
-    const int64_t nLd = H->levels[Ld].A.nrows;
+    const int64_t nLd = S.nrows[Ld];
     for (DRank &R : D->ranks) {
         const int64_t n = 3 * R.nloc0;
         const LocalMat &A0 = R.dl[0].A;
@@ -730,8 +783,10 @@ DHierarchy *dsetup(std::unique_ptr<Hierarchy> H, ncclComm_t comm, int nranks,
     CK(cudaEventCreateWithFlags(&D->ev_pack, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&D->ev_halo, cudaEventDisableTiming));
     CK(cudaStreamSynchronize(s));
-    D->H = std::move(H);
-    D->comm = comm;
+    D->Hc = std::move(S.coarse);
+    D->pieces = std::move(S.lv);
+    D->setup_seconds = std::chrono::duration<double>(
+        std::chrono::steady_clock::now().time_since_epoch()).count() - t0;
     return D.release();
 }
 
@@ -740,126 +795,58 @@ DHierarchy *dsetup(std::unique_ptr<Hierarchy> H, ncclComm_t comm, int nranks,
 // ---- entry points used by capi.cu ------------------------------------------
 namespace samgb {
 
-// Row-sliced Galerkin product for the multi-GPU setup.  Every rank runs the
-// (deterministic) setup on the whole matrix, except for the dominant step:
-// rank q forms only the coarse rows it will own, [cst[q], cst[q+1]) -- the
-// same partition chain dsetup derives from the aggregation seeds -- as
-// (R[cst[q]:cst[q+1]] A) P, and the rows are then assembled on every rank
-// (one all-reduce of the block counts, then grouped in-place ncclBroadcasts
-// of each rank's ptr / col / val piece).  Every output row is computed by
-// exactly the kernels of the single-GPU product, so A_c is bit-identical to
-// it.  Levels below min_rows * nranks coarse rows are formed redundantly.
-// Emulated group (comm == nullptr): the pieces of all ranks are formed one
-// after the other and assembled by device copies (verification on one GPU).
-struct DistSlicer : GalerkinSlicer {
-    ncclComm_t comm = nullptr;
-    int nranks = 1, rank = 0;
-    int64_t min_rows = 4096;
-    std::vector<int64_t> st;  // fine row starts of the current level
-    bool active = true;
-    int sliced_levels = 0;
-
-    bool galerkin(size_t, const Bsr3 &A, const int *seedno, int64_t nnodes, int64_t naggs,
-                  const Bsr3 &R, const Bsr3 &P, Bsr3 &Ac, bool scalar_order, cudaStream_t s) override {
-        if (!active || nnodes == 0 || naggs == 0) return active = false;
-        const int64_t h = A.nrows / nnodes, kb = P.ncols / naggs;
-        std::vector<int64_t> nidx(nranks + 1);
-        for (int q = 0; q <= nranks; ++q) nidx[q] = st[q] / h;
-        std::vector<int> sn(nranks + 1);
-        {
-            DevBuf<int64_t> di(nranks + 1, s);
-            DevBuf<int> dv(nranks + 1, s);
-            CK(cudaMemcpyAsync(di.p, nidx.data(), sizeof(int64_t) * (nranks + 1), cudaMemcpyHostToDevice, s));
-            k_gather_ptr<<<1, 32, 0, s>>>(nranks + 1, di.p, seedno, dv.p);
-            CK(cudaMemcpyAsync(sn.data(), dv.p, sizeof(int) * (nranks + 1), cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
-        }
-        std::vector<int64_t> cst(nranks + 1);
-        for (int q = 0; q <= nranks; ++q) cst[q] = kb * sn[q];
-        bool slice = R.nrows >= min_rows * nranks && cst[nranks] == R.nrows;
-        for (int q = 0; q < nranks && slice; ++q) slice = cst[q + 1] > cst[q];
-        if (!slice) return active = false;
-        st = cst;  // the next level's fine partition
-        ++sliced_levels;
-        std::vector<int> mine;
-        if (comm) mine.push_back(rank);
-        else for (int q = 0; q < nranks; ++q) mine.push_back(q);
-        // each driven rank's piece
-        std::vector<Bsr3> piece(nranks);
-        std::vector<int64_t> cnt(nranks, 0);
-        for (int q : mine) {
-            Bsr3 Rs;
-            slice_rows(R, cst[q], cst[q + 1], Rs, s);
-            galerkin_rows(Rs, A, P, R, piece[q], s, scalar_order);
-            cnt[q] = piece[q].nnzb;
-        }
-        if (comm) {  // block counts of every rank (an all-gather as a sum)
-            DevBuf<int64_t> dc(nranks, s);
-            CK(cudaMemcpyAsync(dc.p, cnt.data(), sizeof(int64_t) * nranks, cudaMemcpyHostToDevice, s));
-            NK(nccl().AllReduce(dc.p, dc.p, nranks, ncclInt64, ncclSum, comm, s));
-            CK(cudaMemcpyAsync(cnt.data(), dc.p, sizeof(int64_t) * nranks, cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
-        }
-        std::vector<int64_t> off(nranks + 1, 0);
-        for (int q = 0; q < nranks; ++q) off[q + 1] = off[q] + cnt[q];
-        Ac.alloc(R.nrows, P.ncols, off[nranks], s);
-        for (int q : mine) {  // own pieces into place, ptr rebased
-            const int *pp = piece[q].ptr.p;
-            int *ap = Ac.ptr.p + cst[q];
-            const int o = static_cast<int>(off[q]);
-            const int64_t nr = cst[q + 1] - cst[q] + (q == nranks - 1 ? 1 : 0);
-            for_each_rebase(nr, pp, o, ap, s);
-            if (cnt[q]) {
-                CK(cudaMemcpyAsync(Ac.col.p + off[q], piece[q].col.p, sizeof(int) * cnt[q],
-                                   cudaMemcpyDeviceToDevice, s));
-                CK(cudaMemcpyAsync(Ac.val.p + 9 * off[q], piece[q].val.p, sizeof(double) * 9 * cnt[q],
-                                   cudaMemcpyDeviceToDevice, s));
-            }
-            piece[q] = Bsr3();
-        }
-        if (comm) {
-            NK(nccl().GroupStart());
-            for (int q = 0; q < nranks; ++q) {
-                const int64_t nr = cst[q + 1] - cst[q] + (q == nranks - 1 ? 1 : 0);
-                int *pq = Ac.ptr.p + cst[q];
-                NK(nccl().Broadcast(pq, pq, nr, ncclInt32, q, comm, s));
-                if (cnt[q]) {
-                    int *cq = Ac.col.p + off[q];
-                    double *vq = Ac.val.p + 9 * off[q];
-                    NK(nccl().Broadcast(cq, cq, cnt[q], ncclInt32, q, comm, s));
-                    NK(nccl().Broadcast(vq, vq, 9 * cnt[q], ncclDouble, q, comm, s));
-                }
-            }
-            NK(nccl().GroupEnd());
-        }
-        return true;
-    }
-};
-
-// id == nullptr: emulate all nranks in this process (no NCCL).
-DHierarchy *dsetup_all(const unsigned char *id, int nranks, int rank, Bsr3 &&A0,
-                       const double *B, int64_t b_rows, int64_t b_cols,
+// Distributed setup.  NCCL (id != nullptr): this process is `rank` and
+// passes only its own rows -- block rows [row_starts[rank],
+// row_starts[rank+1]) as (nloc, ptr from 0, global column ids, values) and
+// its nullspace rows (3*nloc x b_cols, column-major).  Emulated (id ==
+// nullptr): every rank in this process, the rows and nullspace given for
+// the whole matrix and cut here.
+DHierarchy *dsetup_all(const unsigned char *id, int nranks, int rank, int64_t nbrows,
+                       Bsr3 &&A_rows, const double *B, int64_t b_cols,
                        const int64_t *row_starts, int64_t min_rows, const samg_amg_params &prm,
                        cudaStream_t s, double t0, int pipeline) {
     if (!id && nranks > kMaxEmulated) fail(SAMG_INVALID_ARGUMENT, "dsetup: at most 16 emulated ranks");
     if (prm.smoother == SAMG_SMOOTHER_ILU0)
         fail(SAMG_UNSUPPORTED, "multi-GPU solve: the ILU(0) sweeps are sequential across row partitions");
-    const int64_t nb = A0.nrows;
     std::vector<int64_t> st(nranks + 1);
     if (row_starts) {
         st.assign(row_starts, row_starts + nranks + 1);
-        if (st[0] != 0 || st[nranks] != nb)
+        if (st[0] != 0 || st[nranks] != nbrows)
             fail(SAMG_INVALID_ARGUMENT, "dsetup: row_starts must span [0, nbrows]");
     } else {
-        for (int q = 0; q <= nranks; ++q) st[q] = nb * q / nranks;
+        for (int q = 0; q <= nranks; ++q) st[q] = nbrows * q / nranks;
     }
     for (int q = 0; q < nranks; ++q)
         if (st[q + 1] <= st[q]) fail(SAMG_INVALID_ARGUMENT, "dsetup: every rank needs at least one block row");
-    std::vector<int> mine;
+    Xport x;
+    x.nranks = nranks;
+    x.s = s;
+    if (id) x.mine.push_back(rank);
+    else for (int q = 0; q < nranks; ++q) x.mine.push_back(q);
+    const bool block = pipeline == SAMG_PIPELINE_BLOCK;
+    std::vector<Bsr3> A_own(x.mine.size());
+    std::vector<DevBuf<double>> B_own(x.mine.size());
     if (id) {
-        mine.push_back(rank);
+        if (A_rows.nrows != st[rank + 1] - st[rank])
+            fail(SAMG_DIMENSION_MISMATCH, "dsetup: local rows disagree with row_starts");
+        A_own[0] = std::move(A_rows);
+        if (!block) {
+            const int64_t n3 = 3 * A_own[0].nrows;
+            B_own[0].alloc(n3 * b_cols + 1, s);
+            CK(cudaMemcpyAsync(B_own[0].p, B, sizeof(double) * n3 * b_cols, cudaMemcpyDefault, s));
+        }
     } else {
-        for (int q = 0; q < nranks; ++q) mine.push_back(q);
+        // cut the global input
+        for (int q = 0; q < nranks; ++q) {
+            slice_rows(A_rows, st[q], st[q + 1], A_own[q], s);
+            if (!block) {
+                const int64_t n3 = 3 * (st[q + 1] - st[q]), N3 = 3 * nbrows;
+                B_own[q].alloc(n3 * b_cols + 1, s);
+                CK(cudaMemcpy2DAsync(B_own[q].p, sizeof(double) * n3, B + 3 * st[q], sizeof(double) * N3,
+                                     sizeof(double) * n3, b_cols, cudaMemcpyDefault, s));
+            }
+        }
+        A_rows = Bsr3();
     }
     ncclComm_t comm = nullptr;
     if (id) {
@@ -867,24 +854,11 @@ DHierarchy *dsetup_all(const unsigned char *id, int nranks, int rank, Bsr3 &&A0,
         std::memcpy(&uid, id, sizeof uid);
         NK(nccl().CommInitRank(&comm, nranks, uid, rank));
     }
+    x.comm = comm;
     try {
-        DistSlicer slicer;
-        slicer.comm = comm;
-        slicer.nranks = nranks;
-        slicer.rank = rank;
-        slicer.min_rows = min_rows;
-        slicer.st = st;
-        static const bool slice_env = [] {
-            const char *e = std::getenv("SAMG_DIST_SLICED_GALERKIN");
-            return !e || e[0] != '0';
-        }();
-        std::unique_ptr<Hierarchy> H(setup_hierarchy(std::move(A0), B, b_rows, b_cols, prm, s, t0,
-                                                     pipeline, slice_env ? &slicer : nullptr));
-        H->owns_stream = false;  // the caller destroys s if anything below throws
-        DHierarchy *d = dsetup(std::move(H), comm, nranks, mine, st, min_rows);
-        d->sliced_levels = slicer.sliced_levels;
-        d->H->owns_stream = true;
-        return d;
+        DSetup S = dist_setup(x, std::move(A_own), std::move(B_own), b_cols, st, min_rows, prm,
+                              pipeline, t0);
+        return dbuild(std::move(S), x, prm, pipeline, t0);
     } catch (...) {
         if (comm) nccl().CommDestroy(comm);
         throw;
@@ -914,13 +888,35 @@ void dinfo(const DHierarchy *d, int64_t *row0, int64_t *row1, int *nlevels, int 
            double *setup_s) {
     *row0 = d->ranks.front().row0;
     *row1 = d->ranks.back().row0 + d->ranks.back().nloc0;
-    *nlevels = static_cast<int>(d->H->levels.size());
+    *nlevels = static_cast<int>(d->Ld + d->Hc->levels.size());
     *dist_levels = static_cast<int>(d->Ld);
-    *setup_s = d->H->setup_seconds;
+    *setup_s = d->setup_seconds;
 }
 
-int dsliced_levels(const DHierarchy *d) { return d->sliced_levels; }
-const Hierarchy &dfull(const DHierarchy *d) { return *d->H; }
+int64_t dheld_rows(const DHierarchy *d) { return d->held_rows0; }
+
+// Parity tap: level `level`'s A (0), P (1) or R (2) as the global matrix --
+// assembled from every rank's rows for a distributed level (a collective
+// over the communicator), the replicated matrix otherwise.
+const Bsr3 &dlevel(DHierarchy *d, int level, int which, Bsr3 &tmp) {
+    if (level < 0) fail(SAMG_INVALID_ARGUMENT, "level out of range");
+    if (static_cast<size_t>(level) >= d->Ld) {
+        const size_t l = level - d->Ld;
+        if (l >= d->Hc->levels.size()) fail(SAMG_INVALID_ARGUMENT, "level out of range");
+        const Level &lv = d->Hc->levels[l];
+        if (which != 0 && !lv.has_transfer) fail(SAMG_INVALID_ARGUMENT, "no transfer operators on the coarsest level");
+        return which == 0 ? lv.A : which == 1 ? lv.P : lv.R;
+    }
+    if (which < 0 || which > 2) fail(SAMG_INVALID_ARGUMENT, "which must be 0, 1 or 2");
+    CK(cudaSetDevice(d->device));
+    const Xport x = d->xport();
+    std::vector<const Bsr3 *> own;
+    for (const DPiece &pc : d->pieces[level]) own.push_back(which == 0 ? &pc.A : which == 1 ? &pc.P : &pc.R);
+    const std::vector<int64_t> &rows = which == 2 ? d->starts[level + 1] : d->starts[level];
+    const int64_t ncols = which == 1 ? d->nrows[level + 1] : d->nrows[level];
+    gather_matrix(x, own, rows, ncols, tmp);
+    return tmp;
+}
 
 void nccl_unique_id(unsigned char *out) {
     ncclUniqueId uid;

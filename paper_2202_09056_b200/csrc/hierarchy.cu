@@ -51,7 +51,6 @@ Hierarchy::~Hierarchy() {
     pinned_small_free(sc_host);
     pinned_small_free(sc_stage);
     if (cg_exec) cudaGraphExecDestroy(cg_exec);
-    if (l2_window_bytes) cudaCtxResetPersistingL2Cache();  // demote the lines to normal
     if (stream && owns_stream) {
         cudaStreamSynchronize(stream);
         cudaStreamDestroy(stream);
@@ -79,7 +78,7 @@ uint64_t Hierarchy::memory_footprint() const {
 
 Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int64_t b_cols,
                            const samg_amg_params &prm, cudaStream_t s, double t_start, int pipeline,
-                           GalerkinSlicer *slicer) {
+                           GalerkinSlicer *slicer, int first_level) {
     auto H = std::make_unique<Hierarchy>();
     H->stream = s;
     H->prm = prm;
@@ -193,7 +192,7 @@ Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int6
         }
         // ns pipelines force point_block_size = 3 on the fine level
         // (hierarchy.hpp:284-285), then use the nullspace width (:351-353)
-        const int pbs = H->levels.size() == 1 ? 3 : k;
+        const int pbs = (H->levels.size() == 1 && first_level == 0) ? 3 : k;
         if (pbs % 3) fail(SAMG_NOT_DIVISIBLE, "ns_block: node size must be a multiple of 3");
         const int h = pbs / 3;
         if (Li.A.nrows % h)
@@ -293,7 +292,6 @@ Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int6
     H->sc_host = static_cast<CgScalars *>(pinned_small_alloc(sizeof(CgScalars)));
     H->sc_stage = static_cast<CgScalars *>(pinned_small_alloc(sizeof(CgScalars)));
     CK(cudaStreamSynchronize(s));
-    H->set_l2_residency();
     mark("workspace", L - 1);
     H->setup_seconds = now_s() - t_start;
     H->owns_stream = true;
@@ -344,36 +342,6 @@ void choose_coarse_solver(Hierarchy &H, DevError *err, cudaStream_t s, bool inve
     dense_lu_ref(Ac, H.lu, err, s);
     H.coarse_lu = true;
     H.Ainv.release();
-}
-
-// The coarse GEMV streams the whole n_c x n_c inverse every V-cycle (C1:
-// 68 MB); the 126 MB L2 can hold it across iterations while the fine-level
-// streams pass through.  The window marks its lines persisting (the
-// persisting carve-out is sized to it); everything else is normal.
-void Hierarchy::set_l2_residency() {
-    static const int mode = [] {
-        const char *e = std::getenv("SAMG_L2_PERSIST");
-        return e ? std::atoi(e) : 1;
-    }();
-    if (!mode || coarse_lu || !Ainv.p) return;
-    int maxp = 0, maxw = 0;
-    CK(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, device));
-    CK(cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, device));
-    const size_t bytes = Ainv.bytes();
-    if (maxp <= 0 || maxw <= 0) return;
-    const size_t win = std::min<size_t>(bytes, static_cast<size_t>(maxw));
-    const size_t carve = std::min<size_t>(win, static_cast<size_t>(maxp));
-    size_t cur = 0;
-    CK(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
-    if (cur < carve) CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve));
-    cudaStreamAttrValue v{};
-    v.accessPolicyWindow.base_ptr = Ainv.p;
-    v.accessPolicyWindow.num_bytes = win;
-    v.accessPolicyWindow.hitRatio = static_cast<float>(std::min(1.0, static_cast<double>(carve) / win));
-    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    CK(cudaStreamSetAttribute(stream, cudaStreamAttributeAccessPolicyWindow, &v));
-    l2_window_bytes = win;
 }
 
 void Hierarchy::coarse_solve(const double *f, double *u) {

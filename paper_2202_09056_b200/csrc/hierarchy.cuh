@@ -40,10 +40,6 @@ struct Hierarchy {
     CgScalars *sc_stage = nullptr; // pinned staging for loop parameters
     cudaGraphExec_t cg_exec = nullptr;  // device-resident CG loop (while node)
     void build_cg_graph();
-    // keep the dense coarse inverse L2-resident across V-cycles (access
-    // policy window on the solve stream; SAMG_L2_PERSIST=0 disables)
-    size_t l2_window_bytes = 0;
-    void set_l2_residency();
 
     ~Hierarchy();
     int64_t finest_dim() const { return 3 * levels.front().A.nrows; }
@@ -67,8 +63,11 @@ struct GalerkinSlicer {
 
 // Setup from a device BSR3 fine matrix (consumed) and a host nullspace.
 // pipeline: ns_block, or ns_hybrid1/2 (Galerkin in scalar order)
+// first_level: the global index of A0's level (the multi-GPU setup hands in
+// a gathered coarse level: its nodes are k-row tiles, not 3-row ones)
 Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int64_t b_cols,
                            const samg_amg_params &prm, cudaStream_t stream, double t_start,
-                           int pipeline = SAMG_PIPELINE_NS_BLOCK, GalerkinSlicer *slicer = nullptr);
+                           int pipeline = SAMG_PIPELINE_NS_BLOCK, GalerkinSlicer *slicer = nullptr,
+                           int first_level = 0);
 
 } // namespace samgb

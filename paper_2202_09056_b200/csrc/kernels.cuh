@@ -26,6 +26,23 @@ struct Bsr3 {
     }
 };
 
+// Rows [r0, r1) of M as a non-owning matrix (ptr offset; col / val shared,
+// so the ptr values stay absolute).  Vectors indexed by row (f, u, out, M)
+// are offset by the caller.
+struct RowView {
+    Bsr3 m;
+    RowView(const Bsr3 &src, int64_t r0, int64_t r1) {
+        m.nrows = r1 - r0;
+        m.ncols = src.ncols;
+        m.nnzb = src.nnzb;  // bounds of the shared arrays (the TMA path's end checks)
+        m.ptr.p = src.ptr.p + r0;
+        m.col.p = src.col.p;
+        m.val.p = src.val.p;
+        m.val32.p = src.val32.p;
+    }
+    RowView(const RowView &) = delete;
+    ~RowView() { m.ptr.p = nullptr; m.col.p = nullptr; m.val.p = nullptr; m.val32.p = nullptr; }
+};
 enum SmootherKind { SM_POINT = 0, SM_BLOCK = 1, SM_ILU = 2 };
 
 // Per-level smoother: point (3 doubles per block row: omega / a_rr), block
@@ -60,6 +77,9 @@ void launch_smooth(const Bsr3 &A, const Smoother &M, const double *f, const doub
 // cap on the persistent SpMV's CTAs for this host thread (-1: default /
 // SAMG_TMA_CTAS, 0: one per SM)
 void set_spmv_cta_cap(int ctas);
+// programmatic dependent launch of the TMA-fed SpMV for this host thread
+// (back-to-back standalone SpMVs; solve.cu)
+void set_spmv_pdl(bool on);
 // fp32 copy of the values (A.val32) for the mixed-precision V-cycle
 void make_lowp(Bsr3 &A, cudaStream_t s);
 // u = M f  (one sweep from a zero guess: the residual is f exactly)
@@ -78,6 +98,7 @@ void launch_dense_gemv(int64_t n, const double *Ainv, const double *f, double *u
 struct CgScalars {
     double pq, rho, rho_new, rr, alpha, beta;
     double tmp;  // raw local sum (CG_STORE) awaiting a cross-rank allreduce
+    double tmp2; // a second one (CG_STORE2), all-reduced together with tmp
     double norm_f, tol;
     int breakdown, iter, max_iter;
     unsigned ticket;  // last-CTA counter of the fused reductions
@@ -88,12 +109,16 @@ struct CgScalars {
 // RZ: beta = rz/rho, rho = rz; RHO: rho; RR_LOOP: rr, ++iter and the graph
 // loop condition ||r||/||f|| > tol && iter < max && !breakdown.
 // STORE: only tmp = s (multi-GPU: allreduce tmp, then launch_cg_finish).
-enum { CG_RR = 0, CG_PQ = 1, CG_RZ = 2, CG_RHO = 3, CG_RR_LOOP = 4, CG_STORE = 5, CG_ADD = 6 };
+enum { CG_RR = 0, CG_PQ = 1, CG_RZ = 2, CG_RHO = 3, CG_RR_LOOP = 4, CG_STORE = 5, CG_ADD = 6,
+       CG_STORE2 = 7 };
 // q = A x and p.q on a row range (x the whole halo-extended vector)
 void launch_spmv_dot_split(const Bsr3 &A, const double *x, const double *p, double *q,
                            double *partials, CgScalars *sc, cudaStream_t s, int what);
 // apply `what` to sc->tmp (after the allreduce of the partial sums)
 void launch_cg_finish(CgScalars *sc, int what, cudaStream_t s);
+// after the allreduce of (tmp, tmp2) = (r.r, r.z): r.r -> `rr_what` (CG_RR,
+// or CG_RR_LOOP setting the graph's loop condition h), r.z -> CG_RZ
+void launch_cg_finish2(CgScalars *sc, int rr_what, cudaGraphConditionalHandle h, cudaStream_t s);
 constexpr int kRedBlocks = 592;   // 4 x 148 SMs: fixed => deterministic sums
 // q = A p fused with p.q (cg.hpp:63-64) -> PQ
 void launch_spmv_dot(const Bsr3 &A, const double *p, double *q, double *partials,
@@ -133,18 +158,24 @@ void strength_graph(const Bsr3 &A, int h, double eps_strong, Graph &G, cudaStrea
 int64_t aggregate(const Graph &G, DevBuf<int> &agg, cudaStream_t s, DevBuf<int> *seedno = nullptr);
 // tentative prolongation with QR of the nullspace (coarsening.hpp:238-312):
 // Pt[nfine*k] row values (columns agg*k + c), Bc column-major (naggs*k)-by-k
+// [a0, a1): only these aggregates (the distributed setup's own; B must
+// hold their nodes' rows); Pt / Bc keep the global layout
 void tentative(const DevBuf<int> &agg, int64_t nnodes, int64_t naggs, int pbs, const double *B,
-               int k, DevBuf<double> &Pt, DevBuf<double> &Bc, DevError *err, cudaStream_t s);
+               int k, DevBuf<double> &Pt, DevBuf<double> &Bc, DevError *err, cudaStream_t s,
+               int64_t a0 = 0, int64_t a1 = -1);
 // smoothed prolongation in scalar semantics, emitted as BSR3
 // (coarsening.hpp:319-416 + to_block<3>)
+// [node0, node1): only these nodes' rows of P (local row numbering; A in
+// global numbering holding at least their rows)
 void smooth_prolongation(const Bsr3 &A, const Graph &G, const DevBuf<int> &agg, int64_t naggs,
                          int pbs, int k, const double *Pt, double omega, Bsr3 &P, DevError *err,
-                         cudaStream_t s);
+                         cudaStream_t s, int64_t node0 = 0, int64_t node1 = -1);
 // block pipeline transfer (block_transfer_operators, coarsening.hpp:471-560):
 // identity-block tentative scaled by 1/sqrt(|aggregate|), smoothed with the
 // inverse of the lumped filtered block diagonal; P is n-by-naggs blocks
 void block_transfer(const Bsr3 &A, const Graph &G, const DevBuf<int> &agg, int64_t naggs,
-                    double omega, Bsr3 &P, DevError *err, cudaStream_t s);
+                    double omega, Bsr3 &P, DevError *err, cudaStream_t s, int64_t r0 = 0,
+                    int64_t r1 = -1);
 // R = P^T with transposed blocks (csr.hpp:173-194)
 void transpose(const Bsr3 &P, Bsr3 &R, cudaStream_t s);
 // C = A*B in the reference's order (csr.hpp:199-255): block arithmetic
@@ -155,18 +186,21 @@ void spgemm(const Bsr3 &A, const Bsr3 &B, Bsr3 &C, cudaStream_t s, bool scalar_o
 // A_c = (R A) P with R = P^T exactly (the hierarchy's transfer operators)
 void galerkin(const Bsr3 &R, const Bsr3 &A, const Bsr3 &P, Bsr3 &Ac, cudaStream_t s,
               bool scalar_order = false);
-// rows of (Rl A) P for a row slice Rl of R (P's columns read through R)
+// rows of (Rl A) P for a row slice Rl of R (P's columns read through R);
+// subset: A / P / R hold only the rows these products touch (global
+// numbering, other rows empty; the distributed setup)
 void galerkin_rows(const Bsr3 &Rl, const Bsr3 &A, const Bsr3 &P, const Bsr3 &R, Bsr3 &Ac,
-                   cudaStream_t s, bool scalar_order = false);
+                   cudaStream_t s, bool scalar_order = false, bool subset = false);
 // rows [r0, r1) of M as a matrix of their own
 void slice_rows(const Bsr3 &M, int64_t r0, int64_t r1, Bsr3 &out, cudaStream_t s);
-void fix_decoupled_rows(Bsr3 &A, cudaStream_t s);
+// row0: global id of A's local row 0 (a row slice: the diagonal is row0 + i)
+void fix_decoupled_rows(Bsr3 &A, cudaStream_t s, int64_t row0 = 0);
 // sum over the union pattern of (A - G)^2 and of G^2 (the Galerkin
 // consistency check, hierarchy.hpp:382-401); out[0] = diff, out[1] = ref
 void union_diff(const Bsr3 &A, const Bsr3 &G, double out[2], cudaStream_t s);
 // smoother setup: kind SAMG_SMOOTHER_*
 void setup_smoother(const Bsr3 &A, int kind, double omega, Smoother &M, DevError *err,
-                    cudaStream_t s);
+                    cudaStream_t s, int64_t row0 = 0);
 // block ILU(0) (ilu.cu): factorization, and one smoothing application
 // u_out = u_in + (LU)^-1 (f - A u_in)  (u_in == nullptr: zero guess, r = f)
 void setup_ilu0(const Bsr3 &A, Smoother &M, DevError *err, cudaStream_t s);

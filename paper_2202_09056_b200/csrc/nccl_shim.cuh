@@ -12,8 +12,10 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <chrono>
 #include <cstdlib>
 #include <string>
+#include <thread>
 
 #include "common.cuh"
 
@@ -32,6 +34,10 @@ struct NcclApi {
                               ncclComm_t, cudaStream_t);
     ncclResult_t (*Broadcast)(const void *, void *, size_t, ncclDataType_t, int, ncclComm_t,
                               cudaStream_t);
+    ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t,
+                              cudaStream_t);
+    ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t *);
+    ncclResult_t (*CommAbort)(ncclComm_t);
 };
 
 inline const NcclApi &nccl() {
@@ -58,9 +64,42 @@ inline const NcclApi &nccl() {
         a.Recv = reinterpret_cast<decltype(a.Recv)>(get("ncclRecv"));
         a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(get("ncclAllReduce"));
         a.Broadcast = reinterpret_cast<decltype(a.Broadcast)>(get("ncclBroadcast"));
+        a.AllGather = reinterpret_cast<decltype(a.AllGather)>(get("ncclAllGather"));
+        a.CommGetAsyncError =
+            reinterpret_cast<decltype(a.CommGetAsyncError)>(get("ncclCommGetAsyncError"));
+        a.CommAbort = reinterpret_cast<decltype(a.CommAbort)>(get("ncclCommAbort"));
         return a;
     }();
     return api;
+}
+
+inline void nccl_check(ncclResult_t r, const char *what) {
+    if (r != ncclSuccess && r != ncclInProgress)
+        fail(SAMG_NCCL_ERROR, std::string(what) + " failed: " + nccl().GetErrorString(r));
+}
+#define NK(x) ::samgb::nccl_check((x), #x)
+
+// Wait for stream s while polling the communicator for asynchronous errors
+// (a dead or failed peer): a plain cudaStreamSynchronize would hang on an
+// NCCL kernel that never completes.  On an error the communicator is
+// aborted (its kernels return) and SAMG_NCCL_ERROR is raised.
+inline void stream_wait(ncclComm_t comm, cudaStream_t s) {
+    if (!comm) {
+        CK(cudaStreamSynchronize(s));
+        return;
+    }
+    for (int spin = 0;; ++spin) {
+        const cudaError_t q = cudaStreamQuery(s);
+        if (q == cudaSuccess) return;
+        if (q != cudaErrorNotReady) CK(q);
+        ncclResult_t ar = ncclSuccess;
+        NK(nccl().CommGetAsyncError(comm, &ar));
+        if (ar != ncclSuccess && ar != ncclInProgress) {
+            nccl().CommAbort(comm);
+            fail(SAMG_NCCL_ERROR, std::string("NCCL asynchronous error: ") + nccl().GetErrorString(ar));
+        }
+        if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
 }
 
 } // namespace samgb

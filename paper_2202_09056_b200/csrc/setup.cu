@@ -332,13 +332,13 @@ constexpr int kQrLanes = 16;
 
 __global__ void __launch_bounds__(256) k_tentative_qr(int64_t naggs, int pbs, int k,
         const int *nodes, const int *agg_ptr, const double *B, int64_t bnrows, double *work,
-        double *Qw, double *Pt, double *Bc) {
+        double *Qw, double *Pt, double *Bc, int64_t a0, int64_t a1) {
     __shared__ double Rs[256 / kQrLanes][144];
-    const int64_t a = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / kQrLanes;
+    const int64_t a = a0 + (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / kQrLanes;
     const int lane = threadIdx.x % kQrLanes;
     const int base = (threadIdx.x % 32) & ~(kQrLanes - 1);
     const unsigned mask = 0xffffu << base;
-    if (a >= naggs) return;  // whole group
+    if (a >= a1) return;  // whole group
     double *R = Rs[threadIdx.x / kQrLanes];
     const int n0 = agg_ptr[a], n1 = agg_ptr[a + 1];
     const int64_t m = static_cast<int64_t>(pbs) * (n1 - n0);
@@ -451,10 +451,11 @@ __device__ __forceinline__ bool strong(const int *gp, const int *gc, int node, i
 // touched aggregates of each node: agg(node) + agg(c) for kept node columns
 __global__ void k_psm_touch(int nnodes, int h, const int *ptr, const int *col, const int *gp,
                             const int *gc, const int *agg, const int *toff, int *tlist,
-                            int *tcnt) {
-    const int node = blockIdx.x * blockDim.x + threadIdx.x;
-    if (node >= nnodes) return;
-    int *L = tlist + toff[node];
+                            int *tcnt, int node0 = 0) {
+    const int ln = blockIdx.x * blockDim.x + threadIdx.x;  // local node (lists)
+    if (ln >= nnodes) return;
+    const int node = node0 + ln;                           // global node
+    int *L = tlist + toff[ln];
     int n = 0;
     L[n++] = agg[node];
     for (int r = 0; r < h; ++r) {
@@ -481,7 +482,7 @@ __global__ void k_psm_touch(int nnodes, int h, const int *ptr, const int *col, c
         while (q > 0 && L[q - 1] > v) { L[q] = L[q - 1]; --q; }
         L[q] = v;
     }
-    tcnt[node] = n;
+    tcnt[ln] = n;
 }
 
 __global__ void k_psm_cols(int nbrows, int h, int kb, const int *toff, const int *tlist,
@@ -498,9 +499,10 @@ __global__ void k_psm_cols(int nbrows, int h, int kb, const int *toff, const int
 // filtered scalar diagonal D_f (coarsening.hpp:335-358)
 __global__ void k_psm_diag(int64_t nsc, int pbs, const int *ptr, const int *col,
                            const double *val, const int *gp, const int *gc, double *dinv,
-                           double *diag, DevError *err) {
-    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (i >= nsc) return;
+                           double *diag, DevError *err, int64_t off = 0) {
+    const int64_t li = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (li >= nsc) return;
+    const int64_t i = li + off;  // global scalar row
     const int br = static_cast<int>(i / 3), rr = static_cast<int>(i % 3);
     const int node = static_cast<int>(i / pbs);
     double d = 0.0;
@@ -519,10 +521,10 @@ __global__ void k_psm_diag(int64_t nsc, int pbs, const int *ptr, const int *col,
             }
         }
     }
-    diag[i] = d;
-    if (d == 0.0) { raise(err, SAMG_ZERO_DIAGONAL, i); dinv[i] = 0.0; return; }
-    if (fabs(d) < 1e-300) { raise(err, SAMG_SINGULAR_BLOCK, i); dinv[i] = 0.0; return; }
-    dinv[i] = __ddiv_rn(1.0, d);
+    diag[li] = d;
+    if (d == 0.0) { raise(err, SAMG_ZERO_DIAGONAL, i); dinv[li] = 0.0; return; }
+    if (fabs(d) < 1e-300) { raise(err, SAMG_SINGULAR_BLOCK, i); dinv[li] = 0.0; return; }
+    dinv[li] = __ddiv_rn(1.0, d);
 }
 
 // P row values: for each touched aggregate g, in ascending scalar column
@@ -531,15 +533,17 @@ __global__ void k_psm_vals(int64_t nsc, int pbs, int h, int k, const int *ptr, c
                            const double *val, const int *gp, const int *gc, const int *agg,
                            const int *toff, const int *tlist, const int *tcnt,
                            const double *dinv, const double *diag, const double *Pt,
-                           double omega, const int *pptr, double *pval) {
-    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (i >= nsc) return;
+                           double omega, const int *pptr, double *pval, int64_t off = 0) {
+    const int64_t li = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (li >= nsc) return;
+    const int64_t i = li + off;  // global scalar row
     const int br = static_cast<int>(i / 3), rr = static_cast<int>(i % 3);
     const int node = static_cast<int>(i / pbs);
+    const int lnode = static_cast<int>(li / pbs), lbr = static_cast<int>(li / 3);
     const int kb = k / 3;
-    const int *L = tlist + toff[node];
-    const int nt = tcnt[node];
-    const double di = dinv[i], dg = diag[i];
+    const int *L = tlist + toff[lnode];
+    const int nt = tcnt[lnode];
+    const double di = dinv[li], dg = diag[li];
     const double nom = -omega;
     for (int t = 0; t < nt; ++t) {
         const int g = L[t];
@@ -566,7 +570,7 @@ __global__ void k_psm_vals(int64_t nsc, int pbs, int h, int k, const int *ptr, c
                 }
             }
         }
-        const int64_t base = pptr[br] + static_cast<int64_t>(t) * kb;
+        const int64_t base = pptr[lbr] + static_cast<int64_t>(t) * kb;
         for (int c = 0; c < k; ++c) pval[9 * (base + c / 3) + 3 * rr + c % 3] = acc[c];
     }
 }
@@ -596,20 +600,23 @@ __device__ __forceinline__ void bt_tent(double v, double *t) {
 
 // omega == 0: P = P_tent
 __global__ void k_bt_tent(int n, const int *agg, const double *pv, int *pptr, int *pcol,
-                          double *pval) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+                          double *pval, int row0 = 0) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;  // local row
     if (i > n) return;
     pptr[i] = i;
     if (i == n) return;
-    pcol[i] = agg[i];
-    bt_tent(pv[agg[i]], pval + 9 * static_cast<int64_t>(i));
+    const int g = agg[row0 + i];
+    pcol[i] = g;
+    bt_tent(pv[g], pval + 9 * static_cast<int64_t>(i));
 }
 
 // lumped filtered diagonal and its inverse, a thread per block row
 __global__ void k_bt_diag(int n, const int *ptr, const int *col, const double *val,
-                          const int *gp, const int *gc, double *dg, double *dinv, DevError *err) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+                          const int *gp, const int *gc, double *dg, double *dinv, DevError *err,
+                          int row0 = 0) {
+    const int li = blockIdx.x * blockDim.x + threadIdx.x;  // local row (dg / dinv)
+    if (li >= n) return;
+    const int i = row0 + li;                                 // global row
     double d[9];
     for (int e = 0; e < 9; ++e) d[e] = 0.0;
     for (int j = ptr[i]; j < ptr[i + 1]; ++j) {
@@ -620,34 +627,35 @@ __global__ void k_bt_diag(int n, const int *ptr, const int *col, const double *v
     }
     bool zero = true;
     for (int e = 0; e < 9; ++e) {
-        dg[9 * static_cast<int64_t>(i) + e] = d[e];
+        dg[9 * static_cast<int64_t>(li) + e] = d[e];
         if (d[e] != 0.0) zero = false;
     }
     double inv[9];
     if (zero) { raise(err, SAMG_ZERO_DIAGONAL, i); return; }
     if (!blk_inverse_ref(d, inv)) { raise(err, SAMG_SINGULAR_BLOCK, i); return; }
-    for (int e = 0; e < 9; ++e) dinv[9 * static_cast<int64_t>(i) + e] = inv[e];
+    for (int e = 0; e < 9; ++e) dinv[9 * static_cast<int64_t>(li) + e] = inv[e];
 }
 
 // one thread per P entry (row i, aggregate column g)
 __global__ void k_bt_vals(int64_t nnzb, int n, const int *ptr, const int *col, const double *val,
                           const int *gp, const int *gc, const int *agg, const double *pv,
                           const double *dg, const double *dinv, double omega, const int *pptr,
-                          const int *pcol, double *pval) {
+                          const int *pcol, double *pval, int row0 = 0) {
     const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (e >= nnzb) return;
-    const int i = lower_bound_int(pptr, n + 1, static_cast<int>(e) + 1) - 1;
+    const int li = lower_bound_int(pptr, n + 1, static_cast<int>(e) + 1) - 1;  // local row
+    const int i = row0 + li;                                                   // global row
     const int g = pcol[e];
     double acc[9], inv[9];
     bool touched = agg[i] == g;
     if (touched) bt_tent(pv[g], acc);
-    for (int q = 0; q < 9; ++q) inv[q] = dinv[9 * static_cast<int64_t>(i) + q];
+    for (int q = 0; q < 9; ++q) inv[q] = dinv[9 * static_cast<int64_t>(li) + q];
     const double nom = -omega;
     for (int j = ptr[i]; j < ptr[i + 1]; ++j) {
         const int k = col[j];
         if (agg[k] != g) continue;
         if (k != i && !strong(gp, gc, i, k)) continue;
-        const double *coef = k == i ? dg + 9 * static_cast<int64_t>(i) : val + 9 * static_cast<int64_t>(j);
+        const double *coef = k == i ? dg + 9 * static_cast<int64_t>(li) : val + 9 * static_cast<int64_t>(j);
         double sc[9], t[9], prod[9];
         blk_mul_ref(inv, coef, sc);
         for (int q = 0; q < 9; ++q) sc[q] = __dmul_rn(sc[q], nom);
@@ -665,19 +673,20 @@ __global__ void k_bt_vals(int64_t nnzb, int n, const int *ptr, const int *col, c
 
 // omega == 0: P is the tentative operator (coarsening.hpp:326)
 __global__ void k_ptent_bsr(int nbrows, int h, int k, const int *agg, const double *Pt,
-                            int *pptr, int *pcol, double *pval) {
-    const int br = blockIdx.x * blockDim.x + threadIdx.x;
+                            int *pptr, int *pcol, double *pval, int row0 = 0) {
+    const int br = blockIdx.x * blockDim.x + threadIdx.x;  // local block row
     if (br > nbrows) return;
     const int kb = k / 3;
     pptr[br] = br * kb;
     if (br == nbrows) return;
-    const int g = agg[br / h];
+    const int gb = row0 + br;  // global block row
+    const int g = agg[gb / h];
     for (int q = 0; q < kb; ++q) {
         pcol[br * kb + q] = g * kb + q;
         for (int r = 0; r < 3; ++r)
             for (int c = 0; c < 3; ++c)
                 pval[9 * (static_cast<int64_t>(br) * kb + q) + 3 * r + c] =
-                    Pt[(3 * static_cast<int64_t>(br) + r) * k + 3 * q + c];
+                    Pt[(3 * static_cast<int64_t>(gb) + r) * k + 3 * q + c];
     }
 }
 
@@ -1431,7 +1440,9 @@ int64_t aggregate(const Graph &G, DevBuf<int> &agg, cudaStream_t s, DevBuf<int> 
 }
 
 void tentative(const DevBuf<int> &agg, int64_t nnodes, int64_t naggs, int pbs, const double *B,
-               int k, DevBuf<double> &Pt, DevBuf<double> &Bc, DevError *err, cudaStream_t s) {
+               int k, DevBuf<double> &Pt, DevBuf<double> &Bc, DevError *err, cudaStream_t s,
+               int64_t a0, int64_t a1) {
+    if (a1 < 0) a1 = naggs;
     const int64_t nfine = nnodes * pbs;
     DevBuf<int> keys2(nnodes, s), iota(nnodes, s), nodes(nnodes, s), agg_ptr(naggs + 1, s);
     int *io = iota.p;
@@ -1453,22 +1464,26 @@ void tentative(const DevBuf<int> &agg, int64_t nnodes, int64_t naggs, int pbs, c
     Pt.alloc(nfine * k, s);
     Bc.alloc(naggs * k * k, s);
     DevBuf<double> work(nfine * k, s), Qw(nfine * k, s);
-    k_tentative_qr<<<ceil_div(naggs * kQrLanes, 256), 256, 0, s>>>(naggs, pbs, k, nodes.p,
-                                                                   agg_ptr.p, B, nfine, work.p,
-                                                                   Qw.p, Pt.p, Bc.p);
+    if (a1 > a0)
+        k_tentative_qr<<<ceil_div((a1 - a0) * kQrLanes, 256), 256, 0, s>>>(
+            naggs, pbs, k, nodes.p, agg_ptr.p, B, nfine, work.p, Qw.p, Pt.p, Bc.p, a0, a1);
     (void)err;
     CK_LAUNCH();
 }
 
 void smooth_prolongation(const Bsr3 &A, const Graph &G, const DevBuf<int> &agg, int64_t naggs,
                          int pbs, int k, const double *Pt, double omega, Bsr3 &P, DevError *err,
-                         cudaStream_t s) {
+                         cudaStream_t s, int64_t node0, int64_t node1) {
     const int h = pbs / 3, kb = k / 3;
-    const int64_t nbrows = A.nrows, nnodes = nbrows / h, nsc = 3 * nbrows;
+    if (node1 < 0) node1 = A.nrows / h;
+    // rows of the nodes [node0, node1): A (global numbering) must hold them
+    const int64_t nnodes = node1 - node0, nbrows = nnodes * h, nsc = 3 * nbrows;
+    const int64_t row0 = node0 * h;
     if (omega == 0.0) {
         P.alloc(nbrows, naggs * kb, nbrows * kb, s);
         k_ptent_bsr<<<ceil_div(nbrows + 1, 256), 256, 0, s>>>(static_cast<int>(nbrows), h, k, agg.p,
-                                                             Pt, P.ptr.p, P.col.p, P.val.p);
+                                                             Pt, P.ptr.p, P.col.p, P.val.p,
+                                                             static_cast<int>(row0));
         CK_LAUNCH();
         return;
     }
@@ -1477,13 +1492,14 @@ void smooth_prolongation(const Bsr3 &A, const Graph &G, const DevBuf<int> &agg, 
     const int *ap = A.ptr.p;
     int *rlp = rl.p;
     for_each(nnodes, [=] __device__(int64_t nd) {
-        rlp[nd] = ap[(nd + 1) * h] - ap[nd * h] + 1;
+        rlp[nd] = ap[(node0 + nd + 1) * h] - ap[(node0 + nd) * h] + 1;
     }, s);
     const int64_t tl = scan_counts(rl.p, toff.p, nnodes, s);
     DevBuf<int> tlist(tl + 1, s);
-    k_psm_touch<<<ceil_div(nnodes, 128), 128, 0, s>>>(static_cast<int>(nnodes), h, A.ptr.p,
-                                                      A.col.p, G.ptr.p, G.col.p, agg.p, toff.p,
-                                                      tlist.p, tcnt.p);
+    if (nnodes)
+        k_psm_touch<<<ceil_div(nnodes, 128), 128, 0, s>>>(static_cast<int>(nnodes), h, A.ptr.p,
+                                                          A.col.p, G.ptr.p, G.col.p, agg.p, toff.p,
+                                                          tlist.p, tcnt.p, static_cast<int>(node0));
     CK_LAUNCH();
     DevBuf<int> bcnt(nbrows + 1, s);
     int *bc = bcnt.p;
@@ -1495,33 +1511,37 @@ void smooth_prolongation(const Bsr3 &A, const Graph &G, const DevBuf<int> &agg, 
     P.nnzb = scan_counts(bcnt.p, P.ptr.p, nbrows, s);
     P.col.alloc(P.nnzb, s);
     P.val.alloc(9 * P.nnzb, s);
+    if (nbrows == 0) return;
     k_psm_cols<<<ceil_div(nbrows, 256), 256, 0, s>>>(static_cast<int>(nbrows), h, kb, toff.p,
                                                      tlist.p, tcnt.p, P.ptr.p, P.col.p);
     CK_LAUNCH();
     DevBuf<double> dinv(nsc, s), diag(nsc, s);
     k_psm_diag<<<ceil_div(nsc, 256), 256, 0, s>>>(nsc, pbs, A.ptr.p, A.col.p, A.val.p, G.ptr.p,
-                                                  G.col.p, dinv.p, diag.p, err);
+                                                  G.col.p, dinv.p, diag.p, err, 3 * row0);
     CK_LAUNCH();
     check_dev_error(err, s);
     k_psm_vals<<<ceil_div(nsc, 128), 128, 0, s>>>(nsc, pbs, h, k, A.ptr.p, A.col.p, A.val.p,
                                                   G.ptr.p, G.col.p, agg.p, toff.p, tlist.p,
                                                   tcnt.p, dinv.p, diag.p, Pt, omega, P.ptr.p,
-                                                  P.val.p);
+                                                  P.val.p, 3 * row0);
     CK_LAUNCH();
 }
 
 void block_transfer(const Bsr3 &A, const Graph &G, const DevBuf<int> &agg, int64_t naggs,
-                    double omega, Bsr3 &P, DevError *err, cudaStream_t s) {
-    const int n = static_cast<int>(A.nrows);
+                    double omega, Bsr3 &P, DevError *err, cudaStream_t s, int64_t r0, int64_t r1) {
+    const int nall = static_cast<int>(A.nrows);  // aggregate sizes over every node
+    if (r1 < 0) r1 = nall;
+    const int n = static_cast<int>(r1 - r0);      // rows [r0, r1) of P
     DevBuf<int> cnt(naggs + 1, s);
     DevBuf<double> pv(naggs + 1, s);
     CK(cudaMemsetAsync(cnt.p, 0, sizeof(int) * (naggs + 1), s));
-    k_bt_count<<<ceil_div(n, 256), 256, 0, s>>>(n, agg.p, cnt.p);
+    k_bt_count<<<ceil_div(nall, 256), 256, 0, s>>>(nall, agg.p, cnt.p);
     k_bt_scale<<<ceil_div(naggs, 256), 256, 0, s>>>(static_cast<int>(naggs), cnt.p, pv.p);
     CK_LAUNCH();
     if (omega == 0.0) {
         P.alloc(n, naggs, n, s);
-        k_bt_tent<<<ceil_div(n + 1, 256), 256, 0, s>>>(n, agg.p, pv.p, P.ptr.p, P.col.p, P.val.p);
+        k_bt_tent<<<ceil_div(n + 1, 256), 256, 0, s>>>(n, agg.p, pv.p, P.ptr.p, P.col.p, P.val.p,
+                                                       static_cast<int>(r0));
         CK_LAUNCH();
         return;
     }
@@ -1530,11 +1550,12 @@ void block_transfer(const Bsr3 &A, const Graph &G, const DevBuf<int> &agg, int64
     DevBuf<int> rl(n + 1, s), toff(n + 1, s), tcnt(n + 1, s);
     const int *ap = A.ptr.p;
     int *rlp = rl.p;
-    for_each(n, [=] __device__(int64_t i) { rlp[i] = ap[i + 1] - ap[i] + 1; }, s);
+    for_each(n, [=] __device__(int64_t i) { rlp[i] = ap[r0 + i + 1] - ap[r0 + i] + 1; }, s);
     const int64_t tl = scan_counts(rl.p, toff.p, n, s);
     DevBuf<int> tlist(tl + 1, s);
-    k_psm_touch<<<ceil_div(n, 128), 128, 0, s>>>(n, 1, A.ptr.p, A.col.p, G.ptr.p, G.col.p, agg.p,
-                                                 toff.p, tlist.p, tcnt.p);
+    if (n)
+        k_psm_touch<<<ceil_div(n, 128), 128, 0, s>>>(n, 1, A.ptr.p, A.col.p, G.ptr.p, G.col.p, agg.p,
+                                                     toff.p, tlist.p, tcnt.p, static_cast<int>(r0));
     CK_LAUNCH();
     P.nrows = n;
     P.ncols = naggs;
@@ -1542,16 +1563,17 @@ void block_transfer(const Bsr3 &A, const Graph &G, const DevBuf<int> &agg, int64
     P.nnzb = scan_counts(tcnt.p, P.ptr.p, n, s);
     P.col.alloc(P.nnzb, s);
     P.val.alloc(9 * P.nnzb, s);
+    if (n == 0) return;
     k_psm_cols<<<ceil_div(n, 256), 256, 0, s>>>(n, 1, 1, toff.p, tlist.p, tcnt.p, P.ptr.p,
                                                 P.col.p);
     DevBuf<double> dg(9 * static_cast<int64_t>(n) + 1, s), dinv(9 * static_cast<int64_t>(n) + 1, s);
     k_bt_diag<<<ceil_div(n, 128), 128, 0, s>>>(n, A.ptr.p, A.col.p, A.val.p, G.ptr.p, G.col.p,
-                                               dg.p, dinv.p, err);
+                                               dg.p, dinv.p, err, static_cast<int>(r0));
     CK_LAUNCH();
     check_dev_error(err, s);
     k_bt_vals<<<std::max<int64_t>(1, ceil_div(P.nnzb, 128)), 128, 0, s>>>(
         P.nnzb, n, A.ptr.p, A.col.p, A.val.p, G.ptr.p, G.col.p, agg.p, pv.p, dg.p, dinv.p, omega,
-        P.ptr.p, P.col.p, P.val.p);
+        P.ptr.p, P.col.p, P.val.p, static_cast<int>(r0));
     CK_LAUNCH();
 }
 
@@ -1902,7 +1924,7 @@ void slice_rows(const Bsr3 &M, int64_t r0, int64_t r1, Bsr3 &out, cudaStream_t s
 // Rows of the Galerkin product for the rows of Rl (a row slice of R, or R):
 // (Rl A) P, with P's columns read through the full R = P^T.
 void galerkin_rows(const Bsr3 &Rl, const Bsr3 &A, const Bsr3 &P, const Bsr3 &R, Bsr3 &Ac,
-                   cudaStream_t s, bool scalar_order) {
+                   cudaStream_t s, bool scalar_order, bool subset) {
     Bsr3 RA;
     {
         DevBuf<int> tpos(std::max<int64_t>(1, A.nnzb), s), bad(1, s);
@@ -1916,7 +1938,11 @@ void galerkin_rows(const Bsr3 &Rl, const Bsr3 &A, const Bsr3 &P, const Bsr3 &R, 
         CK(cudaStreamSynchronize(s));
         BCols ba;
         ba.cp = A.ptr.p; ba.ri = A.col.p; ba.pos = tpos.p; ba.val = A.val.p; ba.tr = false;
-        const BCols *pa = (hbad || A.nrows != A.ncols) ? nullptr : &ba;
+        // subset: A holds only some rows (global numbering, the others
+        // empty), so transpose positions into rows it lacks are missing;
+        // they are never read -- a hit needs the row in Rl's pattern, whose
+        // rows A holds (dsetup.cu)
+        const BCols *pa = ((hbad && !subset) || A.nrows != A.ncols) ? nullptr : &ba;
         if (scalar_order) spgemm_impl<true>(Rl, A, RA, s, pa);
         else spgemm_impl<false>(Rl, A, RA, s, pa);
     }
@@ -1971,13 +1997,14 @@ void union_diff(const Bsr3 &A, const Bsr3 &G, double out[2], cudaStream_t s) {
     CK(cudaStreamSynchronize(s));
 }
 
-void fix_decoupled_rows(Bsr3 &A, cudaStream_t s) {
+void fix_decoupled_rows(Bsr3 &A, cudaStream_t s, int64_t row0) {
     const int *ap = A.ptr.p, *ac = A.col.p;
     double *av = A.val.p;
+    const int r0 = static_cast<int>(row0);
     for_each(A.nrows, [=] __device__(int64_t i) {
         int dg = -1;
         for (int j = ap[i]; j < ap[i + 1]; ++j)
-            if (ac[j] == i) { dg = j; break; }
+            if (ac[j] == r0 + i) { dg = j; break; }
         for (int r = 0; r < 3; ++r) {
             bool zero_row = true;
             for (int j = ap[i]; zero_row && j < ap[i + 1]; ++j)
@@ -1989,8 +2016,9 @@ void fix_decoupled_rows(Bsr3 &A, cudaStream_t s) {
 }
 
 void setup_smoother(const Bsr3 &A, int kind, double omega, Smoother &M, DevError *err,
-                    cudaStream_t s) {
+                    cudaStream_t s, int64_t row0) {
     const int *ap = A.ptr.p, *ac = A.col.p;
+    const int r0 = static_cast<int>(row0);  // global id of local row 0 (diagonal = r0 + i)
     const double *av = A.val.p;
     DevError *ep = err;
     if (kind == SAMG_SMOOTHER_ILU0) {
@@ -2005,7 +2033,7 @@ void setup_smoother(const Bsr3 &A, int kind, double omega, Smoother &M, DevError
         double *m = M.data.p;
         for_each(A.nrows, [=] __device__(int64_t i) {
             int dg = -1;
-            for (int j = ap[i]; j < ap[i + 1]; ++j) if (ac[j] == i) { dg = j; break; }
+            for (int j = ap[i]; j < ap[i + 1]; ++j) if (ac[j] == r0 + i) { dg = j; break; }
             for (int r = 0; r < 3; ++r) {
                 const double d = dg >= 0 ? av[9 * static_cast<int64_t>(dg) + 4 * r] : 0.0;
                 if (d == 0.0) { raise(ep, SAMG_ZERO_DIAGONAL, 3 * i + r); m[3 * i + r] = 0.0; continue; }
@@ -2022,7 +2050,7 @@ void setup_smoother(const Bsr3 &A, int kind, double omega, Smoother &M, DevError
         int dg = -1;
         double den = 0.0;
         for (int j = ap[i]; j < ap[i + 1]; ++j) {
-            if (ac[j] == i) dg = j;
+            if (ac[j] == r0 + i) dg = j;
             const double *b = av + 9 * static_cast<int64_t>(j);
             for (int e = 0; e < 9; ++e) den = __dadd_rn(den, __dmul_rn(b[e], b[e]));
         }

@@ -26,6 +26,51 @@ namespace samgb {
 
 namespace {
 
+// ---- programmatic dependent launch (PDL) ------------------------------------
+// Back-to-back standalone SpMVs (samg_bsr3_spmv_device: a caller's loop of
+// y = A x) are launched with programmatic stream serialization: SpMV k+1 is
+// scheduled while the last CTAs of SpMV k run, its TMA producer streams the
+// matrix at once (independent of k), and its consumers read x only after
+// griddepcontrol.wait (k complete, its writes visible) plus a GPU-scope
+// acquire fence.  The fence is needed: a dependent grid is not preceded by
+// the launch-time L1 invalidation of a normal launch, and x is gathered
+// through L1 (measured: without it CG lost its convergence).  Inside the
+// CG graph PDL is not used: the fence and the early-resident dependents cost
+// more than the overlapped tails gained (C1 0.521 -> 0.546 ms per
+// iteration, C4 13.9 -> 17.7 ms; profiles/README.md).  SAMG_PDL=0 disables.
+__device__ __forceinline__ void pdl_wait() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char *e = std::getenv("SAMG_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+thread_local bool g_spmv_pdl = false;  // set around standalone SpMV launches
+
+// kernel launch, with the PDL attribute if `pdl` (the kernel then calls
+// pdl_wait before it reads a predecessor's output)
+template <class... KArgs, class... Args>
+void launch_k(bool pdl, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+              Args &&...args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    CK(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...));
+}
+
 __device__ __forceinline__ double ld_stream(const double *p) { return __ldcs(p); }
 
 __device__ __forceinline__ double2 ldg2(const double *p) {
@@ -309,6 +354,7 @@ __device__ void cg_apply(int what, double s, CgScalars *sc, cudaGraphConditional
             break;
         case CG_RHO: sc->rho = s; break;
         case CG_STORE: sc->tmp = s; break;
+        case CG_STORE2: sc->tmp2 = s; break;
         case CG_ADD: sc->tmp += s; break;  // further row ranges of one product
         case CG_RR_LOOP: {
             sc->rr = s;
@@ -416,6 +462,8 @@ struct TmaHdr {
 
 struct TmaCfg {
     int nrows, nchunks, stages;
+    int pmis;     // ptr's misalignment in ints (a row view of a larger matrix: ptr + r0)
+    int pdl;      // launched as a programmatic dependent (consumers wait + fence)
     int per_cta;  // > 0: CTA b owns the contiguous chunks [b*per_cta, (b+1)*per_cta)
                   // (neighbouring rows share x, so the gathers hit L1); 0: strided
     unsigned vcap, ccap, pcap;  // stage layout: val | col | ptr (bytes)
@@ -480,23 +528,24 @@ __global__ void __launch_bounds__(32 * (TW * NT + 1), 1) k_bsr3_tma(TmaCfg cfg, 
                     constexpr long long BB = 9 * sizeof(VT);  // bytes per stored block
                     const long long vb = (BB * p0) & ~15LL, ve = (BB * p1 + 15) & ~15LL;
                     const long long cb = (4LL * p0) & ~15LL, ce = (4LL * p1 + 15) & ~15LL;
-                    const long long pe = 4LL * (r0 + RPC + 4);
+                    // ptr entries [r0 - pmis, r0 - pmis + RPC + 8): a 16-byte
+                    // aligned window holding [r0, r0 + RPC]
+                    const long long pbytes = 4LL * (RPC + 8);
                     const bool direct = ve - vb > cfg.vcap || ce - cb > cfg.ccap ||
                                         ve > BB * cfg.nnzb || ce > 4LL * cfg.nnzb ||
-                                        r0 + RPC + 4 > cfg.nrows + 1 || p1 == p0;
+                                        r0 - cfg.pmis + RPC + 8 > cfg.nrows + 1 || p1 == p0;
                     hdr[st] = TmaHdr{p0, direct ? 1 : 0,
                                      static_cast<int>((BB * p0 - vb) / static_cast<long long>(sizeof(VT))),
                                      static_cast<int>((4LL * p0 - cb) / 4)};
                     if (!direct) {
                         unsigned char *sv = data + static_cast<size_t>(st) * stage_bytes;
-                        mbar_arrive_tx(full + st, static_cast<unsigned>((ve - vb) + (ce - cb) +
-                                                                        (pe - 4LL * r0)));
+                        mbar_arrive_tx(full + st, static_cast<unsigned>((ve - vb) + (ce - cb) + pbytes));
                         bulk_g2s(sv, reinterpret_cast<const char *>(val) + vb,
                                  static_cast<unsigned>(ve - vb), full + st);
                         bulk_g2s(sv + cfg.vcap, reinterpret_cast<const char *>(col) + cb,
                                  static_cast<unsigned>(ce - cb), full + st);
-                        bulk_g2s(sv + cfg.vcap + cfg.ccap, ptr + r0,
-                                 static_cast<unsigned>(pe - 4LL * r0), full + st);
+                        bulk_g2s(sv + cfg.vcap + cfg.ccap, ptr + r0 - cfg.pmis,
+                                 static_cast<unsigned>(pbytes), full + st);
                     } else {
                         mbar_arrive(full + st);
                     }
@@ -506,7 +555,10 @@ __global__ void __launch_bounds__(32 * (TW * NT + 1), 1) k_bsr3_tma(TmaCfg cfg, 
         }
     } else {
         // NT teams of TW consumer warps take the CTA's chunks in turn, so NT
-        // chunks are computed concurrently while the ring fills
+        // chunks are computed concurrently while the ring fills.  The
+        // producer streams the matrix (independent of the previous kernel)
+        // at once; x / f / u are read only after the PDL wait.
+        if (cfg.pdl) pdl_wait();
         const int team = warp / TW, tt = threadIdx.x - 32 * TW * team;
         const int lane = tt % G, grp = tt / G;
         for (int i = team, c = chunk_of(cfg, team); c >= 0; i += NT, c = chunk_of(cfg, i)) {
@@ -523,7 +575,7 @@ __global__ void __launch_bounds__(32 * (TW * NT + 1), 1) k_bsr3_tma(TmaCfg cfg, 
                 const unsigned char *sv = data + static_cast<size_t>(st) * stage_bytes;
                 const VT *svd = reinterpret_cast<const VT *>(sv);
                 const int *svc = reinterpret_cast<const int *>(sv + cfg.vcap);
-                const int *svp = reinterpret_cast<const int *>(sv + cfg.vcap + cfg.ccap);
+                const int *svp = reinterpret_cast<const int *>(sv + cfg.vcap + cfg.ccap) + cfg.pmis;
                 double a0 = 0.0, a1 = 0.0, a2 = 0.0;
                 constexpr int kUnr = sizeof(VT) == 4 ? 4 : 2;
                 if (valid) {
@@ -557,6 +609,7 @@ __global__ void __launch_bounds__(32 * (TW * NT + 1), 1) k_bsr3_tma(TmaCfg cfg, 
             }
         }
     }
+    if (cfg.pdl) pdl_trigger();
     if constexpr (kReduce) grid_finish(d, partials, sc, what, 0);
 }
 
@@ -651,8 +704,10 @@ template <bool kReduce, class VT, class Epi>
 bool launch_tma(const Bsr3 &A, const VT *val, const double *x, Epi epi, double *partials,
                 CgScalars *sc, int what, cudaStream_t s) {
     if (A.nrows < 8 || A.nnzb == 0) return false;
-    if ((reinterpret_cast<uintptr_t>(val) | reinterpret_cast<uintptr_t>(A.col.p) |
-         reinterpret_cast<uintptr_t>(A.ptr.p)) & 15)
+    // val / col: the full arrays (16-byte aligned allocations); ptr may be a
+    // row view's offset pointer (the multi-GPU interior rows), handled in-kernel
+    if ((reinterpret_cast<uintptr_t>(val) | reinterpret_cast<uintptr_t>(A.col.p)) & 15 ||
+        reinterpret_cast<uintptr_t>(A.ptr.p) & 3)
         return false;
     static const int forced_g = env_int("SAMG_TMA_G", 0);
     static const int budget64 = env_int("SAMG_TMA_SMEM", 226000);
@@ -674,7 +729,9 @@ bool launch_tma(const Bsr3 &A, const VT *val, const double *x, Epi epi, double *
     cfg.nnzb = A.nnzb;
     cfg.vcap = up(rpc * est * 9 * static_cast<long long>(sizeof(VT)) + 16);
     cfg.ccap = up(rpc * est * 4 + 16);
-    cfg.pcap = up(4LL * (rpc + 4));
+    cfg.pcap = up(4LL * (rpc + 8));
+    cfg.pmis = static_cast<int>((reinterpret_cast<uintptr_t>(A.ptr.p) & 15) / 4);
+    cfg.pdl = g_spmv_pdl && pdl_enabled() ? 1 : 0;
     const long long stage = cfg.vcap + cfg.ccap + cfg.pcap;
     cfg.stages = static_cast<int>(std::min<long long>(16, (budget - kTmaHdrBytes) / stage));
     if (cfg.stages < NT + 1) return false;
@@ -713,7 +770,7 @@ bool launch_tma(const Bsr3 &A, const VT *val, const double *x, Epi epi, double *
         if (tma_cta_cap() > 0) grid = std::min(grid, tma_cta_cap());
         static const int blocked = env_int("SAMG_TMA_BLOCKED", 0);
         cfg.per_cta = blocked ? (cfg.nchunks + grid - 1) / grid : 0;
-        kern<<<grid, threads, smem, s>>>(cfg, A.ptr.p, A.col.p, val, x, epi, partials, sc, what);
+        launch_k(cfg.pdl != 0, kern, grid, threads, smem, s, cfg, A.ptr.p, A.col.p, val, x, epi, partials, sc, what);
         ok = true;
     });
     if (ok) CK_LAUNCH();
@@ -728,13 +785,13 @@ void launch_rows_t(const Bsr3 &A, const VT *val, const double *x, Epi epi, cudaS
     const int n = static_cast<int>(A.nrows);
     if (std::is_same_v<VT, double> && spmv_variant() == 0) {
         const double *vd = reinterpret_cast<const double *>(val);
-        if (G == 32) k_bsr3<32, 0><<<grid, 256, 0, s>>>(n, A.ptr.p, A.col.p, vd, x, epi);
-        else if (G == 16) k_bsr3<16, 0><<<grid, 256, 0, s>>>(n, A.ptr.p, A.col.p, vd, x, epi);
-        else k_bsr3<8, 0><<<grid, 256, 0, s>>>(n, A.ptr.p, A.col.p, vd, x, epi);
+        if (G == 32) launch_k(false, k_bsr3<32, 0, Epi, double>, grid, 256, 0, s, n, A.ptr.p, A.col.p, vd, x, epi);
+        else if (G == 16) launch_k(false, k_bsr3<16, 0, Epi, double>, grid, 256, 0, s, n, A.ptr.p, A.col.p, vd, x, epi);
+        else launch_k(false, k_bsr3<8, 0, Epi, double>, grid, 256, 0, s, n, A.ptr.p, A.col.p, vd, x, epi);
     } else {
         dispatch_group(G, [&](auto g) {
             constexpr int GG = decltype(g)::value;
-            k_bsr3<GG, 1, Epi, VT><<<grid, 256, 0, s>>>(n, A.ptr.p, A.col.p, val, x, epi);
+            launch_k(false, k_bsr3<GG, 1, Epi, VT>, grid, 256, 0, s, n, A.ptr.p, A.col.p, val, x, epi);
         });
     }
     CK_LAUNCH();
@@ -767,7 +824,8 @@ void launch_reduce_t(const Bsr3 &A, const VT *val, const double *x, Epi epi, dou
         }();
         const int grid = std::max(1, std::min({kReduceCtas, resident,
                                                ceil_div(A.nrows * static_cast<int64_t>(GG), 256)}));
-        k_bsr3_reduce<GG, Epi, VT><<<grid, 256, 0, s>>>(n, A.ptr.p, A.col.p, val, x, epi, partials, sc, what);
+        launch_k(false, k_bsr3_reduce<GG, Epi, VT>, grid, 256, 0, s, n, A.ptr.p, A.col.p, val, x, epi, partials,
+                 sc, what);
     });
     CK_LAUNCH();
 }
@@ -809,8 +867,7 @@ __global__ void k_smooth_zero_block(int64_t nrows, const double *__restrict__ m,
 }
 
 // u = Ainv f, Ainv row-major with an even leading dimension (zero padded):
-// one 128-thread CTA per row, 16-byte loads, 4 in flight per thread.
-// One 64-thread CTA per row: 2 922 rows at C1 fit in one wave (32 resident
+// one 64-thread CTA per row: 2 922 rows at C1 fit in one wave (32 resident
 // CTAs per SM; 128-thread CTAs needed 1.23 waves, 20.4 us -> see profiles/),
 // eight 16-byte loads in flight per thread.
 constexpr int kGemvThreads = 64;
@@ -917,7 +974,14 @@ __global__ void k_fill(int64_t n, double v, double *x) {
         x[i] = v;
 }
 
-__global__ void k_cg_finish(CgScalars *sc, int what) { cg_apply(what, sc->tmp, sc, 0); }
+__global__ void k_cg_finish(CgScalars *sc, int what) {
+    cg_apply(what, sc->tmp, sc, 0);
+}
+
+__global__ void k_cg_finish2(CgScalars *sc, int rr_what, cudaGraphConditionalHandle h) {
+    cg_apply(CG_RZ, sc->tmp2, sc, 0);
+    cg_apply(rr_what, sc->tmp, sc, h);
+}
 
 int vec_grid(int64_t n) {
     const int64_t g = (n + 255) / 256;
@@ -927,6 +991,7 @@ int vec_grid(int64_t n) {
 } // namespace
 
 void set_spmv_cta_cap(int ctas) { g_tma_cta_cap = ctas; }
+void set_spmv_pdl(bool on) { g_spmv_pdl = on; }
 
 void launch_spmv(const Bsr3 &A, double alpha, const double *x, double beta, double *y,
                  cudaStream_t s, bool lowp) {
@@ -943,7 +1008,7 @@ void launch_spmv_rows(const Bsr3 &A, const int *rows, int64_t nlist, int group, 
     const EpiSpmv epi{alpha, beta, y};
     dispatch_group(G, [&](auto g) {
         constexpr int GG = decltype(g)::value;
-        k_bsr3_rows<GG><<<grid, 256, 0, s>>>(n, rows, A.ptr.p, A.col.p, A.val.p, x, epi);
+        launch_k(false, k_bsr3_rows<GG, EpiSpmv>, grid, 256, 0, s, n, rows, A.ptr.p, A.col.p, A.val.p, x, epi);
     });
     CK_LAUNCH();
 }
@@ -974,8 +1039,8 @@ void launch_smooth_zero(int64_t nrows, const Smoother &M, const double *f, doubl
                         cudaStream_t s) {
     if (nrows == 0) return;
     if (M.kind == SM_ILU) return launch_ilu_smooth(nullptr, M, f, nullptr, u, s);
-    if (M.kind == SM_POINT) k_smooth_zero_point<<<vec_grid(3 * nrows), 256, 0, s>>>(3 * nrows, M.data.p, f, u);
-    else k_smooth_zero_block<<<vec_grid(nrows), 256, 0, s>>>(nrows, M.data.p, f, u);
+    if (M.kind == SM_POINT) launch_k(false, k_smooth_zero_point, vec_grid(3 * nrows), 256, 0, s, 3 * nrows, M.data.p, f, u);
+    else launch_k(false, k_smooth_zero_block, vec_grid(nrows), 256, 0, s, nrows, M.data.p, f, u);
     CK_LAUNCH();
 }
 
@@ -1016,37 +1081,42 @@ void make_lowp(Bsr3 &A, cudaStream_t s) {
 void launch_dense_gemv(int64_t n, const double *Ainv, const double *f, double *u,
                        cudaStream_t s) {
     if (n == 0) return;
-    k_dense_gemv<<<static_cast<int>(n), kGemvThreads, 0, s>>>(static_cast<int>(n), dense_ld(n), Ainv, f, u);
+    launch_k(false, k_dense_gemv, static_cast<int>(n), kGemvThreads, 0, s, static_cast<int>(n), dense_ld(n), Ainv, f, u);
     CK_LAUNCH();
 }
 
 void launch_dot(int64_t n, const double *x, const double *y, double *partials, CgScalars *sc,
                 int what, cudaStream_t s) {
-    k_dot<<<vec_grid(n / 2 + 1), 256, 0, s>>>(n, x, y, partials, sc, what);
+    launch_k(false, k_dot, vec_grid(n / 2 + 1), 256, 0, s, n, x, y, partials, sc, what);
     CK_LAUNCH();
 }
 
 void launch_cg_update(int64_t n, CgScalars *sc, const double *p, const double *q, double *u,
                       double *r, double *partials, int what, cudaGraphConditionalHandle h,
                       cudaStream_t s) {
-    k_cg_update<<<vec_grid(n / 2 + 1), 256, 0, s>>>(n, sc, p, q, u, r, partials, what, h);
+    launch_k(false, k_cg_update, vec_grid(n / 2 + 1), 256, 0, s, n, sc, p, q, u, r, partials, what, h);
     CK_LAUNCH();
 }
 
 void launch_p_update(int64_t n, const CgScalars *sc, const double *z, double *p,
                      cudaStream_t s) {
-    k_p_update<<<vec_grid(n / 2 + 1), 256, 0, s>>>(n, sc, z, p);
+    launch_k(false, k_p_update, vec_grid(n / 2 + 1), 256, 0, s, n, static_cast<const CgScalars *>(sc), z, p);
     CK_LAUNCH();
 }
 
 void launch_cg_finish(CgScalars *sc, int what, cudaStream_t s) {
-    k_cg_finish<<<1, 1, 0, s>>>(sc, what);
+    launch_k(false, k_cg_finish, 1, 1, 0, s, sc, what);
+    CK_LAUNCH();
+}
+
+void launch_cg_finish2(CgScalars *sc, int rr_what, cudaGraphConditionalHandle h, cudaStream_t s) {
+    launch_k(false, k_cg_finish2, 1, 1, 0, s, sc, rr_what, h);
     CK_LAUNCH();
 }
 
 void launch_fill(int64_t n, double v, double *x, cudaStream_t s) {
     if (n == 0) return;
-    k_fill<<<vec_grid(n), 256, 0, s>>>(n, v, x);
+    launch_k(false, k_fill, vec_grid(n), 256, 0, s, n, v, x);
     CK_LAUNCH();
 }
 

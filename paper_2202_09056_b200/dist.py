@@ -192,16 +192,26 @@ def nccl_unique_id() -> bytes:
 
 
 class DistHierarchy:
-    """Multi-GPU ns_block hierarchy (samg_dsetup): every rank passes the same
-    global problem; the solve runs on the rank's rows with NCCL halos.  The
-    NCCL id is created on rank 0 and broadcast with torch.distributed.
+    """Multi-GPU hierarchy with a distributed setup (samg_dsetup*): every
+    rank builds only its rows of the large levels (dsetup.cu); the solve runs
+    on the rank's rows with NCCL halos.  The NCCL id is created on rank 0 and
+    broadcast with torch.distributed.
 
+    Input, one of:
+      * the global matrix (nbrows, ptr, col, val) and nullspace B on every
+        rank -- only the rank's rows are uploaded (samg_dsetup);
+      * ``local=(ptr, col, val, B_local)``: the rank's own rows (ptr from 0,
+        global column ids) and nullspace rows, with ``row_starts``
+        (samg_dsetup_local);
+      * ``device=(bsr3, d_B_ptr)``: the rank's rows as a device Bsr3 and
+        its nullspace rows in device memory (samg_dsetup_device).
     ``emulate=True`` drives all ``nranks`` slices from this process on one
-    GPU without NCCL (the halo, all-reduce and gather steps become device
-    copies); f and u are then the global vectors."""
+    GPU without NCCL (every exchange a device copy); f and u are then the
+    global vectors."""
 
     def __init__(self, nbrows, ptr, col, val, B, rank, nranks, dist=None, row_starts=None,
-                 min_rows=4096, prm=None, uid=None, emulate=False, pipeline="ns_block"):
+                 min_rows=4096, prm=None, uid=None, emulate=False, pipeline="ns_block",
+                 local=None, device=None, b_cols=6):
         from .api import AmgParams, _nullspace, _pipeline
         prm = prm or AmgParams()
         idbuf = None
@@ -215,18 +225,38 @@ class DistHierarchy:
                     dist.broadcast_object_list(obj, src=0)
                 uid = obj[0]
             idbuf = (C.c_ubyte * 128).from_buffer_copy(uid)
-        ptr, col = _i64(ptr), _i64(col)
-        val = np.ascontiguousarray(val, dtype=np.float64)
-        Bv, brows, k = _nullspace(B, 3 * nbrows)
         rs = None if row_starts is None else _i64(row_starts)
         pc = prm.c()
         h = vp()
-        check(lib.samg_dsetup(idbuf, nranks, rank, nbrows, ptr.ctypes.data_as(i64p),
-                              col.ctypes.data_as(i64p), val.ctypes.data_as(f64p),
-                              Bv.ctypes.data_as(f64p) if Bv is not None else None, brows, k,
-                              rs.ctypes.data_as(i64p) if rs is not None else None, min_rows,
-                              _pipeline(pipeline),
-                              C.byref(pc), C.byref(h)))
+        if local is not None or device is not None:
+            if emulate or rs is None:
+                raise ValueError("local / device input needs NCCL and row_starts")
+            if device is not None:
+                A, bptr = device
+                check(lib.samg_dsetup_device(idbuf, nranks, rank, rs.ctypes.data_as(i64p), A.h,
+                                             bptr or None, b_cols, min_rows, _pipeline(pipeline),
+                                             C.byref(pc), C.byref(h)))
+            else:
+                lp, lc, lv, lb = local
+                lp, lc = _i64(lp), _i64(lc)
+                lv = np.ascontiguousarray(lv, dtype=np.float64)
+                lb = None if lb is None else np.ascontiguousarray(lb, dtype=np.float64)
+                check(lib.samg_dsetup_local(idbuf, nranks, rank, rs.ctypes.data_as(i64p),
+                                            lp.ctypes.data_as(i64p), lc.ctypes.data_as(i64p),
+                                            lv.ctypes.data_as(f64p),
+                                            lb.ctypes.data_as(f64p) if lb is not None else None,
+                                            b_cols, min_rows, _pipeline(pipeline), C.byref(pc),
+                                            C.byref(h)))
+        else:
+            ptr, col = _i64(ptr), _i64(col)
+            val = np.ascontiguousarray(val, dtype=np.float64)
+            Bv, brows, k = _nullspace(B, 3 * nbrows)
+            check(lib.samg_dsetup(idbuf, nranks, rank, nbrows, ptr.ctypes.data_as(i64p),
+                                  col.ctypes.data_as(i64p), val.ctypes.data_as(f64p),
+                                  Bv.ctypes.data_as(f64p) if Bv is not None else None, brows, k,
+                                  rs.ctypes.data_as(i64p) if rs is not None else None, min_rows,
+                                  _pipeline(pipeline),
+                                  C.byref(pc), C.byref(h)))
         self.h = h
         self.rank, self.nranks = rank, nranks
 
@@ -247,14 +277,14 @@ class DistHierarchy:
         ss = C.c_double()
         check(lib.samg_dinfo(self.h, C.byref(r0), C.byref(r1), C.byref(nl), C.byref(dl),
                              C.byref(ss)))
-        sl = C.c_int()
-        check(lib.samg_dsliced_levels(self.h, C.byref(sl)))
+        hr = C.c_int64()
+        check(lib.samg_dheld_rows(self.h, C.byref(hr)))
         return dict(row0=r0.value, row1=r1.value, nlevels=nl.value, dist_levels=dl.value,
-                    setup_seconds=ss.value, sliced_levels=sl.value)
+                    setup_seconds=ss.value, held_rows=hr.value)
 
     def level(self, level, which=0):
         """(nrows, ncols, ptr, col, val[nnzb,3,3]) of the global A (0), P (1)
-        or R (2) of `level` (every rank holds them)."""
+        or R (2) of `level`, assembled from every rank's rows (collective)."""
         import numpy as np
         nr, nc, nz = C.c_int64(), C.c_int64(), C.c_int64()
         check(lib.samg_dlevel_info(self.h, level, which, C.byref(nr), C.byref(nc), C.byref(nz)))

@@ -166,13 +166,16 @@ def test_emulated_rejects_empty_rank(gpu):
                       emulate=True)
 
 
-@pytest.mark.parametrize("world,uneven,pipeline", [(2, False, "ns_block"), (3, True, "ns_block"),
-                                                   (4, False, "ns_hybrid2"), (3, False, "block")])
-def test_sliced_galerkin_setup_is_bit_identical(gpu, world, uneven, pipeline):
-    """The multi-GPU setup forms each level's Galerkin product row-sliced
-    (rank q its own coarse rows, then assembled on every rank).  Emulated
-    here rank by rank: every level matrix must be bit-identical to the
-    single-GPU setup's, and the slicing must actually have happened."""
+@pytest.mark.parametrize("world,uneven,pipeline,min_rows", [
+    (2, False, "ns_block", 1), (3, True, "ns_block", 1), (4, False, "ns_hybrid2", 1),
+    (3, False, "block", 1), (5, True, "ns_block", 1), (3, False, "ns_hybrid1", 1),
+    (4, False, "ns_block", 200)])
+def test_distributed_setup_is_bit_identical(gpu, world, uneven, pipeline, min_rows):
+    """The multi-GPU setup is distributed (dsetup.cu): every rank builds only
+    its rows of each level from its own rows plus fetched halo rows; the
+    node graph is gathered so that the aggregation is global.  Emulated here
+    rank by rank: every level matrix, assembled from the ranks' rows, must
+    be bit-identical to the single-GPU setup's (and so to the reference)."""
     from paper_2202_09056_b200.dist import DistHierarchy
     pb = gpu
     p = pb.generate_hex(nx=16, ny=8, nz=8, dirichlet="eliminate", load="traction_xend")
@@ -181,15 +184,50 @@ def test_sliced_galerkin_setup_is_bit_identical(gpu, world, uneven, pipeline):
     h = pb.setup_bsr3(p.nbrows, p.ptr, p.col, p.val.reshape(-1), B, pipeline, prm)
     rs = None
     if uneven:
-        rs = np.array([0, p.nbrows // 5, p.nbrows // 2, p.nbrows], np.int64)
+        cuts = np.cumsum([1] + [2 * k + 1 for k in range(world - 1)])
+        rs = np.concatenate([[0], np.round(p.nbrows * cuts / cuts[-1] * 0.999).astype(np.int64)])
+        rs[-1] = p.nbrows
     dh = DistHierarchy(p.nbrows, p.ptr, p.col, p.val.reshape(-1), B, 0, world, row_starts=rs,
-                       min_rows=1, prm=prm, emulate=True, pipeline=pipeline)
+                       min_rows=min_rows, prm=prm, emulate=True, pipeline=pipeline)
     inf = dh.info()
     assert inf["nlevels"] == h.nlevels
-    assert inf["sliced_levels"] >= 1
+    if min_rows == 1:
+        assert inf["dist_levels"] >= 2
     for lvl in range(h.nlevels):
         for w in ((0, 1, 2) if lvl + 1 < h.nlevels else (0,)):
             a, b = h.level(lvl, w), dh.level(lvl, w)
             assert a[0] == b[0] and a[1] == b[1], (lvl, w)
             for x, y in zip(a[2:], b[2:]):
                 assert np.array_equal(x, y), (lvl, w)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_distributed_setup_holds_slab_plus_halo(gpu, world):
+    """No rank holds more of A_0 than its slab plus the halo layers the
+    setup needs (strength: one node layer; Galerkin: the rows within the
+    support of its aggregates' prolongator columns and their neighbours).
+    A slender x-slowest beam: every rank owns 10 x-planes of 49 nodes."""
+    from paper_2202_09056_b200.dist import DistHierarchy
+    pb = gpu
+    p = pb.generate_hex(nx=10 * world, ny=6, nz=6, lx=10.0 * world / 6, dirichlet="eliminate",
+                        load="traction_xend", x_slowest=True)
+    plane = 7 * 7
+    rs = np.array([10 * plane * r for r in range(world + 1)], np.int64)
+    prm = pb.AmgParams(coarse_enough=60)
+    h = pb.setup_bsr3(p.nbrows, p.ptr, p.col, p.val.reshape(-1), p.nullspace(), "ns_block", prm)
+    dh = DistHierarchy(p.nbrows, p.ptr, p.col, p.val.reshape(-1), p.nullspace(), 0, world,
+                       row_starts=rs, min_rows=1, prm=prm, emulate=True)
+    inf = dh.info()
+    # rank 0: its 10 planes + at most 6 halo planes on its one neighbour side
+    assert 10 * plane < inf["held_rows"] <= 16 * plane, inf
+    assert inf["held_rows"] < p.nbrows
+    for lvl in range(h.nlevels):
+        for w in ((0, 1, 2) if lvl + 1 < h.nlevels else (0,)):
+            a, b = h.level(lvl, w), dh.level(lvl, w)
+            for x, y in zip(a[2:], b[2:]):
+                assert np.array_equal(x, y), (lvl, w)
+    u1, r1 = h.cg_solve(p.rhs)
+    u2, r2 = dh.cg_solve(p.rhs)
+    assert r1["converged"] and r2["converged"]
+    assert abs(r1["iterations"] - r2["iterations"]) <= 1
+    assert np.linalg.norm(u1 - u2) <= 1e-9 * np.linalg.norm(u1)
