@@ -684,7 +684,7 @@ def run_dist_amg(args, rank, world, local, dist):
             t2 = time.perf_counter()
             u = torch.zeros(dp.n + 3, dtype=torch.float64, device=dev)
             rep = dh.cg_solve_device(dp.rhs_ptr, u.data_ptr(),
-                                     pb.CgParams(max_iterations=2) if it == 0 else None)
+                                     pb.CgParams(max_iterations=2 if it == 0 else 5000))
             torch.cuda.synchronize(dev)
             t3 = time.perf_counter()
             inf = dh.info()

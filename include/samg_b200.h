@@ -257,6 +257,11 @@ SAMG_API int samg_dist_set_send(samg_dist *d, int npeers, const int *peers,
         const int64_t *counts, const int64_t *global_ids);
 SAMG_API int samg_dist_send_plan(const samg_dist *d, int *peers,
         int64_t *counts, int64_t *offsets, int64_t *local_rows);
+/* Step 2 without the transport: the send plan derived from the rank's own
+ * rows -- for a structurally symmetric matrix, peer q reads exactly the
+ * owned rows that hold a column in q's range (the rule the distributed
+ * setup and solve use for every operator, dsolve.cu build_local_rows). */
+SAMG_API int samg_dist_derive_send(samg_dist *d);
 /* the renumbered local matrix (columns: owned [0,nloc), ghosts nloc+g) */
 SAMG_API int samg_dist_local_matrix(const samg_dist *d, int64_t *ptr,
         int64_t *col, double *val);

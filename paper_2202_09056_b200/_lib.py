@@ -134,6 +134,7 @@ PROTOTYPES = {
     "samg_dist_ghosts": ([vp, i64p], C.c_int),
     "samg_dist_set_send": ([vp, C.c_int, C.POINTER(C.c_int), i64p, i64p], C.c_int),
     "samg_dist_send_plan": ([vp, C.POINTER(C.c_int), i64p, i64p, i64p], C.c_int),
+    "samg_dist_derive_send": ([vp], C.c_int),
     "samg_dist_local_matrix": ([vp, i64p, i64p, f64p], C.c_int),
     "samg_dist_to_device": ([vp, C.c_int, C.c_int], C.c_int),
     "samg_dist_pack": ([vp, vp, vp, vp], C.c_int),

@@ -1150,6 +1150,13 @@ SAMG_API int samg_dist_set_send(samg_dist *d, int npeers, const int *peers, cons
     });
 }
 
+SAMG_API int samg_dist_derive_send(samg_dist *d) {
+    return guarded([&] {
+        require(d != nullptr, SAMG_INVALID_ARGUMENT, "NULL dist");
+        dist_derive_send(d);
+    });
+}
+
 SAMG_API int samg_dist_send_plan(const samg_dist *d, int *peers, int64_t *counts, int64_t *offsets,
                                  int64_t *local_rows) {
     return guarded([&] {

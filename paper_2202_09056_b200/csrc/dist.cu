@@ -136,6 +136,34 @@ void dist_set_send(samg_dist *d, int npeers, const int *peers, const int64_t *co
     d->send_set = true;
 }
 
+// Peer q reads our row i iff row i of q holds column i, i.e. (structural
+// symmetry) iff our row i holds a column in q's range: the owner derives
+// the plan from its own rows, ascending global ids per peer -- the order of
+// the receiver's sorted ghost segment.
+void dist_derive_send(samg_dist *d) {
+    std::vector<int> peers;
+    std::vector<int64_t> counts, ids;
+    const int64_t nl = d->nloc;
+    // columns are renumbered: ghosts nl + g -> global d->ghost[g]
+    for (int q = 0; q < d->nranks; ++q) {
+        if (q == d->rank) continue;
+        const int64_t lo = d->row_starts[q], hi = d->row_starts[q + 1];
+        int64_t c = 0;
+        for (int64_t i = 0; i < nl; ++i) {
+            bool hit = false;
+            for (int64_t j = d->ptr[i]; j < d->ptr[i + 1] && !hit; ++j) {
+                const int64_t lc = d->col[j];
+                if (lc < nl) continue;
+                const int64_t g = d->ghost[lc - nl];
+                hit = g >= lo && g < hi;
+            }
+            if (hit) { ids.push_back(d->row0 + i); ++c; }
+        }
+        if (c) { peers.push_back(q); counts.push_back(c); }
+    }
+    dist_set_send(d, static_cast<int>(peers.size()), peers.data(), counts.data(), ids.data());
+}
+
 void dist_to_device(samg_dist *d, int device, int group) {
     CK(cudaSetDevice(device));
     d->device = device;

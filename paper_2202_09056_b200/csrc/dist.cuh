@@ -29,6 +29,8 @@ samg_dist *dist_create(int64_t row0, int64_t row1, const int64_t *ptr, const int
                        const double *val, int nranks, const int64_t *row_starts, int rank);
 void dist_set_send(samg_dist *d, int npeers, const int *peers, const int64_t *counts,
                    const int64_t *ids);
+// the send plan from the rank's own rows (structurally symmetric matrix)
+void dist_derive_send(samg_dist *d);
 void dist_to_device(samg_dist *d, int device, int group);
 void dist_pack(const samg_dist *d, const double *x, double *buf, cudaStream_t s);
 void dist_spmv(const samg_dist *d, int part, double alpha, const double *xext, double beta,

@@ -75,6 +75,11 @@ class DistMatrix:
         check(lib.samg_dist_set_send(self.h, len(peers), arr, counts.ctypes.data_as(i64p),
                                      ids.ctypes.data_as(i64p)))
 
+    def derive_send(self):
+        """The send plan from the rank's own rows (structural symmetry; no
+        transport): samg_dist_derive_send."""
+        check(lib.samg_dist_derive_send(self.h))
+
     def send_plan(self):
         """(peers, counts, offsets, local block rows) of the send side."""
         n = self.info()["nsend"]

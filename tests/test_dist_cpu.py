@@ -65,7 +65,16 @@ def _worker(rank, world, port, outdir):
     np.testing.assert_array_equal(mine.val, full.val[full.ptr[r0]:full.ptr[r1]])
 
     dm = DistMatrix(mine.ptr, mine.col, mine.val.reshape(-1), starts, rank)
+    # the rule the distributed setup / solve use (dsolve.cu build_local_rows):
+    # the owner derives what each peer reads from its own rows ...
+    dm.derive_send()
+    derived = dm.send_plan()
+    # ... and it must equal what the peers' ghost lists say (gloo exchange)
     exchange_plan(dm, dist)
+    got = dm.send_plan()
+    assert derived[0] == got[0]
+    for a, b in zip(derived[1:], got[1:]):
+        np.testing.assert_array_equal(a, b)
     inf = dm.info()
     assert inf["nloc"] == r1 - r0
     assert inf["ninterior"] + inf["nboundary"] == inf["nloc"]

@@ -231,3 +231,42 @@ def test_distributed_setup_holds_slab_plus_halo(gpu, world):
     assert r1["converged"] and r2["converged"]
     assert abs(r1["iterations"] - r2["iterations"]) <= 1
     assert np.linalg.norm(u1 - u2) <= 1e-9 * np.linalg.norm(u1)
+
+
+@pytest.mark.parametrize("mode", ["device", "local"])
+def test_rank_local_input_single_rank(gpu, mode):
+    """samg_dsetup_device / samg_dsetup_local: the rank passes only its own
+    rows (here, one NCCL rank: all of them) -- from the on-GPU assembly or
+    from host arrays -- and the distributed setup + graph-captured PCG
+    reproduce the single-GPU hierarchy and solve."""
+    import torch
+
+    from paper_2202_09056_b200.dist import DistHierarchy
+    pb = gpu
+    kw = dict(nx=12, ny=6, nz=6, lx=2.0, dirichlet="eliminate", load="traction_xend", x_slowest=True)
+    host = pb.generate_hex(**kw)
+    prm = pb.AmgParams(coarse_enough=60)
+    h = pb.setup_bsr3(host.nbrows, host.ptr, host.col, host.val.reshape(-1), host.nullspace(),
+                      "ns_block", prm)
+    u1, r1 = h.cg_solve(host.rhs)
+    rs = np.array([0, host.nbrows], np.int64)
+    if mode == "device":
+        dp = pb.generate_hex_device(**kw)
+        dh = DistHierarchy(0, None, None, None, None, 0, 1, row_starts=rs, min_rows=1, prm=prm,
+                           device=(dp.A, dp.nullspace_ptr))
+    else:
+        dh = DistHierarchy(0, None, None, None, None, 0, 1, row_starts=rs, min_rows=1, prm=prm,
+                           local=(host.ptr, host.col, host.val.reshape(-1), host.nullspace()))
+    inf = dh.info()
+    assert inf["nlevels"] == h.nlevels and inf["dist_levels"] >= 1
+    for lvl in range(h.nlevels):
+        for w in ((0, 1, 2) if lvl + 1 < h.nlevels else (0,)):
+            a, b = h.level(lvl, w), dh.level(lvl, w)
+            for x, y in zip(a[2:], b[2:]):
+                assert np.array_equal(x, y), (lvl, w)
+    f = torch.from_numpy(host.rhs).cuda()
+    u = torch.zeros_like(f)
+    r2 = dh.cg_solve_device(f.data_ptr(), u.data_ptr())
+    assert r1["converged"] and r2["converged"]
+    assert abs(r1["iterations"] - r2["iterations"]) <= 1
+    assert np.linalg.norm(u1 - u.cpu().numpy()) <= 1e-9 * np.linalg.norm(u1)
