@@ -270,6 +270,22 @@ Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int6
         }
         mark("verify_galerkin", L - 1);
     }
+    // 6x6 node-blocked copies of the operators of levels >= 1 (pbs 6 nodes:
+    // rows and columns pair up) for the V-cycle's SpMVs.  Opt-in
+    // (SAMG_NODE6=1): measured slower than the 3x3 kernels on C1's levels 1
+    // and 2 (35.5 -> 39.9 us and 17.3 -> 28.5 us per residual; DESIGN 5.9)
+    if (!block && k == 6) {
+        static const bool node6 = [] {
+            const char *e = std::getenv("SAMG_NODE6");
+            return e && e[0] == '1';
+        }();
+        for (size_t i = (first_level > 0 ? 0 : 1); node6 && i + 1 < L; ++i) {
+            make_node6(H->levels[i].A, s);
+            make_node6(H->levels[i].P, s);
+            make_node6(H->levels[i].R, s);
+        }
+        mark("node6", L - 1);
+    }
     H->nc = 3 * H->levels.back().A.nrows;
     const bool inverse_ok = dense_inverse(H->levels.back().A, H->Ainv, err, s);
     mark("dense_inv", L - 1);
@@ -361,7 +377,7 @@ bool Hierarchy::vcycle(const double *f0, double *u0, bool zero_guess, bool fuse_
 // The V-cycle restricted to levels start..L-1 (f0, u0 live on level
 // `start`); the multi-GPU driver runs the replicated coarse levels this way.
 bool Hierarchy::vcycle_from(size_t start, const double *f0, double *u0, bool zero_guess,
-                            bool fuse_rz) {
+                            bool fuse_rz, bool presmoothed) {
     cudaStream_t s = stream;
     const size_t L = levels.size();
     const bool lowp = prm.vcycle_precision == SAMG_PRECISION_MIXED;
@@ -371,6 +387,9 @@ bool Hierarchy::vcycle_from(size_t start, const double *f0, double *u0, bool zer
     }
     bool fused = false;
     std::vector<double *> cur(L);
+    // pre: the first sweep from a zero guess of this level was fused into
+    // the kernel that produced its f (u = M f already in lv.u)
+    bool pre = presmoothed && zero_guess && prm.pre_sweeps > 0;
     for (size_t i = start; i + 1 < L; ++i) {
         Level &lv = levels[i];
         const double *fi = i == start ? f0 : lv.f.p;
@@ -380,7 +399,7 @@ bool Hierarchy::vcycle_from(size_t start, const double *f0, double *u0, bool zer
         if (!zero) CK(cudaMemcpyAsync(a, u0, sizeof(double) * 3 * lv.A.nrows, cudaMemcpyDeviceToDevice, s));
         if (zero) {
             if (sweeps > 0) {
-                launch_smooth_zero(lv.A.nrows, lv.M, fi, a, s);
+                if (!pre) launch_smooth_zero(lv.A.nrows, lv.M, fi, a, s);
                 --sweeps;
             } else {
                 launch_fill(3 * lv.A.nrows, 0.0, a, s);
@@ -391,7 +410,13 @@ bool Hierarchy::vcycle_from(size_t start, const double *f0, double *u0, bool zer
             std::swap(a, b);
         }
         launch_residual(lv.A, fi, a, lv.r.p, s, lowp);
-        launch_spmv(lv.R, 1.0, lv.r.p, 0.0, levels[i + 1].f.p, s, lowp);
+        // restriction, fused with the next level's first sweep from zero
+        // when that level has a block-diagonal smoother
+        Level &nx = levels[i + 1];
+        pre = false;
+        if (i + 2 < L && prm.pre_sweeps > 0)
+            pre = launch_restrict_smooth(lv.R, lv.r.p, nx.f.p, nx.M, nx.u.p, s, lowp);
+        if (!pre) launch_spmv(lv.R, 1.0, lv.r.p, 0.0, nx.f.p, s, lowp);
         cur[i] = a;
     }
     coarse_solve(levels[L - 1].f.p, levels[L - 1].u.p);
@@ -445,9 +470,15 @@ void Hierarchy::build_cg_graph() {
     cudaGraph_t body = np.conditional.phGraph_out[0];
     CK(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
     launch_spmv_dot(A0, p.p, q.p, partials.p, sc.p, s);
-    launch_cg_update(n, sc.p, p.p, q.p, ubuf.p, r.p, partials.p, CG_RR_LOOP, h, s);
-    if (!vcycle(r.p, z.p, true, true)) launch_dot(n, r.p, z.p, partials.p, sc.p, CG_RZ, s);
-    launch_p_update(n, sc.p, z.p, p.p, s);
+    // r -= alpha q, r.r and the loop condition, fused with the V-cycle's
+    // first level-0 sweep z0 = M r; u += alpha p is deferred to the p update
+    const bool fz = prm.pre_sweeps > 0 && levels.size() > 1 &&
+                    launch_cg_update_smooth(A0.nrows, sc.p, q.p, r.p, levels[0].M, levels[0].u.p,
+                                            partials.p, CG_RR_LOOP, h, s);
+    if (!fz) launch_cg_update(n, sc.p, p.p, q.p, ubuf.p, r.p, partials.p, CG_RR_LOOP, h, s);
+    if (!vcycle_from(0, r.p, z.p, true, true, fz)) launch_dot(n, r.p, z.p, partials.p, sc.p, CG_RZ, s);
+    if (fz) launch_p_update_u(n, sc.p, z.p, p.p, ubuf.p, s);
+    else launch_p_update(n, sc.p, z.p, p.p, s);
     cudaGraph_t captured = body;
     CK(cudaStreamEndCapture(s, &captured));
     CK(cudaGraphInstantiate(&cg_exec, g, 0));
@@ -515,17 +546,25 @@ samg_solve_report Hierarchy::cg(const double *d_f, double *d_u, const samg_cg_pa
         res_norm = std::sqrt(sc_host->rr);
     }
     while (!use_graph && res_norm / norm_f > cp.tol && iter < cp.max_iterations) {
+        // the same kernels as the graph body (build_cg_graph)
         launch_spmv_dot(A0, pp, pq, partials.p, sc.p, s);
-        launch_cg_update(n, sc.p, pp, pq, pu, pr, partials.p, CG_RR, 0, s);
+        const bool fz = prm.pre_sweeps > 0 && levels.size() > 1 &&
+                        launch_cg_update_smooth(A0.nrows, sc.p, pq, pr, levels[0].M, levels[0].u.p,
+                                                partials.p, CG_RR, 0, s);
+        if (!fz) launch_cg_update(n, sc.p, pp, pq, pu, pr, partials.p, CG_RR, 0, s);
         CK(cudaMemcpyAsync(sc_host, sc.p, sizeof(CgScalars), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         if (sc_host->breakdown)
             fail(SAMG_BREAKDOWN_NON_SPD, "cg: p'Ap <= 0, matrix or preconditioner not SPD");
         ++iter;
         res_norm = std::sqrt(sc_host->rr);
-        if (res_norm / norm_f <= cp.tol) break;
-        if (!vcycle(pr, pz, true, true)) launch_dot(n, pr, pz, partials.p, sc.p, CG_RZ, s);
-        launch_p_update(n, sc.p, pz, pp, s);
+        if (res_norm / norm_f <= cp.tol || iter >= cp.max_iterations) {
+            if (fz) launch_u_update(n, sc.p, pp, pu, s);  // the deferred u += alpha p
+            break;
+        }
+        if (!vcycle_from(0, pr, pz, true, true, fz)) launch_dot(n, pr, pz, partials.p, sc.p, CG_RZ, s);
+        if (fz) launch_p_update_u(n, sc.p, pz, pp, pu, s);
+        else launch_p_update(n, sc.p, pz, pp, s);
     }
     rep.iterations = iter;
     rep.converged = res_norm / norm_f <= cp.tol;

@@ -46,8 +46,10 @@ struct Hierarchy {
     uint64_t memory_footprint() const;
 
     bool vcycle(const double *f, double *u, bool zero_guess, bool fuse_rz = false);
+    // presmoothed: the first sweep of level `start` from a zero guess is
+    // already in levels[start].u (fused into the kernel that produced f)
     bool vcycle_from(size_t start, const double *f, double *u, bool zero_guess,
-                     bool fuse_rz = false);
+                     bool fuse_rz = false, bool presmoothed = false);
     samg_solve_report cg(const double *d_f, double *d_u, const samg_cg_params &prm);
 };
 

@@ -16,6 +16,13 @@ struct Bsr3 {
     DevBuf<int> ptr, col;
     DevBuf<double> val;
     DevBuf<float> val32;  // optional fp32 copy of val (mixed-precision V-cycle)
+    // optional node-blocked copy (make_node6): rows and columns paired into
+    // 6x6 blocks -- the operators of levels >= 1 of the ns pipelines, whose
+    // nodes are 2 block rows (pbs 6).  One column index and one 48-byte x
+    // gather per four 3x3 blocks; used by the V-cycle's SpMV family.
+    int64_t nrows6 = 0, nnzb6 = 0;
+    DevBuf<int> ptr6, col6;
+    DevBuf<double> val6;
     void alloc(int64_t nr, int64_t nc, int64_t nz, cudaStream_t s) {
         if (nz > INT32_MAX || nr > INT32_MAX || nc > INT32_MAX)
             fail(SAMG_UNSUPPORTED, "BSR3: more than 2^31-1 blocks per matrix");
@@ -82,6 +89,9 @@ void set_spmv_cta_cap(int ctas);
 void set_spmv_pdl(bool on);
 // fp32 copy of the values (A.val32) for the mixed-precision V-cycle
 void make_lowp(Bsr3 &A, cudaStream_t s);
+// 6x6 node-blocked copy (A.val6) if A's rows and columns pair up (returns
+// whether it did)
+bool make_node6(Bsr3 &A, cudaStream_t s);
 // u = M f  (one sweep from a zero guess: the residual is f exactly)
 // launch_smooth with the gathered x apart from the row-indexed u / f / M / out
 void launch_smooth_split(const Bsr3 &A, const Smoother &M, const double *f, const double *x,
@@ -119,7 +129,9 @@ void launch_cg_finish(CgScalars *sc, int what, cudaStream_t s);
 // after the allreduce of (tmp, tmp2) = (r.r, r.z): r.r -> `rr_what` (CG_RR,
 // or CG_RR_LOOP setting the graph's loop condition h), r.z -> CG_RZ
 void launch_cg_finish2(CgScalars *sc, int rr_what, cudaGraphConditionalHandle h, cudaStream_t s);
-constexpr int kRedBlocks = 592;   // 4 x 148 SMs: fixed => deterministic sums
+// CTAs of the vector kernels: 4 x 148 SMs (8 x 148 measured slower for the
+// fused CG update, 13.7 -> 17.4 us at C1); fixed => deterministic sums
+constexpr int kRedBlocks = 592;
 // q = A p fused with p.q (cg.hpp:63-64) -> PQ
 void launch_spmv_dot(const Bsr3 &A, const double *p, double *q, double *partials,
                      CgScalars *sc, cudaStream_t s, int what = CG_PQ);
@@ -137,6 +149,21 @@ void launch_cg_update(int64_t n, CgScalars *sc, const double *p, const double *q
 // p = z + beta p
 void launch_p_update(int64_t n, const CgScalars *sc, const double *z, double *p,
                      cudaStream_t s);
+// r -= alpha q with r.r -> what, and z0 = M r (the V-cycle's first level-0
+// sweep from zero); u's update is deferred to launch_p_update_u.  false
+// (nothing launched) for an ILU(0) smoother.
+bool launch_cg_update_smooth(int64_t nrows, CgScalars *sc, const double *q, double *r,
+                             const Smoother &M, double *z0, double *partials, int what,
+                             cudaGraphConditionalHandle h, cudaStream_t s);
+// u += alpha p_old; p = z + beta p_old
+void launch_p_update_u(int64_t n, const CgScalars *sc, const double *z, double *p, double *u,
+                       cudaStream_t s);
+// u += alpha p
+void launch_u_update(int64_t n, const CgScalars *sc, const double *p, double *u, cudaStream_t s);
+// f = R r fused with u = M f (next level's first sweep from zero); false
+// (nothing launched) for an ILU(0) smoother
+bool launch_restrict_smooth(const Bsr3 &R, const double *r, double *f, const Smoother &M, double *u,
+                            cudaStream_t s, bool lowp = false);
 void launch_fill(int64_t n, double v, double *x, cudaStream_t s);
 
 // ---- setup phase (setup.cu, compiled with --fmad=false) ----------------------

@@ -234,9 +234,23 @@ __device__ __forceinline__ double epilogue(const Epi &epi, int row, int lane, do
     return d;
 }
 
+// Bulk L2 prefetch (cp.async.bulk.prefetch, sm_90+) of `bytes` from p,
+// widened to 16-byte bounds: the TMA producer issues it for the rows of a
+// chunk it has just scheduled, so the epilogue's per-row vector loads hit L2.
+__device__ __forceinline__ void bulk_prefetch(const void *p, size_t bytes) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    const uintptr_t b = a & ~static_cast<uintptr_t>(15), e = (a + bytes + 15) & ~static_cast<uintptr_t>(15);
+    if (e > b)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(b), "r"(static_cast<unsigned>(e - b))
+                     : "memory");
+}
+
 struct EpiSpmv {
     double alpha, beta;
     double *y;
+    __device__ void prefetch(int r0, int n) const {
+        if (beta != 0.0) bulk_prefetch(y + 3 * static_cast<size_t>(r0), 24 * static_cast<size_t>(n));
+    }
     __device__ double operator()(int row, int c, double s0, double s1, double s2) const {
         double *yi = y + 3 * static_cast<size_t>(row) + c;
         const double s = pick3(c, s0, s1, s2);
@@ -248,6 +262,9 @@ struct EpiSpmv {
 struct EpiResidual {
     const double *f;
     double *r;
+    __device__ void prefetch(int r0, int n) const {
+        bulk_prefetch(f + 3 * static_cast<size_t>(r0), 24 * static_cast<size_t>(n));
+    }
     __device__ double operator()(int row, int c, double s0, double s1, double s2) const {
         const size_t i = 3 * static_cast<size_t>(row) + c;
         r[i] = f[i] - pick3(c, s0, s1, s2);
@@ -259,6 +276,12 @@ struct EpiResidual {
 struct EpiSmoothPoint {
     const double *f, *u, *m;
     double *out;
+    __device__ void prefetch(int r0, int n) const {
+        const size_t o = 3 * static_cast<size_t>(r0), b = 24 * static_cast<size_t>(n);
+        bulk_prefetch(f + o, b);
+        bulk_prefetch(u + o, b);
+        bulk_prefetch(m + o, b);
+    }
     __device__ double operator()(int row, int c, double s0, double s1, double s2) const {
         const size_t i = 3 * static_cast<size_t>(row) + c;
         const double fi = f[i];
@@ -272,6 +295,12 @@ struct EpiSmoothPoint {
 struct EpiSmoothBlock {
     const double *f, *u, *m;
     double *out;
+    __device__ void prefetch(int r0, int n) const {
+        const size_t o = 3 * static_cast<size_t>(r0), b = 24 * static_cast<size_t>(n);
+        bulk_prefetch(f + o, b);
+        bulk_prefetch(u + o, b);
+        bulk_prefetch(m + 3 * o, 3 * b);
+    }
     __device__ double operator()(int row, int c, double s0, double s1, double s2) const {
         const size_t b = 3 * static_cast<size_t>(row);
         const double r0 = f[b] - s0, r1 = f[b + 1] - s1, r2 = f[b + 2] - s2;
@@ -282,10 +311,38 @@ struct EpiSmoothBlock {
     }
 };
 
+// Restriction fused with the next level's first smoothing sweep from a zero
+// guess: f_c = (R r)_row, u_c = M_row f_c (hierarchy.hpp:429 then :426 /
+// relaxation.hpp:165-173 with u = 0: the residual is f_c exactly).
+// kBlock: 3x3 M_i; else point (3 per row).
+template <bool kBlock>
+struct EpiRestrictSmooth {
+    double *f, *u;
+    const double *m;
+    __device__ void prefetch(int r0, int n) const {
+        bulk_prefetch(m + (kBlock ? 9 : 3) * static_cast<size_t>(r0),
+                      (kBlock ? 72 : 24) * static_cast<size_t>(n));
+    }
+    __device__ double operator()(int row, int c, double s0, double s1, double s2) const {
+        const size_t b = 3 * static_cast<size_t>(row);
+        f[b + c] = pick3(c, s0, s1, s2);
+        if constexpr (kBlock) {
+            const double *M = m + 9 * static_cast<size_t>(row) + 3 * c;
+            u[b + c] = M[0] * s0 + M[1] * s1 + M[2] * s2;
+        } else {
+            u[b + c] = m[b + c] * pick3(c, s0, s1, s2);
+        }
+        return 0.0;
+    }
+};
+
 // q = A p; returns p*q (CG p'Ap)
 struct EpiDot {
     const double *p;
     double *q;
+    __device__ void prefetch(int r0, int n) const {
+        bulk_prefetch(p + 3 * static_cast<size_t>(r0), 24 * static_cast<size_t>(n));
+    }
     __device__ double operator()(int row, int c, double s0, double s1, double s2) const {
         const size_t i = 3 * static_cast<size_t>(row) + c;
         const double qi = pick3(c, s0, s1, s2);
@@ -318,6 +375,52 @@ __global__ void __launch_bounds__(256) k_bsr3_rows(int nlist, const int *__restr
     double s0, s1, s2;
     row_sums<G, 1, double>(row, valid, lane, ptr, col, val, x, s0, s1, s2);
     if (valid) epilogue<G>(epi, row, lane, s0, s1, s2);
+}
+
+// 6x6 node-blocked SpMV family (make_node6): a group of G lanes per node row
+// (2 block rows); a lane pair shares a 6x6 block -- lane 2m+h takes its
+// half-rows 3h..3h+2 (nine 16-byte loads, 144 B) and the whole 48-byte x
+// gather (three 16-byte loads) of blocks beg+m, beg+m+G/2, ...  The three
+// half-row sums are combined over the lanes of the same half, then lane h
+// runs the epilogue of block row 2 row + h.
+template <int G, class Epi>
+__global__ void __launch_bounds__(256) k_bsr6(int nrows6, const int *__restrict__ ptr,
+        const int *__restrict__ col, const double *__restrict__ val,
+        const double *__restrict__ x, Epi epi) {
+    static_assert(G >= 2 && G <= 32, "k_bsr6: 2..32 lanes per node row");
+    const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int row = gtid / G, lane = threadIdx.x % G;
+    const int half = lane & 1, m = lane >> 1;
+    const bool valid = row < nrows6;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    if (valid) {
+        const int beg = __ldg(ptr + row), end = __ldg(ptr + row + 1);
+#pragma unroll 2
+        for (int j = beg + m; j < end; j += G / 2) {
+            const int c = __ldg(col + j);
+            const double2 *bp =
+                reinterpret_cast<const double2 *>(val + 36 * static_cast<size_t>(j) + 18 * half);
+            double2 b[9];
+#pragma unroll
+            for (int k = 0; k < 9; ++k) b[k] = __ldg(bp + k);
+            const double2 *xp = reinterpret_cast<const double2 *>(x + 6 * static_cast<size_t>(c));
+            const double2 x01 = __ldg(xp), x23 = __ldg(xp + 1), x45 = __ldg(xp + 2);
+            a0 = fma(b[0].x, x01.x, a0); a0 = fma(b[0].y, x01.y, a0); a0 = fma(b[1].x, x23.x, a0);
+            a0 = fma(b[1].y, x23.y, a0); a0 = fma(b[2].x, x45.x, a0); a0 = fma(b[2].y, x45.y, a0);
+            a1 = fma(b[3].x, x01.x, a1); a1 = fma(b[3].y, x01.y, a1); a1 = fma(b[4].x, x23.x, a1);
+            a1 = fma(b[4].y, x23.y, a1); a1 = fma(b[5].x, x45.x, a1); a1 = fma(b[5].y, x45.y, a1);
+            a2 = fma(b[6].x, x01.x, a2); a2 = fma(b[6].y, x01.y, a2); a2 = fma(b[7].x, x23.x, a2);
+            a2 = fma(b[7].y, x23.y, a2); a2 = fma(b[8].x, x45.x, a2); a2 = fma(b[8].y, x45.y, a2);
+        }
+    }
+#pragma unroll
+    for (int off = G / 2; off >= 2; off >>= 1) {
+        a0 += __shfl_xor_sync(0xffffffffu, a0, off, G);
+        a1 += __shfl_xor_sync(0xffffffffu, a1, off, G);
+        a2 += __shfl_xor_sync(0xffffffffu, a2, off, G);
+    }
+    if (valid && m == 0)
+        for (int c = 0; c < 3; ++c) epi(2 * row + half, c, a0, a1, a2);
 }
 
 __device__ __forceinline__ double block_sum(double v) {
@@ -546,6 +649,9 @@ __global__ void __launch_bounds__(32 * (TW * NT + 1), 1) k_bsr3_tma(TmaCfg cfg, 
                                  static_cast<unsigned>(ce - cb), full + st);
                         bulk_g2s(sv + cfg.vcap + cfg.ccap, ptr + r0 - cfg.pmis,
                                  static_cast<unsigned>(pbytes), full + st);
+                        // the chunk's epilogue vectors towards L2 (after a
+                        // PDL wait only: they may be the previous kernel's output)
+                        if (!cfg.pdl) epi.prefetch(r0, min(RPC, cfg.nrows - r0));
                     } else {
                         mbar_arrive(full + st);
                     }
@@ -777,8 +883,33 @@ bool launch_tma(const Bsr3 &A, const VT *val, const double *x, Epi epi, double *
     return ok;
 }
 
+bool node6_enabled() { return true; }  // a matrix carries val6 only if setup built it
+
+template <class Epi>
+void launch_node6(const Bsr3 &A, const double *x, Epi epi, cudaStream_t s) {
+    const double bpr = static_cast<double>(A.nnzb6) / static_cast<double>(A.nrows6);
+    int G = 2;  // a lane pair per block, ~2 blocks per pair
+    while (G < 32 && G < bpr) G *= 2;
+    while (G < 32 && A.nrows6 * G < 148LL * 1024) G *= 2;
+    const int grid = ceil_div(A.nrows6 * static_cast<int64_t>(G), 256);
+    const int n = static_cast<int>(A.nrows6);
+    switch (G) {
+        case 2: k_bsr6<2, Epi><<<grid, 256, 0, s>>>(n, A.ptr6.p, A.col6.p, A.val6.p, x, epi); break;
+        case 4: k_bsr6<4, Epi><<<grid, 256, 0, s>>>(n, A.ptr6.p, A.col6.p, A.val6.p, x, epi); break;
+        case 8: k_bsr6<8, Epi><<<grid, 256, 0, s>>>(n, A.ptr6.p, A.col6.p, A.val6.p, x, epi); break;
+        case 16: k_bsr6<16, Epi><<<grid, 256, 0, s>>>(n, A.ptr6.p, A.col6.p, A.val6.p, x, epi); break;
+        default: k_bsr6<32, Epi><<<grid, 256, 0, s>>>(n, A.ptr6.p, A.col6.p, A.val6.p, x, epi); break;
+    }
+    CK_LAUNCH();
+}
+
 template <class VT, class Epi>
 void launch_rows_t(const Bsr3 &A, const VT *val, const double *x, Epi epi, cudaStream_t s) {
+    if (std::is_same_v<VT, double> && A.val6.p && node6_enabled() &&
+        reinterpret_cast<const void *>(val) == reinterpret_cast<const void *>(A.val.p)) {
+        launch_node6(A, x, epi, s);
+        return;
+    }
     if (spmv_variant() == 3 && launch_tma<false>(A, val, x, epi, nullptr, nullptr, 0, s)) return;
     const int G = choose_group(A);
     const int grid = ceil_div(A.nrows * static_cast<int64_t>(G), 256);
@@ -835,6 +966,43 @@ void launch_reduce(const Bsr3 &A, const double *x, Epi epi, double *partials, Cg
                    int what, cudaStream_t s, bool lowp = false) {
     if (lowp && A.val32.p) launch_reduce_t(A, static_cast<const float *>(A.val32.p), x, epi, partials, sc, what, s);
     else launch_reduce_t(A, static_cast<const double *>(A.val.p), x, epi, partials, sc, what, s);
+}
+
+// node row i of a pairable matrix: rows 2i, 2i+1 with equal column lists of
+// consecutive pairs (2j, 2j+1)
+__global__ void k_node6_check(int64_t nr6, const int *ptr, const int *col, int *bad, int *cnt) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= nr6) return;
+    const int a0 = ptr[2 * i], a1 = ptr[2 * i + 1], a2 = ptr[2 * i + 2];
+    const int n = a1 - a0;
+    bool ok = (n == a2 - a1) && !(n & 1);
+    for (int k = 0; ok && k < n; k += 2)
+        ok = col[a0 + k] == col[a1 + k] && col[a0 + k + 1] == col[a1 + k + 1] &&
+             !(col[a0 + k] & 1) && col[a0 + k + 1] == col[a0 + k] + 1;
+    if (!ok) atomicExch(bad, 1);
+    cnt[i] = n / 2;
+}
+
+__global__ void k_node6_fill(int64_t nr6, const int *ptr, const int *col, const double *val,
+                             int *ptr6, int *col6, double *val6) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i > nr6) return;
+    // block rows 0..2i-1 hold ptr[2i] 3x3 blocks = ptr[2i]/4 6x6 blocks
+    ptr6[i] = ptr[2 * i] / 4;
+    if (i == nr6) return;
+    const int a0 = ptr[2 * i], a1 = ptr[2 * i + 1];
+    const int n = a1 - a0;
+    const int o6 = ptr[2 * i] / 4;
+    for (int k = 0; k < n / 2; ++k) {
+        col6[o6 + k] = col[a0 + 2 * k] / 2;
+        double *d = val6 + 36 * static_cast<int64_t>(o6 + k);
+        for (int hr = 0; hr < 2; ++hr)
+            for (int hc = 0; hc < 2; ++hc) {
+                const double *b = val + 9 * static_cast<int64_t>((hr ? a1 : a0) + 2 * k + hc);
+                for (int r = 0; r < 3; ++r)
+                    for (int c = 0; c < 3; ++c) d[(3 * hr + r) * 6 + 3 * hc + c] = b[3 * r + c];
+            }
+    }
 }
 
 __global__ void k_to_f32(int64_t n, const double *__restrict__ a, float *__restrict__ b) {
@@ -968,6 +1136,101 @@ __global__ void k_p_update(int64_t n, const CgScalars *__restrict__ sc,
     if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) p[n - 1] = fma(b, p[n - 1], z[n - 1]);
 }
 
+// CG step with the u update deferred (to k_p_update_u) and the V-cycle's
+// first level-0 sweep fused (cg.hpp:68-71, then relaxation.hpp:165-173 from
+// u = 0): r -= alpha q; r.r; z0 = M r.  One thread per block row.
+template <bool kBlock>
+__global__ void __launch_bounds__(256) k_cg_update_smooth(int64_t nrows, CgScalars *sc,
+        const double *__restrict__ q, double *__restrict__ r, const double *__restrict__ m,
+        double *__restrict__ z0, double *__restrict__ partials, int what,
+        cudaGraphConditionalHandle h) {
+    const double a = sc->alpha;
+    double s = 0.0;
+    if constexpr (kBlock) {
+        // row pairs: 48 B of q and r and 144 B of M per pair, all 16-byte
+        // aligned -> fifteen 16-byte loads in flight per thread
+        const int64_t npair = nrows / 2;
+        for (int64_t pr = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; pr < npair;
+             pr += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+            const double2 *q2 = reinterpret_cast<const double2 *>(q + 6 * pr);
+            double2 *r2 = reinterpret_cast<double2 *>(r + 6 * pr);
+            const double2 *m2 = reinterpret_cast<const double2 *>(m + 18 * pr);
+            double2 qq[3], rr[3], mm[9];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) { qq[k] = q2[k]; rr[k] = r2[k]; }
+#pragma unroll
+            for (int k = 0; k < 9; ++k) mm[k] = __ldcs(m2 + k);
+            double v[6] = {fma(-a, qq[0].x, rr[0].x), fma(-a, qq[0].y, rr[0].y),
+                           fma(-a, qq[1].x, rr[1].x), fma(-a, qq[1].y, rr[1].y),
+                           fma(-a, qq[2].x, rr[2].x), fma(-a, qq[2].y, rr[2].y)};
+#pragma unroll
+            for (int k = 0; k < 3; ++k) r2[k] = make_double2(v[2 * k], v[2 * k + 1]);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) s = fma(v[k], v[k], s);
+            const double *M = reinterpret_cast<const double *>(mm);
+            double z[6];
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int i = 0; i < 3; ++i)
+                    z[3 * h + i] = M[9 * h + 3 * i] * v[3 * h] + M[9 * h + 3 * i + 1] * v[3 * h + 1] +
+                                   M[9 * h + 3 * i + 2] * v[3 * h + 2];
+            double2 *z2 = reinterpret_cast<double2 *>(z0 + 6 * pr);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) z2[k] = make_double2(z[2 * k], z[2 * k + 1]);
+        }
+    }
+    for (int64_t row = (kBlock ? 2 * (nrows / 2) : 0) + blockIdx.x * static_cast<int64_t>(blockDim.x) +
+                       threadIdx.x;
+         row < nrows; row += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const size_t b = 3 * static_cast<size_t>(row);
+        const double r0 = fma(-a, q[b], r[b]), r1 = fma(-a, q[b + 1], r[b + 1]),
+                     r2 = fma(-a, q[b + 2], r[b + 2]);
+        r[b] = r0; r[b + 1] = r1; r[b + 2] = r2;
+        s = fma(r0, r0, s); s = fma(r1, r1, s); s = fma(r2, r2, s);
+        if constexpr (kBlock) {
+            const double *M = m + 9 * static_cast<size_t>(row);
+            double Mv[9];
+#pragma unroll
+            for (int e = 0; e < 9; ++e) Mv[e] = __ldcs(M + e);
+            z0[b] = Mv[0] * r0 + Mv[1] * r1 + Mv[2] * r2;
+            z0[b + 1] = Mv[3] * r0 + Mv[4] * r1 + Mv[5] * r2;
+            z0[b + 2] = Mv[6] * r0 + Mv[7] * r1 + Mv[8] * r2;
+        } else {
+            z0[b] = m[b] * r0; z0[b + 1] = m[b + 1] * r1; z0[b + 2] = m[b + 2] * r2;
+        }
+    }
+    grid_finish(s, partials, sc, what, h);
+}
+
+// p_old -> u += alpha p_old (the deferred update), p = z + beta p_old
+__global__ void k_p_update_u(int64_t n, const CgScalars *__restrict__ sc,
+        const double *__restrict__ z, double *__restrict__ p, double *__restrict__ u) {
+    const double a = sc->alpha, b = sc->beta;
+    const int64_t n2 = n / 2;
+    const double2 *z2 = reinterpret_cast<const double2 *>(z);
+    double2 *p2 = reinterpret_cast<double2 *>(p), *u2 = reinterpret_cast<double2 *>(u);
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n2;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double2 zz = z2[i], pp = p2[i], uu = u2[i];
+        u2[i] = make_double2(fma(a, pp.x, uu.x), fma(a, pp.y, uu.y));
+        p2[i] = make_double2(fma(b, pp.x, zz.x), fma(b, pp.y, zz.y));
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        u[n - 1] = fma(a, p[n - 1], u[n - 1]);
+        p[n - 1] = fma(b, p[n - 1], z[n - 1]);
+    }
+}
+
+// u += alpha p (the deferred update of the last iteration, host loop)
+__global__ void k_u_update(int64_t n, const CgScalars *__restrict__ sc, const double *__restrict__ p,
+                           double *__restrict__ u) {
+    const double a = sc->alpha;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        u[i] = fma(a, p[i], u[i]);
+}
+
 __global__ void k_fill(int64_t n, double v, double *x) {
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -1072,6 +1335,32 @@ void launch_smooth_dot(const Bsr3 &A, const Smoother &M, const double *f, const 
         launch_reduce(A, u, EpiSmoothBlock{f, u, M.data.p, u_out}, partials, sc, what, s, lowp);
 }
 
+// 6x6 node-blocked copy: node rows i = block rows (2i, 2i+1) whose column
+// lists are equal and made of consecutive pairs (2j, 2j+1)
+bool make_node6(Bsr3 &A, cudaStream_t s) {
+    if (A.nrows < 2 || (A.nrows & 1) || (A.ncols & 1) || A.nnzb == 0 || (A.nnzb & 3)) return false;
+    const int64_t nr6 = A.nrows / 2;
+    DevBuf<int> bad(1, s), cnt(nr6 + 1, s);
+    CK(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
+    const int *ap = A.ptr.p, *ac = A.col.p;
+    int *bp = bad.p, *cp = cnt.p;
+    k_node6_check<<<ceil_div(nr6, 256), 256, 0, s>>>(nr6, ap, ac, bp, cp);
+    CK_LAUNCH();
+    int hb = 0;
+    CK(cudaMemcpyAsync(&hb, bad.p, sizeof hb, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (hb) return false;
+    A.nrows6 = nr6;
+    A.nnzb6 = A.nnzb / 4;
+    A.ptr6.alloc(nr6 + 1, s);
+    A.col6.alloc(A.nnzb6, s);
+    A.val6.alloc(36 * A.nnzb6, s);
+    k_node6_fill<<<ceil_div(nr6, 128), 128, 0, s>>>(nr6, ap, ac, A.val.p, A.ptr6.p, A.col6.p, A.val6.p);
+    CK_LAUNCH();
+    CK(cudaStreamSynchronize(s));
+    return true;
+}
+
 void make_lowp(Bsr3 &A, cudaStream_t s) {
     A.val32.alloc(9 * A.nnzb, s);
     if (A.nnzb) k_to_f32<<<vec_grid(9 * A.nnzb), 256, 0, s>>>(9 * A.nnzb, A.val.p, A.val32.p);
@@ -1096,6 +1385,40 @@ void launch_cg_update(int64_t n, CgScalars *sc, const double *p, const double *q
                       cudaStream_t s) {
     launch_k(false, k_cg_update, vec_grid(n / 2 + 1), 256, 0, s, n, sc, p, q, u, r, partials, what, h);
     CK_LAUNCH();
+}
+
+bool launch_cg_update_smooth(int64_t nrows, CgScalars *sc, const double *q, double *r,
+                             const Smoother &M, double *z0, double *partials, int what,
+                             cudaGraphConditionalHandle h, cudaStream_t s) {
+    if (M.kind != SM_POINT && M.kind != SM_BLOCK) return false;
+    const int grid = std::max(1, std::min<int>(kRedBlocks, ceil_div(nrows, 256)));
+    if (M.kind == SM_BLOCK)
+        launch_k(false, k_cg_update_smooth<true>, grid, 256, 0, s, nrows, sc, q, r,
+                 static_cast<const double *>(M.data.p), z0, partials, what, h);
+    else
+        launch_k(false, k_cg_update_smooth<false>, grid, 256, 0, s, nrows, sc, q, r,
+                 static_cast<const double *>(M.data.p), z0, partials, what, h);
+    CK_LAUNCH();
+    return true;
+}
+
+void launch_p_update_u(int64_t n, const CgScalars *sc, const double *z, double *p, double *u,
+                       cudaStream_t s) {
+    launch_k(false, k_p_update_u, vec_grid(n / 2 + 1), 256, 0, s, n, sc, z, p, u);
+    CK_LAUNCH();
+}
+
+void launch_u_update(int64_t n, const CgScalars *sc, const double *p, double *u, cudaStream_t s) {
+    launch_k(false, k_u_update, vec_grid(n), 256, 0, s, n, sc, p, u);
+    CK_LAUNCH();
+}
+
+bool launch_restrict_smooth(const Bsr3 &R, const double *r, double *f, const Smoother &M, double *u,
+                            cudaStream_t s, bool lowp) {
+    if (M.kind == SM_BLOCK) launch_rows(R, r, EpiRestrictSmooth<true>{f, u, M.data.p}, s, lowp);
+    else if (M.kind == SM_POINT) launch_rows(R, r, EpiRestrictSmooth<false>{f, u, M.data.p}, s, lowp);
+    else return false;
+    return true;
 }
 
 void launch_p_update(int64_t n, const CgScalars *sc, const double *z, double *p,

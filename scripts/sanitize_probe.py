@@ -30,3 +30,19 @@ print("device assembly", dp.nnzb, flush=True)
 dh = DistHierarchy(p.nbrows, p.ptr, p.col, p.val.reshape(-1), p.nullspace(), 0, 3,
                    min_rows=1, prm=pb.AmgParams(coarse_enough=300), emulate=True)
 print("emulated 3 ranks", dh.cg_solve(p.rhs)[1]["iterations"], flush=True)
+# round 2: 6x6 node-blocked level >= 1 operators, the fused CG kernels (graph),
+# verify_galerkin, the distributed setup (emulated), PDL back-to-back SpMVs
+r = pb.generate_hex(nx=12, ny=10, nz=10, dirichlet="eliminate", noise=0.01, seed=5)
+h3 = pb.setup(r.csr(), r.nullspace(), "ns_block",
+              pb.AmgParams(coarse_enough=150, verify_galerkin=True))
+print("levels", h3.nlevels, "cg", h3.cg_solve(r.rhs)[1]["iterations"], flush=True)
+dh2 = DistHierarchy(r.nbrows, r.ptr, r.col, r.val.reshape(-1), r.nullspace(), 0, 4,
+                    min_rows=1, prm=pb.AmgParams(coarse_enough=150), emulate=True)
+print("distributed setup 4 ranks", dh2.info(), dh2.cg_solve(r.rhs)[1]["iterations"], flush=True)
+import torch  # noqa: E402
+xd = torch.ones(q.n, dtype=torch.float64, device="cuda")
+yd = torch.zeros(q.n, dtype=torch.float64, device="cuda")
+for _ in range(3):
+    M.spmv_device(xd.data_ptr(), yd.data_ptr())
+torch.cuda.synchronize()
+print("pdl spmv", float(yd.sum()), flush=True)

@@ -59,6 +59,11 @@ CONFIGS = {
                 load="traction_xend", x_slowest=True), "spai0", 0.72, 5000),
     "C3i": (dict(nx=511, ny=63, nz=63, lx=511 / 63, dirichlet="eliminate",
                  load="traction_xend", x_slowest=True), "ilu0", 0.72, 1000),
+    # 23.88 M unknowns: the reference setup needs ~130 GB and ~6 min, its
+    # solve ~1.5 h single-threaded -> hierarchy only (--no-solve), run on
+    # the GPU box's host (196 GB)
+    "C4": (dict(nx=199, ny=199, nz=199, dirichlet="eliminate", noise=0.01, seed=2022),
+           "spai0", 0.72, 1000),
 }
 
 
@@ -83,6 +88,7 @@ def main():
     ap.add_argument("--smoother", default=None)
     ap.add_argument("--omega", type=float, default=None)
     ap.add_argument("--no-solve", action="store_true")
+    ap.add_argument("--outdir", default=HERE)
     ap.add_argument("--maxit", type=int, default=None,
                     help="CG iteration cap (C2: a fixed-iteration comparison)")
     args = ap.parse_args()
@@ -128,11 +134,11 @@ def main():
                    converged=rep["converged"], solve_s=rep["solve_seconds"],
                    u_norm=float(np.linalg.norm(u)), u_sha=sha(u, np.float64),
                    u_stride=stride_for(n))
-        np.save(os.path.join(HERE, name + "_u.npy"), u[::stride_for(n)])
+        np.save(os.path.join(args.outdir, name + "_u.npy"), u[::stride_for(n)])
         print(f"[{args.config}] solve {rep}", flush=True)
     rec["max_rss_gb"] = resource.getrusage(resource.RUSAGE_SELF).ru_maxrss / 2**20
     rec["host"] = os.uname().nodename
-    with open(os.path.join(HERE, name + ".json"), "w") as f:
+    with open(os.path.join(args.outdir, name + ".json"), "w") as f:
         json.dump(rec, f, indent=1)
     print(json.dumps({k: v for k, v in rec.items() if k != "levels"}), flush=True)
 

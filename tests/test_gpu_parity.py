@@ -306,6 +306,49 @@ def test_second_device_after_first(gpu):
     assert np.linalg.norm(res[0] - res[1]) <= 1e-12 * np.linalg.norm(res[0])
 
 
+NODE6_CHILD = r"""
+import sys
+sys.path.insert(0, %r)
+import numpy as np
+import paper_2202_09056_b200 as pb
+from oracle.oracle import Ref
+ref = Ref()
+p = pb.generate_hex(nx=16, ny=10, nz=10, dirichlet="eliminate", noise=0.01, seed=4)
+h = pb.setup_bsr3(p.nbrows, p.ptr, p.col, p.val.reshape(-1), p.nullspace(), "ns_block",
+                  pb.AmgParams(coarse_enough=150))
+assert h.nlevels >= 3
+rng = np.random.default_rng(21)
+for lvl in range(1, h.nlevels - 1):
+    for w in (0, 1, 2):
+        nr, nc, ptr, col, val = h.level(lvl, w)
+        M = h.level_matrix(lvl, w)
+        x = rng.uniform(-1, 1, 3 * nc)
+        y0 = rng.uniform(-1, 1, 3 * nr)
+        for alpha, beta in ((1.0, 0.0), (-0.5, 2.0)):
+            yg = M.spmv(x, alpha, beta, y0)
+            yr = ref.spmv_bsr3(nr, nc, ptr, col, val.reshape(-1), x, alpha, beta, y0)
+            assert np.abs(yg - yr).max() <= 1e-13 * np.abs(yr).max(), (lvl, w)
+u, rep = h.cg_solve(p.rhs)
+assert rep["converged"], rep
+print("node6 ok", rep["iterations"])
+"""
+
+
+def test_node6_spmv_matches_reference(gpu, ref):
+    """Levels >= 1 of the ns pipelines can carry a 6x6 node-blocked copy of
+    A, P and R (make_node6, opt-in SAMG_NODE6=1, read once per process --
+    hence a child process) that the V-cycle's SpMV family then reads: the
+    products must equal the reference's spmv<static_block<3>> on the 3x3
+    matrices, and CG must converge."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", NODE6_CHILD % root], capture_output=True, text=True,
+                         env={**os.environ, "SAMG_NODE6": "1"}, timeout=600)
+    assert out.returncode == 0 and "node6 ok" in out.stdout, out.stderr[-2000:]
+
+
 def test_spmv_matches_reference(gpu, ref):
     pb = gpu
     p = make_problem(pb, 19, dirichlet="eliminate")
