@@ -52,10 +52,15 @@ enum samg_status {
 
 /* samg::pipeline (hierarchy.hpp:30).  SAMG_PIPELINE_NS_BLOCK is the B200
  * hot path; NS_HYBRID2 and NS_HYBRID1 (scalar-space Galerkin, block storage,
- * hierarchy.hpp:233-330; NS_HYBRID1 without ILU(0), whose scalar smoother
- * is not on this path) are supported with the same bit-exact parity, and so
- * is BLOCK (no nullspace: B may be NULL and is ignored, hierarchy.hpp:340-347);
- * SCALAR and NS_SCALAR return SAMG_UNSUPPORTED. */
+ * hierarchy.hpp:233-330) are supported with the same bit-exact parity, and
+ * so is BLOCK (no nullspace: B may be NULL and is ignored,
+ * hierarchy.hpp:340-347).  SCALAR (no nullspace: aggregate indicator with
+ * 3-unknown points, B ignored) and NS_SCALAR (hierarchy.hpp:298-330) keep
+ * scalar CSR levels in the reference: here the same values as 3x3 blocks
+ * (their patterns are whole blocks for matrices with full 3x3 blocks),
+ * memory_footprint in the reference's scalar accounting, damped Jacobi
+ * only.  ilu0<double> (the scalar pipelines' and NS_HYBRID1's scalar ILU)
+ * returns SAMG_UNSUPPORTED; so do the scalar pipelines on several GPUs. */
 enum samg_pipeline {
     SAMG_PIPELINE_SCALAR = 0,
     SAMG_PIPELINE_BLOCK = 1,

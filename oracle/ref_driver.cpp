@@ -14,6 +14,7 @@
 // The 3x3 block smoothers the reference lacks (SPAI0, block Jacobi) use a
 // harness V-cycle that follows hierarchy.hpp:408-441 line by line and the
 // reference's generic cg_solve_op (cg.hpp:39-83).
+#include <array>
 #include <chrono>
 #include <cstdint>
 #include <cstdlib>
@@ -74,6 +75,9 @@ struct ref_handle {
     std::vector<samg::index> agg_count;
     std::vector<std::vector<double>> sm;  // block smoother data per level
     double setup_seconds = 0;
+    // scalar pipelines: the level matrices as 3x3 blocks (to_block<3>, for
+    // the parity taps; the hierarchy itself keeps them scalar)
+    std::vector<std::array<csr<block3>, 3>> blockview;
 };
 
 using clk = std::chrono::steady_clock;
@@ -208,15 +212,27 @@ static void setup_impl(scalar_csr &&A, const double *B, int64_t bcols, double ep
     h->smoother = smoother;
     h->smoother_omega = smoother_omega;
     auto t0 = clk::now();
-    // samg::pipeline numbering (hierarchy.hpp:30): 3 ns_hybrid1, 4 ns_hybrid2, 5 ns_block
-    const pipeline pl = pipeline_id == 1 ? pipeline::block
+    // samg::pipeline numbering (hierarchy.hpp:30): 0 scalar, 1 block,
+    // 2 ns_scalar, 3 ns_hybrid1, 4 ns_hybrid2, 5 ns_block
+    const pipeline pl = pipeline_id == 0 ? pipeline::scalar
+                      : pipeline_id == 1 ? pipeline::block
+                      : pipeline_id == 2 ? pipeline::ns_scalar
                       : pipeline_id == 3 ? pipeline::ns_hybrid1
                       : pipeline_id == 4 ? pipeline::ns_hybrid2 : pipeline::ns_block;
+    const bool scalar_levels = pl == pipeline::scalar || pl == pipeline::ns_scalar;
     h->H = setup(A, Bd, pl, prm);
     const samg::index L = h->H.nlevels();
     // Smoother override through the public level members.
     h->sm.resize(L);
     for (samg::index l = 0; l + 1 < L; ++l) {
+        if (scalar_levels) {  // the reference's scalar smoothers only
+            if (smoother == SM_JACOBI && smoother_omega != damped_jacobi::default_damping)
+                h->H.levels[l].smoother =
+                    damped_jacobi(std::get<scalar_csr>(h->H.levels[l].A), smoother_omega);
+            else if (smoother != SM_JACOBI && smoother != SM_ILU0)
+                throw error("scalar pipelines: block smoothers are not defined");
+            continue;
+        }
         const csr<block3> &Al = blk(h->H.levels[l].A);
         if (smoother == SM_JACOBI && smoother_omega != damped_jacobi::default_damping) {
             h->H.levels[l].smoother = damped_jacobi(Al, smoother_omega);
@@ -250,6 +266,9 @@ static void setup_impl(scalar_csr &&A, const double *B, int64_t bcols, double ep
         adjacency G;
         if (pl == pipeline::block) {  // block_transfer_operators, coarsening.hpp:471
             G = strength_graph(blk(h->H.levels[l].A), eps_strong, 1);
+        } else if (scalar_levels) {  // scalar_setup (hierarchy.hpp:234-259)
+            const int pbs = (l == 0 || pl == pipeline::scalar) ? 3 : static_cast<int>(bcols);
+            G = strength_graph(std::get<scalar_csr>(h->H.levels[l].A), eps_strong, pbs);
         } else {
             scalar_csr S = to_scalar(blk(h->H.levels[l].A));
             const int pbs = l == 0 ? 3 : static_cast<int>(bcols);
@@ -258,6 +277,17 @@ static void setup_impl(scalar_csr &&A, const double *B, int64_t bcols, double ep
         aggregates a = aggregate(G);
         h->agg[l] = a.id;
         h->agg_count[l] = a.count;
+    }
+    if (scalar_levels) {
+        h->blockview.resize(L);
+        for (samg::index l = 0; l < L; ++l) {
+            const samg::level &lv = h->H.levels[l];
+            h->blockview[l][0] = to_block<3>(std::get<scalar_csr>(lv.A));
+            if (lv.has_transfer) {
+                h->blockview[l][1] = to_block<3>(std::get<scalar_csr>(lv.P));
+                h->blockview[l][2] = to_block<3>(std::get<scalar_csr>(lv.R));
+            }
+        }
     }
     *out = h.release();
 }
@@ -324,7 +354,8 @@ int ref_level_matrix(void *hp, int level, int which, int64_t *nrows,
     if (level < 0 || level >= h->H.nlevels()) return 1;
     const samg::level &lv = h->H.levels[level];
     if (which != 0 && !lv.has_transfer) return 1;
-    const csr<block3> &M = blk(which == 0 ? lv.A : which == 1 ? lv.P : lv.R);
+    const csr<block3> &M = h->blockview.empty() ? blk(which == 0 ? lv.A : which == 1 ? lv.P : lv.R)
+                                                : h->blockview[level][which];
     *nrows = M.nrows;
     *ncols = M.ncols;
     *ptr = M.ptr.data();

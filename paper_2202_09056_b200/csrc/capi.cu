@@ -142,11 +142,19 @@ void validate_params(const samg_amg_params *prm, int pipeline) {
     // arithmetic (scalar order, hierarchy.hpp:233-260) and, for ns_hybrid1,
     // in scalar smoothers (ilu0<double> is not on the B200 path)
     // block: no nullspace, block strength / transfer (hierarchy.hpp:340-347)
-    if (pipeline != SAMG_PIPELINE_NS_BLOCK && pipeline != SAMG_PIPELINE_NS_HYBRID2 &&
-        pipeline != SAMG_PIPELINE_NS_HYBRID1 && pipeline != SAMG_PIPELINE_BLOCK)
-        fail(SAMG_UNSUPPORTED, "setup: pipelines scalar and ns_scalar are not on the B200 path");
-    if (pipeline == SAMG_PIPELINE_NS_HYBRID1 && prm && prm->smoother == SAMG_SMOOTHER_ILU0)
-        fail(SAMG_UNSUPPORTED, "setup: ns_hybrid1 with scalar ILU(0) is not on the B200 path");
+    // scalar / ns_scalar (hierarchy.hpp:298-330): the scalar-space setup with
+    // scalar level matrices -- the same values as 3x3 blocks on the B200
+    // (their patterns are whole blocks), reported in scalar CSR accounting
+    require(pipeline >= SAMG_PIPELINE_SCALAR && pipeline <= SAMG_PIPELINE_NS_BLOCK,
+            SAMG_INVALID_ARGUMENT, "setup: unknown pipeline");
+    const bool scalar_smoother = pipeline == SAMG_PIPELINE_NS_HYBRID1 ||
+                                 pipeline == SAMG_PIPELINE_SCALAR || pipeline == SAMG_PIPELINE_NS_SCALAR;
+    if (scalar_smoother && prm && prm->smoother == SAMG_SMOOTHER_ILU0)
+        fail(SAMG_UNSUPPORTED, "setup: scalar ILU(0) (ilu0<double>) is not on the B200 path");
+    if ((pipeline == SAMG_PIPELINE_SCALAR || pipeline == SAMG_PIPELINE_NS_SCALAR) && prm &&
+        prm->smoother != SAMG_SMOOTHER_JACOBI)
+        fail(SAMG_UNSUPPORTED, "setup: the scalar pipelines take the reference's scalar smoothers "
+                               "(damped Jacobi)");
     require(prm->smoother >= 0 && prm->smoother <= 3, SAMG_INVALID_ARGUMENT, "setup: unknown smoother");
     require(prm->pre_sweeps >= 0 && prm->post_sweeps >= 0, SAMG_INVALID_ARGUMENT,
             "setup: negative sweep count");
@@ -157,7 +165,7 @@ void validate_params(const samg_amg_params *prm, int pipeline) {
 // hierarchy.hpp:267-282 + coarsening.hpp:269-270 checks
 void validate_ns(int64_t n, const double *B, int64_t b_rows, int64_t b_cols, int pipeline) {
     require(n >= 0, SAMG_INVALID_ARGUMENT, "setup: negative dimension");
-    if (pipeline == SAMG_PIPELINE_BLOCK) {  // the block pipeline ignores B
+    if (pipeline == SAMG_PIPELINE_BLOCK || pipeline == SAMG_PIPELINE_SCALAR) {  // no nullspace: B ignored
         if (n % 3) fail(SAMG_NOT_DIVISIBLE, "setup: block pipelines require dimension divisible by 3");
         return;
     }

@@ -675,6 +675,7 @@ PanelPlan plan_panel(int64_t n) {
 } // namespace
 
 bool dense_inverse(const Bsr3 &A, DevBuf<double> &Ainv, DevError *err, cudaStream_t s) {
+    NvtxScope nvtx_scope("samg::dense_lu (Gauss-Jordan inverse)");
     const int64_t n = 3 * A.nrows;
     const int64_t ld = dense_ld(n);
     Ainv.alloc(n * ld, s);

@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <atomic>
 #include <climits>
@@ -108,5 +109,14 @@ struct DeviceCache {
 
 // SM count of the current device (cached per device).
 int sm_count();
+
+// NVTX range for the lifetime of the object (setup phases, solves): shows
+// in Nsight Systems / ncu --nvtx; header-only NVTX v3, no-op without a tool.
+struct NvtxScope {
+    explicit NvtxScope(const char *name) { nvtxRangePushA(name); }
+    ~NvtxScope() { nvtxRangePop(); }
+    NvtxScope(const NvtxScope &) = delete;
+    NvtxScope &operator=(const NvtxScope &) = delete;
+};
 
 } // namespace samgb

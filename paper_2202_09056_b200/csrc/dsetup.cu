@@ -560,6 +560,7 @@ void gather_matrix(const Xport &x, const std::vector<const Bsr3 *> &own,
 DSetup dist_setup(const Xport &x, std::vector<Bsr3> &&A_own, std::vector<DevBuf<double>> &&B_own,
                   int64_t b_cols, const std::vector<int64_t> &row_starts, int64_t min_rows,
                   const samg_amg_params &prm, int pipeline, double t_start) {
+    NvtxScope nvtx_scope("samg::dsetup (distributed)");
     cudaStream_t s = x.s;
     const int nr = x.nranks;
     const size_t nd = x.mine.size();

@@ -623,6 +623,7 @@ void DHierarchy::vcycle() {
 // (all-reduced, identical on every rank) scalars once per iteration.  d_f /
 // d_u are the rank's slices, or the global vectors of an emulated group.
 samg_solve_report DHierarchy::cg(const double *d_f, double *d_u, const samg_cg_params &cp) {
+    NvtxScope nvtx_scope("samg::dcg_solve (distributed)");
     cudaStream_t s = stream();
     const auto t0 = std::chrono::steady_clock::now();
     samg_solve_report rep{};
@@ -808,6 +809,8 @@ DHierarchy *dsetup_all(const unsigned char *id, int nranks, int rank, int64_t nb
     if (!id && nranks > kMaxEmulated) fail(SAMG_INVALID_ARGUMENT, "dsetup: at most 16 emulated ranks");
     if (prm.smoother == SAMG_SMOOTHER_ILU0)
         fail(SAMG_UNSUPPORTED, "multi-GPU solve: the ILU(0) sweeps are sequential across row partitions");
+    if (pipeline == SAMG_PIPELINE_SCALAR || pipeline == SAMG_PIPELINE_NS_SCALAR)
+        fail(SAMG_UNSUPPORTED, "multi-GPU solve: the scalar pipelines are single-GPU");
     std::vector<int64_t> st(nranks + 1);
     if (row_starts) {
         st.assign(row_starts, row_starts + nranks + 1);

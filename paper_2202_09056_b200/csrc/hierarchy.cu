@@ -58,13 +58,22 @@ Hierarchy::~Hierarchy() {
 }
 
 uint64_t Hierarchy::memory_footprint() const {
-    // memory_footprint (hierarchy.hpp:443-458)
+    // memory_footprint (hierarchy.hpp:443-458).  The scalar pipelines keep
+    // scalar CSR level matrices in the reference (hierarchy.hpp:309-327):
+    // their bytes are counted as such -- 9 scalar entries (8-byte index +
+    // 8-byte value) per stored 3x3 block, 3 row pointers per block row --
+    // although the B200 stores the same values as 3x3 blocks.
+    const bool scalar = pipeline == SAMG_PIPELINE_SCALAR || pipeline == SAMG_PIPELINE_NS_SCALAR;
+    auto mbytes = [&](const Bsr3 &M) {
+        return scalar ? static_cast<uint64_t>(3 * M.nrows + 1) * 8 + static_cast<uint64_t>(M.nnzb) * 9 * 16
+                      : matrix_bytes(M);
+    };
     uint64_t bytes = 0;
     for (const Level &lv : levels) {
-        bytes += matrix_bytes(lv.A);
+        bytes += mbytes(lv.A);
         if (lv.has_transfer) {
-            bytes += matrix_bytes(lv.P);
-            bytes += matrix_bytes(lv.R);
+            bytes += mbytes(lv.P);
+            bytes += mbytes(lv.R);
         }
         if (lv.M.kind == SM_ILU)  // ilu0::bytes (relaxation.hpp:93-95)
             bytes += static_cast<uint64_t>(lv.M.nrows + 1) * 8 + static_cast<uint64_t>(lv.M.nnzb) * 80 +
@@ -79,14 +88,21 @@ uint64_t Hierarchy::memory_footprint() const {
 Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int64_t b_cols,
                            const samg_amg_params &prm, cudaStream_t s, double t_start, int pipeline,
                            GalerkinSlicer *slicer, int first_level) {
+    NvtxScope nvtx_scope("samg::setup");
     auto H = std::make_unique<Hierarchy>();
     H->stream = s;
     H->prm = prm;
     H->pipeline = pipeline;
     // the hybrids run the scalar-space setup (hierarchy.hpp:233-260): the
     // same transfer operators, the Galerkin product in scalar arithmetic
+    // (and so do the scalar pipelines, hierarchy.hpp:298-330, whose level
+    // matrices are the same values in scalar CSR)
     const bool scalar_galerkin =
-        pipeline == SAMG_PIPELINE_NS_HYBRID1 || pipeline == SAMG_PIPELINE_NS_HYBRID2;
+        pipeline == SAMG_PIPELINE_NS_HYBRID1 || pipeline == SAMG_PIPELINE_NS_HYBRID2 ||
+        pipeline == SAMG_PIPELINE_SCALAR || pipeline == SAMG_PIPELINE_NS_SCALAR;
+    // `scalar`: no nullspace; the indicator tentative operator with point
+    // block size 3 on every level (hierarchy.hpp:284-285, coarsening.hpp:249-266)
+    const bool indicator = pipeline == SAMG_PIPELINE_SCALAR;
     CK(cudaGetDevice(&H->device));
     H->err.alloc(1, s);
     CK(cudaMemsetAsync(H->err.p, 0, sizeof(DevError), s));
@@ -141,9 +157,9 @@ Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int6
         mark("pool", 0);
     }
     const bool block = pipeline == SAMG_PIPELINE_BLOCK;  // no nullspace
-    const int k = block ? 0 : static_cast<int>(b_cols);
+    const int k = block ? 0 : (indicator ? 3 : static_cast<int>(b_cols));
     DevBuf<double> B;
-    if (!block) {
+    if (!block && !indicator) {
         B.alloc(b_rows * b_cols, s);
         // B may be host (pageable/pinned) or device memory (samg_setup_device)
         CK(cudaMemcpyAsync(B.p, B_host, sizeof(double) * b_rows * b_cols, cudaMemcpyDefault, s));
@@ -192,7 +208,7 @@ Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int6
         }
         // ns pipelines force point_block_size = 3 on the fine level
         // (hierarchy.hpp:284-285), then use the nullspace width (:351-353)
-        const int pbs = (H->levels.size() == 1 && first_level == 0) ? 3 : k;
+        const int pbs = (H->levels.size() == 1 && first_level == 0) || indicator ? 3 : k;
         if (pbs % 3) fail(SAMG_NOT_DIVISIBLE, "ns_block: node size must be a multiple of 3");
         const int h = pbs / 3;
         if (Li.A.nrows % h)
@@ -205,10 +221,11 @@ Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int6
         const int64_t naggs = aggregate(G, agg, s, &seedno);
         mark("aggregate", lvl);
         DevBuf<double> Pt, Bc;
-        tentative(agg, G.nnodes, naggs, pbs, B.p, k, Pt, Bc, err, s);
+        if (indicator) tentative_indicator(agg, G.nnodes, naggs, pbs, Pt, s);
+        else tentative(agg, G.nnodes, naggs, pbs, B.p, k, Pt, Bc, err, s);
         mark("tentative", lvl);
         Bsr3 P;
-        smooth_prolongation(Li.A, G, agg, naggs, pbs, k, Pt.p, prm.omega, P, err, s);
+        smooth_prolongation(Li.A, G, agg, naggs, pbs, indicator ? 0 : k, Pt.p, prm.omega, P, err, s);
         check_dev_error(err, s);
         mark("smooth_P", lvl);
         // stagnation guard (hierarchy.hpp:355)
@@ -491,6 +508,7 @@ void Hierarchy::build_cg_graph() {
 // (no host round trip per iteration); SAMG_CG_GRAPH=0 selects the host loop
 // that reads ||r|| back every iteration.
 samg_solve_report Hierarchy::cg(const double *d_f, double *d_u, const samg_cg_params &cp) {
+    NvtxScope nvtx_scope("samg::cg_solve");
     static const bool use_graph = [] {
         const char *e = std::getenv("SAMG_CG_GRAPH");
         return !(e && e[0] == '0');

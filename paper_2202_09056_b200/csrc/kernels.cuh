@@ -192,8 +192,14 @@ void tentative(const DevBuf<int> &agg, int64_t nnodes, int64_t naggs, int pbs, c
                int64_t a0 = 0, int64_t a1 = -1);
 // smoothed prolongation in scalar semantics, emitted as BSR3
 // (coarsening.hpp:319-416 + to_block<3>)
+// the `scalar` pipeline's tentative operator (no nullspace): the unit
+// aggregate indicator per point-block component, one value per scalar row
+// (coarsening.hpp:249-266); smooth it with k = 0
+void tentative_indicator(const DevBuf<int> &agg, int64_t nnodes, int64_t naggs, int pbs,
+                         DevBuf<double> &Pt1, cudaStream_t s);
 // [node0, node1): only these nodes' rows of P (local row numbering; A in
-// global numbering holding at least their rows)
+// global numbering holding at least their rows).  k == 0: Pt is the
+// indicator of tentative_indicator (pbs 3)
 void smooth_prolongation(const Bsr3 &A, const Graph &G, const DevBuf<int> &agg, int64_t naggs,
                          int pbs, int k, const double *Pt, double omega, Bsr3 &P, DevError *err,
                          cudaStream_t s, int64_t node0 = 0, int64_t node1 = -1);

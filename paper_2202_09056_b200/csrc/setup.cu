@@ -575,6 +575,65 @@ __global__ void k_psm_vals(int64_t nsc, int pbs, int h, int k, const int *ptr, c
     }
 }
 
+// The `scalar` pipeline's tentative operator has no nullspace: the unit
+// aggregate indicator expanded per point-block component
+// (coarsening.hpp:249-266), one entry per scalar row -- P_tent(i, agg(i)*3 +
+// i%3) = 1/sqrt(|aggregate|), Pt1[i] holds it.  The smoothing then follows
+// coarsening.hpp:387-414 with a first touch per column: scalar column sc of
+// A's row contributes only to column comp(sc) of the aggregate group.
+__global__ void k_tent_indicator(int64_t nnodes, int pbs, const int *agg, const int *cnt,
+                                 double *Pt1) {
+    const int64_t n = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (n >= nnodes) return;
+    const double v = __ddiv_rn(1.0, __dsqrt_rn(static_cast<double>(cnt[agg[n]])));
+    for (int c = 0; c < pbs; ++c) Pt1[n * pbs + c] = v;
+}
+
+__global__ void k_psm_vals_ind(int64_t nsc, int pbs, int h, const int *ptr, const int *col,
+                               const double *val, const int *gp, const int *gc, const int *agg,
+                               const int *toff, const int *tlist, const int *tcnt,
+                               const double *dinv, const double *diag, const double *Pt1,
+                               double omega, const int *pptr, double *pval, int64_t off) {
+    const int64_t li = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (li >= nsc) return;
+    const int64_t i = li + off;
+    const int br = static_cast<int>(i / 3), rr = static_cast<int>(i % 3);
+    const int node = static_cast<int>(i / pbs);
+    const int lnode = static_cast<int>(li / pbs), lbr = static_cast<int>(li / 3);
+    const int *L = tlist + toff[lnode];
+    const int nt = tcnt[lnode];
+    const double di = dinv[li], dg = diag[li];
+    const double nom = -omega;
+    for (int t = 0; t < nt; ++t) {
+        const int g = L[t];
+        double acc[3] = {0.0, 0.0, 0.0};
+        bool touched[3] = {false, false, false};
+        if (agg[node] == g) {  // P_tent's own entry first
+            const int c = static_cast<int>(i % pbs);
+            acc[c] = Pt1[i];
+            touched[c] = true;
+        }
+        for (int j = ptr[br]; j < ptr[br + 1]; ++j) {
+            const int64_t sc0 = 3 * static_cast<int64_t>(col[j]);
+            const int cn = static_cast<int>(sc0 / pbs);
+            if (agg[cn] != g) continue;
+            if (cn != node && !strong(gp, gc, node, cn)) continue;
+            const double *b = val + 9 * static_cast<int64_t>(j) + 3 * rr;
+            for (int c3 = 0; c3 < 3; ++c3) {
+                const int64_t sc = sc0 + c3;
+                const double coef = (sc == i) ? dg : b[c3];
+                const double scaled = __dmul_rn(__dmul_rn(di, coef), nom);
+                const int c = static_cast<int>(sc % pbs);
+                const double pr = __dmul_rn(scaled, Pt1[sc]);
+                if (touched[c]) acc[c] = __dadd_rn(acc[c], pr);
+                else { acc[c] = pr; touched[c] = true; }
+            }
+        }
+        const int64_t base = pptr[lbr] + t;  // one 3x3 block per touched aggregate
+        for (int c = 0; c < 3; ++c) pval[9 * base + 3 * rr + c] = acc[c];
+    }
+}
+
 // ---------------------------------------------------------------------------
 // block pipeline transfer (block_transfer_operators, coarsening.hpp:471-560).
 // Tentative: block v_g * I for node i in aggregate g, v_g = 1/sqrt(|g|).
@@ -1321,6 +1380,7 @@ void scalar_to_bsr3(int64_t n, const int64_t *d_ptr, const int64_t *d_col, const
 
 void strength_graph(const Bsr3 &A, int h, double eps_strong, Graph &G, cudaStream_t s,
                     bool fnorm) {
+    NvtxScope nvtx_scope("samg::strength_graph");
     const int n = static_cast<int>(A.nrows / h);
     const double eps2 = eps_strong * eps_strong;
     DevBuf<double> d(n, s), wblk(A.nnzb + 1, s);
@@ -1376,6 +1436,7 @@ void strength_graph(const Bsr3 &A, int h, double eps_strong, Graph &G, cudaStrea
 }
 
 int64_t aggregate(const Graph &G, DevBuf<int> &agg, cudaStream_t s, DevBuf<int> *seedno_out) {
+    NvtxScope nvtx_scope("samg::aggregate");
     const int n = static_cast<int>(G.nnodes);
     agg.alloc(n, s);
     if (n == 0) return 0;
@@ -1442,6 +1503,7 @@ int64_t aggregate(const Graph &G, DevBuf<int> &agg, cudaStream_t s, DevBuf<int> 
 void tentative(const DevBuf<int> &agg, int64_t nnodes, int64_t naggs, int pbs, const double *B,
                int k, DevBuf<double> &Pt, DevBuf<double> &Bc, DevError *err, cudaStream_t s,
                int64_t a0, int64_t a1) {
+    NvtxScope nvtx_scope("samg::tentative_prolongation");
     if (a1 < 0) a1 = naggs;
     const int64_t nfine = nnodes * pbs;
     DevBuf<int> keys2(nnodes, s), iota(nnodes, s), nodes(nnodes, s), agg_ptr(naggs + 1, s);
@@ -1474,12 +1536,21 @@ void tentative(const DevBuf<int> &agg, int64_t nnodes, int64_t naggs, int pbs, c
 void smooth_prolongation(const Bsr3 &A, const Graph &G, const DevBuf<int> &agg, int64_t naggs,
                          int pbs, int k, const double *Pt, double omega, Bsr3 &P, DevError *err,
                          cudaStream_t s, int64_t node0, int64_t node1) {
+    NvtxScope nvtx_scope("samg::smooth_prolongation");
+    // k == 0: the indicator tentative operator of the `scalar` pipeline
+    // (pbs 3 on every level: one 3x3 block column group per aggregate)
+    const bool ind = k == 0;
+    if (ind) {
+        if (pbs != 3) fail(SAMG_UNSUPPORTED, "smooth_prolongation: indicator tentative needs pbs 3");
+        k = 3;
+    }
     const int h = pbs / 3, kb = k / 3;
     if (node1 < 0) node1 = A.nrows / h;
     // rows of the nodes [node0, node1): A (global numbering) must hold them
     const int64_t nnodes = node1 - node0, nbrows = nnodes * h, nsc = 3 * nbrows;
     const int64_t row0 = node0 * h;
     if (omega == 0.0) {
+        if (ind) fail(SAMG_UNSUPPORTED, "smooth_prolongation: omega 0 with the indicator tentative");
         P.alloc(nbrows, naggs * kb, nbrows * kb, s);
         k_ptent_bsr<<<ceil_div(nbrows + 1, 256), 256, 0, s>>>(static_cast<int>(nbrows), h, k, agg.p,
                                                              Pt, P.ptr.p, P.col.p, P.val.p,
@@ -1520,15 +1591,34 @@ void smooth_prolongation(const Bsr3 &A, const Graph &G, const DevBuf<int> &agg, 
                                                   G.col.p, dinv.p, diag.p, err, 3 * row0);
     CK_LAUNCH();
     check_dev_error(err, s);
-    k_psm_vals<<<ceil_div(nsc, 128), 128, 0, s>>>(nsc, pbs, h, k, A.ptr.p, A.col.p, A.val.p,
-                                                  G.ptr.p, G.col.p, agg.p, toff.p, tlist.p,
-                                                  tcnt.p, dinv.p, diag.p, Pt, omega, P.ptr.p,
-                                                  P.val.p, 3 * row0);
+    if (ind)
+        k_psm_vals_ind<<<ceil_div(nsc, 128), 128, 0, s>>>(nsc, pbs, h, A.ptr.p, A.col.p, A.val.p,
+                                                          G.ptr.p, G.col.p, agg.p, toff.p, tlist.p,
+                                                          tcnt.p, dinv.p, diag.p, Pt, omega, P.ptr.p,
+                                                          P.val.p, 3 * row0);
+    else
+        k_psm_vals<<<ceil_div(nsc, 128), 128, 0, s>>>(nsc, pbs, h, k, A.ptr.p, A.col.p, A.val.p,
+                                                      G.ptr.p, G.col.p, agg.p, toff.p, tlist.p,
+                                                      tcnt.p, dinv.p, diag.p, Pt, omega, P.ptr.p,
+                                                      P.val.p, 3 * row0);
+    CK_LAUNCH();
+}
+
+void tentative_indicator(const DevBuf<int> &agg, int64_t nnodes, int64_t naggs, int pbs,
+                         DevBuf<double> &Pt1, cudaStream_t s) {
+    NvtxScope nvtx_scope("samg::tentative_prolongation (indicator)");
+    DevBuf<int> cnt(naggs + 1, s);
+    CK(cudaMemsetAsync(cnt.p, 0, sizeof(int) * (naggs + 1), s));
+    if (nnodes) k_bt_count<<<ceil_div(nnodes, 256), 256, 0, s>>>(static_cast<int>(nnodes), agg.p, cnt.p);
+    Pt1.alloc(nnodes * pbs + 1, s);
+    if (nnodes)
+        k_tent_indicator<<<ceil_div(nnodes, 256), 256, 0, s>>>(nnodes, pbs, agg.p, cnt.p, Pt1.p);
     CK_LAUNCH();
 }
 
 void block_transfer(const Bsr3 &A, const Graph &G, const DevBuf<int> &agg, int64_t naggs,
                     double omega, Bsr3 &P, DevError *err, cudaStream_t s, int64_t r0, int64_t r1) {
+    NvtxScope nvtx_scope("samg::block_transfer_operators");
     const int nall = static_cast<int>(A.nrows);  // aggregate sizes over every node
     if (r1 < 0) r1 = nall;
     const int n = static_cast<int>(r1 - r0);      // rows [r0, r1) of P
@@ -1578,6 +1668,7 @@ void block_transfer(const Bsr3 &A, const Graph &G, const DevBuf<int> &agg, int64
 }
 
 void transpose(const Bsr3 &P, Bsr3 &R, cudaStream_t s) {
+    NvtxScope nvtx_scope("samg::transpose");
     const int64_t nnz = P.nnzb;
     R.alloc(P.ncols, P.nrows, nnz, s);
     DevBuf<int> rowidx(nnz + 1, s), iota(nnz + 1, s), perm(nnz + 1, s), skeys(nnz + 1, s);
@@ -1900,6 +1991,7 @@ void spgemm(const Bsr3 &A, const Bsr3 &B, Bsr3 &C, cudaStream_t s, bool scalar_o
 // is symmetric (every level matrix: R = P^T), B = P through R's blocks.
 void galerkin(const Bsr3 &R, const Bsr3 &A, const Bsr3 &P, Bsr3 &Ac, cudaStream_t s,
               bool scalar_order) {
+    NvtxScope nvtx_scope("samg::galerkin");
     galerkin_rows(R, A, P, R, Ac, s, scalar_order);
 }
 
@@ -1925,6 +2017,7 @@ void slice_rows(const Bsr3 &M, int64_t r0, int64_t r1, Bsr3 &out, cudaStream_t s
 // (Rl A) P, with P's columns read through the full R = P^T.
 void galerkin_rows(const Bsr3 &Rl, const Bsr3 &A, const Bsr3 &P, const Bsr3 &R, Bsr3 &Ac,
                    cudaStream_t s, bool scalar_order, bool subset) {
+    NvtxScope nvtx_scope("samg::galerkin");
     Bsr3 RA;
     {
         DevBuf<int> tpos(std::max<int64_t>(1, A.nnzb), s), bad(1, s);
@@ -2017,6 +2110,7 @@ void fix_decoupled_rows(Bsr3 &A, cudaStream_t s, int64_t row0) {
 
 void setup_smoother(const Bsr3 &A, int kind, double omega, Smoother &M, DevError *err,
                     cudaStream_t s, int64_t row0) {
+    NvtxScope nvtx_scope("samg::smoother_setup");
     const int *ap = A.ptr.p, *ac = A.col.p;
     const int r0 = static_cast<int>(row0);  // global id of local row 0 (diagonal = r0 + i)
     const double *av = A.val.p;

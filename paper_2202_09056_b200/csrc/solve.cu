@@ -755,7 +755,10 @@ int choose_group(const Bsr3 &A) {
     if (bpr >= 64.0 && G < 32 && forced == 0) G = 32;
     // small (coarse-level / restriction) matrices cannot fill 148 SMs:
     // spend more lanes per row to shorten the serial chains instead
-    // (R1 of C1: 3 822 rows; 8 lanes -> 40 us, 32 lanes -> ~6 us)
+    // (R1 of C1: 3 822 rows; 8 lanes -> 40 us, 32 lanes -> ~6 us).  Keeping
+    // the grid within one wave instead (C1's level 2 at 32 lanes: 0.65
+    // waves) measured slower than 64 lanes in 1.29 waves (17.3 -> 25.9 us
+    // per residual): the shorter per-lane chains win
     while (G < 128 && A.nrows * G < 148LL * 1024) G *= 2;
     return G;
 }
