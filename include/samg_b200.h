@@ -58,9 +58,11 @@ enum samg_status {
  * 3-unknown points, B ignored) and NS_SCALAR (hierarchy.hpp:298-330) keep
  * scalar CSR levels in the reference: here the same values as 3x3 blocks
  * (their patterns are whole blocks for matrices with full 3x3 blocks),
- * memory_footprint in the reference's scalar accounting, damped Jacobi
- * only.  ilu0<double> (the scalar pipelines' and NS_HYBRID1's scalar ILU)
- * returns SAMG_UNSUPPORTED; so do the scalar pipelines on several GPUs. */
+ * memory_footprint in the reference's scalar accounting, the reference's
+ * scalar smoothers (damped Jacobi, ilu0<double>).  ILU0 with SCALAR,
+ * NS_SCALAR and NS_HYBRID1 is the scalar ilu0<double> of the level matrix
+ * (hierarchy.hpp:288-291), bit-identical.  The scalar pipelines and ILU(0)
+ * are single-GPU. */
 enum samg_pipeline {
     SAMG_PIPELINE_SCALAR = 0,
     SAMG_PIPELINE_BLOCK = 1,
@@ -73,7 +75,8 @@ enum samg_pipeline {
 /* Smoothers.  JACOBI = the reference's point damped_jacobi
  * (relaxation.hpp:141-180, omega default 0.72).  SPAI0 and BLOCK_JACOBI are
  * 3x3 block smoothers.  ILU0 = the reference's default
- * ilu0<block3> (relaxation.hpp:20-139), bit-identical factors and sweeps
+ * ilu0<block3> (relaxation.hpp:20-139; ilu0<double> for the scalar-smoother
+ * pipelines), bit-identical factors and sweeps
  * (single GPU; the partitioned solver returns SAMG_UNSUPPORTED). */
 enum samg_smoother {
     SAMG_SMOOTHER_JACOBI = 0,

@@ -513,14 +513,16 @@ class RefHier:
         return (nrows, nc.value, _copy(ptr, nrows + 1, np.int64), _copy(col, nnz, np.int64),
                 _copy(val, nnz * 9, np.float64).reshape(-1, 3, 3))
 
-    def ilu(self, l):
-        """[factors (9*nnzb) | inverted pivots (9*nrows)] of level l's ilu0<block3>"""
+    def ilu(self, l, scalar=False):
+        """[factors (9*nnzb) | inverted pivots (9*nrows)] of level l's
+        ilu0<block3>; scalar: ilu0<double>'s factors re-blocked and its 3
+        pivots per block row"""
         nz, nr = C.c_int64(), C.c_int64()
         lp, ip = f64p(), f64p()
         if self.be.lib.ref_ilu_factors(self.h, l, C.byref(nz), C.byref(nr), C.byref(lp), C.byref(ip)):
             raise KeyError(l)
         return np.concatenate([np.ctypeslib.as_array(lp, (9 * nz.value,)).copy(),
-                               np.ctypeslib.as_array(ip, (9 * nr.value,)).copy()])
+                               np.ctypeslib.as_array(ip, ((3 if scalar else 9) * nr.value,)).copy()])
 
     def aggregates(self, l):
         nn, cnt, idp = C.c_int64(), C.c_int64(), i64p()

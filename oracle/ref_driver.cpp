@@ -78,6 +78,7 @@ struct ref_handle {
     // scalar pipelines: the level matrices as 3x3 blocks (to_block<3>, for
     // the parity taps; the hierarchy itself keeps them scalar)
     std::vector<std::array<csr<block3>, 3>> blockview;
+    std::vector<csr<block3>> ilu_blockview;  // ilu0<double> factors as 3x3 blocks
 };
 
 using clk = std::chrono::steady_clock;
@@ -370,6 +371,18 @@ int ref_ilu_factors(void *hp, int level, int64_t *nnz, int64_t *nrows, const dou
         const double **inv) {
     auto *h = static_cast<ref_handle *>(hp);
     if (level < 0 || level + 1 >= h->H.nlevels()) return 1;
+    // ilu0<double>: the scalar factors re-blocked (to_block<3>: the scalar
+    // pattern is whole blocks), the 3 scalar pivots per block row as they are
+    if (const auto *ss = std::get_if<ilu0<double>>(&h->H.levels[level].smoother)) {
+        h->ilu_blockview.resize(h->H.nlevels());
+        csr<block3> &fb = h->ilu_blockview[level];
+        fb = to_block<3>(ss->factors());
+        *nnz = static_cast<int64_t>(fb.val.size());
+        *nrows = static_cast<int64_t>(ss->inverted_pivots().size()) / 3;
+        *lu = reinterpret_cast<const double *>(fb.val.data());
+        *inv = ss->inverted_pivots().data();
+        return 0;
+    }
     const auto *sm = std::get_if<ilu0<block3>>(&h->H.levels[level].smoother);
     if (!sm) return 1;
     *nnz = static_cast<int64_t>(sm->factors().val.size());

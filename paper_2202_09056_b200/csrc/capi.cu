@@ -147,14 +147,10 @@ void validate_params(const samg_amg_params *prm, int pipeline) {
     // (their patterns are whole blocks), reported in scalar CSR accounting
     require(pipeline >= SAMG_PIPELINE_SCALAR && pipeline <= SAMG_PIPELINE_NS_BLOCK,
             SAMG_INVALID_ARGUMENT, "setup: unknown pipeline");
-    const bool scalar_smoother = pipeline == SAMG_PIPELINE_NS_HYBRID1 ||
-                                 pipeline == SAMG_PIPELINE_SCALAR || pipeline == SAMG_PIPELINE_NS_SCALAR;
-    if (scalar_smoother && prm && prm->smoother == SAMG_SMOOTHER_ILU0)
-        fail(SAMG_UNSUPPORTED, "setup: scalar ILU(0) (ilu0<double>) is not on the B200 path");
     if ((pipeline == SAMG_PIPELINE_SCALAR || pipeline == SAMG_PIPELINE_NS_SCALAR) && prm &&
-        prm->smoother != SAMG_SMOOTHER_JACOBI)
+        prm->smoother != SAMG_SMOOTHER_JACOBI && prm->smoother != SAMG_SMOOTHER_ILU0)
         fail(SAMG_UNSUPPORTED, "setup: the scalar pipelines take the reference's scalar smoothers "
-                               "(damped Jacobi)");
+                               "(damped Jacobi, ilu0<double>)");
     require(prm->smoother >= 0 && prm->smoother <= 3, SAMG_INVALID_ARGUMENT, "setup: unknown smoother");
     require(prm->pre_sweeps >= 0 && prm->post_sweeps >= 0, SAMG_INVALID_ARGUMENT,
             "setup: negative sweep count");
@@ -615,8 +611,8 @@ SAMG_API int samg_smoother_info(const samg_hierarchy *hp, int level, int64_t *le
         if (level < 0 || level + 1 >= static_cast<int>(h.levels.size()))
             fail(SAMG_INVALID_ARGUMENT, "level has no smoother");
         const Smoother &M = h.levels[level].M;
-        // ILU(0): [factors (9*nnzb) | inverted pivots (9*nrows)]
-        *len = M.kind == SM_ILU ? 9 * (M.nnzb + M.nrows) : static_cast<int64_t>(M.data.n);
+        // ILU(0): [factors (9*nnzb) | inverted pivots (9*nrows; ilu0<double>: 3*nrows)]
+        *len = M.kind == SM_ILU ? 9 * M.nnzb + (M.scalar ? 3 : 9) * M.nrows : static_cast<int64_t>(M.data.n);
     });
 }
 
@@ -629,7 +625,7 @@ SAMG_API int samg_get_smoother(const samg_hierarchy *hp, int level, double *data
         const Smoother &M = h.levels[level].M;
         if (M.kind == SM_ILU) {
             CK(cudaMemcpyAsync(data, M.lu.p, sizeof(double) * 9 * M.nnzb, cudaMemcpyDeviceToHost, h.stream));
-            CK(cudaMemcpyAsync(data + 9 * M.nnzb, M.data.p, sizeof(double) * 9 * M.nrows,
+            CK(cudaMemcpyAsync(data + 9 * M.nnzb, M.data.p, sizeof(double) * (M.scalar ? 3 : 9) * M.nrows,
                                cudaMemcpyDeviceToHost, h.stream));
         } else {
             CK(cudaMemcpyAsync(data, M.data.p, M.data.bytes(), cudaMemcpyDeviceToHost, h.stream));

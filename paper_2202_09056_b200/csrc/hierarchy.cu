@@ -75,7 +75,10 @@ uint64_t Hierarchy::memory_footprint() const {
             bytes += mbytes(lv.P);
             bytes += mbytes(lv.R);
         }
-        if (lv.M.kind == SM_ILU)  // ilu0::bytes (relaxation.hpp:93-95)
+        if (lv.M.kind == SM_ILU && lv.M.scalar)  // ilu0<double>::bytes: scalar factors + pivots
+            bytes += static_cast<uint64_t>(3 * lv.M.nrows + 1) * 8 + static_cast<uint64_t>(lv.M.nnzb) * 9 * 16 +
+                     static_cast<uint64_t>(lv.M.nrows) * 24;
+        else if (lv.M.kind == SM_ILU)  // ilu0::bytes (relaxation.hpp:93-95)
             bytes += static_cast<uint64_t>(lv.M.nrows + 1) * 8 + static_cast<uint64_t>(lv.M.nnzb) * 80 +
                      static_cast<uint64_t>(lv.M.nrows) * 72;
         else
@@ -256,8 +259,17 @@ Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int6
     }
     B.release();
     const size_t L = H->levels.size();
-    for (size_t i = 0; i + 1 < L; ++i)
-        setup_smoother(H->levels[i].A, prm.smoother, prm.smoother_omega, H->levels[i].M, err, s);
+    // the scalar pipelines and ns_hybrid1 smooth with scalar smoothers
+    // (hierarchy.hpp:288-291): ILU(0) is ilu0<double> of the scalar view
+    const bool scalar_smoothers = pipeline == SAMG_PIPELINE_SCALAR ||
+                                  pipeline == SAMG_PIPELINE_NS_SCALAR ||
+                                  pipeline == SAMG_PIPELINE_NS_HYBRID1;
+    for (size_t i = 0; i + 1 < L; ++i) {
+        if (scalar_smoothers && prm.smoother == SAMG_SMOOTHER_ILU0)
+            setup_ilu0_scalar(H->levels[i].A, H->levels[i].M, err, s);
+        else
+            setup_smoother(H->levels[i].A, prm.smoother, prm.smoother_omega, H->levels[i].M, err, s);
+    }
     check_dev_error(err, s);
     mark("smoothers", L - 1);
     if (prm.vcycle_precision == SAMG_PRECISION_MIXED) {

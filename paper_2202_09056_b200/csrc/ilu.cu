@@ -432,6 +432,223 @@ void level_orders(const Bsr3 &A, const DevBuf<int> &dpos, DevBuf<int> &order, in
     CK(cudaStreamSynchronize(s));  // host vectors go out of scope
 }
 
+// ---- ilu0<double> on the scalar view --------------------------------------
+// The scalar pipelines (and ns_hybrid1) smooth with the SCALAR ILU(0) of the
+// level matrix (hierarchy.hpp:288-291, relaxation.hpp:20-139 with
+// V = double).  Its scalar rows 3b, 3b+1, 3b+2 form block row b and the
+// pattern is the blocks' entries, so the factors keep the 3x3 block layout
+// (entry (3b+r, 3c+q) at lu[9j + 3r + q] for block j = (b, c)).  A scalar
+// row depends on the scalar rows of the lower blocks of its block row and on
+// the earlier scalar rows of its own block row: one warp per block row, in
+// the block rows' dependency-level order (level_orders), its three scalar
+// rows in sequence.  Every operation is the reference's, in its order.
+
+// IKJ (relaxation.hpp:115-132) for the three scalar rows of a block row.
+__global__ void __launch_bounds__(256) k_ilu_factor_s(int n, const int *__restrict__ order,
+        const int *__restrict__ ptr, const int *__restrict__ col, const int *__restrict__ dpos,
+        double *lu, double *inv, int *done, int *counter, DevError *err) {
+    extern __shared__ __align__(16) unsigned char fsm[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double *srow = reinterpret_cast<double *>(fsm) + static_cast<size_t>(w) * 9 * kFMax;
+    int *scol = reinterpret_cast<int *>(fsm + sizeof(double) * 9 * kFMax * 8) + w * kFMax;
+    for (;;) {
+        int t = 0;
+        if (lane == 0) t = atomicAdd(counter, 1);
+        t = __shfl_sync(kFull, t, 0);
+        if (t >= n) return;
+        const int i = __ldg(order + t);
+        const int b = ptr[i], e = ptr[i + 1], di = dpos[i], len = e - b;
+        const bool in_smem = len <= kFMax;
+        double *rv = in_smem ? srow - 9LL * b : lu;
+        const int *rc = in_smem ? scol - b : col;
+        if (in_smem) {
+            for (int q = lane; q < len; q += 32) scol[q] = col[b + q];
+            for (int q = lane; q < 9 * len; q += 32) srow[q] = lu[9LL * b + q];
+        }
+        // every lower block row must be factored (flags, then acquire)
+        for (int j = b + lane; j < di; j += 32)
+            while (ld_relaxed(done + static_cast<int64_t>(col[j]) * kFS) == 0) {
+            }
+        __syncwarp();
+        cuda::atomic_thread_fence(cuda::memory_order_acquire, cuda::thread_scope_device);
+        __syncwarp();
+        double own_inv[3] = {0.0, 0.0, 0.0};
+        for (int r = 0; r < 3; ++r) {
+            // steps k = 3c + q over the lower blocks (c < i), ascending
+            for (int j = b; j < di; ++j) {
+                const int c = rc[j];
+                const int dc = __ldg(dpos + c), ec = __ldg(ptr + c + 1);
+                for (int q = 0; q < 3; ++q) {
+                    // L_ik = a_ik * (1 / u_kk)
+                    const double L = __dmul_rn(rv[9LL * j + 3 * r + q], __ldcg(inv + 3LL * c + q));
+                    __syncwarp();
+                    if (lane == 0) rv[9LL * j + 3 * r + q] = L;
+                    // row k's U part: its diagonal block's entries right of
+                    // q (they land in block j of row i), then its blocks
+                    // right of the diagonal
+                    if (lane < 2 - q) {
+                        const int qq = q + 1 + lane;
+                        double *dst = rv + 9LL * j + 3 * r + qq;
+                        *dst = __dsub_rn(*dst, __dmul_rn(L, __ldcg(lu + 9LL * dc + 3 * q + qq)));
+                    }
+                    for (int l = dc + 1 + lane; l < ec; l += 32) {
+                        const int cc = __ldg(col + l);
+                        int lo = b, hi = e - 1, pos = -1;
+                        while (lo <= hi) {
+                            const int m = (lo + hi) >> 1, cm = rc[m];
+                            if (cm == cc) { pos = m; break; }
+                            if (cm < cc) lo = m + 1;
+                            else hi = m - 1;
+                        }
+                        if (pos < 0) continue;
+                        double *dst = rv + 9LL * pos + 3 * r;
+#pragma unroll
+                        for (int q2 = 0; q2 < 3; ++q2)
+                            dst[q2] = __dsub_rn(dst[q2], __dmul_rn(L, __ldcg(lu + 9LL * l + 3 * q + q2)));
+                    }
+                    __syncwarp();
+                }
+            }
+            // steps k = 3i + q, q < r: the earlier scalar rows of this block row
+            for (int q = 0; q < r; ++q) {
+                const double L = __dmul_rn(rv[9LL * di + 3 * r + q], own_inv[q]);
+                __syncwarp();
+                if (lane == 0) rv[9LL * di + 3 * r + q] = L;
+                if (lane < 2 - q) {
+                    const int qq = q + 1 + lane;
+                    double *dst = rv + 9LL * di + 3 * r + qq;
+                    *dst = __dsub_rn(*dst, __dmul_rn(L, rv[9LL * di + 3 * q + qq]));
+                }
+                for (int l = di + 1 + lane; l < e; l += 32) {
+                    double *dst = rv + 9LL * l + 3 * r;
+#pragma unroll
+                    for (int q2 = 0; q2 < 3; ++q2)
+                        dst[q2] = __dsub_rn(dst[q2], __dmul_rn(L, rv[9LL * l + 3 * q + q2]));
+                }
+                __syncwarp();
+            }
+            // inverted pivot (value_traits<double>::inverse, static_block.hpp:170-173)
+            const double piv = rv[9LL * di + 4 * r];
+            if (fabs(piv) < 1e-300) {
+                if (lane == 0) raise_err(err, SAMG_SINGULAR_BLOCK, 3LL * i + r);
+                own_inv[r] = 0.0;
+            } else {
+                own_inv[r] = __ddiv_rn(1.0, piv);
+            }
+            __syncwarp();
+        }
+        if (in_smem)
+            for (int q = lane; q < 9 * len; q += 32) lu[9LL * b + q] = srow[q];
+        if (lane < 3) inv[3LL * i + lane] = own_inv[lane];
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence();
+            st_release(done + static_cast<int64_t>(i) * kFS, 1);
+        }
+    }
+}
+
+// The scalar triangular sweeps (relaxation.hpp:44-88, V = double), a warp
+// per block row in level order, the output value its own flag (as
+// k_ilu_sweep).  Forward: lanes 0..2 run the chains of scalar rows 3i+p over
+// the lower blocks (ascending scalar columns), then the rows of the own
+// block in sequence (their within-block terms come last).  Backward: the
+// within-block terms come FIRST in each chain, so the rows run in sequence
+// 3i+2, 3i+1, 3i over the products of the higher blocks, formed in parallel
+// beforehand (one window: at most kWinS higher blocks, checked at setup);
+// x_i = (chain) * inv_i; u_out = x (+ u_in, kernels::axpby(1, x, 1, u)).
+constexpr int kWinS = 192;
+constexpr int kSweepSmemS = 8 * kWinS * 9 * static_cast<int>(sizeof(double));
+
+template <bool kFwd, bool kZero>
+__global__ void __launch_bounds__(256) k_ilu_sweep_s(int n, const int *__restrict__ order,
+        const int *__restrict__ ptr, const int *__restrict__ col, const int *__restrict__ dpos,
+        const double *__restrict__ lu, const double *__restrict__ inv, const double *src,
+        double *out, const double *u_in, double *u_out, unsigned *counter) {
+    extern __shared__ __align__(16) double ssm[];  // per warp: kWinS x 9 products
+    const int lane = threadIdx.x & 31;
+    double *bs = ssm + static_cast<size_t>(threadIdx.x >> 5) * kWinS * 9;
+    for (;;) {
+        unsigned t = 0;
+        if (lane == 0) t = atomicAdd(counter, 1u) + 1u;  // counter starts at 0xffffffff
+        t = __shfl_sync(kFull, t, 0);
+        if (t >= static_cast<unsigned>(n)) return;
+        const int i = __ldg(order + t);
+        const int di = __ldg(dpos + i);
+        const int b = kFwd ? __ldg(ptr + i) : di + 1, e = kFwd ? di : __ldg(ptr + i + 1);
+        double a = lane < 3 ? src[3LL * i + lane] : 0.0;  // lane p: the chain of row 3i+p
+        for (int w0 = b; w0 < e; w0 += kWinS) {
+            const int m = min(kWinS, e - w0);
+            for (int q = lane; q < 9 * m; q += 32) bs[q] = __ldg(lu + 9LL * w0 + q);
+            __syncwarp();
+            // each dependency: wait for its value, form its 9 products in place
+            for (int d = lane; d < m; d += 32) {
+                const double *g = out + 3LL * __ldg(col + w0 + d);
+                unsigned long long v0, v1, v2;
+                do {
+                    v0 = ld_poll(g); v1 = ld_poll(g + 1); v2 = ld_poll(g + 2);
+                } while (v0 == kSent || v1 == kSent || v2 == kSent);
+                const double x0 = __longlong_as_double(static_cast<long long>(v0)),
+                             x1 = __longlong_as_double(static_cast<long long>(v1)),
+                             x2 = __longlong_as_double(static_cast<long long>(v2));
+                double *bl = bs + 9 * d;
+#pragma unroll
+                for (int r = 0; r < 3; ++r) {
+                    bl[3 * r] = __dmul_rn(bl[3 * r], x0);
+                    bl[3 * r + 1] = __dmul_rn(bl[3 * r + 1], x1);
+                    bl[3 * r + 2] = __dmul_rn(bl[3 * r + 2], x2);
+                }
+            }
+            __syncwarp();
+            if (kFwd && lane < 3)  // the lower blocks' terms, the three chains in parallel
+                for (int d = 0; d < m; ++d) {
+                    a = __dsub_rn(a, bs[9 * d + 3 * lane]);
+                    a = __dsub_rn(a, bs[9 * d + 3 * lane + 1]);
+                    a = __dsub_rn(a, bs[9 * d + 3 * lane + 2]);
+                }
+            if (kFwd) __syncwarp();  // the window's staging is reused
+        }
+        const double a0 = __shfl_sync(kFull, a, 0), a1 = __shfl_sync(kFull, a, 1),
+                     a2 = __shfl_sync(kFull, a, 2);
+        const double *dl = lu + 9LL * di;
+        double res[3];
+        if constexpr (kFwd) {
+            // own block, unit lower factor: y0; y1 - L10 y0; (y2 - L20 y0) - L21 y1
+            res[0] = a0;
+            res[1] = __dsub_rn(a1, __dmul_rn(__ldg(dl + 3), res[0]));
+            res[2] = __dsub_rn(__dsub_rn(a2, __dmul_rn(__ldg(dl + 6), res[0])),
+                               __dmul_rn(__ldg(dl + 7), res[1]));
+        } else {
+            const int m = e - b;
+            const double y[3] = {a0, a1, a2};
+            for (int r = 2; r >= 0; --r) {
+                double c = y[r];
+                for (int q = r + 1; q < 3; ++q) c = __dsub_rn(c, __dmul_rn(__ldg(dl + 3 * r + q), res[q]));
+                for (int d = 0; d < m; ++d) {
+                    c = __dsub_rn(c, bs[9 * d + 3 * r]);
+                    c = __dsub_rn(c, bs[9 * d + 3 * r + 1]);
+                    c = __dsub_rn(c, bs[9 * d + 3 * r + 2]);
+                }
+                res[r] = __dmul_rn(c, __ldg(inv + 3LL * i + r));
+            }
+            __syncwarp();  // the staging is reused by the next row
+        }
+        if (lane < 3) {
+            st_publish(out + 3LL * i + lane, res[lane]);
+            if constexpr (!kFwd)
+                u_out[3LL * i + lane] = kZero ? res[lane] : __dadd_rn(res[lane], u_in[3LL * i + lane]);
+        }
+        __syncwarp();
+    }
+}
+
+// the longest run of blocks right of the diagonal (the scalar backward
+// sweep keeps them in one window)
+__global__ void k_max_upper(int n, const int *ptr, const int *dpos, int *mx) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) atomicMax(mx, ptr[i + 1] - dpos[i] - 1);
+}
+
 } // namespace
 
 void setup_ilu0(const Bsr3 &A, Smoother &M, DevError *err, cudaStream_t s) {
@@ -462,6 +679,51 @@ void setup_ilu0(const Bsr3 &A, Smoother &M, DevError *err, cudaStream_t s) {
         return 1;
     });
     k_ilu_factor<<<persistent_grid(reinterpret_cast<const void *>(k_ilu_factor), n), 256, fsmem, s>>>(
+        n, M.order.p, A.ptr.p, A.col.p, M.dpos.p, M.lu.p, M.data.p, M.flags.p,
+        M.flags.p + static_cast<int64_t>(n) * kFS, err);
+    CK_LAUNCH();
+}
+
+void setup_ilu0_scalar(const Bsr3 &A, Smoother &M, DevError *err, cudaStream_t s) {
+    if (A.nrows != A.ncols) fail(SAMG_NON_SQUARE, "ilu0: matrix must be square");
+    const int n = static_cast<int>(A.nrows);
+    M.kind = SM_ILU;
+    M.scalar = true;
+    M.ptr = A.ptr.p;
+    M.col = A.col.p;
+    M.nrows = A.nrows;
+    M.nnzb = A.nnzb;
+    M.data.alloc(3 * A.nrows + 3, s);
+    M.lu.alloc(9 * A.nnzb + 1, s);
+    M.tmp.alloc(3 * A.nrows + 3, s);
+    M.dpos.alloc(A.nrows + 1, s);
+    M.flags.alloc(A.nrows * kFS + 2, s);
+    M.sweep.alloc(6 * A.nrows + 1, s);
+    if (n == 0) return;
+    k_ilu_dpos<<<ceil_div(n, 256), 256, 0, s>>>(n, A.ptr.p, A.col.p, M.dpos.p, err);
+    CK_LAUNCH();
+    check_dev_error(err, s);
+    {
+        DevBuf<int> mx(1, s);
+        CK(cudaMemsetAsync(mx.p, 0, sizeof(int), s));
+        k_max_upper<<<ceil_div(n, 256), 256, 0, s>>>(n, A.ptr.p, M.dpos.p, mx.p);
+        CK_LAUNCH();
+        int hm = 0;
+        CK(cudaMemcpyAsync(&hm, mx.p, sizeof hm, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (hm > kWinS)
+            fail(SAMG_UNSUPPORTED, "ilu0<double>: more than 192 blocks right of a diagonal block");
+    }
+    level_orders(A, M.dpos, M.order, M.depth, s);
+    CK(cudaMemcpyAsync(M.lu.p, A.val.p, sizeof(double) * 9 * A.nnzb, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemsetAsync(M.flags.p, 0, sizeof(int) * (A.nrows * kFS + 2), s));
+    constexpr int fsmem = 8 * kFMax * (9 * static_cast<int>(sizeof(double)) + static_cast<int>(sizeof(int)));
+    static DeviceCache fattr;
+    fattr.get([] {
+        CK(cudaFuncSetAttribute(k_ilu_factor_s, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem));
+        return 1;
+    });
+    k_ilu_factor_s<<<persistent_grid(reinterpret_cast<const void *>(k_ilu_factor_s), n), 256, fsmem, s>>>(
         n, M.order.p, A.ptr.p, A.col.p, M.dpos.p, M.lu.p, M.data.p, M.flags.p,
         M.flags.p + static_cast<int64_t>(n) * kFS, err);
     CK_LAUNCH();
@@ -504,6 +766,28 @@ void launch_ilu_smooth(const Bsr3 *A, const Smoother &M, const double *f, const 
     };
     const int gridf = grid_for(M.depth[0]), gridb = grid_for(M.depth[1]);
     const int *of = M.order.p, *ob = M.order.p + n;
+    if (M.scalar) {  // ilu0<double>
+        static DeviceCache sattr;
+        sattr.get([] {
+            for (const void *k : {reinterpret_cast<const void *>(k_ilu_sweep_s<true, true>),
+                                   reinterpret_cast<const void *>(k_ilu_sweep_s<false, false>),
+                                   reinterpret_cast<const void *>(k_ilu_sweep_s<false, true>)})
+                CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSweepSmemS));
+            return 1;
+        });
+        const int gs = std::max(1, std::min(gridf, sm_count()));  // one 8-warp CTA per SM (110 KB)
+        const int gb = std::max(1, std::min(gridb, sm_count()));
+        k_ilu_sweep_s<true, true><<<gs, 256, kSweepSmemS, s>>>(n, of, M.ptr, M.col, M.dpos.p, M.lu.p,
+                                                              M.data.p, rin, y, nullptr, nullptr, cnt);
+        if (u_in)
+            k_ilu_sweep_s<false, false><<<gb, 256, kSweepSmemS, s>>>(n, ob, M.ptr, M.col, M.dpos.p, M.lu.p,
+                                                                    M.data.p, y, x, u_in, u_out, cnt + 1);
+        else
+            k_ilu_sweep_s<false, true><<<gb, 256, kSweepSmemS, s>>>(n, ob, M.ptr, M.col, M.dpos.p, M.lu.p,
+                                                                   M.data.p, y, x, nullptr, u_out, cnt + 1);
+        CK_LAUNCH();
+        return;
+    }
     k_ilu_sweep<true, true><<<gridf, 256, kSweepSmem, s>>>(n, of, M.ptr, M.col, M.dpos.p, M.lu.p, M.data.p,
                                                           rin, y, nullptr, nullptr, cnt);
     if (u_in)

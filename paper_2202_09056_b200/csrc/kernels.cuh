@@ -67,6 +67,10 @@ struct Smoother {
     int depth[2] = {1, 1};       // number of forward / backward dependency levels
     const int *ptr = nullptr, *col = nullptr;  // A's pattern
     int64_t nrows = 0, nnzb = 0;
+    // ilu0<double> on the scalar view (the scalar pipelines' and
+    // ns_hybrid1's smoother): factors in the same 3x3 block layout, data =
+    // the inverted scalar pivots (3 per block row)
+    bool scalar = false;
 };
 
 // ---- solve phase (solve.cu) -------------------------------------------------
@@ -237,6 +241,9 @@ void setup_smoother(const Bsr3 &A, int kind, double omega, Smoother &M, DevError
 // block ILU(0) (ilu.cu): factorization, and one smoothing application
 // u_out = u_in + (LU)^-1 (f - A u_in)  (u_in == nullptr: zero guess, r = f)
 void setup_ilu0(const Bsr3 &A, Smoother &M, DevError *err, cudaStream_t s);
+// ilu0<double> (relaxation.hpp:20-139 with V = double) of the scalar view of
+// A (whole 3x3 blocks: the scalar pattern is the blocks' entries)
+void setup_ilu0_scalar(const Bsr3 &A, Smoother &M, DevError *err, cudaStream_t s);
 void launch_ilu_smooth(const Bsr3 *A, const Smoother &M, const double *f, const double *u_in,
                        double *u_out, cudaStream_t s, bool lowp = false);
 // coarsest level: dense inverse (row-major n x n), n = 3*A.nrows

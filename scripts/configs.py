@@ -39,7 +39,7 @@ CONFIGS = {
 SM = {"spai0": 1, "jacobi": 0, "block_jacobi": 2, "ilu0": 3}
 
 
-PIPE = {"block": 1, "ns_hybrid1": 3, "ns_hybrid2": 4, "ns_block": 5}
+PIPE = {"scalar": 0, "block": 1, "ns_scalar": 2, "ns_hybrid1": 3, "ns_hybrid2": 4, "ns_block": 5}
 
 
 def run(name, ref_on, max_it, out, smoother=None, pipeline="ns_block", precision="fp64"):
@@ -49,7 +49,7 @@ def run(name, ref_on, max_it, out, smoother=None, pipeline="ns_block", precision
     t0 = time.perf_counter()
     p = pb.generate_hex(**kw)
     tgen = time.perf_counter() - t0
-    B = None if pipeline == "block" else p.nullspace()
+    B = None if pipeline in ("block", "scalar") else p.nullspace()
     for sm, om in smoothers:
         rec = {"config": name, "pipeline": pipeline, "smoother": sm, "omega": om, "unknowns": p.n,
                "nnzb": p.nnzb, "generate_s": tgen, "vcycle_precision": precision}

@@ -54,8 +54,8 @@ def test_validation_before_device():
     n, ptr, col, val = A
     with pytest.raises(pb.NotDivisible):
         pb.setup((n - 1, ptr[:-1], col[:ptr[n - 1]], val[:ptr[n - 1]]), np.zeros((n - 1, 6)))
-    with pytest.raises(pb.Unsupported):
-        pb.setup(A, B, "ns_scalar")
+    with pytest.raises(pb.Unsupported):  # scalar pipelines: damped Jacobi only
+        pb.setup(A, B, "ns_scalar", pb.AmgParams(smoother="spai0"))
     with pytest.raises(pb.InvalidArgument):
         pb.setup(A, B, "ns_block", pb.AmgParams(smoother=7))
     with pytest.raises(pb.NotDivisible):

@@ -29,7 +29,7 @@ def rel_fro(a, b):
     return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
 
 
-def compare_hierarchies(h, hr, orc_h=None, smoother="spai0", omega=0.72):
+def compare_hierarchies(h, hr, orc_h=None, smoother="spai0", omega=0.72, pipeline="ns_block"):
     assert h.nlevels == hr.nlevels
     for l in range(h.nlevels):
         for w in (0, 1, 2):
@@ -53,8 +53,9 @@ def compare_hierarchies(h, hr, orc_h=None, smoother="spai0", omega=0.72):
                 if smoother == "jacobi":
                     sm_o = omega * sm_o
                 np.testing.assert_array_equal(sm_g, sm_o)
-            if smoother == "ilu0":  # factors + inverted pivots of ilu0<block3> itself
-                np.testing.assert_array_equal(h.smoother(l), hr.ilu(l))
+            if smoother == "ilu0":  # factors + inverted pivots of ilu0<block3> / <double> itself
+                scalar = pipeline in ("scalar", "ns_scalar", "ns_hybrid1")
+                np.testing.assert_array_equal(h.smoother(l), hr.ilu(l, scalar))
     assert h.coarse_dim == hr.coarse_dim
     assert h.memory_footprint() == hr.memory_footprint
 
@@ -99,8 +100,30 @@ CASES = [
     # the coarse inverse must be equilibrated to match the reference's LU
     ("beam16_hetero_illscaled", dict(nx=16, ny=4, nz=4, lx=4.0, dirichlet="eliminate",
                                      heterogeneous=True, load="random", seed=9), "spai0", 0.72, 150),
+    # the scalar pipelines (hierarchy.hpp:298-330): scalar CSR levels in the
+    # reference (compared as to_block<3>), the reference's damped Jacobi
+    ("box975_scalar_jacobi05", dict(nx=9, ny=7, nz=5, dirichlet="eliminate", load="traction_xend"),
+     "jacobi", 0.5, 150, "scalar"),
+    ("cube6_keep_scalar_jacobi", dict(nx=6, dirichlet="keep_rows"), "jacobi", 0.72, 100, "scalar"),
+    ("beam_xslow_scalar_jacobi05", dict(nx=12, ny=4, nz=4, lx=3.0, dirichlet="eliminate",
+                                        load="traction_xend", x_slowest=True), "jacobi", 0.5, 60,
+     "scalar"),
+    ("box975_ns_scalar_jacobi05", dict(nx=9, ny=7, nz=5, dirichlet="eliminate", load="traction_xend"),
+     "jacobi", 0.5, 150, "ns_scalar"),
+    ("cube7_hetero_ns_scalar_jacobi", dict(nx=7, dirichlet="eliminate", heterogeneous=True,
+                                           load="random", seed=7), "jacobi", 0.5, 120, "ns_scalar"),
+    # ilu0<double>, the scalar pipelines' and ns_hybrid1's ILU (hierarchy.hpp:288-291)
+    ("box975_ns_scalar_ilu0", dict(nx=9, ny=7, nz=5, dirichlet="eliminate", load="traction_xend"),
+     "ilu0", 0.72, 150, "ns_scalar"),
+    ("cube6_keep_scalar_ilu0", dict(nx=6, dirichlet="keep_rows"), "ilu0", 0.72, 100, "scalar"),
+    ("cube7_hetero_hybrid1_ilu0", dict(nx=7, dirichlet="eliminate", heterogeneous=True,
+                                       load="random", seed=7), "ilu0", 0.72, 120, "ns_hybrid1"),
+    ("beam_xslow_ns_scalar_ilu0", dict(nx=16, ny=4, nz=4, lx=4.0, dirichlet="eliminate",
+                                       load="traction_xend", x_slowest=True), "ilu0", 0.72, 120,
+     "ns_scalar"),
 ]
-PIPE = {"block": 1, "ns_hybrid1": 3, "ns_hybrid2": 4, "ns_block": 5}
+PIPE = {"scalar": 0, "block": 1, "ns_scalar": 2, "ns_hybrid1": 3, "ns_hybrid2": 4, "ns_block": 5}
+SCALAR_PIPES = ("scalar", "ns_scalar")
 
 
 @pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
@@ -110,15 +133,19 @@ def test_setup_and_solve_parity(gpu, ref, orc, case):
     pb = gpu
     p = make_problem(pb, **kw)
     A = p.csr()
-    B = None if pipeline == "block" else p.nullspace()
+    B = None if pipeline in ("block", "scalar") else p.nullspace()
     prm = pb.AmgParams(smoother=smoother, smoother_omega=omega, coarse_enough=ce)
     h = pb.setup(A, B, pipeline, prm)
     rp = Params(smoother=SM[smoother], smoother_omega=omega, coarse_enough=ce,
                 pipeline=PIPE[pipeline])
     hr = ref.setup(A[0], A[1], A[2], A[3], B, rp)
-    ho = orc.setup(A[0], A[1], A[2], A[3], B, rp)
+    # the C restatement covers the block-storage pipelines; the scalar ones
+    # are checked against the reference alone
+    # (and ilu0<double>, the scalar ILU of ns_hybrid1)
+    scalar_ilu = pipeline == "ns_hybrid1" and smoother == "ilu0"
+    ho = None if pipeline in SCALAR_PIPES or scalar_ilu else orc.setup(A[0], A[1], A[2], A[3], B, rp)
     assert h.nlevels >= 2
-    compare_hierarchies(h, hr, ho, smoother, omega)
+    compare_hierarchies(h, hr, ho, smoother, omega, pipeline)
 
     # the explicit coarse inverse is kept unless it fails its accuracy check
     # (numerically singular coarse operator -> the reference's LU, exactly)
@@ -137,7 +164,7 @@ def test_setup_and_solve_parity(gpu, ref, orc, case):
     rng = np.random.default_rng(5)
     u0 = rng.uniform(-1, 1, f.size)
     vg = h.vcycle(f, u0)
-    vo = ho.vcycle(f)  # oracle V-cycle from zero
+    vo = ho.vcycle(f) if ho is not None else hr.vcycle(f)  # V-cycle from zero
     vz = h.vcycle(f)
     # rounding-level (FMA in the solve kernels); the numerically singular
     # coarse operator of the ill-scaled case amplifies it
@@ -210,11 +237,11 @@ def test_zero_diagonal_rejected(gpu):
 def test_unsupported_pipelines(gpu):
     pb = gpu
     p = make_problem(pb, 3, dirichlet="eliminate")
-    for pl in ("scalar", "ns_scalar"):
+    for pl in ("scalar", "ns_scalar"):  # the reference's scalar smoothers only
         with pytest.raises(pb.Unsupported):
-            pb.setup(p.csr(), p.nullspace(), pl)
-    with pytest.raises(pb.Unsupported):  # ilu0<double> is not on the B200 path
-        pb.setup(p.csr(), p.nullspace(), "ns_hybrid1", pb.AmgParams(smoother="ilu0"))
+            pb.setup(p.csr(), p.nullspace(), pl, pb.AmgParams(smoother="spai0"))
+    with pytest.raises(pb.Unsupported):  # block smoothers need block storage: block_jacobi ok,
+        pb.setup(p.csr(), p.nullspace(), "scalar", pb.AmgParams(smoother="block_jacobi"))
 
 
 def test_spmv_batch_matches_single(gpu):
