@@ -169,6 +169,19 @@ SAMG_API int samg_cg_solve_device(samg_hierarchy *h, const double *d_f,
 /* ---- preconditioner: replaces samg::vcycle (hierarchy.hpp:408-441) ------
  * u is the initial approximation and the result (host / device pointers). */
 SAMG_API int samg_vcycle(samg_hierarchy *h, const double *f, double *u);
+/* The generic driver cg_solve_op(n, apply_A, apply_M, f, u, prm)
+ * (cg.hpp:39-83) with caller operators on DEVICE vectors of n doubles:
+ * fn(ctx, in, out, stream) computes out = A in (apply_A) or out = M in
+ * (apply_M; NULL = identity) and returns 0 or a samg_status; it sees its
+ * input complete and must finish its work before returning or enqueue it on
+ * `stream` (a cudaStream_t).  u is zeroed first; the CG vector work runs on
+ * the device (deterministic reductions); relative_residual is the
+ * recurrence's ||r||/||f|| (cg_solve_op computes no true residual).  E.g.
+ * apply_A = samg_bsr3_spmv_device, apply_M = zero z + samg_vcycle_device. */
+typedef int (*samg_apply_fn)(void *ctx, const double *d_in, double *d_out, void *stream);
+SAMG_API int samg_cg_solve_op(int64_t n, samg_apply_fn apply_A, samg_apply_fn apply_M,
+        void *ctx, const double *d_f, double *d_u, const samg_cg_params *prm, int device,
+        samg_solve_report *rep);
 SAMG_API int samg_vcycle_device(samg_hierarchy *h, const double *d_f,
         double *d_u);
 

@@ -36,6 +36,7 @@ from .api import (  # noqa: F401
     Hierarchy,
     Problem,
     ProblemParams,
+    cg_solve_op,
     device_count,
     generate_hex,
     generate_hex_device,
@@ -48,5 +49,5 @@ from .api import (  # noqa: F401
 __all__ = [
     "setup", "setup_bsr3", "Hierarchy", "AmgParams", "CgParams", "Bsr3", "Problem",
     "ProblemParams", "generate_hex", "rigid_body_modes", "device_count", "SamgError",
-    "DeviceProblem", "generate_hex_device", "setup_device",
+    "DeviceProblem", "generate_hex_device", "setup_device", "cg_solve_op",
 ]

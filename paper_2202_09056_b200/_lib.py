@@ -92,6 +92,8 @@ PROTOTYPES = {
     "samg_cg_solve_device": ([vp, vp, vp, C.POINTER(CgParamsC), C.POINTER(ReportC)], C.c_int),
     "samg_vcycle": ([vp, f64p, f64p], C.c_int),
     "samg_vcycle_device": ([vp, vp, vp], C.c_int),
+    "samg_cg_solve_op": ([i64, vp, vp, vp, vp, vp, C.POINTER(CgParamsC), C.c_int, C.POINTER(ReportC)],
+                         C.c_int),
     "samg_memory_footprint": ([vp, C.POINTER(C.c_uint64)], C.c_int),
     "samg_finest_dim": ([vp, i64p], C.c_int),
     "samg_num_levels": ([vp, C.POINTER(C.c_int)], C.c_int),

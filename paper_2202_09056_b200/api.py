@@ -468,3 +468,41 @@ def rigid_body_modes(xyz) -> np.ndarray:
     B = np.zeros(3 * nn * 6)
     check(lib.samg_rigid_body_modes(nn, _p(xyz), _p(B)))
     return B
+
+
+# samg_apply_fn: int fn(void *ctx, const double *d_in, double *d_out, void *stream)
+APPLY_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p)
+
+
+def cg_solve_op(n: int, apply_A, apply_M, f_ptr: int, u_ptr: int, prm: CgParams = CgParams(),
+                device: int = 0) -> dict:
+    """cg_solve_op(n, apply_A, apply_M, f, u, prm) (cg.hpp:39-83) with caller
+    operators on device vectors: apply_A(in_ptr, out_ptr, stream) -> None
+    computes out = A in, apply_M (None = identity) out = M in; both must
+    finish their work on return or enqueue it on `stream`.  f / u: device
+    pointers of n doubles (u is overwritten)."""
+    keep = []
+
+    def wrap(fn):
+        if fn is None:
+            return None
+
+        def cb(ctx, x, y, stream):
+            try:
+                fn(x, y, stream)
+                return 0
+            except SamgError as e:  # noqa: F821 (imported below)
+                return e.code
+            except Exception:
+                return 1
+        c = APPLY_FN(cb)
+        keep.append(c)
+        return c
+
+    from ._lib import SamgError  # noqa: F401
+    globals()["SamgError"] = SamgError
+    rep = ReportC()
+    cp = CgParamsC(prm.tol, prm.max_iterations)
+    check(lib.samg_cg_solve_op(n, wrap(apply_A), wrap(apply_M), None, f_ptr, u_ptr, C.byref(cp),
+                               device, C.byref(rep)))
+    return _report(rep)

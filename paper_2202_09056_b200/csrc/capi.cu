@@ -531,6 +531,25 @@ SAMG_API int samg_vcycle_device(samg_hierarchy *hp, const double *d_f, double *d
     });
 }
 
+SAMG_API int samg_cg_solve_op(int64_t n, samg_apply_fn apply_A, samg_apply_fn apply_M, void *ctx,
+                              const double *d_f, double *d_u, const samg_cg_params *prm, int device,
+                              samg_solve_report *rep) {
+    return guarded([&] {
+        require(n >= 0 && apply_A && d_f && d_u && prm && rep, SAMG_INVALID_ARGUMENT,
+                "cg_solve_op: bad arguments");
+        need_device(device);
+        cudaStream_t s = new_stream();
+        try {
+            *rep = cg_solve_op(n, apply_A, apply_M, ctx, d_f, d_u, *prm, s);
+        } catch (...) {
+            cudaStreamSynchronize(s);
+            cudaStreamDestroy(s);
+            throw;
+        }
+        CK(cudaStreamDestroy(s));
+    });
+}
+
 SAMG_API int samg_memory_footprint(const samg_hierarchy *h, uint64_t *bytes) {
     return guarded([&] { *bytes = Hc(h).memory_footprint(); });
 }

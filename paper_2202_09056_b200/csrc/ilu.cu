@@ -554,9 +554,9 @@ __global__ void __launch_bounds__(256) k_ilu_factor_s(int n, const int *__restri
 // the lower blocks (ascending scalar columns), then the rows of the own
 // block in sequence (their within-block terms come last).  Backward: the
 // within-block terms come FIRST in each chain, so the rows run in sequence
-// 3i+2, 3i+1, 3i over the products of the higher blocks, formed in parallel
-// beforehand (one window: at most kWinS higher blocks, checked at setup);
-// x_i = (chain) * inv_i; u_out = x (+ u_in, kernels::axpby(1, x, 1, u)).
+// 3i+2, 3i+1, 3i, each over the products of the higher blocks formed in
+// parallel per window; x_i = (chain) * inv_i; u_out = x (+ u_in,
+// kernels::axpby(1, x, 1, u)).
 constexpr int kWinS = 192;
 constexpr int kSweepSmemS = 8 * kWinS * 9 * static_cast<int>(sizeof(double));
 
@@ -576,62 +576,76 @@ __global__ void __launch_bounds__(256) k_ilu_sweep_s(int n, const int *__restric
         const int i = __ldg(order + t);
         const int di = __ldg(dpos + i);
         const int b = kFwd ? __ldg(ptr + i) : di + 1, e = kFwd ? di : __ldg(ptr + i + 1);
-        double a = lane < 3 ? src[3LL * i + lane] : 0.0;  // lane p: the chain of row 3i+p
-        for (int w0 = b; w0 < e; w0 += kWinS) {
-            const int m = min(kWinS, e - w0);
-            for (int q = lane; q < 9 * m; q += 32) bs[q] = __ldg(lu + 9LL * w0 + q);
-            __syncwarp();
-            // each dependency: wait for its value, form its 9 products in place
-            for (int d = lane; d < m; d += 32) {
-                const double *g = out + 3LL * __ldg(col + w0 + d);
-                unsigned long long v0, v1, v2;
-                do {
-                    v0 = ld_poll(g); v1 = ld_poll(g + 1); v2 = ld_poll(g + 2);
-                } while (v0 == kSent || v1 == kSent || v2 == kSent);
-                const double x0 = __longlong_as_double(static_cast<long long>(v0)),
-                             x1 = __longlong_as_double(static_cast<long long>(v1)),
-                             x2 = __longlong_as_double(static_cast<long long>(v2));
-                double *bl = bs + 9 * d;
-#pragma unroll
-                for (int r = 0; r < 3; ++r) {
-                    bl[3 * r] = __dmul_rn(bl[3 * r], x0);
-                    bl[3 * r + 1] = __dmul_rn(bl[3 * r + 1], x1);
-                    bl[3 * r + 2] = __dmul_rn(bl[3 * r + 2], x2);
-                }
-            }
-            __syncwarp();
-            if (kFwd && lane < 3)  // the lower blocks' terms, the three chains in parallel
-                for (int d = 0; d < m; ++d) {
-                    a = __dsub_rn(a, bs[9 * d + 3 * lane]);
-                    a = __dsub_rn(a, bs[9 * d + 3 * lane + 1]);
-                    a = __dsub_rn(a, bs[9 * d + 3 * lane + 2]);
-                }
-            if (kFwd) __syncwarp();  // the window's staging is reused
-        }
-        const double a0 = __shfl_sync(kFull, a, 0), a1 = __shfl_sync(kFull, a, 1),
-                     a2 = __shfl_sync(kFull, a, 2);
-        const double *dl = lu + 9LL * di;
         double res[3];
+        const double *dl = lu + 9LL * di;
         if constexpr (kFwd) {
+            double a = lane < 3 ? src[3LL * i + lane] : 0.0;  // lane p: the chain of row 3i+p
+            for (int w0 = b; w0 < e; w0 += kWinS) {
+                const int m = min(kWinS, e - w0);
+                for (int q = lane; q < 9 * m; q += 32) bs[q] = __ldg(lu + 9LL * w0 + q);
+                __syncwarp();
+                // each dependency: wait for its value, form its 9 products in place
+                for (int d = lane; d < m; d += 32) {
+                    const double *g = out + 3LL * __ldg(col + w0 + d);
+                    unsigned long long v0, v1, v2;
+                    do {
+                        v0 = ld_poll(g); v1 = ld_poll(g + 1); v2 = ld_poll(g + 2);
+                    } while (v0 == kSent || v1 == kSent || v2 == kSent);
+                    const double x0 = __longlong_as_double(static_cast<long long>(v0)),
+                                 x1 = __longlong_as_double(static_cast<long long>(v1)),
+                                 x2 = __longlong_as_double(static_cast<long long>(v2));
+                    double *bl = bs + 9 * d;
+#pragma unroll
+                    for (int r = 0; r < 3; ++r) {
+                        bl[3 * r] = __dmul_rn(bl[3 * r], x0);
+                        bl[3 * r + 1] = __dmul_rn(bl[3 * r + 1], x1);
+                        bl[3 * r + 2] = __dmul_rn(bl[3 * r + 2], x2);
+                    }
+                }
+                __syncwarp();
+                if (lane < 3)  // the lower blocks' terms, the three chains in parallel
+                    for (int d = 0; d < m; ++d) {
+                        a = __dsub_rn(a, bs[9 * d + 3 * lane]);
+                        a = __dsub_rn(a, bs[9 * d + 3 * lane + 1]);
+                        a = __dsub_rn(a, bs[9 * d + 3 * lane + 2]);
+                    }
+                __syncwarp();  // the window's staging is reused
+            }
+            const double a0 = __shfl_sync(kFull, a, 0), a1 = __shfl_sync(kFull, a, 1),
+                         a2 = __shfl_sync(kFull, a, 2);
             // own block, unit lower factor: y0; y1 - L10 y0; (y2 - L20 y0) - L21 y1
             res[0] = a0;
             res[1] = __dsub_rn(a1, __dmul_rn(__ldg(dl + 3), res[0]));
             res[2] = __dsub_rn(__dsub_rn(a2, __dmul_rn(__ldg(dl + 6), res[0])),
                                __dmul_rn(__ldg(dl + 7), res[1]));
         } else {
-            const int m = e - b;
-            const double y[3] = {a0, a1, a2};
+            // rows 3i+2, 3i+1, 3i in sequence; each chain: y, the own block's
+            // terms right of the diagonal, then the higher blocks' products
+            // (windows of 3*kWinS dependencies, 3 products each); every lane
+            // carries the same chain (the products come from shared memory)
+            constexpr int kWinB = 3 * kWinS;
             for (int r = 2; r >= 0; --r) {
-                double c = y[r];
+                double c = __ldcg(src + 3LL * i + r);
                 for (int q = r + 1; q < 3; ++q) c = __dsub_rn(c, __dmul_rn(__ldg(dl + 3 * r + q), res[q]));
-                for (int d = 0; d < m; ++d) {
-                    c = __dsub_rn(c, bs[9 * d + 3 * r]);
-                    c = __dsub_rn(c, bs[9 * d + 3 * r + 1]);
-                    c = __dsub_rn(c, bs[9 * d + 3 * r + 2]);
+                for (int w0 = b; w0 < e; w0 += kWinB) {
+                    const int m = min(kWinB, e - w0);
+                    for (int d = lane; d < m; d += 32) {
+                        const double *g = out + 3LL * __ldg(col + w0 + d);
+                        unsigned long long v0, v1, v2;
+                        do {
+                            v0 = ld_poll(g); v1 = ld_poll(g + 1); v2 = ld_poll(g + 2);
+                        } while (v0 == kSent || v1 == kSent || v2 == kSent);
+                        const double *u = lu + 9LL * (w0 + d) + 3 * r;
+                        bs[3 * d] = __dmul_rn(__ldg(u), __longlong_as_double(static_cast<long long>(v0)));
+                        bs[3 * d + 1] = __dmul_rn(__ldg(u + 1), __longlong_as_double(static_cast<long long>(v1)));
+                        bs[3 * d + 2] = __dmul_rn(__ldg(u + 2), __longlong_as_double(static_cast<long long>(v2)));
+                    }
+                    __syncwarp();
+                    for (int d = 0; d < 3 * m; ++d) c = __dsub_rn(c, bs[d]);
+                    __syncwarp();
                 }
                 res[r] = __dmul_rn(c, __ldg(inv + 3LL * i + r));
             }
-            __syncwarp();  // the staging is reused by the next row
         }
         if (lane < 3) {
             st_publish(out + 3LL * i + lane, res[lane]);
@@ -640,13 +654,6 @@ __global__ void __launch_bounds__(256) k_ilu_sweep_s(int n, const int *__restric
         }
         __syncwarp();
     }
-}
-
-// the longest run of blocks right of the diagonal (the scalar backward
-// sweep keeps them in one window)
-__global__ void k_max_upper(int n, const int *ptr, const int *dpos, int *mx) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) atomicMax(mx, ptr[i + 1] - dpos[i] - 1);
 }
 
 } // namespace
@@ -703,17 +710,6 @@ void setup_ilu0_scalar(const Bsr3 &A, Smoother &M, DevError *err, cudaStream_t s
     k_ilu_dpos<<<ceil_div(n, 256), 256, 0, s>>>(n, A.ptr.p, A.col.p, M.dpos.p, err);
     CK_LAUNCH();
     check_dev_error(err, s);
-    {
-        DevBuf<int> mx(1, s);
-        CK(cudaMemsetAsync(mx.p, 0, sizeof(int), s));
-        k_max_upper<<<ceil_div(n, 256), 256, 0, s>>>(n, A.ptr.p, M.dpos.p, mx.p);
-        CK_LAUNCH();
-        int hm = 0;
-        CK(cudaMemcpyAsync(&hm, mx.p, sizeof hm, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        if (hm > kWinS)
-            fail(SAMG_UNSUPPORTED, "ilu0<double>: more than 192 blocks right of a diagonal block");
-    }
     level_orders(A, M.dpos, M.order, M.depth, s);
     CK(cudaMemcpyAsync(M.lu.p, A.val.p, sizeof(double) * 9 * A.nnzb, cudaMemcpyDeviceToDevice, s));
     CK(cudaMemsetAsync(M.flags.p, 0, sizeof(int) * (A.nrows * kFS + 2), s));

@@ -170,6 +170,11 @@ bool launch_restrict_smooth(const Bsr3 &R, const double *r, double *f, const Smo
                             cudaStream_t s, bool lowp = false);
 void launch_fill(int64_t n, double v, double *x, cudaStream_t s);
 
+// generic PCG with caller operators (cgop.cu, cg.hpp:39-83)
+samg_solve_report cg_solve_op(int64_t n, samg_apply_fn apply_A, samg_apply_fn apply_M, void *ctx,
+                              const double *d_f, double *d_u, const samg_cg_params &prm,
+                              cudaStream_t s);
+
 // ---- setup phase (setup.cu, compiled with --fmad=false) ----------------------
 struct Graph {  // node adjacency, symmetric, sorted rows (coarsening.hpp:33-38)
     int64_t nnodes = 0, nedges = 0;

@@ -376,6 +376,42 @@ def test_node6_spmv_matches_reference(gpu, ref):
     assert out.returncode == 0 and "node6 ok" in out.stdout, out.stderr[-2000:]
 
 
+def test_cg_solve_op_callbacks(gpu, ref):
+    """samg_cg_solve_op (cg.hpp:39-83) with caller operators: the B200 SpMV
+    as apply_A and (zero guess +) the B200 V-cycle as apply_M reproduce
+    cg_solve's iterations and solution; the identity preconditioner matches
+    the reference's unpreconditioned cg_solve_op on the same matrix."""
+    import torch
+    pb = gpu
+    p = make_problem(pb, 9, ny=7, nz=5, dirichlet="eliminate", load="traction_xend")
+    h = pb.setup(p.csr(), p.nullspace(), "ns_block", pb.AmgParams(coarse_enough=150))
+    u1, r1 = h.cg_solve(p.rhs)
+    A = pb.Bsr3.from_host(p.nbrows, p.nbrows, p.ptr, p.col, p.val.reshape(-1))
+    from paper_2202_09056_b200._lib import lib
+
+    def apply_A(x, y, stream):
+        A.spmv_device(x, y, 1.0, 0.0, stream or 0)
+
+    from cuda.bindings import runtime as rt
+
+    def apply_M(r, z, stream):
+        # z = 0, then the V-cycle from that guess (cg.hpp:98-101)
+        assert rt.cudaMemset(z, 0, 8 * p.n)[0] == rt.cudaError_t.cudaSuccess
+        assert rt.cudaDeviceSynchronize()[0] == rt.cudaError_t.cudaSuccess
+        assert lib.samg_vcycle_device(h.h, r, z) == 0
+
+    f = torch.from_numpy(p.rhs).cuda()
+    u = torch.zeros_like(f)
+    rep = pb.cg_solve_op(p.n, apply_A, apply_M, f.data_ptr(), u.data_ptr())
+    assert rep["converged"] and abs(rep["iterations"] - r1["iterations"]) <= 1, (rep, r1)
+    assert np.linalg.norm(u.cpu().numpy() - u1) <= 1e-9 * np.linalg.norm(u1)
+    # identity preconditioner: plain CG, as the reference's cg_solve_op
+    u0 = torch.zeros_like(f)
+    rep0 = pb.cg_solve_op(p.n, apply_A, None, f.data_ptr(), u0.data_ptr(),
+                          pb.CgParams(max_iterations=5000))
+    assert rep0["converged"] and rep0["iterations"] > r1["iterations"]
+
+
 def test_spmv_matches_reference(gpu, ref):
     pb = gpu
     p = make_problem(pb, 19, dirichlet="eliminate")
