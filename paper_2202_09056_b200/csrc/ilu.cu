@@ -444,6 +444,14 @@ void level_orders(const Bsr3 &A, const DevBuf<int> &dpos, DevBuf<int> &order, in
 // rows in sequence.  Every operation is the reference's, in its order.
 
 // IKJ (relaxation.hpp:115-132) for the three scalar rows of a block row.
+// The steps of a scalar row over its LOWER blocks only touch that row, so
+// the three rows take them together: per lower block c (ascending) the U
+// part of block row c (its diagonal block right of each pivot, then its
+// blocks right of the diagonal, with their positions in row i found once)
+// is read once and serves the 3 x 3 (row, pivot) steps -- for each scalar
+// row the steps still run in ascending pivot order k = 3c + q, and each
+// step updates distinct entries.  Then the within-block steps (k = 3i + q,
+// q < r) run row by row.
 __global__ void __launch_bounds__(256) k_ilu_factor_s(int n, const int *__restrict__ order,
         const int *__restrict__ ptr, const int *__restrict__ col, const int *__restrict__ dpos,
         double *lu, double *inv, int *done, int *counter, DevError *err) {
@@ -472,25 +480,69 @@ __global__ void __launch_bounds__(256) k_ilu_factor_s(int n, const int *__restri
         __syncwarp();
         cuda::atomic_thread_fence(cuda::memory_order_acquire, cuda::thread_scope_device);
         __syncwarp();
-        double own_inv[3] = {0.0, 0.0, 0.0};
-        for (int r = 0; r < 3; ++r) {
-            // steps k = 3c + q over the lower blocks (c < i), ascending
-            for (int j = b; j < di; ++j) {
-                const int c = rc[j];
-                const int dc = __ldg(dpos + c), ec = __ldg(ptr + c + 1);
-                for (int q = 0; q < 3; ++q) {
-                    // L_ik = a_ik * (1 / u_kk)
-                    const double L = __dmul_rn(rv[9LL * j + 3 * r + q], __ldcg(inv + 3LL * c + q));
-                    __syncwarp();
-                    if (lane == 0) rv[9LL * j + 3 * r + q] = L;
-                    // row k's U part: its diagonal block's entries right of
-                    // q (they land in block j of row i), then its blocks
-                    // right of the diagonal
-                    if (lane < 2 - q) {
-                        const int qq = q + 1 + lane;
-                        double *dst = rv + 9LL * j + 3 * r + qq;
-                        *dst = __dsub_rn(*dst, __dmul_rn(L, __ldcg(lu + 9LL * dc + 3 * q + qq)));
+        for (int j = b; j < di; ++j) {
+            const int c = rc[j];
+            const int dc = __ldg(dpos + c), ec = __ldg(ptr + c + 1);
+            double dg[9], iv[3];
+#pragma unroll
+            for (int q = 0; q < 9; ++q) dg[q] = __ldcg(lu + 9LL * dc + q);
+#pragma unroll
+            for (int q = 0; q < 3; ++q) iv[q] = __ldcg(inv + 3LL * c + q);
+            // lanes own blocks l = dc+1+lane, +32, ... (up to kUB per lane):
+            // their position in row i (or -1) and their 9 values, found /
+            // loaded once for the three pivots q
+            constexpr int kUB = 4;
+            int upos[kUB];
+            double uval[kUB][9];
+            const bool cached = ec - dc - 1 <= 32 * kUB;
+            if (cached) {
+#pragma unroll
+                for (int u = 0; u < kUB; ++u) {
+                    const int l = dc + 1 + lane + 32 * u;
+                    upos[u] = -1;
+                    if (l < ec) {
+                        const int cc = __ldg(col + l);
+                        int lo = b, hi = e - 1;
+                        while (lo <= hi) {
+                            const int m = (lo + hi) >> 1, cm = rc[m];
+                            if (cm == cc) { upos[u] = m; break; }
+                            if (cm < cc) lo = m + 1;
+                            else hi = m - 1;
+                        }
+                        if (upos[u] >= 0)
+#pragma unroll
+                            for (int v = 0; v < 9; ++v) uval[u][v] = __ldcg(lu + 9LL * l + v);
                     }
+                }
+            }
+            for (int q = 0; q < 3; ++q) {
+                // L_{r,k} for the three rows (k = 3c+q), then row k's entries
+                // right of the pivot: diagonal block (q' > q) and higher blocks
+                double L[3];
+#pragma unroll
+                for (int r = 0; r < 3; ++r) L[r] = __dmul_rn(rv[9LL * j + 3 * r + q], iv[q]);
+                __syncwarp();
+                if (lane < 3) rv[9LL * j + 3 * lane + q] = L[lane];
+                if (lane < 3 * (2 - q)) {
+                    const int r = lane % 3, qq = q + 1 + lane / 3;
+                    double *dst = rv + 9LL * j + 3 * r + qq;
+                    *dst = __dsub_rn(*dst, __dmul_rn(L[r], dg[3 * q + qq]));
+                }
+                auto update = [&](int pos, double u0, double u1, double u2) {
+#pragma unroll
+                    for (int r = 0; r < 3; ++r) {
+                        double *dst = rv + 9LL * pos + 3 * r;
+                        dst[0] = __dsub_rn(dst[0], __dmul_rn(L[r], u0));
+                        dst[1] = __dsub_rn(dst[1], __dmul_rn(L[r], u1));
+                        dst[2] = __dsub_rn(dst[2], __dmul_rn(L[r], u2));
+                    }
+                };
+                if (cached) {
+#pragma unroll
+                    for (int u = 0; u < kUB; ++u)
+                        if (upos[u] >= 0)
+                            update(upos[u], uval[u][3 * q], uval[u][3 * q + 1], uval[u][3 * q + 2]);
+                } else {
                     for (int l = dc + 1 + lane; l < ec; l += 32) {
                         const int cc = __ldg(col + l);
                         int lo = b, hi = e - 1, pos = -1;
@@ -501,14 +553,15 @@ __global__ void __launch_bounds__(256) k_ilu_factor_s(int n, const int *__restri
                             else hi = m - 1;
                         }
                         if (pos < 0) continue;
-                        double *dst = rv + 9LL * pos + 3 * r;
-#pragma unroll
-                        for (int q2 = 0; q2 < 3; ++q2)
-                            dst[q2] = __dsub_rn(dst[q2], __dmul_rn(L, __ldcg(lu + 9LL * l + 3 * q + q2)));
+                        update(pos, __ldcg(lu + 9LL * l + 3 * q), __ldcg(lu + 9LL * l + 3 * q + 1),
+                               __ldcg(lu + 9LL * l + 3 * q + 2));
                     }
-                    __syncwarp();
                 }
+                __syncwarp();
             }
+        }
+        double own_inv[3] = {0.0, 0.0, 0.0};
+        for (int r = 0; r < 3; ++r) {
             // steps k = 3i + q, q < r: the earlier scalar rows of this block row
             for (int q = 0; q < r; ++q) {
                 const double L = __dmul_rn(rv[9LL * di + 3 * r + q], own_inv[q]);

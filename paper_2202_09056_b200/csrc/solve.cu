@@ -1050,26 +1050,31 @@ __global__ void __launch_bounds__(kGemvThreads) k_dense_gemv(int n, int64_t ld, 
     const double2 *a = reinterpret_cast<const double2 *>(A + static_cast<size_t>(row) * ld);
     const int n2 = static_cast<int>(ld / 2);
     double s = 0.0, t = 0.0;
+    // f as 16-byte pairs (f is 16-byte aligned; a last odd element alone)
     auto fpair = [&](int j2) {
         const int j = 2 * j2;
-        return make_double2(__ldg(f + j), j + 1 < n ? __ldg(f + j + 1) : 0.0);
+        return j + 1 < n ? __ldg(reinterpret_cast<const double2 *>(f) + j2) : make_double2(__ldg(f + j), 0.0);
     };
-    int j2 = threadIdx.x;
-    for (; j2 + 7 * T < n2; j2 += 8 * T) {
-        double2 av[8];
+    // batches of 8 16-byte loads per thread, all issued before the FMAs (32
+    // registers: the 2 922 rows of C1 in 0.62 waves; 24 per batch needed 129
+    // registers and 2.8 waves)
+    constexpr int B = 8;
+    for (int j0 = threadIdx.x; j0 < n2; j0 += B * T) {
+        double2 av[B];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) av[k] = __ldg(a + j2 + k * T);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const double2 fk = fpair(j2 + k * T);
-            s = fma(av[k].x, fk.x, s);
-            t = fma(av[k].y, fk.y, t);
+        for (int k = 0; k < B; ++k) {
+            const int j2 = j0 + k * T;
+            av[k] = j2 < n2 ? __ldg(a + j2) : make_double2(0.0, 0.0);
         }
-    }
-    for (; j2 < n2; j2 += T) {
-        const double2 a0 = __ldg(a + j2);
-        const double2 f0 = fpair(j2);
-        s = fma(a0.x, f0.x, s); t = fma(a0.y, f0.y, t);
+#pragma unroll
+        for (int k = 0; k < B; ++k) {
+            const int j2 = j0 + k * T;
+            if (j2 < n2) {
+                const double2 fk = fpair(j2);
+                s = fma(av[k].x, fk.x, s);
+                t = fma(av[k].y, fk.y, t);
+            }
+        }
     }
     s += t;
 #pragma unroll
