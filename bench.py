@@ -142,7 +142,7 @@ class ClockSampler:
 
 def ncu_traffic():
     """dram bytes per launch of the SpMV kernel from the committed ncu capture."""
-    path = os.path.join(ROOT, "profiles", "ncu_spmv_c1.json")
+    path = os.path.join(ROOT, "profiles", "r02_ncu_full_spmv_tma_c1.json")
     if os.path.exists(path):
         with open(path) as f:
             return json.load(f).get("dram_bytes_per_launch")
@@ -624,7 +624,7 @@ def run_b200_dist(args, rank, world, local, dist):
             "roofline": {"bound": "hbm", "achieved": gb_rank, "peak": peak, "unit": "GB/s",
                          "frac": gb_rank / peak, "traffic": ncu_traffic(),
                          "peak_source": peak_src,
-                         "kernel": "k_bsr3_rows<4,EpiSpmv> interior+boundary (solve.cu)"},
+                         "kernel": "k_bsr3_tma<8,8,2,false,EpiSpmv> on the interior row view + k_bsr3 on the boundary rows (dist.cu, solve.cu)"},
             "e2e": {"value": e2e_val, "unit": "GB/s", "h2d_bytes_per_step": 8 * 3 * nloc * world,
                     "d2h_bytes_per_step": 8 * 3 * nloc * world,
                     "path": "samg_dist_pack/spmv (C-ABI) + torch.distributed NCCL halo"},

@@ -82,8 +82,18 @@ int main() {
     try { setup(A, dense_columns(12, 6), pipeline::ns_block, prm); } catch (const bad_nullspace_shape &) { thrown = true; }
     EXPECT(thrown);
     thrown = false;
-    try { setup(A, B, pipeline::ns_scalar, prm); } catch (const unsupported &) { thrown = true; }
+    {   // block smoothers are defined for block pipelines only
+        amg_params ps = prm;
+        ps.smoother = smoother_kind::spai0;
+        try { setup(A, B, pipeline::ns_scalar, ps); } catch (const unsupported &) { thrown = true; }
+    }
     EXPECT(thrown);
+    // ns_scalar with its own ilu0<double> smoother (hierarchy.hpp:298-330)
+    hierarchy Hs = setup(A, B, pipeline::ns_scalar, prm);
+    std::vector<double> us(n, 0.0);
+    solve_report rs = cg_solve(Hs, rhs, us, cg_params{});
+    EXPECT(rs.converged && rs.relative_residual <= 1e-8);
+    EXPECT(rs.variant == pipeline::ns_scalar);
     thrown = false;
     try { std::vector<double> bad(5); cg_solve(H, bad, u, cg_params{}); } catch (const dimension_mismatch &) { thrown = true; }
     EXPECT(thrown);
