@@ -4,6 +4,7 @@
 // kernels on one stream and reads back sizes and the CG residual.
 #include "hierarchy.cuh"
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstddef>
@@ -48,6 +49,7 @@ Hierarchy::~Hierarchy() {
     lu.X.release(); lu.Lt.release(); lu.perm.release();
     r.release(); z.release(); p.release(); q.release();
     fbuf.release(); ubuf.release(); partials.release(); sc.release(); err.release();
+    tail_ph.release(); tail_bar.release();
     pinned_small_free(sc_host);
     pinned_small_free(sc_stage);
     if (cg_exec) cudaGraphExecDestroy(cg_exec);
@@ -336,6 +338,7 @@ Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int6
     CK(cudaMemsetAsync(H->sc.p, 0, sizeof(CgScalars), s));
     H->sc_host = static_cast<CgScalars *>(pinned_small_alloc(sizeof(CgScalars)));
     H->sc_stage = static_cast<CgScalars *>(pinned_small_alloc(sizeof(CgScalars)));
+    H->build_tail();
     CK(cudaStreamSynchronize(s));
     mark("workspace", L - 1);
     H->setup_seconds = now_s() - t_start;
@@ -389,6 +392,128 @@ void choose_coarse_solver(Hierarchy &H, DevError *err, cudaStream_t s, bool inve
     H.Ainv.release();
 }
 
+// The V-cycle's small levels as one persistent launch (k_vtail, solve.cu).
+// tail_start t = the first level >= 1 whose operator is at most
+// SAMG_VTAIL_MB (default 96) MB; the phases replay vcycle_from's level
+// loop for levels t..L-1 exactly (same kernels' arithmetic, same buffers,
+// same ping-pong), starting with level t-1's restriction and ending with its
+// prolongation, whose target (level t-1's current iterate) is passed at
+// launch.  Needs block / point smoothers on the tail levels, the explicit
+// coarse inverse and the fp64 V-cycle; SAMG_VTAIL=0 disables.
+void Hierarchy::build_tail() {
+    static const int on = [] {
+        const char *e = std::getenv("SAMG_VTAIL");
+        return e ? std::atoi(e) : 0;
+    }();
+    static const double mb = [] {
+        const char *e = std::getenv("SAMG_VTAIL_MB");
+        return e ? std::atof(e) : 96.0;
+    }();
+    tail_nph = 0;
+    const size_t L = levels.size();
+    if (!on || L < 2 || coarse_lu || !Ainv.p || prm.vcycle_precision == SAMG_PRECISION_MIXED) return;
+    size_t t = L - 1;
+    for (size_t i = 1; i + 1 < L; ++i)
+        if (levels[i].A.nnzb * 76.0 <= mb * 1e6) { t = i; break; }
+    for (size_t i = t; i + 1 < L; ++i)
+        if (levels[i].M.kind != SM_POINT && levels[i].M.kind != SM_BLOCK) return;
+    const int64_t ld = dense_ld(nc);
+    const size_t smem = static_cast<size_t>(8 * ld) <= 96 * 1024 ? static_cast<size_t>(8 * ld) : 0;
+    const int grid = vtail_grid(smem);
+    if (grid <= 0) return;
+    const int64_t threads = static_cast<int64_t>(grid) * 1024;  // kVtThreads per CTA
+    std::vector<VPhase> ph;
+    auto mat = [&](int kind, const Bsr3 &A, const double *x) {
+        VPhase v{};
+        v.kind = kind;
+        v.nrows = static_cast<int>(A.nrows);
+        v.G = vtail_group(A.nrows, A.nnzb, threads);
+        v.ptr = A.ptr.p; v.col = A.col.p; v.val = A.val.p; v.x = x;
+        v.alpha = 1.0;
+        return v;
+    };
+    auto restrict_into = [&](size_t i) {  // level i's residual -> level i+1 (+ first sweep)
+        Level &lv = levels[i], &nx = levels[i + 1];
+        if (i + 2 < L && prm.pre_sweeps > 0) {
+            VPhase v = mat(nx.M.kind == SM_BLOCK ? VP_RSMOOTH_B : VP_RSMOOTH_P, lv.R, lv.r.p);
+            v.out = nx.f.p; v.out2 = nx.u.p; v.m = nx.M.data.p;
+            ph.push_back(v);
+            return true;
+        }
+        VPhase v = mat(VP_SPMV, lv.R, lv.r.p);
+        v.out = nx.f.p; v.beta = 0.0;
+        ph.push_back(v);
+        return false;
+    };
+    std::vector<double *> cur(L, nullptr);
+    bool pre = restrict_into(t - 1);
+    for (size_t i = t; i + 1 < L; ++i) {
+        Level &lv = levels[i];
+        double *a = lv.u.p, *b = lv.t.p;
+        int sweeps = prm.pre_sweeps;
+        if (sweeps > 0) {
+            if (!pre) return;  // (not reached: block / point smoothers fuse it)
+            --sweeps;
+        } else {
+            VPhase v{};
+            v.kind = VP_FILL; v.nrows = static_cast<int>(lv.A.nrows); v.out = a; v.alpha = 0.0;
+            ph.push_back(v);
+        }
+        for (; sweeps > 0; --sweeps) {
+            VPhase v = mat(lv.M.kind == SM_BLOCK ? VP_SMOOTH_B : VP_SMOOTH_P, lv.A, a);
+            v.f = lv.f.p; v.m = lv.M.data.p; v.out = b;
+            ph.push_back(v);
+            std::swap(a, b);
+        }
+        VPhase r = mat(VP_RESIDUAL, lv.A, a);
+        r.f = lv.f.p; r.out = lv.r.p;
+        ph.push_back(r);
+        pre = restrict_into(i);
+        cur[i] = a;
+    }
+    {
+        VPhase g{};
+        g.kind = VP_GEMV; g.nrows = static_cast<int>(nc); g.ld = ld; g.val = Ainv.p;
+        g.x = levels[L - 1].f.p; g.out = levels[L - 1].u.p;
+        ph.push_back(g);
+        cur[L - 1] = levels[L - 1].u.p;
+    }
+    for (size_t ii = L - 1; ii-- > t;) {
+        Level &lv = levels[ii];
+        double *a = cur[ii];
+        double *b = (a == lv.u.p) ? lv.t.p : lv.u.p;
+        VPhase pr = mat(VP_SPMV, lv.P, cur[ii + 1]);
+        pr.out = a; pr.beta = 1.0;
+        ph.push_back(pr);
+        for (int sw = prm.post_sweeps; sw > 0; --sw) {
+            VPhase v = mat(lv.M.kind == SM_BLOCK ? VP_SMOOTH_B : VP_SMOOTH_P, lv.A, a);
+            v.f = lv.f.p; v.m = lv.M.data.p; v.out = b;
+            ph.push_back(v);
+            std::swap(a, b);
+        }
+        cur[ii] = a;
+    }
+    {
+        VPhase pr = mat(VP_SPMV, levels[t - 1].P, cur[t]);
+        pr.beta = 1.0; pr.last_out = 1;
+        ph.push_back(pr);
+    }
+    cudaStream_t s = stream;
+    tail_ph.alloc(ph.size(), s);
+    CK(cudaMemcpyAsync(tail_ph.p, ph.data(), sizeof(VPhase) * ph.size(), cudaMemcpyHostToDevice, s));
+    tail_bar.alloc(2, s);
+    CK(cudaMemsetAsync(tail_bar.p, 0, 2 * sizeof(unsigned), s));
+    CK(cudaStreamSynchronize(s));
+    tail_nph = static_cast<int>(ph.size());
+    if (std::getenv("SAMG_VTAIL_TRACE")) {
+        tail_trace.alloc(2 * ph.size() + 1 + static_cast<size_t>(grid) * (ph.size() + 1), s);
+        CK(cudaMemsetAsync(tail_trace.p, 0, tail_trace.bytes(), s));
+    }
+    tail_grid = grid;
+    tail_start = t;
+    tail_smem = smem;
+}
+
 void Hierarchy::coarse_solve(const double *f, double *u) {
     if (coarse_lu) launch_lu_solve(lu, f, u, stream);
     else launch_dense_gemv(nc, Ainv.p, f, u, stream);
@@ -414,7 +539,7 @@ bool Hierarchy::vcycle_from(size_t start, const double *f0, double *u0, bool zer
         coarse_solve(f0, u0);
         return false;
     }
-    bool fused = false;
+    bool fused = false, tail_used = false;
     std::vector<double *> cur(L);
     // pre: the first sweep from a zero guess of this level was fused into
     // the kernel that produced its f (u = M f already in lv.u)
@@ -439,6 +564,14 @@ bool Hierarchy::vcycle_from(size_t start, const double *f0, double *u0, bool zer
             std::swap(a, b);
         }
         launch_residual(lv.A, fi, a, lv.r.p, s, lowp);
+        if (tail_nph && i + 1 == tail_start) {
+            // levels i+1 .. L-1 and the prolongation into `a` in one launch
+            launch_vtail(tail_ph.p, tail_nph, tail_bar.p, tail_grid, tail_smem, dense_ld(nc), a, s,
+                         tail_trace.p);
+            cur[i] = a;
+            tail_used = true;
+            break;
+        }
         // restriction, fused with the next level's first sweep from zero
         // when that level has a block-diagonal smoother
         Level &nx = levels[i + 1];
@@ -448,14 +581,16 @@ bool Hierarchy::vcycle_from(size_t start, const double *f0, double *u0, bool zer
         if (!pre) launch_spmv(lv.R, 1.0, lv.r.p, 0.0, nx.f.p, s, lowp);
         cur[i] = a;
     }
-    coarse_solve(levels[L - 1].f.p, levels[L - 1].u.p);
-    cur[L - 1] = levels[L - 1].u.p;
-    for (size_t ii = L - 1; ii-- > start;) {
+    if (!tail_used) {
+        coarse_solve(levels[L - 1].f.p, levels[L - 1].u.p);
+        cur[L - 1] = levels[L - 1].u.p;
+    }
+    for (size_t ii = tail_used ? tail_start : L - 1; ii-- > start;) {
         Level &lv = levels[ii];
         const double *fi = ii == start ? f0 : lv.f.p;
         double *a = cur[ii];
         double *b = (a == lv.u.p) ? lv.t.p : lv.u.p;
-        launch_spmv(lv.P, 1.0, cur[ii + 1], 1.0, a, s, lowp);
+        if (!(tail_used && ii + 1 == tail_start)) launch_spmv(lv.P, 1.0, cur[ii + 1], 1.0, a, s, lowp);
         for (int sw = prm.post_sweeps; sw > 0; --sw) {
             const bool last0 = ii == start && sw == 1;
             double *out = last0 ? u0 : b;
@@ -608,6 +743,24 @@ samg_solve_report Hierarchy::cg(const double *d_f, double *d_u, const samg_cg_pa
     rep.relative_residual = std::sqrt(sc_host->rr) / norm_f;
     rep.preconditioner_bytes = memory_footprint();
     rep.solve_seconds = now_s() - t0;
+    if (tail_trace.p) {  // the last tail launch: per phase, CTA 0's end / release and the
+                         // spread of the CTAs' phase ends (us from CTA 0's start)
+        std::vector<unsigned long long> t(tail_trace.n);
+        CK(cudaMemcpy(t.data(), tail_trace.p, tail_trace.bytes(), cudaMemcpyDeviceToHost));
+        const int np = tail_nph, g = tail_grid;
+        const unsigned long long t0 = t[2 * np];
+        const unsigned long long *pe = t.data() + 2 * np + 1;  // [k * g + cta], k = np: start
+        std::fprintf(stderr, "vtail trace (%d phases, grid %d)\n", np, g);
+        for (int k = 0; k <= np; ++k) {
+            std::vector<std::pair<double, int>> v;
+            for (int b = 0; b < g; ++b) v.push_back({(static_cast<double>(pe[k * g + b]) - t0) * 1e-3, b});
+            std::sort(v.begin(), v.end());
+            std::fprintf(stderr, "  %s %d: release %.2f  ends min %.2f med %.2f p90 %.2f max %.2f (cta %d, %d, %d)\n",
+                         k < np ? "phase" : "start", k, k < np ? (t[2 * k + 1] - t0) * 1e-3 : 0.0,
+                         v[0].first, v[g / 2].first, v[g * 9 / 10].first, v[g - 1].first, v[g - 1].second,
+                         v[g - 2].second, v[g - 3].second);
+        }
+    }
     return rep;
 }
 

@@ -40,6 +40,15 @@ struct Hierarchy {
     CgScalars *sc_stage = nullptr; // pinned staging for loop parameters
     cudaGraphExec_t cg_exec = nullptr;  // device-resident CG loop (while node)
     void build_cg_graph();
+    // V-cycle tail (solve.cu k_vtail): the levels >= tail_start, the coarse
+    // solve and the prolongation into level tail_start - 1 in one
+    // cooperative launch (tail_nph == 0: not used)
+    DevBuf<VPhase> tail_ph;
+    DevBuf<unsigned> tail_bar;
+    int tail_nph = 0, tail_grid = 0;
+    size_t tail_start = 0, tail_smem = 0;
+    DevBuf<unsigned long long> tail_trace;  // SAMG_VTAIL_TRACE=1: per-phase timestamps
+    void build_tail();
 
     ~Hierarchy();
     int64_t finest_dim() const { return 3 * levels.front().A.nrows; }

@@ -170,6 +170,35 @@ bool launch_restrict_smooth(const Bsr3 &R, const double *r, double *f, const Smo
                             cudaStream_t s, bool lowp = false);
 void launch_fill(int64_t n, double v, double *x, cudaStream_t s);
 
+// ---- V-cycle tail (solve.cu): the small levels in one persistent launch ----
+// One phase = one of the V-cycle's level operations on the small levels
+// (hierarchy.hpp:418-440), executed by every CTA of a cooperative grid with a
+// grid barrier between consecutive phases.
+enum VPhaseKind {
+    VP_SPMV = 0,      // out = alpha A x + beta out
+    VP_RESIDUAL = 1,  // out = f - A x
+    VP_SMOOTH_B = 2,  // out = x + M_row (f - A x)_row   (3x3 M_i)
+    VP_SMOOTH_P = 3,  // out = x + m .* (f - A x)        (point)
+    VP_RSMOOTH_B = 4, // out = A x (restriction), out2 = M_row out_row (next level's first sweep)
+    VP_RSMOOTH_P = 5,
+    VP_GEMV = 6,      // out = Ainv x (dense, row-major, leading dimension ld), nrows = n
+    VP_FILL = 7,      // out[0 .. 3 nrows) = alpha
+};
+struct VPhase {
+    int kind, G, nrows, last_out;  // last_out: out is the launch's final_out argument
+    const int *ptr, *col;
+    const double *val, *x, *f, *m;
+    double *out, *out2;
+    double alpha, beta;
+    long long ld;
+};
+// lanes per block row for a tail phase over `threads` resident threads
+int vtail_group(int64_t nrows, int64_t nnzb, int64_t threads);
+// resident CTAs of the tail kernel (0: cooperative launch not possible)
+int vtail_grid(size_t smem);
+void launch_vtail(const VPhase *d_ph, int nph, unsigned *bar, int grid, size_t smem, int64_t gemv_ld,
+                  double *final_out, cudaStream_t s, unsigned long long *trace = nullptr);
+
 // generic PCG with caller operators (cgop.cu, cg.hpp:39-83)
 samg_solve_report cg_solve_op(int64_t n, samg_apply_fn apply_A, samg_apply_fn apply_M, void *ctx,
                               const double *d_f, double *d_u, const samg_cg_params &prm,

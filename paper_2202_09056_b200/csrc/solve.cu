@@ -53,6 +53,16 @@ bool pdl_enabled() {
 }
 thread_local bool g_spmv_pdl = false;  // set around standalone SpMV launches
 
+// L2 cache policies (SAMG_L2_HINTS, default on): the TMA matrix streams
+// evict-first, the coarse inverse evict-last (it is re-read every V-cycle)
+bool l2_hints() {
+    static const bool on = [] {
+        const char *e = std::getenv("SAMG_L2_HINTS");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 // kernel launch, with the PDL attribute if `pdl` (the kernel then calls
 // pdl_wait before it reads a predecessor's output)
 template <class... KArgs, class... Args>
@@ -80,7 +90,7 @@ __device__ __forceinline__ double2 ldg2(const double *p) {
 // Sum three values over the G lanes of a group; every lane gets the totals.
 // G > 32 spans G/32 warps of the 256-thread CTA (shared memory, CTA barrier:
 // every thread of the CTA must call it).
-template <int G>
+template <int G, int kThreads = 256>
 __device__ __forceinline__ void group_reduce3(double &v0, double &v1, double &v2) {
     constexpr int W = G < 32 ? G : 32;
 #pragma unroll
@@ -90,7 +100,7 @@ __device__ __forceinline__ void group_reduce3(double &v0, double &v1, double &v2
         v2 += __shfl_xor_sync(0xffffffffu, v2, off, W);
     }
     if constexpr (G > 32) {
-        __shared__ double red[3][8];
+        __shared__ double red[3][kThreads / 32];
         const int w = threadIdx.x / 32;
         if (threadIdx.x % 32 == 0) { red[0][w] = v0; red[1][w] = v1; red[2][w] = v2; }
         __syncthreads();
@@ -175,7 +185,10 @@ __device__ __forceinline__ void blk9(const float *v, int odd, double (&b)[9]) {
     b[6] = odd ? q2.y : q3.x; b[7] = odd ? q3.x : q3.y; b[8] = odd ? q3.y : e;
 }
 
-template <int G, class VT = double>
+// kNcX = false: x is gathered through L2 only (ld.global.cg) -- inside the
+// persistent V-cycle tail x was written by other CTAs of the same launch, so
+// neither the read-only path nor L1 may serve it.
+template <int G, class VT = double, bool kNcX = true, int kThreads = 256>
 __device__ __forceinline__ void row_sums_blocks(int row, bool valid, int lane,
         const int *__restrict__ ptr, const int *__restrict__ col,
         const VT *__restrict__ val, const double *__restrict__ x,
@@ -192,8 +205,8 @@ __device__ __forceinline__ void row_sums_blocks(int row, bool valid, int lane,
             blk9<true>(val + 9 * static_cast<size_t>(j), j & 1, bb);
             const double *xp = x + 3 * static_cast<size_t>(c);
             const int xo = c & 1;
-            const double2 xq = ldg2(xp + xo);
-            const double xe = __ldg(xp + (xo ? 0 : 2));
+            const double2 xq = kNcX ? ldg2(xp + xo) : __ldcg(reinterpret_cast<const double2 *>(xp + xo));
+            const double xe = kNcX ? __ldg(xp + (xo ? 0 : 2)) : __ldcg(xp + (xo ? 0 : 2));
             const double x0 = xo ? xe : xq.x, x1 = xo ? xq.x : xq.y, x2 = xo ? xq.y : xe;
             const double b0 = bb[0], b1 = bb[1], b2 = bb[2], b3 = bb[3], b4 = bb[4], b5 = bb[5],
                          b6 = bb[6], b7 = bb[7], b8 = bb[8];
@@ -203,7 +216,7 @@ __device__ __forceinline__ void row_sums_blocks(int row, bool valid, int lane,
         }
     }
     s0 = a0; s1 = a1; s2 = a2;
-    group_reduce3<G>(s0, s1, s2);
+    group_reduce3<G, kThreads>(s0, s1, s2);
 }
 
 template <int G, int V, class VT>
@@ -558,6 +571,31 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
         ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
+// the same with an L2 cache policy (createpolicy): the matrix stream marked
+// evict-first, so it does not push the small, re-read operands (vectors, the
+// coarse inverse) out of the 126 MB L2
+__device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, unsigned bytes, uint64_t *bar,
+                                              uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol) : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ double2 ldg2_hint(const double2 *p, uint64_t pol) {
+    double2 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                 : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
 
 struct TmaHdr {
     int p0, direct, voff, coff;  // first block, fallback flag, block p0's offset (doubles / ints)
@@ -569,6 +607,7 @@ struct TmaCfg {
     int pdl;      // launched as a programmatic dependent (consumers wait + fence)
     int per_cta;  // > 0: CTA b owns the contiguous chunks [b*per_cta, (b+1)*per_cta)
                   // (neighbouring rows share x, so the gathers hit L1); 0: strided
+    int evict_first;  // stream val / col with an L2 evict-first policy
     unsigned vcap, ccap, pcap;  // stage layout: val | col | ptr (bytes)
     long long nnzb;
 };
@@ -643,10 +682,18 @@ __global__ void __launch_bounds__(32 * (TW * NT + 1), 1) k_bsr3_tma(TmaCfg cfg, 
                     if (!direct) {
                         unsigned char *sv = data + static_cast<size_t>(st) * stage_bytes;
                         mbar_arrive_tx(full + st, static_cast<unsigned>((ve - vb) + (ce - cb) + pbytes));
-                        bulk_g2s(sv, reinterpret_cast<const char *>(val) + vb,
-                                 static_cast<unsigned>(ve - vb), full + st);
-                        bulk_g2s(sv + cfg.vcap, reinterpret_cast<const char *>(col) + cb,
-                                 static_cast<unsigned>(ce - cb), full + st);
+                        if (cfg.evict_first) {
+                            const uint64_t pol = policy_evict_first();
+                            bulk_g2s_hint(sv, reinterpret_cast<const char *>(val) + vb,
+                                          static_cast<unsigned>(ve - vb), full + st, pol);
+                            bulk_g2s_hint(sv + cfg.vcap, reinterpret_cast<const char *>(col) + cb,
+                                          static_cast<unsigned>(ce - cb), full + st, pol);
+                        } else {
+                            bulk_g2s(sv, reinterpret_cast<const char *>(val) + vb,
+                                     static_cast<unsigned>(ve - vb), full + st);
+                            bulk_g2s(sv + cfg.vcap, reinterpret_cast<const char *>(col) + cb,
+                                     static_cast<unsigned>(ce - cb), full + st);
+                        }
                         bulk_g2s(sv + cfg.vcap + cfg.ccap, ptr + r0 - cfg.pmis,
                                  static_cast<unsigned>(pbytes), full + st);
                         // the chunk's epilogue vectors towards L2 (after a
@@ -829,6 +876,8 @@ bool launch_tma(const Bsr3 &A, const VT *val, const double *x, Epi epi, double *
     int G = 4;
     while (G < 32 && 3.3 * G * 1.5 * (sizeof(VT) == 4 ? 2 : 1) < bpr) G *= 2;
     if (forced_g == 4 || forced_g == 8 || forced_g == 16 || forced_g == 32) G = forced_g;
+    static const int gmax = env_int("SAMG_TMA_GMAX", 32);
+    G = std::min(G, std::max(4, gmax));
     const int rpc = 32 * TW / G;
     auto up = [](long long b) { return static_cast<unsigned>((b + 127) / 128 * 128); };
     const long long est = static_cast<long long>(std::ceil(bpr * 1.1)) + 1;
@@ -841,6 +890,7 @@ bool launch_tma(const Bsr3 &A, const VT *val, const double *x, Epi epi, double *
     cfg.pcap = up(4LL * (rpc + 8));
     cfg.pmis = static_cast<int>((reinterpret_cast<uintptr_t>(A.ptr.p) & 15) / 4);
     cfg.pdl = g_spmv_pdl && pdl_enabled() ? 1 : 0;
+    cfg.evict_first = l2_hints() ? 1 : 0;
     const long long stage = cfg.vcap + cfg.ccap + cfg.pcap;
     cfg.stages = static_cast<int>(std::min<long long>(16, (budget - kTmaHdrBytes) / stage));
     if (cfg.stages < NT + 1) return false;
@@ -1043,12 +1093,13 @@ __global__ void k_smooth_zero_block(int64_t nrows, const double *__restrict__ m,
 // eight 16-byte loads in flight per thread.
 constexpr int kGemvThreads = 64;
 __global__ void __launch_bounds__(kGemvThreads) k_dense_gemv(int n, int64_t ld, const double *__restrict__ A,
-        const double *__restrict__ f, double *__restrict__ u) {
+        const double *__restrict__ f, double *__restrict__ u, int keep) {
     constexpr int T = kGemvThreads;
     __shared__ double red[T / 32];
     const int row = blockIdx.x;
     const double2 *a = reinterpret_cast<const double2 *>(A + static_cast<size_t>(row) * ld);
     const int n2 = static_cast<int>(ld / 2);
+    const uint64_t pol = policy_evict_last();
     double s = 0.0, t = 0.0;
     // f as 16-byte pairs (f is 16-byte aligned; a last odd element alone)
     auto fpair = [&](int j2) {
@@ -1064,7 +1115,7 @@ __global__ void __launch_bounds__(kGemvThreads) k_dense_gemv(int n, int64_t ld, 
 #pragma unroll
         for (int k = 0; k < B; ++k) {
             const int j2 = j0 + k * T;
-            av[k] = j2 < n2 ? __ldg(a + j2) : make_double2(0.0, 0.0);
+            av[k] = j2 < n2 ? (keep ? ldg2_hint(a + j2, pol) : __ldg(a + j2)) : make_double2(0.0, 0.0);
         }
 #pragma unroll
         for (int k = 0; k < B; ++k) {
@@ -1082,6 +1133,82 @@ __global__ void __launch_bounds__(kGemvThreads) k_dense_gemv(int n, int64_t ld, 
     if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = s;
     __syncthreads();
     if (threadIdx.x == 0) u[row] = red[0] + red[1];
+}
+
+// TMA-fed dense GEMV (the coarse solve u = Ainv f, a 68 MB stream at C1):
+// one persistent CTA per SM owns a contiguous range of rows; a producer lane
+// streams whole rows (8*ld bytes, contiguous) into an S-stage shared-memory
+// ring with cp.async.bulk + mbarriers, after f itself; 8 consumer warps take
+// the CTA's rows in turn (warp w: rows w, w+8, ...) and form each dot
+// product from shared memory.  The per-thread-load variant (k_dense_gemv)
+// keeps one DRAM round trip per batch of 8 loads on every thread's chain
+// (3.3 TB/s at C1); here the bytes in flight per SM are set by the ring.
+constexpr int kGemvWarps = 8;
+__global__ void __launch_bounds__(32 * (kGemvWarps + 1), 1) k_dense_gemv_tma(int n, int64_t ld,
+        const double *__restrict__ A, const double *__restrict__ f, double *__restrict__ u, int stages,
+        int evict_first) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(sm);  // [16]
+    uint64_t *empty = full + 16;                          // [16]
+    uint64_t *fbar = empty + 16;
+    double *fs = reinterpret_cast<double *>(sm + 384);
+    const unsigned rowb = static_cast<unsigned>(8 * ld);
+    double *ring = fs + ld;
+    const int r0 = static_cast<int>((static_cast<long long>(n) * blockIdx.x) / gridDim.x);
+    const int r1 = static_cast<int>((static_cast<long long>(n) * (blockIdx.x + 1)) / gridDim.x);
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < stages; ++st) {
+            mbar_init(full + st, 1);
+            mbar_init(empty + st, 1);
+        }
+        mbar_init(fbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == kGemvWarps) {
+        if (lane == 0) {
+            const uint64_t pol = evict_first ? policy_evict_first() : 0;
+            // f's first n & ~1 entries (an odd n's last entry is read from global)
+            const unsigned fb = static_cast<unsigned>(8 * (n & ~1));
+            mbar_arrive_tx(fbar, fb);
+            if (fb) bulk_g2s(fs, f, fb, fbar);
+            int st = 0;
+            unsigned ph = 0;
+            for (int r = r0; r < r1; ++r) {
+                mbar_wait(empty + st, ph ^ 1);
+                mbar_arrive_tx(full + st, rowb);
+                if (evict_first)
+                    bulk_g2s_hint(ring + static_cast<size_t>(st) * ld, A + static_cast<size_t>(r) * ld, rowb,
+                                  full + st, pol);
+                else
+                    bulk_g2s(ring + static_cast<size_t>(st) * ld, A + static_cast<size_t>(r) * ld, rowb, full + st);
+                if (++st == stages) { st = 0; ph ^= 1; }
+            }
+        }
+        return;
+    }
+    mbar_wait(fbar, 0);
+    const int n2 = static_cast<int>(ld / 2);
+    const double2 *f2 = reinterpret_cast<const double2 *>(fs);
+    for (int i = warp; r0 + i < r1; i += kGemvWarps) {
+        const int st = i % stages;
+        mbar_wait(full + st, (i / stages) & 1);
+        const double2 *a2 = reinterpret_cast<const double2 *>(ring + static_cast<size_t>(st) * ld);
+        double s = 0.0, t = 0.0;
+        for (int j = lane; j < n2; j += 32) {
+            const double2 av = a2[j];
+            const double2 fv = 2 * j + 1 < n ? f2[j] : make_double2(__ldg(f + 2 * j), 0.0);
+            s = fma(av.x, fv.x, s);
+            t = fma(av.y, fv.y, t);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + st);
+        s += t;
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (lane == 0) u[r0 + i] = s;
+    }
 }
 
 // Vector kernels: 2 elements per thread per step (16-byte loads; the
@@ -1254,6 +1381,169 @@ __global__ void k_cg_finish2(CgScalars *sc, int rr_what, cudaGraphConditionalHan
     cg_apply(rr_what, sc->tmp, sc, h);
 }
 
+// ---- V-cycle tail: the small levels in one persistent launch ----------------
+// Below a size threshold a level's operators are a few MB: as separate
+// launches each is latency-bound (C1 level 2 and the coarse GEMV: seven
+// kernels at 0.2-2.6 TB/s, ~99 us of the 540 us iteration; profiles/
+// r02_ncu_cg_iteration.txt).  Here one cooperative grid (every CTA resident)
+// runs the whole list of phases -- restriction into the first small level,
+// its sweeps and residuals, the coarser levels, the dense coarse solve and
+// the prolongations back up -- with a grid barrier between phases, so the
+// launch gaps and ramp-downs are paid once.  Vectors written by an earlier
+// phase are read through L2 (ld.global.cg gathers) or after the barrier's
+// acquire fence (epilogue loads); the matrices stay on the read-only path.
+
+// Generation barrier over the whole grid (bar[0] = arrivals, bar[1] =
+// generation; both start at 0 and are left consistent for the next launch).
+__device__ __forceinline__ void vt_grid_sync(unsigned *bar, int sleep_ns) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        // (relaxed loads for the generation: an acquire load would invalidate
+        // this SM's L1 on every poll)
+        unsigned gen;
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(gen) : "l"(bar + 1) : "memory");
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");  // release this CTA's phase output
+        unsigned prev;
+        asm volatile("atom.relaxed.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(bar) : "memory");
+        if (prev == gridDim.x - 1) {
+            asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(bar) : "memory");
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(bar + 1), "r"(gen + 1) : "memory");
+        } else {
+            unsigned g2;
+            do {
+                if (sleep_ns) __nanosleep(sleep_ns);
+                asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g2) : "l"(bar + 1) : "memory");
+            } while (g2 == gen);
+        }
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire the other CTAs' outputs
+    }
+    __syncthreads();
+}
+
+// One SpMV-family phase: groups of G lanes per block row, consecutive rows
+// on consecutive groups of a CTA; uniform trip count (G > 32 reduces with
+// CTA barriers).
+constexpr int kVtThreads = 1024;  // one CTA per SM: 148 arrivals per grid barrier
+
+template <int G, class Epi>
+__device__ __forceinline__ void vt_rows(const VPhase &P, const Epi &epi) {
+    constexpr int GPC = kVtThreads / G;
+    const int total = gridDim.x * GPC;
+    const int nit = (P.nrows + total - 1) / total;
+    const int lane = threadIdx.x % G;
+    const int g0 = blockIdx.x * GPC + threadIdx.x / G;
+    for (int it = 0; it < nit; ++it) {
+        const int row = g0 + it * total;
+        const bool valid = row < P.nrows;
+        double s0, s1, s2;
+        row_sums_blocks<G, double, false, kVtThreads>(row, valid, lane, P.ptr, P.col, P.val, P.x, s0, s1, s2);
+        if (valid) epilogue<G>(epi, row, lane, s0, s1, s2);
+    }
+}
+
+template <class Epi>
+__device__ __forceinline__ void vt_spmv(const VPhase &P, const Epi &epi) {
+    switch (P.G) {
+        case 4: vt_rows<4>(P, epi); break;
+        case 8: vt_rows<8>(P, epi); break;
+        case 16: vt_rows<16>(P, epi); break;
+        case 32: vt_rows<32>(P, epi); break;
+        case 64: vt_rows<64>(P, epi); break;
+        default: vt_rows<128>(P, epi); break;
+    }
+}
+
+// u = Ainv f: one warp per row, f staged once per CTA in shared memory
+// (when it fits: fs != nullptr), eight 16-byte loads in flight per lane.
+__device__ __forceinline__ void vt_gemv(const VPhase &P, double *fs, bool keep) {
+    const uint64_t pol = policy_evict_last();
+    const int n = P.nrows;
+    const int n2 = static_cast<int>(P.ld / 2);
+    const double *f = P.x;
+    if (fs) {
+        for (int j = threadIdx.x; j < n; j += blockDim.x) fs[j] = __ldcg(f + j);
+        if (threadIdx.x == 0 && (n & 1)) fs[n] = 0.0;
+        __syncthreads();
+    }
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int nw = gridDim.x * (blockDim.x / 32);
+    for (int row = blockIdx.x * (blockDim.x / 32) + warp; row < n; row += nw) {
+        const double2 *a = reinterpret_cast<const double2 *>(P.val + static_cast<size_t>(row) * P.ld);
+        double s = 0.0, t = 0.0;
+        constexpr int B = 8;
+        for (int j0 = lane; j0 < n2; j0 += B * 32) {
+            double2 av[B];
+#pragma unroll
+            for (int k = 0; k < B; ++k) {
+                const int j2 = j0 + k * 32;
+                av[k] = j2 < n2 ? (keep ? ldg2_hint(a + j2, pol) : __ldg(a + j2)) : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int k = 0; k < B; ++k) {
+                const int j2 = j0 + k * 32;
+                if (j2 < n2) {
+                    const int j = 2 * j2;
+                    double2 fk;
+                    if (fs) fk = make_double2(fs[j], fs[j + 1]);
+                    else fk = make_double2(__ldcg(f + j), j + 1 < n ? __ldcg(f + j + 1) : 0.0);
+                    s = fma(av[k].x, fk.x, s);
+                    t = fma(av[k].y, fk.y, t);
+                }
+            }
+        }
+        s += t;
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (lane == 0) P.out[row] = s;
+    }
+}
+
+__global__ void __launch_bounds__(kVtThreads, 1) k_vtail(const VPhase *__restrict__ phases, int nph,
+                                                   unsigned *bar, double *final_out, int flags,
+                                                   unsigned long long *trace) {
+    extern __shared__ double vt_fs[];
+    auto stamp = [&](int slot) {
+        if (trace && blockIdx.x == 0 && threadIdx.x == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            trace[slot] = t;
+        }
+    };
+    stamp(2 * nph);
+    auto stamp_cta = [&](int k) {  // every CTA's end of phase k (k == nph: its start)
+        if (trace && threadIdx.x == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            trace[2 * nph + 1 + static_cast<size_t>(k) * gridDim.x + blockIdx.x] = t;
+        }
+    };
+    stamp_cta(nph);
+    for (int k = 0; k < nph; ++k) {
+        VPhase P = phases[k];
+        if (P.last_out) P.out = final_out;
+        switch (P.kind) {
+            case VP_SPMV: vt_spmv(P, EpiSpmv{P.alpha, P.beta, P.out}); break;
+            case VP_RESIDUAL: vt_spmv(P, EpiResidual{P.f, P.out}); break;
+            case VP_SMOOTH_B: vt_spmv(P, EpiSmoothBlock{P.f, P.x, P.m, P.out}); break;
+            case VP_SMOOTH_P: vt_spmv(P, EpiSmoothPoint{P.f, P.x, P.m, P.out}); break;
+            case VP_RSMOOTH_B: vt_spmv(P, EpiRestrictSmooth<true>{P.out, P.out2, P.m}); break;
+            case VP_RSMOOTH_P: vt_spmv(P, EpiRestrictSmooth<false>{P.out, P.out2, P.m}); break;
+            case VP_GEMV: vt_gemv(P, (flags & 1) ? vt_fs : nullptr, (flags & 2) != 0); break;
+            case VP_FILL:
+                for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+                     i < 3LL * P.nrows; i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+                    P.out[i] = P.alpha;
+                break;
+            default: break;
+        }
+        stamp(2 * k);
+        __syncthreads();
+        stamp_cta(k);
+        if (k + 1 < nph) vt_grid_sync(bar, flags >> 8);
+        stamp(2 * k + 1);
+    }
+}
+
 int vec_grid(int64_t n) {
     const int64_t g = (n + 255) / 256;
     return static_cast<int>(g < kRedBlocks ? (g > 0 ? g : 1) : kRedBlocks);
@@ -1378,7 +1668,28 @@ void make_lowp(Bsr3 &A, cudaStream_t s) {
 void launch_dense_gemv(int64_t n, const double *Ainv, const double *f, double *u,
                        cudaStream_t s) {
     if (n == 0) return;
-    launch_k(false, k_dense_gemv, static_cast<int>(n), kGemvThreads, 0, s, static_cast<int>(n), dense_ld(n), Ainv, f, u);
+    static const int tma = env_int("SAMG_GEMV_TMA", 1);
+    const int64_t ld = dense_ld(n);
+    // f and at least 4 row stages in shared memory, 16-byte aligned rows
+    if (tma && 8 * ld * 5 + 384 <= 227 * 1024 && (reinterpret_cast<uintptr_t>(Ainv) & 15) == 0 &&
+        (reinterpret_cast<uintptr_t>(f) & 15) == 0) {
+        static DeviceCache attr;
+        const int ok = attr.get([] {
+            return cudaFuncSetAttribute(k_dense_gemv_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        227 * 1024) == cudaSuccess ? 1 : (cudaGetLastError(), 0);
+        });
+        if (ok) {
+            const int stages = static_cast<int>(std::min<int64_t>(16, (227 * 1024 - 384 - 8 * ld) / (8 * ld)));
+            const size_t smem = 384 + static_cast<size_t>(8 * ld) * (stages + 1);
+            const int grid = static_cast<int>(std::min<int64_t>(sm_count(), n));
+            launch_k(false, k_dense_gemv_tma, grid, 32 * (kGemvWarps + 1), smem, s, static_cast<int>(n), ld, Ainv, f,
+                     u, stages, 0);
+            CK_LAUNCH();
+            return;
+        }
+    }
+    launch_k(false, k_dense_gemv, static_cast<int>(n), kGemvThreads, 0, s, static_cast<int>(n), dense_ld(n), Ainv, f, u,
+             l2_hints() ? 1 : 0);
     CK_LAUNCH();
 }
 
@@ -1449,6 +1760,57 @@ void launch_fill(int64_t n, double v, double *x, cudaStream_t s) {
     if (n == 0) return;
     launch_k(false, k_fill, vec_grid(n), 256, 0, s, n, v, x);
     CK_LAUNCH();
+}
+
+
+int vtail_group(int64_t nrows, int64_t nnzb, int64_t threads) {
+    static const int forced = env_int("SAMG_VTAIL_G", 0);
+    if (forced) return forced;
+    // ~8 blocks per lane, then as many lanes as the resident grid allows in
+    // one pass (shorter per-lane chains), at most 128
+    const double bpr = nrows ? static_cast<double>(nnzb) / nrows : 0.0;
+    int G = 4;
+    while (G < 128 && G * 8.0 < bpr) G *= 2;
+    while (G < 128 && nrows * G * 2 <= threads) G *= 2;
+    return G;
+}
+
+int vtail_grid(size_t smem) {
+    static DeviceCache attr;
+    const int ok = attr.get([&] {
+        int dev = 0, coop = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+        if (!coop) return 0;
+        // up to 96 KB of staged coarse right-hand side
+        return cudaFuncSetAttribute(k_vtail, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024) ==
+                       cudaSuccess ? 1 : (cudaGetLastError(), 0);
+    });
+    if (!ok || smem > 96 * 1024) return 0;
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_vtail, kVtThreads, smem) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return occ * sm_count();
+}
+
+void launch_vtail(const VPhase *d_ph, int nph, unsigned *bar, int grid, size_t smem, int64_t gemv_ld,
+                  double *final_out, cudaStream_t s, unsigned long long *trace) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kVtThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    static const int sleep_ns = env_int("SAMG_VTAIL_SLEEP", 0);
+    const int flags = (smem >= static_cast<size_t>(8 * gemv_ld) && gemv_ld > 0 ? 1 : 0) | (l2_hints() ? 2 : 0) |
+                      (sleep_ns << 8);
+    CK(cudaLaunchKernelEx(&cfg, k_vtail, d_ph, nph, bar, final_out, flags, trace));
 }
 
 } // namespace samgb

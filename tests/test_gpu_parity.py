@@ -376,6 +376,62 @@ def test_node6_spmv_matches_reference(gpu, ref):
     assert out.returncode == 0 and "node6 ok" in out.stdout, out.stderr[-2000:]
 
 
+VTAIL_CHILD = r"""
+import sys, json
+sys.path.insert(0, %r)
+import numpy as np
+import paper_2202_09056_b200 as pb
+out = {}
+for name, kw, prm in (
+        ("cube", dict(nx=24, ny=24, nz=24, dirichlet="eliminate", noise=0.01, seed=3), dict(coarse_enough=300)),
+        ("cantilever_keep", dict(nx=40, ny=8, nz=8, dirichlet="keep_rows", load="traction_xend"),
+         dict(coarse_enough=200, pre_sweeps=2, post_sweeps=3)),
+        ("cube_jacobi", dict(nx=20, ny=20, nz=20, dirichlet="eliminate", noise=0.01, seed=5),
+         dict(coarse_enough=200, smoother="jacobi", smoother_omega=0.5)),
+        ("block", dict(nx=16, ny=16, nz=16, dirichlet="eliminate", noise=0.01, seed=4),
+         dict(coarse_enough=300, pipeline="block"))):
+    pl = prm.pop("pipeline", "ns_block")
+    p = pb.generate_hex(**kw)
+    h = pb.setup(p.csr(), None if pl == "block" else p.nullspace(), pl, pb.AmgParams(**prm))
+    f = np.random.default_rng(7).uniform(-1, 1, p.n)
+    v = h.vcycle(f)
+    u, rep = h.cg_solve(p.rhs)
+    out[name] = {"v": v.tolist(), "u": u.tolist(), "its": rep["iterations"], "levels": h.nlevels,
+                 "converged": rep["converged"]}
+print("JSON" + json.dumps(out))
+"""
+
+
+def test_vcycle_tail_matches_per_kernel_vcycle(gpu):
+    """The persistent V-cycle tail (k_vtail: the small levels, the coarse
+    GEMV and the prolongation back up in one cooperative launch, solve.cu)
+    computes the same V-cycle as the per-kernel path (SAMG_VTAIL=0) up to
+    summation order (1e-12), with equal CG iteration counts -- including
+    several pre/post sweeps, point Jacobi and the block pipeline."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for tail in ("0", "1"):
+        env = {**os.environ, "SAMG_VTAIL": tail, "SAMG_VTAIL_MB": "1000"}
+        out = subprocess.run([sys.executable, "-c", VTAIL_CHILD % root], capture_output=True,
+                             text=True, env=env, timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        line = [ln for ln in out.stdout.splitlines() if ln.startswith("JSON")][-1]
+        res[tail] = json.loads(line[4:])
+    for name in res["0"]:
+        a, b = res["0"][name], res["1"][name]
+        assert a["levels"] >= 3, (name, a["levels"])
+        va, vb = np.array(a["v"]), np.array(b["v"])
+        assert np.abs(va - vb).max() <= 1e-12 * np.abs(va).max(), name
+        assert a["its"] == b["its"], (name, a["its"], b["its"])
+        assert a["converged"] and b["converged"], name
+        ua, ub = np.array(a["u"]), np.array(b["u"])
+        assert np.linalg.norm(ua - ub) <= 1e-9 * np.linalg.norm(ua), name
+
+
 def test_cg_solve_op_callbacks(gpu, ref):
     """samg_cg_solve_op (cg.hpp:39-83) with caller operators: the B200 SpMV
     as apply_A and (zero guess +) the B200 V-cycle as apply_M reproduce
