@@ -859,12 +859,18 @@ int tma_cta_cap() {
 template <bool kReduce, class VT, class Epi>
 bool launch_tma(const Bsr3 &A, const VT *val, const double *x, Epi epi, double *partials,
                 CgScalars *sc, int what, cudaStream_t s) {
-    if (A.nrows < 8 || A.nnzb == 0) return false;
+    static const int dbg = env_int("SAMG_TMA_DEBUG", 0);
+    auto why = [&](const char *r) {
+        if (dbg) std::fprintf(stderr, "launch_tma: %lld rows %lld blocks: %s\n", (long long)A.nrows,
+                              (long long)A.nnzb, r);
+        return false;
+    };
+    if (A.nrows < 8 || A.nnzb == 0) return why("small");
     // val / col: the full arrays (16-byte aligned allocations); ptr may be a
     // row view's offset pointer (the multi-GPU interior rows), handled in-kernel
     if ((reinterpret_cast<uintptr_t>(val) | reinterpret_cast<uintptr_t>(A.col.p)) & 15 ||
         reinterpret_cast<uintptr_t>(A.ptr.p) & 3)
-        return false;
+        return why("alignment");
     static const int forced_g = env_int("SAMG_TMA_G", 0);
     static const int budget64 = env_int("SAMG_TMA_SMEM", 226000);
     static const int budget32 = env_int("SAMG_TMA_SMEM32", 226000);
@@ -880,7 +886,17 @@ bool launch_tma(const Bsr3 &A, const VT *val, const double *x, Epi epi, double *
     G = std::min(G, std::max(4, gmax));
     const int rpc = 32 * TW / G;
     auto up = [](long long b) { return static_cast<unsigned>((b + 127) / 128 * 128); };
-    const long long est = static_cast<long long>(std::ceil(bpr * 1.1)) + 1;
+    long long est = static_cast<long long>(std::ceil(bpr * 1.1)) + 1;
+    // blocks per row a stage holds: ~10 % above the mean, but shrunk (down to
+    // the mean + 2 %) so that NT + 1 stages still fit -- C4's fine level (26.7
+    // blocks per row) missed the third stage by 1 % and ran without TMA;
+    // a rarer chunk above the capacity is computed from global memory
+    {
+        const long long per_block = 9 * static_cast<long long>(sizeof(VT)) + 4;
+        const long long room = (budget - kTmaHdrBytes) / (NT + 1) - 4LL * (rpc + 8) - 3 * 128 - 32;
+        const long long fit = room / (rpc * per_block);
+        if (fit < est && fit >= static_cast<long long>(std::ceil(bpr * 1.02))) est = fit;
+    }
     TmaCfg cfg{};
     cfg.nrows = static_cast<int>(A.nrows);
     cfg.nchunks = static_cast<int>((A.nrows + rpc - 1) / rpc);
@@ -893,13 +909,13 @@ bool launch_tma(const Bsr3 &A, const VT *val, const double *x, Epi epi, double *
     cfg.evict_first = l2_hints() ? 1 : 0;
     const long long stage = cfg.vcap + cfg.ccap + cfg.pcap;
     cfg.stages = static_cast<int>(std::min<long long>(16, (budget - kTmaHdrBytes) / stage));
-    if (cfg.stages < NT + 1) return false;
+    if (cfg.stages < NT + 1) return why("stages");
     const int smem = kTmaHdrBytes + static_cast<int>(cfg.stages * stage);
     const int sms = sm_count();
     // one persistent CTA per SM only pays off when every CTA streams many
     // chunks (C1: fine level 8 064 chunks, P0 4 032 -> TMA; A1 2 580 -> variant 1)
     static const int min_chunks_per_sm = env_int("SAMG_TMA_MIN_CHUNKS", 24);
-    if (cfg.nchunks < min_chunks_per_sm * sms) return false;
+    if (cfg.nchunks < min_chunks_per_sm * sms) return why("chunks");
     bool ok = false;
     dispatch_tma_shape(G, [&](auto sh) {
         using Sh = decltype(sh);
@@ -922,7 +938,7 @@ bool launch_tma(const Bsr3 &A, const VT *val, const double *x, Epi epi, double *
             }
             return m;
         });
-        if (smem > max_dyn) return;
+        if (smem > max_dyn) { why("smem"); return; }
         int occ = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
         int grid = std::max(1, std::min(cfg.nchunks, std::max(1, occ) * sms));
