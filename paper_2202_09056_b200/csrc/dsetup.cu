@@ -587,6 +587,9 @@ DSetup dist_setup(const Xport &x, std::vector<Bsr3> &&A_own, std::vector<DevBuf<
     }();
     double t_mark = t_start;
     auto mark = [&](const char *what, size_t level) {
+        char nv[64];
+        std::snprintf(nv, sizeof nv, "dsetup L%zu %s done", level, what);
+        nvtxMarkA(nv);
         if (!timing) return;
         CK(cudaStreamSynchronize(s));
         const double t = std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();

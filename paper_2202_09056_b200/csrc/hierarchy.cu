@@ -121,6 +121,11 @@ Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int6
     }();
     double t_mark = t_start;
     auto mark = [&](const char *what, size_t level) {
+        // an NVTX marker at the end of every setup phase (Nsight timelines:
+        // the phases between the markers inside the samg::setup range)
+        char nv[64];
+        std::snprintf(nv, sizeof nv, "setup L%zu %s done", level, what);
+        nvtxMarkA(nv);
         if (!timing) return;
         CK(cudaStreamSynchronize(s));
         const double t = now_s();
