@@ -344,14 +344,22 @@ SAMG_API int samg_setup(int64_t n, const int64_t *ptr, const int64_t *col, const
         Bsr3 A0;
         try {
             const int64_t nnz = ptr[n];
-            DevBuf<int64_t> dp(n + 1, s), dc(nnz, s);
+            DevBuf<int64_t> dp(n + 1, s);
             DevBuf<double> dv(nnz, s);
             h2d(dp.p, ptr, sizeof(int64_t) * (n + 1), s);
-            if (nnz) {
-                h2d(dc.p, col, sizeof(int64_t) * nnz, s);
-                h2d(dv.p, val, sizeof(double) * nnz, s);
+            if (nnz) h2d(dv.p, val, sizeof(double) * nnz, s);
+            if (n <= INT32_MAX) {
+                // column indices narrowed to 32 bits by the staging threads
+                // (half the PCIe bytes of the int64 array; range-checked)
+                DevBuf<int32_t> dc(nnz, s);
+                require(h2d_narrow(dc.p, col, static_cast<size_t>(nnz), n, s), SAMG_INVALID_ARGUMENT,
+                        "setup: column index out of range");
+                scalar_to_bsr3(n, dp.p, dc.p, dv.p, A0, s);
+            } else {
+                DevBuf<int64_t> dc(nnz, s);
+                if (nnz) h2d(dc.p, col, sizeof(int64_t) * nnz, s);
+                scalar_to_bsr3(n, dp.p, dc.p, dv.p, A0, s);
             }
-            scalar_to_bsr3(n, dp.p, dc.p, dv.p, A0, s);
         } catch (...) {
             cudaStreamSynchronize(s);
             cudaStreamDestroy(s);

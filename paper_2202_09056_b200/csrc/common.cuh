@@ -81,6 +81,8 @@ inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) 
 // Host -> device copy on stream s; large pageable sources are staged through
 // a pinned buffer pool by parallel host threads (hostcopy.cpp).
 void h2d(void *dst, const void *src, size_t bytes, cudaStream_t s);
+// int64 -> int32 staged copy; false if a value lies outside [0, bound)
+bool h2d_narrow(int32_t *dst, const int64_t *src, size_t count, int64_t bound, cudaStream_t s);
 // small (<= 256 B) pinned host objects from a process-wide slab pool
 void *pinned_small_alloc(size_t bytes);
 void pinned_small_free(void *p);

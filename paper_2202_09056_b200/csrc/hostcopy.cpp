@@ -123,6 +123,70 @@ void h2d(void *dst, const void *src, size_t bytes, cudaStream_t s) {
     // next work
 }
 
+// int64 -> int32 host -> device copy with a range check (the scalar CSR
+// column indices of samg_setup: half the PCIe bytes of the int64 array).
+// The staging threads narrow while they copy into the pinned buffers;
+// returns false if any value lies outside [0, bound).
+bool h2d_narrow(int32_t *dst, const int64_t *src, size_t count, int64_t bound, cudaStream_t s) {
+    if (count == 0) return true;
+    constexpr size_t kElems = kChunk / sizeof(int32_t);
+    auto narrow = [bound](int32_t *out, const int64_t *in, size_t n) {
+        bool ok = true;
+        for (size_t i = 0; i < n; ++i) {
+            const int64_t v = in[i];
+            ok &= (v >= 0) & (v < bound);
+            out[i] = static_cast<int32_t>(v);
+        }
+        return ok;
+    };
+    if (count * sizeof(int64_t) < kDirect) {
+        std::vector<int32_t> tmp(count);
+        const bool ok = narrow(tmp.data(), src, count);
+        CK(cudaMemcpyAsync(dst, tmp.data(), sizeof(int32_t) * count, cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));
+        return ok;
+    }
+    Pool &P = pool();
+    std::lock_guard<std::mutex> lock(P.mu);
+    P.init();
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    const size_t nchunks = (count + kElems - 1) / kElems;
+    static const int threads = [] {
+        const char *e = std::getenv("SAMG_H2D_THREADS");
+        const int hw = static_cast<int>(std::thread::hardware_concurrency());
+        const int v = e ? std::atoi(e) : std::min(12, std::max(1, hw - 2));
+        return std::min(kThreads, std::max(1, v));
+    }();
+    const int T = static_cast<int>(std::min<size_t>(threads, nchunks));
+    std::vector<std::exception_ptr> errs(T);
+    std::vector<char> oks(T, 1);
+    auto work = [&](int t) {
+        try {
+            CK(cudaSetDevice(dev));
+            int b = 0;
+            for (size_t c = t; c < nchunks; c += T, b ^= 1) {
+                const size_t off = c * kElems, n = std::min(kElems, count - off);
+                CK(cudaEventSynchronize(P.ev[t][b]));
+                if (!narrow(reinterpret_cast<int32_t *>(P.buf[t][b]), src + off, n)) oks[t] = 0;
+                CK(cudaMemcpyAsync(dst + off, P.buf[t][b], sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+                CK(cudaEventRecord(P.ev[t][b], s));
+            }
+        } catch (...) {
+            errs[t] = std::current_exception();
+        }
+    };
+    std::vector<std::thread> th;
+    for (int t = 1; t < T; ++t) th.emplace_back(work, t);
+    work(0);
+    for (auto &x : th) x.join();
+    for (auto &e : errs)
+        if (e) std::rethrow_exception(e);
+    for (char o : oks)
+        if (!o) return false;
+    return true;
+}
+
 // Small pinned objects (CG scalar mirrors, ...): 256-byte slots carved
 // from 1 MB pinned slabs, so a hierarchy setup does not pay cudaMallocHost
 // (~2 ms each) for a few hundred bytes.

@@ -213,6 +213,9 @@ struct Graph {  // node adjacency, symmetric, sorted rows (coarsening.hpp:33-38)
 // scalar CSR (int64 on host layout) uploaded -> BSR3 (csr.hpp:268-324)
 void scalar_to_bsr3(int64_t n, const int64_t *d_ptr, const int64_t *d_col, const double *d_val,
                     Bsr3 &out, cudaStream_t s);
+// the same from 32-bit column indices (samg_setup narrows them on upload)
+void scalar_to_bsr3(int64_t n, const int64_t *d_ptr, const int32_t *d_col, const double *d_val,
+                    Bsr3 &out, cudaStream_t s);
 // strength graph on nodes of h block rows (coarsening.hpp:52-123); tile
 // weight max|a| of the scalar view, or with fnorm (the block pipeline's
 // csr<block3> strength, pbs 1) the block's Frobenius norm

@@ -143,20 +143,24 @@ __device__ __forceinline__ void accum_block(const double *a, const double *b, do
 // to_block<3> of a sorted scalar CSR (csr.hpp:268-324): 3-way merge of the
 // scalar rows' block columns; absent tile entries stay zero.
 
-__global__ void k_s2b_count(int64_t nb, const int64_t *ptr, const int64_t *col, int *cnt,
+template <class CT>
+__global__ void k_s2b_count(int64_t nb, const int64_t *ptr, const CT *col, int *cnt,
                             DevError *err) {
     for (int64_t bi = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; bi < nb;
          bi += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         int64_t h[3], e[3];
         for (int r = 0; r < 3; ++r) { h[r] = ptr[3 * bi + r]; e[r] = ptr[3 * bi + r + 1]; }
-        for (int r = 0; r < 3; ++r)
+        for (int r = 0; r < 3; ++r) {
+            if (h[r] < e[r] && (col[h[r]] < 0 || col[e[r] - 1] >= 3 * nb))
+                raise(err, SAMG_INVALID_ARGUMENT, 3 * bi + r);  // column out of range
             for (int64_t j = h[r] + 1; j < e[r]; ++j)
                 if (col[j] <= col[j - 1]) raise(err, SAMG_INVALID_ARGUMENT, 3 * bi + r);
+        }
         int c = 0;
         while (true) {
             int64_t m = INT64_MAX;
             for (int r = 0; r < 3; ++r)
-                if (h[r] < e[r]) m = min(m, col[h[r]] / 3);
+                if (h[r] < e[r]) m = min(m, static_cast<int64_t>(col[h[r]]) / 3);
             if (m == INT64_MAX) break;
             ++c;
             for (int r = 0; r < 3; ++r)
@@ -166,7 +170,8 @@ __global__ void k_s2b_count(int64_t nb, const int64_t *ptr, const int64_t *col, 
     }
 }
 
-__global__ void k_s2b_fill(int64_t nb, const int64_t *ptr, const int64_t *col,
+template <class CT>
+__global__ void k_s2b_fill(int64_t nb, const int64_t *ptr, const CT *col,
                            const double *val, const int *bptr, int *bcol, double *bval) {
     for (int64_t bi = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; bi < nb;
          bi += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -176,7 +181,7 @@ __global__ void k_s2b_fill(int64_t nb, const int64_t *ptr, const int64_t *col,
         while (true) {
             int64_t m = INT64_MAX;
             for (int r = 0; r < 3; ++r)
-                if (h[r] < e[r]) m = min(m, col[h[r]] / 3);
+                if (h[r] < e[r]) m = min(m, static_cast<int64_t>(col[h[r]]) / 3);
             if (m == INT64_MAX) break;
             bcol[out] = static_cast<int>(m);
             double *blk = bval + 9 * static_cast<int64_t>(out);
@@ -1357,8 +1362,9 @@ void check_dev_error(DevError *err, cudaStream_t s) {
     fail(h.code, std::string(what) + " (at index " + std::to_string(h.where) + ")");
 }
 
-void scalar_to_bsr3(int64_t n, const int64_t *d_ptr, const int64_t *d_col, const double *d_val,
-                    Bsr3 &out, cudaStream_t s) {
+template <class CT>
+void scalar_to_bsr3_t(int64_t n, const int64_t *d_ptr, const CT *d_col, const double *d_val,
+                      Bsr3 &out, cudaStream_t s) {
     const int64_t nb = n / 3;
     DevBuf<int> cnt(nb + 1, s);
     DevBuf<DevError> err(1, s);
@@ -1376,6 +1382,16 @@ void scalar_to_bsr3(int64_t n, const int64_t *d_ptr, const int64_t *d_col, const
     out.val.alloc(9 * nnzb, s);
     k_s2b_fill<<<grid, 256, 0, s>>>(nb, d_ptr, d_col, d_val, out.ptr.p, out.col.p, out.val.p);
     CK_LAUNCH();
+}
+
+void scalar_to_bsr3(int64_t n, const int64_t *d_ptr, const int64_t *d_col, const double *d_val,
+                    Bsr3 &out, cudaStream_t s) {
+    scalar_to_bsr3_t(n, d_ptr, d_col, d_val, out, s);
+}
+
+void scalar_to_bsr3(int64_t n, const int64_t *d_ptr, const int32_t *d_col, const double *d_val,
+                    Bsr3 &out, cudaStream_t s) {
+    scalar_to_bsr3_t(n, d_ptr, d_col, d_val, out, s);
 }
 
 void strength_graph(const Bsr3 &A, int h, double eps_strong, Graph &G, cudaStream_t s,

@@ -314,6 +314,34 @@ def test_dense_inverse_singular_is_reported(gpu):
         A.dense_inverse()
 
 
+def test_setup_scalar_csr_column_range(gpu):
+    """samg_setup narrows the scalar CSR's int64 column indices to 32 bits
+    while staging them (h2d_narrow): a large problem (staged path) sets up
+    bit-identically to the block input, and an index outside [0, n) -- on
+    the staged or the small direct path -- is an invalid argument, not a
+    wrapped index."""
+    pb = gpu
+    from paper_2202_09056_b200._lib import InvalidArgument
+    p = make_problem(pb, 20, dirichlet="eliminate", noise=0.01, seed=3)
+    ptr, col, val = p.csr()[1:]
+    h1 = pb.setup(p.csr(), p.nullspace(), "ns_block", pb.AmgParams())
+    h2 = pb.setup_bsr3(p.nbrows, p.ptr, p.col, p.val.reshape(-1), p.nullspace(), "ns_block",
+                       pb.AmgParams())
+    assert h1.nlevels == h2.nlevels
+    for l in range(h1.nlevels):
+        assert np.array_equal(h1.level(l, 0)[4], h2.level(l, 0)[4]), l
+    for big in (True, False):
+        q = p if big else make_problem(pb, 4, dirichlet="eliminate")
+        A = q.csr()
+        bad = A[2].copy()
+        bad[len(bad) // 2] = A[0] + (1 << 32)  # wraps to a valid-looking int32
+        with pytest.raises(InvalidArgument):
+            pb.setup((A[0], A[1], bad, A[3]), q.nullspace(), "ns_block", pb.AmgParams())
+        bad[len(bad) // 2] = -3
+        with pytest.raises(InvalidArgument):
+            pb.setup((A[0], A[1], bad, A[3]), q.nullspace(), "ns_block", pb.AmgParams())
+
+
 def test_second_device_after_first(gpu):
     """Function attributes (dynamic shared memory opt-in, cluster limits)
     are per device: setup + solve on device 1 after device 0 in the same
