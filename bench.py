@@ -75,6 +75,19 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+# Read-only HBM stream on a round-2 B200 (scripts/micro/read_bw.cu, best of
+# 10 over 4 GiB, profiles/r02_read_bw.txt): the SpMV moves ~99 % reads,
+# while MEASURED_PEAKS' copy figure is half reads and half writes (a copy
+# measured 6141 GB/s on the same box), so a read stream can exceed it.
+READ_PEAK_GBS = 7199.0
+
+
+def read_peak_fields(achieved):
+    return {"peak_read_only": READ_PEAK_GBS, "frac_read_only": achieved / READ_PEAK_GBS,
+            "peak_read_only_source": "16-byte grid-stride loads over 4 GiB, scripts/micro/read_bw.cu "
+                                     "(profiles/r02_read_bw.txt)"}
+
+
 def dist_init(args):
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
@@ -480,6 +493,7 @@ def run_b200(args, rank, world, local, dist):
             "config": config_dict(p, world),
             "roofline": {"bound": "hbm", "achieved": gbs_rank, "peak": peak, "unit": "GB/s",
                          "frac": gbs_rank / peak, "traffic": traffic, "peak_source": peak_src,
+                         **read_peak_fields(gbs_rank),
                          "kernel": "k_bsr3_tma<8,8,2,false,EpiSpmv> (solve.cu, TMA-fed)"},
             "e2e": {"value": e2e_val, "unit": "GB/s", "h2d_bytes_per_step": 8 * p.n,
                     "d2h_bytes_per_step": 8 * p.n,
@@ -623,7 +637,7 @@ def run_b200_dist(args, rank, world, local, dist):
                        "parallelism": f"row partition x{world} (NCCL P2P halo)"},
             "roofline": {"bound": "hbm", "achieved": gb_rank, "peak": peak, "unit": "GB/s",
                          "frac": gb_rank / peak, "traffic": ncu_traffic(),
-                         "peak_source": peak_src,
+                         "peak_source": peak_src, **read_peak_fields(gb_rank),
                          "kernel": "k_bsr3_tma<8,8,2,false,EpiSpmv> on the interior row view + k_bsr3 on the boundary rows (dist.cu, solve.cu)"},
             "e2e": {"value": e2e_val, "unit": "GB/s", "h2d_bytes_per_step": 8 * 3 * nloc * world,
                     "d2h_bytes_per_step": 8 * 3 * nloc * world,
