@@ -27,6 +27,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <type_traits>
 #include <vector>
 
@@ -257,7 +258,15 @@ __device__ __forceinline__ void warp_argmax(double v, int idx, double &bv, int &
     bv = __longlong_as_double(static_cast<long long>((static_cast<unsigned long long>(mh) << 32) | ml));
 }
 
-template <int RPW, int kRW>
+// kPivot = false: Gauss-Jordan without row exchanges (pivot row k itself),
+// for the symmetric positive definite coarse operators of SA-AMG after the
+// symmetric equilibration (unit diagonal; the pivots of an SPD matrix stay
+// positive): per column only row k travels through the cluster -- no
+// candidate search, no candidate rows, no row moves afterwards.  A pivot
+// below kNoPivotTol reports failure and the caller repeats with pivoting.
+constexpr double kNoPivotTol = 1e-8;
+
+template <int RPW, int kRW, bool kPivot = true>
 __global__ void __launch_bounds__(kRW * 32, 1) k_panel_reg(int n, int64_t ld, int k0, int bk, int R,
                                                             double *X, int64_t *piv, DevError *err) {
     cg::cluster_group cl = cg::this_cluster();
@@ -272,7 +281,8 @@ __global__ void __launch_bounds__(kRW * 32, 1) k_panel_reg(int n, int64_t ld, in
     const int lane = threadIdx.x % 32, w = threadIdx.x / 32;
     const int rw0 = r0 + w;  // row of slot j: rw0 + kRW * j
     const int jend = r1 > rw0 ? (r1 - rw0 + kRW - 1) / kRW : 0;  // own slots [0, jend)
-    const unsigned tx = static_cast<unsigned>(C * (sizeof(Cand) + kRB * sizeof(double)) + kRB * sizeof(double));
+    const unsigned tx = kPivot ? static_cast<unsigned>(C * (sizeof(Cand) + kRB * sizeof(double)) + kRB * sizeof(double))
+                               : static_cast<unsigned>(kRB * sizeof(double));
     if (threadIdx.x == 0) {
         mbar_init_cta(&bar[0], 1);
         mbar_init_cta(&bar[1], 1);
@@ -287,51 +297,56 @@ __global__ void __launch_bounds__(kRW * 32, 1) k_panel_reg(int n, int64_t ld, in
         const int k = k0 + q;
         const int buf = q & 1;
         if (threadIdx.x == 0) mbar_expect(&bar[buf], tx);
-        // 1. the warp's candidate: lane q holds column q of the warp's rows
-        //    (slots jmin.. are rows >= k; ascending rows: first on ties)
-        const int jmin = k > rw0 ? (k - rw0 + kRW - 1) / kRW : 0;
-        double best = -1.0;
-        int bj = -1;
-        if (lane == q) {
-#pragma unroll
-            for (int j = 0; j < RPW; ++j) {
-                const double a = fabs(val[j]);
-                if (j >= jmin && j < jend && a > best) { best = a; bj = j; }
-            }
-        }
-        best = __shfl_sync(0xffffffffu, best, q);
-        bj = __shfl_sync(0xffffffffu, bj, q);
-        if (lane == 0) { wv[w] = best; wi[w] = bj >= 0 ? rw0 + kRW * bj : n; }
         if (k >= r0 && k < r1 && (k - r0) % kRW == w) {  // the owner of row k pushes it
             const double x = pick_reg(val, (k - rw0) / kRW);
             const uint32_t la = smem_addr(&rowk[buf][lane]), lb = smem_addr(&bar[buf]);
             for (int c = 0; c < C; ++c) st_async(mapa(la, c), x, mapa(lb, c));
         }
-        __syncthreads();
-        if (w == 0) {  // the CTA's candidate, to every CTA (one lane per destination)
-            double bv;
-            int bx;
-            warp_argmax(lane < kRW ? wv[lane] : -1.0, lane < kRW ? wi[lane] : n, bv, bx);
-            if (bx >= n) bv = -1.0;
-            if (lane == 0) s_b = bx;
-            if (lane < C)
-                st_async2(mapa(smem_addr(&cand[buf][rank]), lane), bv, bx, mapa(smem_addr(&bar[buf]), lane));
-        }
-        __syncthreads();
-        const int cb = s_b;
-        if (cb < n ? (cb - r0) % kRW == w : w == 0) {  // its warp pushes the row (warp 0 if none)
-            const double x = cb < n ? pick_reg(val, (cb - rw0) / kRW) : 0.0;
-            const uint32_t la = smem_addr(&crow[buf][rank][lane]), lb = smem_addr(&bar[buf]);
-            for (int c = 0; c < C; ++c) st_async(mapa(la, c), x, mapa(lb, c));
+        int p = k;
+        if constexpr (kPivot) {
+            // 1. the warp's candidate: lane q holds column q of the warp's rows
+            //    (slots jmin.. are rows >= k; ascending rows: first on ties)
+            const int jmin = k > rw0 ? (k - rw0 + kRW - 1) / kRW : 0;
+            double best = -1.0;
+            int bj = -1;
+            if (lane == q) {
+#pragma unroll
+                for (int j = 0; j < RPW; ++j) {
+                    const double a = fabs(val[j]);
+                    if (j >= jmin && j < jend && a > best) { best = a; bj = j; }
+                }
+            }
+            best = __shfl_sync(0xffffffffu, best, q);
+            bj = __shfl_sync(0xffffffffu, bj, q);
+            if (lane == 0) { wv[w] = best; wi[w] = bj >= 0 ? rw0 + kRW * bj : n; }
+            __syncthreads();
+            if (w == 0) {  // the CTA's candidate, to every CTA (one lane per destination)
+                double bv;
+                int bx;
+                warp_argmax(lane < kRW ? wv[lane] : -1.0, lane < kRW ? wi[lane] : n, bv, bx);
+                if (bx >= n) bv = -1.0;
+                if (lane == 0) s_b = bx;
+                if (lane < C)
+                    st_async2(mapa(smem_addr(&cand[buf][rank]), lane), bv, bx, mapa(smem_addr(&bar[buf]), lane));
+            }
+            __syncthreads();
+            const int cb = s_b;
+            if (cb < n ? (cb - r0) % kRW == w : w == 0) {  // its warp pushes the row (warp 0 if none)
+                const double x = cb < n ? pick_reg(val, (cb - rw0) / kRW) : 0.0;
+                const uint32_t la = smem_addr(&crow[buf][rank][lane]), lb = smem_addr(&bar[buf]);
+                for (int c = 0; c < C; ++c) st_async(mapa(la, c), x, mapa(lb, c));
+            }
         }
         mbar_wait_cluster(&bar[buf], (q >> 1) & 1);
         // 2. global pivot (identical in every warp of every CTA), local reads
-        double gv;
-        int p;
-        warp_argmax(lane < C ? cand[buf][lane].v : -1.0, lane < C ? static_cast<int>(cand[buf][lane].i) : n,
-                    gv, p);
-        const double v = p < n ? crow[buf][p / R][q] : 0.0;
-        if (!(fabs(v) >= 1e-300)) {
+        if constexpr (kPivot) {
+            double gv;
+            warp_argmax(lane < C ? cand[buf][lane].v : -1.0, lane < C ? static_cast<int>(cand[buf][lane].i) : n,
+                        gv, p);
+        }
+        const double v = kPivot ? (p < n ? crow[buf][p / R][q] : 0.0) : rowk[buf][q];
+        // (without pivoting: positive pivots of a symmetric matrix = SPD)
+        if (!(kPivot ? fabs(v) >= 1e-300 : v >= kNoPivotTol)) {
             if (rank == 0 && threadIdx.x == 0) {
                 if (atomicCAS(&err->code, 0, SAMG_ERROR) == 0) err->where = k;
                 for (int t = q; t < bk; ++t) piv[t] = k0 + t;  // keep later kernels in bounds
@@ -339,7 +354,7 @@ __global__ void __launch_bounds__(kRW * 32, 1) k_panel_reg(int n, int64_t ld, in
             break;  // uniform across the cluster
         }
         const double inv = 1.0 / v;
-        const double rl = (lane == q ? 1.0 : crow[buf][p / R][lane]) * inv;
+        const double rl = (lane == q ? 1.0 : (kPivot ? crow[buf][p / R][lane] : rowk[buf][lane])) * inv;
         const double kq = rowk[buf][q], kl = rowk[buf][lane];
         if (rank == 0 && threadIdx.x == 0) piv[q] = p;
         // 3. eliminate column q in registers; column q becomes column k of
@@ -350,7 +365,7 @@ __global__ void __launch_bounds__(kRW * 32, 1) k_panel_reg(int n, int64_t ld, in
             const double f = __shfl_sync(0xffffffffu, val[j], q);
             val[j] = lq ? -f * inv : fma(-f, rl, val[j]);
         }
-        if (p >= r0 && p < r1 && (p - r0) % kRW == w)
+        if (kPivot && p >= r0 && p < r1 && (p - r0) % kRW == w)
             set_reg(val, (p - rw0) / kRW, lq ? -kq * inv : fma(-kq, rl, kl));
         if (k >= r0 && k < r1 && (k - r0) % kRW == w) set_reg(val, (k - rw0) / kRW, rl);
     }
@@ -551,6 +566,30 @@ __global__ void __launch_bounds__(kTThreads, 2) k_trailing(int64_t n, int64_t ld
 // cond(A) ~ 1e30 while cond(SAS) is modest; the reference's dense LU solve
 // is backward stable there, an explicit inverse of the unscaled A is not.
 // A^-1 = S (S A S)^-1 S (k_gather_cols).
+// max |X_ij - X_ji| and max |X_ij| (as ordered bit patterns of
+// non-negative doubles): the no-pivot elimination is tried only for a
+// matrix symmetric to rounding
+__global__ void k_sym_check(int64_t n, int64_t ld, const double *__restrict__ X,
+                            unsigned long long *out) {
+    unsigned long long d = 0, m = 0;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n * n;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = e / n, j = e - i * n;
+        const double a = X[i * ld + j];
+        m = max(m, static_cast<unsigned long long>(__double_as_longlong(fabs(a))));
+        if (j > i)
+            d = max(d, static_cast<unsigned long long>(__double_as_longlong(fabs(a - X[j * ld + i]))));
+    }
+    for (int off = 16; off >= 1; off >>= 1) {
+        d = max(d, __shfl_xor_sync(0xffffffffu, d, off));
+        m = max(m, __shfl_xor_sync(0xffffffffu, m, off));
+    }
+    if (threadIdx.x % 32 == 0) {
+        atomicMax(out, d);
+        atomicMax(out + 1, m);
+    }
+}
+
 __global__ void k_equilibrate(int64_t n, int64_t ld, double *X, double *sc) {
     const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (i >= n) return;
@@ -684,73 +723,109 @@ bool dense_inverse(const Bsr3 &A, DevBuf<double> &Ainv, DevError *err, cudaStrea
     DevBuf<double> X(n * ld, s), Rk(static_cast<int64_t>(pp.kB) * n + 1, s),
         T(static_cast<int64_t>(2 * pp.kB) * n + 1, s);
     DevBuf<int64_t> piv(pp.kB, s), piv_all(n, s), perm(n, s), mv(1 + 2 * kMv, s);
-    CK(cudaMemsetAsync(X.p, 0, X.bytes(), s));
-    k_scatter<<<ceil_div(A.nrows, 128), 128, 0, s>>>(static_cast<int>(A.nrows), A.ptr.p, A.col.p,
-                                                    A.val.p, ld, X.p);
     DevBuf<double> sc(n, s);
-    k_equilibrate<<<ceil_div(n, 256), 256, 0, s>>>(n, ld, X.p, sc.p);
-    k_scale_sym<<<grid_for(n * ld), 256, 0, s>>>(n, ld, sc.p, X.p);
-    CK_LAUNCH();
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(pp.C);
-    cfg.blockDim = dim3(pp.reg ? pp.nw * 32 : kPT);
-    cfg.dynamicSmemBytes = pp.smem;
-    cfg.stream = s;
-    cudaLaunchAttribute at{};
-    at.id = cudaLaunchAttributeClusterDimension;
-    at.val.clusterDim.x = pp.C;
-    at.val.clusterDim.y = 1;
-    at.val.clusterDim.z = 1;
-    cfg.attrs = &at;
-    cfg.numAttrs = 1;
-    const dim3 tg(static_cast<unsigned>((n + kTT - 1) / kTT), static_cast<unsigned>((n + kTT - 1) / kTT));
-    for (int64_t k0 = 0; k0 < n; k0 += pp.kB) {
-        const int bk = static_cast<int>(std::min<int64_t>(pp.kB, n - k0));
-        if (pp.reg) {
-            dispatch_rpw(pp.rpw, pp.nw, [&](auto r, auto nw) {
-                constexpr int RPW = decltype(r)::value, NW = decltype(nw)::value;
-                static DeviceCache nonportable;
-                nonportable.get([] {
-                    const bool ok = cudaFuncSetAttribute(k_panel_reg<RPW, NW>,
-                                        cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
-                    cudaGetLastError();
-                    return ok ? 1 : 0;
-                });
-                CK(cudaLaunchKernelEx(&cfg, k_panel_reg<RPW, NW>, static_cast<int>(n), ld,
-                                      static_cast<int>(k0), bk, pp.R, X.p, piv.p, err));
-            });
-        } else {
-            CK(cudaLaunchKernelEx(&cfg, k_panel_cluster, n, ld, k0, bk, pp.kB, pp.R, X.p, piv.p, err));
-        }
-        k_copy_piv<<<1, kMaxB, 0, s>>>(bk, piv.p, piv_all.p + k0);
-        k_moves_build<<<1, 32, 0, s>>>(k0, bk, piv.p, mv.p);
-        k_moves_gather<<<grid_for(2 * bk * n), 256, 0, s>>>(n, ld, mv.p, X.p, T.p);
-        k_moves_apply<<<grid_for(3 * bk * n), 256, 0, s>>>(n, ld, k0, bk, mv.p, T.p, X.p, Rk.p);
-        k_trailing<<<tg, kTThreads, 0, s>>>(n, ld, k0, bk, Rk.p, X.p);
+    // SPD coarse operators (SA-AMG Galerkin products of SPD matrices) are
+    // inverted without row exchanges first (k_panel_reg<.., false>); a pivot
+    // below kNoPivotTol of the equilibrated matrix falls back to the
+    // partially pivoted elimination.  SAMG_GJ_NOPIVOT=0 always pivots.
+    static const bool try_nopivot = [] {
+        const char *e = std::getenv("SAMG_GJ_NOPIVOT");
+        return !(e && e[0] == '0');
+    }();
+    auto run = [&](bool pivot) {
+        CK(cudaMemsetAsync(X.p, 0, X.bytes(), s));
+        k_scatter<<<ceil_div(A.nrows, 128), 128, 0, s>>>(static_cast<int>(A.nrows), A.ptr.p, A.col.p,
+                                                        A.val.p, ld, X.p);
+        k_equilibrate<<<ceil_div(n, 256), 256, 0, s>>>(n, ld, X.p, sc.p);
+        k_scale_sym<<<grid_for(n * ld), 256, 0, s>>>(n, ld, sc.p, X.p);
         CK_LAUNCH();
+        if (!pivot) CK(cudaMemsetAsync(mv.p, 0, mv.bytes(), s));  // no row moves
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(pp.C);
+        cfg.blockDim = dim3(pp.reg ? pp.nw * 32 : kPT);
+        cfg.dynamicSmemBytes = pp.smem;
+        cfg.stream = s;
+        cudaLaunchAttribute at{};
+        at.id = cudaLaunchAttributeClusterDimension;
+        at.val.clusterDim.x = pp.C;
+        at.val.clusterDim.y = 1;
+        at.val.clusterDim.z = 1;
+        cfg.attrs = &at;
+        cfg.numAttrs = 1;
+        const dim3 tg(static_cast<unsigned>((n + kTT - 1) / kTT), static_cast<unsigned>((n + kTT - 1) / kTT));
+        for (int64_t k0 = 0; k0 < n; k0 += pp.kB) {
+            const int bk = static_cast<int>(std::min<int64_t>(pp.kB, n - k0));
+            if (pp.reg) {
+                dispatch_rpw(pp.rpw, pp.nw, [&](auto r, auto nw) {
+                    constexpr int RPW = decltype(r)::value, NW = decltype(nw)::value;
+                    auto launch = [&](auto kern) {
+                        // (per kernel and device; cheap, so set before every launch)
+                        if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+                            cudaSuccess)
+                            cudaGetLastError();
+                        CK(cudaLaunchKernelEx(&cfg, kern, static_cast<int>(n), ld, static_cast<int>(k0), bk, pp.R,
+                                              X.p, piv.p, err));
+                    };
+                    if (pivot) launch(k_panel_reg<RPW, NW, true>);
+                    else launch(k_panel_reg<RPW, NW, false>);
+                });
+            } else {
+                CK(cudaLaunchKernelEx(&cfg, k_panel_cluster, n, ld, k0, bk, pp.kB, pp.R, X.p, piv.p, err));
+            }
+            if (pivot) {
+                k_copy_piv<<<1, kMaxB, 0, s>>>(bk, piv.p, piv_all.p + k0);
+                k_moves_build<<<1, 32, 0, s>>>(k0, bk, piv.p, mv.p);
+                k_moves_gather<<<grid_for(2 * bk * n), 256, 0, s>>>(n, ld, mv.p, X.p, T.p);
+            }
+            k_moves_apply<<<grid_for(3 * bk * n), 256, 0, s>>>(n, ld, k0, bk, mv.p, T.p, X.p, Rk.p);
+            k_trailing<<<tg, kTThreads, 0, s>>>(n, ld, k0, bk, Rk.p, X.p);
+            CK_LAUNCH();
+        }
+        // column permutation of the in-place algorithm: every swap undone in
+        // reverse order (composed on the host, n steps); identity without pivoting
+        std::vector<int64_t> hperm(n);
+        for (int64_t j = 0; j < n; ++j) hperm[j] = j;
+        if (pivot) {
+            std::vector<int64_t> hp(n);
+            CK(cudaMemcpyAsync(hp.data(), piv_all.p, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            for (int64_t k = n - 1; k >= 0; --k) {
+                const int64_t p = std::min<int64_t>(std::max<int64_t>(hp[k], 0), n - 1);
+                std::swap(hperm[k], hperm[p]);
+            }
+        }
+        CK(cudaMemcpyAsync(perm.p, hperm.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
+        k_gather_cols<<<grid_for(n * ld), 256, 0, s>>>(n, ld, perm.p, X.p, sc.p, Ainv.p);
+        CK_LAUNCH();
+        DevError h{};
+        CK(cudaMemcpyAsync(&h, err, sizeof h, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));  // (hperm outlives the copy)
+        if (h.code == SAMG_ERROR) {  // a pivot below the bound: report, let the caller fall back
+            CK(cudaMemsetAsync(err, 0, sizeof(DevError), s));
+            return false;
+        }
+        check_dev_error(err, s);
+        return true;
+    };
+    bool symmetric = false;
+    if (try_nopivot && pp.reg) {
+        CK(cudaMemsetAsync(X.p, 0, X.bytes(), s));
+        k_scatter<<<ceil_div(A.nrows, 128), 128, 0, s>>>(static_cast<int>(A.nrows), A.ptr.p, A.col.p,
+                                                        A.val.p, ld, X.p);
+        DevBuf<unsigned long long> dm(2, s);
+        CK(cudaMemsetAsync(dm.p, 0, dm.bytes(), s));
+        k_sym_check<<<grid_for(n * n), 256, 0, s>>>(n, ld, X.p, dm.p);
+        CK_LAUNCH();
+        unsigned long long h[2];
+        CK(cudaMemcpyAsync(h, dm.p, sizeof h, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        double dv, mv_;
+        std::memcpy(&dv, &h[0], 8);
+        std::memcpy(&mv_, &h[1], 8);
+        symmetric = dv <= 1e-12 * mv_;
     }
-    // column permutation of the in-place algorithm: every swap undone in
-    // reverse order (composed on the host, n steps)
-    std::vector<int64_t> hp(n), hperm(n);
-    CK(cudaMemcpyAsync(hp.data(), piv_all.p, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    for (int64_t j = 0; j < n; ++j) hperm[j] = j;
-    for (int64_t k = n - 1; k >= 0; --k) {
-        const int64_t p = std::min<int64_t>(std::max<int64_t>(hp[k], 0), n - 1);
-        std::swap(hperm[k], hperm[p]);
-    }
-    CK(cudaMemcpyAsync(perm.p, hperm.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
-    k_gather_cols<<<grid_for(n * ld), 256, 0, s>>>(n, ld, perm.p, X.p, sc.p, Ainv.p);
-    CK_LAUNCH();
-    DevError h{};
-    CK(cudaMemcpyAsync(&h, err, sizeof h, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    if (h.code == SAMG_ERROR) {  // pivot below 1e-300: report, let the caller fall back
-        CK(cudaMemsetAsync(err, 0, sizeof(DevError), s));
-        return false;
-    }
-    check_dev_error(err, s);
-    return true;
+    if (symmetric && run(false)) return true;
+    return run(true);
 }
 
 } // namespace samgb
