@@ -1689,8 +1689,9 @@ void launch_dense_gemv(int64_t n, const double *Ainv, const double *f, double *u
             const int stages = static_cast<int>(std::min<int64_t>(16, (227 * 1024 - 384 - 8 * ld) / (8 * ld)));
             const size_t smem = 384 + static_cast<size_t>(8 * ld) * (stages + 1);
             const int grid = static_cast<int>(std::min<int64_t>(sm_count(), n));
+            static const int gemv_ef = env_int("SAMG_GEMV_EVICT_FIRST", 1);
             launch_k(false, k_dense_gemv_tma, grid, 32 * (kGemvWarps + 1), smem, s, static_cast<int>(n), ld, Ainv, f,
-                     u, stages, 0);
+                     u, stages, l2_hints() && gemv_ef ? 1 : 0);
             CK_LAUNCH();
             return;
         }

@@ -4,7 +4,7 @@ whole solve in host-loop mode (SAMG_CG_GRAPH=0: the kernels of the graph's
 conditional body are not reported by CUPTI).  Kernels are grouped by name; per-iteration time =
 total / iterations for kernels launched once per iteration.
 
-    python scripts/iter_timeline.py [C1|C4] [--json OUT] [ENV=V ...]"""
+    python scripts/iter_timeline.py [C1|C4] [smoother] [--json OUT] [ENV=V ...]"""
 import collections
 import json
 import os
@@ -24,6 +24,7 @@ for a in [a for a in args if "=" in a]:
     os.environ[k] = v
     args.remove(a)
 cfg = args[0] if args else "C1"
+smoother = args[1] if len(args) > 1 else "spai0"
 import torch  # noqa: E402
 from torch.profiler import ProfilerActivity, profile  # noqa: E402
 
@@ -32,7 +33,7 @@ import paper_2202_09056_b200 as pb  # noqa: E402
 C = {"C1": dict(nx=63, ny=63, nz=63, dirichlet="eliminate", noise=0.01, seed=2022),
      "C4": dict(nx=199, ny=199, nz=199, dirichlet="eliminate", noise=0.01, seed=2022)}[cfg]
 dp = pb.generate_hex_device(pb.ProblemParams(**C), device=0)
-h = pb.setup_device(dp.A, dp.nullspace_ptr, 6, "ns_block", pb.AmgParams(smoother="spai0"))
+h = pb.setup_device(dp.A, dp.nullspace_ptr, 6, "ns_block", pb.AmgParams(smoother=smoother))
 u = torch.zeros(dp.n, dtype=torch.float64, device="cuda")
 for _ in range(2):
     rep = h.cg_solve_device(dp.rhs_ptr, u.data_ptr())
@@ -64,6 +65,14 @@ for n, t in rows:
     print(f"{t / its:9.2f} us/it  n={cnt[n]:6d}  {t / cnt[n]:8.2f} us/launch  {n[:100]}")
     res.append({"kernel": n[:120], "us_per_iteration": t / its, "launches": cnt[n],
                 "us_per_launch": t / cnt[n]})
+# one iteration in launch order (between the 2nd and 3rd q = A p kernels)
+evs = sorted([e for e in prof.events() if e.device_type.name == "CUDA"], key=lambda e: e.time_range.start)
+marks = [k for k, e in enumerate(evs) if "EpiDot" in e.name]
+if len(marks) >= 3:
+    print("one iteration in launch order:")
+    for e in evs[marks[1]:marks[2]]:
+        nm = e.name.replace("(anonymous namespace)::", "").split("(")[0].replace("samgb::", "").replace("void ", "")
+        print(f"   {(e.time_range.end - e.time_range.start):9.2f} us  {nm[:90]}")
 if out_json:
     json.dump({"config": cfg, "iterations": its, "solve_ms": rep["solve_seconds"] * 1e3,
                "busy_ms": busy / 1e3, "span_ms": (t_last - t_first) / 1e3, "kernels": res},
