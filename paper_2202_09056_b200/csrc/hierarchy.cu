@@ -346,6 +346,16 @@ Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int6
     H->build_tail();
     CK(cudaStreamSynchronize(s));
     mark("workspace", L - 1);
+    if (timing) {  // the pool's high-water mark over this setup (SAMG_POOL_RESERVE tuning)
+        cudaMemPool_t pool;
+        uint64_t high = 0, reserved = 0, used = 0;
+        if (cudaDeviceGetDefaultMemPool(&pool, H->device) == cudaSuccess &&
+            cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &high) == cudaSuccess &&
+            cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) == cudaSuccess &&
+            cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess)
+            std::fprintf(stderr, "setup pool after: used %.2f GB (high-water %.2f GB) reserved %.2f GB\n",
+                         used / 1e9, high / 1e9, reserved / 1e9);
+    }
     H->setup_seconds = now_s() - t_start;
     H->owns_stream = true;
     return H.release();

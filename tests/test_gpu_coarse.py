@@ -92,3 +92,44 @@ def test_coarse_level_inverse(gpu):
     D = dense_of(nr, ptr, col, val.reshape(-1))
     X = Ac.dense_inverse()
     assert np.abs(D @ X - np.eye(3 * nr)).max() <= 1e-9
+
+
+def spd_bsr3(nb, density, rng, shift):
+    """Symmetric block pattern and values (A = M + M^T + shift I): SPD for a
+    large enough shift, indefinite for a small one."""
+    D = np.zeros((3 * nb, 3 * nb))
+    for i in range(nb):
+        for c in set(rng.choice(nb, size=max(1, int(density * nb)), replace=False)) | {i}:
+            D[3 * i:3 * i + 3, 3 * c:3 * c + 3] += rng.standard_normal((3, 3))
+    D = D + D.T + shift * np.eye(3 * nb)
+    ptr, col, val = [0], [], []
+    for i in range(nb):
+        for c in range(nb):
+            blk = D[3 * i:3 * i + 3, 3 * c:3 * c + 3]
+            if np.any(blk != 0.0):
+                col.append(c)
+                val.append(blk)
+        ptr.append(len(col))
+    return np.array(ptr, np.int64), np.array(col, np.int64), np.array(val).reshape(-1), D
+
+
+@pytest.mark.parametrize("nb,shift", [(700, 40.0), (973, 60.0), (500, 0.5)])
+def test_dense_inverse_symmetric(gpu, nb, shift):
+    """Symmetric coarse operators take the Gauss-Jordan path without row
+    exchanges (k_panel_reg<.., false>) when every pivot of the equilibrated
+    matrix stays positive (SPD; large shift, odd and even n), and fall back to
+    partial pivoting when one does not (indefinite; small shift): the inverse
+    is accurate either way."""
+    pb = gpu
+    rng = np.random.default_rng(nb)
+    ptr, col, val, D = spd_bsr3(nb, 0.01, rng, shift)
+    if shift > 1.0:
+        assert np.linalg.eigvalsh(D).min() > 0.0
+    else:
+        assert np.linalg.eigvalsh(D).min() < 0.0
+    A = pb.Bsr3.from_host(nb, nb, ptr, col, val)
+    X = A.dense_inverse()
+    cond = np.linalg.cond(D)
+    ref = np.linalg.inv(D)
+    assert np.abs(X - ref).max() <= (1e-15 * cond * 3 * nb + 1e-13) * np.abs(ref).max(), cond
+    assert np.abs(D @ X - np.eye(3 * nb)).max() <= 1e-14 * cond * 3 * nb + 1e-12
