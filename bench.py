@@ -174,6 +174,33 @@ def config_dict(p, world):
             "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"}
 
 
+def dist_problem_kw(world):
+    """The N > 1 SpMV workload: a cantilever of `world` C1-sized slabs (63
+    x-planes of 64 x 64 nodes per GPU, x slowest, so a rank owns contiguous
+    planes), free-DOF form."""
+    return dict(nx=63 * world, ny=63, nz=63, lx=float(world), dirichlet="eliminate", noise=0.01,
+                seed=2022, x_slowest=True)
+
+
+class Whole:
+    """Global sizes of the N-slab problem (for dist_config on the b200 arm,
+    where each rank generates only its slab)."""
+
+    def __init__(self, n, nbrows, nnzb):
+        self.n, self.nbrows, self.nnzb = n, nbrows, nnzb
+
+
+def dist_config(world, p):
+    """The N > 1 `config` object, identical in both arms."""
+    return {"workload": f"cantilever {63 * world}x63x63 hex8 elements (x slowest), free-DOF, one "
+                        f"C1-sized slab (258,048 block rows) per GPU, row-partitioned SpMV with an "
+                        f"NCCL halo exchange per step",
+            "unknowns": p.n, "block_rows": p.nbrows, "nnzb": p.nnzb,
+            "spmv_bytes_per_step": spmv_bytes(p),
+            "l2": "no flush: per-GPU matrix stream > 126 MB L2",
+            "parallelism": f"row partition x{world} (NCCL P2P halo)"}
+
+
 def cpu_reference_spmv(p, seconds, steps=None):
     """The reference's spmv<static_block<3>> (csr.hpp:129-160) from
     oracle/_ref on one host core over the C1 matrix: time-bounded sample."""
@@ -254,7 +281,9 @@ def run_reference(args, rank, world, dist):
         return
     from oracle.oracle import Params, Ref, SM_SPAI0
     ref = Ref()
-    p = ref.gen_hex(**C1)
+    # the same workload as the b200 arm at this N: C1 on one GPU, the
+    # N-slab cantilever of the row-partitioned SpMV above
+    p = ref.gen_hex(**(C1 if world == 1 else dist_problem_kw(world)))
     nbytes = spmv_bytes(p)
     # each step: one full SpMV (5 ms class on all threads); bound the run
     steps = args.steps
@@ -268,7 +297,11 @@ def run_reference(args, rank, world, dist):
     gbs = nbytes / t / 1e9
     t1 = statistics.median(cpu_reference_spmv(p, 0, steps=5))
     amg = None
-    if os.environ.get("SAMG_BENCH_REF_AMG", "1") == "1":
+    if world > 1:
+        amg = {"note": "the b200 arm's N > 1 AMG leg strong-scales C4 / C3; the reference's C4 "
+                       "setup takes 182 s and its solve about 1.5 h on one core (DESIGN.md section 3): "
+                       "not run here"}
+    elif os.environ.get("SAMG_BENCH_REF_AMG", "1") == "1":
         n, ptr, col, val = p.csr()
         B = p.nullspace()
         h = ref.setup(n, ptr, col, val, B, Params(smoother=SM_SPAI0))
@@ -284,9 +317,10 @@ def run_reference(args, rank, world, dist):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_dict(p, world),
+        "config": config_dict(p, world) if world == 1 else dist_config(world, p),
         "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "reference",
-                         "sample": f"{len(times)} x samg::spmv<static_block<3>> over the full C1 "
+                         "sample": f"{len(times)} x samg::spmv<static_block<3>> over the full "
+                                   f"{'C1' if world == 1 else 'cantilever'} "
                                    f"matrix (median), oracle/_ref, {cores} threads on row slices "
                                    f"of equal block count (the reference is single-threaded: "
                                    f"one thread runs {nbytes / t1 / 1e9:.2f} GB/s)",
@@ -559,8 +593,7 @@ def run_b200_dist(args, rank, world, local, dist):
     from paper_2202_09056_b200.dist import DistMatrix, Halo, exchange_plan
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    pp = pb.ProblemParams(nx=63 * world, ny=63, nz=63, lx=float(world), dirichlet="eliminate",
-                          noise=0.01, seed=2022, x_slowest=True)
+    pp = pb.ProblemParams(**dist_problem_kw(world))
     per_plane = 64 * 64
     starts = np.array([63 * r * per_plane for r in range(world + 1)], dtype=np.int64)
     r0, r1 = int(starts[rank]), int(starts[rank + 1])
@@ -600,9 +633,10 @@ def run_b200_dist(args, rank, world, local, dist):
     t = torch.tensor([ms], device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
-    tb = torch.tensor([float(nbytes)], device=dev, dtype=torch.float64)
+    tb = torch.tensor([float(nbytes), float(mine.nnzb)], device=dev, dtype=torch.float64)
     dist.all_reduce(tb)
-    total_bytes = float(tb.item())
+    total_bytes = float(tb[0].item())
+    nnzb_total = int(tb[1].item())
     ms_per = ms / args.steps
     value = total_bytes / (ms_per * 1e-3) / 1e9
     # e2e: host x_local in, host y_local out, same distributed step
@@ -631,13 +665,9 @@ def run_b200_dist(args, rank, world, local, dist):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"cantilever {63 * world}x63x63 hex8 elements (x slowest), "
-                                   f"free-DOF, one C1-sized slab (258,048 block rows) per GPU, "
-                                   f"row-partitioned SpMV with NCCL halo exchange per step",
-                       "block_rows_rank0": nloc, "ghost_block_rows_rank0": ngh,
-                       "interior_rows_rank0": inf["ninterior"], "nnzb_rank0": mine.nnzb,
-                       "l2": "no flush: per-GPU matrix stream > 126 MB L2",
-                       "parallelism": f"row partition x{world} (NCCL P2P halo)"},
+            "config": dist_config(world, Whole(3 * 258048 * world, 258048 * world, nnzb_total)),
+            "partition": {"block_rows_rank0": nloc, "ghost_block_rows_rank0": ngh,
+                          "interior_rows_rank0": inf["ninterior"], "nnzb_rank0": mine.nnzb},
             "roofline": {"bound": "hbm", "achieved": gb_rank, "peak": peak, "unit": "GB/s",
                          "frac": gb_rank / peak, "traffic": ncu_traffic(),
                          "peak_source": peak_src, **read_peak_fields(gb_rank),
