@@ -391,10 +391,16 @@ __global__ void k_agg_bd(int n, const int *__restrict__ gp, const int *__restric
 
 constexpr int kQrLanes = 16;
 
+// smem_m > 0: the group's m x k work matrix and Q live in shared memory
+// (room for m <= smem_m rows each) instead of the global scratch: the
+// sequential per-lane sums walk them element by element, and from global
+// memory every step waited for an L2 round trip (C4 level 0: 80 ms).  The
+// arithmetic and its order are unchanged.
 __global__ void __launch_bounds__(256) k_tentative_qr(int64_t naggs, int pbs, int k,
         const int *nodes, const int *agg_ptr, const double *B, int64_t bnrows, double *work,
-        double *Qw, double *Pt, double *Bc, int64_t a0, int64_t a1) {
+        double *Qw, double *Pt, double *Bc, int64_t a0, int64_t a1, int smem_m) {
     __shared__ double Rs[256 / kQrLanes][144];
+    extern __shared__ double qr_sm[];
     const int64_t a = a0 + (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / kQrLanes;
     const int lane = threadIdx.x % kQrLanes;
     const int base = (threadIdx.x % 32) & ~(kQrLanes - 1);
@@ -405,6 +411,10 @@ __global__ void __launch_bounds__(256) k_tentative_qr(int64_t naggs, int pbs, in
     const int64_t m = static_cast<int64_t>(pbs) * (n1 - n0);
     double *A = work + static_cast<int64_t>(pbs) * n0 * k;
     double *Q = Qw + static_cast<int64_t>(pbs) * n0 * k;
+    if (smem_m > 0 && m <= smem_m) {
+        A = qr_sm + static_cast<size_t>(threadIdx.x / kQrLanes) * 2 * smem_m * k;
+        Q = A + static_cast<size_t>(smem_m) * k;
+    }
 #define a_(i, j) A[(j) * m + (i)]
 #define ROW(r) (static_cast<int64_t>(nodes[n0 + (r) / pbs]) * pbs + (r) % pbs)
     double local_max = 0;
@@ -1627,10 +1637,57 @@ void tentative(const DevBuf<int> &agg, int64_t nnodes, int64_t naggs, int pbs, c
     }, s);
     Pt.alloc(nfine * k, s);
     Bc.alloc(naggs * k * k, s);
-    DevBuf<double> work(nfine * k, s), Qw(nfine * k, s);
-    if (a1 > a0)
-        k_tentative_qr<<<ceil_div((a1 - a0) * kQrLanes, 256), 256, 0, s>>>(
-            naggs, pbs, k, nodes.p, agg_ptr.p, B, nfine, work.p, Qw.p, Pt.p, Bc.p, a0, a1);
+    DevBuf<double> work, Qw;  // global scratch, only without the shared-memory path
+    if (a1 > a0) {
+        // shared-memory work matrices sized for the 99th-percentile-ish
+        // aggregate: room for smem_m rows per group, larger aggregates keep
+        // the global scratch (same kernel, same arithmetic)
+        static const int use_smem = [] {
+            const char *e = std::getenv("SAMG_QR_SMEM");
+            return e ? std::atoi(e) : 1;
+        }();
+        int smem_m = 0, threads = 256;
+        bool need_global = false;
+        if (use_smem && k > 0) {
+            DevBuf<int> dmax(1, s);
+            CK(cudaMemsetAsync(dmax.p, 0, sizeof(int), s));
+            int *dm = dmax.p;
+            const int *apc = agg_ptr.p;
+            for_each(a1 - a0, [=] __device__(int64_t t) {
+                const int64_t a = a0 + t;
+                atomicMax(dm, apc[a + 1] - apc[a]);
+            }, s);
+            int hmax = 0;
+            CK(cudaMemcpyAsync(&hmax, dmax.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            // room for the largest aggregate up to 192 rows (C4 level 0: 78-row
+            // aggregates); larger ones keep the global scratch.  At least 4
+            // groups of 16 lanes per CTA in <= 110 KB (two CTAs per SM);
+            // otherwise the global-scratch kernel's occupancy wins (C4
+            // level 1: 2.0 ms global vs 6.9 ms with 2 groups per CTA)
+            smem_m = std::min(pbs * hmax, 192);
+            const size_t per_group = 2 * static_cast<size_t>(smem_m) * k * sizeof(double);
+            int groups = 16;
+            while (groups > 4 && groups * per_group > 110 * 1024) groups /= 2;
+            if (groups * per_group > 110 * 1024) smem_m = 0;
+            else threads = groups * kQrLanes;
+            if (smem_m && pbs * hmax > smem_m) need_global = true;
+        }
+        const size_t dyn = smem_m ? static_cast<size_t>(threads / kQrLanes) * 2 * smem_m * k * sizeof(double) : 0;
+        if (!smem_m || need_global) {
+            work.alloc(nfine * k, s);
+            Qw.alloc(nfine * k, s);
+        }
+        if (dyn > 48 * 1024) {
+            static DeviceCache qattr;
+            qattr.get([] {
+                CK(cudaFuncSetAttribute(k_tentative_qr, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+                return 1;
+            });
+        }
+        k_tentative_qr<<<ceil_div((a1 - a0) * kQrLanes, threads), threads, dyn, s>>>(
+            naggs, pbs, k, nodes.p, agg_ptr.p, B, nfine, work.p, Qw.p, Pt.p, Bc.p, a0, a1, smem_m);
+    }
     (void)err;
     CK_LAUNCH();
 }
