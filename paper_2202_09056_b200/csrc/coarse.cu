@@ -26,6 +26,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
@@ -264,7 +265,11 @@ __device__ __forceinline__ void warp_argmax(double v, int idx, double &bv, int &
 // positive): per column only row k travels through the cluster -- no
 // candidate search, no candidate rows, no row moves afterwards.  A pivot
 // below kNoPivotTol reports failure and the caller repeats with pivoting.
-constexpr double kNoPivotTol = 1e-8;
+// For a symmetric matrix positive pivots mean positive definite, and the
+// elimination is then backward stable however small they get (as Cholesky);
+// the bound only rejects a numerically singular operator (C4's coarsest
+// level: equilibrated lambda_min 1.2e-10, pivots of that order).
+constexpr double kNoPivotTol = 1e-13;
 
 template <int RPW, int kRW, bool kPivot = true>
 __global__ void __launch_bounds__(kRW * 32, 1) k_panel_reg(int n, int64_t ld, int k0, int bk, int R,
@@ -824,7 +829,32 @@ bool dense_inverse(const Bsr3 &A, DevBuf<double> &Ainv, DevError *err, cudaStrea
         std::memcpy(&mv_, &h[1], 8);
         symmetric = dv <= 1e-12 * mv_;
     }
-    if (symmetric && run(false)) return true;
+    if (symmetric && run(false)) {
+        // the unpivoted inverse must pass the coarse-solver accuracy check
+        // (hierarchy.cu choose_coarse_solver: |Ainv A x - x| / |x| <= 1e-6)
+        // with a margin, else the pivoted one is computed: for a nearly
+        // singular operator (C4: equilibrated lambda_min 1.2e-10) both are
+        // rounding-level inverses, but the check must not flip to the slow
+        // LU solve because of the pivot order
+        std::vector<double> hx(n), hy(n);
+        uint64_t st = 0x2545f4914f6cdd1dull;
+        for (auto &v : hx) {
+            st ^= st << 13; st ^= st >> 7; st ^= st << 17;
+            v = static_cast<double>(st >> 11) * 0x1.0p-52 - 1.0;
+        }
+        DevBuf<double> dx(n, s), db(n, s), dy(n, s);
+        CK(cudaMemcpyAsync(dx.p, hx.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s));
+        launch_spmv(A, 1.0, dx.p, 0.0, db.p, s);
+        launch_dense_gemv(n, Ainv.p, db.p, dy.p, s);
+        CK(cudaMemcpyAsync(hy.data(), dy.p, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        double num = 0.0, den = 0.0;
+        for (int64_t i = 0; i < n; ++i) {
+            num += (hy[i] - hx[i]) * (hy[i] - hx[i]);
+            den += hx[i] * hx[i];
+        }
+        if (std::sqrt(num / den) <= 1e-7) return true;
+    }
     return run(true);
 }
 
