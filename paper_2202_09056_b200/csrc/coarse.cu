@@ -46,11 +46,13 @@ constexpr int kMaxCluster = 16;
 
 // scatter A (BSR3) into X (row-major, leading dimension ld; to_dense,
 // csr.hpp:370-382)
+// a warp per block row, a lane per block (a thread per row serialised the
+// ~120-block coarse rows: 0.7 ms at C1)
 __global__ void k_scatter(int nrows, const int *ptr, const int *col, const double *val,
                           int64_t ld, double *X) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
     if (i >= nrows) return;
-    for (int j = ptr[i]; j < ptr[i + 1]; ++j)
+    for (int j = ptr[i] + lane; j < ptr[i + 1]; j += 32)
         for (int r = 0; r < 3; ++r)
             for (int c = 0; c < 3; ++c)
                 X[(3 * static_cast<int64_t>(i) + r) * ld + 3 * static_cast<int64_t>(col[j]) + c] =
@@ -739,7 +741,7 @@ bool dense_inverse(const Bsr3 &A, DevBuf<double> &Ainv, DevError *err, cudaStrea
     }();
     auto run = [&](bool pivot) {
         CK(cudaMemsetAsync(X.p, 0, X.bytes(), s));
-        k_scatter<<<ceil_div(A.nrows, 128), 128, 0, s>>>(static_cast<int>(A.nrows), A.ptr.p, A.col.p,
+        k_scatter<<<ceil_div(A.nrows * 32, 256), 256, 0, s>>>(static_cast<int>(A.nrows), A.ptr.p, A.col.p,
                                                         A.val.p, ld, X.p);
         k_equilibrate<<<ceil_div(n, 256), 256, 0, s>>>(n, ld, X.p, sc.p);
         k_scale_sym<<<grid_for(n * ld), 256, 0, s>>>(n, ld, sc.p, X.p);
@@ -815,7 +817,7 @@ bool dense_inverse(const Bsr3 &A, DevBuf<double> &Ainv, DevError *err, cudaStrea
     bool symmetric = false;
     if (try_nopivot && pp.reg) {
         CK(cudaMemsetAsync(X.p, 0, X.bytes(), s));
-        k_scatter<<<ceil_div(A.nrows, 128), 128, 0, s>>>(static_cast<int>(A.nrows), A.ptr.p, A.col.p,
+        k_scatter<<<ceil_div(A.nrows * 32, 256), 256, 0, s>>>(static_cast<int>(A.nrows), A.ptr.p, A.col.p,
                                                         A.val.p, ld, X.p);
         DevBuf<unsigned long long> dm(2, s);
         CK(cudaMemsetAsync(dm.p, 0, dm.bytes(), s));
