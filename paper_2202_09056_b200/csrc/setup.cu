@@ -646,6 +646,85 @@ __global__ void k_psm_vals(int64_t nsc, int pbs, int h, int k, const int *ptr, c
     }
 }
 
+// The same values with a thread per BLOCK row (its three scalar rows share
+// the node, the candidate groups, the row's blocks, the strength tests and
+// every P_tent row they read): each scalar row's accumulator sees exactly
+// the terms of k_psm_vals in the same order -- one third of the index work
+// and of the P_tent gathers.  K = the nullspace width (6 for the ns
+// pipelines).
+template <int K>
+__global__ void __launch_bounds__(128) k_psm_vals3(int64_t nbr, int pbs, const int *ptr, const int *col,
+        const double *val, const int *gp, const int *gc, const int *agg, const int *toff,
+        const int *tlist, const int *tcnt, const double *dinv, const double *diag, const double *Pt,
+        double omega, const int *pptr, double *pval, int64_t off) {
+    const int64_t lb = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (lb >= nbr) return;
+    const int64_t li0 = 3 * lb, i0 = li0 + off;
+    const int br = static_cast<int>(i0 / 3);
+    const int node = static_cast<int>(i0 / pbs);
+    const int lnode = static_cast<int>(li0 / pbs);
+    constexpr int kb = K / 3;
+    const int *L = tlist + toff[lnode];
+    const int nt = tcnt[lnode];
+    double di[3], dg[3];
+#pragma unroll
+    for (int rr = 0; rr < 3; ++rr) { di[rr] = dinv[li0 + rr]; dg[rr] = diag[li0 + rr]; }
+    const double nom = -omega;
+    const int jb = ptr[br], je = ptr[br + 1];
+    const int ownagg = agg[node];
+    for (int t = 0; t < nt; ++t) {
+        const int g = L[t];
+        double acc[3][K];
+        bool touched = ownagg == g;  // the same for the three rows throughout
+        if (touched) {
+#pragma unroll
+            for (int rr = 0; rr < 3; ++rr)
+#pragma unroll
+                for (int c = 0; c < K; ++c) acc[rr][c] = Pt[(i0 + rr) * K + c];
+        }
+        for (int j = jb; j < je; ++j) {
+            const int64_t sc0 = 3 * static_cast<int64_t>(col[j]);
+            const int cn = static_cast<int>(sc0 / pbs);
+            if (agg[cn] != g) continue;
+            if (cn != node && !strong(gp, gc, node, cn)) continue;
+            const double *b = val + 9 * static_cast<int64_t>(j);
+#pragma unroll
+            for (int c3 = 0; c3 < 3; ++c3) {
+                const int64_t sc = sc0 + c3;
+                double pk[K];
+#pragma unroll
+                for (int c = 0; c < K; ++c) pk[c] = Pt[sc * K + c];
+#pragma unroll
+                for (int rr = 0; rr < 3; ++rr) {
+                    const double coef = (sc == i0 + rr) ? dg[rr] : b[3 * rr + c3];
+                    const double scaled = __dmul_rn(__dmul_rn(di[rr], coef), nom);
+                    if (touched) {
+#pragma unroll
+                        for (int c = 0; c < K; ++c) acc[rr][c] = __dadd_rn(acc[rr][c], __dmul_rn(scaled, pk[c]));
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < K; ++c) acc[rr][c] = __dmul_rn(scaled, pk[c]);
+                    }
+                }
+                touched = true;
+            }
+        }
+        const int64_t base = pptr[lb] + static_cast<int64_t>(t) * kb;
+#pragma unroll
+        for (int rr = 0; rr < 3; ++rr)
+#pragma unroll
+            for (int c = 0; c < K; ++c) pval[9 * (base + c / 3) + 3 * rr + c % 3] = acc[rr][c];
+    }
+}
+
+bool psm_block_rows() {  // SAMG_PSM_BLOCKROW=0 selects the thread-per-scalar-row kernel
+    static const bool on = [] {
+        const char *e = std::getenv("SAMG_PSM_BLOCKROW");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 // The `scalar` pipeline's tentative operator has no nullspace: the unit
 // aggregate indicator expanded per point-block component
 // (coarsening.hpp:249-266), one entry per scalar row -- P_tent(i, agg(i)*3 +
@@ -1755,6 +1834,11 @@ void smooth_prolongation(const Bsr3 &A, const Graph &G, const DevBuf<int> &agg, 
                                                           G.ptr.p, G.col.p, agg.p, toff.p, tlist.p,
                                                           tcnt.p, dinv.p, diag.p, Pt, omega, P.ptr.p,
                                                           P.val.p, 3 * row0);
+    else if (k == 6 && psm_block_rows() && nsc % 3 == 0)
+        k_psm_vals3<6><<<ceil_div(nsc / 3, 128), 128, 0, s>>>(nsc / 3, pbs, A.ptr.p, A.col.p, A.val.p,
+                                                             G.ptr.p, G.col.p, agg.p, toff.p, tlist.p,
+                                                             tcnt.p, dinv.p, diag.p, Pt, omega, P.ptr.p,
+                                                             P.val.p, 3 * row0);
     else
         k_psm_vals<<<ceil_div(nsc, 128), 128, 0, s>>>(nsc, pbs, h, k, A.ptr.p, A.col.p, A.val.p,
                                                       G.ptr.p, G.col.p, agg.p, toff.p, tlist.p,
