@@ -2202,7 +2202,10 @@ void spgemm_impl(const Bsr3 &A, const Bsr3 &B, Bsr3 &C, cudaStream_t s, const BC
             const char *e = std::getenv("SAMG_PULL_BATCH");
             return e ? std::atoi(e) : 0;
         }();
-        const int batch = batch_env > 0 ? batch_env : (n >= 50000 && n < 200000 ? 4 : 1);
+        // (round 2: C1's level 1 (3 822 rows) 2.02 / 0.85 ms with 1 -> 1.37 /
+        // 0.75 with 4: few rows per SM, latency-bound column scans)
+        const int batch = batch_env > 0 ? batch_env
+                                        : ((n >= 50000 && n < 200000) || (!wide_cta && n < 12000) ? 4 : 1);
         using KP = decltype(&k_spgemm_pull<kScalar, true, 128, 1>);
         KP kp;
         auto pick = [&](auto bt) {
