@@ -341,20 +341,37 @@ SAMG_API int samg_setup(int64_t n, const int64_t *ptr, const int64_t *col, const
                 "setup: malformed CSR arrays");
         need_device(prm->device);
         cudaStream_t s = new_stream();
+        static const bool timing = [] {
+            const char *e = std::getenv("SAMG_SETUP_TIMING");
+            return e && e[0] == '1';
+        }();
+        double tm = now_s();
+        auto tmark = [&](const char *what) {  // SAMG_SETUP_TIMING: the upload's parts
+            if (!timing) return;
+            CK(cudaStreamSynchronize(s));
+            const double t = now_s();
+            std::fprintf(stderr, "setup upload %-14s %8.3f ms\n", what, 1e3 * (t - tm));
+            tm = t;
+        };
+        tmark("stream");
         Bsr3 A0;
         try {
             const int64_t nnz = ptr[n];
             DevBuf<int64_t> dp(n + 1, s);
             DevBuf<double> dv(nnz, s);
+            tmark("alloc");
             h2d(dp.p, ptr, sizeof(int64_t) * (n + 1), s);
             if (nnz) h2d(dv.p, val, sizeof(double) * nnz, s);
+            tmark("h2d values");
             if (n <= INT32_MAX) {
                 // column indices narrowed to 32 bits by the staging threads
                 // (half the PCIe bytes of the int64 array; range-checked)
                 DevBuf<int32_t> dc(nnz, s);
                 require(h2d_narrow(dc.p, col, static_cast<size_t>(nnz), n, s), SAMG_INVALID_ARGUMENT,
                         "setup: column index out of range");
+                tmark("h2d columns");
                 scalar_to_bsr3(n, dp.p, dc.p, dv.p, A0, s);
+                tmark("to_block");
             } else {
                 DevBuf<int64_t> dc(nnz, s);
                 if (nnz) h2d(dc.p, col, sizeof(int64_t) * nnz, s);

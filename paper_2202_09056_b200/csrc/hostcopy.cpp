@@ -42,13 +42,21 @@ struct Pool {
         if (ready && dev == device) return;
         release();
         for (int t = 0; t < kThreads; ++t)
-            for (int b = 0; b < 2; ++b) {
-                CK(cudaHostAlloc(reinterpret_cast<void **>(&buf[t][b]), kChunk, cudaHostAllocPortable));
+            for (int b = 0; b < 2; ++b)
                 CK(cudaEventCreateWithFlags(&ev[t][b], cudaEventDisableTiming));
-            }
         device = dev;
         ready = true;
     }
+    // pin the buffers of the first T thread slots (before the copy threads
+    // start: concurrent cudaHostAlloc calls serialise in the driver).  Only
+    // the slots in use are pinned (cudaHostAlloc costs ~0.5 ms per MB in a
+    // cold process; the pool used to pin all 16 x 2 slots)
+    void pin(int T) {
+        for (int t = 0; t < T; ++t)
+            for (int b = 0; b < 2; ++b)
+                if (!buf[t][b]) CK(cudaHostAlloc(reinterpret_cast<void **>(&buf[t][b]), kChunk, cudaHostAllocPortable));
+    }
+    char *slot(int t, int b) { return buf[t][b]; }
     void release() {
         for (int t = 0; t < kThreads; ++t)
             for (int b = 0; b < 2; ++b) {
@@ -95,6 +103,7 @@ void h2d(void *dst, const void *src, size_t bytes, cudaStream_t s) {
         return std::min(kThreads, std::max(1, v));
     }();
     const int T = static_cast<int>(std::min<size_t>(threads, nchunks));
+    P.pin(T);
     std::vector<std::exception_ptr> errs(T);
     auto work = [&](int t) {
         try {
@@ -103,7 +112,7 @@ void h2d(void *dst, const void *src, size_t bytes, cudaStream_t s) {
             for (size_t c = t; c < nchunks; c += T, b ^= 1) {
                 const size_t off = c * kChunk, n = std::min(kChunk, bytes - off);
                 CK(cudaEventSynchronize(P.ev[t][b]));  // previous DMA from this buffer done
-                std::memcpy(P.buf[t][b], static_cast<const char *>(src) + off, n);
+                std::memcpy(P.slot(t, b), static_cast<const char *>(src) + off, n);
                 CK(cudaMemcpyAsync(static_cast<char *>(dst) + off, P.buf[t][b], n,
                                    cudaMemcpyHostToDevice, s));
                 CK(cudaEventRecord(P.ev[t][b], s));
@@ -159,6 +168,7 @@ bool h2d_narrow(int32_t *dst, const int64_t *src, size_t count, int64_t bound, c
         return std::min(kThreads, std::max(1, v));
     }();
     const int T = static_cast<int>(std::min<size_t>(threads, nchunks));
+    P.pin(T);
     std::vector<std::exception_ptr> errs(T);
     std::vector<char> oks(T, 1);
     auto work = [&](int t) {
@@ -168,7 +178,7 @@ bool h2d_narrow(int32_t *dst, const int64_t *src, size_t count, int64_t bound, c
             for (size_t c = t; c < nchunks; c += T, b ^= 1) {
                 const size_t off = c * kElems, n = std::min(kElems, count - off);
                 CK(cudaEventSynchronize(P.ev[t][b]));
-                if (!narrow(reinterpret_cast<int32_t *>(P.buf[t][b]), src + off, n)) oks[t] = 0;
+                if (!narrow(reinterpret_cast<int32_t *>(P.slot(t, b)), src + off, n)) oks[t] = 0;
                 CK(cudaMemcpyAsync(dst + off, P.buf[t][b], sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
                 CK(cudaEventRecord(P.ev[t][b], s));
             }
