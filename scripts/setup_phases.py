@@ -16,7 +16,7 @@ from scripts.configs import CONFIGS  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "C1"
 kw, _ = CONFIGS[name]
-prm = pb.AmgParams(smoother="spai0")
+prm = pb.AmgParams(smoother=os.environ.get("SAMG_PROBE_SMOOTHER", "spai0"))
 for rep in range(2):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
