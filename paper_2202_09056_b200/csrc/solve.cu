@@ -672,10 +672,11 @@ __global__ void __launch_bounds__(32 * (TW * NT + 1), 1) k_bsr3_tma(TmaCfg cfg, 
                     const long long cb = (4LL * p0) & ~15LL, ce = (4LL * p1 + 15) & ~15LL;
                     // ptr entries [r0 - pmis, r0 - pmis + RPC + 8): a 16-byte
                     // aligned window holding [r0, r0 + RPC]
-                    const long long pbytes = 4LL * (RPC + 8);
+                    constexpr int PW = (RPC + 8 + 3) / 4 * 4;  // whole 16-byte units
+                    const long long pbytes = 4LL * PW;
                     const bool direct = ve - vb > cfg.vcap || ce - cb > cfg.ccap ||
                                         ve > BB * cfg.nnzb || ce > 4LL * cfg.nnzb ||
-                                        r0 - cfg.pmis + RPC + 8 > cfg.nrows + 1 || p1 == p0;
+                                        r0 - cfg.pmis + PW > cfg.nrows + 1 || p1 == p0;
                     hdr[st] = TmaHdr{p0, direct ? 1 : 0,
                                      static_cast<int>((BB * p0 - vb) / static_cast<long long>(sizeof(VT))),
                                      static_cast<int>((4LL * p0 - cb) / 4)};
@@ -832,17 +833,25 @@ int env_int(const char *name, int dflt) {
 
 // Variant 3 launch; false if the matrix does not suit it (then the caller
 // uses the register-streaming kernel).
-template <int G_>
+template <int G_, int TW_ = 8, int NT_ = 2>
 struct TmaShape {
-    static constexpr int G = G_, TW = 8, NT = 2;
+    static constexpr int G = G_, TW = TW_, NT = NT_;
 };
 
+// Teams: two of 8 warps by default.  Long rows (G = 32, a warp per row) can
+// run as more, smaller teams (tw = 4 or 2 warps per team, 16 / tw teams):
+// a chunk is then tw rows, so more chunks fit the ring and more rows are in
+// different phases of gather / reduce / epilogue at once.
 template <class F>
-void dispatch_tma_shape(int G, F f) {
+void dispatch_tma_shape(int G, int tw, F f) {
     switch (G) {
         case 4: f(TmaShape<4>{}); break;
         case 16: f(TmaShape<16>{}); break;
-        case 32: f(TmaShape<32>{}); break;
+        case 32:
+            if (tw == 4) f(TmaShape<32, 4, 4>{});
+            else if (tw == 2) f(TmaShape<32, 2, 8>{});
+            else f(TmaShape<32>{});
+            break;
         default: f(TmaShape<8>{}); break;
     }
 }
@@ -875,7 +884,7 @@ bool launch_tma(const Bsr3 &A, const VT *val, const double *x, Epi epi, double *
     static const int budget64 = env_int("SAMG_TMA_SMEM", 226000);
     static const int budget32 = env_int("SAMG_TMA_SMEM32", 226000);
     const int budget = sizeof(VT) == 4 ? budget32 : budget64;
-    constexpr int TW = 8, NT = 2;  // two teams of 8 consumer warps (measured best on C1)
+    int TW = 8, NT = 2;  // two teams of 8 consumer warps (measured best on C1's fine level)
     const double bpr = static_cast<double>(A.nnzb) / A.nrows;
     // ~3 blocks per lane (C1 fine level, 26 blocks per row: G = 8)
     // (fp32 values: twice the blocks per lane, C1 mixed solve 0.080 -> 0.074 s)
@@ -884,9 +893,20 @@ bool launch_tma(const Bsr3 &A, const VT *val, const double *x, Epi epi, double *
     if (forced_g == 4 || forced_g == 8 || forced_g == 16 || forced_g == 32) G = forced_g;
     static const int gmax = env_int("SAMG_TMA_GMAX", 32);
     G = std::min(G, std::max(4, gmax));
+    static const int tw32 = env_int("SAMG_TMA_TW32", 8);
+    if (G == 32 && (tw32 == 4 || tw32 == 2)) {
+        TW = tw32;
+        NT = 16 / tw32;
+    }
     const int rpc = 32 * TW / G;
     auto up = [](long long b) { return static_cast<unsigned>((b + 127) / 128 * 128); };
-    long long est = static_cast<long long>(std::ceil(bpr * 1.1)) + 1;
+    // (smaller teams: fewer rows per chunk average out less, so more slack)
+    static const double slack_env = [] {
+        const char *e = std::getenv("SAMG_TMA_SLACK");
+        return e ? std::atof(e) : 0.0;
+    }();
+    const double slack = slack_env > 1.0 ? slack_env : (TW < 8 ? 1.25 : 1.1);
+    long long est = static_cast<long long>(std::ceil(bpr * slack)) + 1;
     // blocks per row a stage holds: ~10 % above the mean, but shrunk (down to
     // the mean + 2 %) so that NT + 1 stages still fit -- C4's fine level (26.7
     // blocks per row) missed the third stage by 1 % and ran without TMA;
@@ -917,7 +937,7 @@ bool launch_tma(const Bsr3 &A, const VT *val, const double *x, Epi epi, double *
     static const int min_chunks_per_sm = env_int("SAMG_TMA_MIN_CHUNKS", 24);
     if (cfg.nchunks < min_chunks_per_sm * sms) return why("chunks");
     bool ok = false;
-    dispatch_tma_shape(G, [&](auto sh) {
+    dispatch_tma_shape(G, TW, [&](auto sh) {
         using Sh = decltype(sh);
         auto kern = k_bsr3_tma<Sh::G, Sh::TW, Sh::NT, kReduce, Epi, VT>;
         const int threads = 32 * (Sh::TW * Sh::NT + 1);
