@@ -219,11 +219,67 @@ __device__ __forceinline__ void row_sums_blocks(int row, bool valid, int lane,
     group_reduce3<G, kThreads>(s0, s1, s2);
 }
 
+// Variant 2 (long rows, a warp per row; SAMG_LONG_PIPE=0 restores variant 1):
+// variant 1 with col read one iteration ahead, so an iteration's x gather is
+// issued together with its value loads instead of after a col round trip of
+// its own: the row's chain is ptr -> col -> {val, x} -> {val, x} ... instead
+// of ptr -> {col, val} -> x -> {col, val} -> x ...  Same blocks per lane in
+// the same order: identical sums.  Compiled for 5 CTAs per SM (<= 51
+// registers; ptxas otherwise takes 52 for most epilogues and loses a CTA).
+// C1's level-1 kernels: 42.6 / 33.3 / 32.6 -> 40.6 / 30.6 / 30.1 us.
+template <int G, class VT = double>
+__device__ __forceinline__ void row_sums_pipe(int row, bool valid, int lane,
+        const int *__restrict__ ptr, const int *__restrict__ col,
+        const VT *__restrict__ val, const double *__restrict__ x,
+        double &s0, double &s1, double &s2) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    if (valid) {
+        const int beg = __ldg(ptr + row), end = __ldg(ptr + row + 1);
+        int j = beg + lane;
+        int c0 = j < end ? __ldg(col + j) : -1, c1 = j + G < end ? __ldg(col + j + G) : -1;
+        // both blocks of a pair in flight together (no branch between them)
+        auto load = [&](int jj, int c, double (&bb)[9], double &x0, double &x1, double &x2) {
+            blk9<true>(val + 9 * static_cast<size_t>(jj), jj & 1, bb);
+            const double *xp = x + 3 * static_cast<size_t>(c);
+            const int xo = c & 1;
+            const double2 xq = ldg2(xp + xo);
+            const double xe = __ldg(xp + (xo ? 0 : 2));
+            x0 = xo ? xe : xq.x;
+            x1 = xo ? xq.x : xq.y;
+            x2 = xo ? xq.y : xe;
+        };
+        auto acc = [&](const double (&bb)[9], double x0, double x1, double x2) {
+            a0 = fma(bb[0], x0, a0); a0 = fma(bb[1], x1, a0); a0 = fma(bb[2], x2, a0);
+            a1 = fma(bb[3], x0, a1); a1 = fma(bb[4], x1, a1); a1 = fma(bb[5], x2, a1);
+            a2 = fma(bb[6], x0, a2); a2 = fma(bb[7], x1, a2); a2 = fma(bb[8], x2, a2);
+        };
+        for (; j + G < end; j += 2 * G) {
+            const int n0 = j + 2 * G < end ? __ldg(col + j + 2 * G) : -1;
+            const int n1 = j + 3 * G < end ? __ldg(col + j + 3 * G) : -1;
+            double b0[9], b1[9], p0, p1, p2, q0, q1, q2;
+            load(j, c0, b0, p0, p1, p2);
+            load(j + G, c1, b1, q0, q1, q2);
+            acc(b0, p0, p1, p2);
+            acc(b1, q0, q1, q2);
+            c0 = n0;
+            c1 = n1;
+        }
+        if (j < end) {
+            double b0[9], p0, p1, p2;
+            load(j, c0, b0, p0, p1, p2);
+            acc(b0, p0, p1, p2);
+        }
+    }
+    s0 = a0; s1 = a1; s2 = a2;
+    group_reduce3<G>(s0, s1, s2);
+}
+
 template <int G, int V, class VT>
 __device__ __forceinline__ void row_sums(int row, bool valid, int lane, const int *__restrict__ ptr,
         const int *__restrict__ col, const VT *__restrict__ val,
         const double *__restrict__ x, double &s0, double &s1, double &s2) {
     if constexpr (V == 0 && std::is_same_v<VT, double>) row_sums_units<G>(row, valid, lane, ptr, col, val, x, s0, s1, s2);
+    else if constexpr (V == 2) row_sums_pipe<G, VT>(row, valid, lane, ptr, col, val, x, s0, s1, s2);
     else row_sums_blocks<G, VT>(row, valid, lane, ptr, col, val, x, s0, s1, s2);
 }
 
@@ -365,14 +421,14 @@ struct EpiDot {
 };
 
 template <int G, int V, class Epi, class VT = double>
-__global__ void __launch_bounds__(256) k_bsr3(int nrows, const int *__restrict__ ptr,
+__global__ void __launch_bounds__(256, V == 2 ? 5 : 0) k_bsr3(int nrows, const int *__restrict__ ptr,
         const int *__restrict__ col, const VT *__restrict__ val,
         const double *__restrict__ x, Epi epi) {
     const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const int row = gtid / G, lane = threadIdx.x % G;
     const bool valid = row < nrows;
     double s0, s1, s2;
-    row_sums<G, V>(row, valid, lane, ptr, col, val, x, s0, s1, s2);
+    row_sums<G, V, VT>(row, valid, lane, ptr, col, val, x, s0, s1, s2);
     if (valid) epilogue<G>(epi, row, lane, s0, s1, s2);
 }
 
@@ -1009,10 +1065,15 @@ void launch_rows_t(const Bsr3 &A, const VT *val, const double *x, Epi epi, cudaS
         else if (G == 16) launch_k(false, k_bsr3<16, 0, Epi, double>, grid, 256, 0, s, n, A.ptr.p, A.col.p, vd, x, epi);
         else launch_k(false, k_bsr3<8, 0, Epi, double>, grid, 256, 0, s, n, A.ptr.p, A.col.p, vd, x, epi);
     } else {
-        dispatch_group(G, [&](auto g) {
-            constexpr int GG = decltype(g)::value;
-            launch_k(false, k_bsr3<GG, 1, Epi, VT>, grid, 256, 0, s, n, A.ptr.p, A.col.p, val, x, epi);
-        });
+        static const int pipe = env_int("SAMG_LONG_PIPE", 1);
+        if (G == 32 && pipe) {
+            launch_k(false, k_bsr3<32, 2, Epi, VT>, grid, 256, 0, s, n, A.ptr.p, A.col.p, val, x, epi);
+        } else {
+            dispatch_group(G, [&](auto g) {
+                constexpr int GG = decltype(g)::value;
+                launch_k(false, k_bsr3<GG, 1, Epi, VT>, grid, 256, 0, s, n, A.ptr.p, A.col.p, val, x, epi);
+            });
+        }
     }
     CK_LAUNCH();
 }

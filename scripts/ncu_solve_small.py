@@ -12,7 +12,8 @@ import paper_2202_09056_b200 as pb  # noqa: E402
 
 its = int(sys.argv[1]) if len(sys.argv) > 1 else 6
 dp = pb.generate_hex_device(pb.ProblemParams(nx=63, ny=63, nz=63, dirichlet="eliminate", noise=0.01, seed=2022), device=0)
-h = pb.setup_device(dp.A, dp.nullspace_ptr, 6, "ns_block", pb.AmgParams())
+sm = sys.argv[2] if len(sys.argv) > 2 else None
+h = pb.setup_device(dp.A, dp.nullspace_ptr, 6, "ns_block", pb.AmgParams(smoother=sm) if sm else pb.AmgParams())
 u = torch.zeros(dp.n, dtype=torch.float64, device="cuda")
 rep = h.cg_solve_device(dp.rhs_ptr, u.data_ptr(), pb.CgParams(max_iterations=its))
 torch.cuda.synchronize()
