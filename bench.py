@@ -477,6 +477,8 @@ def run_b200(args, rank, world, local, dist):
         # ILU(0), bit-identical) and with the mixed-precision V-cycle
         variants = {}
         for key, vprm in (("ilu0", pb.AmgParams(smoother="ilu0", device=local)),
+                          ("ilu0_latest_last", pb.AmgParams(smoother="ilu0", device=local,
+                                                            ilu_sweep_order="latest_last")),
                           ("spai0_mixed", pb.AmgParams(smoother="spai0", device=local,
                                                        vcycle_precision="mixed"))):
             st, sv, vr = [], [], None

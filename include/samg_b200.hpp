@@ -124,6 +124,7 @@ struct amg_params {
     bool verify_galerkin = false;
     int device = 0;
     bool mixed_precision_vcycle = false;  // extension: fp32 operator copies (samg_precision)
+    bool ilu_latest_last = false;         // extension: relaxed backward-sweep order (samg_ilu_order)
 };
 
 struct cg_params {
@@ -212,6 +213,7 @@ inline samg_amg_params to_c(const amg_params &p) {
     c.verify_galerkin = p.verify_galerkin ? 1 : 0;
     c.device = p.device;
     c.vcycle_precision = p.mixed_precision_vcycle ? SAMG_PRECISION_MIXED : SAMG_PRECISION_FP64;
+    c.ilu_sweep_order = p.ilu_latest_last ? SAMG_ILU_ORDER_LATEST_LAST : SAMG_ILU_ORDER_REFERENCE;
     return c;
 }
 } // namespace detail

@@ -53,7 +53,8 @@ class AmgParamsC(C.Structure):
                 ("smoother_omega", C.c_double), ("pre_sweeps", C.c_int),
                 ("post_sweeps", C.c_int), ("coarse_enough", C.c_int64),
                 ("stagnation_ratio", C.c_double), ("verify_galerkin", C.c_int),
-                ("device", C.c_int), ("vcycle_precision", C.c_int)]
+                ("device", C.c_int), ("vcycle_precision", C.c_int),
+                ("ilu_sweep_order", C.c_int)]
 
 
 class CgParamsC(C.Structure):

@@ -17,6 +17,7 @@ PIPELINES = {"scalar": 0, "block": 1, "ns_scalar": 2, "ns_hybrid1": 3, "ns_hybri
              "ns_block": 5}
 SMOOTHERS = {"jacobi": 0, "spai0": 1, "block_jacobi": 2, "ilu0": 3}
 PRECISIONS = {"fp64": 0, "mixed": 1}
+ILU_ORDERS = {"reference": 0, "latest_last": 1}
 
 
 def _i64(a):
@@ -53,6 +54,10 @@ class AmgParams:
     vcycle_precision: str = "fp64"
     # hierarchy.hpp:382-401: recompute each coarse operator and compare
     verify_galerkin: bool = False
+    # block ILU(0) backward sweep: "reference" (bit-identical applications) or
+    # "latest_last" (descending columns: same sums up to rounding, shorter chain
+    # after the last hand-off)
+    ilu_sweep_order: str = "reference"
 
     def c(self) -> AmgParamsC:
         return AmgParamsC(self.eps_strong, self.omega, self.point_block_size,
@@ -60,7 +65,8 @@ class AmgParams:
                           else int(self.smoother), self.smoother_omega, self.pre_sweeps,
                           self.post_sweeps, self.coarse_enough, self.stagnation_ratio,
                           int(self.verify_galerkin),
-                          self.device, PRECISIONS[self.vcycle_precision])
+                          self.device, PRECISIONS[self.vcycle_precision],
+                          ILU_ORDERS[self.ilu_sweep_order])
 
 
 @dataclass

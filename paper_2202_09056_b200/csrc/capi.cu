@@ -156,6 +156,13 @@ void validate_params(const samg_amg_params *prm, int pipeline) {
             "setup: negative sweep count");
     require(prm->vcycle_precision == SAMG_PRECISION_FP64 || prm->vcycle_precision == SAMG_PRECISION_MIXED,
             SAMG_INVALID_ARGUMENT, "setup: unknown vcycle_precision");
+    require(prm->ilu_sweep_order == SAMG_ILU_ORDER_REFERENCE ||
+                prm->ilu_sweep_order == SAMG_ILU_ORDER_LATEST_LAST,
+            SAMG_INVALID_ARGUMENT, "setup: unknown ilu_sweep_order");
+    if (prm->ilu_sweep_order != SAMG_ILU_ORDER_REFERENCE &&
+        (prm->smoother != SAMG_SMOOTHER_ILU0 || pipeline == SAMG_PIPELINE_SCALAR ||
+         pipeline == SAMG_PIPELINE_NS_SCALAR || pipeline == SAMG_PIPELINE_NS_HYBRID1))
+        fail(SAMG_UNSUPPORTED, "setup: ilu_sweep_order applies to the block ILU(0) smoother only");
 }
 
 // hierarchy.hpp:267-282 + coarsening.hpp:269-270 checks
@@ -286,6 +293,7 @@ SAMG_API void samg_default_amg_params(samg_amg_params *p) {
     p->verify_galerkin = 0;
     p->device = 0;
     p->vcycle_precision = SAMG_PRECISION_FP64;
+    p->ilu_sweep_order = SAMG_ILU_ORDER_REFERENCE;
 }
 
 SAMG_API void samg_default_cg_params(samg_cg_params *p) {

@@ -276,6 +276,7 @@ Hierarchy *setup_hierarchy(Bsr3 &&A0, const double *B_host, int64_t b_rows, int6
             setup_ilu0_scalar(H->levels[i].A, H->levels[i].M, err, s);
         else
             setup_smoother(H->levels[i].A, prm.smoother, prm.smoother_omega, H->levels[i].M, err, s);
+        H->levels[i].M.latest_last = prm.ilu_sweep_order == SAMG_ILU_ORDER_LATEST_LAST;
     }
     check_dev_error(err, s);
     mark("smoothers", L - 1);

@@ -257,7 +257,7 @@ __device__ __forceinline__ void st_publish(double *p, double x) {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-template <bool kFwd, bool kZero>
+template <bool kFwd, bool kZero, bool kRev = false>
 __global__ void __launch_bounds__(256) k_ilu_sweep(int n, const int *__restrict__ order,
         const int *__restrict__ ptr, const int *__restrict__ col, const int *__restrict__ dpos,
         const double *__restrict__ lu, const double *__restrict__ inv, const double *src,
@@ -274,16 +274,27 @@ __global__ void __launch_bounds__(256) k_ilu_sweep(int n, const int *__restrict_
         const int b = kFwd ? __ldg(ptr + i) : __ldg(dpos + i) + 1, e = kFwd ? __ldg(dpos + i) : __ldg(ptr + i + 1);
         double acc = 0.0;
         if (lane < 3) acc = src[3LL * i + lane];
-        for (int w0 = b; w0 < e; w0 += kWin) {
-            const int m = min(kWin, e - w0);
-            for (int q = lane; q < 9 * m; q += 32) bs[q] = __ldg(lu + 9LL * w0 + q);
+        for (int wd = 0; wd < e - b; wd += kWin) {
+            const int m = min(kWin, e - b - wd);
+            // kRev (backward, relaxed order): the chain runs over descending
+            // columns -- windows from the row's end, reversed inside -- so
+            // the latest dependency (row i + 1) is its last term
+            const int w0 = kRev ? e - wd - m : b + wd;
+            if constexpr (kRev) {
+                for (int q = lane; q < 9 * m; q += 32) {
+                    const int d = q / 9;
+                    bs[q] = __ldg(lu + 9LL * (w0 + m - 1 - d) + (q - 9 * d));
+                }
+            } else {
+                for (int q = lane; q < 9 * m; q += 32) bs[q] = __ldg(lu + 9LL * w0 + q);
+            }
             int kk[3];
             unsigned pend = 0;
 #pragma unroll
             for (int s = 0; s < 3; ++s) {
                 const int d = lane + 32 * s;
                 kk[s] = 0;
-                if (d < m) { kk[s] = __ldg(col + w0 + d); pend |= 1u << s; }
+                if (d < m) { kk[s] = __ldg(col + w0 + (kRev ? m - 1 - d : d)); pend |= 1u << s; }
             }
             __syncwarp();  // the staged blocks are multiplied by their dependency's lane
             int done = 0;
@@ -884,7 +895,9 @@ void launch_ilu_smooth(const Bsr3 *A, const Smoother &M, const double *f, const 
     const int gf = gf_cache.get([] {
         for (const void *k : {reinterpret_cast<const void *>(k_ilu_sweep<true, true>),
                                reinterpret_cast<const void *>(k_ilu_sweep<false, false>),
-                               reinterpret_cast<const void *>(k_ilu_sweep<false, true>)})
+                               reinterpret_cast<const void *>(k_ilu_sweep<false, true>),
+                               reinterpret_cast<const void *>(k_ilu_sweep<false, false, true>),
+                               reinterpret_cast<const void *>(k_ilu_sweep<false, true, true>)})
             CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSweepSmem));
         const char *e = std::getenv("SAMG_ILU_CTAS_PER_SM");
         return persistent_grid(reinterpret_cast<const void *>(k_ilu_sweep<true, true>), 1 << 30, kSweepSmem,
@@ -927,7 +940,14 @@ void launch_ilu_smooth(const Bsr3 *A, const Smoother &M, const double *f, const 
     }
     k_ilu_sweep<true, true><<<gridf, 256, kSweepSmem, s>>>(n, of, M.ptr, M.col, M.dpos.p, M.lu.p, M.data.p,
                                                           rin, y, nullptr, nullptr, cnt);
-    if (u_in)
+    if (M.latest_last) {
+        if (u_in)
+            k_ilu_sweep<false, false, true><<<gridb, 256, kSweepSmem, s>>>(n, ob, M.ptr, M.col, M.dpos.p, M.lu.p,
+                                                                          M.data.p, y, x, u_in, u_out, cnt + 1);
+        else
+            k_ilu_sweep<false, true, true><<<gridb, 256, kSweepSmem, s>>>(n, ob, M.ptr, M.col, M.dpos.p, M.lu.p,
+                                                                         M.data.p, y, x, nullptr, u_out, cnt + 1);
+    } else if (u_in)
         k_ilu_sweep<false, false><<<gridb, 256, kSweepSmem, s>>>(n, ob, M.ptr, M.col, M.dpos.p, M.lu.p,
                                                                 M.data.p, y, x, u_in, u_out, cnt + 1);
     else

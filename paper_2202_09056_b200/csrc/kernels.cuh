@@ -71,6 +71,9 @@ struct Smoother {
     // ns_hybrid1's smoother): factors in the same 3x3 block layout, data =
     // the inverted scalar pivots (3 per block row)
     bool scalar = false;
+    // backward sweep's subtraction chain over descending columns
+    // (samg_ilu_order LATEST_LAST; block ILU(0) only)
+    bool latest_last = false;
 };
 
 // ---- solve phase (solve.cu) -------------------------------------------------

@@ -10,7 +10,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CHILD = r'''
-import json, statistics, sys, time
+import json, os, statistics, sys, time
 sys.path.insert(0, %r)
 import numpy as np, torch
 import paper_2202_09056_b200 as pb
@@ -18,7 +18,7 @@ C = {"C1": dict(nx=63, ny=63, nz=63, dirichlet="eliminate", noise=0.01, seed=202
      "C3": dict(nx=511, ny=63, nz=63, lx=511 / 63, dirichlet="eliminate", load="traction_xend", x_slowest=True),
      "C4": dict(nx=199, ny=199, nz=199, dirichlet="eliminate", noise=0.01, seed=2022)}[%r]
 dp = pb.generate_hex_device(pb.ProblemParams(**C), device=0)
-h = pb.setup_device(dp.A, dp.nullspace_ptr, 6, "ns_block", pb.AmgParams(smoother="spai0"))
+h = pb.setup_device(dp.A, dp.nullspace_ptr, 6, "ns_block", pb.AmgParams(smoother=os.environ.get("SWEEP_SMOOTHER", "spai0")))
 u = torch.zeros(dp.n, dtype=torch.float64, device="cuda")
 ts, its = [], None
 for k in range(6):

@@ -66,6 +66,11 @@ def test_validation_before_device():
     c.vcycle_precision = 5
     with pytest.raises(pb.InvalidArgument):
         pb.setup(A, B, "ns_block", type("P", (), {"c": lambda self: c})())
+    c2 = pb.AmgParams(smoother="ilu0", ilu_sweep_order="latest_last").c()
+    assert c2.ilu_sweep_order == 1
+    c2.ilu_sweep_order = 4
+    with pytest.raises(pb.InvalidArgument):
+        pb.setup(A, B, "ns_block", type("P", (), {"c": lambda self: c2})())
 
 
 def test_no_cpu_fallback():

@@ -618,6 +618,47 @@ def test_mixed_precision_vcycle(gpu, ref, case):
     assert 1e-12 < d < 1e-5, d
 
 
+ILU_ORDER_CASES = [
+    ("cube6_free", dict(nx=6, dirichlet="eliminate", noise=0.01, seed=1), "ns_block"),
+    ("box975_free", dict(nx=9, ny=7, nz=5, dirichlet="eliminate", load="traction_xend"), "ns_block"),
+    ("cube5_block", dict(nx=5, dirichlet="eliminate", noise=0.01, seed=5), "block"),
+]
+
+
+@pytest.mark.parametrize("case", ILU_ORDER_CASES, ids=[c[0] for c in ILU_ORDER_CASES])
+def test_ilu_latest_last_order(gpu, ref, case):
+    """ilu_sweep_order="latest_last": the block ILU(0) backward sweep walks
+    its subtraction chain over descending columns (relaxation.hpp:73-88 runs
+    ascending).  Same factors (bit-identical hierarchy and smoother data),
+    every V-cycle equal to the reference-order one up to rounding, the same
+    convergence (+-1 iteration), solution within 1e-7 of the reference's."""
+    name, kw, pipeline = case
+    pb = gpu
+    p = make_problem(pb, **kw)
+    A = p.csr()
+    B = None if pipeline == "block" else p.nullspace()
+    h = pb.setup(A, B, pipeline, pb.AmgParams(smoother="ilu0", coarse_enough=150,
+                                              ilu_sweep_order="latest_last"))
+    h0 = pb.setup(A, B, pipeline, pb.AmgParams(smoother="ilu0", coarse_enough=150))
+    hr = ref.setup(A[0], A[1], A[2], A[3], B, Params(smoother=SM_ILU0, coarse_enough=150,
+                                                     pipeline=PIPE[pipeline]))
+    compare_hierarchies(h, hr, None, "ilu0", 0.72, pipeline)
+    assert h.nlevels >= 2
+    f = np.random.default_rng(17).uniform(-1, 1, p.n)
+    v, v0, vr = h.vcycle(f), h0.vcycle(f), hr.vcycle(f)
+    # the V-cycle around the sweeps is within 1e-12 of the reference's in
+    # either order; the two orders differ from each other at rounding level
+    d0, d1, d2 = rel_fro(v0, vr), rel_fro(v, vr), rel_fro(v, v0)
+    assert max(d0, d1, d2) <= 1e-12, (d0, d1, d2)
+    u, rep = h.cg_solve(p.rhs)
+    ur, rr = hr.cg_solve(p.rhs)
+    assert rep["converged"] and rr["converged"], (rep, rr)
+    assert abs(rep["iterations"] - rr["iterations"]) <= 1, (rep, rr)
+    assert rel_fro(u, ur) <= 1e-7
+    with pytest.raises(pb.Unsupported):  # block ILU(0) only
+        pb.setup(A, B, pipeline, pb.AmgParams(smoother="spai0", ilu_sweep_order="latest_last"))
+
+
 def test_coarse_lu_is_the_references(gpu, ref):
     """A single-level hierarchy on a numerically singular operator (the
     coarse operator of the ill-scaled cantilever): the V-cycle is the coarse
