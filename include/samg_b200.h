@@ -103,8 +103,8 @@ enum samg_precision {
  * LATEST_LAST: descending columns, so the dependency that completes last
  * (row i + 1) is the chain's last term instead of its first and only a few
  * subtractions follow the hand-off; the same factors and the same sums up to
- * rounding (C1: the same 38 iterations, backward sweeps 1.37 -> 0.78 ms,
- * solve 0.47 -> 0.33 s).  Block ILU(0) only. */
+ * rounding (C1: the same 38 iterations, backward sweeps 1.19 -> 0.57 ms,
+ * solve 0.42 -> 0.28 s).  Block ILU(0) only. */
 enum samg_ilu_order {
     SAMG_ILU_ORDER_REFERENCE = 0,
     SAMG_ILU_ORDER_LATEST_LAST = 1

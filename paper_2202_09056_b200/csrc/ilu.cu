@@ -274,6 +274,18 @@ __global__ void __launch_bounds__(256) k_ilu_sweep(int n, const int *__restrict_
         const int b = kFwd ? __ldg(ptr + i) : __ldg(dpos + i) + 1, e = kFwd ? __ldg(dpos + i) : __ldg(ptr + i + 1);
         double acc = 0.0;
         if (lane < 3) acc = src[3LL * i + lane];
+        // backward: the row of U_ii^-1 (and u_in) ahead of the chain -- loaded
+        // after it they put a memory round trip on every hand-off
+        double dv0 = 0.0, dv1 = 0.0, dv2 = 0.0, uin = 0.0;
+        if constexpr (!kFwd) {
+            if (lane < 3) {
+                const double *d = inv + 9LL * i + 3 * lane;
+                dv0 = __ldg(d);
+                dv1 = __ldg(d + 1);
+                dv2 = __ldg(d + 2);
+                if constexpr (!kZero) uin = u_in[3LL * i + lane];
+            }
+        }
         for (int wd = 0; wd < e - b; wd += kWin) {
             const int m = min(kWin, e - b - wd);
             // kRev (backward, relaxed order): the chain runs over descending
@@ -361,6 +373,34 @@ __global__ void __launch_bounds__(256) k_ilu_sweep(int n, const int *__restrict_
                 }
                 done = ready;
                 if (done == m) break;
+                // only the chain's last term is pending (forward: row i - 1,
+                // the usual case): lanes 0..2 poll that dependency themselves
+                // and finish the chain from registers -- no product staging,
+                // warp vote or shared-memory round trip after the hand-off
+                // (the same products and subtractions)
+                // (not in the reference-order backward sweep, whose last term
+                // is the earliest dependency: there the extra path only cost
+                // the chain walk its code shape, 1.19 -> 1.43 ms)
+                if ((kFwd || kRev) && done == m - 1 && wd + m == e - b) {
+                    const int dl = m - 1;
+                    const int ks = dl < 32 ? kk[0] : (dl < 64 ? kk[1] : kk[2]);
+                    const int kl = __shfl_sync(kFull, ks, dl & 31);
+                    if (lane < 3) {
+                        const double *pr = bs + 9 * dl + 3 * lane;  // still the factor block: its lane never saw the value
+                        const double b0 = pr[0], b1 = pr[1], b2 = pr[2];
+                        const double *g = out + 3LL * kl;
+                        unsigned long long v0, v1, v2;
+                        do {
+                            v0 = ld_poll(g);
+                            v1 = ld_poll(g + 1);
+                            v2 = ld_poll(g + 2);
+                        } while (v0 == kSent || v1 == kSent || v2 == kSent);
+                        acc = __dsub_rn(acc, __dmul_rn(b0, __longlong_as_double(static_cast<long long>(v0))));
+                        acc = __dsub_rn(acc, __dmul_rn(b1, __longlong_as_double(static_cast<long long>(v1))));
+                        acc = __dsub_rn(acc, __dmul_rn(b2, __longlong_as_double(static_cast<long long>(v2))));
+                    }
+                    break;
+                }
             }
             __syncwarp();  // the window's staging is reused
         }
@@ -369,18 +409,16 @@ __global__ void __launch_bounds__(256) k_ilu_sweep(int n, const int *__restrict_
             const double a0 = __shfl_sync(kFull, acc, 0), a1 = __shfl_sync(kFull, acc, 1),
                          a2 = __shfl_sync(kFull, acc, 2);
             if (lane < 3) {
-                const double *d = inv + 9LL * i + 3 * lane;
                 double tt = 0.0;
-                tt = __dadd_rn(tt, __dmul_rn(d[0], a0));
-                tt = __dadd_rn(tt, __dmul_rn(d[1], a1));
-                tt = __dadd_rn(tt, __dmul_rn(d[2], a2));
+                tt = __dadd_rn(tt, __dmul_rn(dv0, a0));
+                tt = __dadd_rn(tt, __dmul_rn(dv1, a1));
+                tt = __dadd_rn(tt, __dmul_rn(dv2, a2));
                 res = tt;
             }
         }
         if (lane < 3) {
             st_publish(out + 3LL * i + lane, res);
-            if constexpr (!kFwd)
-                u_out[3LL * i + lane] = kZero ? res : __dadd_rn(res, u_in[3LL * i + lane]);
+            if constexpr (!kFwd) u_out[3LL * i + lane] = kZero ? res : __dadd_rn(res, uin);
         }
         __syncwarp();
     }
@@ -719,6 +757,7 @@ __global__ void __launch_bounds__(256) k_ilu_sweep_s(int n, const int *__restric
         const double *dl = lu + 9LL * di;
         if constexpr (kFwd) {
             double a = lane < 3 ? src[3LL * i + lane] : 0.0;  // lane p: the chain of row 3i+p
+            const double l10 = __ldg(dl + 3), l20 = __ldg(dl + 6), l21 = __ldg(dl + 7);  // ahead of the chain
             for (int w0 = b; w0 < e; w0 += kWinS) {
                 const int m = min(kWinS, e - w0);
                 for (int q = lane; q < 9 * m; q += 32) bs[q] = __ldg(lu + 9LL * w0 + q);
@@ -754,9 +793,8 @@ __global__ void __launch_bounds__(256) k_ilu_sweep_s(int n, const int *__restric
                          a2 = __shfl_sync(kFull, a, 2);
             // own block, unit lower factor: y0; y1 - L10 y0; (y2 - L20 y0) - L21 y1
             res[0] = a0;
-            res[1] = __dsub_rn(a1, __dmul_rn(__ldg(dl + 3), res[0]));
-            res[2] = __dsub_rn(__dsub_rn(a2, __dmul_rn(__ldg(dl + 6), res[0])),
-                               __dmul_rn(__ldg(dl + 7), res[1]));
+            res[1] = __dsub_rn(a1, __dmul_rn(l10, res[0]));
+            res[2] = __dsub_rn(__dsub_rn(a2, __dmul_rn(l20, res[0])), __dmul_rn(l21, res[1]));
         } else {
             // rows 3i+2, 3i+1, 3i in sequence; each chain: y, the own block's
             // terms right of the diagonal, then the higher blocks' products
@@ -765,25 +803,29 @@ __global__ void __launch_bounds__(256) k_ilu_sweep_s(int n, const int *__restric
             constexpr int kWinB = 3 * kWinS;
             for (int r = 2; r >= 0; --r) {
                 double c = __ldcg(src + 3LL * i + r);
+                // the pivot and the factor entries are read before the polls:
+                // after them they add a memory round trip to every hand-off
+                const double piv = __ldg(inv + 3LL * i + r);
                 for (int q = r + 1; q < 3; ++q) c = __dsub_rn(c, __dmul_rn(__ldg(dl + 3 * r + q), res[q]));
                 for (int w0 = b; w0 < e; w0 += kWinB) {
                     const int m = min(kWinB, e - w0);
                     for (int d = lane; d < m; d += 32) {
                         const double *g = out + 3LL * __ldg(col + w0 + d);
+                        const double *u = lu + 9LL * (w0 + d) + 3 * r;
+                        const double f0 = __ldg(u), f1 = __ldg(u + 1), f2 = __ldg(u + 2);
                         unsigned long long v0, v1, v2;
                         do {
                             v0 = ld_poll(g); v1 = ld_poll(g + 1); v2 = ld_poll(g + 2);
                         } while (v0 == kSent || v1 == kSent || v2 == kSent);
-                        const double *u = lu + 9LL * (w0 + d) + 3 * r;
-                        bs[3 * d] = __dmul_rn(__ldg(u), __longlong_as_double(static_cast<long long>(v0)));
-                        bs[3 * d + 1] = __dmul_rn(__ldg(u + 1), __longlong_as_double(static_cast<long long>(v1)));
-                        bs[3 * d + 2] = __dmul_rn(__ldg(u + 2), __longlong_as_double(static_cast<long long>(v2)));
+                        bs[3 * d] = __dmul_rn(f0, __longlong_as_double(static_cast<long long>(v0)));
+                        bs[3 * d + 1] = __dmul_rn(f1, __longlong_as_double(static_cast<long long>(v1)));
+                        bs[3 * d + 2] = __dmul_rn(f2, __longlong_as_double(static_cast<long long>(v2)));
                     }
                     __syncwarp();
                     for (int d = 0; d < 3 * m; ++d) c = __dsub_rn(c, bs[d]);
                     __syncwarp();
                 }
-                res[r] = __dmul_rn(c, __ldg(inv + 3LL * i + r));
+                res[r] = __dmul_rn(c, piv);
             }
         }
         if (lane < 3) {

@@ -33,7 +33,8 @@ import paper_2202_09056_b200 as pb  # noqa: E402
 C = {"C1": dict(nx=63, ny=63, nz=63, dirichlet="eliminate", noise=0.01, seed=2022),
      "C4": dict(nx=199, ny=199, nz=199, dirichlet="eliminate", noise=0.01, seed=2022)}[cfg]
 dp = pb.generate_hex_device(pb.ProblemParams(**C), device=0)
-h = pb.setup_device(dp.A, dp.nullspace_ptr, 6, "ns_block", pb.AmgParams(smoother=smoother))
+h = pb.setup_device(dp.A, dp.nullspace_ptr, 6, "ns_block", pb.AmgParams(smoother=smoother,
+                                 ilu_sweep_order=os.environ.get("SAMG_ILU_ORDER", "reference")))
 u = torch.zeros(dp.n, dtype=torch.float64, device="cuda")
 for _ in range(2):
     rep = h.cg_solve_device(dp.rhs_ptr, u.data_ptr())

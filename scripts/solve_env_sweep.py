@@ -18,7 +18,8 @@ C = {"C1": dict(nx=63, ny=63, nz=63, dirichlet="eliminate", noise=0.01, seed=202
      "C3": dict(nx=511, ny=63, nz=63, lx=511 / 63, dirichlet="eliminate", load="traction_xend", x_slowest=True),
      "C4": dict(nx=199, ny=199, nz=199, dirichlet="eliminate", noise=0.01, seed=2022)}[%r]
 dp = pb.generate_hex_device(pb.ProblemParams(**C), device=0)
-h = pb.setup_device(dp.A, dp.nullspace_ptr, 6, "ns_block", pb.AmgParams(smoother=os.environ.get("SWEEP_SMOOTHER", "spai0")))
+h = pb.setup_device(dp.A, dp.nullspace_ptr, 6, "ns_block", pb.AmgParams(smoother=os.environ.get("SWEEP_SMOOTHER", "spai0"),
+                                 ilu_sweep_order=os.environ.get("SAMG_ILU_ORDER", "reference")))
 u = torch.zeros(dp.n, dtype=torch.float64, device="cuda")
 ts, its = [], None
 for k in range(6):
