@@ -226,7 +226,8 @@ __device__ __forceinline__ void row_sums_blocks(int row, bool valid, int lane,
 // of ptr -> {col, val} -> x -> {col, val} -> x ...  Same blocks per lane in
 // the same order: identical sums.  Compiled for 5 CTAs per SM (<= 51
 // registers; ptxas otherwise takes 52 for most epilogues and loses a CTA).
-// C1's level-1 kernels: 42.6 / 33.3 / 32.6 -> 40.6 / 30.6 / 30.1 us.
+// C1's level-1 kernels: 42.6 / 33.3 / 32.6 -> 40.6 / 30.6 / 30.1 us; the
+// G = 64 rows of its level 2 gain another 2.5 us per iteration.
 template <int G, class VT = double>
 __device__ __forceinline__ void row_sums_pipe(int row, bool valid, int lane,
         const int *__restrict__ ptr, const int *__restrict__ col,
@@ -1065,9 +1066,11 @@ void launch_rows_t(const Bsr3 &A, const VT *val, const double *x, Epi epi, cudaS
         else if (G == 16) launch_k(false, k_bsr3<16, 0, Epi, double>, grid, 256, 0, s, n, A.ptr.p, A.col.p, vd, x, epi);
         else launch_k(false, k_bsr3<8, 0, Epi, double>, grid, 256, 0, s, n, A.ptr.p, A.col.p, vd, x, epi);
     } else {
-        static const int pipe = env_int("SAMG_LONG_PIPE", 1);
+        static const int pipe = env_int("SAMG_LONG_PIPE", 2);  // 0: variant 1; 1: G = 32 only; 2: also G = 64
         if (G == 32 && pipe) {
             launch_k(false, k_bsr3<32, 2, Epi, VT>, grid, 256, 0, s, n, A.ptr.p, A.col.p, val, x, epi);
+        } else if (G == 64 && pipe >= 2) {
+            launch_k(false, k_bsr3<64, 2, Epi, VT>, grid, 256, 0, s, n, A.ptr.p, A.col.p, val, x, epi);
         } else {
             dispatch_group(G, [&](auto g) {
                 constexpr int GG = decltype(g)::value;
