@@ -425,10 +425,17 @@ class DeviceProblem:
         self.n, self.nbrows, self.nnzb = n.value, nb.value, nz.value
         a = vp()
         check(lib.samg_dproblem_matrix(handle, C.byref(a)))
-        self.A = Bsr3(a, owner=self)
+        self._a = a
         r, b, x = vp(), vp(), vp()
         check(lib.samg_dproblem_vectors(handle, C.byref(r), C.byref(b), C.byref(x)))
         self.rhs_ptr, self.nullspace_ptr, self.xyz_ptr = r.value, b.value, x.value
+
+    @property
+    def A(self) -> "Bsr3":
+        # a fresh borrowed view per access: storing one on the problem would
+        # make a reference cycle (view -> owner -> view) and leave the device
+        # memory to the cyclic collector instead of `del` / scope exit
+        return Bsr3(self._a, owner=self)
 
     def __del__(self):
         if getattr(self, "h", None):
@@ -437,6 +444,9 @@ class DeviceProblem:
             except Exception:
                 pass
             self.h = None
+
+    def close(self):
+        self.__del__()
 
     def download(self):
         """(rhs, nullspace (6 x 3n column-major blocks, flat), xyz) on the host"""
