@@ -29,8 +29,11 @@ def main():
     ap.add_argument("--algorithmic", type=float, default=None)
     ap.add_argument("--config", default="")
     a = ap.parse_args()
-    raw = subprocess.run(["ncu", "-i", a.report, "--page", "raw", "--csv"], capture_output=True,
-                         text=True, check=True).stdout
+    if a.report.endswith(".csv"):  # the raw page already exported on the GPU box (ncu -i REP --page raw --csv)
+        raw = open(a.report).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", a.report, "--page", "raw", "--csv"], capture_output=True,
+                             text=True, check=True).stdout
     rows = list(csv.reader(raw.splitlines()))
     head, units = rows[0], rows[1]
     launches = []
