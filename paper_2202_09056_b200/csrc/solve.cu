@@ -9,7 +9,10 @@
 // (variant 1): lane l accumulates whole 3x3 blocks beg+l, beg+l+G, ... with
 // 16-byte loads, so the row's 72-byte blocks stream as contiguous, coalesced
 // bytes; col[] is read once per block and x[3c..3c+2] is a gather that hits
-// L1/L2 (structured meshes keep the column window small).  Variant 0 (row
+// L1/L2 (structured meshes keep the column window small).  Long rows (a warp
+// or two per row, G = 32 / 64) run variant 2: variant 1 with col read one
+// iteration ahead (row_sums_pipe); large matrices the TMA-fed persistent
+// kernel (variant 3, k_bsr3_tma).  Variant 0 (row
 // units: lane l handles scalar row l%3 of every block, G in {8,16,32}) is kept
 // for comparison (SAMG_SPMV_VARIANT=0).  The three row sums are combined with
 // a width-G butterfly (plus shared memory for G > 32) and the epilogue
