@@ -695,7 +695,8 @@ def run_dist_amg(args, rank, world, local, dist):
     setup is distributed (samg_dsetup_device: every rank builds its rows of
     each large level, dsetup.cu) and the partitioned PCG runs with NCCL halos
     and all-reduces inside one CUDA graph (dsolve.cu).  Times: wall clock
-    around each phase, max over ranks; the first run warms up."""
+    around each phase, max over ranks; the first run warms up, then the
+    best of two per phase."""
     import torch
 
     import paper_2202_09056_b200 as pb
@@ -719,7 +720,7 @@ def run_dist_amg(args, rank, world, local, dist):
         prm = pb.AmgParams(smoother="spai0", device=local)
         uid = None
         runs = []
-        for it in range(1 + max(1, args.amg_repeats // 2)):
+        for it in range(1 + max(2, args.amg_repeats // 2)):
             dist.barrier()
             torch.cuda.synchronize(dev)
             t0 = time.perf_counter()
@@ -744,7 +745,11 @@ def run_dist_amg(args, rank, world, local, dist):
             del dp, u
             if it:
                 runs.append(rec)
-        best = runs[-1]
+        # best per phase over the timed runs, as the single-GPU C4 leg (the
+        # setup's time varies with how much of the memory pool is mapped)
+        best = dict(runs[-1])
+        for k in ("assemble_s", "setup_s", "solve_s"):
+            best[k] = min(r[k] for r in runs)
         out[name] = {**best, "runs": runs, "levels": inf["nlevels"],
                      "distributed_levels": inf["dist_levels"],
                      "held_rows_rank0": inf["held_rows"], "rows_rank0": n1 - n0,
@@ -752,7 +757,7 @@ def run_dist_amg(args, rank, world, local, dist):
                              f"(samg_dsetup_device), partitioned PCG (graph, NCCL halos), SPAI0"}
         torch.cuda.empty_cache()
     out["problem"] = "strong scaling: the same global C4 / C3 on every N"
-    out["timing"] = "wall clock around assemble / setup / solve, max over ranks"
+    out["timing"] = "wall clock around assemble / setup / solve, max over ranks; best of two timed runs per phase"
     return out
 
 
