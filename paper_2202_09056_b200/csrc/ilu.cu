@@ -955,8 +955,10 @@ void launch_ilu_smooth(const Bsr3 *A, const Smoother &M, const double *f, const 
     // (latest-last order: both sweeps hand off at the chain's end, and twice
     // the rows ahead on 3 CTAs per SM measured 4.6 % faster on C1 -- 0.278 ->
     // 0.265 s; the reference order lost 1 % with it)
-    const int64_t gcap = M.latest_last && !std::getenv("SAMG_ILU_CTAS_PER_SM") ? gf / 2 * 3 : gf;
-    const int64_t look = M.latest_last && !std::getenv("SAMG_ILU_AHEAD") ? 2 * ahead : ahead;
+    static const bool env_ctas = std::getenv("SAMG_ILU_CTAS_PER_SM") != nullptr;
+    static const bool env_ahead = std::getenv("SAMG_ILU_AHEAD") != nullptr;
+    const int64_t gcap = M.latest_last && !env_ctas ? gf / 2 * 3 : gf;
+    const int64_t look = M.latest_last && !env_ahead ? 2 * ahead : ahead;
     auto grid_for = [&](int depth) {
         const int64_t warps = (look * n + depth - 1) / std::max(depth, 1);
         return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(gcap, (std::min<int64_t>(warps, n) + 7) / 8)));
