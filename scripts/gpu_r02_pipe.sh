@@ -1,4 +1,6 @@
 # long-row register kernel variants: col one iteration ahead (pipe) under different register budgets
+# (the sweep that picked variant 2; the experiment values 1 / 3 / 5 / 6 of SAMG_LONG_PIPE selected builds that
+# no longer exist -- the shipped switch is 0: variant 1, 1: G = 32 only, 2: also G = 64; results in profiles/r02_long_pipe.txt)
 cd $GRAFT_REPO_ROOT
 O=gpurun_out
 for v in 0 1 3 5 6; do
