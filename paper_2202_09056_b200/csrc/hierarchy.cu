@@ -70,12 +70,19 @@ uint64_t Hierarchy::memory_footprint() const {
         return scalar ? static_cast<uint64_t>(3 * M.nrows + 1) * 8 + static_cast<uint64_t>(M.nnzb) * 9 * 16
                       : matrix_bytes(M);
     };
+    // `scalar` with omega 0: P is the indicator tentative operator, one scalar
+    // entry per row (the diagonal of each stored block; coarsening.hpp:326)
+    const bool diag_transfer = pipeline == SAMG_PIPELINE_SCALAR && prm.omega == 0.0;
+    auto tbytes = [&](const Bsr3 &M) {
+        return diag_transfer ? static_cast<uint64_t>(3 * M.nrows + 1) * 8 + static_cast<uint64_t>(M.nnzb) * 3 * 16
+                             : mbytes(M);
+    };
     uint64_t bytes = 0;
     for (const Level &lv : levels) {
         bytes += mbytes(lv.A);
         if (lv.has_transfer) {
-            bytes += mbytes(lv.P);
-            bytes += mbytes(lv.R);
+            bytes += tbytes(lv.P);
+            bytes += tbytes(lv.R);
         }
         if (lv.M.kind == SM_ILU && lv.M.scalar)  // ilu0<double>::bytes: scalar factors + pivots
             bytes += static_cast<uint64_t>(3 * lv.M.nrows + 1) * 8 + static_cast<uint64_t>(lv.M.nnzb) * 9 * 16 +

@@ -899,6 +899,23 @@ __global__ void k_ptent_bsr(int nbrows, int h, int k, const int *agg, const doub
     }
 }
 
+// omega == 0 with the indicator tentative (the `scalar` pipeline; the
+// reference's own known-answer case, test_coarsening.cpp:172-180): scalar row
+// i holds the single entry P_tent(i, 3 agg(i/3) + i%3) = Pt1[i], i.e. block
+// row br is one diagonal 3x3 block in column agg(br)
+__global__ void k_ptent_ind_bsr(int nbrows, const int *agg, const double *Pt1, int *pptr,
+                                int *pcol, double *pval, int row0) {
+    const int br = blockIdx.x * blockDim.x + threadIdx.x;  // local block row
+    if (br > nbrows) return;
+    pptr[br] = br;
+    if (br == nbrows) return;
+    const int gb = row0 + br;  // global block row = node (point block size 3)
+    pcol[br] = agg[gb];
+    double *b = pval + 9 * static_cast<int64_t>(br);
+    for (int e = 0; e < 9; ++e) b[e] = 0.0;
+    for (int c = 0; c < 3; ++c) b[4 * c] = Pt1[3 * static_cast<int64_t>(gb) + c];
+}
+
 // ---------------------------------------------------------------------------
 // SpGEMM C = A*B (csr.hpp:199-255).  One CTA per output row; a hash set of
 // the row's columns lives in shared memory (or a global scratch slab for
@@ -1788,9 +1805,13 @@ void smooth_prolongation(const Bsr3 &A, const Graph &G, const DevBuf<int> &agg, 
     const int64_t nnodes = node1 - node0, nbrows = nnodes * h, nsc = 3 * nbrows;
     const int64_t row0 = node0 * h;
     if (omega == 0.0) {
-        if (ind) fail(SAMG_UNSUPPORTED, "smooth_prolongation: omega 0 with the indicator tentative");
         P.alloc(nbrows, naggs * kb, nbrows * kb, s);
-        k_ptent_bsr<<<ceil_div(nbrows + 1, 256), 256, 0, s>>>(static_cast<int>(nbrows), h, k, agg.p,
+        if (ind)
+            k_ptent_ind_bsr<<<ceil_div(nbrows + 1, 256), 256, 0, s>>>(static_cast<int>(nbrows), agg.p, Pt,
+                                                                     P.ptr.p, P.col.p, P.val.p,
+                                                                     static_cast<int>(row0));
+        else
+            k_ptent_bsr<<<ceil_div(nbrows + 1, 256), 256, 0, s>>>(static_cast<int>(nbrows), h, k, agg.p,
                                                              Pt, P.ptr.p, P.col.p, P.val.p,
                                                              static_cast<int>(row0));
         CK_LAUNCH();

@@ -766,3 +766,70 @@ def test_c4_full_size_properties(gpu):
     rep = h.cg_solve_device(dp.rhs_ptr, u.data_ptr())
     assert rep["converged"] and rep["relative_residual"] <= 1.01e-8, rep
     h.close()
+
+
+# coarsening_params away from their defaults (coarsening.hpp:26-31) and the
+# stagnation guard (hierarchy.hpp:355): the reference's own tests pin
+# omega = 0 (P = P_tent bitwise, test_coarsening.cpp:172-180) and vary the
+# strength threshold (test_coarsening.cpp:11-56)
+COARSENING_CASES = [
+    # (name, problem kwargs, pipeline, reference Params overrides)
+    ("eps0_all_strong", dict(nx=9, ny=7, nz=5, dirichlet="eliminate", load="traction_xend"),
+     "ns_block", dict(eps_strong=0.0)),
+    ("eps025_sparse_graph", dict(nx=9, ny=7, nz=5, dirichlet="eliminate", load="traction_xend"),
+     "ns_block", dict(eps_strong=0.25)),
+    ("eps05_hetero", dict(nx=7, dirichlet="eliminate", heterogeneous=True, load="random", seed=7),
+     "ns_block", dict(eps_strong=0.5)),
+    ("omega0_tentative_only", dict(nx=8, dirichlet="keep_rows", noise=0.01, seed=3),
+     "ns_block", dict(omega=0.0)),
+    ("omega1_undamped", dict(nx=9, ny=7, nz=5, dirichlet="eliminate", load="traction_xend"),
+     "ns_block", dict(omega=1.0)),
+    ("stagnation_stops_early", dict(nx=9, ny=7, nz=5, dirichlet="eliminate", load="traction_xend"),
+     "ns_block", dict(stagnation_ratio=0.02)),
+    ("block_eps025", dict(nx=9, ny=7, nz=5, dirichlet="eliminate", load="traction_xend"),
+     "block", dict(eps_strong=0.25)),
+    ("scalar_omega0", dict(nx=6, dirichlet="keep_rows"), "scalar", dict(omega=0.0)),
+    ("hybrid2_eps0", dict(nx=7, dirichlet="eliminate", heterogeneous=True, load="random", seed=7),
+     "ns_hybrid2", dict(eps_strong=0.0, omega=0.5)),
+]
+
+
+@pytest.mark.parametrize("case", COARSENING_CASES, ids=[c[0] for c in COARSENING_CASES])
+def test_coarsening_parameter_parity(gpu, ref, case):
+    name, kw, pipeline, over = case
+    pb = gpu
+    p = make_problem(pb, **kw)
+    A = p.csr()
+    B = None if pipeline in ("block", "scalar") else p.nullspace()
+    sm = "jacobi" if pipeline == "scalar" else "spai0"
+    som = 0.5 if pipeline == "scalar" else 0.72
+    ce = 100
+    from oracle.oracle import OracleError
+    gprm = pb.AmgParams(smoother=sm, smoother_omega=som, coarse_enough=ce, **over)
+    try:
+        hr = ref.setup(A[0], A[1], A[2], A[3], B,
+                       Params(smoother=SM[sm], smoother_omega=som, coarse_enough=ce,
+                              pipeline=PIPE[pipeline], **over))
+    except OracleError as e:
+        # the reference rejects the setup (e.g. zero_diagonal of a smoother
+        # on a badly coarsened level): the same exception class here
+        with pytest.raises(pb.SamgError) as g:
+            pb.setup(A, B, pipeline, gprm)
+        assert g.value.code == e.code, (g.value, e)
+        return
+    h = pb.setup(A, B, pipeline, gprm)
+    compare_hierarchies(h, hr, None, sm, som, pipeline)
+    if name == "stagnation_stops_early":
+        # the guard rejects the first coarse level: one level, direct solve
+        assert h.nlevels == hr.nlevels == 1
+    if name == "omega0_tentative_only":
+        # P is the tentative prolongator: a fine node only reaches its own
+        # aggregate's six columns (two column blocks)
+        P = h.level(0, 1)
+        assert np.diff(P[2]).max() <= 2
+    u, rep = h.cg_solve(p.rhs)
+    ur, rr = hr.cg_solve(p.rhs)
+    assert rep["converged"] == rr["converged"]
+    assert abs(rep["iterations"] - rr["iterations"]) <= 1, (rep, rr)
+    if rr["converged"]:
+        assert rel_fro(u, ur) <= 1e-7
