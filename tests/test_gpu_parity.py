@@ -833,3 +833,58 @@ def test_coarsening_parameter_parity(gpu, ref, case):
     assert abs(rep["iterations"] - rr["iterations"]) <= 1, (rep, rr)
     if rr["converged"]:
         assert rel_fro(u, ur) <= 1e-7
+
+
+def _wide_nullspace(p, k):
+    """Column-major (3 nn x k) candidate set: the translations (k = 3), the
+    six rigid-body modes, plus axial stretches (k = 9) and shears (k = 12)."""
+    nn = p.n // 3
+    B6 = np.asarray(p.nullspace()).reshape(6, 3 * nn)
+    if k <= 6:
+        return np.ascontiguousarray(B6[:k]).reshape(-1)
+    xyz = np.asarray(p.xyz).reshape(nn, 3)
+    extra = []
+    for d in range(3):  # stretch along d: u_d = x_d
+        c = np.zeros((nn, 3))
+        c[:, d] = xyz[:, d]
+        extra.append(c.reshape(-1))
+    for d in range(3):  # symmetric shear: u_d = x_e, u_e = x_d
+        e = (d + 1) % 3
+        c = np.zeros((nn, 3))
+        c[:, d] = xyz[:, e]
+        c[:, e] = xyz[:, d]
+        extra.append(c.reshape(-1))
+    return np.concatenate([B6.reshape(-1)] + extra[:k - 6])
+
+
+@pytest.mark.parametrize("k,pipeline,kw", [
+    (3, "ns_block", dict(nx=9, ny=7, nz=5, dirichlet="eliminate", load="traction_xend")),
+    (3, "ns_hybrid2", dict(nx=6, dirichlet="keep_rows")),
+    (3, "ns_scalar", dict(nx=7, dirichlet="eliminate", heterogeneous=True, load="random", seed=7)),
+    (9, "ns_block", dict(nx=9, ny=7, nz=5, dirichlet="eliminate", load="traction_xend")),
+    (9, "ns_hybrid1", dict(nx=8, dirichlet="keep_rows", noise=0.01, seed=3)),
+    (12, "ns_block", dict(nx=10, ny=8, nz=6, dirichlet="eliminate", noise=0.01, seed=11)),
+], ids=lambda v: str(v) if not isinstance(v, dict) else "")
+def test_nullspace_width_parity(gpu, ref, k, pipeline, kw):
+    """Near-nullspace candidate sets other than the six rigid-body modes
+    (tentative_prolongation takes any k divisible by the block size,
+    coarsening.hpp:238-312; coarse point blocks of k rows): 3 (translations
+    only), 9 and 12 columns."""
+    pb = gpu
+    p = make_problem(pb, **kw)
+    A = p.csr()
+    B = _wide_nullspace(p, k)
+    sm = "jacobi" if pipeline in SCALAR_PIPES else "spai0"
+    som = 0.5 if sm == "jacobi" else 0.72
+    ce = 150
+    hr = ref.setup(A[0], A[1], A[2], A[3], B,
+                   Params(smoother=SM[sm], smoother_omega=som, coarse_enough=ce, pipeline=PIPE[pipeline]))
+    h = pb.setup(A, B, pipeline, pb.AmgParams(smoother=sm, smoother_omega=som, coarse_enough=ce))
+    assert h.nlevels >= 2
+    compare_hierarchies(h, hr, None, sm, som, pipeline)
+    u, rep = h.cg_solve(p.rhs)
+    ur, rr = hr.cg_solve(p.rhs)
+    assert rep["converged"] == rr["converged"]
+    assert abs(rep["iterations"] - rr["iterations"]) <= 1, (rep, rr)
+    if rr["converged"]:
+        assert rel_fro(u, ur) <= 1e-7
