@@ -385,6 +385,19 @@ SAMG_API int samg_setup(int64_t n, const int64_t *ptr, const int64_t *col, const
                 if (nnz) h2d(dc.p, col, sizeof(int64_t) * nnz, s);
                 scalar_to_bsr3(n, dp.p, dc.p, dv.p, A0, s);
             }
+            // scalar level matrices in the reference (hierarchy.hpp:298-330)
+            // and ilu0<double> work on the scalar pattern: the 3x3 storage
+            // reproduces them only when every stored block is whole -- a
+            // partial block's padding zeros would join the ILU(0) pattern and
+            // the footprint.  Refused loudly rather than answered differently.
+            const bool scalar_pattern =
+                pipeline == SAMG_PIPELINE_SCALAR || pipeline == SAMG_PIPELINE_NS_SCALAR ||
+                (pipeline == SAMG_PIPELINE_NS_HYBRID1 && prm->smoother == SAMG_SMOOTHER_ILU0);
+            if (scalar_pattern && nnz != 9 * A0.nnzb) {
+                { Bsr3 drop = std::move(A0); }  // freed on s before the handler destroys the stream
+                fail(SAMG_UNSUPPORTED, "setup: this pipeline keeps the scalar pattern; the input must "
+                                       "hold whole 3x3 blocks (all 9 entries of every touched block)");
+            }
         } catch (...) {
             cudaStreamSynchronize(s);
             cudaStreamDestroy(s);

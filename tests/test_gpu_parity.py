@@ -888,3 +888,51 @@ def test_nullspace_width_parity(gpu, ref, k, pipeline, kw):
     assert abs(rep["iterations"] - rr["iterations"]) <= 1, (rep, rr)
     if rr["converged"]:
         assert rel_fro(u, ur) <= 1e-7
+
+
+def _drop_small_entries(A, frac=0.05):
+    """Symmetric scalar CSR with the small off-block entries removed, so that
+    many 3x3 blocks are only partly stored (to_block<3> pads them with zeros,
+    csr.hpp:268-324)."""
+    n, ptr, col, val = A
+    rows = np.repeat(np.arange(n), np.diff(ptr))
+    d = np.zeros(n)
+    d[rows[rows == col]] = val[rows == col]
+    keep = (rows // 3 == col // 3) | (np.abs(val) > frac * np.sqrt(d[rows] * d[col]))
+    nptr = np.zeros(n + 1, np.int64)
+    np.add.at(nptr, rows[keep] + 1, 1)
+    return n, np.cumsum(nptr), col[keep].copy(), val[keep].copy()
+
+
+@pytest.mark.parametrize("pipeline", ["ns_block", "ns_hybrid2", "block"])
+def test_partial_blocks_scalar_input(gpu, ref, pipeline):
+    """samg_setup from a scalar CSR whose 3x3 blocks are partly stored: the
+    device to_block pads like the reference's, every level is bit-identical;
+    the pipelines that keep the scalar pattern refuse such an input."""
+    pb = gpu
+    from paper_2202_09056_b200._lib import Unsupported
+    p = make_problem(pb, 8, dirichlet="eliminate", noise=0.01, seed=3)
+    full = p.csr()
+    A = _drop_small_entries(full)
+    assert A[1][-1] < full[1][-1]
+    nblocks = len(np.unique((np.repeat(np.arange(A[0]), np.diff(A[1])) // 3) * (A[0] // 3) + A[2] // 3))
+    assert A[1][-1] < 9 * nblocks  # some stored block is partial
+    B = None if pipeline == "block" else p.nullspace()
+    ce = 150
+    hr = ref.setup(A[0], A[1], A[2], A[3], B, Params(coarse_enough=ce, pipeline=PIPE[pipeline]))
+    h = pb.setup(A, B, pipeline, pb.AmgParams(coarse_enough=ce))
+    assert h.nlevels >= 2
+    compare_hierarchies(h, hr, None, "spai0", 0.72, pipeline)
+    u, rep = h.cg_solve(p.rhs)
+    ur, rr = hr.cg_solve(p.rhs)
+    assert rep["converged"] == rr["converged"]
+    assert abs(rep["iterations"] - rr["iterations"]) <= 1, (rep, rr)
+    if rr["converged"]:
+        assert rel_fro(u, ur) <= 1e-7
+    if pipeline == "ns_block":
+        for pl, sm in (("scalar", "jacobi"), ("ns_scalar", "jacobi"), ("ns_hybrid1", "ilu0")):
+            with pytest.raises(Unsupported):
+                pb.setup(A, None if pl == "scalar" else p.nullspace(), pl,
+                         pb.AmgParams(coarse_enough=ce, smoother=sm))
+        # whole blocks: accepted
+        pb.setup(full, None, "scalar", pb.AmgParams(coarse_enough=ce, smoother="jacobi")).close()
