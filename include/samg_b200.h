@@ -160,7 +160,12 @@ SAMG_API int samg_device_count(int *count);
 /* ---- setup: replaces samg::setup (hierarchy.hpp:263-405) ----------------
  * Scalar CSR input (int64 ptr/col, fp64 val, n rows), exactly the
  * reference's csr<double> (csr.hpp:26-40).  B is the column-major
- * b_rows-by-b_cols near-nullspace (dense_columns, csr.hpp:46-55) or NULL. */
+ * b_rows-by-b_cols near-nullspace (dense_columns, csr.hpp:46-55) or NULL.
+ * Partly stored 3x3 blocks are padded with zeros like to_block<3>
+ * (csr.hpp:268-324); the pipelines that keep the scalar pattern (scalar,
+ * ns_scalar, ns_hybrid1 with ilu0<double>) return SAMG_UNSUPPORTED for such
+ * an input, since the padding would change their ILU(0) pattern and
+ * footprint. */
 SAMG_API int samg_setup(int64_t n, const int64_t *ptr, const int64_t *col,
         const double *val, const double *B, int64_t b_rows, int64_t b_cols,
         int pipeline, const samg_amg_params *prm, samg_hierarchy **out);
